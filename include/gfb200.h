@@ -1,0 +1,200 @@
+/*
+ * gfb200.h -- C ABI of the B200 backend transformer (libgfb200.so).
+ *
+ * This is the drop-in boundary for the reference interpreter backend.  The
+ * reference has no FFI: its backend API is the Python functions
+ * `compile_function` / `call` / `create_tensor`
+ * (/root/reference/pkg/src/graphforge/interpreter.py:92-245, tensor.py:78-102,
+ * re-exported from __init__.py:10-45).  The Python package
+ * `paper_1801_08058_b200` keeps those signatures and lowers a compiled
+ * Function to a *plan* (arena size, constant pool, launch records); this
+ * library owns everything on the device:
+ *
+ *   gfb_exe_create   <- the device half of compile_function  (interpreter.py:92-170)
+ *   gfb_exe_run      <- call                                  (interpreter.py:191-245)
+ *   gfb_exe_destroy  <- Executable going out of scope
+ *   gfb_comm_*       <- collectives the paper lists as future work
+ *
+ * Conventions: every entry point returns an int status (GFB_OK == 0) and
+ * leaves a thread-local message for gfb_last_error().  No torch or CUDA
+ * types cross the boundary: device buffers are plain pointers, streams are
+ * `void*` (a cudaStream_t, NULL = the per-thread default stream).  The
+ * caller owns input/output buffers ("results and parameters are
+ * caller-allocated"); the library owns the arena, the constant pool, the
+ * device pointer table and the captured CUDA graph.  Runs of one executable
+ * are serialised by an internal mutex (the reference allows concurrent
+ * calls on one Executable).
+ */
+#ifndef GFB200_H
+#define GFB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    GFB_OK = 0,
+    GFB_ERR_CUDA = 1,
+    GFB_ERR_INVALID = 2,
+    GFB_ERR_NCCL = 3,
+    GFB_ERR_UNSUPPORTED = 4,
+};
+
+/* ---- kernel families a launch record can name ------------------------- */
+enum {
+    GFB_K_EW_F32 = 1, /* fused elementwise / broadcast / reduce VM (gfb_ew_args) */
+    GFB_K_EW_F64 = 2,
+    GFB_K_EW_I64 = 3,
+    GFB_K_EW_U8 = 4,
+    GFB_K_DOT_F32 = 10, /* SIMT Dot, sequential k, bit-exact (gfb_dot_args) */
+    GFB_K_DOT_F64 = 11,
+    GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot (gfb_dot_args) */
+    GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
+    GFB_K_CONV_F64 = 21,
+    GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
+};
+
+/* ---- tensor references inside kernel arguments ------------------------- */
+/* A tensor is (slot, byte offset): slot 0 = arena, 1 = constant pool,
+ * 2 + i = input i, 2 + n_inputs + j = output j.  Kernels resolve slots
+ * through the executable's device pointer table, so the captured CUDA graph
+ * stays valid while callers pass new buffers every run. */
+#define GFB_REF(slot, offset) ((((uint64_t)(slot)) << 56) | (uint64_t)(offset))
+#define GFB_SLOT_ARENA 0
+#define GFB_SLOT_CONST 1
+#define GFB_SLOT_IO 2
+
+#define GFB_MAX_LEAVES 16
+#define GFB_MAX_DIGITS 6
+#define GFB_MAX_INSTR 64
+
+/* One mixed-radix digit of an index map: coord = (idx / div) % mod,
+ * offset += coord * stride, idx being the output (src 0) or reduced (src 1)
+ * flat index of the launch.  Division is by multiply-shift:
+ * idx / d == (idx * mul) >> sh for idx < 2^31 (mul == 0 means d == 1);
+ * mod == 0 means "no modulo". */
+typedef struct {
+    uint64_t div_mul;
+    uint64_t mod_mul;
+    uint32_t div_sh;
+    uint32_t mod_sh;
+    uint32_t mod;
+    int32_t stride;
+    int32_t src;
+    int32_t pad;
+} gfb_digit;
+
+/* A load or store site of the fused program. */
+typedef struct {
+    uint64_t ref;   /* GFB_REF(slot, byte offset) */
+    uint64_t splat; /* raw value bits when mode == 1 */
+    int32_t mode;   /* 0 = memory, 1 = splat constant (no memory access) */
+    int32_t ndig;
+    int32_t vec;    /* along the launch's vector axis: 0 gather, 1 contiguous, 2 uniform */
+    int32_t pad;
+    gfb_digit dig[GFB_MAX_DIGITS];
+} gfb_leaf;
+
+/* Fused elementwise / broadcast / reduce launch (one VM program). */
+typedef struct {
+    const void* const* tab; /* patched by gfb_exe_create */
+    uint32_t n_o;           /* output-space extent */
+    uint32_t n_r;           /* reduced extent (1 for a map) */
+    uint32_t ninstr;
+    uint32_t nleaves;
+    int32_t mode;     /* 0 map, 1 row reduce (lanes over r), 2 column reduce (lanes over o) */
+    int32_t red_kind; /* 1 sum, 2 max */
+    int32_t vec_axis; /* 0: vectors run along o, 1: along r */
+    int32_t split;    /* column reduce: threads splitting r per output group */
+    int32_t npre;     /* leaves 0..npre-1 (<= 4) are loaded up front, all in flight at once */
+    int32_t pad;
+    uint32_t prog[GFB_MAX_INSTR];
+    gfb_leaf leaves[GFB_MAX_LEAVES];
+    gfb_leaf red_out;
+} gfb_ew_args;
+
+/* Dot: C[m, n] = sum_k A[m, k] * B[k, n] with arbitrary element strides
+ * (a transposing Reshape feeding a Dot becomes a stride swap). */
+typedef struct {
+    const void* const* tab;
+    uint64_t a, b, c; /* GFB_REF */
+    int64_t m, n, k;
+    int64_t a_sm, a_sk, b_sk, b_sn, c_sm, c_sn;
+} gfb_dot_args;
+
+/* Conv family, operands addressed through per-axis strides (NCHW logical
+ * axes, any storage order, so NHWC layout assignment needs no copies). */
+typedef struct {
+    const void* const* tab;
+    uint64_t x, y, out;   /* op-specific roles, see kernels_conv.cu */
+    int32_t op;           /* 0 Conv2D, 1 ConvBackpropData, 2 ConvBackpropFilter */
+    int32_t pad0;
+    int64_t N, C, H, W, K, R, S, Ho, Wo;
+    int64_t sh, sw, pt, pl;
+    int64_t xs[4], ys[4], os[4]; /* element strides of the three operands */
+} gfb_conv_args;
+
+typedef struct {
+    const void* const* tab;
+    uint64_t buf;   /* GFB_REF of the contiguous gradient bucket */
+    uint64_t count; /* elements */
+    int32_t dtype;  /* 0 f32, 1 f64 */
+    int32_t pad;
+} gfb_allreduce_args;
+
+/* One kernel launch of the plan; its argument block is args[arg_offset, +arg_size). */
+typedef struct {
+    uint32_t kind;
+    uint32_t grid[3];
+    uint32_t block[3];
+    uint32_t smem;
+    uint32_t arg_offset;
+    uint32_t arg_size;
+} gfb_launch;
+
+typedef struct {
+    uint64_t arena_bytes;
+    uint64_t const_bytes;
+    const void* const_data; /* uploaded once at create */
+    uint32_t n_inputs;
+    uint32_t n_outputs;
+    uint32_t n_launches;
+    uint32_t flags; /* GFB_PLAN_* */
+    const gfb_launch* launches;
+    uint64_t args_bytes;
+    const void* args;
+    void* comm; /* gfb_comm* for plans containing GFB_K_ALLREDUCE, else NULL */
+} gfb_plan;
+
+enum { GFB_PLAN_CUDA_GRAPH = 1 };
+
+typedef struct gfb_exe gfb_exe;
+typedef struct gfb_comm gfb_comm;
+
+int gfb_init(int device);
+const char* gfb_last_error(void);
+int gfb_device_info(int* sm_major, int* sm_minor, int* num_sms);
+
+int gfb_exe_create(const gfb_plan* plan, gfb_exe** out);
+/* inputs[i] / outputs[j]: device pointers for this run (caller-owned). */
+int gfb_exe_run(gfb_exe* exe, void* const* inputs, void* const* outputs, void* stream);
+int gfb_exe_destroy(gfb_exe* exe);
+/* Number of kernels one run launches (for bench accounting). */
+int gfb_exe_num_launches(const gfb_exe* exe);
+/* Launch only record `index` of the plan (profiling / per-kernel timing). */
+int gfb_exe_run_one(gfb_exe* exe, uint32_t index, void* const* inputs, void* const* outputs, void* stream);
+
+/* NCCL communicator, one per process / GPU.  `unique_id` is the 128-byte
+ * ncclUniqueId created by rank 0 with gfb_comm_unique_id and shared by the
+ * caller's own rendezvous (torch.distributed in the Python layer). */
+int gfb_comm_unique_id(void* unique_id_128);
+int gfb_comm_create(int nranks, int rank, const void* unique_id_128, gfb_comm** out);
+int gfb_comm_destroy(gfb_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GFB200_H */

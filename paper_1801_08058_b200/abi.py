@@ -1,0 +1,106 @@
+"""ctypes mirror of include/gfb200.h (plan records and kernel argument blocks).
+
+`tests/test_abi.py` compiles a probe against the header and checks every
+size and offset here, so the two cannot drift apart silently.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+GFB_OK = 0
+
+K_EW_F32, K_EW_F64, K_EW_I64, K_EW_U8 = 1, 2, 3, 4
+K_DOT_F32, K_DOT_F64, K_DOT_TC32 = 10, 11, 12
+K_CONV_F32, K_CONV_F64 = 20, 21
+K_ALLREDUCE = 30
+
+SLOT_ARENA, SLOT_CONST, SLOT_IO = 0, 1, 2
+MAX_LEAVES, MAX_DIGITS, MAX_INSTR = 16, 6, 64
+PLAN_CUDA_GRAPH = 1
+
+
+def ref(slot: int, offset: int) -> int:
+    assert 0 <= offset < (1 << 56)
+    return (slot << 56) | offset
+
+
+class Digit(C.Structure):
+    _fields_ = [
+        ("div_mul", C.c_uint64), ("mod_mul", C.c_uint64),
+        ("div_sh", C.c_uint32), ("mod_sh", C.c_uint32), ("mod", C.c_uint32),
+        ("stride", C.c_int32), ("src", C.c_int32), ("pad", C.c_int32),
+    ]
+
+
+class Leaf(C.Structure):
+    _fields_ = [
+        ("ref", C.c_uint64), ("splat", C.c_uint64),
+        ("mode", C.c_int32), ("ndig", C.c_int32), ("vec", C.c_int32), ("pad", C.c_int32),
+        ("dig", Digit * MAX_DIGITS),
+    ]
+
+
+class EwArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p),
+        ("n_o", C.c_uint32), ("n_r", C.c_uint32), ("ninstr", C.c_uint32), ("nleaves", C.c_uint32),
+        ("mode", C.c_int32), ("red_kind", C.c_int32), ("vec_axis", C.c_int32), ("split", C.c_int32),
+        ("npre", C.c_int32), ("pad", C.c_int32),
+        ("prog", C.c_uint32 * MAX_INSTR),
+        ("leaves", Leaf * MAX_LEAVES),
+        ("red_out", Leaf),
+    ]
+
+
+class DotArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p),
+        ("a", C.c_uint64), ("b", C.c_uint64), ("c", C.c_uint64),
+        ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+        ("a_sm", C.c_int64), ("a_sk", C.c_int64), ("b_sk", C.c_int64), ("b_sn", C.c_int64),
+        ("c_sm", C.c_int64), ("c_sn", C.c_int64),
+    ]
+
+
+class ConvArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p),
+        ("x", C.c_uint64), ("y", C.c_uint64), ("out", C.c_uint64),
+        ("op", C.c_int32), ("pad0", C.c_int32),
+        ("N", C.c_int64), ("C", C.c_int64), ("H", C.c_int64), ("W", C.c_int64),
+        ("K", C.c_int64), ("R", C.c_int64), ("S", C.c_int64), ("Ho", C.c_int64), ("Wo", C.c_int64),
+        ("sh", C.c_int64), ("sw", C.c_int64), ("pt", C.c_int64), ("pl", C.c_int64),
+        ("xs", C.c_int64 * 4), ("ys", C.c_int64 * 4), ("os", C.c_int64 * 4),
+    ]
+
+
+class AllReduceArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("buf", C.c_uint64), ("count", C.c_uint64),
+        ("dtype", C.c_int32), ("pad", C.c_int32),
+    ]
+
+
+class Launch(C.Structure):
+    _fields_ = [
+        ("kind", C.c_uint32), ("grid", C.c_uint32 * 3), ("block", C.c_uint32 * 3),
+        ("smem", C.c_uint32), ("arg_offset", C.c_uint32), ("arg_size", C.c_uint32),
+    ]
+
+
+class Plan(C.Structure):
+    _fields_ = [
+        ("arena_bytes", C.c_uint64), ("const_bytes", C.c_uint64), ("const_data", C.c_void_p),
+        ("n_inputs", C.c_uint32), ("n_outputs", C.c_uint32), ("n_launches", C.c_uint32),
+        ("flags", C.c_uint32),
+        ("launches", C.POINTER(Launch)),
+        ("args_bytes", C.c_uint64), ("args", C.c_void_p),
+        ("comm", C.c_void_p),
+    ]
+
+
+STRUCTS = {
+    "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
+    "gfb_conv_args": ConvArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+}

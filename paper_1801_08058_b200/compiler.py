@@ -1,0 +1,951 @@
+"""Lowering of a compiled Function to B200 launches (the transformer proper).
+
+The reference turns every IR node into one interpreter instruction over a
+per-node arena plan (`/root/reference/pkg/src/graphforge/interpreter.py:92-170`,
+`memory.py:77-120`).  This pass instead:
+
+1. **Fusion.**  Memory-bound nodes (elementwise, Broadcast, Reshape,
+   ConvertLayout, Sum) are grouped; only tensors somebody must see are
+   *materialised* — results, Sum outputs, operands of Dot/Conv that cannot
+   be read through strides, and values with several consumers.  Each group
+   becomes one launch of the fused VM kernel (`csrc/ew_vm.cu`): the node
+   expressions compile to a short accumulator-stack program, every read of
+   a materialised tensor becomes a *leaf* addressed through a mixed-radix
+   digit map (Broadcast = dropped digit, axis permutation / ConvertLayout =
+   permuted strides, row-major Reshape = re-split digits), so index ops cost
+   no memory traffic at all.  A Sum whose input is also a result stores that
+   input as a side output of the same pass (config B: one read of a and b,
+   one write of t3, one write of the row sums).
+2. **Strided heavy operands.**  Dot / Conv kernels take per-axis strides,
+   so the `Reshape(x, (1, 0))` transposes autodiff emits
+   (`autodiff.py:163-177`) and NHWC layouts are read in place.
+3. **Liveness over launches.**  Arena placement (`memory.plan_buffers`) is
+   first-fit over materialised buffers with live ranges in launch indices;
+   fused intermediates never touch memory.
+
+The result is a list of launch records + argument blocks (`abi.py`) that
+`libgfb200.so` captures into one CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import abi
+from .errors import UnsupportedOp
+from .ir import (
+    ELEMENTWISE_BINARY,
+    ELEMENTWISE_UNARY,
+    ConstantData,
+    ElementType,
+    Function,
+    OpKind,
+    element_count,
+    reachable_from_results,
+    topological_order,
+)
+from .memory import DEVICE_ALIGNMENT, align_up, plan_buffers
+
+NUM_SMS = 148
+HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER})
+INDEX_OPS = frozenset({OpKind.BROADCAST, OpKind.RESHAPE, OpKind.CONVERT_LAYOUT})
+MAX_STACK = 3
+MAX_PRELOAD = 4
+
+# VM encoding (csrc/ew_vm.cu)
+I_LOAD, I_UN, I_BIN_LEAF, I_BIN_POP, I_BIN_SELF, I_PUSH, I_STORE, I_PUSH_LOAD = 1, 2, 3, 4, 5, 6, 7, 8
+VM_OP = {
+    OpKind.ADD: 0, OpKind.SUBTRACT: 1, OpKind.MULTIPLY: 2, OpKind.DIVIDE: 3, OpKind.MAXIMUM: 4,
+    OpKind.NEGATE: 5, OpKind.EXP: 6, OpKind.LOG: 7, OpKind.TANH: 8, OpKind.SIGMOID: 9, OpKind.RELU: 10,
+}
+EW_KIND = {ElementType.F32: abi.K_EW_F32, ElementType.F64: abi.K_EW_F64, ElementType.I64: abi.K_EW_I64, ElementType.BOOL: abi.K_EW_U8}
+INDEX_LIMIT = 1 << 31
+
+
+def magic_u31(d: int) -> tuple[int, int]:
+    """(mul, sh) with n // d == (n * mul >> 32) >> sh for all 0 <= n < 2**31."""
+    if d <= 0:
+        raise ValueError(d)
+    if d == 1:
+        return 0, 0
+    l = (d - 1).bit_length()  # ceil(log2 d)
+    mul = (1 << (31 + l)) // d + 1
+    assert mul < (1 << 32)
+    return mul, l - 1
+
+
+def _prod(xs) -> int:
+    p = 1
+    for x in xs:
+        p *= x
+    return p
+
+
+# ---------------------------------------------------------------------------
+# Buffers and index maps
+
+
+@dataclass
+class Buffer:
+    key: int
+    et: ElementType
+    shape: tuple
+    strides: tuple  # element stride per logical axis
+    slot: int = abi.SLOT_ARENA
+    offset: int = 0
+    splat: object = None  # python scalar for splat constants (no memory)
+
+    @property
+    def nbytes(self) -> int:
+        return element_count(self.shape) * self.et.byte_size
+
+
+# An axis expression: coordinate = (idx[src] // div) % mod, or None (always 0).
+AxisExpr = tuple  # (src, div, mod)
+
+
+def iteration_axes(shape, src=0) -> list:
+    out = []
+    for a, d in enumerate(shape):
+        out.append(None if d == 1 else (src, _prod(shape[a + 1:]), d))
+    return out
+
+
+class Unexpressible(Exception):
+    pass
+
+
+def through_reshape(node, out_axes) -> list:
+    """Axis expressions of a Reshape's input given those of its output."""
+    in_shape = node.inputs_shape
+    order = node.attrs["input_order"]
+    out_shape = node.output.shape
+    perm_dims = tuple(in_shape[a] for a in order)
+    in_axes = [None] * len(in_shape)
+    if perm_dims == tuple(out_shape):
+        for i, a in enumerate(order):
+            in_axes[a] = out_axes[i]
+        return in_axes
+    # General re-split: the output's axes must be one contiguous digit block.
+    live = [(a, e) for a, e in enumerate(out_axes) if e is not None and out_shape[a] > 1]
+    if not live:
+        return in_axes  # single element
+    srcs = {e[0] for _, e in live}
+    if len(srcs) != 1:
+        raise Unexpressible()
+    src = srcs.pop()
+    last_axis, last = live[-1]
+    base = last[1] // _prod(out_shape[last_axis + 1:])
+    for a, e in live:
+        if e[2] != out_shape[a] or e[1] != base * _prod(out_shape[a + 1:]):
+            raise Unexpressible()
+    for i, a in enumerate(order):
+        d = perm_dims[i]
+        in_axes[a] = None if d == 1 else (src, base * _prod(perm_dims[i + 1:]), d)
+    return in_axes
+
+
+def through_index_op(node, out_axes) -> list:
+    if node.op is OpKind.CONVERT_LAYOUT:
+        return list(out_axes)
+    if node.op is OpKind.BROADCAST:
+        drop = set(node.attrs["broadcast_axes"])
+        return [e for a, e in enumerate(out_axes) if a not in drop]
+    return through_reshape(node, out_axes)
+
+
+def make_digits(buf: Buffer, axes, extents) -> list:
+    """Mixed-radix digits (src, div, mod, stride) addressing `buf` at `axes`."""
+    digs = []
+    for a, e in enumerate(axes):
+        if e is None or buf.strides[a] == 0 or buf.shape[a] <= 1:
+            continue
+        digs.append([e[0], e[1], e[2], buf.strides[a]])
+    digs.sort(key=lambda d: (d[0], d[1]))
+    merged = []
+    for d in digs:
+        if merged:
+            lo = merged[-1]
+            if lo[0] == d[0] and lo[2] is not None and d[1] == lo[1] * lo[2] and d[3] == lo[3] * lo[2]:
+                lo[2] = None if d[2] is None else lo[2] * d[2]
+                continue
+        merged.append(d)
+    out = []
+    for src, div, mod, stride in merged:
+        if mod is not None and div * mod >= extents[src]:
+            mod = None
+        out.append((src, div, mod, stride))
+    return out
+
+
+def vec_class(digits, vec_src: int, is_store: bool) -> int:
+    """0 gather, 1 contiguous (128-bit access), 2 uniform (one value per vector)."""
+    own = [d for d in digits if d[0] == vec_src]
+    unit = [d for d in own if d[1] == 1]
+    if any(d[1] % 4 for d in own if d[1] != 1):
+        return 0
+    if not unit:
+        return 0 if is_store else 2
+    if len(unit) != 1:
+        return 0
+    _, _, mod, stride = unit[0]
+    if stride != 1 or (mod is not None and mod % 4):
+        return 0
+    if any(d[3] % 4 for d in digits if d is not unit[0]):
+        return 0
+    return 1
+
+
+# ---------------------------------------------------------------------------
+# Lowered plan
+
+
+@dataclass
+class LaunchRec:
+    kind: int
+    grid: tuple
+    block: tuple
+    smem: int
+    args: C.Structure
+    reads: list  # buffer keys read
+    writes: list  # buffer keys written
+    label: str = ""
+    algo_bytes: int = 0  # algorithmic HBM bytes (roofline accounting)
+    flops: int = 0
+
+
+@dataclass
+class Lowered:
+    launches: list
+    arena_bytes: int
+    const_blob: bytes
+    n_inputs: int
+    n_outputs: int
+    buffers: dict
+    groups: list = field(default_factory=list)
+    arena_offsets: dict = field(default_factory=dict)
+
+    def pack(self):
+        """(launch array, argument blob) ready for gfb_exe_create."""
+        recs = (abi.Launch * max(1, len(self.launches)))()
+        blob = bytearray()
+        for i, L in enumerate(self.launches):
+            raw = bytes(L.args)
+            off = align_up(len(blob), 16)
+            blob.extend(b"\0" * (off - len(blob)))
+            blob.extend(raw)
+            r = recs[i]
+            r.kind = L.kind
+            r.grid[:] = list(L.grid)
+            r.block[:] = list(L.block)
+            r.smem = L.smem
+            r.arg_offset = off
+            r.arg_size = len(raw)
+        return recs, bytes(blob)
+
+
+class _Retry(Exception):
+    def __init__(self, nid):
+        self.nid = nid
+
+
+class _Node:
+    """IR node plus the shape of its first input (for Reshape inversion)."""
+
+    __slots__ = ("id", "op", "attrs", "inputs", "output", "inputs_shape")
+
+    def __init__(self, node, g):
+        self.id, self.op, self.attrs, self.inputs, self.output = node.id, node.op, node.attrs, node.inputs, node.output
+        self.inputs_shape = g.nodes[node.inputs[0][0]].output.shape if node.inputs else ()
+
+
+# ---------------------------------------------------------------------------
+
+
+class Lowering:
+    def __init__(self, g: Function, layouts: dict, private: bool = False):
+        self.g = g
+        self.layouts = layouts
+        self.private = private
+        self.order = [n for n in topological_order(g) if n in reachable_from_results(g)]
+        self.topo = {n: i for i, n in enumerate(self.order)}
+        self.nodes = {n: _Node(g.nodes[n], g) for n in self.order}
+        self.consumers: dict = {n: [] for n in self.order}
+        for n in self.order:
+            for r, _ in g.nodes[n].inputs:
+                if n not in self.consumers[r]:
+                    self.consumers[r].append(n)
+        self.param_pos = {pid: i for i, pid in enumerate(g.parameters)}
+        self.buf: dict = {}
+        self.n_in = len(g.parameters)
+        self.n_out = len(g.results)
+        self._key = 0
+
+    # -- helpers
+    def new_key(self) -> int:
+        self._key += 1
+        return self._key
+
+    def is_light(self, n) -> bool:
+        op = self.nodes[n].op
+        return op in ELEMENTWISE_BINARY or op in ELEMENTWISE_UNARY or op in INDEX_OPS or op is OpKind.SUM
+
+    def strides_of(self, n) -> tuple:
+        return self.layouts[(n, 0)].strides(self.nodes[n].output.shape)
+
+    # -- materialisation policy
+    def initial_materialised(self) -> set:
+        M = self.M = set()
+        results = {r for r, _ in self.g.results}
+        for n in self.order:
+            node = self.nodes[n]
+            if not self.is_light(n):
+                continue
+            if node.op is OpKind.SUM or n in results:
+                M.add(n)
+                continue
+            cons = self.consumers[n]
+            heavy = [c for c in cons if self.nodes[c].op in HEAVY]
+            light = [c for c in cons if c not in heavy]
+            if heavy and not self.viewable(n):
+                M.add(n)
+                continue
+            if len(light) >= 2 and not self.free_view(n):
+                M.add(n)
+        return M
+
+    def is_source(self, n) -> bool:
+        """Materialised already: parameter, constant, heavy output or member of M."""
+        op = self.nodes[n].op
+        return op in (OpKind.PARAMETER, OpKind.CONSTANT) or op in HEAVY or n in self.M
+
+    def free_view(self, n) -> bool:
+        """Index ops over materialised sources cost nothing to recompute."""
+        node = self.nodes[n]
+        while node.op in INDEX_OPS and node.id not in self.M:
+            node = self.nodes[node.inputs[0][0]]
+        return self.is_source(node.id)
+
+    def viewable(self, n) -> bool:
+        try:
+            return self.heavy_operand(n, probe=True) is not None
+        except Unexpressible:
+            return False
+
+    # -- heavy operands: (buffer, strides per logical axis)
+    def heavy_operand(self, n, probe=False):
+        node = self.nodes[n]
+        if n in self.buf:
+            b = self.buf[n]
+            return b, b.strides
+        if probe and self.is_source(n):
+            return True, None
+        if node.op is OpKind.CONVERT_LAYOUT:
+            return self.heavy_operand(node.inputs[0][0], probe)
+        if node.op is OpKind.RESHAPE:
+            src = node.inputs[0][0]
+            inner = self.heavy_operand(src, probe)
+            if inner is None:
+                return None
+            order = node.attrs["input_order"]
+            in_shape = node.inputs_shape
+            perm = tuple(in_shape[a] for a in order)
+            if perm == tuple(node.output.shape):
+                if probe:
+                    return True, None
+                b, st = inner
+                return b, tuple(st[a] for a in order)
+            if order == tuple(range(len(order))):
+                # row-major re-read of a contiguous identity-order operand
+                if probe:
+                    return (True, None) if self.is_source(src) else None
+                b, st = inner
+                if tuple(st) == _rowmajor(in_shape) or element_count(in_shape) <= 1:
+                    return b, _rowmajor(node.output.shape)
+            return None
+        return None
+
+    # -- main entry
+    def run(self) -> Lowered:
+        self.M = set()
+        self.initial_materialised()
+        for _ in range(1000):
+            try:
+                return self._lower()
+            except _Retry as r:
+                if r.nid in self.M:
+                    raise UnsupportedOp(f"cannot lower node {r.nid} ({self.nodes[r.nid].op.wire_name})")
+                self.M.add(r.nid)
+        raise UnsupportedOp("lowering did not converge")
+
+    def _lower(self) -> Lowered:
+        g = self.g
+        self.buf: dict = {}
+        self.launches: list = []
+        const_blob = bytearray()
+        results = list(g.results)
+        result_slot = {}  # node -> output index written directly by its producer
+        for j, (r, _) in enumerate(results):
+            node = self.nodes[r]
+            if node.op not in (OpKind.PARAMETER, OpKind.CONSTANT) and r not in result_slot:
+                result_slot[r] = j
+
+        for n in self.order:
+            node = self.nodes[n]
+            d = node.output
+            if element_count(d.shape) >= INDEX_LIMIT:
+                raise UnsupportedOp(f"tensor of {element_count(d.shape)} elements exceeds the 2^31 index limit")
+            if node.op is OpKind.PARAMETER:
+                self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, self.strides_of(n), abi.SLOT_IO + self.param_pos[n])
+            elif node.op is OpKind.CONSTANT:
+                data: ConstantData = node.attrs["data"]
+                b = Buffer(self.new_key(), d.element_type, d.shape, _rowmajor(d.shape), abi.SLOT_CONST)
+                if data.is_splat and self._splat_ok(n):
+                    b.splat = data.splat_value()
+                else:
+                    off = align_up(len(const_blob), DEVICE_ALIGNMENT)
+                    const_blob.extend(b"\0" * (off - len(const_blob)))
+                    const_blob.extend(np.ascontiguousarray(data.to_numpy()).tobytes())
+                    b.offset = off
+                self.buf[n] = b
+            elif n in self.M or node.op in HEAVY:
+                slot = abi.SLOT_ARENA
+                if n in result_slot:
+                    slot = abi.SLOT_IO + self.n_in + result_slot[n]
+                self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, self.strides_of(n), slot)
+
+        # merge rule: a materialised node consumed only by one Sum is that Sum's side output
+        side_of = {}
+        for n in self.order:
+            if n in self.M and self.nodes[n].op is not OpKind.SUM and self.is_light(n):
+                cons = self.consumers[n]
+                if len(cons) == 1 and self.nodes[cons[0]].op is OpKind.SUM:
+                    side_of[cons[0]] = n
+        merged = set(side_of.values())
+
+        for n in self.order:
+            node = self.nodes[n]
+            if node.op in HEAVY:
+                self.emit_heavy(n)
+            elif n in self.M and n not in merged:
+                if node.op is OpKind.SUM:
+                    self.emit_reduce(n, side_of.get(n))
+                else:
+                    self.emit_map(n, [n])
+
+        # results that are parameters / constants / repeated: copy launches
+        for j, (r, _) in enumerate(results):
+            if result_slot.get(r) == j:
+                continue
+            src = self.buf[r]
+            d = self.nodes[r].output
+            dst = Buffer(self.new_key(), d.element_type, d.shape, _rowmajor(d.shape), abi.SLOT_IO + self.n_in + j)
+            self.emit_copy(src, dst)
+
+        # arena plan over launch-index live ranges
+        live: dict = {}
+        for i, L in enumerate(self.launches):
+            for k in L.writes + L.reads:
+                lo, hi = live.get(k, (i, i))
+                live[k] = (min(lo, i), max(hi, i))
+        arena_bufs = {b.key: b for b in self.buf.values() if b.slot == abi.SLOT_ARENA}
+        items = {k: (b.nbytes, live.get(k, (0, 0))[0], live.get(k, (0, 0))[1]) for k, b in arena_bufs.items()}
+        plan = plan_buffers(items, private=self.private)
+        for k, b in arena_bufs.items():
+            b.offset = plan.offsets[k]
+        for L in self.launches:
+            L.finalize()
+        return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
+                       {b.key: b for b in self.buf.values()}, arena_offsets=plan.offsets)
+
+    def _splat_ok(self, n) -> bool:
+        """Splat constants stay scalars unless a heavy op or a result reads memory."""
+        results = {r for r, _ in self.g.results}
+        if n in results:
+            return False
+        for c in self.consumers[n]:
+            if self.nodes[c].op in HEAVY:
+                return False
+            # an index view feeding a heavy op also needs memory
+            if self.nodes[c].op in INDEX_OPS and any(self.nodes[cc].op in HEAVY for cc in self.consumers[c]):
+                return False
+        return True
+
+    # -- fused VM groups
+    def emit_map(self, root: int, stores: list):
+        node = self.nodes[root]
+        shape = node.output.shape
+        n_o = element_count(shape)
+        prog = Program(self, extents=(max(n_o, 1), 1), vec_src=0)
+        axes = iteration_axes(shape)
+        prog.eval_store(root, axes, self.buf[root])
+        if n_o == 0:
+            return
+        args = prog.args(mode=0, n_o=n_o, n_r=1)
+        groups = (n_o + 3) // 4
+        grid = max(1, min((groups + 255) // 256, NUM_SMS * 16))
+        self.add_launch(EW_KIND[node.output.element_type], (grid, 1, 1), (256, 1, 1), 0, args, prog, f"map:{node.op.wire_name}#{root}")
+
+    def emit_reduce(self, s: int, side: int | None):
+        node = self.nodes[s]
+        src = node.inputs[0][0]
+        in_shape = node.inputs_shape
+        axes_red = node.attrs["reduction_axes"]
+        kept = [a for a in range(len(in_shape)) if a not in axes_red]
+        n_o = element_count([in_shape[a] for a in kept])
+        n_r = element_count([in_shape[a] for a in axes_red])
+        if n_o == 0:
+            return
+        in_axes = [None] * len(in_shape)
+        for i, a in enumerate(kept):
+            d = in_shape[a]
+            in_axes[a] = None if d == 1 else (0, _prod(in_shape[k] for k in kept[i + 1:]), d)
+        for i, a in enumerate(axes_red):
+            d = in_shape[a]
+            in_axes[a] = None if d == 1 else (1, _prod(in_shape[k] for k in axes_red[i + 1:]), d)
+        et = node.output.element_type
+        # choose orientation from the dominant load's contiguity
+        row = self._prefer_rows(src, in_axes, n_o, n_r)
+        prog = Program(self, extents=(max(n_o, 1), max(n_r, 1)), vec_src=1 if row else 0)
+        if side is not None:
+            prog.eval_store(side, in_axes, self.buf[side])
+        elif n_r > 0:
+            prog.eval_value(src, in_axes)
+        out_b = self.buf[s]
+        prog.set_red_out(out_b, iteration_axes(node.output.shape))
+        kind = 2 if node.attrs["reduction_kind"] == "max" else 1
+        if row:
+            args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=kind)
+            grid = max(1, min((n_o + 7) // 8, NUM_SMS * 16))
+            self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), 0, args, prog, f"rowsum#{s}")
+        else:
+            groups = (n_o + 3) // 4
+            split = 1
+            if n_r > 16:
+                while split < 64 and ((groups * split + 255) // 256) < 2 * NUM_SMS and n_r // (split * 2) >= 8:
+                    split *= 2
+            per_row = 256 // split
+            grid = max(1, (groups + per_row - 1) // per_row)
+            smem = 256 * 4 * et.byte_size if split > 1 else 0
+            args = prog.args(mode=2, n_o=n_o, n_r=n_r, red_kind=kind, split=split)
+            self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), smem, args, prog, f"colsum#{s}")
+
+    def _prefer_rows(self, src, in_axes, n_o, n_r) -> bool:
+        if n_r < 32:
+            return False
+        probe = Program(self, extents=(max(n_o, 1), max(n_r, 1)), vec_src=1, dry=True)
+        try:
+            probe.eval_value(src, in_axes)
+        except _Retry:
+            return n_r >= 128
+        best = max(probe.leaf_specs, key=lambda l: l.buf.nbytes if l.buf.splat is None else -1, default=None)
+        if best is None or best.buf.splat is not None:
+            return True
+        return any(d[0] == 1 and d[1] == 1 and d[3] == 1 for d in best.digits)
+
+    def emit_copy(self, src: Buffer, dst: Buffer):
+        n_o = element_count(dst.shape)
+        if n_o == 0:
+            return
+        prog = Program(self, extents=(n_o, 1), vec_src=0)
+        axes = iteration_axes(dst.shape)
+        k = prog.leaf(src, axes)
+        prog.emit(I_LOAD, k=k)
+        prog.emit(I_STORE, k=prog.store_leaf(dst, axes))
+        args = prog.args(mode=0, n_o=n_o, n_r=1)
+        grid = max(1, min(((n_o + 3) // 4 + 255) // 256, NUM_SMS * 16))
+        self.add_launch(EW_KIND[dst.et], (grid, 1, 1), (256, 1, 1), 0, args, prog, "copy")
+        self.buf[("copy", dst.key)] = dst
+
+    def add_launch(self, kind, grid, block, smem, args, prog, label):
+        rec = LaunchRec(kind, grid, block, smem, args, prog.reads(), prog.writes(), label)
+        rec.algo_bytes = prog.algo_bytes()
+        rec.finalize = prog.finalize_fn(args)
+        self.launches.append(rec)
+
+    # -- heavy ops
+    def operand(self, ref_node):
+        op = self.heavy_operand(ref_node)
+        if op is None:
+            raise _Retry(ref_node)
+        return op
+
+    def emit_heavy(self, n: int):
+        node = self.nodes[n]
+        out = self.buf[n]
+        et = node.output.element_type
+        if node.op is OpKind.DOT:
+            (ab, ast), (bb, bst) = self.operand(node.inputs[0][0]), self.operand(node.inputs[1][0])
+            m, k = self.nodes[node.inputs[0][0]].output.shape
+            nn = node.output.shape[1]
+            if m == 0 or nn == 0:
+                return
+            args = abi.DotArgs(m=m, n=nn, k=k, a_sm=ast[0], a_sk=ast[1], b_sk=bst[0], b_sn=bst[1],
+                               c_sm=out.strides[0], c_sn=out.strides[1])
+            kind = abi.K_DOT_F32 if et is ElementType.F32 else abi.K_DOT_F64
+            grid = ((nn + 63) // 64, (m + 63) // 64, 1)
+            rec = LaunchRec(kind, grid, (256, 1, 1), 0, args, [ab.key, bb.key], [out.key], f"dot#{n}")
+            rec.flops = 2 * m * nn * k
+            rec.algo_bytes = (m * k + k * nn + m * nn) * et.byte_size
+            rec.finalize = _finalize_refs(args, {"a": ab, "b": bb, "c": out})
+            self.launches.append(rec)
+            return
+        x, y = node.inputs[0][0], node.inputs[1][0]
+        (xb, xs), (yb, ys) = self.operand(x), self.operand(y)
+        xshape, yshape = self.nodes[x].output.shape, self.nodes[y].output.shape
+        oshape = node.output.shape
+        a = node.attrs
+        if node.op is OpKind.CONV2D:
+            N, Cc, H, W = xshape
+            K, _, R, S = yshape
+            Ho, Wo = oshape[2], oshape[3]
+            sh, sw = a["strides"]
+            opc, total = 0, N * K * Ho * Wo
+            macs = total * Cc * R * S
+        elif node.op is OpKind.CONV_BACKPROP_DATA:
+            N, K, Ho, Wo = xshape
+            _, Cc, R, S = yshape
+            H, W = oshape[2], oshape[3]
+            sh = sw = 1
+            opc, total = 1, N * Cc * H * W
+            macs = N * K * Ho * Wo * Cc * R * S
+        else:
+            N, Cc, H, W = xshape
+            _, K, Ho, Wo = yshape
+            R, S = oshape[2], oshape[3]
+            sh = sw = 1
+            opc, total = 2, K * Cc * R * S
+            macs = N * K * Ho * Wo * Cc * R * S
+        if total == 0:
+            return
+        pt, _, pl, _ = a["padding"]
+        args = abi.ConvArgs(op=opc, N=N, C=Cc, H=H, W=W, K=K, R=R, S=S, Ho=Ho, Wo=Wo, sh=sh, sw=sw, pt=pt, pl=pl)
+        args.xs[:] = list(xs)
+        args.ys[:] = list(ys)
+        args.os[:] = list(out.strides)
+        kind = abi.K_CONV_F32 if et is ElementType.F32 else abi.K_CONV_F64
+        grid = max(1, min((total + 255) // 256, NUM_SMS * 64))
+        rec = LaunchRec(kind, (grid, 1, 1), (256, 1, 1), 0, args, [xb.key, yb.key], [out.key], f"{node.op.wire_name}#{n}")
+        rec.flops = 2 * macs
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(args, {"x": xb, "y": yb, "out": out})
+        self.launches.append(rec)
+
+
+def _rowmajor(shape) -> tuple:
+    out = [0] * len(shape)
+    s = 1
+    for a in range(len(shape) - 1, -1, -1):
+        out[a] = s
+        s *= shape[a]
+    return tuple(out)
+
+
+def _buf_ref(b: Buffer) -> int:
+    return abi.ref(b.slot, b.offset)
+
+
+def _finalize_refs(args, fields: dict):
+    def fin():
+        for name, b in fields.items():
+            setattr(args, name, _buf_ref(b))
+    return fin
+
+
+# ---------------------------------------------------------------------------
+# VM program construction
+
+
+@dataclass
+class LeafSpec:
+    buf: Buffer
+    digits: list
+    is_store: bool
+    vec: int = 0
+
+
+def _splat_bits(b: Buffer) -> int:
+    v = b.splat
+    if b.et is ElementType.F32:
+        return struct.unpack("<I", struct.pack("<f", v))[0]
+    if b.et is ElementType.F64:
+        return struct.unpack("<Q", struct.pack("<d", v))[0]
+    if b.et is ElementType.I64:
+        return int(v) & ((1 << 64) - 1)
+    return int(bool(v))
+
+
+class Program:
+    def __init__(self, low: Lowering, extents, vec_src: int, dry: bool = False):
+        self.low = low
+        self.extents = extents
+        self.vec_src = vec_src
+        self.dry = dry
+        self.leaf_specs: list = []
+        self.leaf_index: dict = {}
+        self.code: list = []  # (cls, op, k, swap) with k = leaf spec index
+        self.red_out = None
+
+    # -- leaves
+    def leaf(self, buf: Buffer, axes) -> int:
+        digits = make_digits(buf, axes, self.extents) if buf.splat is None else []
+        key = (buf.key, tuple(digits), False)
+        if key not in self.leaf_index:
+            if len(digits) > abi.MAX_DIGITS:
+                raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
+            spec = LeafSpec(buf, digits, False)
+            spec.vec = 2 if buf.splat is not None else vec_class(digits, self.vec_src, False)
+            self.leaf_index[key] = len(self.leaf_specs)
+            self.leaf_specs.append(spec)
+        return self.leaf_index[key]
+
+    def store_leaf(self, buf: Buffer, axes) -> int:
+        digits = make_digits(buf, axes, self.extents)
+        if len(digits) > abi.MAX_DIGITS:
+            raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
+        spec = LeafSpec(buf, digits, True, vec_class(digits, self.vec_src, True))
+        self.leaf_specs.append(spec)
+        return len(self.leaf_specs) - 1
+
+    def set_red_out(self, buf: Buffer, axes):
+        digits = make_digits(buf, axes, self.extents)
+        self.red_out = LeafSpec(buf, digits, True, vec_class(digits, 0, True))
+
+    def emit(self, cls, op=0, k=0, swap=0):
+        self.code.append((cls, op, k, swap))
+
+    # -- expression evaluation
+    def need(self, n, axes) -> int:
+        low = self.low
+        if n in low.buf:
+            return 0
+        node = low.nodes[n]
+        if node.op in INDEX_OPS:
+            try:
+                return self.need(node.inputs[0][0], through_index_op(node, axes))
+            except Unexpressible:
+                raise _Retry(n)
+        if node.op in ELEMENTWISE_UNARY:
+            return self.need(node.inputs[0][0], axes)
+        if node.op in ELEMENTWISE_BINARY:
+            a, b = node.inputs[0][0], node.inputs[1][0]
+            if a == b:
+                return self.need(a, axes)
+            na, nb = self.need(a, axes), self.need(b, axes)
+            la, lb = self.is_plain(a, axes), self.is_plain(b, axes)
+            if la or lb:
+                return max(na, nb)
+            return min(max(na, 1 + nb), max(nb, 1 + na))
+        raise _Retry(n)  # Sum / heavy not inlinable
+
+    def is_plain(self, n, axes) -> bool:
+        low = self.low
+        while n not in low.buf and low.nodes[n].op in INDEX_OPS:
+            node = low.nodes[n]
+            axes = through_index_op(node, axes)
+            n = node.inputs[0][0]
+        return n in low.buf
+
+    def value(self, n, axes):
+        """Emit code leaving node `n` at `axes` in acc; returns ('leaf', k) or ('acc',)."""
+        low = self.low
+        node = low.nodes[n]
+        if n in low.buf and n not in self._inline:
+            return ("leaf", self.leaf(low.buf[n], axes))
+        if node.op in INDEX_OPS:
+            try:
+                inner = through_index_op(node, axes)
+            except Unexpressible:
+                raise _Retry(n)
+            return self.value(node.inputs[0][0], inner)
+        if node.op in ELEMENTWISE_UNARY:
+            self.to_acc(self.value(node.inputs[0][0], axes))
+            self.emit(I_UN, VM_OP[node.op])
+            return ("acc",)
+        if node.op in ELEMENTWISE_BINARY:
+            a, b = node.inputs[0][0], node.inputs[1][0]
+            op = VM_OP[node.op]
+            if a == b:
+                r = self.value(a, axes)
+                if r[0] == "leaf":
+                    self.emit(I_LOAD, k=r[1])
+                    self.emit(I_BIN_LEAF, op, r[1])
+                else:
+                    self.emit(I_BIN_SELF, op)
+                return ("acc",)
+            la, lb = self.is_plain(a, axes), self.is_plain(b, axes)
+            if lb:
+                self.to_acc(self.value(a, axes))
+                rb = self.value(b, axes)
+                self.emit(I_BIN_LEAF, op, rb[1], 0)
+                return ("acc",)
+            if la:
+                self.to_acc(self.value(b, axes))
+                ra = self.value(a, axes)
+                self.emit(I_BIN_LEAF, op, ra[1], 1)
+                return ("acc",)
+            na, nb = self.need(a, axes), self.need(b, axes)
+            if max(na, 1 + nb) <= max(nb, 1 + na):
+                self.to_acc(self.value(a, axes))
+                self.emit(I_PUSH)
+                self.to_acc(self.value(b, axes))
+                self.emit(I_BIN_POP, op, 0, 0)  # acc = op(pop=a, acc=b)
+            else:
+                self.to_acc(self.value(b, axes))
+                self.emit(I_PUSH)
+                self.to_acc(self.value(a, axes))
+                self.emit(I_BIN_POP, op, 0, 1)  # acc = op(acc=a, pop=b)
+            return ("acc",)
+        raise _Retry(n)
+
+    def to_acc(self, r):
+        if r[0] == "leaf":
+            self.emit(I_LOAD, k=r[1])
+
+    def eval_value(self, n, axes):
+        self._inline = set()
+        if self.need(n, axes) > MAX_STACK:
+            raise _Retry(self._deepest_child(n, axes))
+        self.to_acc(self.value(n, axes))
+
+    def eval_store(self, n, axes, out_buf: Buffer):
+        """Compute node `n` itself (even though it is materialised) and store it."""
+        self._inline = {n}
+        node = self.low.nodes[n]
+        if node.op in INDEX_OPS:
+            try:
+                inner = through_index_op(node, axes)
+            except Unexpressible:
+                raise _Retry(n)
+            self._inline = set()
+            r = self.value(node.inputs[0][0], inner)
+        else:
+            if self.need_root(n, axes) > MAX_STACK:
+                raise _Retry(self._deepest_child(n, axes))
+            r = self.value(n, axes)
+        self.to_acc(r)
+        self.emit(I_STORE, k=self.store_leaf(out_buf, axes))
+
+    def need_root(self, n, axes) -> int:
+        node = self.low.nodes[n]
+        saved = self.low.buf.pop(n)
+        try:
+            return self.need(n, axes)
+        finally:
+            self.low.buf[n] = saved
+
+    def _deepest_child(self, n, axes):
+        node = self.low.nodes[n]
+        kids = [r for r, _ in node.inputs if r not in self.low.buf]
+        return max(kids, key=lambda k: self.need(k, axes)) if kids else n
+
+    # -- encoding
+    def finalize_order(self):
+        """Reorder leaves: preloaded loads first, then other loads, then stores."""
+        loads = [i for i, s in enumerate(self.leaf_specs) if not s.is_store]
+        stores = [i for i, s in enumerate(self.leaf_specs) if s.is_store]
+        uses = {i: 0 for i in loads}
+        for cls, _, k, _ in self.code:
+            if cls in (I_LOAD, I_BIN_LEAF, I_PUSH_LOAD) and k in uses:
+                uses[k] += 1
+        mem = [i for i in loads if self.leaf_specs[i].buf.splat is None]
+        mem.sort(key=lambda i: -self.leaf_specs[i].buf.nbytes)
+        pre = mem[:MAX_PRELOAD]
+        rest = [i for i in loads if i not in pre]
+        new_order = pre + rest + stores
+        if len(new_order) > abi.MAX_LEAVES:
+            raise UnsupportedOp(f"fused group needs {len(new_order)} leaves (> {abi.MAX_LEAVES})")
+        remap = {old: new for new, old in enumerate(new_order)}
+        self.leaf_specs = [self.leaf_specs[i] for i in new_order]
+        code = []
+        for cls, op, k, swap in self.code:
+            if cls in (I_LOAD, I_BIN_LEAF, I_STORE, I_PUSH_LOAD):
+                k = remap[k]
+            code.append((cls, op, k, swap))
+        # peephole: PUSH; LOAD k  ->  PUSH_LOAD k
+        out = []
+        for ins in code:
+            if ins[0] == I_LOAD and out and out[-1][0] == I_PUSH:
+                out[-1] = (I_PUSH_LOAD, 0, ins[2], 0)
+            else:
+                out.append(ins)
+        self.code = out
+        if len(self.code) > abi.MAX_INSTR:
+            raise UnsupportedOp(f"fused program of {len(self.code)} instructions (> {abi.MAX_INSTR})")
+        return len(pre)
+
+    def args(self, mode, n_o, n_r, red_kind=0, split=1) -> abi.EwArgs:
+        npre = self.finalize_order()
+        a = abi.EwArgs()
+        a.n_o, a.n_r = n_o, n_r
+        a.ninstr = len(self.code)
+        a.nleaves = len(self.leaf_specs)
+        a.mode, a.red_kind, a.vec_axis, a.split = mode, red_kind, self.vec_src, split
+        a.npre = npre
+        for i, (cls, op, k, swap) in enumerate(self.code):
+            a.prog[i] = cls | (op << 8) | (k << 16) | (swap << 24)
+        return a
+
+    def finalize_fn(self, a: abi.EwArgs):
+        specs = list(self.leaf_specs)
+        red = self.red_out
+
+        def fin():
+            for i, s in enumerate(specs):
+                _encode_leaf(a.leaves[i], s)
+            if red is not None:
+                _encode_leaf(a.red_out, red)
+        return fin
+
+    def reads(self):
+        return [s.buf.key for s in self.leaf_specs if not s.is_store and s.buf.splat is None]
+
+    def writes(self):
+        w = [s.buf.key for s in self.leaf_specs if s.is_store]
+        if self.red_out is not None:
+            w.append(self.red_out.buf.key)
+        return w
+
+    def algo_bytes(self) -> int:
+        seen = set()
+        total = 0
+        for s in self.leaf_specs + ([self.red_out] if self.red_out else []):
+            if s.buf.splat is not None or (s.buf.key, s.is_store) in seen:
+                continue
+            seen.add((s.buf.key, s.is_store))
+            total += s.buf.nbytes
+        return total
+
+    _inline: set = set()
+
+
+def _encode_leaf(L: abi.Leaf, s: LeafSpec):
+    b = s.buf
+    if b.splat is not None:
+        L.mode = 1
+        L.splat = _splat_bits(b)
+        L.ndig = 0
+        L.vec = 2
+        return
+    L.mode = 0
+    L.ref = _buf_ref(b)
+    L.ndig = len(s.digits)
+    L.vec = s.vec
+    for i, (src, div, mod, stride) in enumerate(s.digits):
+        d = L.dig[i]
+        d.src = src
+        d.div_mul, d.div_sh = magic_u31(div)
+        if mod is None:
+            d.mod, d.mod_mul, d.mod_sh = 0, 0, 0
+        else:
+            d.mod = mod
+            d.mod_mul, d.mod_sh = magic_u31(mod)
+        d.stride = stride
+
+
+def lower(g: Function, layouts: dict, private: bool = False) -> Lowered:
+    return Lowering(g, layouts, private).run()

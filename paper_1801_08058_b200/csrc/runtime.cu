@@ -1,0 +1,331 @@
+// Executor behind the C ABI in include/gfb200.h.
+//
+// An executable owns: one device arena (the liveness-planned buffers of all
+// fused launches), the constant pool (uploaded once), a device pointer table
+// that kernels resolve tensor slots through, and a CUDA graph of the launch
+// list captured on the first run.  A run is: write this call's input/output
+// pointers into the table (one 8*(2+n_in+n_out)-byte H2D copy) and launch
+// the graph — the reference's per-instruction Python dispatch
+// (interpreter.py:208-230) becomes a single cudaGraphLaunch.
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gfb200.h"
+
+extern "C" const void* gfb_ew_kernel_ptr(int kind);
+extern "C" const void* gfb_simt_kernel_ptr(int kind);
+extern "C" const void* gfb_tc_kernel_ptr(int kind);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(GFB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+// ---- NCCL, loaded on demand so the library has no hard NCCL dependency ----
+typedef int ncclResult_t;
+typedef void* ncclComm_t;
+struct NcclApi {
+    bool loaded = false;
+    ncclResult_t (*GetUniqueId)(void*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, char[128], int) = nullptr;  // id passed by value in C
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+struct NcclUniqueId {
+    char internal[128];
+};
+typedef ncclResult_t (*InitRankFn)(ncclComm_t*, int, NcclUniqueId, int);
+
+int load_nccl() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.loaded) return GFB_OK;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* n : names)
+        if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return fail(GFB_ERR_NCCL, std::string("cannot dlopen libnccl.so.2: ") + dlerror());
+    g_nccl.GetUniqueId = (ncclResult_t(*)(void*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
+        return fail(GFB_ERR_NCCL, "libnccl is missing required symbols");
+    g_nccl.loaded = true;
+    return GFB_OK;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+    std::string msg = std::string(what) + " failed: ";
+    msg += g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : std::to_string(r);
+    return fail(GFB_ERR_NCCL, msg);
+}
+
+}  // namespace
+
+struct gfb_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+struct gfb_exe {
+    int device = 0;
+    void* arena = nullptr;
+    void* consts = nullptr;
+    void** dtab = nullptr;  // device pointer table
+    void** htab = nullptr;  // pinned staging copy of the table
+    cudaEvent_t tab_done = nullptr;
+    uint32_t n_in = 0, n_out = 0, n_slots = 0;
+    std::vector<gfb_launch> launches;
+    std::vector<const void*> fns;
+    std::vector<unsigned char> args;  // argument blocks, tab pointers patched in
+    bool use_graph = false;
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t capture_stream = nullptr;
+    gfb_comm* comm = nullptr;
+    std::mutex mu;
+};
+
+namespace {
+
+const void* kernel_for(uint32_t kind) {
+    if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EW_U8) return gfb_ew_kernel_ptr((int)kind);
+    if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64)
+        return gfb_simt_kernel_ptr((int)kind);
+    if (kind == GFB_K_DOT_TC32) return gfb_tc_kernel_ptr((int)kind);
+    return nullptr;
+}
+
+int launch_one(gfb_exe* e, size_t i, cudaStream_t s) {
+    const gfb_launch& L = e->launches[i];
+    void* blob = e->args.data() + L.arg_offset;
+    if (L.kind == GFB_K_ALLREDUCE) {
+        const gfb_allreduce_args* a = (const gfb_allreduce_args*)blob;
+        if (!e->comm) return fail(GFB_ERR_INVALID, "plan has an all-reduce but no communicator");
+        if (e->comm->nranks == 1) return GFB_OK;
+        void* ptr = (char*)((a->buf >> 56) == GFB_SLOT_ARENA ? e->arena : nullptr) + (a->buf & ((1ull << 56) - 1));
+        if ((a->buf >> 56) != GFB_SLOT_ARENA) return fail(GFB_ERR_INVALID, "all-reduce bucket must live in the arena");
+        ncclResult_t r = g_nccl.AllReduce(ptr, ptr, (size_t)a->count, a->dtype == 0 ? 7 /*ncclFloat32*/ : 8 /*ncclFloat64*/,
+                                          0 /*ncclSum*/, e->comm->comm, s);
+        if (r != 0) return nccl_fail(r, "ncclAllReduce");
+        return GFB_OK;
+    }
+    void* kargs[1] = {blob};
+    dim3 grid(L.grid[0], L.grid[1], L.grid[2]), block(L.block[0], L.block[1], L.block[2]);
+    cudaError_t err = cudaLaunchKernel(e->fns[i], grid, block, kargs, L.smem, s);
+    if (err != cudaSuccess)
+        return fail(GFB_ERR_CUDA, std::string("launch ") + std::to_string(i) + " (kind " + std::to_string(L.kind) +
+                                      "): " + cudaGetErrorString(err));
+    return GFB_OK;
+}
+
+int launch_all(gfb_exe* e, cudaStream_t s) {
+    for (size_t i = 0; i < e->launches.size(); ++i) {
+        int rc = launch_one(e, i, s);
+        if (rc != GFB_OK) return rc;
+    }
+    return GFB_OK;
+}
+
+int upload_table(gfb_exe* e, void* const* inputs, void* const* outputs, cudaStream_t s) {
+    CUDA_TRY(cudaEventSynchronize(e->tab_done));  // previous run consumed the staging copy
+    e->htab[GFB_SLOT_ARENA] = e->arena;
+    e->htab[GFB_SLOT_CONST] = e->consts;
+    for (uint32_t i = 0; i < e->n_in; ++i) e->htab[GFB_SLOT_IO + i] = inputs[i];
+    for (uint32_t j = 0; j < e->n_out; ++j) e->htab[GFB_SLOT_IO + e->n_in + j] = outputs[j];
+    CUDA_TRY(cudaMemcpyAsync(e->dtab, e->htab, sizeof(void*) * e->n_slots, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaEventRecord(e->tab_done, s));
+    return GFB_OK;
+}
+
+void release(gfb_exe* e) {
+    if (e->graph) cudaGraphExecDestroy(e->graph);
+    if (e->capture_stream) cudaStreamDestroy(e->capture_stream);
+    if (e->tab_done) cudaEventDestroy(e->tab_done);
+    if (e->htab) cudaFreeHost(e->htab);
+    if (e->dtab) cudaFree(e->dtab);
+    if (e->consts) cudaFree(e->consts);
+    if (e->arena) cudaFree(e->arena);
+    delete e;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gfb_last_error(void) { return g_err.c_str(); }
+
+int gfb_init(int device) {
+    int count = 0;
+    CUDA_TRY(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(GFB_ERR_INVALID, "device index out of range");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(GFB_ERR_UNSUPPORTED, std::string("need an sm_100 (B200) device, found ") + prop.name);
+    return GFB_OK;
+}
+
+int gfb_device_info(int* sm_major, int* sm_minor, int* num_sms) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+    *sm_major = prop.major;
+    *sm_minor = prop.minor;
+    *num_sms = prop.multiProcessorCount;
+    return GFB_OK;
+}
+
+int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
+    if (!plan || !out) return fail(GFB_ERR_INVALID, "null plan");
+    gfb_exe* e = new gfb_exe();
+    auto bail = [&](int rc) {
+        release(e);
+        return rc;
+    };
+    if (cudaGetDevice(&e->device) != cudaSuccess) return bail(fail(GFB_ERR_CUDA, "cudaGetDevice failed"));
+    e->n_in = plan->n_inputs;
+    e->n_out = plan->n_outputs;
+    e->n_slots = GFB_SLOT_IO + e->n_in + e->n_out;
+    e->use_graph = (plan->flags & GFB_PLAN_CUDA_GRAPH) != 0;
+    e->comm = (gfb_comm*)plan->comm;
+    cudaError_t err;
+    if (plan->arena_bytes && (err = cudaMalloc(&e->arena, plan->arena_bytes)) != cudaSuccess)
+        return bail(fail(GFB_ERR_CUDA, std::string("arena cudaMalloc: ") + cudaGetErrorString(err)));
+    if (plan->const_bytes) {
+        if ((err = cudaMalloc(&e->consts, plan->const_bytes)) != cudaSuccess)
+            return bail(fail(GFB_ERR_CUDA, std::string("constant pool cudaMalloc: ") + cudaGetErrorString(err)));
+        if ((err = cudaMemcpy(e->consts, plan->const_data, plan->const_bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return bail(fail(GFB_ERR_CUDA, std::string("constant upload: ") + cudaGetErrorString(err)));
+    }
+    if ((err = cudaMalloc(&e->dtab, sizeof(void*) * e->n_slots)) != cudaSuccess ||
+        (err = cudaMallocHost(&e->htab, sizeof(void*) * e->n_slots)) != cudaSuccess ||
+        (err = cudaEventCreateWithFlags(&e->tab_done, cudaEventDisableTiming)) != cudaSuccess ||
+        (err = cudaStreamCreateWithFlags(&e->capture_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(fail(GFB_ERR_CUDA, std::string("executable setup: ") + cudaGetErrorString(err)));
+    e->launches.assign(plan->launches, plan->launches + plan->n_launches);
+    e->args.assign((const unsigned char*)plan->args, (const unsigned char*)plan->args + plan->args_bytes);
+    e->fns.resize(e->launches.size(), nullptr);
+    for (size_t i = 0; i < e->launches.size(); ++i) {
+        const gfb_launch& L = e->launches[i];
+        if ((uint64_t)L.arg_offset + L.arg_size > plan->args_bytes || L.arg_size < sizeof(void*))
+            return bail(fail(GFB_ERR_INVALID, "launch argument block out of range"));
+        // Every argument block starts with the device pointer table.
+        std::memcpy(e->args.data() + L.arg_offset, &e->dtab, sizeof(void*));
+        if (L.kind == GFB_K_ALLREDUCE) {
+            if (!e->comm) return bail(fail(GFB_ERR_INVALID, "all-reduce launch without a communicator"));
+            continue;
+        }
+        e->fns[i] = kernel_for(L.kind);
+        if (!e->fns[i]) return bail(fail(GFB_ERR_INVALID, "unknown kernel kind " + std::to_string(L.kind)));
+        if (L.smem > 48 * 1024) {
+            err = cudaFuncSetAttribute(e->fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+            if (err != cudaSuccess) return bail(fail(GFB_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(err)));
+        }
+    }
+    *out = e;
+    return GFB_OK;
+}
+
+int gfb_exe_run(gfb_exe* e, void* const* inputs, void* const* outputs, void* stream) {
+    if (!e) return fail(GFB_ERR_INVALID, "null executable");
+    std::lock_guard<std::mutex> lk(e->mu);
+    cudaStream_t s = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    int rc = upload_table(e, inputs, outputs, s);
+    if (rc != GFB_OK) return rc;
+    if (!e->use_graph) return launch_all(e, s);
+    if (!e->graph) {
+        // Capture on a private stream: nothing executes during capture, and
+        // the instantiated graph is then launched on the caller's stream.
+        CUDA_TRY(cudaStreamBeginCapture(e->capture_stream, cudaStreamCaptureModeThreadLocal));
+        rc = launch_all(e, e->capture_stream);
+        cudaGraph_t g = nullptr;
+        cudaError_t end = cudaStreamEndCapture(e->capture_stream, &g);
+        if (rc != GFB_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (end != cudaSuccess) return fail(GFB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(end));
+        cudaError_t inst = cudaGraphInstantiate(&e->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (inst != cudaSuccess) return fail(GFB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(inst));
+    }
+    CUDA_TRY(cudaGraphLaunch(e->graph, s));
+    return GFB_OK;
+}
+
+int gfb_exe_run_one(gfb_exe* e, uint32_t index, void* const* inputs, void* const* outputs, void* stream) {
+    if (!e || index >= e->launches.size()) return fail(GFB_ERR_INVALID, "bad launch index");
+    std::lock_guard<std::mutex> lk(e->mu);
+    cudaStream_t s = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    int rc = upload_table(e, inputs, outputs, s);
+    if (rc != GFB_OK) return rc;
+    return launch_one(e, index, s);
+}
+
+int gfb_exe_num_launches(const gfb_exe* e) { return e ? (int)e->launches.size() : 0; }
+
+int gfb_exe_destroy(gfb_exe* e) {
+    if (!e) return GFB_OK;
+    cudaStreamSynchronize(cudaStreamPerThread);
+    release(e);
+    return GFB_OK;
+}
+
+int gfb_comm_unique_id(void* unique_id_128) {
+    int rc = load_nccl();
+    if (rc != GFB_OK) return rc;
+    ncclResult_t r = g_nccl.GetUniqueId(unique_id_128);
+    return r ? nccl_fail(r, "ncclGetUniqueId") : GFB_OK;
+}
+
+int gfb_comm_create(int nranks, int rank, const void* unique_id_128, gfb_comm** out) {
+    int rc = load_nccl();
+    if (rc != GFB_OK) return rc;
+    gfb_comm* c = new gfb_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    NcclUniqueId id;
+    std::memcpy(id.internal, unique_id_128, 128);
+    InitRankFn init = (InitRankFn)g_nccl.CommInitRank;
+    ncclResult_t r = init(&c->comm, nranks, id, rank);
+    if (r) {
+        delete c;
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    *out = c;
+    return GFB_OK;
+}
+
+int gfb_comm_destroy(gfb_comm* c) {
+    if (!c) return GFB_OK;
+    if (c->comm) g_nccl.CommDestroy(c->comm);
+    delete c;
+    return GFB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// Exact-order SIMT kernels for Dot and the convolution family.
+//
+// These keep the reference's accumulation order per output element —
+// Dot: k ascending (kernels.py:123-133); Conv2D: c, r, s (kernels.py:180-206);
+// ConvBackpropData: k, r, s (kernels.py:209-235); ConvBackpropFilter: n, p, q
+// (kernels.py:238-264) — with one IEEE round-to-nearest per multiply and per
+// add (no FMA), so F32/F64 results are bit-identical to the reference.  They
+// serve F64 graphs, small F32 contractions (launch-latency bound anyway) and
+// any shape the tcgen05 path does not take; large F32 Dots run on the tensor
+// cores (gemm_tc.cu) under the normwise tolerance of SURVEY.md §8(c).
+//
+// All operands are addressed through per-axis element strides, so the
+// transposing Reshapes autodiff emits for Dot (autodiff.py:163-177) and the
+// NCHW/NHWC layouts chosen by layout assignment are consumed in place.
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gfb_common.cuh"
+
+namespace gfb {
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// 64x64 output tile per 256-thread block, 4x4 per thread, K staged 16 at a time.
+template <typename T>
+__global__ void __launch_bounds__(256) gfb_dot_kernel(const __grid_constant__ gfb_dot_args p) {
+    constexpr int BM = 64, BN = 64, BK = 16;
+    __shared__ T As[BK][BM + 1];
+    __shared__ T Bs[BK][BN + 1];
+    const T* A = resolve<const T>(p.tab, p.a);
+    const T* B = resolve<const T>(p.tab, p.b);
+    T* C = resolve<T>(p.tab, p.c);
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    // Coalesce the tile loads along whichever axis is contiguous in memory.
+    const bool a_k_fast = p.a_sk <= p.a_sm;
+    const bool b_n_fast = p.b_sn <= p.b_sk;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+
+    for (int64_t k0 = 0; k0 < p.k; k0 += BK) {
+        const int kn = (int)min((int64_t)BK, p.k - k0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = tid + 256 * e;
+            int mm, kk;
+            if (a_k_fast) { mm = idx / BK; kk = idx % BK; } else { mm = idx % BM; kk = idx / BM; }
+            const int64_t gm = m0 + mm, gk = k0 + kk;
+            As[kk][mm] = (gm < p.m && kk < kn) ? A[gm * p.a_sm + gk * p.a_sk] : T(0);
+            int nn, kb;
+            if (b_n_fast) { nn = idx % BN; kb = idx / BN; } else { nn = idx / BK; kb = idx % BK; }
+            const int64_t gn = n0 + nn, gkb = k0 + kb;
+            Bs[kb][nn] = (gn < p.n && kb < kn) ? B[gkb * p.b_sk + gn * p.b_sn] : T(0);
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kn; ++kk) {
+            T a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = add_rn(acc[i][j], mul_rn(a[i], b[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gm = m0 + ty + 16 * i;
+        if (gm >= p.m) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gn = n0 + tx + 16 * j;
+            if (gn < p.n) C[gm * p.c_sm + gn * p.c_sn] = acc[i][j];
+        }
+    }
+}
+
+// One thread per output element, the reference loop nest verbatim.
+template <typename T>
+__global__ void __launch_bounds__(256) gfb_conv_kernel(const __grid_constant__ gfb_conv_args p) {
+    const T* X = resolve<const T>(p.tab, p.x);
+    const T* Y = resolve<const T>(p.tab, p.y);
+    T* O = resolve<T>(p.tab, p.out);
+    int64_t total;
+    if (p.op == 0) total = p.N * p.K * p.Ho * p.Wo;
+    else if (p.op == 1) total = p.N * p.C * p.H * p.W;
+    else total = p.K * p.C * p.R * p.S;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        T acc = T(0);
+        if (p.op == 0) {
+            // out[n,k,p,q] = sum_{c,r,s} x[n,c,p*sh-pt+r,q*sw-pl+s] * f[k,c,r,s]
+            const int64_t q = idx % p.Wo, pp = (idx / p.Wo) % p.Ho, k = (idx / (p.Wo * p.Ho)) % p.K,
+                          n = idx / (p.Wo * p.Ho * p.K);
+            for (int64_t c = 0; c < p.C; ++c)
+                for (int64_t r = 0; r < p.R; ++r) {
+                    const int64_t h = pp * p.sh - p.pt + r;
+                    if (h < 0 || h >= p.H) continue;
+                    for (int64_t s = 0; s < p.S; ++s) {
+                        const int64_t w = q * p.sw - p.pl + s;
+                        if (w < 0 || w >= p.W) continue;
+                        acc = add_rn(acc, mul_rn(X[n * p.xs[0] + c * p.xs[1] + h * p.xs[2] + w * p.xs[3]],
+                                                 Y[k * p.ys[0] + c * p.ys[1] + r * p.ys[2] + s * p.ys[3]]));
+                    }
+                }
+            O[n * p.os[0] + k * p.os[1] + pp * p.os[2] + q * p.os[3]] = acc;
+        } else if (p.op == 1) {
+            // out[n,c,h,w] = sum_{k,r,s} delta[n,k,h+pt-r,w+pl-s] * f[k,c,r,s]
+            const int64_t w = idx % p.W, h = (idx / p.W) % p.H, c = (idx / (p.W * p.H)) % p.C,
+                          n = idx / (p.W * p.H * p.C);
+            for (int64_t k = 0; k < p.K; ++k)
+                for (int64_t r = 0; r < p.R; ++r) {
+                    const int64_t pp = h + p.pt - r;
+                    if (pp < 0 || pp >= p.Ho) continue;
+                    for (int64_t s = 0; s < p.S; ++s) {
+                        const int64_t q = w + p.pl - s;
+                        if (q < 0 || q >= p.Wo) continue;
+                        acc = add_rn(acc, mul_rn(X[n * p.xs[0] + k * p.xs[1] + pp * p.xs[2] + q * p.xs[3]],
+                                                 Y[k * p.ys[0] + c * p.ys[1] + r * p.ys[2] + s * p.ys[3]]));
+                    }
+                }
+            O[n * p.os[0] + c * p.os[1] + h * p.os[2] + w * p.os[3]] = acc;
+        } else {
+            // out[k,c,r,s] = sum_{n,p,q} delta[n,k,p,q] * x[n,c,p+r-pt,q+s-pl]
+            const int64_t s = idx % p.S, r = (idx / p.S) % p.R, c = (idx / (p.S * p.R)) % p.C,
+                          k = idx / (p.S * p.R * p.C);
+            for (int64_t n = 0; n < p.N; ++n)
+                for (int64_t pp = 0; pp < p.Ho; ++pp) {
+                    const int64_t h = pp + r - p.pt;
+                    if (h < 0 || h >= p.H) continue;
+                    for (int64_t q = 0; q < p.Wo; ++q) {
+                        const int64_t w = q + s - p.pl;
+                        if (w < 0 || w >= p.W) continue;
+                        acc = add_rn(acc, mul_rn(Y[n * p.ys[0] + k * p.ys[1] + pp * p.ys[2] + q * p.ys[3]],
+                                                 X[n * p.xs[0] + c * p.xs[1] + h * p.xs[2] + w * p.xs[3]]));
+                    }
+                }
+            O[k * p.os[0] + c * p.os[1] + r * p.os[2] + s * p.os[3]] = acc;
+        }
+    }
+}
+
+template __global__ void gfb_dot_kernel<float>(const __grid_constant__ gfb_dot_args);
+template __global__ void gfb_dot_kernel<double>(const __grid_constant__ gfb_dot_args);
+template __global__ void gfb_conv_kernel<float>(const __grid_constant__ gfb_conv_args);
+template __global__ void gfb_conv_kernel<double>(const __grid_constant__ gfb_conv_args);
+
+}  // namespace gfb
+
+extern "C" const void* gfb_simt_kernel_ptr(int kind) {
+    switch (kind) {
+        case GFB_K_DOT_F32: return (const void*)gfb::gfb_dot_kernel<float>;
+        case GFB_K_DOT_F64: return (const void*)gfb::gfb_dot_kernel<double>;
+        case GFB_K_CONV_F32: return (const void*)gfb::gfb_conv_kernel<float>;
+        case GFB_K_CONV_F64: return (const void*)gfb::gfb_conv_kernel<double>;
+    }
+    return nullptr;
+}

@@ -1,0 +1,389 @@
+"""`compile_function` / `call` on the B200 (drop-in for the reference backend).
+
+Mirrors `/root/reference/pkg/src/graphforge/interpreter.py:92-245`:
+
+* `compile_function(fn, *, optimize=True, conv_layout="identity",
+  parameter_layouts=None)` validates (`ValidationFailure`), runs
+  simplify / cse / fold (folding through the device kernels), assigns
+  layouts, and records the reference's per-node instruction listing and
+  memory plan for compatibility.  It then lowers the graph to fused
+  launches (`compiler.py`) and creates the device executable through the
+  C ABI (`include/gfb200.h`, `libgfb200.so`).
+* `call(exe, inputs, *, private_buffers=False)` checks the signature
+  exactly like the reference (`SignatureMismatch` on descriptor or layout
+  order), uploads host inputs, runs the captured CUDA graph and returns
+  fresh result tensors that never alias inputs.  Device-resident
+  `TensorValue`s (CUDA `torch.Tensor` buffers) are consumed in place, and
+  `call(..., device=True)` leaves results on the GPU.
+
+There is no CPU execution path: if the library or a B200 is missing every
+entry point raises `BackendUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from collections.abc import Mapping
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .compiler import Lowered, lower
+from .errors import BackendUnavailable, DeviceError, SignatureMismatch, ValidationFailure
+from .ir import ConstantData, Function, OpKind, TensorDescriptor, reachable_from_results, topological_order, validate_function
+from .layout import Layout, assign_layouts, layout_policy, tensor_layouts
+from .memory import MemoryPlan, plan_memory
+from .rewrite import run_pipeline
+from .tensor import TensorValue, storage_to_logical, tensor_from_flat, torch_dtype
+
+_LIB = None
+_LOCK = threading.Lock()
+_DEVICE_READY: set = set()
+
+
+def library_path() -> str:
+    return os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgfb200.so")
+
+
+def lib():
+    """Load libgfb200.so (building it in-tree first if it is stale)."""
+    global _LIB
+    with _LOCK:
+        if _LIB is not None:
+            return _LIB
+        from . import _build
+
+        if not _build.up_to_date():
+            try:
+                _build.build()
+            except Exception as exc:  # no silent fallback: the backend is unusable
+                raise BackendUnavailable(f"cannot build libgfb200.so: {exc}") from exc
+        try:
+            L = C.CDLL(library_path())
+        except OSError as exc:
+            raise BackendUnavailable(f"cannot load {library_path()}: {exc}") from exc
+        vp, i32, u32 = C.c_void_p, C.c_int, C.c_uint32
+        L.gfb_init.argtypes = [i32]
+        L.gfb_last_error.restype = C.c_char_p
+        L.gfb_device_info.argtypes = [C.POINTER(i32)] * 3
+        L.gfb_exe_create.argtypes = [C.POINTER(abi.Plan), C.POINTER(vp)]
+        L.gfb_exe_run.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), vp]
+        L.gfb_exe_run_one.argtypes = [vp, u32, C.POINTER(vp), C.POINTER(vp), vp]
+        L.gfb_exe_destroy.argtypes = [vp]
+        L.gfb_exe_num_launches.argtypes = [vp]
+        L.gfb_comm_unique_id.argtypes = [vp]
+        L.gfb_comm_create.argtypes = [i32, i32, vp, C.POINTER(vp)]
+        L.gfb_comm_destroy.argtypes = [vp]
+        _LIB = L
+        return L
+
+
+def check(rc: int, what: str):
+    if rc != abi.GFB_OK:
+        msg = lib().gfb_last_error().decode(errors="replace")
+        raise DeviceError(f"{what}: {msg} (status {rc})")
+
+
+def ensure_device():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device visible; the B200 backend has no CPU fallback")
+    dev = torch.cuda.current_device()
+    if dev not in _DEVICE_READY:
+        check(lib().gfb_init(dev), "gfb_init")
+        _DEVICE_READY.add(dev)
+    return dev
+
+
+# ---------------------------------------------------------------------------
+# Executable
+
+
+@dataclass(frozen=True)
+class Instruction:
+    node_id: int
+    kernel: str
+    input_slots: tuple
+    output_slot: str
+
+
+class _ConstPool(Mapping):
+    """Constant pool as TensorValues, materialised lazily (splats stay scalars)."""
+
+    def __init__(self, g: Function, refs: list):
+        self._g = g
+        self._refs = list(refs)
+        self._cache: dict = {}
+
+    def __getitem__(self, ref):
+        if ref not in self._refs:
+            raise KeyError(ref)
+        if ref not in self._cache:
+            a = self._g.nodes[ref[0]].attrs
+            self._cache[ref] = tensor_from_flat(a["element_type"], a["shape"], a["data"].to_numpy())
+        return self._cache[ref]
+
+    def __iter__(self):
+        return iter(self._refs)
+
+    def __len__(self):
+        return len(self._refs)
+
+
+class DeviceProgram:
+    """Owner of one gfb_exe handle."""
+
+    def __init__(self, lowered: Lowered, cuda_graph: bool = True, comm=None):
+        self.lowered = lowered
+        recs, blob = lowered.pack()
+        self._recs, self._blob = recs, C.create_string_buffer(blob, max(1, len(blob)))
+        self._consts = C.create_string_buffer(lowered.const_blob, max(1, len(lowered.const_blob)))
+        plan = abi.Plan()
+        plan.arena_bytes = lowered.arena_bytes
+        plan.const_bytes = len(lowered.const_blob)
+        plan.const_data = C.cast(self._consts, C.c_void_p)
+        plan.n_inputs, plan.n_outputs = lowered.n_inputs, lowered.n_outputs
+        plan.n_launches = len(lowered.launches)
+        plan.flags = abi.PLAN_CUDA_GRAPH if cuda_graph else 0
+        plan.launches = C.cast(recs, C.POINTER(abi.Launch))
+        plan.args_bytes = len(blob)
+        plan.args = C.cast(self._blob, C.c_void_p)
+        plan.comm = comm
+        handle = C.c_void_p()
+        ensure_device()
+        check(lib().gfb_exe_create(C.byref(plan), C.byref(handle)), "gfb_exe_create")
+        self.handle = handle
+
+    def run(self, in_ptrs: list, out_ptrs: list, stream=None):
+        ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
+        outs = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
+        check(lib().gfb_exe_run(self.handle, ins, outs, stream), "gfb_exe_run")
+
+    def run_one(self, index: int, in_ptrs: list, out_ptrs: list, stream=None):
+        ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
+        outs = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
+        check(lib().gfb_exe_run_one(self.handle, index, ins, outs, stream), "gfb_exe_run_one")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _LIB is not None:
+            _LIB.gfb_exe_destroy(h)
+            self.handle = None
+
+
+class Executable:
+    """Compiled graph: the reference's attributes plus the device program."""
+
+    def __init__(self, function, instructions, plan, pool, layouts, param_index, result_index,
+                 parameter_signature, result_signature, lowered, cuda_graph=True, comm=None):
+        self.function = function
+        self.instructions = instructions
+        self.plan = plan
+        self.pool = pool
+        self.layouts = layouts
+        self.param_index = param_index
+        self.result_index = result_index
+        self.parameter_signature = parameter_signature
+        self.result_signature = result_signature
+        self.lowered = lowered
+        self._cuda_graph = cuda_graph
+        self._comm = comm
+        self._program = DeviceProgram(lowered, cuda_graph, comm)
+        self._private = None
+
+    def listing(self) -> str:
+        """Per-IR-node listing in the reference format (interpreter.py:82-89)."""
+        lines = [f"arena {self.plan.arena_size} bytes"]
+        for i, ins in enumerate(self.instructions):
+            lines.append(f"{i}\t{ins.node_id}\t{ins.kernel}\t{','.join(ins.input_slots) or '-'}\t{ins.output_slot}")
+        return "\n".join(lines) + "\n"
+
+    def launch_listing(self) -> str:
+        """What actually runs: one line per fused B200 launch."""
+        lines = [f"device arena {self.lowered.arena_bytes} bytes, {len(self.lowered.launches)} launches"]
+        for i, L in enumerate(self.lowered.launches):
+            lines.append(f"{i}\t{L.label}\tkind={L.kind}\tgrid={L.grid}\tbytes={L.algo_bytes}\tflops={L.flops}")
+        return "\n".join(lines) + "\n"
+
+    @property
+    def num_launches(self) -> int:
+        return len(self.lowered.launches)
+
+    def program(self, private: bool = False) -> DeviceProgram:
+        if not private:
+            return self._program
+        if self._private is None:
+            g = self.function
+            low = lower(g, self.layouts, private=True)
+            self._private = DeviceProgram(low, self._cuda_graph, self._comm)
+        return self._private
+
+    # -- device-level entry (inputs already resident; bench / DP path)
+    def run_device(self, inputs: list, outputs: list, stream=None, private: bool = False):
+        self.program(private).run([_ptr(t) for t in inputs], [_ptr(t) for t in outputs], stream)
+
+    def allocate_outputs(self):
+        import torch
+
+        return [torch.empty(int(np.prod(d.shape, dtype=np.int64)), dtype=torch_dtype(d.element_type), device="cuda")
+                for d, _ in self.result_signature]
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if t.numel() else 0
+
+
+def _build_listing(g: Function, plan: MemoryPlan):
+    """Reference instruction list + pool refs (interpreter.py:120-159)."""
+    reachable = reachable_from_results(g)
+    result_index: dict = {}
+    for j, ref in enumerate(g.results):
+        result_index.setdefault(ref, j)
+    param_index = {(pid, 0): i for i, pid in enumerate(g.parameters)}
+    pool_refs = []
+    instructions = []
+
+    def slot(ref):
+        if ref in param_index:
+            return f"param{param_index[ref]}"
+        if ref in pool_set:
+            return f"const{ref[0]}"
+        if ref in result_index:
+            return f"result{result_index[ref]}"
+        return f"arena+{plan.placements[ref]}"
+
+    pool_set = set()
+    for nid in topological_order(g):
+        if nid not in reachable:
+            continue
+        node = g.nodes[nid]
+        if node.op is OpKind.PARAMETER:
+            continue
+        if node.op is OpKind.CONSTANT:
+            pool_refs.append((nid, 0))
+            pool_set.add((nid, 0))
+            continue
+        instructions.append(Instruction(nid, node.op.wire_name, tuple(slot(r) for r in node.inputs), slot((nid, 0))))
+    return instructions, pool_refs, param_index, result_index
+
+
+@dataclass
+class HostCompiled:
+    """Everything compile_function decides on the host, before the device."""
+
+    graph: Function
+    layouts: dict
+    plan: MemoryPlan
+    instructions: list
+    pool_refs: list
+    param_index: dict
+    result_index: dict
+    parameter_signature: list
+    result_signature: list
+    lowered: Lowered
+
+    def listing(self) -> str:
+        return Executable.listing(self)
+
+
+def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = "identity",
+                     parameter_layouts=None, evaluate=None, private: bool = False) -> HostCompiled:
+    """Validate, optimise, assign layouts, plan and lower (reference
+    interpreter.py:92-170 plus the B200 lowering).  `evaluate` overrides the
+    constant-folding evaluator (the device by default)."""
+    diags = validate_function(fn)
+    if diags:
+        raise ValidationFailure(diags)
+    policy = layout_policy(conv_layout)
+    g = fn
+    if optimize:
+        g = run_pipeline(g, ["simplify", "cse", "fold"], evaluate=evaluate)
+    g = assign_layouts(g, policy, parameter_layouts)
+    layouts = tensor_layouts(g, policy, parameter_layouts)
+    plan = plan_memory(g)
+    instructions, pool_refs, param_index, result_index = _build_listing(g, plan)
+    param_sig = [(g.nodes[pid].output, layouts[(pid, 0)]) for pid in g.parameters]
+    result_sig = [(g.nodes[r].outputs[p], layouts[(r, p)]) for r, p in g.results]
+    lowered = lower(g, layouts, private=private)
+    return HostCompiled(g, layouts, plan, instructions, pool_refs, param_index, result_index,
+                        param_sig, result_sig, lowered)
+
+
+def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = "identity",
+                     parameter_layouts=None, cuda_graph: bool = True, comm=None) -> Executable:
+    h = prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=parameter_layouts)
+    return Executable(h.graph, h.instructions, h.plan, _ConstPool(h.graph, h.pool_refs), h.layouts,
+                      h.param_index, h.result_index, h.parameter_signature, h.result_signature,
+                      h.lowered, cuda_graph, comm)
+
+
+def _check_signature(exe: Executable, inputs: list):
+    expected = exe.parameter_signature
+    if len(inputs) != len(expected):
+        raise SignatureMismatch(f"expected {len(expected)} inputs, got {len(inputs)}")
+    for i, (t, (desc, layout)) in enumerate(zip(inputs, expected)):
+        if t.descriptor != desc:
+            raise SignatureMismatch(f"input {i}: expected {desc}, got {t.descriptor}")
+        if t.layout.order != layout.order:
+            raise SignatureMismatch(
+                f"input {i}: expected layout order {list(layout.order)}, got {list(t.layout.order)}"
+            )
+
+
+def to_device(t: TensorValue):
+    """Storage-order CUDA tensor for `t` (no copy when already resident)."""
+    import torch
+
+    if t.is_device:
+        return t.buffer
+    host = torch.from_numpy(np.ascontiguousarray(t.buffer))
+    return host.to("cuda", non_blocking=False)
+
+
+def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device: bool = False) -> list:
+    """Execute on the B200; one fresh result tensor per result."""
+    import torch
+
+    _check_signature(exe, inputs)
+    ensure_device()
+    dev_in = [to_device(t) for t in inputs]
+    outs = exe.allocate_outputs()
+    stream = torch.cuda.current_stream().cuda_stream
+    exe.run_device(dev_in, outs, stream=stream, private=private_buffers)
+    results = []
+    if device:
+        for (desc, layout), buf in zip(exe.result_signature, outs):
+            results.append(TensorValue(desc, layout, buf))
+        return results
+    torch.cuda.current_stream().synchronize()
+    for (desc, layout), buf in zip(exe.result_signature, outs):
+        results.append(TensorValue(desc, layout, buf.cpu().numpy()))
+    return results
+
+
+# ---------------------------------------------------------------------------
+# Constant folding through the device kernels (rewrite.constant_fold)
+
+
+_FOLD_CACHE: dict = {}
+
+
+def device_fold_evaluator(node, inputs: list, input_descs: list) -> ConstantData:
+    from .ir import attrs_key
+
+    key = (node.op, attrs_key(node), tuple(input_descs), node.output)
+    exe = _FOLD_CACHE.get(key)
+    if exe is None:
+        f = Function("fold")
+        params = [f.add_parameter(d.element_type, d.shape) for d in input_descs]
+        f.set_results([f.add_node(node.op, params, node.attrs, allow_internal=True)])
+        exe = compile_function(f, optimize=False)
+        if len(_FOLD_CACHE) < 256:
+            _FOLD_CACHE[key] = exe
+    tensors = [tensor_from_flat(d.element_type, d.shape, data.to_numpy()) for data, d in zip(inputs, input_descs)]
+    out = call(exe, tensors)[0]
+    return ConstantData.from_array(node.output.element_type, out.to_numpy().reshape(-1))

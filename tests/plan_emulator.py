@@ -1,0 +1,234 @@
+"""Host emulator of a lowered launch plan (TEST INFRASTRUCTURE).
+
+Executes the exact argument blocks `compiler.lower` produces — magic-number
+digit maps, VM programs, strides — on numpy buffers, so the fusion and
+index-map logic can be checked against the oracle on a GPU-less host.  It
+decodes the same `abi` structures the CUDA kernels read.  Reductions fold
+sequentially (the reference order), so emulated results are bit-comparable
+with the oracle; the GPU's tree orders are checked separately on the box.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_1801_08058_b200 import abi
+from paper_1801_08058_b200.compiler import (
+    I_BIN_LEAF, I_BIN_POP, I_BIN_SELF, I_LOAD, I_PUSH, I_PUSH_LOAD, I_STORE, I_UN,
+)
+
+DT = {abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
+      abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
+
+
+def _fdiv(n, mul, sh):
+    if mul == 0:
+        return n
+    return ((n.astype(np.uint64) * np.uint64(mul)) >> np.uint64(32 + sh)).astype(np.int64)
+
+
+def leaf_offsets(L, o, r):
+    off = np.zeros_like(o)
+    for i in range(L.ndig):
+        d = L.dig[i]
+        n = r if d.src else o
+        q = _fdiv(n, d.div_mul, d.div_sh)
+        if d.mod:
+            q = q - _fdiv(q, d.mod_mul, d.mod_sh) * d.mod
+        off = off + q * d.stride
+    return off
+
+
+class Memory:
+    def __init__(self, lowered, inputs, outputs):
+        self.slots = {abi.SLOT_ARENA: np.zeros(max(lowered.arena_bytes, 8), dtype=np.uint8),
+                      abi.SLOT_CONST: np.frombuffer(lowered.const_blob + b"\0" * 8, dtype=np.uint8).copy()}
+        for i, a in enumerate(inputs):
+            self.slots[abi.SLOT_IO + i] = a.view(np.uint8).reshape(-1)
+        for j, a in enumerate(outputs):
+            self.slots[abi.SLOT_IO + len(inputs) + j] = a.view(np.uint8).reshape(-1)
+
+    def view(self, ref, dtype):
+        slot, off = ref >> 56, ref & ((1 << 56) - 1)
+        raw = self.slots[slot]
+        item = np.dtype(dtype).itemsize
+        n = (raw.size - off) // item
+        return raw[off: off + n * item].view(dtype)
+
+
+def _un(op, a, dt):
+    with np.errstate(all="ignore"):
+        if op == 5:
+            return (-a).astype(dt) if dt != np.int64 else (np.uint64(0) - a.astype(np.uint64)).astype(np.int64)
+        x = a.astype(np.float64)
+        if op == 6:
+            y = np.exp(x)
+        elif op == 7:
+            y = np.where(x < 0, np.nan, np.where(x == 0, -np.inf, np.log(np.where(x > 0, x, 1.0))))
+            y = np.where(np.isnan(x), x, y)
+        elif op == 8:
+            y = np.tanh(x)
+        elif op == 9:
+            pos = 1.0 / (1.0 + np.exp(-np.where(x >= 0, x, 0.0)))
+            e = np.exp(np.where(x < 0, x, 0.0))
+            y = np.where(x >= 0, pos, e / (1.0 + e))
+            y = np.where(np.isnan(x), x, y)
+        elif op == 10:
+            return np.where(a > 0, a, np.zeros_like(a)).astype(dt)
+        else:
+            raise ValueError(op)
+        return y.astype(dt)
+
+
+def _bin(op, x, y, dt):
+    with np.errstate(all="ignore"):
+        if dt == np.int64:
+            ux, uy = x.astype(np.uint64), y.astype(np.uint64)
+            return {0: ux + uy, 1: ux - uy, 2: ux * uy}[op].astype(np.int64)
+        if op == 0:
+            return (x + y).astype(dt)
+        if op == 1:
+            return (x - y).astype(dt)
+        if op == 2:
+            return (x * y).astype(dt)
+        if op == 3:
+            return (x / y).astype(dt)
+        if op == 4:
+            return np.where(x >= y, x, y).astype(dt)
+    raise ValueError(op)
+
+
+def run_ew(mem, a, dt):
+    n_o, n_r = a.n_o, a.n_r
+    if a.mode == 0:
+        o = np.arange(n_o, dtype=np.int64)
+        r = np.zeros_like(o)
+    else:
+        o = np.repeat(np.arange(n_o, dtype=np.int64), n_r)
+        r = np.tile(np.arange(n_r, dtype=np.int64), n_o)
+
+    def load(k):
+        L = a.leaves[k]
+        if L.mode == 1:
+            raw = np.array([L.splat], dtype=np.uint64)
+            if dt == np.float32:
+                v = raw.astype(np.uint32).view(np.float32)[0]
+            elif dt == np.uint8:
+                v = np.uint8(L.splat & 0xFF)
+            else:
+                v = raw.view(dt)[0]
+            return np.full(o.shape, v, dtype=dt)
+        return mem.view(L.ref, dt)[leaf_offsets(L, o, r)]
+
+    acc = None
+    stack = []
+    for pc in range(a.ninstr):
+        ins = a.prog[pc]
+        cls, op, k, swap = ins & 0xFF, (ins >> 8) & 0xFF, (ins >> 16) & 0xFF, ins >> 24
+        if cls == I_LOAD:
+            acc = load(k)
+        elif cls == I_PUSH_LOAD:
+            stack.append(acc)
+            acc = load(k)
+        elif cls == I_PUSH:
+            stack.append(acc)
+        elif cls == I_UN:
+            acc = _un(op, acc, dt)
+        elif cls == I_BIN_LEAF:
+            b = load(k)
+            acc = _bin(op, b, acc, dt) if swap else _bin(op, acc, b, dt)
+        elif cls == I_BIN_POP:
+            b = stack.pop()
+            acc = _bin(op, acc, b, dt) if swap else _bin(op, b, acc, dt)
+        elif cls == I_BIN_SELF:
+            acc = _bin(op, acc, acc, dt)
+        elif cls == I_STORE:
+            L = a.leaves[k]
+            mem.view(L.ref, dt)[leaf_offsets(L, o, r)] = acc
+        else:
+            raise ValueError(cls)
+    if a.mode == 0:
+        return
+    vals = acc.reshape(n_o, n_r) if (acc is not None and n_r) else np.zeros((n_o, 0), dtype=dt)
+    if a.red_kind == 2:
+        red = np.full(n_o, -np.inf, dtype=dt)
+        for j in range(n_r):
+            red = np.where(red >= vals[:, j], red, vals[:, j]).astype(dt)
+    else:
+        red = np.zeros(n_o, dtype=dt)
+        with np.errstate(all="ignore"):
+            for j in range(n_r):
+                red = (red.astype(np.uint64) + vals[:, j].astype(np.uint64)).astype(np.int64) if dt == np.int64 else (red + vals[:, j]).astype(dt)
+    oo = np.arange(n_o, dtype=np.int64)
+    mem.view(a.red_out.ref, dt)[leaf_offsets(a.red_out, oo, np.zeros_like(oo))] = red
+
+
+def run_dot(mem, a, dt):
+    A, B, Cm = mem.view(a.a, dt), mem.view(a.b, dt), mem.view(a.c, dt)
+    i = np.arange(a.m)[:, None]
+    j = np.arange(a.n)[None, :]
+    acc = np.zeros((a.m, a.n), dtype=dt)
+    for k in range(a.k):
+        acc = (acc + (A[i * a.a_sm + k * a.a_sk] * B[k * a.b_sk + j * a.b_sn]).astype(dt)).astype(dt)
+    Cm[i * a.c_sm + j * a.c_sn] = acc
+
+
+def _gather4(buf, shape, strides):
+    idx = np.zeros(shape, dtype=np.int64)
+    for ax in range(4):
+        sh = [1, 1, 1, 1]
+        sh[ax] = shape[ax]
+        idx = idx + np.arange(shape[ax]).reshape(sh) * strides[ax]
+    return buf[idx], idx
+
+
+def run_conv(mem, a, dt):
+    from oracle import interp
+
+    X, Y, O = mem.view(a.x, dt), mem.view(a.y, dt), mem.view(a.out, dt)
+    et = 0 if dt == np.float32 else 1
+    L = interp.lib()
+
+    def p(arr):
+        return arr.ctypes.data_as(interp.ctypes.c_void_p)
+
+    if a.op == 0:
+        x, _ = _gather4(X, (a.N, a.C, a.H, a.W), a.xs)
+        f, _ = _gather4(Y, (a.K, a.C, a.R, a.S), a.ys)
+        oshape = (a.N, a.K, a.Ho, a.Wo)
+        out = np.empty(oshape, dtype=dt)
+        x, f = np.ascontiguousarray(x), np.ascontiguousarray(f)
+        L.orc_conv2d(et, p(x), p(f), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.sh, a.sw, a.pt, a.pl, a.Ho, a.Wo)
+    elif a.op == 1:
+        d, _ = _gather4(X, (a.N, a.K, a.Ho, a.Wo), a.xs)
+        f, _ = _gather4(Y, (a.K, a.C, a.R, a.S), a.ys)
+        oshape = (a.N, a.C, a.H, a.W)
+        out = np.empty(oshape, dtype=dt)
+        d, f = np.ascontiguousarray(d), np.ascontiguousarray(f)
+        L.orc_conv_bwd_data(et, p(d), p(f), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.Ho, a.Wo, a.pt, a.pl)
+    else:
+        x, _ = _gather4(X, (a.N, a.C, a.H, a.W), a.xs)
+        d, _ = _gather4(Y, (a.N, a.K, a.Ho, a.Wo), a.ys)
+        oshape = (a.K, a.C, a.R, a.S)
+        out = np.empty(oshape, dtype=dt)
+        x, d = np.ascontiguousarray(x), np.ascontiguousarray(d)
+        L.orc_conv_bwd_filter(et, p(x), p(d), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.Ho, a.Wo, a.pt, a.pl)
+    _, idx = _gather4(O, oshape, a.os)
+    O[idx] = out
+
+
+def execute(lowered, inputs: list, out_specs: list) -> list:
+    """inputs: storage-order numpy arrays; out_specs: (dtype, count)."""
+    outputs = [np.zeros(max(c, 1), dtype=d) for d, c in out_specs]
+    mem = Memory(lowered, [np.ascontiguousarray(x).reshape(-1) for x in inputs], outputs)
+    for L in lowered.launches:
+        dt = DT.get(L.kind)
+        if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8):
+            run_ew(mem, L.args, dt)
+        elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64):
+            run_dot(mem, L.args, dt)
+        elif L.kind in (abi.K_CONV_F32, abi.K_CONV_F64):
+            run_conv(mem, L.args, dt)
+        else:
+            raise NotImplementedError(L.kind)
+    return [o[:c] for o, (_, c) in zip(outputs, out_specs)]

@@ -1,0 +1,191 @@
+"""B200 parity: the CUDA path against reference-generated goldens and the oracle.
+
+Tolerances (BASELINE.json north_star): index ops and
++ - x / Maximum / Relu are bit-exact; everything else within the
+reference's own corpus tolerance (`_graphgen.tolerance_for`: 1e-12 F64,
+1e-6 F32); Sum / Dot / Conv normwise 1e-5; end-to-end losses and gradients
+1e-4.  Every test runs through `compile_function` / `call` — the public
+API — and therefore through libgfb200.so.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+gf = pytest.importorskip("paper_1801_08058_b200")
+
+
+def _outs(exe, tensors, **kw):
+    return [t.to_numpy() for t in gf.call(exe, tensors, **kw)]
+
+
+def _tol(doc):
+    return 1e-12 if doc["element_type"] == "F64" else 1e-6
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_corpus(seed):
+    case = G.load("corpus.json.gz")[seed]
+    fn = G.fn_of(case["fn"])
+    tensors = [G.tensor_of(d) for d in case["inputs"]]
+    for optimize, key in ((True, "outputs_opt"), (False, "outputs_noopt")):
+        exe = gf.compile_function(fn, optimize=optimize)
+        outs = _outs(exe, tensors)
+        for o, w in zip(outs, case[key]):
+            assert G.max_abs_diff(o, G.logical(w)) <= _tol(w), (seed, key, o, G.logical(w))
+        # plan corruption check: private buffers are bit-identical
+        priv = _outs(exe, tensors, private_buffers=True)
+        for a, b in zip(outs, priv):
+            assert G.same_bits(a, b)
+        # determinism: a second run is bit-identical
+        for a, b in zip(outs, _outs(exe, tensors)):
+            assert G.same_bits(a, b)
+
+
+def test_corpus_f32_mostly_bit_exact():
+    exact = total = 0
+    for case in G.load("corpus.json.gz"):
+        if not any(d["element_type"] == "F32" for d in case["outputs_noopt"]):
+            continue
+        fn = G.fn_of(case["fn"])
+        exe = gf.compile_function(fn, optimize=False)
+        outs = _outs(exe, [G.tensor_of(d) for d in case["inputs"]])
+        for o, w in zip(outs, case["outputs_noopt"]):
+            if w["element_type"] == "F32":
+                total += 1
+                exact += G.same_bits(o, G.logical(w))
+    assert total > 0 and exact / total >= 0.9, (exact, total)
+
+
+@pytest.mark.parametrize("idx", range(12))
+def test_layouts(idx):
+    case = G.load("layouts.json.gz")[idx]
+    fn = G.fn_of(case["fn"])
+    if case["parameter_layouts"] is not None:
+        lays = [gf.Layout(tuple(o)) for o in case["parameter_layouts"]]
+        exe = gf.compile_function(fn, optimize=False, parameter_layouts=lays)
+    else:
+        exe = gf.compile_function(fn, conv_layout=case["conv_layout"])
+    outs = _outs(exe, [G.tensor_of(d) for d in case["inputs"]])
+    for o, w in zip(outs, case["outputs"]):
+        assert G.max_abs_diff(o, G.logical(w)) <= _tol(w)
+
+
+def test_gradient_graphs():
+    for case in G.load("gradients.json.gz"):
+        g = G.fn_of(case["grad_fn"])
+        exe = gf.compile_function(g, optimize=False)
+        for pt in case["points"]:
+            seed = gf.tensor_from_flat(gf.ElementType.F64, (), [1.0])
+            outs = _outs(exe, [G.tensor_of(d) for d in pt["inputs"]] + [seed])
+            for o, w in zip(outs, pt["grads"]):
+                assert G.max_abs_diff(o, G.logical(w)) <= 1e-12, case["name"]
+
+
+@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small"])
+def test_workloads(name):
+    case = next(c for c in G.load("workloads.json.gz") if c["name"] == name)
+    exe = gf.compile_function(G.fn_of(case["fn"]))
+    outs = _outs(exe, [G.tensor_of(d) for d in case["inputs"]])
+    for o, w in zip(outs, case["outputs"]):
+        w = G.logical(w)
+        assert G.normwise(o, w) <= 1e-5, (name, G.normwise(o, w))
+
+
+# ---- known answers (reference tests/test_interpreter.py:56-162) ------------
+
+F32, F64, I64, BOOL = gf.ElementType.F32, gf.ElementType.F64, gf.ElementType.I64, gf.ElementType.BOOL
+K = gf.OpKind
+
+
+def _single(kind, specs, attrs=None):
+    fn = gf.Function("op")
+    ps = [fn.add_parameter(et, sh) for et, sh in specs]
+    fn.set_results([fn.add_node(kind, ps, attrs)])
+    return gf.compile_function(fn, optimize=False)
+
+
+def _t(et, shape, vals):
+    return gf.tensor_from_flat(et, shape, vals)
+
+
+def test_known_answers():
+    exe = _single(K.DOT, [(F64, (2, 2)), (F64, (2, 2))])
+    assert gf.call(exe, [_t(F64, (2, 2), [1, 2, 3, 4]), _t(F64, (2, 2), [5, 6, 7, 8])])[0].to_flat() == [19.0, 22.0, 43.0, 50.0]
+    assert gf.call(_single(K.SIGMOID, [(F64, ())]), [_t(F64, (), [0.0])])[0].get(()) == 0.5
+    assert gf.call(_single(K.TANH, [(F64, ())]), [_t(F64, (), [0.0])])[0].get(()) == 0.0
+    assert gf.call(_single(K.RELU, [(F64, ())]), [_t(F64, (), [-2.0])])[0].get(()) == 0.0
+    v = gf.call(_single(K.DIVIDE, [(F64, (3,)), (F64, (3,))]), [_t(F64, (3,), [1.0, -1.0, 0.0]), _t(F64, (3,), [0.0] * 3)])[0].to_flat()
+    assert v[0] == math.inf and v[1] == -math.inf and math.isnan(v[2])
+    assert gf.call(_single(K.SIGMOID, [(F64, (2,))]), [_t(F64, (2,), [1000.0, -1000.0])])[0].to_flat() == [1.0, 0.0]
+    ramp = [float(i) for i in range(16)]
+    exe = _single(K.CONV2D, [(F64, (1, 1, 4, 4)), (F64, (1, 1, 3, 3))], {"strides": (1, 1), "padding": (0, 0, 0, 0)})
+    want = [float(sum(ramp[(p + r) * 4 + q + s] for r in range(3) for s in range(3))) for p in range(2) for q in range(2)]
+    assert gf.call(exe, [_t(F64, (1, 1, 4, 4), ramp), _t(F64, (1, 1, 3, 3), [1.0] * 9)])[0].to_flat() == want
+    exe = _single(K.CONV2D, [(F64, (1, 1, 2, 2)), (F64, (1, 1, 2, 2))], {"strides": (2, 2), "padding": (1, 1, 1, 1)})
+    assert gf.call(exe, [_t(F64, (1, 1, 2, 2), [1.0, 2.0, 3.0, 4.0]), _t(F64, (1, 1, 2, 2), [1.0] * 4)])[0].to_flat() == [1.0, 2.0, 3.0, 4.0]
+    exe = _single(K.MULTIPLY, [(I64, ()), (I64, ())])
+    assert gf.call(exe, [_t(I64, (), [2**62]), _t(I64, (), [4])])[0].get(()) == 0
+    exe = _single(K.NEGATE, [(I64, ())])
+    assert gf.call(exe, [_t(I64, (), [-(2**63)])])[0].get(()) == -(2**63)
+    exe = _single(K.BROADCAST, [(BOOL, (2,))], {"output_shape": (2, 2), "broadcast_axes": (0,)})
+    assert gf.call(exe, [_t(BOOL, (2,), [True, False])])[0].to_flat() == [True, False, True, False]
+    exe = _single(K.ADD, [(F32, ()), (F32, ())])
+    assert gf.call(exe, [_t(F32, (), [1.0]), _t(F32, (), [2.0**-30])])[0].get(()) == 1.0
+    exe = _single(K.SUM, [(F64, (0, 2))], {"reduction_axes": (0,), "reduction_kind": "max"})
+    assert gf.call(exe, [_t(F64, (0, 2), [])])[0].to_flat() == [-math.inf, -math.inf]
+    exe = _single(K.SUM, [(F64, (0, 2))], {"reduction_axes": (0,)})
+    assert gf.call(exe, [_t(F64, (0, 2), [])])[0].to_flat() == [0.0, 0.0]
+    exe = _single(K.DOT, [(F64, (2, 0)), (F64, (0, 3))])
+    assert gf.call(exe, [_t(F64, (2, 0), []), _t(F64, (0, 3), [])])[0].to_flat() == [0.0] * 6
+
+
+def test_f32_semantics_corner_cases():
+    # Maximum ties / NaN, Relu(-0) / Relu(NaN), subnormal sigmoid, relu-grad -0.0
+    exe = _single(K.MAXIMUM, [(F32, (4,)), (F32, (4,))])
+    out = gf.call(exe, [_t(F32, (4,), [0.0, -0.0, math.nan, 1.0]), _t(F32, (4,), [-0.0, 0.0, 1.0, math.nan])])[0].to_numpy()
+    assert np.signbit(out[0]) == False and np.signbit(out[1]) == True and out[2] == 1.0 and math.isnan(out[3])
+    out = gf.call(_single(K.RELU, [(F32, (2,))]), [_t(F32, (2,), [-0.0, math.nan])])[0].to_numpy()
+    assert out[0] == 0.0 and not np.signbit(out[0]) and out[1] == 0.0
+    s = gf.call(_single(K.SIGMOID, [(F32, ())]), [_t(F32, (), [-100.0])])[0].get(())
+    assert 0.0 < s < 1.2e-38  # subnormal survives: no FTZ
+    fn = gf.Function("relu")
+    x = fn.add_parameter(F32, (4,))
+    fn.set_results([fn.add_node(K.RELU, [x])])
+    g = gf.differentiate(fn, [x])
+    exe = gf.compile_function(g)
+    grad = gf.call(exe, [_t(F32, (4,), [-1.0, 0.0, 2.0, math.inf]), _t(F32, (4,), [1.0] * 4)])[0].to_numpy()
+    assert np.signbit(grad[0]) and grad[0] == 0.0 and grad[1] == 0.0 and grad[2] == 1.0 and grad[3] == 0.0
+
+
+def test_signature_errors():
+    from paper_1801_08058_b200.errors import SignatureMismatch
+
+    fn = gf.Function("f")
+    p = fn.add_parameter(F64, (2, 2))
+    fn.set_results([fn.add_node(K.NEGATE, [p])])
+    exe = gf.compile_function(fn)
+    with pytest.raises(SignatureMismatch):
+        gf.call(exe, [])
+    with pytest.raises(SignatureMismatch):
+        gf.call(exe, [_t(F64, (3,), [1, 2, 3])])
+    with pytest.raises(SignatureMismatch):
+        gf.call(exe, [gf.tensor_from_flat(F64, (2, 2), [1, 2, 3, 4], gf.Layout((1, 0)))])
+
+
+def test_results_do_not_alias_and_duplicates():
+    fn = gf.Function("dup")
+    p = fn.add_parameter(F64, (2,))
+    n = fn.add_node(K.NEGATE, [p])
+    fn.set_results([n, n, p])
+    src = _t(F64, (2,), [1.0, -2.0])
+    out = gf.call(gf.compile_function(fn), [src])
+    assert out[0].to_flat() == out[1].to_flat() == [-1.0, 2.0]
+    assert out[2].to_flat() == [1.0, -2.0]
+    out[2].buffer[0] = 99.0
+    assert src.to_flat() == [1.0, -2.0]

@@ -1,0 +1,54 @@
+"""Full-size BASELINE.json configs on the B200 against the C oracle.
+
+Config A (MLP 784-512-10, batch 128) runs at full size on the oracle in
+well under a second; config B at full size (64 Mi elements) too.  The
+oracle is itself pinned against the reference (tests/test_oracle.py).
+"""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import interp
+
+pytestmark = pytest.mark.gpu
+
+gf = pytest.importorskip("paper_1801_08058_b200")
+from paper_1801_08058_b200 import workloads as W  # noqa: E402
+
+
+def _run_step(step, seed=0):
+    shapes = W.parameter_shapes(step)
+    arrays = W.step_inputs(step, shapes, seed=seed)
+    want = interp.run_function(step.fn, arrays)
+    exe = gf.compile_function(step.fn)
+    outs = [t.to_numpy() for t in gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])]
+    return outs, want
+
+
+def test_config_A_full_size():
+    interp.set_threads(interp.max_threads())
+    outs, want = _run_step(W.mlp_step(gf, batch=128))
+    for o, w in zip(outs, want):
+        assert G.normwise(o, w) <= 1e-4, G.normwise(o, w)
+    assert abs(float(outs[-1]) - float(want[-1])) <= 1e-4 * max(1.0, abs(float(want[-1])))
+
+
+def test_config_C_reduced():
+    interp.set_threads(interp.max_threads())
+    outs, want = _run_step(W.cnn_step(gf, batch=4, image=16, channels=(3, 8, 16)))
+    for o, w in zip(outs, want):
+        assert G.normwise(o, w) <= 1e-4
+
+
+@pytest.mark.parametrize("rows", [257, 4096, 65536])
+def test_config_B(rows):
+    interp.set_threads(interp.max_threads())
+    fn = W.fused_chain(gf, rows=rows, cols=1024)
+    arrays = W.chain_inputs(rows, 1024)
+    want = interp.run_function(fn, arrays)
+    exe = gf.compile_function(fn)
+    assert exe.num_launches == 1  # the whole chain + row sum is one pass
+    outs = [t.to_numpy() for t in gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])]
+    assert G.same_bits(outs[0], want[0])  # elementwise chain: bit-exact
+    assert G.normwise(outs[1], want[1]) <= 1e-5  # tree-ordered row sums

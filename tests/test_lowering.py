@@ -1,0 +1,64 @@
+"""Fusion / index-map lowering checked on the host emulator against goldens.
+
+The emulator executes the exact launch argument blocks the B200 receives
+(magic-number digit maps, VM programs, strides) with sequential folds, so
+every corpus graph must reproduce the reference interpreter's optimised
+outputs.  F32 results must be bit-identical; F64 results may differ only
+through libm-vs-numpy transcendentals (<= 1e-12, the reference corpus
+tolerance, `_graphgen.tolerance_for`).
+"""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from hostcompile import emulate, host_compile
+
+
+def _compare(outs, want_docs, label):
+    for o, w in zip(outs, want_docs):
+        w = G.logical(w)
+        if w.dtype == np.float64:
+            assert G.max_abs_diff(o, w) <= 1e-12, (label, o, w)
+        else:
+            assert G.same_bits(o, w), (label, o, w)
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_corpus_emulated(seed):
+    case = G.load("corpus.json.gz")[seed]
+    fn = G.fn_of(case["fn"])
+    tensors = [G.tensor_of(d) for d in case["inputs"]]
+    h = host_compile(fn)
+    _compare(emulate(h, tensors), case["outputs_opt"], seed)
+    h2 = host_compile(fn, optimize=False, private=(seed % 2 == 0))
+    _compare(emulate(h2, tensors), case["outputs_noopt"], seed)
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_listing_matches_reference(seed):
+    case = G.load("corpus.json.gz")[seed]
+    fn = G.fn_of(case["fn"])
+    assert host_compile(fn).listing() == case["listing_opt"]
+    assert host_compile(fn, optimize=False).listing() == case["listing_noopt"]
+
+
+@pytest.mark.parametrize("idx", range(12))
+def test_layout_cases(idx):
+    case = G.load("layouts.json.gz")[idx]
+    fn = G.fn_of(case["fn"])
+    h = host_compile(fn, optimize=case["conv_layout"] != "identity" or case["parameter_layouts"] is None,
+                     conv_layout=case["conv_layout"], parameter_layouts=case["parameter_layouts"])
+    if case["parameter_layouts"] is not None:
+        h = host_compile(fn, optimize=False, parameter_layouts=case["parameter_layouts"])
+    assert h.listing() == case["listing"]
+    _compare(emulate(h, [G.tensor_of(d) for d in case["inputs"]]), case["outputs"], case["name"])
+
+
+@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small"])
+def test_workloads_emulated(name):
+    case = next(c for c in G.load("workloads.json.gz") if c["name"] == name)
+    fn = G.fn_of(case["fn"])
+    h = host_compile(fn)
+    assert h.listing() == case["listing"]
+    _compare(emulate(h, [G.tensor_of(d) for d in case["inputs"]]), case["outputs"], name)
