@@ -1,0 +1,334 @@
+"""Benchmark driver (one JSON line on rank 0).
+
+Default workload = BASELINE.json configs[1] (config B): the fused
+elementwise / Broadcast / Sum chain over 64 Mi-element fp32 tensors,
+`t3 = Relu(a + Broadcast(c)) * b`, results t3 and its row sums, executed
+through `compile_function` / the C ABI as ONE fused launch per step.
+Metric: fused-op HBM GB/s = algorithmic bytes per step (SURVEY.md §8(d):
+805,572,608 B) / step time.  Inputs (805 MB) exceed the 126 MB L2, so no
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload B|A]
+
+N > 1 (torchrun): config B shards by rows with no collective, each rank
+processing its own 64 Mi-element chain (weak scaling); value = all ranks'
+bytes / max-over-ranks time.  `--impl reference` times the reference
+semantics on the host CPU (the C oracle port, all host threads) on the same
+config; under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+ROWS, COLS = 65536, 1024
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1590.0)), "measured"
+    except Exception:
+        return FALLBACK_HBM, 1590.0, "fallback"
+
+
+def chain_bytes(rows, cols, esize=4):
+    # read a, b (rows*cols each) + c (cols); write t3 (rows*cols) + sums (rows)
+    return esize * (3 * rows * cols + cols + rows)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is busy."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._drain, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _drain(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference(rows, cols, steps, warmup, budget_s=120.0):
+    """Reference semantics on the host: the oracle (C restatement of the
+    reference kernels) over the fused chain, all host threads."""
+    import paper_1801_08058_b200 as gf
+    from oracle import interp
+    from paper_1801_08058_b200 import workloads as W
+
+    threads = interp.max_threads()
+    interp.set_threads(threads)
+    sample_rows = rows
+
+    def one(r):
+        fn = W.fused_chain(gf, rows=r, cols=cols)
+        arrays = W.chain_inputs(r, cols)
+        t0 = time.perf_counter()
+        interp.run_function(fn, arrays)
+        return time.perf_counter() - t0
+
+    probe = one(min(rows, 4096)) * (rows / min(rows, 4096))
+    per_step_budget = budget_s / max(1, steps + warmup)
+    if probe > per_step_budget:
+        sample_rows = max(256, int(rows * per_step_budget / probe) // 256 * 256)
+    for _ in range(warmup):
+        one(sample_rows)
+    times = [one(sample_rows) for _ in range(steps)]
+    t = float(np.mean(times))
+    return chain_bytes(sample_rows, cols) / t / 1e9, threads, f"config B sample [{sample_rows},{cols}] per step, {steps} steps"
+
+
+def bench_chain(args, ws, rank, local):
+    import torch
+
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import workloads as W
+    from paper_1801_08058_b200.runtime import pinned_tensor
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fn = W.fused_chain(gf, rows=ROWS, cols=COLS)
+    exe = gf.compile_function(fn)
+    arrays = W.chain_inputs(ROWS, COLS, seed=1 + rank)
+    dev_in = [torch.from_numpy(a.reshape(-1)).cuda() for a in arrays]
+    outs = exe.allocate_outputs()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    nbytes = chain_bytes(ROWS, COLS)
+    launches_per_step = exe.num_launches
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            exe.run_device(dev_in, outs, stream=sh)
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            exe.run_device(dev_in, outs, stream=sh)
+        t1.record(stream)
+        barrier()
+        ms = t0.elapsed_time(t1) / args.steps
+        # dominant kernel alone, same stream, for the roofline
+        dom = max(range(launches_per_step), key=lambda i: exe.lowered.launches[i].algo_bytes)
+        prog = exe.program()
+        ptr_in = [t.data_ptr() for t in dev_in]
+        ptr_out = [t.data_ptr() for t in outs]
+        for _ in range(3):
+            prog.run_one(dom, ptr_in, ptr_out, sh)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        kreps = max(10, args.steps)
+        for _ in range(kreps):
+            prog.run_one(dom, ptr_in, ptr_out, sh)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        kernel_ms = k0.elapsed_time(k1) / kreps
+    ms_t = torch.tensor([ms], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # end to end through the public API: pinned host inputs -> call() -> pinned host results
+    host_in = []
+    for a in arrays:
+        t = pinned_tensor(gf.ElementType.F32, a.shape)
+        t.buffer[:] = a.reshape(-1)
+        host_in.append(t)
+    host_out = [pinned_tensor(d.element_type, d.shape) for d, _ in exe.result_signature]
+    e2e_steps = max(3, min(20, args.steps))
+    for _ in range(2):
+        gf.call(exe, host_in, out=host_out)
+    barrier()
+    e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        gf.call(exe, host_in, out=host_out)
+    e2e_s = (time.perf_counter() - e0) / e2e_steps
+    e2e_t = torch.tensor([e2e_s], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    h2d = sum(a.nbytes for a in arrays)
+    d2h = sum(t.buffer.nbytes for t in host_out)
+
+    hbm, _, peak_src = peaks()
+    achieved = nbytes / (kernel_ms * 1e-3) / 1e9
+    line = {
+        "metric": "fused-op HBM GB/s (config B: Relu(a+Broadcast(c))*b + row Sum, 64Mi fp32)",
+        "value": ws * nbytes / (ms * 1e-3) / 1e9,
+        "unit": "GB/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (numpy PCG64 seeded U(-1,1))",
+        "config": {"workload": "B: fused_chain rows=65536 cols=1024 per GPU", "bytes_per_step_per_gpu": nbytes,
+                   "l2": "inputs 805 MB > 126 MB L2, no flush needed", "parallelism": f"replicas x{ws} (row shards, no collective)"},
+        "e2e": {"value": ws * nbytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s * 1e3, "api": "paper_1801_08058_b200.call(exe, pinned host tensors, out=pinned host tensors)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": _traffic("B"), "kernel": exe.lowered.launches[dom].label, "kernel_ms": kernel_ms,
+                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    return line
+
+
+def _traffic(workload):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(workload)
+    except Exception:
+        return None
+
+
+def bench_mlp(args, ws, rank, local):
+    """Config A training step (fwd + autodiff bwd + SGD), samples/s."""
+    import torch
+
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    step = W.mlp_step(gf, batch=128)
+    exe = gf.compile_function(step.fn)
+    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=0)
+    dev_in = [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for a in arrays]
+    outs = exe.allocate_outputs()
+    stream = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            exe.run_device(dev_in, outs, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            exe.run_device(dev_in, outs, stream=stream.cuda_stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    flops = sum(L.flops for L in exe.lowered.launches)
+    return {
+        "metric": "training-step samples/sec (config A: MLP 784-512-10, batch 128, fwd+autodiff bwd+SGD)",
+        "value": 128 / (ms * 1e-3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": "A: mlp_step batch=128 784-512-10", "launches": exe.num_launches,
+                                        "flops_per_step": flops},
+        "gpu_launches": exe.num_launches * args.steps, "clocks": clk.summary(),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="B", choices=["B", "A"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        value, threads, sample = cpu_reference(ROWS, COLS, args.steps, args.warmup)
+        line = {
+            "impl": "reference", "metric": "fused-op HBM GB/s (config B: Relu(a+Broadcast(c))*b + row Sum, 64Mi fp32)",
+            "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "B: fused_chain rows=65536 cols=1024 per GPU"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_mlp(args, ws, rank, local)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "B":
+        value, threads, sample = cpu_reference(ROWS, COLS, 2, 1, budget_s=30.0)
+        line["cpu_baseline"] = {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

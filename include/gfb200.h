@@ -93,22 +93,30 @@ typedef struct {
     int32_t mode;   /* 0 = memory, 1 = splat constant (no memory access) */
     int32_t ndig;
     int32_t vec;    /* along the launch's vector axis: 0 gather, 1 contiguous, 2 uniform */
-    int32_t pad;
+    int32_t rlin;   /* r-part of the offset is r * rlin (0: no r digits); -1: general digits */
     gfb_digit dig[GFB_MAX_DIGITS];
 } gfb_leaf;
 
-/* Fused elementwise / broadcast / reduce launch (one VM program). */
+/* Fused elementwise / broadcast / reduce launch (one VM program).
+ * The launch iterates a 2-level index space (o, r), o < n_o, r < n_r.  Each
+ * thread evaluates the program on a vector of V consecutive indices (V = 8
+ * for 1/4-byte types, 4 for 8-byte types) along r (ROW mode: one warp, or
+ * `wpr` warps, per o) or along o (COL mode: r looped per thread, split
+ * `split` ways).  red_kind 0 = map (values leave only through STOREs),
+ * 1 = sum over r, 2 = max over r into red_out. */
 typedef struct {
     const void* const* tab; /* patched by gfb_exe_create */
-    uint32_t n_o;           /* output-space extent */
-    uint32_t n_r;           /* reduced extent (1 for a map) */
+    uint32_t n_o;
+    uint32_t n_r;
     uint32_t ninstr;
     uint32_t nleaves;
-    int32_t mode;     /* 0 map, 1 row reduce (lanes over r), 2 column reduce (lanes over o) */
-    int32_t red_kind; /* 1 sum, 2 max */
-    int32_t vec_axis; /* 0: vectors run along o, 1: along r */
-    int32_t split;    /* column reduce: threads splitting r per output group */
+    int32_t mode;     /* 1 ROW (vectors along r), 2 COL (vectors along o) */
+    int32_t red_kind; /* 0 map, 1 sum, 2 max */
+    int32_t vec_axis; /* 1 for ROW, 0 for COL */
+    int32_t split;    /* COL: threads splitting r per output vector */
     int32_t npre;     /* leaves 0..npre-1 (<= 4) are loaded up front, all in flight at once */
+    int32_t depth;    /* max stack depth of the program (stack lives in shared memory) */
+    int32_t wpr;      /* ROW: warps cooperating on one o */
     int32_t pad;
     uint32_t prog[GFB_MAX_INSTR];
     gfb_leaf leaves[GFB_MAX_LEAVES];

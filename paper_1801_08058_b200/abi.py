@@ -36,7 +36,7 @@ class Digit(C.Structure):
 class Leaf(C.Structure):
     _fields_ = [
         ("ref", C.c_uint64), ("splat", C.c_uint64),
-        ("mode", C.c_int32), ("ndig", C.c_int32), ("vec", C.c_int32), ("pad", C.c_int32),
+        ("mode", C.c_int32), ("ndig", C.c_int32), ("vec", C.c_int32), ("rlin", C.c_int32),
         ("dig", Digit * MAX_DIGITS),
     ]
 
@@ -46,7 +46,7 @@ class EwArgs(C.Structure):
         ("tab", C.c_void_p),
         ("n_o", C.c_uint32), ("n_r", C.c_uint32), ("ninstr", C.c_uint32), ("nleaves", C.c_uint32),
         ("mode", C.c_int32), ("red_kind", C.c_int32), ("vec_axis", C.c_int32), ("split", C.c_int32),
-        ("npre", C.c_int32), ("pad", C.c_int32),
+        ("npre", C.c_int32), ("depth", C.c_int32), ("wpr", C.c_int32), ("pad", C.c_int32),
         ("prog", C.c_uint32 * MAX_INSTR),
         ("leaves", Leaf * MAX_LEAVES),
         ("red_out", Leaf),

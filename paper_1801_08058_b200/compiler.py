@@ -182,22 +182,56 @@ def make_digits(buf: Buffer, axes, extents) -> list:
     return out
 
 
-def vec_class(digits, vec_src: int, is_store: bool) -> int:
-    """0 gather, 1 contiguous (128-bit access), 2 uniform (one value per vector)."""
+def vec_width(et: ElementType) -> int:
+    """Elements per thread-vector in the VM kernel (32 bytes, or 8 for BOOL)."""
+    return 4 if et.byte_size == 8 else 8
+
+
+def vec_class(digits, vec_src: int, is_store: bool, V: int, esize: int) -> int:
+    """0 gather, 1 contiguous (vector access), 2 uniform (one value per vector).
+
+    Vectors are V consecutive indices of `vec_src` starting at a multiple of
+    V; contiguous access also needs the base element offset aligned to the
+    16-byte (8-byte for BOOL) memory transaction.
+    """
+    align = max(1, (8 if esize == 1 else 16) // esize)
     own = [d for d in digits if d[0] == vec_src]
     unit = [d for d in own if d[1] == 1]
-    if any(d[1] % 4 for d in own if d[1] != 1):
+    if any(d[1] % V for d in own if d[1] != 1):
         return 0
     if not unit:
         return 0 if is_store else 2
     if len(unit) != 1:
         return 0
     _, _, mod, stride = unit[0]
-    if stride != 1 or (mod is not None and mod % 4):
+    if stride != 1 or (mod is not None and mod % V):
         return 0
-    if any(d[3] % 4 for d in digits if d is not unit[0]):
+    if any(d[3] % align for d in digits if d is not unit[0]):
         return 0
     return 1
+
+
+def r_linear(digits) -> int:
+    """Stride of the r-part when it is one linear digit, 0 without r, -1 otherwise."""
+    rd = [d for d in digits if d[0] == 1]
+    if not rd:
+        return 0
+    if len(rd) == 1 and rd[0][1] == 1 and rd[0][2] is None:
+        return rd[0][3]
+    return -1
+
+
+def split_axes(shape, inner_from: int) -> list:
+    """Axis expressions with axes < inner_from on o (src 0), the rest on r (src 1)."""
+    out = []
+    for a, d in enumerate(shape):
+        if d == 1:
+            out.append(None)
+        elif a < inner_from:
+            out.append((0, _prod(shape[a + 1:inner_from]), d))
+        else:
+            out.append((1, _prod(shape[a + 1:]), d))
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -476,19 +510,57 @@ class Lowering:
         return True
 
     # -- fused VM groups
+    def _row_launch(self, prog, n_o, n_r, red_kind, label, et):
+        """ROW: warps per o, vectors along r; more warps per o when o is short."""
+        V = vec_width(et)
+        wpr = 1
+        while wpr < 8 and n_o * wpr < 2 * NUM_SMS * 8 and n_r >= 32 * V * wpr * 2:
+            wpr *= 2
+        rpb = 8 // wpr
+        grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
+        args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)
+        self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
+
+    def _col_launch(self, prog, n_o, n_r, red_kind, label, et):
+        """COL: one thread per V-vector of o, r looped (split when o is short)."""
+        V = vec_width(et)
+        vectors = (n_o + V - 1) // V
+        split = 1
+        if red_kind and n_r > 16:
+            while split < 64 and ((vectors * split + 255) // 256) < 2 * NUM_SMS and n_r // (split * 2) >= 8:
+                split *= 2
+        per_row = 256 // split
+        grid = max(1, min((vectors + per_row - 1) // per_row, NUM_SMS * 16))
+        args = prog.args(mode=2, n_o=n_o, n_r=n_r, red_kind=red_kind, split=split)
+        self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
+
     def emit_map(self, root: int, stores: list):
         node = self.nodes[root]
-        shape = node.output.shape
-        n_o = element_count(shape)
-        prog = Program(self, extents=(max(n_o, 1), 1), vec_src=0)
-        axes = iteration_axes(shape)
-        prog.eval_store(root, axes, self.buf[root])
-        if n_o == 0:
+        shape = tuple(node.output.shape)
+        et = node.output.element_type
+        total = element_count(shape)
+        if total == 0:
             return
-        args = prog.args(mode=0, n_o=n_o, n_r=1)
-        groups = (n_o + 3) // 4
-        grid = max(1, min((groups + 255) // 256, NUM_SMS * 16))
-        self.add_launch(EW_KIND[node.output.element_type], (grid, 1, 1), (256, 1, 1), 0, args, prog, f"map:{node.op.wire_name}#{root}")
+        # Split the iteration space into rows (o) x contiguous columns (r)
+        # when the trailing extent is long enough for warp-wide vectors.
+        inner_from = len(shape)
+        while inner_from > 0 and _prod(shape[inner_from:]) < 256:
+            inner_from -= 1
+        n_r = _prod(shape[inner_from:])
+        if n_r >= 128 and inner_from < len(shape):
+            n_o = total // n_r
+            prog = Program(self, extents=(max(n_o, 1), n_r), vec_src=1, et=et)
+            try:
+                prog.eval_store(root, split_axes(shape, inner_from), self.buf[root])
+            except _Retry:
+                prog = None  # a Reshape straddles the row split: use the flat form
+            if prog is not None:
+                self._row_launch(prog, n_o, n_r, 0, f"map:{node.op.wire_name}#{root}", et)
+                return
+        if True:
+            prog = Program(self, extents=(total, 1), vec_src=0, et=et)
+            prog.eval_store(root, iteration_axes(shape), self.buf[root])
+            self._col_launch(prog, total, 1, 0, f"map:{node.op.wire_name}#{root}", et)
 
     def emit_reduce(self, s: int, side: int | None):
         node = self.nodes[s]
@@ -508,57 +580,43 @@ class Lowering:
             d = in_shape[a]
             in_axes[a] = None if d == 1 else (1, _prod(in_shape[k] for k in axes_red[i + 1:]), d)
         et = node.output.element_type
-        # choose orientation from the dominant load's contiguity
-        row = self._prefer_rows(src, in_axes, n_o, n_r)
-        prog = Program(self, extents=(max(n_o, 1), max(n_r, 1)), vec_src=1 if row else 0)
+        row = self._prefer_rows(src, in_axes, n_o, n_r, et)
+        prog = Program(self, extents=(max(n_o, 1), max(n_r, 1)), vec_src=1 if row else 0, et=et)
         if side is not None:
             prog.eval_store(side, in_axes, self.buf[side])
         elif n_r > 0:
             prog.eval_value(src, in_axes)
-        out_b = self.buf[s]
-        prog.set_red_out(out_b, iteration_axes(node.output.shape))
+        prog.set_red_out(self.buf[s], iteration_axes(node.output.shape))
         kind = 2 if node.attrs["reduction_kind"] == "max" else 1
         if row:
-            args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=kind)
-            grid = max(1, min((n_o + 7) // 8, NUM_SMS * 16))
-            self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), 0, args, prog, f"rowsum#{s}")
+            self._row_launch(prog, n_o, n_r, kind, f"rowsum#{s}", et)
         else:
-            groups = (n_o + 3) // 4
-            split = 1
-            if n_r > 16:
-                while split < 64 and ((groups * split + 255) // 256) < 2 * NUM_SMS and n_r // (split * 2) >= 8:
-                    split *= 2
-            per_row = 256 // split
-            grid = max(1, (groups + per_row - 1) // per_row)
-            smem = 256 * 4 * et.byte_size if split > 1 else 0
-            args = prog.args(mode=2, n_o=n_o, n_r=n_r, red_kind=kind, split=split)
-            self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), smem, args, prog, f"colsum#{s}")
+            self._col_launch(prog, n_o, n_r, kind, f"colsum#{s}", et)
 
-    def _prefer_rows(self, src, in_axes, n_o, n_r) -> bool:
+    def _prefer_rows(self, src, in_axes, n_o, n_r, et) -> bool:
         if n_r < 32:
             return False
-        probe = Program(self, extents=(max(n_o, 1), max(n_r, 1)), vec_src=1, dry=True)
+        probe = Program(self, extents=(max(n_o, 1), max(n_r, 1)), vec_src=1, et=et, dry=True)
         try:
             probe.eval_value(src, in_axes)
         except _Retry:
             return n_r >= 128
-        best = max(probe.leaf_specs, key=lambda l: l.buf.nbytes if l.buf.splat is None else -1, default=None)
-        if best is None or best.buf.splat is not None:
+        mem = [l for l in probe.leaf_specs if l.buf.splat is None]
+        if not mem:
             return True
+        best = max(mem, key=lambda l: l.buf.nbytes)
         return any(d[0] == 1 and d[1] == 1 and d[3] == 1 for d in best.digits)
 
     def emit_copy(self, src: Buffer, dst: Buffer):
         n_o = element_count(dst.shape)
         if n_o == 0:
             return
-        prog = Program(self, extents=(n_o, 1), vec_src=0)
+        prog = Program(self, extents=(n_o, 1), vec_src=0, et=dst.et)
         axes = iteration_axes(dst.shape)
         k = prog.leaf(src, axes)
         prog.emit(I_LOAD, k=k)
         prog.emit(I_STORE, k=prog.store_leaf(dst, axes))
-        args = prog.args(mode=0, n_o=n_o, n_r=1)
-        grid = max(1, min(((n_o + 3) // 4 + 255) // 256, NUM_SMS * 16))
-        self.add_launch(EW_KIND[dst.et], (grid, 1, 1), (256, 1, 1), 0, args, prog, "copy")
+        self._col_launch(prog, n_o, 1, 0, "copy", dst.et)
         self.buf[("copy", dst.key)] = dst
 
     def add_launch(self, kind, grid, block, smem, args, prog, label):
@@ -680,10 +738,12 @@ def _splat_bits(b: Buffer) -> int:
 
 
 class Program:
-    def __init__(self, low: Lowering, extents, vec_src: int, dry: bool = False):
+    def __init__(self, low: Lowering, extents, vec_src: int, et: ElementType, dry: bool = False):
         self.low = low
         self.extents = extents
         self.vec_src = vec_src
+        self.et = et
+        self.V = vec_width(et)
         self.dry = dry
         self.leaf_specs: list = []
         self.leaf_index: dict = {}
@@ -698,7 +758,7 @@ class Program:
             if len(digits) > abi.MAX_DIGITS:
                 raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
             spec = LeafSpec(buf, digits, False)
-            spec.vec = 2 if buf.splat is not None else vec_class(digits, self.vec_src, False)
+            spec.vec = 2 if buf.splat is not None else vec_class(digits, self.vec_src, False, self.V, buf.et.byte_size)
             self.leaf_index[key] = len(self.leaf_specs)
             self.leaf_specs.append(spec)
         return self.leaf_index[key]
@@ -707,13 +767,13 @@ class Program:
         digits = make_digits(buf, axes, self.extents)
         if len(digits) > abi.MAX_DIGITS:
             raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
-        spec = LeafSpec(buf, digits, True, vec_class(digits, self.vec_src, True))
+        spec = LeafSpec(buf, digits, True, vec_class(digits, self.vec_src, True, self.V, buf.et.byte_size))
         self.leaf_specs.append(spec)
         return len(self.leaf_specs) - 1
 
     def set_red_out(self, buf: Buffer, axes):
         digits = make_digits(buf, axes, self.extents)
-        self.red_out = LeafSpec(buf, digits, True, vec_class(digits, 0, True))
+        self.red_out = LeafSpec(buf, digits, True, vec_class(digits, 0, True, self.V, buf.et.byte_size))
 
     def emit(self, cls, op=0, k=0, swap=0):
         self.code.append((cls, op, k, swap))
@@ -878,17 +938,31 @@ class Program:
             raise UnsupportedOp(f"fused program of {len(self.code)} instructions (> {abi.MAX_INSTR})")
         return len(pre)
 
-    def args(self, mode, n_o, n_r, red_kind=0, split=1) -> abi.EwArgs:
+    def depth(self) -> int:
+        d = best = 0
+        for cls, _, _, _ in self.code:
+            if cls in (I_PUSH, I_PUSH_LOAD):
+                d += 1
+                best = max(best, d)
+            elif cls == I_BIN_POP:
+                d -= 1
+        return best
+
+    def args(self, mode, n_o, n_r, red_kind=0, split=1, wpr=1) -> abi.EwArgs:
         npre = self.finalize_order()
         a = abi.EwArgs()
         a.n_o, a.n_r = n_o, n_r
         a.ninstr = len(self.code)
         a.nleaves = len(self.leaf_specs)
         a.mode, a.red_kind, a.vec_axis, a.split = mode, red_kind, self.vec_src, split
-        a.npre = npre
+        a.npre, a.depth, a.wpr = npre, self.depth(), wpr
         for i, (cls, op, k, swap) in enumerate(self.code):
             a.prog[i] = cls | (op << 8) | (k << 16) | (swap << 24)
         return a
+
+    def smem_bytes(self, a: abi.EwArgs, threads: int = 256) -> int:
+        es = self.et.byte_size
+        return 4 * a.nleaves * threads + es * a.depth * self.V * threads + es * max(self.V * threads, 8)
 
     def finalize_fn(self, a: abi.EwArgs):
         specs = list(self.leaf_specs)
@@ -930,11 +1004,13 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
         L.splat = _splat_bits(b)
         L.ndig = 0
         L.vec = 2
+        L.rlin = 0
         return
     L.mode = 0
     L.ref = _buf_ref(b)
     L.ndig = len(s.digits)
     L.vec = s.vec
+    L.rlin = r_linear(s.digits)
     for i, (src, div, mod, stride) in enumerate(s.digits):
         d = L.dig[i]
         d.src = src

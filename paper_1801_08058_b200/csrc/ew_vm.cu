@@ -4,13 +4,13 @@
 // group of memory-bound IR nodes into one *program* for this kernel: a short
 // accumulator-stack bytecode over "leaves" (loads / stores through
 // mixed-radix index maps, gfb200.h gfb_digit).  One launch evaluates the
-// whole group in a single pass over HBM:
-//   mode 0  map            out[o]            = prog(o)
-//   mode 1  row reduce     red[o] = fold_r   prog(o, r)   one warp per o, lanes along r
-//   mode 2  column reduce  red[o] = fold_r   prog(o, r)   lanes along o, r split `split` ways
-// Side outputs (STORE) write intermediate values the graph also needs, so
-// e.g. config B's `t3 = Relu(a + Broadcast(c)) * b` and `Sum(t3)` are one read
-// of a and b and one write of t3.
+// whole group in a single pass over HBM over a 2-level index space (o, r):
+//   ROW  one warp (or `wpr` warps) per o, lanes take V-vectors along r
+//   COL  one thread per V-vector of o, r looped (split `split` ways)
+// with an optional fold over r (Sum / max-reduce).  Side outputs (STORE)
+// write intermediates the graph also needs, so config B's
+// `t3 = Relu(a + Broadcast(c)) * b` and `Sum(t3)` are one read of a and b and
+// one write of t3.
 //
 // Arithmetic follows the reference contract (numeric.py / kernels.py):
 // F32 + - x / are IEEE round-to-nearest with no contraction (__f*_rn), so
@@ -20,15 +20,17 @@
 // `x > 0 ? x : 0`; I64 wraps.  No --use_fast_math, no FTZ (sigmoid(-100)
 // in F32 is a subnormal).
 //
-// Each thread evaluates a vector of 4 consecutive indices along the
-// launch's vector axis; leaves classified contiguous/uniform at compile
-// time use 128-bit loads/stores, and the first `npre` leaves are all loaded
-// before the program runs so their HBM requests are in flight together.
+// Interpreter cost is kept off the memory path: leaf base offsets for the
+// thread's o are computed once (shared memory), the per-vector r offset is
+// r * rlin, the first `npre` leaves of every vector are loaded before the
+// program runs (all in flight together, 128-bit accesses), and the operand
+// stack lives in shared memory so the register file holds only data.
 
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "gfb_common.cuh"
 
@@ -49,310 +51,309 @@ enum : uint32_t {
 };
 
 template <typename T>
+struct VecOf {
+    static constexpr int V = sizeof(T) >= 8 ? 4 : 8;
+};
+
+template <typename T>
 __device__ __forceinline__ T from_bits(uint64_t b) {
-    if constexpr (sizeof(T) == 4) return __int_as_float((int)(uint32_t)b);
-    else if constexpr (sizeof(T) == 8 && std::is_same<T, double>::value) return __longlong_as_double((long long)b);
+    if constexpr (std::is_same<T, float>::value) return __int_as_float((int)(uint32_t)b);
+    else if constexpr (std::is_same<T, double>::value) return __longlong_as_double((long long)b);
     else if constexpr (sizeof(T) == 8) return (T)(long long)b;
     else return (T)(b & 0xff);
 }
 
-// ---- vector memory access (4 consecutive elements, 16B-aligned for 4/8-byte T)
-template <typename T>
-__device__ __forceinline__ void load4(const T* p, T (&v)[4]) {
-    if constexpr (sizeof(T) == 4) {
-        float4 x = __ldg(reinterpret_cast<const float4*>(p));
-        v[0] = *reinterpret_cast<T*>(&x.x);
-        v[1] = *reinterpret_cast<T*>(&x.y);
-        v[2] = *reinterpret_cast<T*>(&x.z);
-        v[3] = *reinterpret_cast<T*>(&x.w);
-    } else if constexpr (sizeof(T) == 8) {
-        const longlong2* q = reinterpret_cast<const longlong2*>(p);
-        longlong2 a = __ldg(q), b = __ldg(q + 1);
-        v[0] = *reinterpret_cast<T*>(&a.x);
-        v[1] = *reinterpret_cast<T*>(&a.y);
-        v[2] = *reinterpret_cast<T*>(&b.x);
-        v[3] = *reinterpret_cast<T*>(&b.y);
+// ---- V consecutive elements, one or two 128-bit (or one 64-bit) accesses
+template <typename T, int V>
+__device__ __forceinline__ void loadV(const T* p, T (&v)[V]) {
+    static_assert(V * sizeof(T) == 32 || V * sizeof(T) == 8, "vector width");
+    if constexpr (V * sizeof(T) == 32) {
+        const int4* q = reinterpret_cast<const int4*>(p);
+        int4 a = __ldg(q), b = __ldg(q + 1);
+        const T* pa = reinterpret_cast<const T*>(&a);
+        const T* pb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+        for (int i = 0; i < V / 2; ++i) {
+            v[i] = pa[i];
+            v[i + V / 2] = pb[i];
+        }
     } else {
-        uchar4 x = __ldg(reinterpret_cast<const uchar4*>(p));
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        uint2 a = __ldg(reinterpret_cast<const uint2*>(p));
+        const T* pa = reinterpret_cast<const T*>(&a);
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = pa[i];
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void store4(T* p, const T (&v)[4]) {
-    if constexpr (sizeof(T) == 4) {
-        float4 x;
-        x.x = *reinterpret_cast<const float*>(&v[0]);
-        x.y = *reinterpret_cast<const float*>(&v[1]);
-        x.z = *reinterpret_cast<const float*>(&v[2]);
-        x.w = *reinterpret_cast<const float*>(&v[3]);
-        *reinterpret_cast<float4*>(p) = x;
-    } else if constexpr (sizeof(T) == 8) {
-        longlong2 a, b;
-        a.x = *reinterpret_cast<const long long*>(&v[0]);
-        a.y = *reinterpret_cast<const long long*>(&v[1]);
-        b.x = *reinterpret_cast<const long long*>(&v[2]);
-        b.y = *reinterpret_cast<const long long*>(&v[3]);
-        reinterpret_cast<longlong2*>(p)[0] = a;
-        reinterpret_cast<longlong2*>(p)[1] = b;
+template <typename T, int V>
+__device__ __forceinline__ void storeV(T* p, const T (&v)[V]) {
+    if constexpr (V * sizeof(T) == 32) {
+        int4 a, b;
+        T* pa = reinterpret_cast<T*>(&a);
+        T* pb = reinterpret_cast<T*>(&b);
+#pragma unroll
+        for (int i = 0; i < V / 2; ++i) {
+            pa[i] = v[i];
+            pb[i] = v[i + V / 2];
+        }
+        reinterpret_cast<int4*>(p)[0] = a;
+        reinterpret_cast<int4*>(p)[1] = b;
     } else {
-        *reinterpret_cast<uchar4*>(p) = make_uchar4(v[0], v[1], v[2], v[3]);
+        uint2 a;
+        T* pa = reinterpret_cast<T*>(&a);
+#pragma unroll
+        for (int i = 0; i < V; ++i) pa[i] = v[i];
+        *reinterpret_cast<uint2*>(p) = a;
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void load_leaf(const gfb_leaf& L, const void* const* tab, uint32_t o, uint32_t r,
-                                          int vaxis, int nvalid, T (&out)[4]) {
-    if (L.mode == 1) {
-        const T s = from_bits<T>(L.splat);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) out[v] = s;
-        return;
+// Per-block shared state.
+struct Shared {
+    const char* base[GFB_MAX_LEAVES];  // slot pointer + byte offset of every leaf
+};
+
+__device__ __forceinline__ uint32_t part_offset(const gfb_leaf& L, uint32_t idx, int src) {
+    uint32_t off = 0;
+    const int n = L.ndig;
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) {
+        const gfb_digit& d = L.dig[i];
+        if (d.src != src) continue;
+        uint32_t q = fast_div(idx, (uint32_t)d.div_mul, d.div_sh);
+        if (d.mod) q -= fast_div(q, (uint32_t)d.mod_mul, d.mod_sh) * d.mod;
+        off += q * (uint32_t)d.stride;
     }
-    const T* base = resolve<const T>(tab, L.ref);
-    if (nvalid == 4 && L.vec == 1) {
-        load4(base + leaf_offset(L, o, r), out);
-    } else if (nvalid == 4 && L.vec == 2) {
-        const T s = __ldg(base + leaf_offset(L, o, r));
-#pragma unroll
-        for (int v = 0; v < 4; ++v) out[v] = s;
-    } else {
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            out[v] = v < nvalid ? __ldg(base + leaf_offset(L, o + (vaxis ? 0 : v), r + (vaxis ? v : 0))) : T(0);
-    }
+    return off;
 }
 
-template <typename T>
-__device__ __forceinline__ void store_leaf(const gfb_leaf& L, const void* const* tab, uint32_t o, uint32_t r,
-                                           int vaxis, int nvalid, const T (&val)[4]) {
-    T* base = resolve<T>(tab, L.ref);
-    if (nvalid == 4 && L.vec == 1) {
-        store4(base + leaf_offset(L, o, r), val);
-    } else {
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            if (v < nvalid) base[leaf_offset(L, o + (vaxis ? 0 : v), r + (vaxis ? v : 0))] = val[v];
-    }
+__device__ __forceinline__ uint32_t r_offset(const gfb_leaf& L, uint32_t r) {
+    const int rl = L.rlin;
+    return rl >= 0 ? r * (uint32_t)rl : part_offset(L, r, 1);
 }
+
+// Thread context: the vector at (o, r) with nvalid live lanes.
+template <typename T, int V>
+struct Ctx {
+    const gfb_ew_args& p;
+    const char* const* base;  // Shared::base
+    const uint32_t* ob;       // per-thread o-part offsets, stride `obs`
+    int obs;
+    T* stack;                 // per-thread stack, element stride `obs`
+    uint32_t o, r;
+    int nvalid, vaxis;
+
+    __device__ __forceinline__ void load(int k, T (&out)[V]) const {
+        const gfb_leaf& L = p.leaves[k];
+        if (L.mode == 1) {
+            const T s = from_bits<T>(L.splat);
+#pragma unroll
+            for (int v = 0; v < V; ++v) out[v] = s;
+            return;
+        }
+        const T* bp = reinterpret_cast<const T*>(base[k]);
+        if (nvalid == V && L.vec != 0) {
+            const uint32_t off = ob[k * obs] + r_offset(L, r);
+            if (L.vec == 1) {
+                loadV<T, V>(bp + off, out);
+            } else {
+                const T s = __ldg(bp + off);
+#pragma unroll
+                for (int v = 0; v < V; ++v) out[v] = s;
+            }
+            return;
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            out[v] = v < nvalid ? __ldg(bp + leaf_offset(L, o + (vaxis ? 0 : v), r + (vaxis ? v : 0))) : T(0);
+    }
+
+    __device__ __forceinline__ void store(int k, const T (&val)[V]) const {
+        const gfb_leaf& L = p.leaves[k];
+        T* bp = reinterpret_cast<T*>(const_cast<char*>(base[k]));
+        if (nvalid == V && L.vec == 1) {
+            storeV<T, V>(bp + ob[k * obs] + r_offset(L, r), val);
+            return;
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (v < nvalid) bp[leaf_offset(L, o + (vaxis ? 0 : v), r + (vaxis ? v : 0))] = val[v];
+    }
+};
 
 // ---- scalar semantics (reference numeric.py / kernels.py) ----------------
-__device__ __forceinline__ double safe_log(double x) {
+__device__ __noinline__ double safe_log(double x) {
     if (x != x) return x;
     if (x < 0.0) return __longlong_as_double(0x7ff8000000000000ll);
     if (x == 0.0) return -__longlong_as_double(0x7ff0000000000000ll);
     return log(x);
 }
-__device__ __forceinline__ double sigmoid_d(double x) {
+__device__ __noinline__ double sigmoid_d(double x) {
     if (x != x) return x;
     if (x >= 0.0) return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
     double e = exp(x);
     return __ddiv_rn(e, __dadd_rn(1.0, e));
 }
+__device__ __noinline__ double transcendental(uint32_t op, double x) {
+    switch (op) {
+        case OP_EXP: return exp(x);
+        case OP_LOG: return safe_log(x);
+        case OP_TANH: return tanh(x);
+        default: return sigmoid_d(x);
+    }
+}
 
-template <typename T>
-__device__ __forceinline__ void apply_unary(uint32_t op, T (&a)[4]) {
-    if constexpr (std::is_same<T, float>::value) {
+template <typename T, int V>
+__device__ __forceinline__ void apply_unary(uint32_t op, T (&a)[V]) {
+    if constexpr (std::is_floating_point<T>::value) {
         switch (op) {
             case OP_NEG:
 #pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = -a[v];
-                break;
-            case OP_EXP:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = __double2float_rn(exp((double)a[v]));
-                break;
-            case OP_LOG:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = __double2float_rn(safe_log((double)a[v]));
-                break;
-            case OP_TANH:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = __double2float_rn(tanh((double)a[v]));
-                break;
-            case OP_SIGMOID:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = __double2float_rn(sigmoid_d((double)a[v]));
+                for (int v = 0; v < V; ++v) a[v] = -a[v];
                 break;
             case OP_RELU:
 #pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = a[v] > 0.0f ? a[v] : 0.0f;
+                for (int v = 0; v < V; ++v) a[v] = a[v] > T(0) ? a[v] : T(0);
                 break;
-        }
-    } else if constexpr (std::is_same<T, double>::value) {
-        switch (op) {
-            case OP_NEG:
+            default:  // transcendentals: double precision, rounded once
 #pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = -a[v];
-                break;
-            case OP_EXP:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = exp(a[v]);
-                break;
-            case OP_LOG:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = safe_log(a[v]);
-                break;
-            case OP_TANH:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = tanh(a[v]);
-                break;
-            case OP_SIGMOID:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = sigmoid_d(a[v]);
-                break;
-            case OP_RELU:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) a[v] = a[v] > 0.0 ? a[v] : 0.0;
+                for (int v = 0; v < V; ++v) {
+                    const double y = transcendental(op, (double)a[v]);
+                    if constexpr (std::is_same<T, float>::value) a[v] = __double2float_rn(y);
+                    else a[v] = y;
+                }
                 break;
         }
     } else if constexpr (std::is_same<T, long long>::value) {
         if (op == OP_NEG) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v) a[v] = (long long)(0ull - (unsigned long long)a[v]);
+            for (int v = 0; v < V; ++v) a[v] = (long long)(0ull - (unsigned long long)a[v]);
         }
     }
 }
 
-// out = op(x, y) elementwise
 template <typename T>
-__device__ __forceinline__ void apply_binary(uint32_t op, const T (&x)[4], const T (&y)[4], T (&out)[4]) {
+__device__ __forceinline__ T bin1(uint32_t op, T x, T y) {
     if constexpr (std::is_same<T, float>::value) {
         switch (op) {
-            case OP_ADD:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __fadd_rn(x[v], y[v]);
-                break;
-            case OP_SUB:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __fsub_rn(x[v], y[v]);
-                break;
-            case OP_MUL:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __fmul_rn(x[v], y[v]);
-                break;
-            case OP_DIV:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __fdiv_rn(x[v], y[v]);
-                break;
-            case OP_MAX:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = x[v] >= y[v] ? x[v] : y[v];
-                break;
+            case OP_ADD: return __fadd_rn(x, y);
+            case OP_SUB: return __fsub_rn(x, y);
+            case OP_MUL: return __fmul_rn(x, y);
+            case OP_DIV: return __fdiv_rn(x, y);
+            default: return x >= y ? x : y;
         }
     } else if constexpr (std::is_same<T, double>::value) {
         switch (op) {
-            case OP_ADD:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __dadd_rn(x[v], y[v]);
-                break;
-            case OP_SUB:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __dsub_rn(x[v], y[v]);
-                break;
-            case OP_MUL:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __dmul_rn(x[v], y[v]);
-                break;
-            case OP_DIV:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = __ddiv_rn(x[v], y[v]);
-                break;
-            case OP_MAX:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = x[v] >= y[v] ? x[v] : y[v];
-                break;
+            case OP_ADD: return __dadd_rn(x, y);
+            case OP_SUB: return __dsub_rn(x, y);
+            case OP_MUL: return __dmul_rn(x, y);
+            case OP_DIV: return __ddiv_rn(x, y);
+            default: return x >= y ? x : y;
         }
     } else if constexpr (std::is_same<T, long long>::value) {
         typedef unsigned long long U;
         switch (op) {
-            case OP_ADD:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = (long long)((U)x[v] + (U)y[v]);
-                break;
-            case OP_SUB:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = (long long)((U)x[v] - (U)y[v]);
-                break;
-            case OP_MUL:
-#pragma unroll
-                for (int v = 0; v < 4; ++v) out[v] = (long long)((U)x[v] * (U)y[v]);
-                break;
+            case OP_ADD: return (long long)((U)x + (U)y);
+            case OP_SUB: return (long long)((U)x - (U)y);
+            default: return (long long)((U)x * (U)y);
         }
+    } else {
+        return x;
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void copy4(T (&d)[4], const T (&s)[4]) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) d[v] = s[v];
+// acc = swap ? op(b, acc) : op(acc, b); the op switch is outside the lanes.
+template <typename T, int V>
+__device__ __forceinline__ void apply_binary(uint32_t op, uint32_t swap, T (&acc)[V], const T (&b)[V]) {
+#define GFB_BIN_CASE(OPC)                                                                 \
+    case OPC:                                                                             \
+        if (swap) {                                                                       \
+            _Pragma("unroll") for (int v = 0; v < V; ++v) acc[v] = bin1<T>(OPC, b[v], acc[v]); \
+        } else {                                                                          \
+            _Pragma("unroll") for (int v = 0; v < V; ++v) acc[v] = bin1<T>(OPC, acc[v], b[v]); \
+        }                                                                                 \
+        break;
+    switch (op) {
+        GFB_BIN_CASE(OP_ADD)
+        GFB_BIN_CASE(OP_SUB)
+        GFB_BIN_CASE(OP_MUL)
+        GFB_BIN_CASE(OP_DIV)
+        GFB_BIN_CASE(OP_MAX)
+    }
+#undef GFB_BIN_CASE
 }
 
-// Run the program at the vector group starting at (o, r).  The value left
-// in `acc` is what a reduce launch folds.
-template <typename T>
-__device__ __forceinline__ void vm_run(const gfb_ew_args& p, uint32_t o, uint32_t r, int nvalid, T (&acc)[4]) {
-    const void* const* tab = p.tab;
-    const int vaxis = p.vec_axis;
+template <typename T, int V>
+__device__ __forceinline__ void copyV(T (&d)[V], const T (&s)[V]) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) d[v] = s[v];
+}
+
+// Run the program on the context's vector; leaves the last value in acc.
+template <typename T, int V>
+__device__ __forceinline__ void vm_run(const Ctx<T, V>& c, T (&acc)[V]) {
+    const gfb_ew_args& p = c.p;
     const int npre = p.npre;
-    T pre0[4], pre1[4], pre2[4], pre3[4];
-    if (npre > 0) load_leaf(p.leaves[0], tab, o, r, vaxis, nvalid, pre0);
-    if (npre > 1) load_leaf(p.leaves[1], tab, o, r, vaxis, nvalid, pre1);
-    if (npre > 2) load_leaf(p.leaves[2], tab, o, r, vaxis, nvalid, pre2);
-    if (npre > 3) load_leaf(p.leaves[3], tab, o, r, vaxis, nvalid, pre3);
-
-    auto fetch = [&](uint32_t k, T(&b)[4]) {
-        if ((int)k < npre) {
-            switch (k) {
-                case 0: copy4(b, pre0); break;
-                case 1: copy4(b, pre1); break;
-                case 2: copy4(b, pre2); break;
-                default: copy4(b, pre3); break;
-            }
-        } else {
-            load_leaf(p.leaves[k], tab, o, r, vaxis, nvalid, b);
-        }
-    };
-
-    T s0[4], s1[4], s2[4];
+    T p0[V], p1[V], p2[V], p3[V];
+    if (npre > 0) c.load(0, p0);
+    if (npre > 1) c.load(1, p1);
+    if (npre > 2) c.load(2, p2);
+    if (npre > 3) c.load(3, p3);
+    int sp = 0;
     const uint32_t n = p.ninstr;
 #pragma unroll 1
     for (uint32_t pc = 0; pc < n; ++pc) {
         const uint32_t ins = p.prog[pc];
         const uint32_t cls = ins & 0xffu, op = (ins >> 8) & 0xffu, k = (ins >> 16) & 0xffu, swap = ins >> 24;
+        if (cls == I_PUSH || cls == I_PUSH_LOAD) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) c.stack[(sp * V + v) * c.obs] = acc[v];
+            ++sp;
+            if (cls == I_PUSH) continue;
+        }
         switch (cls) {
             case I_PUSH_LOAD:
-                copy4(s2, s1); copy4(s1, s0); copy4(s0, acc);
-                fetch(k, acc);
-                break;
             case I_LOAD:
-                fetch(k, acc);
-                break;
-            case I_PUSH:
-                copy4(s2, s1); copy4(s1, s0); copy4(s0, acc);
+                if ((int)k < npre) {
+                    switch (k) {
+                        case 0: copyV<T, V>(acc, p0); break;
+                        case 1: copyV<T, V>(acc, p1); break;
+                        case 2: copyV<T, V>(acc, p2); break;
+                        default: copyV<T, V>(acc, p3); break;
+                    }
+                } else {
+                    c.load(k, acc);
+                }
                 break;
             case I_UN:
-                apply_unary<T>(op, acc);
+                apply_unary<T, V>(op, acc);
                 break;
-            case I_BIN_LEAF: {
-                T b[4];
-                fetch(k, b);
-                if (swap) apply_binary<T>(op, b, acc, acc);
-                else apply_binary<T>(op, acc, b, acc);
+            case I_BIN_LEAF:
+                if ((int)k < npre) {
+                    switch (k) {
+                        case 0: apply_binary<T, V>(op, swap, acc, p0); break;
+                        case 1: apply_binary<T, V>(op, swap, acc, p1); break;
+                        case 2: apply_binary<T, V>(op, swap, acc, p2); break;
+                        default: apply_binary<T, V>(op, swap, acc, p3); break;
+                    }
+                } else {
+                    T b[V];
+                    c.load(k, b);
+                    apply_binary<T, V>(op, swap, acc, b);
+                }
                 break;
-            }
             case I_BIN_POP: {
-                T b[4];
-                copy4(b, s0); copy4(s0, s1); copy4(s1, s2);
-                if (swap) apply_binary<T>(op, acc, b, acc);
-                else apply_binary<T>(op, b, acc, acc);
+                --sp;
+                T b[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) b[v] = c.stack[(sp * V + v) * c.obs];
+                apply_binary<T, V>(op, swap ^ 1u, acc, b);  // default: acc = op(popped, acc)
                 break;
             }
             case I_BIN_SELF:
-                apply_binary<T>(op, acc, acc, acc);
+                apply_binary<T, V>(op, 0, acc, acc);
                 break;
             case I_STORE:
-                store_leaf(p.leaves[k], tab, o, r, vaxis, nvalid, acc);
+                c.store(k, acc);
                 break;
         }
     }
@@ -372,92 +373,134 @@ __device__ __forceinline__ T fold_init(int kind) {
     else return T(0);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) gfb_ew_kernel(const __grid_constant__ gfb_ew_args p) {
-    const int mode = p.mode;
-    if (mode == 0) {
-        const uint32_t n = p.n_o;
-        const uint32_t groups = (n + 3) >> 2;
-        for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += gridDim.x * blockDim.x) {
-            const uint32_t o = g << 2;
-            const int nvalid = min(4u, n - o);
-            T acc[4];
-            vm_run<T>(p, o, 0, nvalid, acc);
+// Dynamic shared memory: [ob: nleaves x blockDim u32][stack: depth*V x blockDim T][fold: V x blockDim T]
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ gfb_ew_args p) {
+    __shared__ Shared sh;
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int nthr = blockDim.x, tid = threadIdx.x;
+    const int nleaves = p.nleaves;
+    uint32_t* ob = reinterpret_cast<uint32_t*>(dyn) + tid;
+    T* stack = reinterpret_cast<T*>(dyn + sizeof(uint32_t) * nleaves * nthr) + tid;
+    T* scratch = reinterpret_cast<T*>(dyn + sizeof(uint32_t) * nleaves * nthr + sizeof(T) * p.depth * V * nthr);
+    if (tid < nleaves) {
+        const gfb_leaf& L = p.leaves[tid];
+        sh.base[tid] = L.mode == 1 ? nullptr : reinterpret_cast<const char*>(p.tab[L.ref >> 56]) + (L.ref & kOffsetMask);
+    }
+    __syncthreads();
+    const int kind = p.red_kind;
+
+    if (p.mode == 1) {
+        // ROW: `wpr` warps per o, lanes along r.  Loop bounds are block-uniform
+        // so the cross-warp combine may use __syncthreads.
+        const int lane = tid & 31, warp = tid >> 5;
+        const int wpr = p.wpr, rpb = (nthr >> 5) / wpr;
+        const int sub = warp % wpr, slot = warp / wpr;
+        const uint32_t rstep = 32u * V * wpr, nr = p.n_r;
+        T* red = kind ? resolve<T>(p.tab, p.red_out.ref) : nullptr;
+        for (uint32_t o0 = blockIdx.x * rpb; o0 < p.n_o; o0 += gridDim.x * rpb) {
+            const uint32_t o = o0 + slot;
+            const bool active = o < p.n_o;
+            T part = fold_init<T>(kind);
+            if (active) {
+                for (int k = 0; k < nleaves; ++k) ob[k * nthr] = part_offset(p.leaves[k], o, 0);
+                Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, V, 1};
+                for (uint32_t r = (sub * 32u + lane) * V; r < nr; r += rstep) {
+                    c.r = r;
+                    c.nvalid = (int)min((uint32_t)V, nr - r);
+                    T acc[V];
+                    vm_run<T, V>(c, acc);
+                    if (kind) {
+#pragma unroll
+                        for (int v = 0; v < V; ++v)
+                            if (v < c.nvalid) part = fold<T>(kind, part, acc[v]);
+                    }
+                }
+            }
+            if (!kind) continue;
+            if constexpr (sizeof(T) > 1) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) part = fold<T>(kind, part, __shfl_xor_sync(0xffffffffu, part, off));
+                if (wpr > 1) {
+                    if (lane == 0) scratch[warp] = part;
+                    __syncthreads();
+                    if (active && sub == 0 && lane == 0) {
+                        for (int s = 1; s < wpr; ++s) part = fold<T>(kind, part, scratch[warp + s]);
+                        red[leaf_offset(p.red_out, o, 0)] = part;
+                    }
+                    __syncthreads();
+                } else if (active && lane == 0) {
+                    red[leaf_offset(p.red_out, o, 0)] = part;
+                }
+            }
         }
         return;
     }
-    if constexpr (sizeof(T) == 1) {
-        return;  // BOOL has no reductions (reference ir.py:178-180)
-    } else {
-        const int kind = p.red_kind;
-        const void* const* tab = p.tab;
-        if (mode == 1) {
-            // One warp per output row, lanes stride along r in vectors of 4.
-            const int lane = threadIdx.x & 31;
-            const uint32_t warps = blockDim.x >> 5;
-            const uint32_t nr = p.n_r;
-            for (uint32_t o = blockIdx.x * warps + (threadIdx.x >> 5); o < p.n_o; o += gridDim.x * warps) {
-                T part = fold_init<T>(kind);
-                for (uint32_t r = lane * 4; r < nr; r += 128) {
-                    const int nvalid = min(4u, nr - r);
-                    T acc[4];
-                    vm_run<T>(p, o, r, nvalid, acc);
-#pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        if (v < nvalid) part = fold<T>(kind, part, acc[v]);
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) part = fold<T>(kind, part, __shfl_xor_sync(0xffffffffu, part, off));
-                if (lane == 0) resolve<T>(tab, p.red_out.ref)[leaf_offset(p.red_out, o, 0)] = part;
-            }
-            return;
-        }
-        // mode 2: lanes along o (vectors of 4 outputs), r split `split` ways.
-        extern __shared__ unsigned char smem_raw[];
-        T* smem = reinterpret_cast<T*>(smem_raw);
-        const uint32_t split = p.split;
-        const uint32_t per_row = blockDim.x / split;
-        const uint32_t lane_o = threadIdx.x % per_row, rs = threadIdx.x / per_row;
-        const uint32_t o = (blockIdx.x * per_row + lane_o) * 4;
+
+    // COL: one thread per V-vector of o, r looped, split `split` ways.
+    const uint32_t split = p.split;
+    const uint32_t per_row = nthr / split;
+    const uint32_t lane_o = tid % per_row, rs = tid / per_row;
+    const uint32_t o_stride = gridDim.x * per_row * V;
+    for (uint32_t o0 = (blockIdx.x * per_row) * V; o0 < p.n_o; o0 += o_stride) {
+        const uint32_t o = o0 + lane_o * V;
         const bool active = o < p.n_o;
-        const int nvalid = active ? (int)min(4u, p.n_o - o) : 0;
-        T part[4];
+        const int nvalid = active ? (int)min((uint32_t)V, p.n_o - o) : 0;
+        T part[V];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) part[v] = fold_init<T>(kind);
+        for (int v = 0; v < V; ++v) part[v] = fold_init<T>(kind);
         if (active) {
+            for (int k = 0; k < nleaves; ++k) ob[k * nthr] = part_offset(p.leaves[k], o, 0);
+            Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, nvalid, 0};
             for (uint32_t r = rs; r < p.n_r; r += split) {
-                T acc[4];
-                vm_run<T>(p, o, r, nvalid, acc);
+                c.r = r;
+                T acc[V];
+                vm_run<T, V>(c, acc);
+                if (kind) {
 #pragma unroll
-                for (int v = 0; v < 4; ++v) part[v] = fold<T>(kind, part[v], acc[v]);
+                    for (int v = 0; v < V; ++v) part[v] = fold<T>(kind, part[v], acc[v]);
+                }
             }
         }
+        if (!kind) continue;
         if (split > 1) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) smem[(rs * per_row + lane_o) * 4 + v] = part[v];
             __syncthreads();
-            if (rs != 0) return;
-            for (uint32_t s = 1; s < split; ++s)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) part[v] = fold<T>(kind, part[v], smem[(s * per_row + lane_o) * 4 + v]);
+            for (int v = 0; v < V; ++v) scratch[v * nthr + tid] = part[v];
+            __syncthreads();
+            if (rs == 0) {
+                for (uint32_t s = 1; s < split; ++s)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) part[v] = fold<T>(kind, part[v], scratch[v * nthr + s * per_row + lane_o]);
+            }
         }
-        if (active) store_leaf(p.red_out, tab, o, 0, 0, nvalid, part);
+        if (active && rs == 0) {
+            const gfb_leaf& L = p.red_out;
+            T* bp = resolve<T>(p.tab, L.ref);
+            if (nvalid == V && L.vec == 1) {
+                storeV<T, V>(bp + part_offset(L, o, 0), part);
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (v < nvalid) bp[leaf_offset(L, o + v, 0)] = part[v];
+            }
+        }
     }
 }
 
-template __global__ void gfb_ew_kernel<float>(const __grid_constant__ gfb_ew_args);
-template __global__ void gfb_ew_kernel<double>(const __grid_constant__ gfb_ew_args);
-template __global__ void gfb_ew_kernel<long long>(const __grid_constant__ gfb_ew_args);
-template __global__ void gfb_ew_kernel<unsigned char>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_kernel<float, 8>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_kernel<double, 4>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_kernel<long long, 4>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_kernel<unsigned char, 8>(const __grid_constant__ gfb_ew_args);
 
 }  // namespace gfb
 
 extern "C" const void* gfb_ew_kernel_ptr(int kind) {
     switch (kind) {
-        case GFB_K_EW_F32: return (const void*)gfb::gfb_ew_kernel<float>;
-        case GFB_K_EW_F64: return (const void*)gfb::gfb_ew_kernel<double>;
-        case GFB_K_EW_I64: return (const void*)gfb::gfb_ew_kernel<long long>;
-        case GFB_K_EW_U8: return (const void*)gfb::gfb_ew_kernel<unsigned char>;
+        case GFB_K_EW_F32: return (const void*)gfb::gfb_ew_kernel<float, 8>;
+        case GFB_K_EW_F64: return (const void*)gfb::gfb_ew_kernel<double, 4>;
+        case GFB_K_EW_I64: return (const void*)gfb::gfb_ew_kernel<long long, 4>;
+        case GFB_K_EW_U8: return (const void*)gfb::gfb_ew_kernel<unsigned char, 8>;
     }
     return nullptr;
 }

@@ -341,25 +341,49 @@ def to_device(t: TensorValue):
     if t.is_device:
         return t.buffer
     host = torch.from_numpy(np.ascontiguousarray(t.buffer))
-    return host.to("cuda", non_blocking=False)
+    return host.to("cuda", non_blocking=host.is_pinned())
 
 
-def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device: bool = False) -> list:
-    """Execute on the B200; one fresh result tensor per result."""
+def pinned_tensor(et, shape) -> TensorValue:
+    """Zero host TensorValue in page-locked memory (fast H2D / D2H DMA)."""
+    import torch
+
+    from .ir import TensorDescriptor, element_count
+    from .layout import identity_layout
+
+    buf = torch.zeros(element_count(shape), dtype=torch_dtype(et), pin_memory=True).numpy()
+    return TensorValue(TensorDescriptor(et, tuple(shape)), identity_layout(len(shape)), buf)
+
+
+def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device: bool = False, out=None) -> list:
+    """Execute on the B200; one fresh result tensor per result.
+
+    `out`, if given, is a list of host TensorValues (e.g. `pinned_tensor`)
+    the results are copied into instead of newly allocated ones.
+    """
     import torch
 
     _check_signature(exe, inputs)
     ensure_device()
     dev_in = [to_device(t) for t in inputs]
     outs = exe.allocate_outputs()
-    stream = torch.cuda.current_stream().cuda_stream
-    exe.run_device(dev_in, outs, stream=stream, private=private_buffers)
-    results = []
+    cur = torch.cuda.current_stream()
+    exe.run_device(dev_in, outs, stream=cur.cuda_stream, private=private_buffers)
     if device:
-        for (desc, layout), buf in zip(exe.result_signature, outs):
-            results.append(TensorValue(desc, layout, buf))
+        return [TensorValue(desc, layout, buf) for (desc, layout), buf in zip(exe.result_signature, outs)]
+    results = []
+    if out is not None:
+        if len(out) != len(outs):
+            raise SignatureMismatch(f"expected {len(outs)} output tensors, got {len(out)}")
+        for (desc, layout), buf, host in zip(exe.result_signature, outs, out):
+            if host.descriptor != desc:
+                raise SignatureMismatch(f"output buffer {host.descriptor} != result {desc}")
+            dst = torch.from_numpy(host.buffer)
+            dst.copy_(buf, non_blocking=dst.is_pinned())
+            results.append(host)
+        cur.synchronize()
         return results
-    torch.cuda.current_stream().synchronize()
+    cur.synchronize()
     for (desc, layout), buf in zip(exe.result_signature, outs):
         results.append(TensorValue(desc, layout, buf.cpu().numpy()))
     return results

@@ -28,6 +28,9 @@ def _fdiv(n, mul, sh):
 
 
 def leaf_offsets(L, o, r):
+    if L.rlin >= 0:  # the kernel's fast path must agree with the digits
+        rd = [L.dig[i] for i in range(L.ndig) if L.dig[i].src == 1]
+        assert (not rd and L.rlin == 0) or (len(rd) == 1 and rd[0].div_mul == 0 and rd[0].mod == 0 and rd[0].stride == L.rlin)
     off = np.zeros_like(o)
     for i in range(L.ndig):
         d = L.dig[i]
@@ -100,12 +103,9 @@ def _bin(op, x, y, dt):
 
 def run_ew(mem, a, dt):
     n_o, n_r = a.n_o, a.n_r
-    if a.mode == 0:
-        o = np.arange(n_o, dtype=np.int64)
-        r = np.zeros_like(o)
-    else:
-        o = np.repeat(np.arange(n_o, dtype=np.int64), n_r)
-        r = np.tile(np.arange(n_r, dtype=np.int64), n_o)
+    assert a.mode in (1, 2) and a.vec_axis == (1 if a.mode == 1 else 0)
+    o = np.repeat(np.arange(n_o, dtype=np.int64), n_r)
+    r = np.tile(np.arange(n_r, dtype=np.int64), n_o)
 
     def load(k):
         L = a.leaves[k]
@@ -147,7 +147,7 @@ def run_ew(mem, a, dt):
             mem.view(L.ref, dt)[leaf_offsets(L, o, r)] = acc
         else:
             raise ValueError(cls)
-    if a.mode == 0:
+    if a.red_kind == 0:
         return
     vals = acc.reshape(n_o, n_r) if (acc is not None and n_r) else np.zeros((n_o, 0), dtype=dt)
     if a.red_kind == 2:
