@@ -56,8 +56,57 @@ INDEX_OPS = frozenset({OpKind.BROADCAST, OpKind.RESHAPE, OpKind.CONVERT_LAYOUT})
 MAX_STACK = 3
 MAX_PRELOAD = 4
 
-# VM encoding (csrc/ew_vm.cu)
+# Program construction opcodes (internal), encoded to the kernel's flat
+# jump-table opcodes by `encode_flat` (csrc/ew_vm.cu, "Flat opcodes").
 I_LOAD, I_UN, I_BIN_LEAF, I_BIN_POP, I_BIN_SELF, I_PUSH, I_STORE, I_PUSH_LOAD = 1, 2, 3, 4, 5, 6, 7, 8
+F_LOADP, F_LOADM, F_PUSH, F_STORE, F_UN, F_BIN = 1, 5, 6, 7, 8, 16
+SRC_MEM, SRC_POP, SRC_SELF = 4, 5, 6
+
+
+def encode_flat(code, npre: int) -> list:
+    """(cls, op, leaf, swap) tuples -> kernel words (low byte opcode, leaf << 8)."""
+    out = []
+    for cls, op, k, swap in code:
+        if cls == I_PUSH_LOAD:
+            out.append(F_PUSH)
+            cls = I_LOAD
+        if cls == I_LOAD:
+            out.append(F_LOADP + k if k < npre else F_LOADM | (k << 8))
+        elif cls == I_PUSH:
+            out.append(F_PUSH)
+        elif cls == I_STORE:
+            out.append(F_STORE | (k << 8))
+        elif cls == I_UN:
+            out.append(F_UN + op - 5)
+        elif cls == I_BIN_LEAF:
+            src = k if k < npre else SRC_MEM
+            out.append(F_BIN + (src * 5 + op) * 2 + swap | ((k << 8) if src == SRC_MEM else 0))
+        elif cls == I_BIN_POP:
+            out.append(F_BIN + (SRC_POP * 5 + op) * 2 + (1 - swap))
+        elif cls == I_BIN_SELF:
+            out.append(F_BIN + (SRC_SELF * 5 + op) * 2)
+        else:
+            raise ValueError(cls)
+    return out
+
+
+def decode_flat(word: int):
+    """Kernel word -> (kind, arg...) for the host emulator."""
+    code, k = word & 0xFF, (word >> 8) & 0xFF
+    if F_LOADP <= code < F_LOADP + 4:
+        return ("loadp", code - F_LOADP)
+    if code == F_LOADM:
+        return ("loadm", k)
+    if code == F_PUSH:
+        return ("push",)
+    if code == F_STORE:
+        return ("store", k)
+    if F_UN <= code < F_UN + 6:
+        return ("un", code - F_UN + 5)
+    rel = code - F_BIN
+    s, rest = rel % 2, rel // 2
+    src, op = rest // 5, rest % 5
+    return ("bin", src, op, s, k)
 VM_OP = {
     OpKind.ADD: 0, OpKind.SUBTRACT: 1, OpKind.MULTIPLY: 2, OpKind.DIVIDE: 3, OpKind.MAXIMUM: 4,
     OpKind.NEGATE: 5, OpKind.EXP: 6, OpKind.LOG: 7, OpKind.TANH: 8, OpKind.SIGMOID: 9, OpKind.RELU: 10,
@@ -926,14 +975,7 @@ class Program:
             if cls in (I_LOAD, I_BIN_LEAF, I_STORE, I_PUSH_LOAD):
                 k = remap[k]
             code.append((cls, op, k, swap))
-        # peephole: PUSH; LOAD k  ->  PUSH_LOAD k
-        out = []
-        for ins in code:
-            if ins[0] == I_LOAD and out and out[-1][0] == I_PUSH:
-                out[-1] = (I_PUSH_LOAD, 0, ins[2], 0)
-            else:
-                out.append(ins)
-        self.code = out
+        self.code = code
         if len(self.code) > abi.MAX_INSTR:
             raise UnsupportedOp(f"fused program of {len(self.code)} instructions (> {abi.MAX_INSTR})")
         return len(pre)
@@ -956,8 +998,12 @@ class Program:
         a.nleaves = len(self.leaf_specs)
         a.mode, a.red_kind, a.vec_axis, a.split = mode, red_kind, self.vec_src, split
         a.npre, a.depth, a.wpr = npre, self.depth(), wpr
-        for i, (cls, op, k, swap) in enumerate(self.code):
-            a.prog[i] = cls | (op << 8) | (k << 16) | (swap << 24)
+        words = encode_flat(self.code, npre)
+        if len(words) > abi.MAX_INSTR:
+            raise UnsupportedOp(f"fused program of {len(words)} instructions (> {abi.MAX_INSTR})")
+        a.ninstr = len(words)
+        for i, w in enumerate(words):
+            a.prog[i] = w
         return a
 
     def smem_bytes(self, a: abi.EwArgs, threads: int = 256) -> int:

@@ -36,16 +36,16 @@
 
 namespace gfb {
 
-enum : uint32_t {
-    I_LOAD = 1,
-    I_UN = 2,
-    I_BIN_LEAF = 3,
-    I_BIN_POP = 4,
-    I_BIN_SELF = 5,
-    I_PUSH = 6,
-    I_STORE = 7,
-    I_PUSH_LOAD = 8,
-};
+// Flat opcodes (low byte of a program word; bits 8..15 hold a leaf index).
+// One jump-table dispatch per instruction; every body is specialised at
+// compile time (operand source, op, operand order), so a VM instruction
+// costs a handful of SASS instructions per 8 elements.
+//   1..4   acc = pre[k]             5  acc = load(leaf)
+//   6      push acc                 7  store(leaf) = acc
+//   8..13  acc = unary(acc)         (Negate, Exp, Log, Tanh, Sigmoid, Relu)
+//   16 + ((src * 5 + op) * 2 + s)   acc = s ? op(B, acc) : op(acc, B),
+//          src 0..3 = pre[src], 4 = load(leaf), 5 = pop, 6 = acc itself
+enum : uint32_t { F_LOADP = 1, F_LOADM = 5, F_PUSH = 6, F_STORE = 7, F_UN = 8, F_BIN = 16 };
 enum : uint32_t {
     OP_ADD = 0, OP_SUB, OP_MUL, OP_DIV, OP_MAX, OP_NEG, OP_EXP, OP_LOG, OP_TANH, OP_SIGMOID, OP_RELU,
 };
@@ -261,102 +261,116 @@ __device__ __forceinline__ T bin1(uint32_t op, T x, T y) {
     }
 }
 
-// acc = swap ? op(b, acc) : op(acc, b); the op switch is outside the lanes.
-template <typename T, int V>
-__device__ __forceinline__ void apply_binary(uint32_t op, uint32_t swap, T (&acc)[V], const T (&b)[V]) {
-#define GFB_BIN_CASE(OPC)                                                                 \
-    case OPC:                                                                             \
-        if (swap) {                                                                       \
-            _Pragma("unroll") for (int v = 0; v < V; ++v) acc[v] = bin1<T>(OPC, b[v], acc[v]); \
-        } else {                                                                          \
-            _Pragma("unroll") for (int v = 0; v < V; ++v) acc[v] = bin1<T>(OPC, acc[v], b[v]); \
-        }                                                                                 \
-        break;
-    switch (op) {
-        GFB_BIN_CASE(OP_ADD)
-        GFB_BIN_CASE(OP_SUB)
-        GFB_BIN_CASE(OP_MUL)
-        GFB_BIN_CASE(OP_DIV)
-        GFB_BIN_CASE(OP_MAX)
-    }
-#undef GFB_BIN_CASE
-}
-
 template <typename T, int V>
 __device__ __forceinline__ void copyV(T (&d)[V], const T (&s)[V]) {
 #pragma unroll
     for (int v = 0; v < V; ++v) d[v] = s[v];
 }
 
+// Register-cached addressing of a preloaded leaf for the thread's current o.
+template <typename T>
+struct Pre {
+    const T* ptr;  // leaf base + o-part offset
+    int rl;        // r-part = r * rl (-1: general digits)
+    int vec;       // 1 contiguous, 2 uniform, 0 gather
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void setup_pre(const Ctx<T, V>& c, Pre<T> (&pr)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k < c.p.npre) {
+            const gfb_leaf& L = c.p.leaves[k];
+            pr[k].ptr = reinterpret_cast<const T*>(c.base[k]) + c.ob[k * c.obs];
+            pr[k].rl = L.rlin;
+            pr[k].vec = L.vec;
+        }
+    }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void load_pre(const Ctx<T, V>& c, const Pre<T>& q, int k, T (&out)[V]) {
+    if (c.nvalid == V && q.vec != 0 && q.rl >= 0) {
+        const T* a = q.ptr + c.r * (uint32_t)q.rl;
+        if (q.vec == 1) {
+            loadV<T, V>(a, out);
+        } else {
+            const T x = __ldg(a);
+#pragma unroll
+            for (int v = 0; v < V; ++v) out[v] = x;
+        }
+    } else {
+        c.load(k, out);
+    }
+}
+
 // Run the program on the context's vector; leaves the last value in acc.
 template <typename T, int V>
-__device__ __forceinline__ void vm_run(const Ctx<T, V>& c, T (&acc)[V]) {
+__device__ __forceinline__ void vm_run(const Ctx<T, V>& c, const Pre<T> (&pr)[4], T (&acc)[V]) {
     const gfb_ew_args& p = c.p;
     const int npre = p.npre;
     T p0[V], p1[V], p2[V], p3[V];
-    if (npre > 0) c.load(0, p0);
-    if (npre > 1) c.load(1, p1);
-    if (npre > 2) c.load(2, p2);
-    if (npre > 3) c.load(3, p3);
+    if (npre > 0) load_pre<T, V>(c, pr[0], 0, p0);
+    if (npre > 1) load_pre<T, V>(c, pr[1], 1, p1);
+    if (npre > 2) load_pre<T, V>(c, pr[2], 2, p2);
+    if (npre > 3) load_pre<T, V>(c, pr[3], 3, p3);
     int sp = 0;
     const uint32_t n = p.ninstr;
+#define GFB_APPLY(OPC, S, B) \
+    _Pragma("unroll") for (int v = 0; v < V; ++v) acc[v] = (S) ? bin1<T>(OPC, B[v], acc[v]) : bin1<T>(OPC, acc[v], B[v]);
+#define GFB_CASE(SRC, OPC, S, PREP, B)                 \
+    case F_BIN + ((SRC) * 5 + (OPC)) * 2 + (S): {      \
+        PREP                                          \
+        GFB_APPLY(OPC, S, B)                          \
+        break;                                        \
+    }
+#define GFB_OPS(SRC, PREP, B)                                                     \
+    GFB_CASE(SRC, OP_ADD, 0, PREP, B) GFB_CASE(SRC, OP_ADD, 1, PREP, B)           \
+    GFB_CASE(SRC, OP_SUB, 0, PREP, B) GFB_CASE(SRC, OP_SUB, 1, PREP, B)           \
+    GFB_CASE(SRC, OP_MUL, 0, PREP, B) GFB_CASE(SRC, OP_MUL, 1, PREP, B)           \
+    GFB_CASE(SRC, OP_DIV, 0, PREP, B) GFB_CASE(SRC, OP_DIV, 1, PREP, B)           \
+    GFB_CASE(SRC, OP_MAX, 0, PREP, B) GFB_CASE(SRC, OP_MAX, 1, PREP, B)
+#define GFB_PREP_NONE
+#define GFB_PREP_MEM T b[V]; c.load(k, b);
+#define GFB_PREP_POP                                                        \
+    T b[V];                                                                 \
+    --sp;                                                                   \
+    _Pragma("unroll") for (int v = 0; v < V; ++v) b[v] = c.stack[(sp * V + v) * c.obs];
+#define GFB_UN(OPC) \
+    case F_UN + (OPC) - OP_NEG: apply_unary<T, V>(OPC, acc); break;
 #pragma unroll 1
     for (uint32_t pc = 0; pc < n; ++pc) {
         const uint32_t ins = p.prog[pc];
-        const uint32_t cls = ins & 0xffu, op = (ins >> 8) & 0xffu, k = (ins >> 16) & 0xffu, swap = ins >> 24;
-        if (cls == I_PUSH || cls == I_PUSH_LOAD) {
+        const int k = (int)((ins >> 8) & 0xffu);
+        switch (ins & 0xffu) {
+            case F_LOADP + 0: copyV<T, V>(acc, p0); break;
+            case F_LOADP + 1: copyV<T, V>(acc, p1); break;
+            case F_LOADP + 2: copyV<T, V>(acc, p2); break;
+            case F_LOADP + 3: copyV<T, V>(acc, p3); break;
+            case F_LOADM: c.load(k, acc); break;
+            case F_PUSH:
 #pragma unroll
-            for (int v = 0; v < V; ++v) c.stack[(sp * V + v) * c.obs] = acc[v];
-            ++sp;
-            if (cls == I_PUSH) continue;
-        }
-        switch (cls) {
-            case I_PUSH_LOAD:
-            case I_LOAD:
-                if ((int)k < npre) {
-                    switch (k) {
-                        case 0: copyV<T, V>(acc, p0); break;
-                        case 1: copyV<T, V>(acc, p1); break;
-                        case 2: copyV<T, V>(acc, p2); break;
-                        default: copyV<T, V>(acc, p3); break;
-                    }
-                } else {
-                    c.load(k, acc);
-                }
+                for (int v = 0; v < V; ++v) c.stack[(sp * V + v) * c.obs] = acc[v];
+                ++sp;
                 break;
-            case I_UN:
-                apply_unary<T, V>(op, acc);
-                break;
-            case I_BIN_LEAF:
-                if ((int)k < npre) {
-                    switch (k) {
-                        case 0: apply_binary<T, V>(op, swap, acc, p0); break;
-                        case 1: apply_binary<T, V>(op, swap, acc, p1); break;
-                        case 2: apply_binary<T, V>(op, swap, acc, p2); break;
-                        default: apply_binary<T, V>(op, swap, acc, p3); break;
-                    }
-                } else {
-                    T b[V];
-                    c.load(k, b);
-                    apply_binary<T, V>(op, swap, acc, b);
-                }
-                break;
-            case I_BIN_POP: {
-                --sp;
-                T b[V];
-#pragma unroll
-                for (int v = 0; v < V; ++v) b[v] = c.stack[(sp * V + v) * c.obs];
-                apply_binary<T, V>(op, swap ^ 1u, acc, b);  // default: acc = op(popped, acc)
-                break;
-            }
-            case I_BIN_SELF:
-                apply_binary<T, V>(op, 0, acc, acc);
-                break;
-            case I_STORE:
-                c.store(k, acc);
-                break;
+            case F_STORE: c.store(k, acc); break;
+            GFB_UN(OP_NEG) GFB_UN(OP_EXP) GFB_UN(OP_LOG) GFB_UN(OP_TANH) GFB_UN(OP_SIGMOID) GFB_UN(OP_RELU)
+            GFB_OPS(0, GFB_PREP_NONE, p0)
+            GFB_OPS(1, GFB_PREP_NONE, p1)
+            GFB_OPS(2, GFB_PREP_NONE, p2)
+            GFB_OPS(3, GFB_PREP_NONE, p3)
+            GFB_OPS(4, GFB_PREP_MEM, b)
+            GFB_OPS(5, GFB_PREP_POP, b)
+            GFB_OPS(6, GFB_PREP_NONE, acc)
         }
     }
+#undef GFB_APPLY
+#undef GFB_CASE
+#undef GFB_OPS
+#undef GFB_PREP_NONE
+#undef GFB_PREP_MEM
+#undef GFB_PREP_POP
+#undef GFB_UN
 }
 
 template <typename T>
@@ -405,11 +419,13 @@ __global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ 
             if (active) {
                 for (int k = 0; k < nleaves; ++k) ob[k * nthr] = part_offset(p.leaves[k], o, 0);
                 Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, V, 1};
+                Pre<T> pr[4];
+                setup_pre<T, V>(c, pr);
                 for (uint32_t r = (sub * 32u + lane) * V; r < nr; r += rstep) {
                     c.r = r;
                     c.nvalid = (int)min((uint32_t)V, nr - r);
                     T acc[V];
-                    vm_run<T, V>(c, acc);
+                    vm_run<T, V>(c, pr, acc);
                     if (kind) {
 #pragma unroll
                         for (int v = 0; v < V; ++v)
@@ -452,10 +468,12 @@ __global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ 
         if (active) {
             for (int k = 0; k < nleaves; ++k) ob[k * nthr] = part_offset(p.leaves[k], o, 0);
             Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, nvalid, 0};
+            Pre<T> pr[4];
+            setup_pre<T, V>(c, pr);
             for (uint32_t r = rs; r < p.n_r; r += split) {
                 c.r = r;
                 T acc[V];
-                vm_run<T, V>(c, acc);
+                vm_run<T, V>(c, pr, acc);
                 if (kind) {
 #pragma unroll
                     for (int v = 0; v < V; ++v) part[v] = fold<T>(kind, part[v], acc[v]);

@@ -13,9 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from paper_1801_08058_b200 import abi
-from paper_1801_08058_b200.compiler import (
-    I_BIN_LEAF, I_BIN_POP, I_BIN_SELF, I_LOAD, I_PUSH, I_PUSH_LOAD, I_STORE, I_UN,
-)
+from paper_1801_08058_b200.compiler import decode_flat
 
 DT = {abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
       abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
@@ -122,31 +120,31 @@ def run_ew(mem, a, dt):
 
     acc = None
     stack = []
+    pre = [load(k) for k in range(a.npre)]
     for pc in range(a.ninstr):
-        ins = a.prog[pc]
-        cls, op, k, swap = ins & 0xFF, (ins >> 8) & 0xFF, (ins >> 16) & 0xFF, ins >> 24
-        if cls == I_LOAD:
-            acc = load(k)
-        elif cls == I_PUSH_LOAD:
+        ins = decode_flat(a.prog[pc])
+        if ins[0] == "loadp":
+            acc = pre[ins[1]]
+        elif ins[0] == "loadm":
+            acc = load(ins[1])
+        elif ins[0] == "push":
             stack.append(acc)
-            acc = load(k)
-        elif cls == I_PUSH:
-            stack.append(acc)
-        elif cls == I_UN:
-            acc = _un(op, acc, dt)
-        elif cls == I_BIN_LEAF:
-            b = load(k)
-            acc = _bin(op, b, acc, dt) if swap else _bin(op, acc, b, dt)
-        elif cls == I_BIN_POP:
-            b = stack.pop()
-            acc = _bin(op, acc, b, dt) if swap else _bin(op, b, acc, dt)
-        elif cls == I_BIN_SELF:
-            acc = _bin(op, acc, acc, dt)
-        elif cls == I_STORE:
-            L = a.leaves[k]
+        elif ins[0] == "store":
+            L = a.leaves[ins[1]]
             mem.view(L.ref, dt)[leaf_offsets(L, o, r)] = acc
+        elif ins[0] == "un":
+            acc = _un(ins[1], acc, dt)
         else:
-            raise ValueError(cls)
+            _, src, op, sw, k = ins
+            if src < 4:
+                b = pre[src]
+            elif src == 4:
+                b = load(k)
+            elif src == 5:
+                b = stack.pop()
+            else:
+                b = acc
+            acc = _bin(op, b, acc, dt) if sw else _bin(op, acc, b, dt)
     if a.red_kind == 0:
         return
     vals = acc.reshape(n_o, n_r) if (acc is not None and n_r) else np.zeros((n_o, 0), dtype=dt)
