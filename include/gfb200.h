@@ -48,6 +48,8 @@ enum {
     GFB_K_EW_F64 = 2,
     GFB_K_EW_I64 = 3,
     GFB_K_EW_U8 = 4,
+    GFB_K_EWS_F32 = 5, /* staged ROW variant: cp.async.bulk double-buffered stages (gfb_ew_args, mode 3) */
+    GFB_K_EWS_F64 = 6,
     GFB_K_DOT_F32 = 10, /* SIMT Dot, sequential k, bit-exact (gfb_dot_args) */
     GFB_K_DOT_F64 = 11,
     GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot (gfb_dot_args) */

@@ -560,15 +560,54 @@ class Lowering:
 
     # -- fused VM groups
     def _row_launch(self, prog, n_o, n_r, red_kind, label, et):
-        """ROW: warps per o, vectors along r; more warps per o when o is short."""
+        """ROW: warps per o, vectors along r; more warps per o when o is short.
+
+        Programs whose memory operands are all row-contiguous (or constant
+        along the row) take the staged kernel: cp.async.bulk double-buffered
+        shared-memory stages, one dispatch per 16 elements per thread."""
         V = vec_width(et)
+        staged = self._staged_ok(prog, n_o, n_r, et)
         wpr = 1
-        while wpr < 8 and n_o * wpr < 2 * NUM_SMS * 8 and n_r >= 32 * V * wpr * 2:
+        while not staged and wpr < 8 and n_o * wpr < 2 * NUM_SMS * 8 and n_r >= 32 * V * wpr * 2:
             wpr *= 2
         rpb = 8 // wpr
+        if staged:
+            args = prog.args(mode=3, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=1)
+            chunk = 32 * 2 * (16 // et.byte_size) * 2
+            smem = 8 * 2 * args.npre * chunk * et.byte_size
+            per_sm = max(1, min(8, (200 * 1024) // max(smem, 1)))
+            grid = max(1, min((n_o + 7) // 8, NUM_SMS * per_sm))
+            kind = abi.K_EWS_F32 if et is ElementType.F32 else abi.K_EWS_F64
+            self.add_launch(kind, (grid, 1, 1), (256, 1, 1), smem, args, prog, label + ":staged")
+            return
         grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)
         self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
+
+    def _staged_ok(self, prog, n_o, n_r, et) -> bool:
+        if et not in (ElementType.F32, ElementType.F64) or n_r < 256:
+            return False
+        es = et.byte_size
+        if (n_r * es) % 16:
+            return False
+        if any(c[0] in (I_PUSH, I_PUSH_LOAD, I_BIN_POP) for c in prog.code):
+            return False
+        loads = [l for l in prog.leaf_specs if not l.is_store and l.buf.splat is None]
+        if len(loads) > MAX_PRELOAD:
+            return False
+        def o_aligned(l):
+            return all((d[3] * es) % 16 == 0 for d in l.digits if d[0] == 0)
+        for l in loads:
+            rl = r_linear(l.digits)
+            if rl == 1:
+                if not o_aligned(l):
+                    return False
+            elif rl != 0 or any(d[0] == 1 for d in l.digits):
+                return False
+        for l in prog.leaf_specs:
+            if l.is_store and r_linear(l.digits) == 1 and not o_aligned(l):
+                return False
+        return True
 
     def _col_launch(self, prog, n_o, n_r, red_kind, label, et):
         """COL: one thread per V-vector of o, r looped (split when o is short)."""

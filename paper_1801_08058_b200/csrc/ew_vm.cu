@@ -506,6 +506,262 @@ __global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Staged ROW kernel (mode 3): the Blackwell path for row-contiguous programs.
+//
+// Each warp walks (row, chunk) pairs; lane 0 streams the next chunk of every
+// preloaded leaf into a per-warp, double-buffered shared-memory stage with
+// cp.async.bulk (TMA bulk copies completing on an mbarrier) while the warp
+// computes on the current one.  A VM instruction is dispatched once per
+// U x V elements per thread, operands come from shared memory, leaves that
+// do not depend on r (e.g. a column Broadcast) are per-row scalars, and the
+// accumulator stays in registers.  Requirements (checked by the compiler):
+// no operand stack, every memory leaf preloaded (<= 4), staged leaves with
+// r-stride 1 and 16-byte aligned rows.
+
+__device__ __forceinline__ void fence_proxy() {
+    // generic-proxy reads of a stage must complete before the async proxy rewrites it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T>
+struct StagedCfg {
+    static constexpr int HV = 16 / sizeof(T);  // elements per 16-byte half
+    static constexpr int V = 2 * HV;           // elements per thread per sub-vector
+    static constexpr int U = 2;                // sub-vectors per dispatch
+    static constexpr int CH = 32 * V * U;      // elements per warp chunk
+};
+
+// element index (within a chunk) of (u, half h, j) for `lane`
+template <typename T>
+__device__ __forceinline__ int sidx(int u, int h, int lane, int j) {
+    constexpr int HV = StagedCfg<T>::HV, V = StagedCfg<T>::V;
+    return u * 32 * V + h * 32 * HV + lane * HV + j;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constant__ gfb_ew_args p) {
+    using Cfg = StagedCfg<T>;
+    constexpr int HV = Cfg::HV, V = Cfg::V, U = Cfg::U, CH = Cfg::CH;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    __shared__ uint64_t bars[8][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int npre = p.npre, kind = p.red_kind;
+    const uint32_t n_o = p.n_o, n_r = p.n_r;
+    // per-warp stages: [2][npre][CH] elements
+    T* stage0 = reinterpret_cast<T*>(dyn) + (size_t)warp * 2 * npre * CH;
+    if (lane == 0) {
+        mbar_init(&bars[warp][0], 1);
+        mbar_init(&bars[warp][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, tw = gridDim.x * (blockDim.x >> 5);
+    if (gw >= n_o) return;
+    const uint32_t nch = (n_r + CH - 1) / CH;
+    const uint32_t nrows = (n_o - gw + tw - 1) / tw;
+    const uint32_t total = nrows * nch;
+    // leaf classes (uniform): 1 = staged (r-contiguous), 2 = row scalar, 3 = splat
+    int cls[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cls[k] = 0;
+        if (k < npre) {
+            const gfb_leaf& L = p.leaves[k];
+            cls[k] = L.mode == 1 ? 3 : (L.rlin == 1 ? 1 : 2);
+        }
+    }
+    const char* lbase[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        lbase[k] = (k < npre && cls[k] != 3) ? reinterpret_cast<const char*>(p.tab[p.leaves[k].ref >> 56]) + (p.leaves[k].ref & kOffsetMask) : nullptr;
+
+    auto issue = [&](uint32_t it) {
+        const uint32_t o = gw + (it / nch) * tw, chunk = it % nch;
+        const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
+        const int st = it & 1;
+        uint32_t nst = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nst += (k < npre && cls[k] == 1);
+        if (lane == 0) {
+            fence_proxy();
+            mbar_expect_tx(&bars[warp][st], len * sizeof(T) * nst);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k < npre && cls[k] == 1) {
+                    const T* src = reinterpret_cast<const T*>(lbase[k]) + part_offset(p.leaves[k], o, 0) + r0;
+                    bulk_g2s(stage0 + ((size_t)st * npre + k) * CH, src, len * sizeof(T), &bars[warp][st]);
+                }
+            }
+        }
+    };
+
+    issue(0);
+    if (total > 1) issue(1);
+    uint32_t phase[2] = {0u, 0u};
+    T part = fold_init<T>(kind);
+    T rs[4];  // row scalars
+    uint32_t cur_o = 0xffffffffu;
+    for (uint32_t it = 0; it < total; ++it) {
+        const int st = it & 1;
+        const uint32_t o = gw + (it / nch) * tw, chunk = it % nch;
+        const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
+        if (o != cur_o) {
+            cur_o = o;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k < npre && cls[k] == 2)
+                    rs[k] = __ldg(reinterpret_cast<const T*>(lbase[k]) + part_offset(p.leaves[k], o, 0));
+                else if (k < npre && cls[k] == 3)
+                    rs[k] = from_bits<T>(p.leaves[k].splat);
+            }
+        }
+        mbar_wait(&bars[warp][st], phase[st]);
+        phase[st] ^= 1u;
+        const T* sb = stage0 + (size_t)st * npre * CH;
+        const bool full = len == (uint32_t)CH;
+
+        T acc[U][V];
+        auto operand = [&](int k, int u, T(&b)[V]) {
+            if (cls[k] == 1) {
+                const T* src = sb + k * CH;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int4 q = *reinterpret_cast<const int4*>(src + sidx<T>(u, h, lane, 0));
+                    const T* qq = reinterpret_cast<const T*>(&q);
+#pragma unroll
+                    for (int j = 0; j < HV; ++j) b[h * HV + j] = qq[j];
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) b[v] = rs[k];
+            }
+        };
+        const uint32_t n = p.ninstr;
+#define GFB_S_APPLY(OPC, S, B) \
+    _Pragma("unroll") for (int v = 0; v < V; ++v) acc[u][v] = (S) ? bin1<T>(OPC, B[v], acc[u][v]) : bin1<T>(OPC, acc[u][v], B[v]);
+#define GFB_S_CASE(SRC, OPC, S)                                    \
+    case F_BIN + ((SRC) * 5 + (OPC)) * 2 + (S):                    \
+        _Pragma("unroll") for (int u = 0; u < U; ++u) {            \
+            T b[V];                                                \
+            operand(SRC, u, b);                                    \
+            GFB_S_APPLY(OPC, S, b)                                 \
+        }                                                          \
+        break;
+#define GFB_S_OPS(SRC)                                                           \
+    GFB_S_CASE(SRC, OP_ADD, 0) GFB_S_CASE(SRC, OP_ADD, 1)                        \
+    GFB_S_CASE(SRC, OP_SUB, 0) GFB_S_CASE(SRC, OP_SUB, 1)                        \
+    GFB_S_CASE(SRC, OP_MUL, 0) GFB_S_CASE(SRC, OP_MUL, 1)                        \
+    GFB_S_CASE(SRC, OP_DIV, 0) GFB_S_CASE(SRC, OP_DIV, 1)                        \
+    GFB_S_CASE(SRC, OP_MAX, 0) GFB_S_CASE(SRC, OP_MAX, 1)
+#define GFB_S_SELF(OPC) \
+    case F_BIN + ((SRC_SELF_) * 5 + (OPC)) * 2: \
+        _Pragma("unroll") for (int u = 0; u < U; ++u) { GFB_S_APPLY(OPC, 0, acc[u]) } break;
+#define GFB_S_UN(OPC) \
+    case F_UN + (OPC) - OP_NEG: _Pragma("unroll") for (int u = 0; u < U; ++u) apply_unary<T, V>(OPC, acc[u]); break;
+        constexpr int SRC_SELF_ = 6;
+#pragma unroll 1
+        for (uint32_t pc = 0; pc < n; ++pc) {
+            const uint32_t ins = p.prog[pc];
+            const int k = (int)((ins >> 8) & 0xffu);
+            switch (ins & 0xffu) {
+                case F_LOADP + 0:
+#pragma unroll
+                    for (int u = 0; u < U; ++u) operand(0, u, acc[u]);
+                    break;
+                case F_LOADP + 1:
+#pragma unroll
+                    for (int u = 0; u < U; ++u) operand(1, u, acc[u]);
+                    break;
+                case F_LOADP + 2:
+#pragma unroll
+                    for (int u = 0; u < U; ++u) operand(2, u, acc[u]);
+                    break;
+                case F_LOADP + 3:
+#pragma unroll
+                    for (int u = 0; u < U; ++u) operand(3, u, acc[u]);
+                    break;
+                case F_STORE: {
+                    const gfb_leaf& L = p.leaves[k];
+                    T* dst = resolve<T>(p.tab, L.ref);
+                    if (full && L.rlin == 1) {
+                        T* row = dst + part_offset(L, o, 0) + r0;
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                int4 q;
+                                T* qq = reinterpret_cast<T*>(&q);
+#pragma unroll
+                                for (int j = 0; j < HV; ++j) qq[j] = acc[u][h * HV + j];
+                                *reinterpret_cast<int4*>(row + sidx<T>(u, h, lane, 0)) = q;
+                            }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int j = 0; j < HV; ++j) {
+                                    const uint32_t e = sidx<T>(u, h, lane, j);
+                                    if (e < len) dst[leaf_offset(L, o, r0 + e)] = acc[u][h * HV + j];
+                                }
+                    }
+                    break;
+                }
+                GFB_S_UN(OP_NEG) GFB_S_UN(OP_EXP) GFB_S_UN(OP_LOG) GFB_S_UN(OP_TANH) GFB_S_UN(OP_SIGMOID) GFB_S_UN(OP_RELU)
+                GFB_S_OPS(0) GFB_S_OPS(1) GFB_S_OPS(2) GFB_S_OPS(3)
+                GFB_S_SELF(OP_ADD) GFB_S_SELF(OP_SUB) GFB_S_SELF(OP_MUL) GFB_S_SELF(OP_DIV) GFB_S_SELF(OP_MAX)
+            }
+        }
+#undef GFB_S_APPLY
+#undef GFB_S_CASE
+#undef GFB_S_OPS
+#undef GFB_S_SELF
+#undef GFB_S_UN
+        if (kind) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int j = 0; j < HV; ++j)
+                        if (full || sidx<T>(u, h, lane, j) < (int)len) part = fold<T>(kind, part, acc[u][h * HV + j]);
+            if (chunk == nch - 1) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) part = fold<T>(kind, part, __shfl_xor_sync(0xffffffffu, part, off));
+                if (lane == 0) resolve<T>(p.tab, p.red_out.ref)[leaf_offset(p.red_out, o, 0)] = part;
+                part = fold_init<T>(kind);
+            }
+        }
+        __syncwarp();
+        if (it + 2 < total) issue(it + 2);
+    }
+}
+
+template __global__ void gfb_ew_staged_kernel<float>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_staged_kernel<double>(const __grid_constant__ gfb_ew_args);
+
 template __global__ void gfb_ew_kernel<float, 8>(const __grid_constant__ gfb_ew_args);
 template __global__ void gfb_ew_kernel<double, 4>(const __grid_constant__ gfb_ew_args);
 template __global__ void gfb_ew_kernel<long long, 4>(const __grid_constant__ gfb_ew_args);
@@ -519,6 +775,8 @@ extern "C" const void* gfb_ew_kernel_ptr(int kind) {
         case GFB_K_EW_F64: return (const void*)gfb::gfb_ew_kernel<double, 4>;
         case GFB_K_EW_I64: return (const void*)gfb::gfb_ew_kernel<long long, 4>;
         case GFB_K_EW_U8: return (const void*)gfb::gfb_ew_kernel<unsigned char, 8>;
+        case GFB_K_EWS_F32: return (const void*)gfb::gfb_ew_staged_kernel<float>;
+        case GFB_K_EWS_F64: return (const void*)gfb::gfb_ew_staged_kernel<double>;
     }
     return nullptr;
 }

@@ -112,7 +112,7 @@ struct gfb_exe {
 namespace {
 
 const void* kernel_for(uint32_t kind) {
-    if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EW_U8) return gfb_ew_kernel_ptr((int)kind);
+    if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EWS_F64) return gfb_ew_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64)
         return gfb_simt_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_TC32) return gfb_tc_kernel_ptr((int)kind);

@@ -15,7 +15,7 @@ import numpy as np
 from paper_1801_08058_b200 import abi
 from paper_1801_08058_b200.compiler import decode_flat
 
-DT = {abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
+DT = {abi.K_EWS_F32: np.float32, abi.K_EWS_F64: np.float64, abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
       abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
 
 
@@ -101,7 +101,7 @@ def _bin(op, x, y, dt):
 
 def run_ew(mem, a, dt):
     n_o, n_r = a.n_o, a.n_r
-    assert a.mode in (1, 2) and a.vec_axis == (1 if a.mode == 1 else 0)
+    assert a.mode in (1, 2, 3) and a.vec_axis == (0 if a.mode == 2 else 1)
     o = np.repeat(np.arange(n_o, dtype=np.int64), n_r)
     r = np.tile(np.arange(n_r, dtype=np.int64), n_o)
 
@@ -221,7 +221,7 @@ def execute(lowered, inputs: list, out_specs: list) -> list:
     mem = Memory(lowered, [np.ascontiguousarray(x).reshape(-1) for x in inputs], outputs)
     for L in lowered.launches:
         dt = DT.get(L.kind)
-        if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8):
+        if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8, abi.K_EWS_F32, abi.K_EWS_F64):
             run_ew(mem, L.args, dt)
         elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64):
             run_dot(mem, L.args, dt)
