@@ -592,9 +592,9 @@ class Lowering:
             return False
         if any(c[0] in (I_PUSH, I_PUSH_LOAD, I_BIN_POP) for c in prog.code):
             return False
+        if sum(1 for l in prog.leaf_specs if not l.is_store) > MAX_PRELOAD:
+            return False  # every operand must be a preloaded leaf
         loads = [l for l in prog.leaf_specs if not l.is_store and l.buf.splat is None]
-        if len(loads) > MAX_PRELOAD:
-            return False
         def o_aligned(l):
             return all((d[3] * es) % 16 == 0 for d in l.digits if d[0] == 0)
         for l in loads:
@@ -1003,6 +1003,7 @@ class Program:
         mem = [i for i in loads if self.leaf_specs[i].buf.splat is None]
         mem.sort(key=lambda i: -self.leaf_specs[i].buf.nbytes)
         pre = mem[:MAX_PRELOAD]
+        pre += [i for i in loads if i not in pre][: MAX_PRELOAD - len(pre)]  # splats ride along
         rest = [i for i in loads if i not in pre]
         new_order = pre + rest + stores
         if len(new_order) > abi.MAX_LEAVES:

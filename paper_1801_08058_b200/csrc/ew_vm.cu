@@ -362,6 +362,7 @@ __device__ __forceinline__ void vm_run(const Ctx<T, V>& c, const Pre<T> (&pr)[4]
             GFB_OPS(4, GFB_PREP_MEM, b)
             GFB_OPS(5, GFB_PREP_POP, b)
             GFB_OPS(6, GFB_PREP_NONE, acc)
+            default: __trap();
         }
     }
 #undef GFB_APPLY
@@ -732,6 +733,7 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
                 GFB_S_UN(OP_NEG) GFB_S_UN(OP_EXP) GFB_S_UN(OP_LOG) GFB_S_UN(OP_TANH) GFB_S_UN(OP_SIGMOID) GFB_S_UN(OP_RELU)
                 GFB_S_OPS(0) GFB_S_OPS(1) GFB_S_OPS(2) GFB_S_OPS(3)
                 GFB_S_SELF(OP_ADD) GFB_S_SELF(OP_SUB) GFB_S_SELF(OP_MUL) GFB_S_SELF(OP_DIV) GFB_S_SELF(OP_MAX)
+                default: __trap();  // the compiler never emits other opcodes here
             }
         }
 #undef GFB_S_APPLY

@@ -121,6 +121,10 @@ def run_ew(mem, a, dt):
     acc = None
     stack = []
     pre = [load(k) for k in range(a.npre)]
+    if a.mode == 3:  # the staged kernel only implements these sources
+        for pc in range(a.ninstr):
+            ins = decode_flat(a.prog[pc])
+            assert ins[0] in ("loadp", "store", "un") or (ins[0] == "bin" and ins[1] in (0, 1, 2, 3, 6)), ins
     for pc in range(a.ninstr):
         ins = decode_flat(a.prog[pc])
         if ins[0] == "loadp":
