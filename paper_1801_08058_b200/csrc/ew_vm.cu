@@ -283,7 +283,7 @@ __device__ __forceinline__ void setup_pre(const Ctx<T, V>& c, Pre<T> (&pr)[4]) {
             const gfb_leaf& L = c.p.leaves[k];
             pr[k].ptr = reinterpret_cast<const T*>(c.base[k]) + c.ob[k * c.obs];
             pr[k].rl = L.rlin;
-            pr[k].vec = L.vec;
+            pr[k].vec = L.mode == 1 ? 0 : L.vec;  // splats take the generic (register) path
         }
     }
 }

@@ -242,10 +242,18 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
         }
         e->fns[i] = kernel_for(L.kind);
         if (!e->fns[i]) return bail(fail(GFB_ERR_INVALID, "unknown kernel kind " + std::to_string(L.kind)));
-        if (L.smem > 48 * 1024) {
-            err = cudaFuncSetAttribute(e->fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-            if (err != cudaSuccess) return bail(fail(GFB_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(err)));
-        }
+    }
+    // Opt every kernel in to the largest dynamic shared memory any of its
+    // launches needs (the attribute is per function, not per launch).
+    for (size_t i = 0; i < e->launches.size(); ++i) {
+        if (!e->fns[i] || e->launches[i].smem <= 48 * 1024) continue;
+        uint32_t need = 0;
+        for (size_t j = 0; j < e->launches.size(); ++j)
+            if (e->fns[j] == e->fns[i]) need = need > e->launches[j].smem ? need : e->launches[j].smem;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, e->fns[i]) == cudaSuccess && (uint32_t)fa.maxDynamicSharedSizeBytes >= need) continue;
+        err = cudaFuncSetAttribute(e->fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+        if (err != cudaSuccess) return bail(fail(GFB_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(err)));
     }
     *out = e;
     return GFB_OK;
