@@ -52,7 +52,8 @@ enum {
     GFB_K_EWS_F64 = 6,
     GFB_K_DOT_F32 = 10, /* SIMT Dot, sequential k, bit-exact (gfb_dot_args) */
     GFB_K_DOT_F64 = 11,
-    GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot (gfb_dot_args) */
+    GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot on split planes (gfb_tc_args) */
+    GFB_K_SPLIT_TF32 = 13, /* F32 -> TF32 hi/lo K-major planes (gfb_split_args) */
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
@@ -145,6 +146,36 @@ typedef struct {
     int64_t sh, sw, pt, pl;
     int64_t xs[4], ys[4], os[4]; /* element strides of the three operands */
 } gfb_conv_args;
+
+/* Split an F32 operand into TF32 hi / lo planes, K-major, rows x kp:
+ * hi = rna_tf32(x), lo = rna_tf32(x - hi); src element (row, k) at
+ * row * s_r + k * s_k (any strides, so transposes fold in here). */
+typedef struct {
+    const void* const* tab;
+    uint64_t src, hi, lo; /* GFB_REF */
+    int64_t rows, k, kp;
+    int64_t s_r, s_k;
+} gfb_split_args;
+
+#if defined(__GNUC__) || defined(__CUDACC__)
+#define GFB_ALIGN64 __attribute__((aligned(64)))
+#else
+#define GFB_ALIGN64
+#endif
+
+/* tcgen05 Dot on split planes: C[m, n] = sum_k (Ahi*Bhi + Ahi*Blo + Alo*Bhi).
+ * A planes are [M, kp_a] and B planes [N, kp_b] (both K-major); the four
+ * CUtensorMap blocks are encoded by gfb_exe_create from the plane refs. */
+typedef struct GFB_ALIGN64 {
+    const void* const* tab;
+    uint64_t c;
+    int64_t M, N, K;
+    int64_t c_sm, c_sn;
+    uint64_t a_hi, a_lo, b_hi, b_lo;
+    int64_t kp_a, kp_b;
+    int64_t pad[3];
+    uint64_t tmap[4][16];
+} gfb_tc_args;
 
 typedef struct {
     const void* const* tab;

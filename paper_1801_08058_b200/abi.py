@@ -12,7 +12,7 @@ GFB_OK = 0
 
 K_EW_F32, K_EW_F64, K_EW_I64, K_EW_U8 = 1, 2, 3, 4
 K_EWS_F32, K_EWS_F64 = 5, 6
-K_DOT_F32, K_DOT_F64, K_DOT_TC32 = 10, 11, 12
+K_DOT_F32, K_DOT_F64, K_DOT_TC32, K_SPLIT_TF32 = 10, 11, 12, 13
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
 
@@ -64,6 +64,24 @@ class DotArgs(C.Structure):
     ]
 
 
+class SplitArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("src", C.c_uint64), ("hi", C.c_uint64), ("lo", C.c_uint64),
+        ("rows", C.c_int64), ("k", C.c_int64), ("kp", C.c_int64), ("s_r", C.c_int64), ("s_k", C.c_int64),
+    ]
+
+
+class TcArgs(C.Structure):
+    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 128, size 640.
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64),
+        ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("c_sm", C.c_int64), ("c_sn", C.c_int64),
+        ("a_hi", C.c_uint64), ("a_lo", C.c_uint64), ("b_hi", C.c_uint64), ("b_lo", C.c_uint64),
+        ("kp_a", C.c_int64), ("kp_b", C.c_int64), ("pad", C.c_int64 * 3),
+        ("tmap", (C.c_uint64 * 16) * 4),
+    ]
+
+
 class ConvArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p),
@@ -103,5 +121,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

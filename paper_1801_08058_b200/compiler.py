@@ -114,6 +114,24 @@ VM_OP = {
 EW_KIND = {ElementType.F32: abi.K_EW_F32, ElementType.F64: abi.K_EW_F64, ElementType.I64: abi.K_EW_I64, ElementType.BOOL: abi.K_EW_U8}
 INDEX_LIMIT = 1 << 31
 
+# tcgen05 Dot (csrc/gemm_tc.cu): 128x128 tiles, 3 stages of 64 KB + barriers.
+TC_TILE = 128
+TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
+
+
+def use_tensor_cores(m: int, n: int, k: int) -> bool:
+    """F32 Dots big enough to fill tensor-core tiles go to tcgen05 3xTF32
+    (normwise 1e-5 contract); small / skinny ones keep the exact-order SIMT
+    kernel (bit-exact).  GFB_DOT=simt|tc overrides for tests."""
+    import os
+
+    mode = os.environ.get("GFB_DOT", "auto")
+    if mode == "simt":
+        return False
+    if mode == "tc":
+        return m >= 1 and n >= 1 and k >= 1
+    return m >= 64 and n >= 64 and k >= 64 and m * n * k >= (1 << 22)
+
 
 def magic_u31(d: int) -> tuple[int, int]:
     """(mul, sh) with n // d == (n * mul >> 32) >> sh for all 0 <= n < 2**31."""
@@ -318,7 +336,7 @@ class Lowered:
         blob = bytearray()
         for i, L in enumerate(self.launches):
             raw = bytes(L.args)
-            off = align_up(len(blob), 16)
+            off = align_up(len(blob), 64)  # tensor maps inside TcArgs need 64 B
             blob.extend(b"\0" * (off - len(blob)))
             blob.extend(raw)
             r = recs[i]
@@ -720,6 +738,34 @@ class Lowering:
             raise _Retry(ref_node)
         return op
 
+    def emit_dot_tc(self, n, a_op, b_op, out, m, nn, k):
+        """Split both operands into K-major TF32 hi/lo planes, then one
+        tcgen05 3xTF32 GEMM (csrc/gemm_tc.cu)."""
+        kp = align_up(k, 4)
+        planes = {}
+        for name, (buf, st), rows, s_r, s_k in (("a", a_op, m, a_op[1][0], a_op[1][1]),
+                                                 ("b", b_op, nn, b_op[1][1], b_op[1][0])):
+            hi = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
+            lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
+            self.buf[("tc", n, name, "hi")] = hi
+            self.buf[("tc", n, name, "lo")] = lo
+            sa = abi.SplitArgs(rows=rows, k=k, kp=kp, s_r=s_r, s_k=s_k)
+            rec = LaunchRec(abi.K_SPLIT_TF32, ((kp + 31) // 32, (rows + 31) // 32, 1), (256, 1, 1), 0, sa,
+                            [buf.key], [hi.key, lo.key], f"split_{name}#{n}")
+            rec.algo_bytes = rows * k * 4 + 2 * rows * kp * 4
+            rec.finalize = _finalize_refs(sa, {"src": buf, "hi": hi, "lo": lo})
+            self.launches.append(rec)
+            planes[name] = (hi, lo)
+        ta = abi.TcArgs(M=m, N=nn, K=k, c_sm=out.strides[0], c_sn=out.strides[1], kp_a=kp, kp_b=kp)
+        grid = ((nn + TC_TILE - 1) // TC_TILE, (m + TC_TILE - 1) // TC_TILE, 1)
+        (ahi, alo), (bhi, blo) = planes["a"], planes["b"]
+        rec = LaunchRec(abi.K_DOT_TC32, grid, (192, 1, 1), TC_SMEM, ta,
+                        [ahi.key, alo.key, bhi.key, blo.key], [out.key], f"dot_tc#{n}")
+        rec.flops = 2 * m * nn * k
+        rec.algo_bytes = (m * k + k * nn + m * nn) * 4
+        rec.finalize = _finalize_refs(ta, {"c": out, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
+        self.launches.append(rec)
+
     def emit_heavy(self, n: int):
         node = self.nodes[n]
         out = self.buf[n]
@@ -729,6 +775,9 @@ class Lowering:
             m, k = self.nodes[node.inputs[0][0]].output.shape
             nn = node.output.shape[1]
             if m == 0 or nn == 0:
+                return
+            if et is ElementType.F32 and use_tensor_cores(m, nn, k):
+                self.emit_dot_tc(n, (ab, ast), (bb, bst), out, m, nn, k)
                 return
             args = abi.DotArgs(m=m, n=nn, k=k, a_sm=ast[0], a_sk=ast[1], b_sk=bst[0], b_sn=bst[1],
                                c_sm=out.strides[0], c_sn=out.strides[1])

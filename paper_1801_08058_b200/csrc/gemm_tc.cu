@@ -1,4 +1,266 @@
-// tcgen05 tensor-core Dot (3xTF32) -- placeholder until the kernel lands.
+// tcgen05 tensor-core Dot for F32 graphs (3xTF32), sm_100a.
+//
+// The reference Dot (kernels.py:123-133) is an f32 multiply-add chain.  A
+// single TF32 product keeps 11 significant bits, which gives a normwise
+// error of ~3e-4 on config A's shapes (SURVEY.md §7 hard part 1).  So every
+// operand x is split as hi = rna_tf32(x), lo = rna_tf32(x - hi), and
+//   C = Ahi*Bhi + Ahi*Blo + Alo*Bhi
+// is accumulated in one fp32 TMEM accumulator by three tcgen05.mma
+// kind::tf32 instructions per K-step.  The result is about 1e-7 normwise,
+// within the 1e-5 Dot tolerance of SURVEY.md §8(c).
+//
+// gfb_split_kernel writes the hi/lo planes in K-major layout into the
+// arena.  Any operand strides are accepted, so autodiff's
+// Reshape(x, (1, 0)) transposes fold into this pass.  The GEMM itself is
+// one 128x128 output tile per CTA, 192 threads:
+//   warp 0        TMA producer: 4 tensor-map loads per K-block (SW128) into a
+//                 3-stage ring, completion on full[s] mbarriers
+//   warp 1        TMEM allocator + single-thread MMA issuer; tcgen05.commit
+//                 frees a stage (empty[s]) and finally signals the epilogue
+//   warps 2..5    epilogue: tcgen05.ld 32x32b from TMEM -> registers -> global
+// Shared memory: 3 x (16 KB Ahi + 16 KB Alo + 16 KB Bhi + 16 KB Blo).
+
+#include <cuda.h>
 #include <cuda_runtime.h>
-#include "gfb200.h"
-extern "C" const void* gfb_tc_kernel_ptr(int kind) { (void)kind; return nullptr; }
+
+#include <cstdint>
+
+#include "gfb_common.cuh"
+
+namespace gfb {
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB (BN == BM)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t TMEM_COLS = 128;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+// Bounded wait: a protocol bug traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint32_t spin = 0; spin < (1u << 28); ++spin) {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P;\n}"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+    }
+    __trap();
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms of 1 KB.
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+    const uint64_t addr = su32(p);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;          // start address
+    d |= (uint64_t)0 << 16;                // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;      // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                // version (sm100)
+    d |= (uint64_t)2 << 61;                // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, K-major A and B.
+constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4)               // c_format F32
+           | (2u << 7)             // a_format TF32
+           | (2u << 10)            // b_format TF32
+           | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+
+}  // namespace tc
+
+__global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_constant__ gfb_tc_args p) {
+    using namespace tc;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* accum = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int nk = (int)((p.K + BK - 1) / BK);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 4; ++i) prefetch_tmap(p.tmap[i]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                unsigned char* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], STAGE_BYTES);
+                const int kc = kb * BK;
+                tma_load_2d(st + 0 * TILE_BYTES, p.tmap[0], kc, m0, &full[s]);
+                tma_load_2d(st + 1 * TILE_BYTES, p.tmap[1], kc, m0, &full[s]);
+                tma_load_2d(st + 2 * TILE_BYTES, p.tmap[2], kc, n0, &full[s]);
+                tma_load_2d(st + 3 * TILE_BYTES, p.tmap[3], kc, n0, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                unsigned char* st = smem + s * STAGE_BYTES;
+                const uint64_t ah = smem_desc(st), al = smem_desc(st + TILE_BYTES);
+                const uint64_t bh = smem_desc(st + 2 * TILE_BYTES), bl = smem_desc(st + 3 * TILE_BYTES);
+#pragma unroll
+                for (int j = 0; j < BK / 8; ++j) {
+                    const uint64_t adv = (uint64_t)(j * 32) >> 4;  // 8 tf32 = 32 B along K inside the atom
+                    const uint32_t first = (kb | j) != 0;
+                    mma_tf32(tmem, ah + adv, bh + adv, idesc, first);
+                    mma_tf32(tmem, ah + adv, bl + adv, idesc, 1);
+                    mma_tf32(tmem, al + adv, bh + adv, idesc, 1);
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(accum);
+        }
+    } else {
+        // Epilogue: warp w reads TMEM lanes [32*(w%4), +32) = tile rows.
+        const int q = warp & 3;
+        mbar_wait(accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float* C = resolve<float>(p.tab, p.c);
+        const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                  "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+                  "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                  "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (row < p.M) {
+                const int col0 = n0 + c * 32;
+                float* dst = C + (int64_t)row * p.c_sm;
+                if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dst + col0 + j) =
+                            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                        __uint_as_float(r[j + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = __uint_as_float(r[j]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+// hi/lo TF32 planes, K-major [rows, kp], zero-padded past k.  32x32 tiles
+// through shared memory so both the strided read and the plane writes are
+// coalesced whichever axis of the source is contiguous.
+__global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ gfb_split_args p) {
+    __shared__ float tile[32][33];
+    const float* src = resolve<const float>(p.tab, p.src);
+    float* hi = resolve<float>(p.tab, p.hi);
+    float* lo = resolve<float>(p.tab, p.lo);
+    const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const bool k_fast = p.s_k <= p.s_r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int rr, kk;
+        if (k_fast) { rr = ty + 8 * i; kk = tx; } else { rr = tx; kk = ty + 8 * i; }
+        const int64_t r = r0 + rr, k = k0 + kk;
+        tile[rr][kk] = (r < p.rows && k < p.k) ? src[r * p.s_r + k * p.s_k] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = ty + 8 * i, kk = tx;
+        const int64_t r = r0 + rr, k = k0 + kk;
+        if (r < p.rows && k < p.kp) {
+            const float x = tile[rr][kk];
+            uint32_t h, l;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+            const float rest = __fsub_rn(x, __uint_as_float(h));
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(rest));
+            hi[r * p.kp + k] = __uint_as_float(h);
+            lo[r * p.kp + k] = __uint_as_float(l);
+        }
+    }
+}
+
+}  // namespace gfb
+
+extern "C" const void* gfb_tc_kernel_ptr(int kind) {
+    if (kind == GFB_K_DOT_TC32) return (const void*)gfb::gfb_gemm_tc_kernel;
+    if (kind == GFB_K_SPLIT_TF32) return (const void*)gfb::gfb_split_kernel;
+    return nullptr;
+}
+
+extern "C" int gfb_tc_smem_bytes(void) { return gfb::tc::SMEM_BYTES; }

@@ -219,6 +219,36 @@ def run_conv(mem, a, dt):
     O[idx] = out
 
 
+def _rna_tf32(x: np.ndarray) -> np.ndarray:
+    """cvt.rna.tf32.f32: round to nearest (ties away) keeping 10 mantissa bits."""
+    b = x.astype(np.float32).view(np.uint32).astype(np.uint64)
+    fin = np.isfinite(x)
+    r = ((b + 0x1000) & 0xFFFFE000).astype(np.uint32)
+    return np.where(fin, r.view(np.float32), x.astype(np.float32))
+
+
+def run_split(mem, a):
+    src = mem.view(a.src, np.float32)
+    r = np.arange(a.rows)[:, None]
+    k = np.arange(a.kp)[None, :]
+    x = np.where(k < a.k, src[np.minimum(r * a.s_r + np.minimum(k, max(a.k - 1, 0)) * a.s_k, src.size - 1)], 0.0).astype(np.float32)
+    hi = _rna_tf32(x)
+    lo = _rna_tf32((x - hi).astype(np.float32))
+    mem.view(a.hi, np.float32)[: a.rows * a.kp] = hi.reshape(-1)
+    mem.view(a.lo, np.float32)[: a.rows * a.kp] = lo.reshape(-1)
+
+
+def run_tc(mem, a):
+    ahi = mem.view(a.a_hi, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64)
+    alo = mem.view(a.a_lo, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64)
+    bhi = mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64)
+    blo = mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64)
+    c = (ahi @ bhi.T + ahi @ blo.T + alo @ bhi.T).astype(np.float32)
+    i = np.arange(a.M)[:, None]
+    j = np.arange(a.N)[None, :]
+    mem.view(a.c, np.float32)[i * a.c_sm + j * a.c_sn] = c
+
+
 def execute(lowered, inputs: list, out_specs: list) -> list:
     """inputs: storage-order numpy arrays; out_specs: (dtype, count)."""
     outputs = [np.zeros(max(c, 1), dtype=d) for d, c in out_specs]
@@ -231,6 +261,10 @@ def execute(lowered, inputs: list, out_specs: list) -> list:
             run_dot(mem, L.args, dt)
         elif L.kind in (abi.K_CONV_F32, abi.K_CONV_F64):
             run_conv(mem, L.args, dt)
+        elif L.kind == abi.K_SPLIT_TF32:
+            run_split(mem, L.args)
+        elif L.kind == abi.K_DOT_TC32:
+            run_tc(mem, L.args)
         else:
             raise NotImplementedError(L.kind)
     return [o[:c] for o, (_, c) in zip(outputs, out_specs)]

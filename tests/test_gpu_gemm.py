@@ -1,0 +1,56 @@
+"""tcgen05 3xTF32 Dot vs the oracle (normwise 1e-5)."""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import interp
+
+pytestmark = pytest.mark.gpu
+gf = pytest.importorskip("paper_1801_08058_b200")
+K = gf.OpKind
+F32 = gf.ElementType.F32
+
+
+def _dot_graph(m, k, n, ta=False, tb=False):
+    fn = gf.Function("dot")
+    a = fn.add_parameter(F32, (k, m) if ta else (m, k))
+    b = fn.add_parameter(F32, (n, k) if tb else (k, n))
+    x = fn.add_node(K.RESHAPE, [a], {"input_order": (1, 0), "output_shape": (m, k)}) if ta else a
+    y = fn.add_node(K.RESHAPE, [b], {"input_order": (1, 0), "output_shape": (k, n)}) if tb else b
+    fn.set_results([fn.add_node(K.DOT, [x, y])])
+    return fn
+
+
+@pytest.mark.parametrize("m,k,n,ta,tb", [
+    (128, 128, 128, False, False),
+    (256, 512, 384, False, False),
+    (130, 90, 70, False, False),
+    (300, 777, 129, True, False),
+    (257, 64, 511, False, True),
+    (200, 301, 190, True, True),
+    (1, 40, 3, False, False),
+])
+def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
+    monkeypatch.setenv("GFB_DOT", "tc")
+    fn = _dot_graph(m, k, n, ta, tb)
+    rng = np.random.default_rng(m * 7 + k + n)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    exe = gf.compile_function(fn)
+    assert any("dot_tc" in L.label for L in exe.lowered.launches)
+    out = gf.call(exe, [gf.tensor_from_flat(F32, a.shape, a) for a in ins])[0].to_numpy()
+    want = interp.run_function(fn, ins)[0]
+    err = G.normwise(out, want)
+    assert err <= 1e-5, err
+
+
+def test_tc_dot_large_config_E_layer():
+    fn = _dot_graph(2048, 4096, 4096)
+    rng = np.random.default_rng(0)
+    a = rng.uniform(-1, 1, size=(2048, 4096)).astype(np.float32)
+    b = rng.uniform(-1 / 64, 1 / 64, size=(4096, 4096)).astype(np.float32)
+    exe = gf.compile_function(fn)
+    assert any("dot_tc" in L.label for L in exe.lowered.launches)
+    out = gf.call(exe, [gf.tensor_from_flat(F32, a.shape, a), gf.tensor_from_flat(F32, b.shape, b)])[0].to_numpy()
+    ref = (a.astype(np.float64) @ b.astype(np.float64))
+    assert G.normwise(out, ref) <= 1e-5

@@ -62,3 +62,26 @@ def test_workloads_emulated(name):
     h = host_compile(fn)
     assert h.listing() == case["listing"]
     _compare(emulate(h, [G.tensor_of(d) for d in case["inputs"]]), case["outputs"], name)
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True)])
+def test_tensor_core_lowering_emulated(monkeypatch, ta, tb):
+    """Split planes + 3xTF32 product, emulated: normwise within 1e-5."""
+    import paper_1801_08058_b200 as gf
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_DOT", "tc")
+    m, k, n = 37, 70, 45
+    fn = gf.Function("dot")
+    K, F32 = gf.OpKind, gf.ElementType.F32
+    a = fn.add_parameter(F32, (k, m) if ta else (m, k))
+    b = fn.add_parameter(F32, (n, k) if tb else (k, n))
+    x = fn.add_node(K.RESHAPE, [a], {"input_order": (1, 0), "output_shape": (m, k)}) if ta else a
+    y = fn.add_node(K.RESHAPE, [b], {"input_order": (1, 0), "output_shape": (k, n)}) if tb else b
+    fn.set_results([fn.add_node(K.DOT, [x, y])])
+    h = host_compile(fn)
+    assert [L.label.split("#")[0] for L in h.lowered.launches] == ["split_a", "split_b", "dot_tc"]
+    rng = np.random.default_rng(1)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    out = emulate(h, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
