@@ -5,9 +5,11 @@
 // error of ~3e-4 on config A's shapes (SURVEY.md §7 hard part 1).  So every
 // operand x is split as hi = rna_tf32(x), lo = rna_tf32(x - hi), and
 //   C = Ahi*Bhi + Ahi*Blo + Alo*Bhi
-// is accumulated in one fp32 TMEM accumulator by three tcgen05.mma
-// kind::tf32 instructions per K-step.  The result is about 1e-7 normwise,
-// within the 1e-5 Dot tolerance of SURVEY.md §8(c).
+// is accumulated by three tcgen05.mma kind::tf32 instructions per K-step
+// into fp32 TMEM accumulators that are promoted into round-to-nearest fp32
+// registers every 128 K (the tensor core's own accumulation truncates),
+// which keeps the result well inside the 1e-5 normwise Dot tolerance of
+// SURVEY.md §8(c).
 //
 // gfb_split_kernel writes the hi/lo planes in K-major layout into the
 // arena.  Any operand strides are accepted, so autodiff's
@@ -16,8 +18,9 @@
 //   warp 0        TMA producer: 4 tensor-map loads per K-block (SW128) into a
 //                 3-stage ring, completion on full[s] mbarriers
 //   warp 1        TMEM allocator + single-thread MMA issuer; tcgen05.commit
-//                 frees a stage (empty[s]) and finally signals the epilogue
-//   warps 2..5    epilogue: tcgen05.ld 32x32b from TMEM -> registers -> global
+//                 frees a stage (empty[s]) and marks an accumulator chunk done
+//   warps 2..5    epilogue: tcgen05.ld 32x32b of each finished chunk, fp32
+//                 register accumulation, then 128-bit stores to global
 // Shared memory: 3 x (16 KB Ahi + 16 KB Alo + 16 KB Bhi + 16 KB Blo).
 
 #include <cuda.h>
@@ -34,7 +37,14 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
 constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB (BN == BM)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr uint32_t TMEM_COLS = 128;
+// The tensor core's fp32 accumulation truncates, so a 4096-deep K chain
+// drifts by ~3e-5.  Partial sums are promoted to CUDA-core fp32 registers
+// (round-to-nearest adds) every CHUNK_KB K-blocks (128 K): the MMA warp
+// cycles through NBUF TMEM accumulators while the epilogue warps drain the
+// finished ones, so the promotion overlaps the MMAs.
+constexpr int CHUNK_KB = 4;
+constexpr int NBUF = 4;
+constexpr uint32_t TMEM_COLS = BN * NBUF;  // 512: the whole TMEM of the SM
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -110,19 +120,24 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* accum = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+    uint64_t* tfull = empty + STAGES;   // [NBUF] accumulator chunk ready
+    uint64_t* tempty = tfull + NBUF;    // [NBUF] accumulator drained (4 epilogue warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int nk = (int)((p.K + BK - 1) / BK);
+    const int nchunk = nk > 0 ? (nk + CHUNK_KB - 1) / CHUNK_KB : 0;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum, 1);
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 4; ++i) prefetch_tmap(p.tmap[i]);
     }
@@ -157,57 +172,78 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % STAGES;
                 const uint32_t ph = (kb / STAGES) & 1;
+                const int chunk = kb / CHUNK_KB, b = chunk % NBUF;
+                const bool chunk_start = kb % CHUNK_KB == 0;
+                if (chunk_start) {
+                    mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);  // epilogue drained this buffer
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
                 mbar_wait(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 unsigned char* st = smem + s * STAGE_BYTES;
                 const uint64_t ah = smem_desc(st), al = smem_desc(st + TILE_BYTES);
                 const uint64_t bh = smem_desc(st + 2 * TILE_BYTES), bl = smem_desc(st + 3 * TILE_BYTES);
+                const uint32_t d = tmem + (uint32_t)(b * BN);
 #pragma unroll
                 for (int j = 0; j < BK / 8; ++j) {
                     const uint64_t adv = (uint64_t)(j * 32) >> 4;  // 8 tf32 = 32 B along K inside the atom
-                    const uint32_t first = (kb | j) != 0;
-                    mma_tf32(tmem, ah + adv, bh + adv, idesc, first);
-                    mma_tf32(tmem, ah + adv, bl + adv, idesc, 1);
-                    mma_tf32(tmem, al + adv, bh + adv, idesc, 1);
+                    const uint32_t acc = !(chunk_start && j == 0);
+                    mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+                    mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+                    mma_tf32(d, al + adv, bh + adv, idesc, 1);
                 }
                 mma_commit(&empty[s]);
+                if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == nk - 1) mma_commit(&tfull[b]);
             }
-            mma_commit(accum);
         }
     } else {
-        // Epilogue: warp w reads TMEM lanes [32*(w%4), +32) = tile rows.
+        // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows; it
+        // promotes every finished chunk into fp32 registers, then stores.
         const int q = warp & 3;
-        mbar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
+        float acc[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+        for (int chunk = 0; chunk < nchunk; ++chunk) {
+            const int b = chunk % NBUF;
+            mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+        }
         float* C = resolve<float>(p.tab, p.c);
         const int row = m0 + q * 32 + lane;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-                  "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-                  "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-                  "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (row < p.M) {
+        if (row < p.M) {
+            float* dst = C + (int64_t)row * p.c_sm;
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
                 const int col0 = n0 + c * 32;
-                float* dst = C + (int64_t)row * p.c_sm;
                 if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
                         *reinterpret_cast<float4*>(dst + col0 + j) =
-                            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                        __uint_as_float(r[j + 3]));
+                            make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = __uint_as_float(r[j]);
+                        if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
                 }
             }
         }
