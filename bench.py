@@ -255,18 +255,63 @@ def _traffic(workload):
         return None
 
 
-def bench_mlp(args, ws, rank, local):
-    """Config A training step (fwd + autodiff bwd + SGD), samples/s."""
+def launch_times(exe, dev_in, outs, stream, reps=3):
+    """Each launch alone (CUDA events on the launch stream), worst first, to stderr."""
+    import torch
+
+    prog = exe.program()
+    pin = [t.data_ptr() for t in dev_in]
+    pout = [t.data_ptr() for t in outs]
+    rows = []
+    for i, L in enumerate(exe.lowered.launches):
+        prog.run_one(i, pin, pout, stream.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            prog.run_one(i, pin, pout, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        rows.append((t, i, L))
+    total = sum(r[0] for r in rows)
+    sys.stderr.write(f"# per-launch times (ms), total {total:.3f}\n")
+    for t, i, L in sorted(rows, key=lambda r: -r[0])[:40]:
+        gbs = L.algo_bytes / (t * 1e-3) / 1e9 if t else 0
+        tfs = L.flops / (t * 1e-3) / 1e12 if t else 0
+        sys.stderr.write(f"{t:9.3f} {100 * t / total:5.1f}% #{i:3d} {L.label:28s} grid={L.grid} {gbs:8.1f} GB/s {tfs:7.1f} TF/s\n")
+
+
+def _step_for(workload, batch=None):
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import workloads as W
+
+    if workload == "A":
+        return W.mlp_step(gf, batch=batch or 128), batch or 128, "A: MLP 784-512-10"
+    if workload == "C":
+        return W.cnn_step(gf, batch=batch or 256), batch or 256, "C: CNN 32x32x3, conv 3->16->32, maxpool, fc 8192->10"
+    if workload == "E":
+        b = batch or 65536
+        return (W.mlp_step(gf, batch=b, in_dim=4096, hidden=(4096,) * 7, out_dim=4096, loss_batch=65536), b,
+                "E: wide MLP 4096 x 8 layers")
+    raise ValueError(workload)
+
+
+def bench_step(args, ws, rank, local):
+    """Training step (fwd + autodiff bwd + SGD as one Function), samples/s."""
     import torch
 
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import workloads as W
 
     torch.cuda.set_device(local)
-    step = W.mlp_step(gf, batch=128)
+    step, batch, desc = _step_for(args.workload, args.batch)
+    t_compile = time.perf_counter()
     exe = gf.compile_function(step.fn)
-    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=0)
+    t_compile = time.perf_counter() - t_compile
+    shapes = W.parameter_shapes(step)
+    arrays = W.step_inputs(step, shapes, seed=rank)
     dev_in = [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for a in arrays]
+    del arrays
     outs = exe.allocate_outputs()
     stream = torch.cuda.current_stream()
     with ClockSampler(local) as clk:
@@ -280,13 +325,18 @@ def bench_mlp(args, ws, rank, local):
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
+    if args.launch_times:
+        launch_times(exe, dev_in, outs, stream)
     flops = sum(L.flops for L in exe.lowered.launches)
+    _, tf_peak, _ = peaks()
     return {
-        "metric": "training-step samples/sec (config A: MLP 784-512-10, batch 128, fwd+autodiff bwd+SGD)",
-        "value": 128 / (ms * 1e-3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "metric": f"training-step samples/sec (config {desc}, batch {batch}, fwd+autodiff bwd+SGD)",
+        "value": batch / (ms * 1e-3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": "A: mlp_step batch=128 784-512-10", "launches": exe.num_launches,
-                                        "flops_per_step": flops},
+        "data": "synthetic", "config": {"workload": desc, "batch": batch, "launches": exe.num_launches,
+                                        "flops_per_step": flops, "arena_bytes": exe.lowered.arena_bytes,
+                                        "compile_s": t_compile},
+        "achieved_tflops": flops / (ms * 1e-3) / 1e12,
         "gpu_launches": exe.num_launches * args.steps, "clocks": clk.summary(),
     }
 
@@ -297,7 +347,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="B", choices=["B", "A"])
+    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "E"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -318,7 +370,7 @@ def main():
         print(json.dumps(line))
         return
 
-    line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_mlp(args, ws, rank, local)
+    line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_step(args, ws, rank, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "B":
         value, threads, sample = cpu_reference(ROWS, COLS, 2, 1, budget_s=30.0)
         line["cpu_baseline"] = {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}

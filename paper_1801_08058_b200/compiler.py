@@ -590,13 +590,31 @@ class Lowering:
             wpr *= 2
         rpb = 8 // wpr
         if staged:
-            args = prog.args(mode=3, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=1)
             chunk = 32 * 2 * (16 // et.byte_size) * 2
-            smem = 8 * 2 * args.npre * chunk * et.byte_size
+            nch = (n_r + chunk - 1) // chunk
+            smem = 8 * 2 * min(MAX_PRELOAD, max(1, sum(1 for l in prog.leaf_specs if not l.is_store))) * chunk * et.byte_size
             per_sm = max(1, min(8, (200 * 1024) // max(smem, 1)))
-            grid = max(1, min((n_o + 7) // 8, NUM_SMS * per_sm))
+            slots = NUM_SMS * per_sm * 8  # resident warps
+            chunkwise = n_o < slots and nch > 1
+            partial = None
+            if chunkwise and red_kind:
+                # few long rows: per-chunk partials, then a short second pass
+                partial = Buffer(self.new_key(), et, (n_o, nch), (nch, 1))
+                self.buf[("partial", partial.key)] = partial
+                final = prog.red_out
+                prog.red_out = LeafSpec(partial, [(0, 1, None, 1)], True, 0)
+            args = prog.args(mode=3, n_o=n_o, n_r=n_r, red_kind=red_kind, split=1 if chunkwise else 0, wpr=1)
+            smem = 8 * 2 * args.npre * chunk * et.byte_size
+            items = n_o * nch if chunkwise else n_o
+            grid = max(1, min((items + 7) // 8, NUM_SMS * per_sm))
             kind = abi.K_EWS_F32 if et is ElementType.F32 else abi.K_EWS_F64
-            self.add_launch(kind, (grid, 1, 1), (256, 1, 1), smem, args, prog, label + ":staged")
+            self.add_launch(kind, (grid, 1, 1), (256, 1, 1), smem, args, prog, label + (":staged2" if chunkwise else ":staged"))
+            if partial is not None:
+                p2 = Program(self, extents=(n_o, nch), vec_src=0, et=et)
+                k = p2.leaf(partial, [(0, 1, n_o), (1, 1, nch)] if n_o > 1 else [None, (1, 1, nch)])
+                p2.emit(I_LOAD, k=k)
+                p2.red_out = final
+                self._col_launch(p2, n_o, nch, red_kind, label + ":pass2", et)
             return
         grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)

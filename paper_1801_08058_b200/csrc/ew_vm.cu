@@ -578,10 +578,31 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
     }
     __syncwarp();
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, tw = gridDim.x * (blockDim.x >> 5);
-    if (gw >= n_o) return;
     const uint32_t nch = (n_r + CH - 1) / CH;
-    const uint32_t nrows = (n_o - gw + tw - 1) / tw;
-    const uint32_t total = nrows * nch;
+    // Work items are (o, chunk).  Row-wise (split == 0): a warp owns whole
+    // rows (o = gw, gw + tw, ...) and folds them itself.  Chunk-wise
+    // (split == 1, few long rows): items gw, gw + tw, ... of the flattened
+    // (o, chunk) space, and a fold writes one partial per chunk to
+    // red_out[o * nch + chunk] for a second, deterministic pass.
+    const bool chunkwise = p.split == 1;
+    uint32_t total;
+    if (chunkwise) {
+        const uint32_t items = n_o * nch;
+        total = gw < items ? (items - gw + tw - 1) / tw : 0;
+    } else {
+        total = gw < n_o ? ((n_o - gw + tw - 1) / tw) * nch : 0;
+    }
+    if (total == 0) return;
+    auto item_of = [&](uint32_t it, uint32_t& o, uint32_t& chunk) {
+        if (chunkwise) {
+            const uint32_t g = gw + it * tw;
+            o = g / nch;
+            chunk = g % nch;
+        } else {
+            o = gw + (it / nch) * tw;
+            chunk = it % nch;
+        }
+    };
     // leaf classes (uniform): 1 = staged (r-contiguous), 2 = row scalar, 3 = splat
     int cls[4];
 #pragma unroll
@@ -598,7 +619,8 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
         lbase[k] = (k < npre && cls[k] != 3) ? reinterpret_cast<const char*>(p.tab[p.leaves[k].ref >> 56]) + (p.leaves[k].ref & kOffsetMask) : nullptr;
 
     auto issue = [&](uint32_t it) {
-        const uint32_t o = gw + (it / nch) * tw, chunk = it % nch;
+        uint32_t o, chunk;
+        item_of(it, o, chunk);
         const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
         const int st = it & 1;
         uint32_t nst = 0;
@@ -625,7 +647,8 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
     uint32_t cur_o = 0xffffffffu;
     for (uint32_t it = 0; it < total; ++it) {
         const int st = it & 1;
-        const uint32_t o = gw + (it / nch) * tw, chunk = it % nch;
+        uint32_t o, chunk;
+        item_of(it, o, chunk);
         const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
         if (o != cur_o) {
             cur_o = o;
@@ -749,10 +772,14 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
 #pragma unroll
                     for (int j = 0; j < HV; ++j)
                         if (full || sidx<T>(u, h, lane, j) < (int)len) part = fold<T>(kind, part, acc[u][h * HV + j]);
-            if (chunk == nch - 1) {
+            if (chunkwise || chunk == nch - 1) {
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) part = fold<T>(kind, part, __shfl_xor_sync(0xffffffffu, part, off));
-                if (lane == 0) resolve<T>(p.tab, p.red_out.ref)[leaf_offset(p.red_out, o, 0)] = part;
+                if (lane == 0) {
+                    T* red = resolve<T>(p.tab, p.red_out.ref);
+                    if (chunkwise) red[(size_t)o * nch + chunk] = part;  // scratch partials
+                    else red[leaf_offset(p.red_out, o, 0)] = part;
+                }
                 part = fold_init<T>(kind);
             }
         }

@@ -56,7 +56,8 @@ def _append_sgd(api, g, wrt_ids_in_g, grad_refs, lr: float, et):
 
 
 def _softmax_xent(api, fn, logits, t, batch, et):
-    """loss = -sum(t * log softmax(logits)) / batch."""
+    """loss = -sum(t * log softmax(logits)) / batch (batch = the GLOBAL batch
+    under data parallelism, so per-rank partial losses and gradients sum)."""
     K = api.OpKind
     p = api.build_softmax(fn, logits, 1)
     tl = fn.add_node(K.MULTIPLY, [t, fn.add_node(K.LOG, [p])])
@@ -75,8 +76,12 @@ def _training_step(api, fwd, loss, names, weights, lr, et) -> StepGraph:
     return StepGraph(g, names + ["seed"], list(weights), len(new))
 
 
-def mlp_step(api, batch=128, in_dim=784, hidden=(512,), out_dim=10, lr=0.01, bias=True, f32=True) -> StepGraph:
-    """MLP training step (config A; config E with hidden=[4096]*7, in=out=4096)."""
+def mlp_step(api, batch=128, in_dim=784, hidden=(512,), out_dim=10, lr=0.01, bias=True, f32=True,
+             loss_batch=None) -> StepGraph:
+    """MLP training step (config A; config E with hidden=[4096]*7, in=out=4096).
+
+    `batch` is the per-replica batch the graph is specialised to;
+    `loss_batch` (default `batch`) is the divisor of the summed loss."""
     et = api.ElementType.F32 if f32 else api.ElementType.F64
     K = api.OpKind
     fn = api.Function("mlp_step")
@@ -101,7 +106,7 @@ def mlp_step(api, batch=128, in_dim=784, hidden=(512,), out_dim=10, lr=0.01, bia
             h = fn.add_node(K.ADD, [h, fn.add_node(K.BROADCAST, [b], {"output_shape": (batch, dims[i + 1]), "broadcast_axes": (0,)})])
         if i < len(layers) - 1:
             h = fn.add_node(K.RELU, [h])
-    loss = _softmax_xent(api, fn, h, t, batch, et)
+    loss = _softmax_xent(api, fn, h, t, loss_batch or batch, et)
     weights = [n for n in names if n[0] in "Wb"]
     return _training_step(api, fn, loss, names, weights, lr, et)
 

@@ -161,6 +161,18 @@ def run_ew(mem, a, dt):
         with np.errstate(all="ignore"):
             for j in range(n_r):
                 red = (red.astype(np.uint64) + vals[:, j].astype(np.uint64)).astype(np.int64) if dt == np.int64 else (red + vals[:, j]).astype(dt)
+    if a.mode == 3 and a.split == 1:  # chunk-wise staged: per-chunk partials
+        chunk = 32 * 2 * (16 // np.dtype(dt).itemsize) * 2
+        nch = (n_r + chunk - 1) // chunk
+        part = np.zeros((n_o, nch), dtype=dt)
+        for c in range(nch):
+            sub = vals[:, c * chunk:(c + 1) * chunk]
+            acc2 = np.full(n_o, -np.inf, dtype=dt) if a.red_kind == 2 else np.zeros(n_o, dtype=dt)
+            for j in range(sub.shape[1]):
+                acc2 = (np.where(acc2 >= sub[:, j], acc2, sub[:, j]) if a.red_kind == 2 else acc2 + sub[:, j]).astype(dt)
+            part[:, c] = acc2
+        mem.view(a.red_out.ref, dt)[: n_o * nch] = part.reshape(-1)
+        return
     oo = np.arange(n_o, dtype=np.int64)
     mem.view(a.red_out.ref, dt)[leaf_offsets(a.red_out, oo, np.zeros_like(oo))] = red
 

@@ -52,3 +52,19 @@ def test_config_B(rows):
     outs = [t.to_numpy() for t in gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])]
     assert G.same_bits(outs[0], want[0])  # elementwise chain: bit-exact
     assert G.normwise(outs[1], want[1]) <= 1e-5  # tree-ordered row sums
+
+
+@pytest.mark.parametrize("shape,axes", [((3, 5000), (1,)), ((2, 300, 40), (1, 2)), ((1 << 22,), (0,)), ((16, 65536), (0, 1))])
+def test_long_row_reductions(shape, axes):
+    K, F32 = gf.OpKind, gf.ElementType.F32
+    fn = gf.Function("red")
+    x = fn.add_parameter(F32, shape)
+    e = fn.add_node(K.EXP, [x])
+    fn.set_results([fn.add_node(K.SUM, [e], {"reduction_axes": axes}), fn.add_node(K.NEGATE, [e])])
+    rng = np.random.default_rng(0)
+    v = rng.uniform(-1, 1, size=shape).astype(np.float32)
+    outs = [t.to_numpy() for t in gf.call(gf.compile_function(fn), [gf.tensor_from_flat(F32, shape, v)])]
+    interp.set_threads(interp.max_threads())
+    want = interp.run_function(fn, [v])
+    assert G.normwise(outs[0], want[0]) <= 1e-5
+    assert G.same_bits(outs[1], want[1])
