@@ -281,32 +281,49 @@ def launch_times(exe, dev_in, outs, stream, reps=3):
         sys.stderr.write(f"{t:9.3f} {100 * t / total:5.1f}% #{i:3d} {L.label:28s} grid={L.grid} {gbs:8.1f} GB/s {tfs:7.1f} TF/s\n")
 
 
-def _step_for(workload, batch=None):
+def _step_for(workload, batch=None, ws=1):
+    """(step graph, per-GPU batch, description); `batch` is the GLOBAL batch."""
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import workloads as W
 
     if workload == "A":
-        return W.mlp_step(gf, batch=batch or 128), batch or 128, "A: MLP 784-512-10"
+        g = batch or 128
+        return W.mlp_step(gf, batch=g // ws, loss_batch=g), g // ws, "A: MLP 784-512-10"
     if workload == "C":
-        return W.cnn_step(gf, batch=batch or 256), batch or 256, "C: CNN 32x32x3, conv 3->16->32, maxpool, fc 8192->10"
+        g = batch or 256
+        return (W.cnn_step(gf, batch=g // ws, loss_batch=g), g // ws,
+                "C: CNN 32x32x3, conv 3->16->32, maxpool, fc 8192->10")
     if workload == "E":
-        b = batch or 65536
-        return (W.mlp_step(gf, batch=b, in_dim=4096, hidden=(4096,) * 7, out_dim=4096, loss_batch=65536), b,
+        g = batch or 65536
+        return (W.mlp_step(gf, batch=g // ws, in_dim=4096, hidden=(4096,) * 7, out_dim=4096, loss_batch=g), g // ws,
                 "E: wide MLP 4096 x 8 layers")
     raise ValueError(workload)
 
 
 def bench_step(args, ws, rank, local):
-    """Training step (fwd + autodiff bwd + SGD as one Function), samples/s."""
+    """Training step (fwd + autodiff bwd + SGD as one Function), samples/s.
+
+    Under torchrun the global batch is sharded over the ranks (strong
+    scaling): each rank runs the graph specialised to batch/ws with the loss
+    still divided by the global batch, and the partial gradients are summed
+    by NCCL all-reduces captured inside the step's CUDA graph."""
     import torch
 
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import workloads as W
 
     torch.cuda.set_device(local)
-    step, batch, desc = _step_for(args.workload, args.batch)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    step, batch, desc = _step_for(args.workload, args.batch, ws)
     t_compile = time.perf_counter()
-    exe = gf.compile_function(step.fn)
+    dp = None
+    if ws > 1 or args.dp:
+        names = step.param_names
+        dp = gf.DataParallel([step.fn.parameters[names.index("x")], step.fn.parameters[names.index("t")]], world_size=ws)
+    exe = gf.compile_function(step.fn, data_parallel=dp)
     t_compile = time.perf_counter() - t_compile
     shapes = W.parameter_shapes(step)
     arrays = W.step_inputs(step, shapes, seed=rank)
@@ -314,29 +331,41 @@ def bench_step(args, ws, rank, local):
     del arrays
     outs = exe.allocate_outputs()
     stream = torch.cuda.current_stream()
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
             exe.run_device(dev_in, outs, stream=stream.cuda_stream)
-        torch.cuda.synchronize()
+        barrier()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
             exe.run_device(dev_in, outs, stream=stream.cuda_stream)
         t1.record(stream)
-        torch.cuda.synchronize()
+        barrier()
     ms = t0.elapsed_time(t1) / args.steps
+    if ws > 1:
+        ms_t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(ms_t.item())
     if args.launch_times:
         launch_times(exe, dev_in, outs, stream)
     flops = sum(L.flops for L in exe.lowered.launches)
     _, tf_peak, _ = peaks()
+    gbatch = batch * ws
     return {
-        "metric": f"training-step samples/sec (config {desc}, batch {batch}, fwd+autodiff bwd+SGD)",
-        "value": batch / (ms * 1e-3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "metric": f"training-step samples/sec (config {desc}, global batch {gbatch}, fwd+autodiff bwd+SGD)",
+        "value": gbatch / (ms * 1e-3), "unit": "samples/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": desc, "batch": batch, "launches": exe.num_launches,
-                                        "flops_per_step": flops, "arena_bytes": exe.lowered.arena_bytes,
+        "data": "synthetic", "config": {"workload": desc, "global_batch": gbatch, "batch_per_gpu": batch,
+                                        "parallelism": f"dp{ws}", "launches": exe.num_launches,
+                                        "allreduces": len(getattr(exe, "allreduce", ()) or ()),
+                                        "flops_per_step_per_gpu": flops, "arena_bytes": exe.lowered.arena_bytes,
                                         "compile_s": t_compile},
-        "achieved_tflops": flops / (ms * 1e-3) / 1e12,
+        "achieved_tflops": ws * flops / (ms * 1e-3) / 1e12,
         "gpu_launches": exe.num_launches * args.steps, "clocks": clk.summary(),
     }
 
@@ -350,6 +379,7 @@ def main():
     ap.add_argument("--workload", default="B", choices=["B", "A", "C", "E"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
+    ap.add_argument("--dp", action="store_true", help="data-parallel plan even at one GPU (NCCL all-reduces)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

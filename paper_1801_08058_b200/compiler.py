@@ -368,10 +368,11 @@ class _Node:
 
 
 class Lowering:
-    def __init__(self, g: Function, layouts: dict, private: bool = False):
+    def __init__(self, g: Function, layouts: dict, private: bool = False, allreduce=frozenset()):
         self.g = g
         self.layouts = layouts
         self.private = private
+        self.allreduce = set(allreduce)  # data-parallel partial roots (dp.analyse)
         self.order = [n for n in topological_order(g) if n in reachable_from_results(g)]
         self.topo = {n: i for i, n in enumerate(self.order)}
         self.nodes = {n: _Node(g.nodes[n], g) for n in self.order}
@@ -492,7 +493,8 @@ class Lowering:
         result_slot = {}  # node -> output index written directly by its producer
         for j, (r, _) in enumerate(results):
             node = self.nodes[r]
-            if node.op not in (OpKind.PARAMETER, OpKind.CONSTANT) and r not in result_slot:
+            # all-reduced roots need a fixed (arena) address inside the CUDA graph
+            if node.op not in (OpKind.PARAMETER, OpKind.CONSTANT) and r not in result_slot and r not in self.allreduce:
                 result_slot[r] = j
 
         for n in self.order:
@@ -537,6 +539,8 @@ class Lowering:
                     self.emit_reduce(n, side_of.get(n))
                 else:
                     self.emit_map(n, [n])
+            if n in self.allreduce:
+                self.emit_allreduce(n)
 
         # results that are parameters / constants / repeated: copy launches
         for j, (r, _) in enumerate(results):
@@ -671,7 +675,10 @@ class Lowering:
         while inner_from > 0 and _prod(shape[inner_from:]) < 256:
             inner_from -= 1
         n_r = _prod(shape[inner_from:])
-        if n_r >= 128 and inner_from < len(shape):
+        # rows x columns only when there are enough rows to fill the GPU;
+        # a map has no reason to run few, very long rows (flat mode instead)
+        few_rows = total // max(n_r, 1) < NUM_SMS * 8 and n_r > 8192
+        if n_r >= 128 and inner_from < len(shape) and not few_rows:
             n_o = total // n_r
             prog = Program(self, extents=(max(n_o, 1), n_r), vec_src=1, et=et)
             try:
@@ -747,6 +754,20 @@ class Lowering:
         rec = LaunchRec(kind, grid, block, smem, args, prog.reads(), prog.writes(), label)
         rec.algo_bytes = prog.algo_bytes()
         rec.finalize = prog.finalize_fn(args)
+        self.launches.append(rec)
+
+    def emit_allreduce(self, n: int):
+        """In-place NCCL sum of a data-parallel partial root across ranks."""
+        b = self.buf.get(n)
+        if b is None or b.slot != abi.SLOT_ARENA:
+            raise UnsupportedOp(f"data parallel: partial root {n} is not materialised in the arena")
+        d = self.nodes[n].output
+        if d.element_type not in (ElementType.F32, ElementType.F64):
+            raise UnsupportedOp("data parallel all-reduce needs a float tensor")
+        args = abi.AllReduceArgs(count=element_count(d.shape), dtype=0 if d.element_type is ElementType.F32 else 1)
+        rec = LaunchRec(abi.K_ALLREDUCE, (1, 1, 1), (1, 1, 1), 0, args, [b.key], [b.key], f"allreduce#{n}")
+        rec.algo_bytes = b.nbytes
+        rec.finalize = _finalize_refs(args, {"buf": b})
         self.launches.append(rec)
 
     # -- heavy ops
@@ -1176,5 +1197,5 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
         d.stride = stride
 
 
-def lower(g: Function, layouts: dict, private: bool = False) -> Lowered:
-    return Lowering(g, layouts, private).run()
+def lower(g: Function, layouts: dict, private: bool = False, allreduce=frozenset()) -> Lowered:
+    return Lowering(g, layouts, private, allreduce).run()

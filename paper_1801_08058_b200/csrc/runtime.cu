@@ -162,7 +162,6 @@ int launch_one(gfb_exe* e, size_t i, cudaStream_t s) {
     if (L.kind == GFB_K_ALLREDUCE) {
         const gfb_allreduce_args* a = (const gfb_allreduce_args*)blob;
         if (!e->comm) return fail(GFB_ERR_INVALID, "plan has an all-reduce but no communicator");
-        if (e->comm->nranks == 1) return GFB_OK;
         void* ptr = (char*)((a->buf >> 56) == GFB_SLOT_ARENA ? e->arena : nullptr) + (a->buf & ((1ull << 56) - 1));
         if ((a->buf >> 56) != GFB_SLOT_ARENA) return fail(GFB_ERR_INVALID, "all-reduce bucket must live in the arena");
         ncclResult_t r = g_nccl.AllReduce(ptr, ptr, (size_t)a->count, a->dtype == 0 ? 7 /*ncclFloat32*/ : 8 /*ncclFloat64*/,

@@ -285,13 +285,15 @@ class HostCompiled:
     parameter_signature: list
     result_signature: list
     lowered: Lowered
+    allreduce: frozenset = frozenset()
 
     def listing(self) -> str:
         return Executable.listing(self)
 
 
 def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = "identity",
-                     parameter_layouts=None, evaluate=None, private: bool = False) -> HostCompiled:
+                     parameter_layouts=None, evaluate=None, private: bool = False,
+                     data_parallel=None) -> HostCompiled:
     """Validate, optimise, assign layouts, plan and lower (reference
     interpreter.py:92-170 plus the B200 lowering).  `evaluate` overrides the
     constant-folding evaluator (the device by default)."""
@@ -308,17 +310,77 @@ def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     instructions, pool_refs, param_index, result_index = _build_listing(g, plan)
     param_sig = [(g.nodes[pid].output, layouts[(pid, 0)]) for pid in g.parameters]
     result_sig = [(g.nodes[r].outputs[p], layouts[(r, p)]) for r, p in g.results]
-    lowered = lower(g, layouts, private=private)
+    roots = frozenset()
+    if data_parallel is not None:
+        from .dp import analyse
+
+        position = {pid: i for i, pid in enumerate(fn.parameters)}
+        data_parallel.batch_params = [g.parameters[position[p]] if p in position else p for p in data_parallel.batch_params]
+        roots = frozenset(analyse(g, data_parallel))
+    lowered = lower(g, layouts, private=private, allreduce=roots)
     return HostCompiled(g, layouts, plan, instructions, pool_refs, param_index, result_index,
-                        param_sig, result_sig, lowered)
+                        param_sig, result_sig, lowered, roots)
 
 
 def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = "identity",
-                     parameter_layouts=None, cuda_graph: bool = True, comm=None) -> Executable:
-    h = prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=parameter_layouts)
-    return Executable(h.graph, h.instructions, h.plan, _ConstPool(h.graph, h.pool_refs), h.layouts,
-                      h.param_index, h.result_index, h.parameter_signature, h.result_signature,
-                      h.lowered, cuda_graph, comm)
+                     parameter_layouts=None, cuda_graph: bool = True, data_parallel=None,
+                     comm=None) -> Executable:
+    """Reference `compile_function` plus B200 options: `cuda_graph` (capture
+    the launch list once), `data_parallel` (a `dp.DataParallel`: batch-shard
+    the listed parameters and all-reduce the partial gradients) with the
+    NCCL communicator `comm` from `init_distributed()`."""
+    h = prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=parameter_layouts,
+                         data_parallel=data_parallel)
+    if h.allreduce and comm is None:
+        comm = init_distributed()
+    handle = comm.handle if comm is not None else None
+    exe = Executable(h.graph, h.instructions, h.plan, _ConstPool(h.graph, h.pool_refs), h.layouts,
+                     h.param_index, h.result_index, h.parameter_signature, h.result_signature,
+                     h.lowered, cuda_graph, handle)
+    exe.comm = comm
+    exe.allreduce = h.allreduce
+    return exe
+
+
+class Comm:
+    """NCCL communicator owned by libgfb200.so (one per process / GPU)."""
+
+    def __init__(self, handle, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _LIB is not None:
+            _LIB.gfb_comm_destroy(self.handle)
+            self.handle = None
+
+
+_COMM = None
+
+
+def init_distributed(rank: int | None = None, world: int | None = None) -> Comm:
+    """NCCL communicator over the current torch.distributed group (or a
+    single-rank one).  Rank 0 creates the ncclUniqueId; it travels through
+    torch.distributed (any backend) — torch is only the rendezvous."""
+    global _COMM
+    import torch.distributed as dist
+
+    ensure_device()
+    if rank is None:
+        rank = dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
+        world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    if _COMM is not None and (_COMM.rank, _COMM.world) == (rank, world):
+        return _COMM
+    uid = C.create_string_buffer(128)
+    if rank == 0:
+        check(lib().gfb_comm_unique_id(uid), "gfb_comm_unique_id")
+    if world > 1:
+        box = [bytes(uid.raw)]
+        dist.broadcast_object_list(box, src=0)
+        uid = C.create_string_buffer(box[0], 128)
+    handle = C.c_void_p()
+    check(lib().gfb_comm_create(world, rank, uid, C.byref(handle)), "gfb_comm_create")
+    _COMM = Comm(handle, rank, world)
+    return _COMM
 
 
 def _check_signature(exe: Executable, inputs: list):

@@ -128,7 +128,8 @@ def maxpool2x2(api, fn, x, shape):
     return fn.add_node(K.RESHAPE, [top], {"input_order": (0, 1), "output_shape": (n, c, h2, w2)})
 
 
-def cnn_step(api, batch=256, image=32, channels=(3, 16, 32), classes=10, lr=0.01, f32=True) -> StepGraph:
+def cnn_step(api, batch=256, image=32, channels=(3, 16, 32), classes=10, lr=0.01, f32=True,
+             loss_batch=None) -> StepGraph:
     """Small CNN training step (config C): conv-relu-conv-relu-pool-fc-softmax."""
     et = api.ElementType.F32 if f32 else api.ElementType.F64
     K = api.OpKind
@@ -147,7 +148,7 @@ def cnn_step(api, batch=256, image=32, channels=(3, 16, 32), classes=10, lr=0.01
     p = maxpool2x2(api, fn, h, (batch, c2, image, image))
     flat = fn.add_node(K.RESHAPE, [p], {"input_order": (0, 1, 2, 3), "output_shape": (batch, feat)})
     logits = fn.add_node(K.DOT, [flat, wf])
-    loss = _softmax_xent(api, fn, logits, t, batch, et)
+    loss = _softmax_xent(api, fn, logits, t, loss_batch or batch, et)
     return _training_step(api, fn, loss, names, ["K1", "K2", "Wf"], lr, et)
 
 

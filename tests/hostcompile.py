@@ -7,12 +7,12 @@ from paper_1801_08058_b200.runtime import prepare_function
 import plan_emulator
 
 
-def host_compile(fn, optimize=True, conv_layout="identity", parameter_layouts=None, private=False):
+def host_compile(fn, optimize=True, conv_layout="identity", parameter_layouts=None, private=False, data_parallel=None):
     layouts = None
     if parameter_layouts is not None:
         layouts = [None if o is None else Layout(tuple(o)) for o in parameter_layouts]
     return prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=layouts,
-                            evaluate=interp.fold_evaluator, private=private)
+                            evaluate=interp.fold_evaluator, private=private, data_parallel=data_parallel)
 
 
 def emulate(h, tensors):

@@ -261,6 +261,54 @@ def run_tc(mem, a):
     mem.view(a.c, np.float32)[i * a.c_sm + j * a.c_sn] = c
 
 
+def _run_launch(mem, L):
+    dt = DT.get(L.kind)
+    if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8, abi.K_EWS_F32, abi.K_EWS_F64):
+        run_ew(mem, L.args, dt)
+    elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64):
+        run_dot(mem, L.args, dt)
+    elif L.kind in (abi.K_CONV_F32, abi.K_CONV_F64):
+        run_conv(mem, L.args, dt)
+    elif L.kind == abi.K_SPLIT_TF32:
+        run_split(mem, L.args)
+    elif L.kind == abi.K_DOT_TC32:
+        run_tc(mem, L.args)
+    else:
+        raise NotImplementedError(L.kind)
+
+
+def allreduce_view(mem, a):
+    dt = np.float32 if a.dtype == 0 else np.float64
+    return mem.view(a.buf, dt)[: a.count]
+
+
+def execute_ranks(lowered, inputs_per_rank: list, out_specs: list, allreduce=None) -> list:
+    """Lock-step execution of one data-parallel plan on several emulated ranks.
+
+    `allreduce(list_of_arrays)` sums in place (default: rank-order fp sum);
+    a torch.distributed-backed callable makes this a real multi-process run."""
+    mems, outs = [], []
+    for ins in inputs_per_rank:
+        o = [np.zeros(max(c, 1), dtype=d) for d, c in out_specs]
+        mems.append(Memory(lowered, [np.ascontiguousarray(x).reshape(-1) for x in ins], o))
+        outs.append(o)
+    for L in lowered.launches:
+        if L.kind == abi.K_ALLREDUCE:
+            views = [allreduce_view(m, L.args) for m in mems]
+            if allreduce is not None:
+                allreduce(views)
+            else:
+                total = views[0].copy()
+                for v in views[1:]:
+                    total = total + v
+                for v in views:
+                    v[:] = total
+            continue
+        for m in mems:
+            _run_launch(m, L)
+    return [[o[:c] for o, (_, c) in zip(os, out_specs)] for os in outs]
+
+
 def execute(lowered, inputs: list, out_specs: list) -> list:
     """inputs: storage-order numpy arrays; out_specs: (dtype, count)."""
     outputs = [np.zeros(max(c, 1), dtype=d) for d, c in out_specs]
