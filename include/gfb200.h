@@ -148,13 +148,24 @@ typedef struct {
 } gfb_conv_args;
 
 /* Split an F32 operand into TF32 hi / lo planes, K-major, rows x kp:
- * hi = rna_tf32(x), lo = rna_tf32(x - hi); src element (row, k) at
- * row * s_r + k * s_k (any strides, so transposes fold in here). */
+ * hi = rna_tf32(x), lo = rna_tf32(x - hi).  `mode` picks how (row, k)
+ * addresses the source (implicit-GEMM forms of the convolution family):
+ *   0 plain      src[row * s_r + k * s_k]
+ *   1 conv im2col  row=(n,p,q), k=(c,r,s): x[n, c, p*sh-pt+r, q*sw-pl+s]
+ *   2 dgrad gather row=(n,h,w), k=(k,r,s): delta[n, k, h+pt-r, w+pl-s]
+ *   3 digits     src[row * s_r + d0*t0 + d1*t1 + d2*t2], k=(d0,d1,d2) over e0,e1,e2
+ *   4 wgrad gather row=(c,r,s), k=(n,p,q): x[n, c, p+r-pt, q+s-pl]
+ * Out-of-range taps read as zero (the reference's zero padding). */
 typedef struct {
     const void* const* tab;
     uint64_t src, hi, lo; /* GFB_REF */
     int64_t rows, k, kp;
     int64_t s_r, s_k;
+    int32_t mode;
+    int32_t pad;
+    /* conv geometry: N, C, H, W, R, S, Ho, Wo, sh, sw, pt, pl, e0, e1, e2, unused */
+    int64_t geo[16];
+    int64_t st[4]; /* element strides of the gathered 4-D tensor, or t0, t1, t2 for mode 3 */
 } gfb_split_args;
 
 #if defined(__GNUC__) || defined(__CUDACC__)
@@ -165,7 +176,12 @@ typedef struct {
 
 /* tcgen05 Dot on split planes: C[m, n] = sum_k (Ahi*Bhi + Ahi*Blo + Alo*Bhi).
  * A planes are [M, kp_a] and B planes [N, kp_b] (both K-major); the four
- * CUtensorMap blocks are encoded by gfb_exe_create from the plane refs. */
+ * CUtensorMap blocks are encoded by gfb_exe_create from the plane refs.
+ * Output element (m, n) lives at (m / c_rdiv) * c_s_hi + (m % c_rdiv) * c_s_lo
+ * + n * c_sn when c_rdiv > 0 (rows that flatten (n, p, q) of a convolution),
+ * else at m * c_sm + n * c_sn.  With k_splits > 1, CTA z reduces the K range
+ * [z * k_per_split, +k_per_split) into C + z * split_stride (a partial to be
+ * summed by a second pass). */
 typedef struct GFB_ALIGN64 {
     const void* const* tab;
     uint64_t c;
@@ -173,7 +189,9 @@ typedef struct GFB_ALIGN64 {
     int64_t c_sm, c_sn;
     uint64_t a_hi, a_lo, b_hi, b_lo;
     int64_t kp_a, kp_b;
-    int64_t pad[3];
+    int64_t c_rdiv, c_s_hi, c_s_lo;
+    int64_t k_splits, k_per_split, split_stride;
+    int64_t pad[5];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

@@ -68,16 +68,21 @@ class SplitArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p), ("src", C.c_uint64), ("hi", C.c_uint64), ("lo", C.c_uint64),
         ("rows", C.c_int64), ("k", C.c_int64), ("kp", C.c_int64), ("s_r", C.c_int64), ("s_k", C.c_int64),
+        ("mode", C.c_int32), ("pad", C.c_int32),
+        ("geo", C.c_int64 * 16), ("st", C.c_int64 * 4),
     ]
 
 
 class TcArgs(C.Structure):
-    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 128, size 640.
+    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 192, size 704.
     _fields_ = [
         ("tab", C.c_void_p), ("c", C.c_uint64),
         ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("c_sm", C.c_int64), ("c_sn", C.c_int64),
         ("a_hi", C.c_uint64), ("a_lo", C.c_uint64), ("b_hi", C.c_uint64), ("b_lo", C.c_uint64),
-        ("kp_a", C.c_int64), ("kp_b", C.c_int64), ("pad", C.c_int64 * 3),
+        ("kp_a", C.c_int64), ("kp_b", C.c_int64),
+        ("c_rdiv", C.c_int64), ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64),
+        ("k_splits", C.c_int64), ("k_per_split", C.c_int64), ("split_stride", C.c_int64),
+        ("pad", C.c_int64 * 5),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
 

@@ -30,6 +30,7 @@ The result is a list of launch records + argument blocks (`abi.py`) that
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -117,6 +118,21 @@ INDEX_LIMIT = 1 << 31
 # tcgen05 Dot (csrc/gemm_tc.cu): 128x128 tiles, 3 stages of 64 KB + barriers.
 TC_TILE = 128
 TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
+
+
+def _conv_tc_ok(m: int, n: int, k: int) -> bool:
+    """Convolutions as implicit GEMMs go to the tensor cores when big enough."""
+    return m * n * k >= (1 << 22) and max(m, n) >= 128 and k >= 16
+
+
+def _conv_out_digits(addr: dict, m: int, ncols: int) -> list:
+    """Digits of the implicit-GEMM output map (o = row * ncols + col)."""
+    if "c_rdiv" in addr:
+        rdiv = addr["c_rdiv"]
+        digs = [(0, ncols * rdiv, None, addr["c_s_hi"]), (0, ncols, rdiv, addr["c_s_lo"]), (0, 1, ncols, addr["c_sn"])]
+    else:
+        digs = [(0, ncols, None, addr["c_sm"]), (0, 1, ncols, addr["c_sn"])]
+    return [d for d in digs if d[3] != 0]
 
 
 def use_tensor_cores(m: int, n: int, k: int) -> bool:
@@ -805,10 +821,122 @@ class Lowering:
         rec.finalize = _finalize_refs(ta, {"c": out, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
         self.launches.append(rec)
 
+    def _split(self, n, name, src, rows, kdim, mode, s_r=0, s_k=0, geo=(), st=()):
+        """hi/lo TF32 planes [rows, kp] of an implicit-GEMM operand."""
+        kp = align_up(kdim, 4)
+        hi = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
+        lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
+        self.buf[("tc", n, name, "hi")] = hi
+        self.buf[("tc", n, name, "lo")] = lo
+        sa = abi.SplitArgs(rows=rows, k=kdim, kp=kp, s_r=s_r, s_k=s_k, mode=mode)
+        sa.geo[:len(geo)] = list(geo)
+        sa.st[:len(st)] = list(st)
+        rec = LaunchRec(abi.K_SPLIT_TF32, ((kp + 31) // 32, (rows + 31) // 32, 1), (256, 1, 1), 0, sa,
+                        [src.key], [hi.key, lo.key], f"split_{name}#{n}")
+        rec.algo_bytes = rows * kdim * 4 + 2 * rows * kp * 4
+        rec.finalize = _finalize_refs(sa, {"src": src, "hi": hi, "lo": lo})
+        self.launches.append(rec)
+        return hi, lo, kp
+
+    def _tc_gemm(self, n, a, b, out, m, ncols, kdim, addr, label):
+        """tcgen05 GEMM over split planes; split-K (+ a reduce pass) when the
+        output has too few tiles to fill the GPU for a long K."""
+        (ahi, alo, kpa), (bhi, blo, kpb) = a, b
+        tiles = ((ncols + TC_TILE - 1) // TC_TILE) * ((m + TC_TILE - 1) // TC_TILE)
+        kblocks = (kdim + 31) // 32
+        splits = 1
+        if tiles < NUM_SMS and kblocks >= 64:
+            splits = max(1, min((2 * NUM_SMS) // tiles, kblocks // 16))
+        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb)
+        target = out
+        if splits > 1:
+            per = ((kblocks + splits - 1) // splits) * 32
+            splits = (kdim + per - 1) // per
+            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
+            self.buf[("splitk", n)] = scratch
+            ta.k_splits, ta.k_per_split, ta.split_stride = splits, per, m * ncols
+            ta.c_sm, ta.c_sn = ncols, 1
+            target = scratch
+        else:
+            for k_, v_ in addr.items():
+                setattr(ta, k_, v_)
+        grid = ((ncols + TC_TILE - 1) // TC_TILE, (m + TC_TILE - 1) // TC_TILE, splits)
+        rec = LaunchRec(abi.K_DOT_TC32, grid, (192, 1, 1), TC_SMEM, ta,
+                        [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.finalize = _finalize_refs(ta, {"c": target, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
+        self.launches.append(rec)
+        if splits > 1:
+            # deterministic second pass: out[o] = sum over splits of scratch[z, o]
+            p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
+            p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+            self._col_launch(p2, m * ncols, splits, 1, label + ":splitk", ElementType.F32)
+        return rec
+
+    def emit_conv_tc(self, n) -> bool:
+        """Conv2D / ConvBackpropData / ConvBackpropFilter as implicit GEMMs on
+        the tensor cores; returns False when the shape or layout does not fit
+        (the exact-order SIMT kernel then runs)."""
+        node = self.nodes[n]
+        if node.output.element_type is not ElementType.F32 or os.environ.get("GFB_CONV", "auto") == "simt":
+            return False
+        x, y = node.inputs[0][0], node.inputs[1][0]
+        try:
+            (xb, xs), (yb, ys) = self.operand(x), self.operand(y)
+        except _Retry:
+            raise
+        out = self.buf[n]
+        os_ = out.strides
+        pt, _, pl, _ = node.attrs["padding"]
+        xshape, yshape, oshape = self.nodes[x].output.shape, self.nodes[y].output.shape, node.output.shape
+        force = os.environ.get("GFB_CONV", "auto") == "tc"
+        if node.op is OpKind.CONV2D:
+            N, Cc, H, W = xshape
+            K, _, R, S = yshape
+            Ho, Wo = oshape[2], oshape[3]
+            sh, sw = node.attrs["strides"]
+            m, ncols, kdim = N * Ho * Wo, K, Cc * R * S
+            if os_[2] != Wo * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
+                return False
+            geo = (N, Cc, H, W, R, S, Ho, Wo, sh, sw, pt, pl)
+            a = self._split(n, "a", xb, m, kdim, 1, geo=geo, st=xs)
+            b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (Cc, R, S), st=ys[1:])
+            addr = {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
+        elif node.op is OpKind.CONV_BACKPROP_DATA:
+            N, K, Ho, Wo = xshape
+            _, Cc, R, S = yshape
+            H, W = oshape[2], oshape[3]
+            m, ncols, kdim = N * H * W, Cc, K * R * S
+            if os_[2] != W * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
+                return False
+            geo = (N, K, H, W, R, S, Ho, Wo, 1, 1, pt, pl)
+            a = self._split(n, "a", xb, m, kdim, 2, geo=geo, st=xs)
+            b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (K, R, S), st=(ys[0], ys[2], ys[3]))
+            addr = {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
+        else:
+            N, Cc, H, W = xshape
+            _, K, Ho, Wo = yshape
+            R, S = oshape[2], oshape[3]
+            m, ncols, kdim = K, Cc * R * S, N * Ho * Wo
+            if os_[1] != R * S * os_[3] or os_[2] != S * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
+                return False
+            a = self._split(n, "a", yb, m, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
+            geo = (N, Cc, H, W, R, S, Ho, Wo, 1, 1, pt, pl)
+            b = self._split(n, "b", xb, ncols, kdim, 4, geo=geo, st=xs)
+            addr = {"c_sm": os_[0], "c_sn": os_[3]}
+        rec = self._tc_gemm(n, a, b, out, m, ncols, kdim, addr, f"{node.op.wire_name}_tc#{n}")
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        return True
+
     def emit_heavy(self, n: int):
         node = self.nodes[n]
         out = self.buf[n]
         et = node.output.element_type
+        if node.op is not OpKind.DOT and self.emit_conv_tc(n):
+            return
         if node.op is OpKind.DOT:
             (ab, ast), (bb, bst) = self.operand(node.inputs[0][0]), self.operand(node.inputs[1][0])
             m, k = self.nodes[node.inputs[0][0]].output.shape

@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    const int nk = (int)((p.K + BK - 1) / BK);
+    // split-K: CTA z owns K range [k_begin, k_end) (k_per_split is a multiple of BK)
+    const int64_t k_begin = p.k_splits > 1 ? (int64_t)blockIdx.z * p.k_per_split : 0;
+    const int64_t k_end = p.k_splits > 1 ? min(p.K, k_begin + p.k_per_split) : p.K;
+    const int nk = k_end > k_begin ? (int)((k_end - k_begin + BK - 1) / BK) : 0;
     const int nchunk = nk > 0 ? (nk + CHUNK_KB - 1) / CHUNK_KB : 0;
 
     if (warp == 0 && lane == 0) {
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
                 mbar_wait(&empty[s], ph ^ 1);
                 unsigned char* st = smem + s * STAGE_BYTES;
                 mbar_expect_tx(&full[s], STAGE_BYTES);
-                const int kc = kb * BK;
+                const int kc = (int)k_begin + kb * BK;
                 tma_load_2d(st + 0 * TILE_BYTES, p.tmap[0], kc, m0, &full[s]);
                 tma_load_2d(st + 1 * TILE_BYTES, p.tmap[1], kc, m0, &full[s]);
                 tma_load_2d(st + 2 * TILE_BYTES, p.tmap[2], kc, n0, &full[s]);
@@ -228,10 +231,12 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
         }
-        float* C = resolve<float>(p.tab, p.c);
+        float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
         const int row = m0 + q * 32 + lane;
         if (row < p.M) {
-            float* dst = C + (int64_t)row * p.c_sm;
+            const int64_t roff = p.c_rdiv > 0 ? (row / p.c_rdiv) * p.c_s_hi + (row % p.c_rdiv) * p.c_s_lo
+                                               : (int64_t)row * p.c_sm;
+            float* dst = C + roff;
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
                 const int col0 = n0 + c * 32;
@@ -256,6 +261,44 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
     }
 }
 
+// Source offset of plane element (row, k) for the gather modes, or -1 for a
+// zero tap (padding / out of range).  See gfb_split_args in gfb200.h.
+__device__ __forceinline__ int64_t gather_offset(const gfb_split_args& p, int64_t row, int64_t k) {
+    const int64_t* g = p.geo;
+    switch (p.mode) {
+        case 1: {  // conv im2col: row=(n,p,q), k=(c,r,s)
+            const int64_t HoWo = g[6] * g[7], RS = g[4] * g[5];
+            const int64_t n = row / HoWo, pq = row % HoWo, pp = pq / g[7], q = pq % g[7];
+            const int64_t c = k / RS, rs = k % RS, r = rs / g[5], s = rs % g[5];
+            const int64_t h = pp * g[8] - g[10] + r, w = q * g[9] - g[11] + s;
+            if (h < 0 || h >= g[2] || w < 0 || w >= g[3]) return -1;
+            return n * p.st[0] + c * p.st[1] + h * p.st[2] + w * p.st[3];
+        }
+        case 2: {  // dgrad: row=(n,h,w), k=(kk,r,s) -> delta[n, kk, h+pt-r, w+pl-s]
+            const int64_t HW = g[2] * g[3], RS = g[4] * g[5];
+            const int64_t n = row / HW, hw = row % HW, h = hw / g[3], w = hw % g[3];
+            const int64_t kk = k / RS, rs = k % RS, r = rs / g[5], s = rs % g[5];
+            const int64_t pp = h + g[10] - r, q = w + g[11] - s;
+            if (pp < 0 || pp >= g[6] || q < 0 || q >= g[7]) return -1;
+            return n * p.st[0] + kk * p.st[1] + pp * p.st[2] + q * p.st[3];
+        }
+        case 3: {  // digits: k = (d0, d1, d2) over extents e0, e1, e2
+            const int64_t d2 = k % g[14], d01 = k / g[14], d1 = d01 % g[13], d0 = d01 / g[13];
+            return row * p.s_r + d0 * p.st[0] + d1 * p.st[1] + d2 * p.st[2];
+        }
+        case 4: {  // wgrad: row=(c,r,s), k=(n,p,q) -> x[n, c, p+r-pt, q+s-pl]
+            const int64_t RS = g[4] * g[5], HoWo = g[6] * g[7];
+            const int64_t c = row / RS, rs = row % RS, r = rs / g[5], s = rs % g[5];
+            const int64_t n = k / HoWo, pq = k % HoWo, pp = pq / g[7], q = pq % g[7];
+            const int64_t h = pp + r - g[10], w = q + s - g[11];
+            if (h < 0 || h >= g[2] || w < 0 || w >= g[3]) return -1;
+            return n * p.st[0] + c * p.st[1] + h * p.st[2] + w * p.st[3];
+        }
+        default:
+            return row * p.s_r + k * p.s_k;
+    }
+}
+
 // hi/lo TF32 planes, K-major [rows, kp], zero-padded past k.  32x32 tiles
 // through shared memory so both the strided read and the plane writes are
 // coalesced whichever axis of the source is contiguous.
@@ -266,13 +309,18 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
     float* lo = resolve<float>(p.tab, p.lo);
     const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const bool k_fast = p.s_k <= p.s_r;
+    const bool k_fast = p.mode != 0 || p.s_k <= p.s_r;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         int rr, kk;
         if (k_fast) { rr = ty + 8 * i; kk = tx; } else { rr = tx; kk = ty + 8 * i; }
         const int64_t r = r0 + rr, k = k0 + kk;
-        tile[rr][kk] = (r < p.rows && k < p.k) ? src[r * p.s_r + k * p.s_k] : 0.0f;
+        float v = 0.0f;
+        if (r < p.rows && k < p.k) {
+            const int64_t off = gather_offset(p, r, k);
+            if (off >= 0) v = src[off];
+        }
+        tile[rr][kk] = v;
     }
     __syncthreads();
 #pragma unroll

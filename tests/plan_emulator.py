@@ -239,11 +239,52 @@ def _rna_tf32(x: np.ndarray) -> np.ndarray:
     return np.where(fin, r.view(np.float32), x.astype(np.float32))
 
 
+def _gather_offsets(a, r, k):
+    g, st = list(a.geo), list(a.st)
+    valid = np.ones(np.broadcast(r, k).shape, dtype=bool)
+    if a.mode == 1:
+        HoWo, RS = g[6] * g[7], g[4] * g[5]
+        n, pq = r // HoWo, r % HoWo
+        pp, q = pq // g[7], pq % g[7]
+        c, rs = k // RS, k % RS
+        rr, ss = rs // g[5], rs % g[5]
+        h, w = pp * g[8] - g[10] + rr, q * g[9] - g[11] + ss
+        valid = (h >= 0) & (h < g[2]) & (w >= 0) & (w < g[3])
+        off = n * st[0] + c * st[1] + h * st[2] + w * st[3]
+    elif a.mode == 2:
+        HW, RS = g[2] * g[3], g[4] * g[5]
+        n, hw = r // HW, r % HW
+        h, w = hw // g[3], hw % g[3]
+        kk, rs = k // RS, k % RS
+        rr, ss = rs // g[5], rs % g[5]
+        pp, q = h + g[10] - rr, w + g[11] - ss
+        valid = (pp >= 0) & (pp < g[6]) & (q >= 0) & (q < g[7])
+        off = n * st[0] + kk * st[1] + pp * st[2] + q * st[3]
+    elif a.mode == 3:
+        d2, d01 = k % g[14], k // g[14]
+        d1, d0 = d01 % g[13], d01 // g[13]
+        off = r * a.s_r + d0 * st[0] + d1 * st[1] + d2 * st[2]
+    elif a.mode == 4:
+        RS, HoWo = g[4] * g[5], g[6] * g[7]
+        c, rs = r // RS, r % RS
+        rr, ss = rs // g[5], rs % g[5]
+        n, pq = k // HoWo, k % HoWo
+        pp, q = pq // g[7], pq % g[7]
+        h, w = pp + rr - g[10], q + ss - g[11]
+        valid = (h >= 0) & (h < g[2]) & (w >= 0) & (w < g[3])
+        off = n * st[0] + c * st[1] + h * st[2] + w * st[3]
+    else:
+        off = r * a.s_r + k * a.s_k
+    return np.where(valid, off, -1)
+
+
 def run_split(mem, a):
     src = mem.view(a.src, np.float32)
-    r = np.arange(a.rows)[:, None]
-    k = np.arange(a.kp)[None, :]
-    x = np.where(k < a.k, src[np.minimum(r * a.s_r + np.minimum(k, max(a.k - 1, 0)) * a.s_k, src.size - 1)], 0.0).astype(np.float32)
+    r = np.arange(a.rows, dtype=np.int64)[:, None]
+    k = np.arange(a.kp, dtype=np.int64)[None, :]
+    off = _gather_offsets(a, r, np.minimum(k, max(a.k - 1, 0)))
+    ok = (k < a.k) & (off >= 0)
+    x = np.where(ok, src[np.clip(off, 0, src.size - 1)], 0.0).astype(np.float32)
     hi = _rna_tf32(x)
     lo = _rna_tf32((x - hi).astype(np.float32))
     mem.view(a.hi, np.float32)[: a.rows * a.kp] = hi.reshape(-1)
@@ -251,14 +292,25 @@ def run_split(mem, a):
 
 
 def run_tc(mem, a):
-    ahi = mem.view(a.a_hi, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64)
-    alo = mem.view(a.a_lo, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64)
-    bhi = mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64)
-    blo = mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64)
-    c = (ahi @ bhi.T + ahi @ blo.T + alo @ bhi.T).astype(np.float32)
-    i = np.arange(a.M)[:, None]
-    j = np.arange(a.N)[None, :]
-    mem.view(a.c, np.float32)[i * a.c_sm + j * a.c_sn] = c
+    A = (mem.view(a.a_hi, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64),
+         mem.view(a.a_lo, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64))
+    B = (mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64),
+         mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64))
+    splits = max(1, a.k_splits)
+    i = np.arange(a.M, dtype=np.int64)[:, None]
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    C = mem.view(a.c, np.float32)
+    for z in range(splits):
+        k0 = z * a.k_per_split if splits > 1 else 0
+        k1 = min(a.K, k0 + a.k_per_split) if splits > 1 else a.K
+        sl = slice(k0, k1)
+        c = (A[0][:, sl] @ B[0][:, sl].T + A[0][:, sl] @ B[1][:, sl].T + A[1][:, sl] @ B[0][:, sl].T).astype(np.float32)
+        base = z * a.split_stride if splits > 1 else 0
+        if a.c_rdiv > 0:
+            off = (i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn
+        else:
+            off = i * a.c_sm + j * a.c_sn
+        C[base + off] = c
 
 
 def _run_launch(mem, L):

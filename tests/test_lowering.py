@@ -107,3 +107,50 @@ def test_chunkwise_reduction_emulated(shape, axes):
     want = interp.run_function(fn, [v])
     assert G.normwise(outs[0], want[0]) <= 1e-5  # reduction order differs from the reference
     assert G.same_bits(outs[1], want[1])
+
+
+def _conv_graph(op, N, C, K, H, W, R, S, stride=(1, 1), pad=(1, 1, 1, 1)):
+    import paper_1801_08058_b200 as gf
+
+    Ko, F32 = gf.OpKind, gf.ElementType.F32
+    fn = gf.Function("conv")
+    x = fn.add_parameter(F32, (N, C, H, W))
+    f = fn.add_parameter(F32, (K, C, R, S))
+    c = fn.add_node(Ko.CONV2D, [x, f], {"strides": stride, "padding": pad})
+    if op == "fwd":
+        fn.set_results([c])
+        return fn
+    d = fn.add_parameter(F32, fn.nodes[c].output.shape)
+    if op == "dgrad":
+        fn.set_results([fn.add_node(Ko.CONV_BACKPROP_DATA, [d, f], {"data_shape": (N, C, H, W), "padding": pad}, allow_internal=True)])
+    else:
+        fn.set_results([fn.add_node(Ko.CONV_BACKPROP_FILTER, [x, d], {"filter_shape": (K, C, R, S), "padding": pad}, allow_internal=True)])
+    return fn
+
+
+@pytest.mark.parametrize("op,shape,stride,pad,layout", [
+    ("fwd", (2, 3, 8, 9, 10, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
+    ("fwd", (2, 3, 9, 9, 10, 3, 2), (2, 1), (0, 1, 1, 0), "identity"),
+    ("fwd", (2, 3, 8, 9, 10, 3, 3), (1, 1), (1, 1, 1, 1), "nhwc"),
+    ("dgrad", (2, 5, 6, 7, 9, 3, 3), (1, 1), (1, 0, 0, 1), "identity"),
+    ("wgrad", (2, 4, 6, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
+])
+def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad, layout):
+    """Implicit-GEMM convolutions (gather-split planes + 3xTF32 GEMM, split-K
+    for the weight gradient), emulated, within 1e-5 normwise of the oracle."""
+    import paper_1801_08058_b200 as gf
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, K, H, W, R, S = shape
+    fn = _conv_graph(op, N, C, K, H, W, R, S, stride, pad)
+    h = host_compile(fn, optimize=False, conv_layout=layout) if op == "fwd" else host_compile(fn, optimize=False)
+    labels = [L.label for L in h.lowered.launches]
+    assert any("_tc#" in l for l in labels), labels
+    if op == "wgrad":
+        assert any(":splitk" in l for l in labels), labels
+    rng = np.random.default_rng(5)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = emulate(h, tens)[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
