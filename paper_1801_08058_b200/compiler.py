@@ -121,8 +121,9 @@ TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
 
 
 def _conv_tc_ok(m: int, n: int, k: int) -> bool:
-    """Convolutions as implicit GEMMs go to the tensor cores when big enough."""
-    return m * n * k >= (1 << 22) and max(m, n) >= 128 and k >= 16
+    """Convolutions as implicit GEMMs go to the tensor cores when big enough
+    (skinny outputs with a deep K run split-K)."""
+    return m * n * k >= (1 << 22) and (max(m, n) >= 128 or k >= 4096) and k >= 16
 
 
 def _conv_out_digits(addr: dict, m: int, ncols: int) -> list:
@@ -146,7 +147,9 @@ def use_tensor_cores(m: int, n: int, k: int) -> bool:
         return False
     if mode == "tc":
         return m >= 1 and n >= 1 and k >= 1
-    return m >= 64 and n >= 64 and k >= 64 and m * n * k >= (1 << 22)
+    if m * n * k < (1 << 22):
+        return False
+    return (m >= 64 and n >= 64 and k >= 64) or k >= 4096  # deep, skinny: split-K
 
 
 def magic_u31(d: int) -> tuple[int, int]:
@@ -795,31 +798,13 @@ class Lowering:
 
     def emit_dot_tc(self, n, a_op, b_op, out, m, nn, k):
         """Split both operands into K-major TF32 hi/lo planes, then one
-        tcgen05 3xTF32 GEMM (csrc/gemm_tc.cu)."""
-        kp = align_up(k, 4)
-        planes = {}
-        for name, (buf, st), rows, s_r, s_k in (("a", a_op, m, a_op[1][0], a_op[1][1]),
-                                                 ("b", b_op, nn, b_op[1][1], b_op[1][0])):
-            hi = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
-            lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
-            self.buf[("tc", n, name, "hi")] = hi
-            self.buf[("tc", n, name, "lo")] = lo
-            sa = abi.SplitArgs(rows=rows, k=k, kp=kp, s_r=s_r, s_k=s_k)
-            rec = LaunchRec(abi.K_SPLIT_TF32, ((kp + 31) // 32, (rows + 31) // 32, 1), (256, 1, 1), 0, sa,
-                            [buf.key], [hi.key, lo.key], f"split_{name}#{n}")
-            rec.algo_bytes = rows * k * 4 + 2 * rows * kp * 4
-            rec.finalize = _finalize_refs(sa, {"src": buf, "hi": hi, "lo": lo})
-            self.launches.append(rec)
-            planes[name] = (hi, lo)
-        ta = abi.TcArgs(M=m, N=nn, K=k, c_sm=out.strides[0], c_sn=out.strides[1], kp_a=kp, kp_b=kp)
-        grid = ((nn + TC_TILE - 1) // TC_TILE, (m + TC_TILE - 1) // TC_TILE, 1)
-        (ahi, alo), (bhi, blo) = planes["a"], planes["b"]
-        rec = LaunchRec(abi.K_DOT_TC32, grid, (192, 1, 1), TC_SMEM, ta,
-                        [ahi.key, alo.key, bhi.key, blo.key], [out.key], f"dot_tc#{n}")
-        rec.flops = 2 * m * nn * k
+        tcgen05 3xTF32 GEMM (csrc/gemm_tc.cu), split-K when the output is
+        too small to fill the GPU."""
+        (ab, ast), (bb, bst) = a_op, b_op
+        a = self._split(n, "a", ab, m, k, 0, s_r=ast[0], s_k=ast[1])
+        b = self._split(n, "b", bb, nn, k, 0, s_r=bst[1], s_k=bst[0])
+        rec = self._tc_gemm(n, a, b, out, m, nn, k, {"c_sm": out.strides[0], "c_sn": out.strides[1]}, f"dot_tc#{n}")
         rec.algo_bytes = (m * k + k * nn + m * nn) * 4
-        rec.finalize = _finalize_refs(ta, {"c": out, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
-        self.launches.append(rec)
 
     def _split(self, n, name, src, rows, kdim, mode, s_r=0, s_k=0, geo=(), st=()):
         """hi/lo TF32 planes [rows, kp] of an implicit-GEMM operand."""

@@ -66,7 +66,12 @@ def test_long_row_reductions(shape, axes):
     outs = [t.to_numpy() for t in gf.call(gf.compile_function(fn), [gf.tensor_from_flat(F32, shape, v)])]
     interp.set_threads(interp.max_threads())
     want = interp.run_function(fn, [v])
-    assert G.normwise(outs[0], want[0]) <= 1e-5
+    # A sequential fp32 sum (the reference order) of millions of terms drifts
+    # by ~1e-3; the tree-ordered device sum must be within 1e-5 of the exact
+    # sum and never less accurate than the reference order.
+    exact = np.exp(v.astype(np.float64)).sum(axis=axes)
+    assert G.normwise(outs[0], exact) <= 1e-5
+    assert G.normwise(outs[0], exact) <= G.normwise(want[0], exact) + 1e-7
     assert G.same_bits(outs[1], want[1])
 
 
