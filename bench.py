@@ -281,6 +281,41 @@ def launch_times(exe, dev_in, outs, stream, reps=3):
         sys.stderr.write(f"{t:9.3f} {100 * t / total:5.1f}% #{i:3d} {L.label:28s} grid={L.grid} {gbs:8.1f} GB/s {tfs:7.1f} TF/s\n")
 
 
+def bench_gemm(args, local):
+    """One config-E layer as a graph: Dot([8192, 4096], [4096, 4096]) on tcgen05."""
+    import torch
+
+    import paper_1801_08058_b200 as gf
+
+    torch.cuda.set_device(local)
+    m = args.batch or 8192
+    fn = gf.Function("layer")
+    a = fn.add_parameter(gf.ElementType.F32, (m, 4096))
+    w = fn.add_parameter(gf.ElementType.F32, (4096, 4096))
+    fn.set_results([fn.add_node(gf.OpKind.DOT, [a, w])])
+    exe = gf.compile_function(fn)
+    rng = np.random.default_rng(0)
+    dev = [torch.from_numpy(rng.uniform(-1, 1, size=s).astype(np.float32).reshape(-1)).cuda() for s in ((m, 4096), (4096, 4096))]
+    outs = exe.allocate_outputs()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        exe.run_device(dev, outs, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        exe.run_device(dev, outs, stream=stream.cuda_stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    if args.launch_times:
+        launch_times(exe, dev, outs, stream)
+    flops = 2 * m * 4096 * 4096
+    return {"metric": "F32 Dot TFLOP/s (config E layer, 3xTF32 tcgen05)", "value": flops / (ms * 1e-3) / 1e12,
+            "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "config": {"workload": f"G: Dot [{m},4096]x[4096,4096]", "launches": exe.num_launches}}
+
+
 def _step_for(workload, batch=None, ws=1):
     """(step graph, per-GPU batch, description); `batch` is the GLOBAL batch."""
     import paper_1801_08058_b200 as gf
@@ -376,7 +411,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "E"])
+    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "E", "G"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
     ap.add_argument("--dp", action="store_true", help="data-parallel plan even at one GPU (NCCL all-reduces)")
@@ -400,7 +435,10 @@ def main():
         print(json.dumps(line))
         return
 
-    line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_step(args, ws, rank, local)
+    if args.workload == "G":
+        line = bench_gemm(args, local)
+    else:
+        line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_step(args, ws, rank, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "B":
         value, threads, sample = cpu_reference(ROWS, COLS, 2, 1, budget_s=30.0)
         line["cpu_baseline"] = {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}
