@@ -613,11 +613,13 @@ class Lowering:
             wpr *= 2
         rpb = 8 // wpr
         if staged:
-            chunk = 32 * 2 * (16 // et.byte_size) * 2
+            chunk = 32 * 2 * (16 // et.byte_size) * 2  # csrc/ew_vm.cu StagedCfg<T, 2>
             nch = (n_r + chunk - 1) // chunk
-            smem = 8 * 2 * min(MAX_PRELOAD, max(1, sum(1 for l in prog.leaf_specs if not l.is_store))) * chunk * et.byte_size
-            per_sm = max(1, min(8, (200 * 1024) // max(smem, 1)))
-            slots = NUM_SMS * per_sm * 8  # resident warps
+            stages, wpb = 2, 8  # ring depth, warps per block (swept: scripts/sweep_staged.sh)
+            nload = min(MAX_PRELOAD, max(1, sum(1 for l in prog.leaf_specs if not l.is_store)))
+            smem = wpb * stages * nload * chunk * et.byte_size
+            per_sm = max(1, min(8, (220 * 1024) // max(smem, 1)))
+            slots = NUM_SMS * per_sm * wpb  # resident warps
             chunkwise = n_o < slots and nch > 1
             partial = None
             if chunkwise and red_kind:
@@ -626,12 +628,13 @@ class Lowering:
                 self.buf[("partial", partial.key)] = partial
                 final = prog.red_out
                 prog.red_out = LeafSpec(partial, [(0, 1, None, 1)], True, 0)
-            args = prog.args(mode=3, n_o=n_o, n_r=n_r, red_kind=red_kind, split=1 if chunkwise else 0, wpr=1)
-            smem = 8 * 2 * args.npre * chunk * et.byte_size
+            args = prog.args(mode=3, n_o=n_o, n_r=n_r, red_kind=red_kind, split=1 if chunkwise else 0, wpr=stages)
+            smem = wpb * stages * args.npre * chunk * et.byte_size
             items = n_o * nch if chunkwise else n_o
-            grid = max(1, min((items + 7) // 8, NUM_SMS * per_sm))
+            grid = max(1, min((items + wpb - 1) // wpb, NUM_SMS * per_sm))
             kind = abi.K_EWS_F32 if et is ElementType.F32 else abi.K_EWS_F64
-            self.add_launch(kind, (grid, 1, 1), (256, 1, 1), smem, args, prog, label + (":staged2" if chunkwise else ":staged"))
+            self.add_launch(kind, (grid, 1, 1), (32 * wpb, 1, 1), smem, args, prog,
+                            label + (":staged2" if chunkwise else ":staged"))
             if partial is not None:
                 p2 = Program(self, extents=(n_o, nch), vec_src=0, et=et)
                 k = p2.leaf(partial, [(0, 1, n_o), (1, 1, nch)] if n_o > 1 else [None, (1, 1, nch)])

@@ -545,35 +545,39 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
-template <typename T>
+template <typename T, int U_>
 struct StagedCfg {
     static constexpr int HV = 16 / sizeof(T);  // elements per 16-byte half
     static constexpr int V = 2 * HV;           // elements per thread per sub-vector
-    static constexpr int U = 2;                // sub-vectors per dispatch
+    static constexpr int U = U_;               // sub-vectors per dispatch
     static constexpr int CH = 32 * V * U;      // elements per warp chunk
 };
 
 // element index (within a chunk) of (u, half h, j) for `lane`
 template <typename T>
 __device__ __forceinline__ int sidx(int u, int h, int lane, int j) {
-    constexpr int HV = StagedCfg<T>::HV, V = StagedCfg<T>::V;
+    constexpr int HV = 16 / sizeof(T), V = 2 * HV;
     return u * 32 * V + h * 32 * HV + lane * HV + j;
 }
 
-template <typename T>
+// U = sub-vectors per thread per dispatch (a 512-float chunk per warp item;
+// smaller chunks measured 1.7x slower: per-item issue/wait overhead), NS =
+// depth of each warp's stage ring (2 measured best: deeper rings cost warps).
+template <typename T, int U_, int NS_>
 __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constant__ gfb_ew_args p) {
-    using Cfg = StagedCfg<T>;
+    using Cfg = StagedCfg<T, U_>;
     constexpr int HV = Cfg::HV, V = Cfg::V, U = Cfg::U, CH = Cfg::CH;
     extern __shared__ __align__(128) unsigned char dyn[];
-    __shared__ uint64_t bars[8][2];
+    constexpr int MAXST = 4;
+    __shared__ uint64_t bars[8][MAXST];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int npre = p.npre, kind = p.red_kind;
+    constexpr int NS = NS_;  // ring depth (stages per warp)
     const uint32_t n_o = p.n_o, n_r = p.n_r;
-    // per-warp stages: [2][npre][CH] elements
-    T* stage0 = reinterpret_cast<T*>(dyn) + (size_t)warp * 2 * npre * CH;
+    // per-warp stages: [NS][npre][CH] elements
+    T* stage0 = reinterpret_cast<T*>(dyn) + (size_t)warp * NS * npre * CH;
     if (lane == 0) {
-        mbar_init(&bars[warp][0], 1);
-        mbar_init(&bars[warp][1], 1);
+        for (int st = 0; st < NS; ++st) mbar_init(&bars[warp][st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
         uint32_t o, chunk;
         item_of(it, o, chunk);
         const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
-        const int st = it & 1;
+        const int st = it % NS;
         uint32_t nst = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) nst += (k < npre && cls[k] == 1);
@@ -639,14 +643,13 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
         }
     };
 
-    issue(0);
-    if (total > 1) issue(1);
-    uint32_t phase[2] = {0u, 0u};
+    for (int k = 0; k < NS && (uint32_t)k < total; ++k) issue(k);
+    uint32_t phase_bits = 0;  // bit st = parity of stage st
     T part = fold_init<T>(kind);
     T rs[4];  // row scalars
     uint32_t cur_o = 0xffffffffu;
     for (uint32_t it = 0; it < total; ++it) {
-        const int st = it & 1;
+        const int st = it % NS;
         uint32_t o, chunk;
         item_of(it, o, chunk);
         const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
@@ -660,8 +663,8 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
                     rs[k] = from_bits<T>(p.leaves[k].splat);
             }
         }
-        mbar_wait(&bars[warp][st], phase[st]);
-        phase[st] ^= 1u;
+        mbar_wait(&bars[warp][st], (phase_bits >> st) & 1u);
+        phase_bits ^= 1u << st;
         const T* sb = stage0 + (size_t)st * npre * CH;
         const bool full = len == (uint32_t)CH;
 
@@ -784,12 +787,12 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
             }
         }
         __syncwarp();
-        if (it + 2 < total) issue(it + 2);
+        if (it + NS < total) issue(it + NS);
     }
 }
 
-template __global__ void gfb_ew_staged_kernel<float>(const __grid_constant__ gfb_ew_args);
-template __global__ void gfb_ew_staged_kernel<double>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_staged_kernel<float, 2, 2>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_staged_kernel<double, 2, 2>(const __grid_constant__ gfb_ew_args);
 
 template __global__ void gfb_ew_kernel<float, 8>(const __grid_constant__ gfb_ew_args);
 template __global__ void gfb_ew_kernel<double, 4>(const __grid_constant__ gfb_ew_args);
@@ -804,8 +807,8 @@ extern "C" const void* gfb_ew_kernel_ptr(int kind) {
         case GFB_K_EW_F64: return (const void*)gfb::gfb_ew_kernel<double, 4>;
         case GFB_K_EW_I64: return (const void*)gfb::gfb_ew_kernel<long long, 4>;
         case GFB_K_EW_U8: return (const void*)gfb::gfb_ew_kernel<unsigned char, 8>;
-        case GFB_K_EWS_F32: return (const void*)gfb::gfb_ew_staged_kernel<float>;
-        case GFB_K_EWS_F64: return (const void*)gfb::gfb_ew_staged_kernel<double>;
+        case GFB_K_EWS_F32: return (const void*)gfb::gfb_ew_staged_kernel<float, 2, 2>;
+        case GFB_K_EWS_F64: return (const void*)gfb::gfb_ew_staged_kernel<double, 2, 2>;
     }
     return nullptr;
 }

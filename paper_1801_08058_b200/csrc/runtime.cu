@@ -295,7 +295,7 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
     // Opt every kernel in to the largest dynamic shared memory any of its
     // launches needs (the attribute is per function, not per launch).
     for (size_t i = 0; i < e->launches.size(); ++i) {
-        if (!e->fns[i] || e->launches[i].smem <= 48 * 1024) continue;
+        if (!e->fns[i] || e->launches[i].smem < 40 * 1024) continue;  // leave room for static smem
         uint32_t need = 0;
         for (size_t j = 0; j < e->launches.size(); ++j)
             if (e->fns[j] == e->fns[i]) need = need > e->launches[j].smem ? need : e->launches[j].smem;

@@ -162,7 +162,7 @@ def run_ew(mem, a, dt):
             for j in range(n_r):
                 red = (red.astype(np.uint64) + vals[:, j].astype(np.uint64)).astype(np.int64) if dt == np.int64 else (red + vals[:, j]).astype(dt)
     if a.mode == 3 and a.split == 1:  # chunk-wise staged: per-chunk partials
-        chunk = 32 * 2 * (16 // np.dtype(dt).itemsize) * 2
+        chunk = 32 * 2 * (16 // np.dtype(dt).itemsize) * STAGED_U
         nch = (n_r + chunk - 1) // chunk
         part = np.zeros((n_o, nch), dtype=dt)
         for c in range(nch):
@@ -311,6 +311,9 @@ def run_tc(mem, a):
         else:
             off = i * a.c_sm + j * a.c_sn
         C[base + off] = c
+
+
+STAGED_U = 2  # csrc/ew_vm.cu StagedCfg<T, 2>
 
 
 def _run_launch(mem, L):
