@@ -616,8 +616,9 @@ class Lowering:
             chunk = 32 * 2 * (16 // et.byte_size) * 2  # csrc/ew_vm.cu StagedCfg<T, 2>
             nch = (n_r + chunk - 1) // chunk
             stages, wpb = 2, 8  # ring depth, warps per block (swept: scripts/sweep_staged.sh)
-            nload = min(MAX_PRELOAD, max(1, sum(1 for l in prog.leaf_specs if not l.is_store)))
-            smem = wpb * stages * nload * chunk * et.byte_size
+            nstaged = max(1, sum(1 for l in prog.leaf_specs if not l.is_store and l.buf.splat is None
+                                 and r_linear(l.digits) == 1))
+            smem = wpb * stages * nstaged * chunk * et.byte_size
             per_sm = max(1, min(8, (220 * 1024) // max(smem, 1)))
             slots = NUM_SMS * per_sm * wpb  # resident warps
             chunkwise = n_o < slots and nch > 1
@@ -629,18 +630,22 @@ class Lowering:
                 final = prog.red_out
                 prog.red_out = LeafSpec(partial, [(0, 1, None, 1)], True, 0)
             args = prog.args(mode=3, n_o=n_o, n_r=n_r, red_kind=red_kind, split=1 if chunkwise else 0, wpr=stages)
-            smem = wpb * stages * args.npre * chunk * et.byte_size
             items = n_o * nch if chunkwise else n_o
             grid = max(1, min((items + wpb - 1) // wpb, NUM_SMS * per_sm))
             kind = abi.K_EWS_F32 if et is ElementType.F32 else abi.K_EWS_F64
             self.add_launch(kind, (grid, 1, 1), (32 * wpb, 1, 1), smem, args, prog,
                             label + (":staged2" if chunkwise else ":staged"))
             if partial is not None:
-                p2 = Program(self, extents=(n_o, nch), vec_src=0, et=et)
+                # second pass over the partials: rows again when they are long
+                row2 = nch >= 4096
+                p2 = Program(self, extents=(n_o, nch), vec_src=1 if row2 else 0, et=et)
                 k = p2.leaf(partial, [(0, 1, n_o), (1, 1, nch)] if n_o > 1 else [None, (1, 1, nch)])
                 p2.emit(I_LOAD, k=k)
-                p2.red_out = final
-                self._col_launch(p2, n_o, nch, red_kind, label + ":pass2", et)
+                p2.red_out = LeafSpec(final.buf, final.digits, True, vec_class(final.digits, 0, True, vec_width(et), et.byte_size))
+                if row2:
+                    self._row_launch(p2, n_o, nch, red_kind, label + ":pass2", et)
+                else:
+                    self._col_launch(p2, n_o, nch, red_kind, label + ":pass2", et)
             return
         grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)

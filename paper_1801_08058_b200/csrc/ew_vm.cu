@@ -574,8 +574,21 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
     const int npre = p.npre, kind = p.red_kind;
     constexpr int NS = NS_;  // ring depth (stages per warp)
     const uint32_t n_o = p.n_o, n_r = p.n_r;
-    // per-warp stages: [NS][npre][CH] elements
-    T* stage0 = reinterpret_cast<T*>(dyn) + (size_t)warp * NS * npre * CH;
+    // leaf classes (uniform): 1 = staged (r-contiguous), 2 = row scalar, 3 = splat;
+    // staged leaves get consecutive stage slots
+    int cls[4], slot[4], nst = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cls[k] = 0;
+        slot[k] = nst;
+        if (k < npre) {
+            const gfb_leaf& L = p.leaves[k];
+            cls[k] = L.mode == 1 ? 3 : (L.rlin == 1 ? 1 : 2);
+            nst += cls[k] == 1;
+        }
+    }
+    // per-warp stages: [NS][nst][CH] elements
+    T* stage0 = reinterpret_cast<T*>(dyn) + (size_t)warp * NS * nst * CH;
     if (lane == 0) {
         for (int st = 0; st < NS; ++st) mbar_init(&bars[warp][st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -607,16 +620,6 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
             chunk = it % nch;
         }
     };
-    // leaf classes (uniform): 1 = staged (r-contiguous), 2 = row scalar, 3 = splat
-    int cls[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        cls[k] = 0;
-        if (k < npre) {
-            const gfb_leaf& L = p.leaves[k];
-            cls[k] = L.mode == 1 ? 3 : (L.rlin == 1 ? 1 : 2);
-        }
-    }
     const char* lbase[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -627,9 +630,6 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
         item_of(it, o, chunk);
         const uint32_t r0 = chunk * CH, len = min((uint32_t)CH, n_r - r0);
         const int st = it % NS;
-        uint32_t nst = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) nst += (k < npre && cls[k] == 1);
         if (lane == 0) {
             fence_proxy();
             mbar_expect_tx(&bars[warp][st], len * sizeof(T) * nst);
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
             for (int k = 0; k < 4; ++k) {
                 if (k < npre && cls[k] == 1) {
                     const T* src = reinterpret_cast<const T*>(lbase[k]) + part_offset(p.leaves[k], o, 0) + r0;
-                    bulk_g2s(stage0 + ((size_t)st * npre + k) * CH, src, len * sizeof(T), &bars[warp][st]);
+                    bulk_g2s(stage0 + ((size_t)st * nst + slot[k]) * CH, src, len * sizeof(T), &bars[warp][st]);
                 }
             }
         }
@@ -665,13 +665,13 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
         }
         mbar_wait(&bars[warp][st], (phase_bits >> st) & 1u);
         phase_bits ^= 1u << st;
-        const T* sb = stage0 + (size_t)st * npre * CH;
+        const T* sb = stage0 + (size_t)st * nst * CH;
         const bool full = len == (uint32_t)CH;
 
         T acc[U][V];
         auto operand = [&](int k, int u, T(&b)[V]) {
             if (cls[k] == 1) {
-                const T* src = sb + k * CH;
+                const T* src = sb + slot[k] * CH;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int4 q = *reinterpret_cast<const int4*>(src + sidx<T>(u, h, lane, 0));
