@@ -54,6 +54,7 @@ enum {
     GFB_K_DOT_F64 = 11,
     GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot on split planes (gfb_tc_args) */
     GFB_K_SPLIT_TF32 = 13, /* F32 -> TF32 hi/lo K-major planes (gfb_split_args) */
+    GFB_K_DOT_TC32W = 14,  /* as GFB_K_DOT_TC32 with 128x256 tiles (gfb_tc_args) */
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */

@@ -115,9 +115,11 @@ VM_OP = {
 EW_KIND = {ElementType.F32: abi.K_EW_F32, ElementType.F64: abi.K_EW_F64, ElementType.I64: abi.K_EW_I64, ElementType.BOOL: abi.K_EW_U8}
 INDEX_LIMIT = 1 << 31
 
-# tcgen05 Dot (csrc/gemm_tc.cu): 128x128 tiles, 3 stages of 64 KB + barriers.
+# tcgen05 Dot (csrc/gemm_tc.cu): 128x128 tiles (3 stages of 64 KB) or, for
+# N >= 256, 128x256 tiles (2 stages of 96 KB, 320 threads).
 TC_TILE = 128
 TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
+TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
 
 
 def _conv_tc_ok(m: int, n: int, k: int) -> bool:
@@ -853,9 +855,11 @@ class Lowering:
         else:
             for k_, v_ in addr.items():
                 setattr(ta, k_, v_)
-        grid = ((ncols + TC_TILE - 1) // TC_TILE, (m + TC_TILE - 1) // TC_TILE, splits)
-        rec = LaunchRec(abi.K_DOT_TC32, grid, (192, 1, 1), TC_SMEM, ta,
-                        [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
+        wide = ncols >= 256 and os.environ.get("GFB_TC_WIDE", "1") == "1"
+        bn = 256 if wide else TC_TILE
+        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, splits)
+        rec = LaunchRec(abi.K_DOT_TC32W if wide else abi.K_DOT_TC32, grid, (320 if wide else 192, 1, 1),
+                        TC_SMEM_W if wide else TC_SMEM, ta, [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
         rec.flops = 2 * m * ncols * kdim
         rec.finalize = _finalize_refs(ta, {"c": target, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
         self.launches.append(rec)

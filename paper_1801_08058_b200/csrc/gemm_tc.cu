@@ -33,18 +33,29 @@
 namespace gfb {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
-constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB (BN == BM)
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-// The tensor core's fp32 accumulation truncates, so a 4096-deep K chain
-// drifts by ~3e-5.  Partial sums are promoted to CUDA-core fp32 registers
-// (round-to-nearest adds) every CHUNK_KB K-blocks (128 K): the MMA warp
-// cycles through NBUF TMEM accumulators while the epilogue warps drain the
-// finished ones, so the promotion overlaps the MMAs.
-constexpr int CHUNK_KB = 4;
-constexpr int NBUF = 4;
-constexpr uint32_t TMEM_COLS = BN * NBUF;  // 512: the whole TMEM of the SM
+// Tile configurations.  BN = 128: 3-stage ring of 64 KB stages, 4 epilogue
+// warps.  BN = 256: 2-stage ring of 96 KB stages, 8 epilogue warps; it moves
+// 25 % fewer operand bytes per MMA clock, which the latency-bound 3xTF32
+// pipeline needs (ncu: the 128-wide tile keeps the tensor pipe 65 % busy
+// with L2 at 47 %).
+template <int BN_>
+struct Cfg {
+    static constexpr int BM = 128, BN = BN_, BK = 32;
+    static constexpr int STAGES = BN_ == 256 ? 2 : 3;
+    static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    // The tensor core's fp32 accumulation truncates, so a 4096-deep K chain
+    // drifts by ~3e-5.  Partial sums are promoted to CUDA-core fp32
+    // registers (round-to-nearest adds) every CHUNK_KB K-blocks (128 K): the
+    // MMA warp cycles through NBUF TMEM accumulators while the epilogue warps
+    // drain finished ones, so the promotion overlaps the MMAs.
+    static constexpr int CHUNK_KB = 4;
+    static constexpr int NBUF = 512 / BN;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4 * (BN / 128);  // each owns 32 rows x 128 columns
+    static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -114,8 +125,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 }  // namespace tc
 
-__global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_constant__ gfb_tc_args p) {
+template <int BN_>
+__global__ void __launch_bounds__(tc::Cfg<BN_>::THREADS, 1) gfb_gemm_tc_kernel(const __grid_constant__ gfb_tc_args p) {
     using namespace tc;
+    using C_ = Cfg<BN_>;
+    constexpr int BM = C_::BM, BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
+    constexpr uint32_t TMEM_COLS = C_::TMEM_COLS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -139,7 +156,7 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
         }
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
+            mbar_init(&tempty[b], EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 4; ++i) prefetch_tmap(p.tmap[i]);
@@ -163,10 +180,10 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
                 unsigned char* st = smem + s * STAGE_BYTES;
                 mbar_expect_tx(&full[s], STAGE_BYTES);
                 const int kc = (int)k_begin + kb * BK;
-                tma_load_2d(st + 0 * TILE_BYTES, p.tmap[0], kc, m0, &full[s]);
-                tma_load_2d(st + 1 * TILE_BYTES, p.tmap[1], kc, m0, &full[s]);
-                tma_load_2d(st + 2 * TILE_BYTES, p.tmap[2], kc, n0, &full[s]);
-                tma_load_2d(st + 3 * TILE_BYTES, p.tmap[3], kc, n0, &full[s]);
+                tma_load_2d(st, p.tmap[0], kc, m0, &full[s]);
+                tma_load_2d(st + A_BYTES, p.tmap[1], kc, m0, &full[s]);
+                tma_load_2d(st + 2 * A_BYTES, p.tmap[2], kc, n0, &full[s]);
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, n0, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -184,8 +201,8 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
                 mbar_wait(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 unsigned char* st = smem + s * STAGE_BYTES;
-                const uint64_t ah = smem_desc(st), al = smem_desc(st + TILE_BYTES);
-                const uint64_t bh = smem_desc(st + 2 * TILE_BYTES), bl = smem_desc(st + 3 * TILE_BYTES);
+                const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
                 const uint32_t d = tmem + (uint32_t)(b * BN);
 #pragma unroll
                 for (int j = 0; j < BK / 8; ++j) {
@@ -200,20 +217,22 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
             }
         }
     } else {
-        // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows; it
-        // promotes every finished chunk into fp32 registers, then stores.
-        const int q = warp & 3;
-        float acc[BN];
+        // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows and
+        // 128 columns (group cg); it promotes every finished chunk into fp32
+        // registers, then stores.
+        constexpr int EC = 128;  // columns per epilogue warp
+        const int q = warp & 3, cg = (warp - 2) >> 2;
+        float acc[EC];
 #pragma unroll
-        for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+        for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
         for (int chunk = 0; chunk < nchunk; ++chunk) {
             const int b = chunk % NBUF;
             mbar_wait(&tfull[b], (chunk / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = 0; c < EC / 32; ++c) {
                 uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + cg * EC + c * 32);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -238,8 +257,8 @@ __global__ void __launch_bounds__(192, 1) gfb_gemm_tc_kernel(const __grid_consta
                                                : (int64_t)row * p.c_sm;
             float* dst = C + roff;
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) {
-                const int col0 = n0 + c * 32;
+            for (int c = 0; c < EC / 32; ++c) {
+                const int col0 = n0 + cg * EC + c * 32;
                 if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
@@ -341,10 +360,14 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
 
 }  // namespace gfb
 
+template __global__ void gfb::gfb_gemm_tc_kernel<128>(const __grid_constant__ gfb_tc_args);
+template __global__ void gfb::gfb_gemm_tc_kernel<256>(const __grid_constant__ gfb_tc_args);
+
 extern "C" const void* gfb_tc_kernel_ptr(int kind) {
-    if (kind == GFB_K_DOT_TC32) return (const void*)gfb::gfb_gemm_tc_kernel;
+    if (kind == GFB_K_DOT_TC32) return (const void*)gfb::gfb_gemm_tc_kernel<128>;
+    if (kind == GFB_K_DOT_TC32W) return (const void*)gfb::gfb_gemm_tc_kernel<256>;
     if (kind == GFB_K_SPLIT_TF32) return (const void*)gfb::gfb_split_kernel;
     return nullptr;
 }
 
-extern "C" int gfb_tc_smem_bytes(void) { return gfb::tc::SMEM_BYTES; }
+extern "C" int gfb_tc_smem_bytes(int wide) { return wide ? gfb::tc::Cfg<256>::SMEM_BYTES : gfb::tc::Cfg<128>::SMEM_BYTES; }

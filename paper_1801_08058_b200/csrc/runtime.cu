@@ -43,14 +43,14 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// K-major fp32 plane [rows, kp] -> 128B-swizzled boxes of 32 (K) x 128 (rows).
-bool encode_plane_map(void* gaddr, int64_t rows, int64_t kp, void* out) {
+// K-major fp32 plane [rows, kp] -> 128B-swizzled boxes of 32 (K) x box_rows.
+bool encode_plane_map(void* gaddr, int64_t rows, int64_t kp, uint32_t box_rows, void* out) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     alignas(64) CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
-    cuuint32_t box[2] = {32, 128};
+    cuuint32_t box[2] = {32, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, gaddr, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -152,7 +152,7 @@ const void* kernel_for(uint32_t kind) {
     if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EWS_F64) return gfb_ew_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64)
         return gfb_simt_kernel_ptr((int)kind);
-    if (kind == GFB_K_DOT_TC32 || kind == GFB_K_SPLIT_TF32) return gfb_tc_kernel_ptr((int)kind);
+    if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_SPLIT_TF32) return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
 }
 
@@ -278,7 +278,7 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
         }
         e->fns[i] = kernel_for(L.kind);
         if (!e->fns[i]) return bail(fail(GFB_ERR_INVALID, "unknown kernel kind " + std::to_string(L.kind)));
-        if (L.kind == GFB_K_DOT_TC32) {
+        if (L.kind == GFB_K_DOT_TC32 || L.kind == GFB_K_DOT_TC32W) {
             // Tensor maps need fixed addresses: the split planes live in the arena.
             gfb_tc_args* a = (gfb_tc_args*)(e->args.data() + L.arg_offset);
             const uint64_t refs[4] = {a->a_hi, a->a_lo, a->b_hi, a->b_lo};
@@ -287,7 +287,8 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                     return bail(fail(GFB_ERR_INVALID, "tensor-core operand planes must live in the arena"));
                 void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
                 const int64_t rows = t < 2 ? a->M : a->N, kp = t < 2 ? a->kp_a : a->kp_b;
-                if (!encode_plane_map(addr, rows, kp, a->tmap[t]))
+                const uint32_t box_rows = (t >= 2 && L.kind == GFB_K_DOT_TC32W) ? 256 : 128;
+                if (!encode_plane_map(addr, rows, kp, box_rows, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
             }
         }

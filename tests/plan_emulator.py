@@ -326,7 +326,7 @@ def _run_launch(mem, L):
         run_conv(mem, L.args, dt)
     elif L.kind == abi.K_SPLIT_TF32:
         run_split(mem, L.args)
-    elif L.kind == abi.K_DOT_TC32:
+    elif L.kind in (abi.K_DOT_TC32, abi.K_DOT_TC32W):
         run_tc(mem, L.args)
     else:
         raise NotImplementedError(L.kind)
