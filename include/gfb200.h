@@ -156,6 +156,7 @@ typedef struct {
  *   2 dgrad gather row=(n,h,w), k=(k,r,s): delta[n, k, h+pt-r, w+pl-s]
  *   3 digits     src[row * s_r + d0*t0 + d1*t1 + d2*t2], k=(d0,d1,d2) over e0,e1,e2
  *   4 wgrad gather row=(c,r,s), k=(n,p,q): x[n, c, p+r-pt, q+s-pl]
+ *   5 streaming  as 0 with s_k == 1, k == kp (128-bit grid-stride pass)
  * Out-of-range taps read as zero (the reference's zero padding). */
 typedef struct {
     const void* const* tab;

@@ -823,11 +823,14 @@ class Lowering:
         lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
         self.buf[("tc", n, name, "hi")] = hi
         self.buf[("tc", n, name, "lo")] = lo
+        if mode == 0 and s_k == 1 and kdim == kp and s_r % 4 == 0 and src.splat is None:
+            mode = 5  # streaming, 128-bit
         sa = abi.SplitArgs(rows=rows, k=kdim, kp=kp, s_r=s_r, s_k=s_k, mode=mode)
         sa.geo[:len(geo)] = list(geo)
         sa.st[:len(st)] = list(st)
-        rec = LaunchRec(abi.K_SPLIT_TF32, ((kp + 31) // 32, (rows + 31) // 32, 1), (256, 1, 1), 0, sa,
-                        [src.key], [hi.key, lo.key], f"split_{name}#{n}")
+        grid = (max(1, min((rows * kp // 4 + 255) // 256, NUM_SMS * 16)), 1, 1) if mode == 5 else \
+               ((kp + 31) // 32, (rows + 31) // 32, 1)
+        rec = LaunchRec(abi.K_SPLIT_TF32, grid, (256, 1, 1), 0, sa, [src.key], [hi.key, lo.key], f"split_{name}#{n}")
         rec.algo_bytes = rows * kdim * 4 + 2 * rows * kp * 4
         rec.finalize = _finalize_refs(sa, {"src": src, "hi": hi, "lo": lo})
         self.launches.append(rec)

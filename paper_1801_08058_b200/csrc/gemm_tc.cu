@@ -321,11 +321,38 @@ __device__ __forceinline__ int64_t gather_offset(const gfb_split_args& p, int64_
 // hi/lo TF32 planes, K-major [rows, kp], zero-padded past k.  32x32 tiles
 // through shared memory so both the strided read and the plane writes are
 // coalesced whichever axis of the source is contiguous.
+__device__ __forceinline__ void split_tf32(float x, float& h, float& l) {
+    uint32_t hb, lb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+    const float rest = __fsub_rn(x, __uint_as_float(hb));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(rest));
+    h = __uint_as_float(hb);
+    l = __uint_as_float(lb);
+}
+
 __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ gfb_split_args p) {
     __shared__ float tile[32][33];
     const float* src = resolve<const float>(p.tab, p.src);
     float* hi = resolve<float>(p.tab, p.hi);
     float* lo = resolve<float>(p.tab, p.lo);
+    if (p.mode == 5) {
+        // Row-contiguous source (s_k == 1, k == kp, 16-byte aligned rows): a
+        // streaming pass with 128-bit loads and stores.
+        const int64_t n4 = p.rows * p.kp / 4;
+        const int64_t k4 = p.kp / 4;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t r = i / k4, c = (i % k4) * 4;
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src + r * p.s_r + c));
+            float4 h, l;
+            split_tf32(x.x, h.x, l.x);
+            split_tf32(x.y, h.y, l.y);
+            split_tf32(x.z, h.z, l.z);
+            split_tf32(x.w, h.w, l.w);
+            reinterpret_cast<float4*>(hi)[i] = h;
+            reinterpret_cast<float4*>(lo)[i] = l;
+        }
+        return;
+    }
     const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const bool k_fast = p.mode != 0 || p.s_k <= p.s_r;
