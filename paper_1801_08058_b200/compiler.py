@@ -618,9 +618,11 @@ class Lowering:
             chunk = 32 * 2 * (16 // et.byte_size) * 2  # csrc/ew_vm.cu StagedCfg<T, 2>
             nch = (n_r + chunk - 1) // chunk
             stages, wpb = 2, 8  # ring depth, warps per block (swept: scripts/sweep_staged.sh)
-            nstaged = max(1, sum(1 for l in prog.leaf_specs if not l.is_store and l.buf.splat is None
-                                 and r_linear(l.digits) == 1))
-            smem = wpb * stages * nstaged * chunk * et.byte_size
+            n_r_pad = nch * chunk
+            lin = [l for l in prog.leaf_specs if not l.is_store and l.buf.splat is None and r_linear(l.digits) == 1]
+            resident = [l for l in lin if all(d[0] == 1 for d in l.digits) and n_r_pad * et.byte_size <= 8192]
+            nstaged = max(1, len(lin) - len(resident))
+            smem = len(resident) * n_r_pad * et.byte_size + wpb * stages * nstaged * chunk * et.byte_size
             per_sm = max(1, min(8, (220 * 1024) // max(smem, 1)))
             slots = NUM_SMS * per_sm * wpb  # resident warps
             chunkwise = n_o < slots and nch > 1

@@ -545,6 +545,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+constexpr uint32_t kResidentBytes = 8192;  // block-resident leaf budget (per leaf)
+
 template <typename T, int U_>
 struct StagedCfg {
     static constexpr int HV = 16 / sizeof(T);  // elements per 16-byte half
@@ -574,26 +576,50 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
     const int npre = p.npre, kind = p.red_kind;
     constexpr int NS = NS_;  // ring depth (stages per warp)
     const uint32_t n_o = p.n_o, n_r = p.n_r;
-    // leaf classes (uniform): 1 = staged (r-contiguous), 2 = row scalar, 3 = splat;
-    // staged leaves get consecutive stage slots
-    int cls[4], slot[4], nst = 0;
+    // leaf classes (uniform): 1 = staged per item (r-contiguous), 2 = row
+    // scalar, 3 = splat, 4 = block-resident (r-contiguous, independent of
+    // o, e.g. a row Broadcast of a bias: copied into shared memory once per
+    // block instead of once per item).  Staged / resident leaves get
+    // consecutive slots in their regions.
+    const uint32_t n_r_pad = (n_r + CH - 1) / CH * CH;
+    int cls[4], slot[4], nst = 0, nres = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         cls[k] = 0;
-        slot[k] = nst;
+        slot[k] = 0;
         if (k < npre) {
             const gfb_leaf& L = p.leaves[k];
             cls[k] = L.mode == 1 ? 3 : (L.rlin == 1 ? 1 : 2);
-            nst += cls[k] == 1;
+            if (cls[k] == 1) {
+                bool o_free = true;
+                for (int i = 0; i < L.ndig; ++i) o_free &= L.dig[i].src == 1;
+                if (o_free && n_r_pad * sizeof(T) <= kResidentBytes) cls[k] = 4;
+            }
+            if (cls[k] == 1) slot[k] = nst++;
+            if (cls[k] == 4) slot[k] = nres++;
         }
     }
-    // per-warp stages: [NS][nst][CH] elements
-    T* stage0 = reinterpret_cast<T*>(dyn) + (size_t)warp * NS * nst * CH;
+    // dynamic smem: [resident: nres x n_r_pad][per-warp stages: NS x nst x CH]
+    T* res0 = reinterpret_cast<T*>(dyn);
+    T* stage0 = res0 + (size_t)nres * n_r_pad + (size_t)warp * NS * nst * CH;
+    __shared__ uint64_t rbar;
     if (lane == 0) {
         for (int st = 0; st < NS; ++st) mbar_init(&bars[warp][st], 1);
+        if (warp == 0) mbar_init(&rbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
+    __syncthreads();
+    if (threadIdx.x == 0 && nres) {
+        mbar_expect_tx(&rbar, (uint32_t)(nres * n_r * sizeof(T)));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < npre && cls[k] == 4) {
+                const gfb_leaf& L = p.leaves[k];
+                bulk_g2s(res0 + (size_t)slot[k] * n_r_pad,
+                         reinterpret_cast<const char*>(p.tab[L.ref >> 56]) + (L.ref & kOffsetMask),
+                         (uint32_t)(n_r * sizeof(T)), &rbar);
+            }
+    }
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, tw = gridDim.x * (blockDim.x >> 5);
     const uint32_t nch = (n_r + CH - 1) / CH;
     // Work items are (o, chunk).  Row-wise (split == 0): a warp owns whole
@@ -644,6 +670,7 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
     };
 
     for (int k = 0; k < NS && (uint32_t)k < total; ++k) issue(k);
+    if (nres) mbar_wait(&rbar, 0);
     uint32_t phase_bits = 0;  // bit st = parity of stage st
     T part = fold_init<T>(kind);
     T rs[4];  // row scalars
@@ -670,8 +697,8 @@ __global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constan
 
         T acc[U][V];
         auto operand = [&](int k, int u, T(&b)[V]) {
-            if (cls[k] == 1) {
-                const T* src = sb + slot[k] * CH;
+            if (cls[k] == 1 || cls[k] == 4) {
+                const T* src = cls[k] == 1 ? sb + slot[k] * CH : res0 + (size_t)slot[k] * n_r_pad + r0;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int4 q = *reinterpret_cast<const int4*>(src + sidx<T>(u, h, lane, 0));
