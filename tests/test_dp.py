@@ -109,3 +109,31 @@ def test_two_process_gloo_allreduce():
         p.join(timeout=120)
     results = sorted(q.get(timeout=5) for _ in procs)
     assert results == [(0, True), (1, True)]
+
+
+def test_rebatch_chunk_graph_equals_row_slices():
+    """streaming.rebatch: the chunk graph computes exactly the rows of the full graph."""
+    from hostcompile import emulate
+
+    from paper_1801_08058_b200.streaming import rebatch
+
+    fn = W.fused_chain(gf, rows=64, cols=256)
+    sub = rebatch(fn, fn.parameters[:2], 4)
+    assert [sub.nodes[p].output.shape for p in sub.parameters] == [(16, 256), (16, 256), (256,)]
+    arrays = W.chain_inputs(64, 256)
+    h = host_compile(sub)
+    full = interp.run_function(fn, arrays)
+    for i in range(4):
+        part = [arrays[0][16 * i:16 * (i + 1)], arrays[1][16 * i:16 * (i + 1)], arrays[2]]
+        outs = emulate(h, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in part])
+        assert G.same_bits(outs[0], full[0][16 * i:16 * (i + 1)])
+        assert G.normwise(outs[1], full[1][16 * i:16 * (i + 1)]) <= 1e-6
+
+
+def test_rebatch_rejects_batch_reductions():
+    from paper_1801_08058_b200.errors import UnsupportedOp
+    from paper_1801_08058_b200.streaming import rebatch
+
+    step = W.mlp_step(gf, batch=8, in_dim=4, hidden=(4,), out_dim=3)
+    with pytest.raises(UnsupportedOp):
+        rebatch(step.fn, [step.fn.parameters[0]], 2)

@@ -89,3 +89,22 @@ def test_data_parallel_plan_single_rank_nccl():
     plain = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
     for a, b in zip(got, plain):
         assert G.same_bits(a, b)
+
+
+def test_call_streamed_equals_call():
+    from paper_1801_08058_b200.runtime import pinned_tensor
+    from paper_1801_08058_b200.streaming import call_streamed
+
+    fn = W.fused_chain(gf, rows=4096, cols=1024)
+    arrays = W.chain_inputs(4096, 1024)
+    exe = gf.compile_function(fn)
+    host = []
+    for a in arrays:
+        t = pinned_tensor(gf.ElementType.F32, a.shape)
+        t.buffer[:] = a.reshape(-1)
+        host.append(t)
+    out = [pinned_tensor(d.element_type, d.shape) for d, _ in exe.result_signature]
+    call_streamed(exe, host, out, chunks=8)
+    ref = [t.to_numpy() for t in gf.call(exe, host)]
+    assert G.same_bits(out[0].to_numpy(), ref[0])
+    assert G.normwise(out[1].to_numpy(), ref[1]) <= 1e-6
