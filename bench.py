@@ -53,54 +53,86 @@ def chain_bytes(rows, cols, esize=4):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled while the GPU is busy."""
+    """SM clocks and throttle reasons sampled during the timed region.
 
-    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    NVML (nvidia_ml_py) is polled from a thread every 2 ms, so even a 30 ms
+    timed region yields samples; nvidia-smi at 100 ms is the fallback."""
+
+    REASONS = {  # nvmlClocksEventReason bits
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
+    }
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], None, set()
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._drain, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for name, bit in self.REASONS.items():
+                            if bits & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            self.mode = "nvml"
+        except Exception:
+            self.mode = "nvidia-smi"
+            self._start_smi()
+        return self
+
+    def _start_smi(self):
+        fields = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={fields}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+            def drain():
+                for line in self.proc.stdout:
+                    parts = [x.strip() for x in line.split(",")]
+                    try:
+                        self.sm.append(float(parts[0]))
+                        self.mx = float(parts[1])
+                    except (ValueError, IndexError):
+                        continue
+                    for name, v in zip(["hw_slowdown", "sw_thermal_slowdown", "hw_thermal_slowdown", "sw_power_cap"], parts[2:6]):
+                        if v.lower() == "active":
+                            self.reasons.add(name)
+
+            self.thread = threading.Thread(target=drain, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
-        return self
-
-    def _drain(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def __exit__(self, *exc):
-        if self.proc:
+        self._stop.set()
+        if self.mode == "nvidia-smi" and getattr(self, "proc", None):
             self.proc.terminate()
             self.proc.wait(timeout=5)
+        elif getattr(self, "thread", None):
+            self.thread.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
-        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = list(self.sm)
+        loaded = [x for x in sm if self.mx and x > 0.5 * self.mx] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": self.mode}
 
 
 def dist_setup():
