@@ -369,6 +369,10 @@ def _step_for(workload, batch=None, ws=1):
         g = batch or 256
         return (W.cnn_step(gf, batch=g // ws, loss_batch=g), g // ws,
                 "C: CNN 32x32x3, conv 3->16->32, maxpool, fc 8192->10")
+    if workload == "D":
+        g = batch or 128 * ws  # config D is weak-scaled: 128 images per GPU
+        return (W.resnet_step(gf, batch=g // ws, loss_batch=g), g // ws,
+                "D: ResNet-18-style 224x224, NHWC layout assignment")
     if workload == "E":
         g = batch or 65536
         return (W.mlp_step(gf, batch=g // ws, in_dim=4096, hidden=(4096,) * 7, out_dim=4096, loss_batch=g), g // ws,
@@ -399,7 +403,7 @@ def bench_step(args, ws, rank, local):
     if ws > 1 or args.dp:
         names = step.param_names
         dp = gf.DataParallel([step.fn.parameters[names.index("x")], step.fn.parameters[names.index("t")]], world_size=ws)
-    exe = gf.compile_function(step.fn, data_parallel=dp)
+    exe = gf.compile_function(step.fn, data_parallel=dp, conv_layout="nhwc" if args.workload == "D" else "identity")
     t_compile = time.perf_counter() - t_compile
     shapes = W.parameter_shapes(step)
     arrays = W.step_inputs(step, shapes, seed=rank)
@@ -435,7 +439,8 @@ def bench_step(args, ws, rank, local):
     return {
         "metric": f"training-step samples/sec (config {desc}, global batch {gbatch}, fwd+autodiff bwd+SGD)",
         "value": gbatch / (ms * 1e-3), "unit": "samples/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if args.workload == "D" else "strong",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": desc, "global_batch": gbatch, "batch_per_gpu": batch,
                                         "parallelism": f"dp{ws}", "launches": exe.num_launches,
                                         "allreduces": len(getattr(exe, "allreduce", ()) or ()),
@@ -452,7 +457,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "E", "G"])
+    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "D", "E", "G"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
     ap.add_argument("--dp", action="store_true", help="data-parallel plan even at one GPU (NCCL all-reduces)")

@@ -13,6 +13,7 @@ Configs (BASELINE.json `configs`):
   A  MLP 784-512-10, batch 128                       `mlp_step`
   B  Relu(a + Broadcast(c)) * b and its row Sum        `fused_chain`
   C  small CNN 2xConv + maxpool composite + fc         `cnn_step`
+  D  ResNet-18-style convnet, NCHW<->NHWC              `resnet_step`
   E  wide MLP, L layers of width W, global batch       `mlp_step(hidden=[W]*L)`
 """
 
@@ -152,6 +153,66 @@ def cnn_step(api, batch=256, image=32, channels=(3, 16, 32), classes=10, lr=0.01
     return _training_step(api, fn, loss, names, ["K1", "K2", "Wf"], lr, et)
 
 
+def resnet_step(api, batch=128, image=224, widths=(64, 128, 256, 512), blocks=2, classes=10, lr=0.01,
+                f32=True, loss_batch=None) -> StepGraph:
+    """ResNet-18-style training step (config D).
+
+    The IR has no strided-conv gradient (`autodiff.py:226-230`), no BatchNorm
+    and no max-pool op, so:
+    * the stem is a 7x7 stride-1 pad-3 conv followed by two pool composites
+      (224 -> 56);
+    * each stage runs `blocks` BasicBlocks of two 3x3 stride-1 convs;
+    * stages are joined by a pool composite and a 1x1 projection shortcut.
+    The head is a spatial Sum scaled by 1/(H*W), then fc -> softmax
+    cross-entropy.  Compile it with conv_layout="nhwc" for the layout
+    assignment the config names."""
+    et = api.ElementType.F32 if f32 else api.ElementType.F64
+    K = api.OpKind
+    fn = api.Function("resnet_step")
+    names = ["x"]
+    x = fn.add_parameter(et, (batch, 3, image, image))
+    pad1 = {"strides": (1, 1), "padding": (1, 1, 1, 1)}
+    weights = []
+
+    def param(shape, name):
+        pid = fn.add_parameter(et, shape)
+        names.append(name)
+        weights.append(name)
+        return pid
+
+    stem = param((widths[0], 3, 7, 7), "K_stem")
+    h = fn.add_node(K.RELU, [fn.add_node(K.CONV2D, [x, stem], {"strides": (1, 1), "padding": (3, 3, 3, 3)})])
+    size, ch = image, widths[0]
+    for _ in range(2):
+        h = maxpool2x2(api, fn, h, (batch, ch, size, size))
+        size //= 2
+    for si, w in enumerate(widths):
+        if si > 0:
+            h = maxpool2x2(api, fn, h, (batch, ch, size, size))
+            size //= 2
+        for bi in range(blocks):
+            k1 = param((w, ch, 3, 3), f"K{si}_{bi}a")
+            k2 = param((w, w, 3, 3), f"K{si}_{bi}b")
+            y = fn.add_node(K.RELU, [fn.add_node(K.CONV2D, [h, k1], pad1)])
+            y = fn.add_node(K.CONV2D, [y, k2], pad1)
+            if ch != w:
+                kp = param((w, ch, 1, 1), f"P{si}_{bi}")
+                short = fn.add_node(K.CONV2D, [h, kp], {"strides": (1, 1), "padding": (0, 0, 0, 0)})
+            else:
+                short = h
+            h = fn.add_node(K.RELU, [fn.add_node(K.ADD, [y, short])])
+            ch = w
+    pooled = fn.add_node(K.SUM, [h], {"reduction_axes": (2, 3)})
+    scale = fn.add_constant(et, (), [1.0 / (size * size)])
+    pooled = fn.add_node(K.MULTIPLY, [pooled, fn.add_node(K.BROADCAST, [scale], {"output_shape": (batch, ch), "broadcast_axes": (0, 1)})])
+    wf = param((ch, classes), "Wf")
+    t = fn.add_parameter(et, (batch, classes))
+    names.append("t")
+    logits = fn.add_node(K.DOT, [pooled, wf])
+    loss = _softmax_xent(api, fn, logits, t, loss_batch or batch, et)
+    return _training_step(api, fn, loss, names, weights, lr, et)
+
+
 def fused_chain(api, rows=65536, cols=1024, f32=True):
     """Config B: t3 = Relu(a + Broadcast(c)) * b; results t3 and Sum_axis1(t3)."""
     et = api.ElementType.F32 if f32 else api.ElementType.F64
@@ -193,6 +254,9 @@ def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True) -> list:
             out.append(_one_hot(rng, shape[0], shape[1], dtype))
         elif name == "seed":
             out.append(np.ones(shape, dtype=dtype))
+        elif len(shape) == 4:  # conv filter [K, C, R, S]: He-style fan-in bound
+            bound = float(np.sqrt(6.0 / (shape[1] * shape[2] * shape[3])))
+            out.append(_uniform(rng, shape, -bound, bound, dtype))
         else:
             fan = shape[0] if len(shape) >= 2 else 10
             bound = 0.1 if fan <= 1024 else 1.0 / 64.0

@@ -171,6 +171,7 @@ def workload_cases():
     out.append(_step_fixture("mlp_E_small", W.mlp_step(gf, batch=16, in_dim=24, hidden=(24, 24), out_dim=24), seed=5))
     out.append(_step_fixture("cnn_C_small", W.cnn_step(gf, batch=2, image=8, channels=(3, 4, 4)), seed=3))
     out.append(_step_fixture("mlp_A_f64", W.mlp_step(gf, batch=3, in_dim=12, hidden=(8,), out_dim=5, f32=False), seed=7, f32=False))
+    out.append(_step_fixture("resnet_D_small", W.resnet_step(gf, batch=2, image=16, widths=(4, 8), blocks=1), seed=11))
     fn = W.fused_chain(gf, rows=16, cols=64)
     arrays = W.chain_inputs(16, 64, seed=1)
     et = gf.ElementType.F32
@@ -190,8 +191,13 @@ def workload_cases():
 
 if __name__ == "__main__":
     t0 = time.time()
-    dump("corpus.json.gz", corpus())
-    dump("layouts.json.gz", layout_cases())
-    dump("gradients.json.gz", gradient_cases())
-    dump("workloads.json.gz", workload_cases())
+    which = set(sys.argv[1:]) or {"corpus", "layouts", "gradients", "workloads"}
+    if "corpus" in which:
+        dump("corpus.json.gz", corpus())
+    if "layouts" in which:
+        dump("layouts.json.gz", layout_cases())
+    if "gradients" in which:
+        dump("gradients.json.gz", gradient_cases())
+    if "workloads" in which:
+        dump("workloads.json.gz", workload_cases())
     print(f"done in {time.time() - t0:.1f}s")

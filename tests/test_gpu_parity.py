@@ -87,7 +87,7 @@ def test_gradient_graphs():
                 assert G.max_abs_diff(o, G.logical(w)) <= 1e-12, case["name"]
 
 
-@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small"])
+@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small", "resnet_D_small"])
 def test_workloads(name):
     case = next(c for c in G.load("workloads.json.gz") if c["name"] == name)
     exe = gf.compile_function(G.fn_of(case["fn"]))

@@ -108,3 +108,17 @@ def test_call_streamed_equals_call():
     ref = [t.to_numpy() for t in gf.call(exe, host)]
     assert G.same_bits(out[0].to_numpy(), ref[0])
     assert G.normwise(out[1].to_numpy(), ref[1]) <= 1e-6
+
+
+@pytest.mark.parametrize("layout", ["identity", "nhwc"])
+def test_config_D_reduced(layout):
+    """ResNet-18-style step (config D topology) at 32x32 / batch 4 with the
+    tensor-core conv path, both layouts, against the oracle."""
+    interp.set_threads(interp.max_threads())
+    step = W.resnet_step(gf, batch=4, image=32, widths=(16, 32), blocks=1)
+    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=4)
+    want = interp.run_function(step.fn, arrays)
+    exe = gf.compile_function(step.fn, conv_layout=layout)
+    outs = [t.to_numpy() for t in gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])]
+    for o, w in zip(outs, want):
+        assert G.normwise(o, w) <= 1e-4

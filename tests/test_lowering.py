@@ -55,7 +55,7 @@ def test_layout_cases(idx):
     _compare(emulate(h, [G.tensor_of(d) for d in case["inputs"]]), case["outputs"], case["name"])
 
 
-@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small"])
+@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small", "resnet_D_small"])
 def test_workloads_emulated(name):
     case = next(c for c in G.load("workloads.json.gz") if c["name"] == name)
     fn = G.fn_of(case["fn"])
@@ -154,3 +154,15 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
     out = emulate(h, tens)[0]
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+def test_resnet_nhwc_layout_assignment_emulated():
+    """Config D at reduced size under conv_layout='nhwc': conversions are
+    inserted by layout assignment and fused away as index maps."""
+    case = next(c for c in G.load("workloads.json.gz") if c["name"] == "resnet_D_small")
+    fn = G.fn_of(case["fn"])
+    ident = host_compile(fn)
+    nhwc = host_compile(fn, conv_layout="nhwc")
+    assert sum(1 for n in nhwc.graph.nodes.values() if n.op.value == "ConvertLayout") > 0
+    assert len(nhwc.lowered.launches) == len(ident.lowered.launches)
+    _compare(emulate(nhwc, [G.tensor_of(d) for d in case["inputs"]]), case["outputs"], "resnet nhwc")

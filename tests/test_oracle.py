@@ -44,7 +44,7 @@ def test_gradient_graphs_bit_exact():
                 assert G.same_bits(o, G.logical(w)), case["name"]
 
 
-@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small"])
+@pytest.mark.parametrize("name", ["mlp_A_small", "mlp_E_small", "cnn_C_small", "mlp_A_f64", "chain_B_small", "resnet_D_small"])
 def test_workload_steps_bit_exact(name):
     case = next(c for c in G.load("workloads.json.gz") if c["name"] == name)
     _run(case, "outputs")
