@@ -831,7 +831,7 @@ class Lowering:
         sa.geo[:len(geo)] = list(geo)
         sa.st[:len(st)] = list(st)
         grid = (max(1, min((rows * kp // 4 + 255) // 256, NUM_SMS * 16)), 1, 1) if mode == 5 else \
-               ((rows + 31) // 32, (kp + 31) // 32, 1)
+               (((rows + 31) // 32) * ((kp + 31) // 32), 1, 1)
         rec = LaunchRec(abi.K_SPLIT_TF32, grid, (256, 1, 1), 0, sa, [src.key], [hi.key, lo.key], f"split_{name}#{n}")
         rec.algo_bytes = rows * kdim * 4 + 2 * rows * kp * 4
         rec.finalize = _finalize_refs(sa, {"src": src, "hi": hi, "lo": lo})
@@ -862,7 +862,9 @@ class Lowering:
                 setattr(ta, k_, v_)
         wide = ncols >= 256 and os.environ.get("GFB_TC_WIDE", "1") == "1"
         bn = 256 if wide else TC_TILE
-        grid = ((m + TC_TILE - 1) // TC_TILE, (ncols + bn - 1) // bn, splits)
+        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, splits)
+        if grid[1] > 65535:
+            raise UnsupportedOp(f"tensor-core GEMM with {m} rows exceeds the 65535-tile grid")
         rec = LaunchRec(abi.K_DOT_TC32W if wide else abi.K_DOT_TC32, grid, (320 if wide else 192, 1, 1),
                         TC_SMEM_W if wide else TC_SMEM, ta, [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
         rec.flops = 2 * m * ncols * kdim

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(tc::Cfg<BN_>::THREADS, 1) gfb_gemm_tc_kernel(c
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;  // M tiles on grid.x (no 65535 limit)
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;  // N-fastest raster: CTAs sharing A tiles run together
     // split-K: CTA z owns K range [k_begin, k_end) (k_per_split is a multiple of BK)
     const int64_t k_begin = p.k_splits > 1 ? (int64_t)blockIdx.z * p.k_per_split : 0;
     const int64_t k_end = p.k_splits > 1 ? min(p.K, k_begin + p.k_per_split) : p.K;
@@ -353,8 +353,11 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
         }
         return;
     }
-    // rows on grid.x (up to 2^31 tiles: N*H*W of a 224x224 batch overflows grid.y)
-    const int64_t r0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+    // 1-D grid over (row tile, k tile): either extent can exceed 65535 (the
+    // N*H*W rows of a 224x224 batch, or the K of a weight gradient)
+    const int64_t row_tiles = (p.rows + 31) / 32;
+    const int64_t tile = blockIdx.x;
+    const int64_t r0 = (tile % row_tiles) * 32, k0 = (tile / row_tiles) * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const bool k_fast = p.mode != 0 || p.s_k <= p.s_r;
 #pragma unroll
