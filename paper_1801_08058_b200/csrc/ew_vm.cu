@@ -392,7 +392,7 @@ __device__ __forceinline__ T fold_init(int kind) {
 template <typename T, int V>
 __global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ gfb_ew_args p) {
     __shared__ Shared sh;
-    extern __shared__ __align__(16) unsigned char dyn[];
+    extern __shared__ __align__(128) unsigned char dyn[];
     const int nthr = blockDim.x, tid = threadIdx.x;
     const int nleaves = p.nleaves;
     uint32_t* ob = reinterpret_cast<uint32_t*>(dyn) + tid;

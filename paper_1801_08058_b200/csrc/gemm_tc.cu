@@ -356,8 +356,8 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
     // 1-D grid over (row tile, k tile): either extent can exceed 65535 (the
     // N*H*W rows of a 224x224 batch, or the K of a weight gradient)
     const int64_t row_tiles = (p.rows + 31) / 32;
-    const int64_t tile = blockIdx.x;
-    const int64_t r0 = (tile % row_tiles) * 32, k0 = (tile / row_tiles) * 32;
+    const int64_t tid2 = blockIdx.x;
+    const int64_t r0 = (tid2 % row_tiles) * 32, k0 = (tid2 / row_tiles) * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const bool k_fast = p.mode != 0 || p.s_k <= p.s_r;
 #pragma unroll
