@@ -55,6 +55,10 @@ enum {
     GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot on split planes (gfb_tc_args) */
     GFB_K_SPLIT_TF32 = 13, /* F32 -> TF32 hi/lo K-major planes (gfb_split_args) */
     GFB_K_DOT_TC32W = 14,  /* as GFB_K_DOT_TC32 with 128x256 tiles (gfb_tc_args) */
+    GFB_K_DOT_SM_F32 = 15, /* SIMT Dot for m <= 8, thread per column, bit-exact (gfb_dot_args) */
+    GFB_K_DOT_SM_F64 = 16,
+    GFB_K_CONV_TCG64 = 17,  /* implicit-GEMM conv, in-kernel gather + TF32 split, 128x64 tiles (gfb_tcg_args) */
+    GFB_K_CONV_TCG128 = 18, /* as GFB_K_CONV_TCG64 with 128x128 tiles */
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
@@ -196,6 +200,29 @@ typedef struct GFB_ALIGN64 {
     int64_t pad[5];
     uint64_t tmap[4][16];
 } gfb_tc_args;
+
+/* Implicit-GEMM convolution with the A gather fused into the tensor-core
+ * kernel.  A is a 4-D activation with unit channel stride (NHWC storage):
+ * GEMM row `row` = (n, y, x) over extents (*, Y, X) has spatial origin
+ * h = y*sy + oy, w = x*sx + ox; K index k = (r, s, c) over (R, S, C = 32*CB)
+ * reads a[n, h + ksign*r, w + ksign*s, c] (element strides xs0, xs2, xs3
+ * along n, h, w), zero outside [0, H) x [0, W).  Conv2D: (Y, X) = (Ho, Wo),
+ * (sy, sx) = strides, (oy, ox) = -(pt, pl), ksign = +1.  ConvBackpropData:
+ * (Y, X) = (H, W), unit strides, (oy, ox) = (pt, pl), ksign = -1, and H, W
+ * here are the delta's Ho, Wo.  B is the filter as TF32 hi/lo planes
+ * [N, K] (K-major, same k order), tensor maps encoded by gfb_exe_create.
+ * The output is addressed as in gfb_tc_args. */
+typedef struct GFB_ALIGN64 {
+    const void* const* tab;
+    uint64_t c;
+    int64_t M, N, K;
+    int64_t c_sm, c_sn, c_rdiv, c_s_hi, c_s_lo;
+    uint64_t a, b_hi, b_lo;
+    int64_t xs0, xs2, xs3;
+    int32_t Y, X, sy, sx, oy, ox, H, W, S, CB, ksign, pad0;
+    int64_t pad[2];
+    uint64_t tmap[2][16];
+} gfb_tcg_args;
 
 typedef struct {
     const void* const* tab;

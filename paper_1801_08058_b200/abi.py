@@ -13,6 +13,8 @@ GFB_OK = 0
 K_EW_F32, K_EW_F64, K_EW_I64, K_EW_U8 = 1, 2, 3, 4
 K_EWS_F32, K_EWS_F64 = 5, 6
 K_DOT_F32, K_DOT_F64, K_DOT_TC32, K_SPLIT_TF32, K_DOT_TC32W = 10, 11, 12, 13, 14
+K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
+K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
 
@@ -87,6 +89,21 @@ class TcArgs(C.Structure):
     ]
 
 
+class TcgArgs(C.Structure):
+    # 64-byte aligned in C: tmap sits at offset 192, size 448.
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64),
+        ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
+        ("c_sm", C.c_int64), ("c_sn", C.c_int64), ("c_rdiv", C.c_int64), ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64),
+        ("a", C.c_uint64), ("b_hi", C.c_uint64), ("b_lo", C.c_uint64),
+        ("xs0", C.c_int64), ("xs2", C.c_int64), ("xs3", C.c_int64),
+        ("Y", C.c_int32), ("X", C.c_int32), ("sy", C.c_int32), ("sx", C.c_int32), ("oy", C.c_int32), ("ox", C.c_int32),
+        ("H", C.c_int32), ("W", C.c_int32), ("S", C.c_int32), ("CB", C.c_int32), ("ksign", C.c_int32), ("pad0", C.c_int32),
+        ("pad", C.c_int64 * 2),
+        ("tmap", (C.c_uint64 * 16) * 2),
+    ]
+
+
 class ConvArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p),
@@ -126,5 +143,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

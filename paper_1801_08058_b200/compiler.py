@@ -50,6 +50,7 @@ from .ir import (
     topological_order,
 )
 from .memory import DEVICE_ALIGNMENT, align_up, plan_buffers
+from .layout import NHWC_ORDER, Layout
 
 NUM_SMS = 148
 HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER})
@@ -120,6 +121,9 @@ INDEX_LIMIT = 1 << 31
 TC_TILE = 128
 TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
 TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
+# gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
+TCG_SMEM = {bn: (2 if bn == 128 else 3) * (2 * 128 + 2 * bn) * 32 * 4 + 4 * 128 * 32 * 4 + 128 * 16 + 256 + 1024
+            for bn in (64, 128)}
 
 
 def _conv_tc_ok(m: int, n: int, k: int) -> bool:
@@ -403,6 +407,9 @@ class Lowering:
                 if n not in self.consumers[r]:
                     self.consumers[r].append(n)
         self.param_pos = {pid: i for i, pid in enumerate(g.parameters)}
+        # NHWC layout policy in force (Conv2D outputs channel-last)?
+        self.channels_last = any(self.nodes[n].op is OpKind.CONV2D and layouts[(n, 0)].order == NHWC_ORDER
+                                 for n in self.order)
         self.buf: dict = {}
         self.n_in = len(g.parameters)
         self.n_out = len(g.results)
@@ -487,7 +494,7 @@ class Lowering:
                 if probe:
                     return (True, None) if self.is_source(src) else None
                 b, st = inner
-                if tuple(st) == _rowmajor(in_shape) or element_count(in_shape) <= 1:
+                if _dense_rowmajor(in_shape, st):
                     return b, _rowmajor(node.output.shape)
             return None
         return None
@@ -538,9 +545,15 @@ class Lowering:
                 self.buf[n] = b
             elif n in self.M or node.op in HEAVY:
                 slot = abi.SLOT_ARENA
+                strides = self.strides_of(n)
                 if n in result_slot:
                     slot = abi.SLOT_IO + self.n_in + result_slot[n]
-                self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, self.strides_of(n), slot)
+                elif self.channels_last and len(d.shape) == 4 and node.op is not OpKind.CONV_BACKPROP_FILTER:
+                    # intermediates are stored channel-last under the NHWC policy: every
+                    # kernel reads through strides, and the convolutions' gathers then
+                    # find 32-channel runs contiguous (gfb_conv_tcg_kernel)
+                    strides = Layout(NHWC_ORDER).strides(d.shape)
+                self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, strides, slot)
 
         # merge rule: a materialised node consumed only by one Sum is that Sum's side output
         side_of = {}
@@ -700,29 +713,50 @@ class Lowering:
         total = element_count(shape)
         if total == 0:
             return
+        # Iterate in the output's storage order so stores coalesce (channel-last
+        # intermediates); fall back to logical order when an index op on the
+        # way down cannot follow the permuted digits.
+        perm = _storage_perm(self.buf[root])
+        if perm != list(range(len(shape))):
+            mark = len(self.launches)
+            try:
+                self._emit_map_in(root, shape, perm, et, total, node)
+                return
+            except (_Retry, Unexpressible):
+                del self.launches[mark:]
+        self._emit_map_in(root, shape, list(range(len(shape))), et, total, node)
+
+    def _emit_map_in(self, root, shape, perm, et, total, node):
+        pshape = tuple(shape[a] for a in perm)
+
+        def logical(axes_p):
+            ax = [None] * len(shape)
+            for i, a in enumerate(perm):
+                ax[a] = axes_p[i]
+            return ax
+
         # Split the iteration space into rows (o) x contiguous columns (r)
         # when the trailing extent is long enough for warp-wide vectors.
-        inner_from = len(shape)
-        while inner_from > 0 and _prod(shape[inner_from:]) < 256:
+        inner_from = len(pshape)
+        while inner_from > 0 and _prod(pshape[inner_from:]) < 256:
             inner_from -= 1
-        n_r = _prod(shape[inner_from:])
+        n_r = _prod(pshape[inner_from:])
         # rows x columns only when there are enough rows to fill the GPU;
         # a map has no reason to run few, very long rows (flat mode instead)
         few_rows = total // max(n_r, 1) < NUM_SMS * 8 and n_r > 8192
-        if n_r >= 128 and inner_from < len(shape) and not few_rows:
+        if n_r >= 128 and inner_from < len(pshape) and not few_rows:
             n_o = total // n_r
             prog = Program(self, extents=(max(n_o, 1), n_r), vec_src=1, et=et)
             try:
-                prog.eval_store(root, split_axes(shape, inner_from), self.buf[root])
+                prog.eval_store(root, logical(split_axes(pshape, inner_from)), self.buf[root])
             except _Retry:
                 prog = None  # a Reshape straddles the row split: use the flat form
             if prog is not None:
                 self._row_launch(prog, n_o, n_r, 0, f"map:{node.op.wire_name}#{root}", et)
                 return
-        if True:
-            prog = Program(self, extents=(total, 1), vec_src=0, et=et)
-            prog.eval_store(root, iteration_axes(shape), self.buf[root])
-            self._col_launch(prog, total, 1, 0, f"map:{node.op.wire_name}#{root}", et)
+        prog = Program(self, extents=(total, 1), vec_src=0, et=et)
+        prog.eval_store(root, logical(iteration_axes(pshape)), self.buf[root])
+        self._col_launch(prog, total, 1, 0, f"map:{node.op.wire_name}#{root}", et)
 
     def emit_reduce(self, s: int, side: int | None):
         node = self.nodes[s]
@@ -880,6 +914,29 @@ class Lowering:
             self._col_launch(p2, m * ncols, splits, 1, label + ":splitk", ElementType.F32)
         return rec
 
+    @staticmethod
+    def _gather_ok(xb, xs, channels, m) -> bool:
+        """The fused-gather conv kernel needs unit channel stride (NHWC
+        storage), whole 32-channel K-blocks and 16-byte aligned runs."""
+        return (os.environ.get("GFB_CONV_GATHER", "1") == "1" and xb.splat is None and xs[1] == 1
+                and channels % 32 == 0 and all(v % 4 == 0 for v in (xs[0], xs[2], xs[3]))
+                and xb.offset % 16 == 0 and (m + TC_TILE - 1) // TC_TILE <= 65535
+                and max(abs(v) for v in xs) * 4 < 2 ** 62)
+
+    def _conv_tcg(self, n, xb, xs, b, out, m, ncols, kdim, geo, addr, yb, label):
+        """Conv2D / ConvBackpropData with the activation gather and TF32
+        split inside the tensor-core kernel (gemm_tc.cu, gfb_conv_tcg_kernel)."""
+        bhi, blo, _ = b
+        bn = 64 if ncols <= 64 else 128
+        ta = abi.TcgArgs(M=m, N=ncols, K=kdim, xs0=xs[0], xs2=xs[2], xs3=xs[3], c_sm=0, **addr, **geo)
+        kind = abi.K_CONV_TCG64 if bn == 64 else abi.K_CONV_TCG128
+        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, 1)
+        rec = LaunchRec(kind, grid, (320, 1, 1), TCG_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [out.key], label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "b_hi": bhi, "b_lo": blo})
+        self.launches.append(rec)
+
     def emit_conv_tc(self, n) -> bool:
         """Conv2D / ConvBackpropData / ConvBackpropFilter as implicit GEMMs on
         the tensor cores; returns False when the shape or layout does not fit
@@ -905,6 +962,12 @@ class Lowering:
             m, ncols, kdim = N * Ho * Wo, K, Cc * R * S
             if os_[2] != Wo * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if self._gather_ok(xb, xs, Cc, m):
+                b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (R, S, Cc), st=(ys[2], ys[3], ys[1]))
+                self._conv_tcg(n, xb, xs, b, out, m, ncols, kdim, dict(Y=Ho, X=Wo, sy=sh, sx=sw, oy=-pt, ox=-pl, H=H, W=W, S=S,
+                               CB=Cc // 32, ksign=1), {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
+                               yb, f"{node.op.wire_name}_tcg#{n}")
+                return True
             geo = (N, Cc, H, W, R, S, Ho, Wo, sh, sw, pt, pl)
             a = self._split(n, "a", xb, m, kdim, 1, geo=geo, st=xs)
             b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (Cc, R, S), st=ys[1:])
@@ -916,6 +979,12 @@ class Lowering:
             m, ncols, kdim = N * H * W, Cc, K * R * S
             if os_[2] != W * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if self._gather_ok(xb, xs, K, m):
+                b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (R, S, K), st=(ys[2], ys[3], ys[0]))
+                self._conv_tcg(n, xb, xs, b, out, m, ncols, kdim, dict(Y=H, X=W, sy=1, sx=1, oy=pt, ox=pl, H=Ho, W=Wo, S=S,
+                               CB=K // 32, ksign=-1), {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
+                               yb, f"{node.op.wire_name}_tcg#{n}")
+                return True
             geo = (N, K, H, W, R, S, Ho, Wo, 1, 1, pt, pl)
             a = self._split(n, "a", xb, m, kdim, 2, geo=geo, st=xs)
             b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (K, R, S), st=(ys[0], ys[2], ys[3]))
@@ -952,8 +1021,12 @@ class Lowering:
                 return
             args = abi.DotArgs(m=m, n=nn, k=k, a_sm=ast[0], a_sk=ast[1], b_sk=bst[0], b_sn=bst[1],
                                c_sm=out.strides[0], c_sn=out.strides[1])
-            kind = abi.K_DOT_F32 if et is ElementType.F32 else abi.K_DOT_F64
-            grid = ((nn + 63) // 64, (m + 63) // 64, 1)
+            if m <= 8 and nn >= 256:
+                kind = abi.K_DOT_SM_F32 if et is ElementType.F32 else abi.K_DOT_SM_F64
+                grid = (max(1, min((nn + 255) // 256, NUM_SMS * 16)), 1, 1)
+            else:
+                kind = abi.K_DOT_F32 if et is ElementType.F32 else abi.K_DOT_F64
+                grid = ((nn + 63) // 64, (m + 63) // 64, 1)
             rec = LaunchRec(kind, grid, (256, 1, 1), 0, args, [ab.key, bb.key], [out.key], f"dot#{n}")
             rec.flops = 2 * m * nn * k
             rec.algo_bytes = (m * k + k * nn + m * nn) * et.byte_size
@@ -1000,6 +1073,19 @@ class Lowering:
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
         rec.finalize = _finalize_refs(args, {"x": xb, "y": yb, "out": out})
         self.launches.append(rec)
+
+
+def _storage_perm(buf) -> list:
+    """Logical axes from outermost to innermost in memory (unit axes stay put)."""
+    live = sorted((a for a in range(len(buf.shape)) if buf.shape[a] > 1), key=lambda a: (-buf.strides[a], a))
+    it = iter(live)
+    return [a if buf.shape[a] <= 1 else next(it) for a in range(len(buf.shape))]
+
+
+def _dense_rowmajor(shape, strides) -> bool:
+    """Row-major contiguous, ignoring the (meaningless) strides of unit axes."""
+    want = _rowmajor(shape)
+    return all(d == 1 or s == w for d, s, w in zip(shape, strides, want))
 
 
 def _rowmajor(shape) -> tuple:

@@ -123,6 +123,100 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// Single-thread MMA issuer: for each K-block, wait for the stage, issue the
+// three 3xTF32 products per 8-wide K step, free the stage, and hand a TMEM
+// accumulator chunk to the epilogue every CHUNK_KB K-blocks.  Stage layout:
+// [A hi | A lo | B hi | B lo], each K-major SW128.
+template <int BN, int STAGES, int STAGE_BYTES, int A_BYTES, int B_BYTES, int CHUNK_KB, int NBUF>
+__device__ __forceinline__ void mma_loop(unsigned char* smem, uint64_t* full, uint64_t* empty, uint64_t* tfull,
+                                         uint64_t* tempty, uint32_t tmem, int nk) {
+    constexpr uint32_t idesc = idesc_tf32(128, BN);
+    for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        const int chunk = kb / CHUNK_KB, b = chunk % NBUF;
+        const bool chunk_start = kb % CHUNK_KB == 0;
+        if (chunk_start) {
+            mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);  // epilogue drained this buffer
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        unsigned char* st = smem + s * STAGE_BYTES;
+        const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+        const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t adv = (uint64_t)(j * 32) >> 4;  // 8 tf32 = 32 B along K inside the atom
+            const uint32_t acc = !(chunk_start && j == 0);
+            mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+            mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+            mma_tf32(d, al + adv, bh + adv, idesc, 1);
+        }
+        mma_commit(&empty[s]);
+        if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == nk - 1) mma_commit(&tfull[b]);
+    }
+}
+
+// Epilogue warp: TMEM lanes [32*(warp%4), +32) = tile rows, and EC columns
+// (column group cg).  Every finished accumulator chunk is promoted into fp32
+// registers with round-to-nearest adds; the sums are stored at the end.
+template <int BN, int EPI_WARPS, int NBUF>
+__device__ __forceinline__ void epilogue(int warp, int lane, uint64_t* tfull, uint64_t* tempty, uint32_t tmem,
+                                         int nchunk, float* C, int m0, int n0, int64_t M, int64_t N, int64_t c_sm,
+                                         int64_t c_sn, int64_t c_rdiv, int64_t c_s_hi, int64_t c_s_lo) {
+    constexpr int EC = BN < 128 ? BN : 128;
+    const int q = warp & 3, cg = ((warp - 2) >> 2) % (BN / EC);
+    float acc[EC];
+#pragma unroll
+    for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+    for (int chunk = 0; chunk < nchunk; ++chunk) {
+        const int b = chunk % NBUF;
+        mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c = 0; c < EC / 32; ++c) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + cg * EC + c * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+    }
+    const int row = m0 + q * 32 + lane;
+    if (row < M) {
+        const int64_t roff = c_rdiv > 0 ? (row / c_rdiv) * c_s_hi + (row % c_rdiv) * c_s_lo : (int64_t)row * c_sm;
+        float* dst = C + roff;
+#pragma unroll
+        for (int c = 0; c < EC / 32; ++c) {
+            const int col0 = n0 + cg * EC + c * 32;
+            if (c_sn == 1 && col0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(dst + col0 + j) =
+                        make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (col0 + j < N) dst[(int64_t)(col0 + j) * c_sn] = acc[c * 32 + j];
+            }
+        }
+    }
+}
+
 }  // namespace tc
 
 template <int BN_>
@@ -187,90 +281,11 @@ __global__ void __launch_bounds__(tc::Cfg<BN_>::THREADS, 1) gfb_gemm_tc_kernel(c
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32(BM, BN);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                const int chunk = kb / CHUNK_KB, b = chunk % NBUF;
-                const bool chunk_start = kb % CHUNK_KB == 0;
-                if (chunk_start) {
-                    mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);  // epilogue drained this buffer
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                mbar_wait(&full[s], ph);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                unsigned char* st = smem + s * STAGE_BYTES;
-                const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
-                const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
-                const uint32_t d = tmem + (uint32_t)(b * BN);
-#pragma unroll
-                for (int j = 0; j < BK / 8; ++j) {
-                    const uint64_t adv = (uint64_t)(j * 32) >> 4;  // 8 tf32 = 32 B along K inside the atom
-                    const uint32_t acc = !(chunk_start && j == 0);
-                    mma_tf32(d, ah + adv, bh + adv, idesc, acc);
-                    mma_tf32(d, ah + adv, bl + adv, idesc, 1);
-                    mma_tf32(d, al + adv, bh + adv, idesc, 1);
-                }
-                mma_commit(&empty[s]);
-                if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == nk - 1) mma_commit(&tfull[b]);
-            }
-        }
+        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
     } else {
-        // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows and
-        // 128 columns (group cg); it promotes every finished chunk into fp32
-        // registers, then stores.
-        constexpr int EC = 128;  // columns per epilogue warp
-        const int q = warp & 3, cg = (warp - 2) >> 2;
-        float acc[EC];
-#pragma unroll
-        for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
-        for (int chunk = 0; chunk < nchunk; ++chunk) {
-            const int b = chunk % NBUF;
-            mbar_wait(&tfull[b], (chunk / NBUF) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-            for (int c = 0; c < EC / 32; ++c) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + cg * EC + c * 32);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
-        }
         float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
-        const int row = m0 + q * 32 + lane;
-        if (row < p.M) {
-            const int64_t roff = p.c_rdiv > 0 ? (row / p.c_rdiv) * p.c_s_hi + (row % p.c_rdiv) * p.c_s_lo
-                                               : (int64_t)row * p.c_sm;
-            float* dst = C + roff;
-#pragma unroll
-            for (int c = 0; c < EC / 32; ++c) {
-                const int col0 = n0 + cg * EC + c * 32;
-                if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(dst + col0 + j) =
-                            make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
-                }
-            }
-        }
+        epilogue<BN, EPI_WARPS, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, C, m0, n0, p.M, p.N, p.c_sm, p.c_sn,
+                                      p.c_rdiv, p.c_s_hi, p.c_s_lo);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -389,16 +404,199 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Implicit-GEMM convolution with the operand gather and the TF32 split fused
+// into the tensor-core kernel (no im2col planes in HBM).
+//
+// A[row, k] is an activation tensor whose channels are contiguous (NHWC
+// layout assignment); k runs (r, s, c) with c fastest, so each 32-wide
+// K-block is one filter tap (r, s) and 32 consecutive channels: per output
+// row a single 128-byte run, or zero padding.  Four gather warps stream those
+// runs with 16-byte cp.async (zero-fill for padding taps) into a 4-deep raw
+// ring laid out in the SW128 K-major pattern, then split each 16-byte chunk
+// into TF32 hi/lo in place of the MMA stage.  B (the filter, small and
+// reused) arrives as hi/lo planes by TMA, K-major in the same (r, s, c)
+// order.  Warp roles: 0 B TMA, 1 TMEM + MMA issuer, 2..5 epilogue,
+// 6..9 A gather + split.
+namespace tc {
+template <int BN_>
+struct GCfg {
+    static constexpr int BM = 128, BN = BN_, BK = 32;
+    static constexpr int STAGES = BN_ == 128 ? 2 : 3;
+    static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int RAW = 4;  // raw A K-blocks in flight per CTA
+    static constexpr int CHUNK_KB = 4, NBUF = 512 / BN;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4, GATHER_WARPS = 4;
+    static constexpr int THREADS = 64 + 32 * (EPI_WARPS + GATHER_WARPS);
+    static constexpr int ROWTAB = BM * 16;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RAW * A_BYTES + ROWTAB + 256 + 1024;
+};
+
+struct RowInfo {
+    int64_t off;  // element offset of tap (0, 0), channel 0
+    int32_t h, w; // its spatial coordinates (invalid rows: h far out of range)
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+}  // namespace tc
+
+template <int BN_>
+__global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel(const __grid_constant__ gfb_tcg_args p) {
+    using namespace tc;
+    using C_ = GCfg<BN_>;
+    constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, RAW = C_::RAW;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GATHER_WARPS = C_::GATHER_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* raw = smem + STAGES * STAGE_BYTES;
+    RowInfo* rowtab = reinterpret_cast<RowInfo*>(raw + RAW * A_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(rowtab) + C_::ROWTAB);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
+    const int nk = (int)(p.K / BK);
+    const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1 + GATHER_WARPS);  // TMA expect_tx arrival + one per gather warp
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(p.tmap[0]);
+        prefetch_tmap(p.tmap[1]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+                unsigned char* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], 2 * B_BYTES);
+                tma_load_2d(st + 2 * A_BYTES, p.tmap[0], kb * BK, n0, &full[s]);
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[1], kb * BK, n0, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
+    } else if (warp < 2 + EPI_WARPS) {
+        epilogue<BN, EPI_WARPS, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, resolve<float>(p.tab, p.c), m0, n0, p.M,
+                                      p.N, p.c_sm, p.c_sn, p.c_rdiv, p.c_s_hi, p.c_s_lo);
+    } else {
+        const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127
+        {
+            const int64_t row = m0 + g;
+            RowInfo ri;
+            if (row < p.M) {
+                const int64_t yx = (int64_t)p.Y * p.X;
+                const int64_t n = row / yx, rem = row - n * yx, y = rem / p.X, x = rem - y * p.X;
+                ri.h = (int32_t)(y * p.sy + p.oy);
+                ri.w = (int32_t)(x * p.sx + p.ox);
+                ri.off = n * p.xs0 + (int64_t)ri.h * p.xs2 + (int64_t)ri.w * p.xs3;
+            } else {
+                ri.off = 0;
+                ri.h = -(1 << 30);
+                ri.w = 0;
+            }
+            rowtab[g] = ri;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(GATHER_WARPS * 32) : "memory");
+        const float* A = resolve<const float>(p.tab, p.a);
+        const int j = g & 7, rb = g >> 3;
+        const uint32_t swz = (uint32_t)((j ^ (rb & 7)) << 4);  // row & 7 == rb & 7 for every row rb + 16 i
+        auto issue = [&](int kb) {
+            const int cb = kb % p.CB, rs = kb / p.CB, r = rs / p.S, s = rs - r * p.S;
+            const int dh = p.ksign * r, dw = p.ksign * s;
+            const int64_t koff = (int64_t)dh * p.xs2 + (int64_t)dw * p.xs3 + cb * 32 + j * 4;
+            unsigned char* dst = raw + (kb % RAW) * A_BYTES + swz;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = rb + 16 * i;
+                const RowInfo ri = rowtab[row];
+                const bool ok = (uint32_t)(ri.h + dh) < (uint32_t)p.H && (uint32_t)(ri.w + dw) < (uint32_t)p.W;
+                cp_async16(dst + row * 128, ok ? (const void*)(A + ri.off + koff) : (const void*)A, ok ? 16u : 0u);
+            }
+        };
+#pragma unroll
+        for (int kb = 0; kb < RAW; ++kb) {
+            if (kb < nk) issue(kb);
+            cp_async_commit();
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+            cp_async_wait<RAW - 1>();  // this thread's copies of K-block kb have landed
+            const int s = kb % STAGES;
+            mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+            const unsigned char* src = raw + (kb % RAW) * A_BYTES + swz;
+            unsigned char* st = smem + s * STAGE_BYTES + swz;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int off = (rb + 16 * i) * 128;
+                const float4 x = *reinterpret_cast<const float4*>(src + off);
+                float4 h, l;
+                split_tf32(x.x, h.x, l.x);
+                split_tf32(x.y, h.y, l.y);
+                split_tf32(x.z, h.z, l.z);
+                split_tf32(x.w, h.w, l.w);
+                *reinterpret_cast<float4*>(st + off) = h;
+                *reinterpret_cast<float4*>(st + A_BYTES + off) = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+            if (kb + RAW < nk) issue(kb + RAW);  // reuses the raw slot just consumed (own chunks only)
+            cp_async_commit();
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 }  // namespace gfb
+
 
 template __global__ void gfb::gfb_gemm_tc_kernel<128>(const __grid_constant__ gfb_tc_args);
 template __global__ void gfb::gfb_gemm_tc_kernel<256>(const __grid_constant__ gfb_tc_args);
+template __global__ void gfb::gfb_conv_tcg_kernel<64>(const __grid_constant__ gfb_tcg_args);
+template __global__ void gfb::gfb_conv_tcg_kernel<128>(const __grid_constant__ gfb_tcg_args);
 
 extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_DOT_TC32) return (const void*)gfb::gfb_gemm_tc_kernel<128>;
     if (kind == GFB_K_DOT_TC32W) return (const void*)gfb::gfb_gemm_tc_kernel<256>;
     if (kind == GFB_K_SPLIT_TF32) return (const void*)gfb::gfb_split_kernel;
+    if (kind == GFB_K_CONV_TCG64) return (const void*)gfb::gfb_conv_tcg_kernel<64>;
+    if (kind == GFB_K_CONV_TCG128) return (const void*)gfb::gfb_conv_tcg_kernel<128>;
     return nullptr;
 }
 
 extern "C" int gfb_tc_smem_bytes(int wide) { return wide ? gfb::tc::Cfg<256>::SMEM_BYTES : gfb::tc::Cfg<128>::SMEM_BYTES; }
+extern "C" int gfb_tcg_smem_bytes(int bn) { return bn == 64 ? gfb::tc::GCfg<64>::SMEM_BYTES : gfb::tc::GCfg<128>::SMEM_BYTES; }

@@ -150,9 +150,12 @@ namespace {
 
 const void* kernel_for(uint32_t kind) {
     if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EWS_F64) return gfb_ew_kernel_ptr((int)kind);
-    if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64)
+    if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64 ||
+        kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64)
         return gfb_simt_kernel_ptr((int)kind);
-    if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_SPLIT_TF32) return gfb_tc_kernel_ptr((int)kind);
+    if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
+        kind == GFB_K_CONV_TCG128)
+        return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
 }
 
@@ -289,6 +292,17 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                 const int64_t rows = t < 2 ? a->M : a->N, kp = t < 2 ? a->kp_a : a->kp_b;
                 const uint32_t box_rows = (t >= 2 && L.kind == GFB_K_DOT_TC32W) ? 256 : 128;
                 if (!encode_plane_map(addr, rows, kp, box_rows, a->tmap[t]))
+                    return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
+            }
+        }
+        if (L.kind == GFB_K_CONV_TCG64 || L.kind == GFB_K_CONV_TCG128) {
+            gfb_tcg_args* a = (gfb_tcg_args*)(e->args.data() + L.arg_offset);
+            const uint64_t refs[2] = {a->b_hi, a->b_lo};
+            for (int t = 0; t < 2; ++t) {
+                if ((refs[t] >> 56) != GFB_SLOT_ARENA)
+                    return bail(fail(GFB_ERR_INVALID, "tensor-core operand planes must live in the arena"));
+                void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
+                if (!encode_plane_map(addr, a->N, a->K, L.kind == GFB_K_CONV_TCG64 ? 64 : 128, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
             }
         }

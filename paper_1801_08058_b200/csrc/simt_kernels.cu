@@ -86,6 +86,33 @@ __global__ void __launch_bounds__(256) gfb_dot_kernel(const __grid_constant__ gf
     }
 }
 
+// Dot with few rows (m <= 8): one thread per output column computes all m
+// outputs, k ascending — the reference order, bit-exact.  This is the shape
+// of the maxpool composite's one-hot selections ([1,4] x [4, N*C*H*W]) and
+// their gradients ([4,1] x [1, M]), where a 64x64 tile would idle 63 of 64
+// threads.  B is read once, coalesced along n.
+template <typename T>
+__global__ void __launch_bounds__(256) gfb_dot_small_m_kernel(const __grid_constant__ gfb_dot_args p) {
+    const T* A = resolve<const T>(p.tab, p.a);
+    const T* B = resolve<const T>(p.tab, p.b);
+    T* C = resolve<T>(p.tab, p.c);
+    const int m = (int)p.m;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += (int64_t)gridDim.x * blockDim.x) {
+        T acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = T(0);
+        for (int64_t t = 0; t < p.k; ++t) {
+            const T b = B[t * p.b_sk + j * p.b_sn];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < m) acc[i] = add_rn(acc[i], mul_rn(__ldg(A + i * p.a_sm + t * p.a_sk), b));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (i < m) C[i * p.c_sm + j * p.c_sn] = acc[i];
+    }
+}
+
 // One thread per output element, the reference loop nest verbatim.
 template <typename T>
 __global__ void __launch_bounds__(256) gfb_conv_kernel(const __grid_constant__ gfb_conv_args p) {
@@ -153,6 +180,8 @@ __global__ void __launch_bounds__(256) gfb_conv_kernel(const __grid_constant__ g
 
 template __global__ void gfb_dot_kernel<float>(const __grid_constant__ gfb_dot_args);
 template __global__ void gfb_dot_kernel<double>(const __grid_constant__ gfb_dot_args);
+template __global__ void gfb_dot_small_m_kernel<float>(const __grid_constant__ gfb_dot_args);
+template __global__ void gfb_dot_small_m_kernel<double>(const __grid_constant__ gfb_dot_args);
 template __global__ void gfb_conv_kernel<float>(const __grid_constant__ gfb_conv_args);
 template __global__ void gfb_conv_kernel<double>(const __grid_constant__ gfb_conv_args);
 
@@ -162,6 +191,8 @@ extern "C" const void* gfb_simt_kernel_ptr(int kind) {
     switch (kind) {
         case GFB_K_DOT_F32: return (const void*)gfb::gfb_dot_kernel<float>;
         case GFB_K_DOT_F64: return (const void*)gfb::gfb_dot_kernel<double>;
+        case GFB_K_DOT_SM_F32: return (const void*)gfb::gfb_dot_small_m_kernel<float>;
+        case GFB_K_DOT_SM_F64: return (const void*)gfb::gfb_dot_small_m_kernel<double>;
         case GFB_K_CONV_F32: return (const void*)gfb::gfb_conv_kernel<float>;
         case GFB_K_CONV_F64: return (const void*)gfb::gfb_conv_kernel<double>;
     }

@@ -16,7 +16,7 @@ from paper_1801_08058_b200 import abi
 from paper_1801_08058_b200.compiler import decode_flat
 
 DT = {abi.K_EWS_F32: np.float32, abi.K_EWS_F64: np.float64, abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
-      abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
+      abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_DOT_SM_F32: np.float32, abi.K_DOT_SM_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
 
 
 def _fdiv(n, mul, sh):
@@ -313,6 +313,35 @@ def run_tc(mem, a):
         C[base + off] = c
 
 
+def run_tcg(mem, a):
+    """gfb_conv_tcg_kernel: gather A rows (n, y, x) x k = (r, s, c) from the
+    channel-contiguous activation, split it like the kernel, contract with
+    the B planes."""
+    src = mem.view(a.a, np.float32)
+    M, K, C = a.M, a.K, 32 * a.CB
+    row = np.arange(M, dtype=np.int64)
+    n, rem = row // (a.Y * a.X), row % (a.Y * a.X)
+    h0 = (rem // a.X) * a.sy + a.oy
+    w0 = (rem % a.X) * a.sx + a.ox
+    k = np.arange(K, dtype=np.int64)
+    c, rs = k % C, k // C
+    dh, dw = a.ksign * (rs // a.S), a.ksign * (rs % a.S)
+    h = h0[:, None] + dh[None, :]
+    w = w0[:, None] + dw[None, :]
+    ok = (h >= 0) & (h < a.H) & (w >= 0) & (w < a.W)
+    off = n[:, None] * a.xs0 + h * a.xs2 + w * a.xs3 + c[None, :]
+    x = np.where(ok, src[np.where(ok, off, 0)], np.float32(0)).astype(np.float32)
+    ahi = _rna_tf32(x)
+    alo = _rna_tf32((x - ahi).astype(np.float32))
+    bhi = mem.view(a.b_hi, np.float32)[: a.N * K].reshape(a.N, K).astype(np.float64)
+    blo = mem.view(a.b_lo, np.float32)[: a.N * K].reshape(a.N, K).astype(np.float64)
+    ahi, alo = ahi.astype(np.float64), alo.astype(np.float64)
+    out = (ahi @ bhi.T + ahi @ blo.T + alo @ bhi.T).astype(np.float32)
+    i = row[:, None]
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    mem.view(a.c, np.float32)[(i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn] = out
+
+
 STAGED_U = 2  # csrc/ew_vm.cu StagedCfg<T, 2>
 
 
@@ -320,7 +349,7 @@ def _run_launch(mem, L):
     dt = DT.get(L.kind)
     if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8, abi.K_EWS_F32, abi.K_EWS_F64):
         run_ew(mem, L.args, dt)
-    elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64):
+    elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64, abi.K_DOT_SM_F32, abi.K_DOT_SM_F64):
         run_dot(mem, L.args, dt)
     elif L.kind in (abi.K_CONV_F32, abi.K_CONV_F64):
         run_conv(mem, L.args, dt)
@@ -328,6 +357,8 @@ def _run_launch(mem, L):
         run_split(mem, L.args)
     elif L.kind in (abi.K_DOT_TC32, abi.K_DOT_TC32W):
         run_tc(mem, L.args)
+    elif L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128):
+        run_tcg(mem, L.args)
     else:
         raise NotImplementedError(L.kind)
 
@@ -369,17 +400,5 @@ def execute(lowered, inputs: list, out_specs: list) -> list:
     outputs = [np.zeros(max(c, 1), dtype=d) for d, c in out_specs]
     mem = Memory(lowered, [np.ascontiguousarray(x).reshape(-1) for x in inputs], outputs)
     for L in lowered.launches:
-        dt = DT.get(L.kind)
-        if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8, abi.K_EWS_F32, abi.K_EWS_F64):
-            run_ew(mem, L.args, dt)
-        elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64):
-            run_dot(mem, L.args, dt)
-        elif L.kind in (abi.K_CONV_F32, abi.K_CONV_F64):
-            run_conv(mem, L.args, dt)
-        elif L.kind == abi.K_SPLIT_TF32:
-            run_split(mem, L.args)
-        elif L.kind == abi.K_DOT_TC32:
-            run_tc(mem, L.args)
-        else:
-            raise NotImplementedError(L.kind)
+        _run_launch(mem, L)
     return [o[:c] for o, (_, c) in zip(outputs, out_specs)]

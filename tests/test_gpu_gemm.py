@@ -44,6 +44,31 @@ def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
     assert err <= 1e-5, err
 
 
+@pytest.mark.parametrize("m,k,n,ta,tb,et", [
+    (1, 4, 5000, False, False, "F32"),
+    (4, 1, 3001, False, False, "F32"),
+    (8, 9, 700, True, False, "F32"),
+    (3, 17, 1025, False, True, "F64"),
+])
+def test_small_m_dot_bit_exact(m, k, n, ta, tb, et):
+    """Few-row Dots (the maxpool one-hot selections) take the thread-per-
+    column SIMT kernel and keep the reference k order: bit-exact."""
+    et = getattr(gf.ElementType, et)
+    fn = gf.Function("dot")
+    a = fn.add_parameter(et, (k, m) if ta else (m, k))
+    b = fn.add_parameter(et, (n, k) if tb else (k, n))
+    x = fn.add_node(K.RESHAPE, [a], {"input_order": (1, 0), "output_shape": (m, k)}) if ta else a
+    y = fn.add_node(K.RESHAPE, [b], {"input_order": (1, 0), "output_shape": (k, n)}) if tb else b
+    fn.set_results([fn.add_node(K.DOT, [x, y])])
+    rng = np.random.default_rng(m + k + n)
+    dt = et.numpy_dtype
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(dt) for p in fn.parameters]
+    exe = gf.compile_function(fn)
+    assert any(L.kind in (15, 16) for L in exe.lowered.launches)
+    out = gf.call(exe, [gf.tensor_from_flat(et, v.shape, v) for v in ins])[0].to_numpy()
+    assert G.same_bits(out, interp.run_function(fn, ins)[0])
+
+
 def test_tc_dot_large_config_E_layer():
     fn = _dot_graph(2048, 4096, 4096)
     rng = np.random.default_rng(0)
@@ -73,6 +98,33 @@ def test_conv_tensor_cores_match_oracle(monkeypatch, op, shape, stride, pad, lay
     exe = gf.compile_function(fn, conv_layout=layout) if op == "fwd" else gf.compile_function(fn)
     assert any("_tc#" in L.label for L in exe.lowered.launches)
     rng = np.random.default_rng(7)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = gf.call(exe, tens)[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("op,shape,stride,pad", [
+    ("fwd", (4, 32, 64, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (2, 64, 96, 33, 31, 3, 3), (2, 2), (1, 1, 1, 1)),
+    ("fwd", (3, 128, 256, 14, 14, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (2, 64, 128, 28, 28, 1, 1), (2, 2), (0, 0, 0, 0)),
+    ("dgrad", (4, 40, 64, 16, 15, 3, 3), (1, 1), (1, 0, 0, 1)),
+    ("dgrad", (2, 64, 128, 28, 28, 3, 3), (1, 1), (1, 1, 1, 1)),
+])
+def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
+    """gfb_conv_tcg_kernel (in-kernel NHWC gather + TF32 split) vs the oracle."""
+    import test_lowering as TL
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, Ko, H, W, R, S = shape
+    fn = TL._conv_graph(op, N, C, Ko, H, W, R, S, stride, pad)
+    nhwc = gf.Layout((0, 2, 3, 1))
+    exe = gf.compile_function(fn, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc][: len(fn.parameters)])
+    assert any(L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128) for L in exe.lowered.launches)
+    rng = np.random.default_rng(11)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
     out = gf.call(exe, tens)[0].to_numpy()

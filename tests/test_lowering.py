@@ -156,6 +156,35 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
 
 
+@pytest.mark.parametrize("op,shape,stride,pad", [
+    ("fwd", (2, 32, 64, 8, 9, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (2, 64, 96, 9, 9, 3, 3), (2, 2), (1, 1, 1, 1)),
+    ("fwd", (1, 32, 64, 7, 7, 1, 1), (2, 2), (0, 0, 0, 0)),
+    ("dgrad", (2, 40, 64, 8, 7, 3, 3), (1, 1), (1, 0, 0, 1)),
+    ("dgrad", (2, 16, 128, 6, 6, 3, 3), (1, 1), (1, 1, 1, 1)),
+])
+def test_conv_fused_gather_emulated(monkeypatch, op, shape, stride, pad):
+    """NHWC convolutions whose gathered channels come in whole 32-blocks take
+    gfb_conv_tcg_kernel (gather + split inside the GEMM): no im2col planes."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, K, H, W, R, S = shape
+    fn = _conv_graph(op, N, C, K, H, W, R, S, stride, pad)
+    nhwc = (0, 2, 3, 1)
+    h = host_compile(fn, optimize=False, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc][: len(fn.parameters)])
+    kinds = [L.kind for L in h.lowered.launches]
+    assert abi.K_CONV_TCG64 in kinds or abi.K_CONV_TCG128 in kinds, [L.label for L in h.lowered.launches]
+    assert not any(L.label.startswith("split_a") for L in h.lowered.launches)
+    rng = np.random.default_rng(9)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = emulate(h, tens)[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
 def test_resnet_nhwc_layout_assignment_emulated():
     """Config D at reduced size under conv_layout='nhwc': conversions are
     inserted by layout assignment and fused away as index maps."""
