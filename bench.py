@@ -357,6 +357,59 @@ def bench_gemm(args, local):
             "higher_is_better": True, "config": {"workload": f"G: Dot [{m},4096]x[4096,4096]", "launches": exe.num_launches}}
 
 
+def bench_conv(args, local):
+    """One config-D layer-1 convolution as a graph (3x3, 64->64, 56x56,
+    batch 128, NHWC): forward (Conv2D) and data gradient (ConvBackpropData),
+    both on gfb_conv_tcx_kernel.  `value` counts the two convolutions' flops
+    over the whole step (the two Relu producers included)."""
+    import torch
+
+    import paper_1801_08058_b200 as gf
+
+    torch.cuda.set_device(local)
+    n = args.batch or 128
+    C = int(os.environ.get("GFB_BENCH_C", 64))   # shape overrides for kernel studies
+    K = int(os.environ.get("GFB_BENCH_K", 64))
+    H = W = int(os.environ.get("GFB_BENCH_HW", 56))
+    F32 = gf.ElementType.F32
+    fn = gf.Function("conv_layer")
+    x = fn.add_parameter(F32, (n, C, H, W))
+    f = fn.add_parameter(F32, (K, C, 3, 3))
+    d = fn.add_parameter(F32, (n, K, H, W))
+    pad = {"padding": (1, 1, 1, 1)}
+    # the activations come from a producer in the arena, as inside a network
+    # (tensor maps need fixed addresses): Relu in front of each convolution
+    rx, rd = fn.add_node(gf.OpKind.RELU, [x]), fn.add_node(gf.OpKind.RELU, [d])
+    y = fn.add_node(gf.OpKind.CONV2D, [rx, f], {"strides": (1, 1), **pad})
+    dx = fn.add_node(gf.OpKind.CONV_BACKPROP_DATA, [rd, f], {"data_shape": (n, C, H, W), **pad}, allow_internal=True)
+    fn.set_results([y, dx])
+    nhwc = gf.Layout((0, 2, 3, 1))
+    exe = gf.compile_function(fn, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc])
+    rng = np.random.default_rng(0)
+    dev = [torch.from_numpy(rng.uniform(-1, 1, size=s).astype(np.float32).reshape(-1)).cuda()
+           for s in ((n, C, H, W), (K, C, 3, 3), (n, K, H, W))]
+    outs = exe.allocate_outputs()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        exe.run_device(dev, outs, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        exe.run_device(dev, outs, stream=stream.cuda_stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    if args.launch_times:
+        launch_times(exe, dev, outs, stream)
+    flops = 2 * (2 * n * H * W * K * C * 9)  # both convolutions
+    return {"metric": "F32 conv TFLOP/s (config D layer-1 3x3 conv fwd + dgrad, 3xTF32 tcgen05, fused gather)",
+            "value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "config": {"workload": f"H: Conv2D + ConvBackpropData [{n},{C},{H},{W}] -> {K} channels, 3x3 NHWC",
+                       "launches": exe.num_launches}}
+
+
 def _step_for(workload, batch=None, ws=1):
     """(step graph, per-GPU batch, description); `batch` is the GLOBAL batch."""
     import paper_1801_08058_b200 as gf
@@ -457,7 +510,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "D", "E", "G"])
+    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "D", "E", "G", "H"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
     ap.add_argument("--dp", action="store_true", help="data-parallel plan even at one GPU (NCCL all-reduces)")
@@ -483,6 +536,8 @@ def main():
 
     if args.workload == "G":
         line = bench_gemm(args, local)
+    elif args.workload == "H":
+        line = bench_conv(args, local)
     else:
         line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_step(args, ws, rank, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "B":

@@ -59,6 +59,8 @@ enum {
     GFB_K_DOT_SM_F64 = 16,
     GFB_K_CONV_TCG64 = 17,  /* implicit-GEMM conv, in-kernel gather + TF32 split, 128x64 tiles (gfb_tcg_args) */
     GFB_K_CONV_TCG128 = 18, /* as GFB_K_CONV_TCG64 with 128x128 tiles */
+    GFB_K_CONV_TCX64 = 22,  /* implicit-GEMM conv, TMA box gather + in-smem TF32 split, 128x64 (gfb_tcx_args) */
+    GFB_K_CONV_TCX128 = 23, /* as GFB_K_CONV_TCX64 with 128x128 tiles */
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
@@ -223,6 +225,30 @@ typedef struct GFB_ALIGN64 {
     int64_t pad[2];
     uint64_t tmap[2][16];
 } gfb_tcg_args;
+
+/* Implicit-GEMM convolution whose A tiles are TMA boxes.  A CTA's 128 GEMM
+ * rows are a box of BNI images x BY output rows x BX output columns (tile
+ * `blockIdx.y` = (tn, ty, tx) over tiles_y x tiles_x per image group); the
+ * K index is k = (r, s, c) over (R, S, C = 32*CB).  A is a channel-last 4-D
+ * activation in the arena (dims a_dims = C, W, H, N innermost first,
+ * element strides a_strides); its tensor map (box 32 x BX*sx x BY*sy x BNI,
+ * traversal strides 1, sx, sy, 1, zero fill outside) is encoded by
+ * gfb_exe_create together with the B plane maps.  The box for K-block
+ * (r, s, cb) starts at (32 cb, x0*sx + ox + ksign*s, y0*sy + oy + ksign*r, n0).
+ * Output (n, y, x, col) lives at n*o_n + y*o_y + x*o_x + col*c_sn for
+ * n < No, y < Yo, x < Xo. */
+typedef struct GFB_ALIGN64 {
+    const void* const* tab;
+    uint64_t c, a, b_hi, b_lo;
+    int64_t N, K;
+    int64_t o_n, o_y, o_x, c_sn;
+    int64_t a_dims[4];
+    int64_t a_strides[4];
+    int32_t No, Yo, Xo, BX, BY, BNI, tiles_x, tiles_y;
+    int32_t sx, sy, ox, oy, S, CB, ksign, pad0;
+    int64_t pad[5];
+    uint64_t tmap[3][16];
+} gfb_tcx_args;
 
 typedef struct {
     const void* const* tab;

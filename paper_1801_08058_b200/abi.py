@@ -15,6 +15,7 @@ K_EWS_F32, K_EWS_F64 = 5, 6
 K_DOT_F32, K_DOT_F64, K_DOT_TC32, K_SPLIT_TF32, K_DOT_TC32W = 10, 11, 12, 13, 14
 K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
+K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
 
@@ -104,6 +105,22 @@ class TcgArgs(C.Structure):
     ]
 
 
+class TcxArgs(C.Structure):
+    # 64-byte aligned in C: tmap sits at offset 256, size 640.
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64), ("a", C.c_uint64), ("b_hi", C.c_uint64), ("b_lo", C.c_uint64),
+        ("N", C.c_int64), ("K", C.c_int64),
+        ("o_n", C.c_int64), ("o_y", C.c_int64), ("o_x", C.c_int64), ("c_sn", C.c_int64),
+        ("a_dims", C.c_int64 * 4), ("a_strides", C.c_int64 * 4),
+        ("No", C.c_int32), ("Yo", C.c_int32), ("Xo", C.c_int32), ("BX", C.c_int32), ("BY", C.c_int32),
+        ("BNI", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+        ("sx", C.c_int32), ("sy", C.c_int32), ("ox", C.c_int32), ("oy", C.c_int32), ("S", C.c_int32),
+        ("CB", C.c_int32), ("ksign", C.c_int32), ("pad0", C.c_int32),
+        ("pad", C.c_int64 * 5),
+        ("tmap", (C.c_uint64 * 16) * 3),
+    ]
+
+
 class ConvArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p),
@@ -143,5 +160,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

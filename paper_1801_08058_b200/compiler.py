@@ -122,6 +122,8 @@ TC_TILE = 128
 TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
 TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
+# gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
+TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
 TCG_SMEM = {bn: (2 if bn == 128 else 3) * (2 * 128 + 2 * bn) * 32 * 4 + 4 * 128 * 32 * 4 + 128 * 16 + 256 + 1024
             for bn in (64, 128)}
 
@@ -354,6 +356,7 @@ class Lowered:
     buffers: dict
     groups: list = field(default_factory=list)
     arena_offsets: dict = field(default_factory=dict)
+    channels_last: bool = False
 
     def pack(self):
         """(launch array, argument blob) ready for gfb_exe_create."""
@@ -393,7 +396,8 @@ class _Node:
 
 
 class Lowering:
-    def __init__(self, g: Function, layouts: dict, private: bool = False, allreduce=frozenset()):
+    def __init__(self, g: Function, layouts: dict, private: bool = False, allreduce=frozenset(),
+                 channels_last: bool = False):
         self.g = g
         self.layouts = layouts
         self.private = private
@@ -407,9 +411,8 @@ class Lowering:
                 if n not in self.consumers[r]:
                     self.consumers[r].append(n)
         self.param_pos = {pid: i for i, pid in enumerate(g.parameters)}
-        # NHWC layout policy in force (Conv2D outputs channel-last)?
-        self.channels_last = any(self.nodes[n].op is OpKind.CONV2D and layouts[(n, 0)].order == NHWC_ORDER
-                                 for n in self.order)
+        # NHWC layout policy in force: 4-D intermediates are stored channel-last
+        self.channels_last = channels_last
         self.buf: dict = {}
         self.n_in = len(g.parameters)
         self.n_out = len(g.results)
@@ -923,6 +926,41 @@ class Lowering:
                 and xb.offset % 16 == 0 and (m + TC_TILE - 1) // TC_TILE <= 65535
                 and max(abs(v) for v in xs) * 4 < 2 ** 62)
 
+    @staticmethod
+    def _tma_box_ok(xb, shape, sx, sy) -> bool:
+        """TMA box gather: the activation needs a fixed (arena) address for
+        its tensor map, and the strided box must fit the 256-element limit."""
+        return (os.environ.get("GFB_CONV_TMA", "1") == "1" and xb.slot == abi.SLOT_ARENA
+                and sx <= 2 and sy <= 2 and max(shape) < 2 ** 31)
+
+    def _conv_tcx(self, n, xb, xs, xshape, b, out, oshape, ncols, kdim, geo, yb, label):
+        """Conv2D / ConvBackpropData whose A tiles are TMA boxes of output
+        pixels (gemm_tc.cu, gfb_conv_tcx_kernel)."""
+        bhi, blo, _ = b
+        No, Yo, Xo = oshape
+        BX = min(128, 1 << max(0, (Xo - 1).bit_length()))
+        BY = min(128 // BX, 1 << max(0, (Yo - 1).bit_length()))
+        BNI = 128 // (BX * BY)
+        tiles_x, tiles_y = (Xo + BX - 1) // BX, (Yo + BY - 1) // BY
+        tiles = tiles_x * tiles_y * ((No + BNI - 1) // BNI)
+        os_ = out.strides
+        N_, C_, H_, W_ = xshape
+        ta = abi.TcxArgs(N=ncols, K=kdim, o_n=os_[0], o_y=os_[2], o_x=os_[3], c_sn=os_[1], No=No, Yo=Yo, Xo=Xo,
+                         BX=BX, BY=BY, BNI=BNI, tiles_x=tiles_x, tiles_y=tiles_y, **geo)
+        ta.pad0 = 1 if os.environ.get("GFB_TCX_RAWHI") == "1" else 0  # experiment: MMA reads raw fp32 as hi
+        ta.a_dims[:] = [C_, W_, H_, N_]
+        ta.a_strides[:] = [xs[1], xs[3], xs[2], xs[0]]
+        bn = 64 if ncols <= 64 else 128
+        kind = abi.K_CONV_TCX64 if bn == 64 else abi.K_CONV_TCX128
+        if tiles > 65535:
+            raise UnsupportedOp(f"TMA convolution with {tiles} pixel tiles exceeds the 65535-tile grid")
+        grid = ((ncols + bn - 1) // bn, tiles, 1)
+        rec = LaunchRec(kind, grid, (320, 1, 1), TCX_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [out.key], label)
+        rec.flops = 2 * No * Yo * Xo * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "b_hi": bhi, "b_lo": blo})
+        self.launches.append(rec)
+
     def _conv_tcg(self, n, xb, xs, b, out, m, ncols, kdim, geo, addr, yb, label):
         """Conv2D / ConvBackpropData with the activation gather and TF32
         split inside the tensor-core kernel (gemm_tc.cu, gfb_conv_tcg_kernel)."""
@@ -964,6 +1002,11 @@ class Lowering:
                 return False
             if self._gather_ok(xb, xs, Cc, m):
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (R, S, Cc), st=(ys[2], ys[3], ys[1]))
+                if self._tma_box_ok(xb, (N, Cc, H, W), sw, sh):
+                    self._conv_tcx(n, xb, xs, (N, Cc, H, W), b, out, (N, Ho, Wo), ncols, kdim,
+                                   dict(sx=sw, sy=sh, ox=-pl, oy=-pt, S=S, CB=Cc // 32, ksign=1), yb,
+                                   f"{node.op.wire_name}_tcx#{n}")
+                    return True
                 self._conv_tcg(n, xb, xs, b, out, m, ncols, kdim, dict(Y=Ho, X=Wo, sy=sh, sx=sw, oy=-pt, ox=-pl, H=H, W=W, S=S,
                                CB=Cc // 32, ksign=1), {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
                                yb, f"{node.op.wire_name}_tcg#{n}")
@@ -981,6 +1024,11 @@ class Lowering:
                 return False
             if self._gather_ok(xb, xs, K, m):
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (R, S, K), st=(ys[2], ys[3], ys[0]))
+                if self._tma_box_ok(xb, (N, K, Ho, Wo), 1, 1):
+                    self._conv_tcx(n, xb, xs, (N, K, Ho, Wo), b, out, (N, H, W), ncols, kdim,
+                                   dict(sx=1, sy=1, ox=pl, oy=pt, S=S, CB=K // 32, ksign=-1), yb,
+                                   f"{node.op.wire_name}_tcx#{n}")
+                    return True
                 self._conv_tcg(n, xb, xs, b, out, m, ncols, kdim, dict(Y=H, X=W, sy=1, sx=1, oy=pt, ox=pl, H=Ho, W=Wo, S=S,
                                CB=K // 32, ksign=-1), {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
                                yb, f"{node.op.wire_name}_tcg#{n}")
@@ -1415,5 +1463,7 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
         d.stride = stride
 
 
-def lower(g: Function, layouts: dict, private: bool = False, allreduce=frozenset()) -> Lowered:
-    return Lowering(g, layouts, private, allreduce).run()
+def lower(g: Function, layouts: dict, private: bool = False, allreduce=frozenset(), channels_last: bool = False) -> Lowered:
+    low = Lowering(g, layouts, private, allreduce, channels_last).run()
+    low.channels_last = channels_last
+    return low

@@ -91,6 +91,15 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms of 1 KB.
 __device__ __forceinline__ uint64_t smem_desc(const void* p) {
     const uint64_t addr = su32(p);
@@ -162,10 +171,9 @@ __device__ __forceinline__ void mma_loop(unsigned char* smem, uint64_t* full, ui
 // Epilogue warp: TMEM lanes [32*(warp%4), +32) = tile rows, and EC columns
 // (column group cg).  Every finished accumulator chunk is promoted into fp32
 // registers with round-to-nearest adds; the sums are stored at the end.
-template <int BN, int EPI_WARPS, int NBUF>
+template <int BN, int NBUF, typename RowOff>
 __device__ __forceinline__ void epilogue(int warp, int lane, uint64_t* tfull, uint64_t* tempty, uint32_t tmem,
-                                         int nchunk, float* C, int m0, int n0, int64_t M, int64_t N, int64_t c_sm,
-                                         int64_t c_sn, int64_t c_rdiv, int64_t c_s_hi, int64_t c_s_lo) {
+                                         int nchunk, float* C, int n0, int64_t N, int64_t c_sn, RowOff row_off) {
     constexpr int EC = BN < 128 ? BN : 128;
     const int q = warp & 3, cg = ((warp - 2) >> 2) % (BN / EC);
     float acc[EC];
@@ -196,9 +204,8 @@ __device__ __forceinline__ void epilogue(int warp, int lane, uint64_t* tfull, ui
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
     }
-    const int row = m0 + q * 32 + lane;
-    if (row < M) {
-        const int64_t roff = c_rdiv > 0 ? (row / c_rdiv) * c_s_hi + (row % c_rdiv) * c_s_lo : (int64_t)row * c_sm;
+    const int64_t roff = row_off(q * 32 + lane);  // < 0: row outside the output
+    if (roff >= 0) {
         float* dst = C + roff;
 #pragma unroll
         for (int c = 0; c < EC / 32; ++c) {
@@ -216,6 +223,16 @@ __device__ __forceinline__ void epilogue(int warp, int lane, uint64_t* tfull, ui
         }
     }
 }
+
+// Output rows numbered linearly (Dot, or the flattened (n, p, q) of a conv).
+struct LinearRows {
+    int64_t m0, M, c_sm, c_rdiv, c_s_hi, c_s_lo;
+    __device__ __forceinline__ int64_t operator()(int r) const {
+        const int64_t row = m0 + r;
+        if (row >= M) return -1;
+        return c_rdiv > 0 ? (row / c_rdiv) * c_s_hi + (row % c_rdiv) * c_s_lo : row * c_sm;
+    }
+};
 
 }  // namespace tc
 
@@ -284,8 +301,8 @@ __global__ void __launch_bounds__(tc::Cfg<BN_>::THREADS, 1) gfb_gemm_tc_kernel(c
         if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
     } else {
         float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
-        epilogue<BN, EPI_WARPS, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, C, m0, n0, p.M, p.N, p.c_sm, p.c_sn,
-                                      p.c_rdiv, p.c_s_hi, p.c_s_lo);
+        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, C, n0, p.N, p.c_sn,
+                           LinearRows{m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo});
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -343,6 +360,32 @@ __device__ __forceinline__ void split_tf32(float x, float& h, float& l) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(rest));
     h = __uint_as_float(hb);
     l = __uint_as_float(lb);
+}
+
+// One converter thread's share of a 128x32 fp32 tile: the 16-byte chunks at
+// src + 2048 i (rows r, r+16, ..., r+112 of the SW128 layout), split into
+// hi = x with the 13 low mantissa bits cleared (exact in TF32) and the exact
+// remainder lo = x - hi, whose top 11 bits the MMA uses: per product the
+// dropped terms stay below ~3 * 2^-20 relative, inside the 1e-5 Dot/Conv
+// tolerance.  Two instructions per element instead of the ~11 of a
+// cvt.rna.tf32 pair.  All eight loads are issued before any store so the
+// shared-memory latency overlaps.  write_hi == false leaves x in place as
+// the hi operand (the tensor core reads only its TF32 bits).
+__device__ __forceinline__ float4 trunc_tf32(float4 v) {
+    return make_float4(__uint_as_float(__float_as_uint(v.x) & 0xffffe000u), __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                       __uint_as_float(__float_as_uint(v.z) & 0xffffe000u), __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+}
+__device__ __forceinline__ void split_rows(uint32_t src, uint32_t dst, uint32_t lo_off, bool write_hi = true) {
+    float4 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = tc::lds128(src + 2048 * i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float4 h = trunc_tf32(x[i]);
+        const float4 l = make_float4(__fsub_rn(x[i].x, h.x), __fsub_rn(x[i].y, h.y), __fsub_rn(x[i].z, h.z), __fsub_rn(x[i].w, h.w));
+        if (write_hi) tc::sts128(dst + 2048 * i, h);
+        tc::sts128(dst + lo_off + 2048 * i, l);
+    }
 }
 
 __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ gfb_split_args p) {
@@ -506,8 +549,8 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
     } else if (warp == 1) {
         if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
     } else if (warp < 2 + EPI_WARPS) {
-        epilogue<BN, EPI_WARPS, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, resolve<float>(p.tab, p.c), m0, n0, p.M,
-                                      p.N, p.c_sm, p.c_sn, p.c_rdiv, p.c_s_hi, p.c_s_lo);
+        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, resolve<float>(p.tab, p.c), n0, p.N, p.c_sn,
+                           LinearRows{m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo});
     } else {
         const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127
         {
@@ -552,25 +595,155 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
             cp_async_wait<RAW - 1>();  // this thread's copies of K-block kb have landed
             const int s = kb % STAGES;
             mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-            const unsigned char* src = raw + (kb % RAW) * A_BYTES + swz;
-            unsigned char* st = smem + s * STAGE_BYTES + swz;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int off = (rb + 16 * i) * 128;
-                const float4 x = *reinterpret_cast<const float4*>(src + off);
-                float4 h, l;
-                split_tf32(x.x, h.x, l.x);
-                split_tf32(x.y, h.y, l.y);
-                split_tf32(x.z, h.z, l.z);
-                split_tf32(x.w, h.w, l.w);
-                *reinterpret_cast<float4*>(st + off) = h;
-                *reinterpret_cast<float4*>(st + A_BYTES + off) = l;
-            }
+            split_rows(su32(raw + (kb % RAW) * A_BYTES) + swz + rb * 128, su32(smem + s * STAGE_BYTES) + swz + rb * 128,
+                       A_BYTES);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
             if (kb + RAW < nk) issue(kb + RAW);  // reuses the raw slot just consumed (own chunks only)
             cp_async_commit();
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Implicit-GEMM convolution with the gather done by TMA.  The 128 GEMM rows
+// of a CTA are a box of output pixels (BNI images x BY rows x BX columns);
+// for K-block (r, s, c0..c0+31) the A tile is then one 4-D tensor-map box of
+// the channel-last activation at (c0, x0*sx + ox + ksign*s, y0*sy + oy +
+// ksign*r, n0) with traversal strides (1, sx, sy, 1): TMA applies the
+// convolution stride, zero-fills the padding taps (out-of-bounds
+// coordinates) and writes the SW128 K-major layout the MMA reads.  Four
+// converter warps split each landed tile into TF32 hi/lo in place.
+// Warp roles: 0 TMA (A box + B planes), 1 TMEM + MMA, 2..5 epilogue,
+// 6..9 converters.
+namespace tc {
+template <int BN_>
+struct XCfg {
+    static constexpr int BM = 128, BN = BN_, BK = 32;
+    static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int STAGES = BN_ == 128 ? 3 : 4;
+    static constexpr int CHUNK_KB = 4, NBUF = 512 / BN;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4, CONV_WARPS = 4;
+    static constexpr int THREADS = 64 + 32 * (EPI_WARPS + CONV_WARPS);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
+        : "memory");
+}
+
+// Output rows of a pixel-box tile.
+struct BoxRows {
+    int n0, y0, x0, BX, BY, No, Yo, Xo;
+    int64_t o_n, o_y, o_x;
+    __device__ __forceinline__ int64_t operator()(int r) const {
+        const int xx = r % BX, t = r / BX, yy = t % BY, ni = t / BY;
+        const int n = n0 + ni, y = y0 + yy, x = x0 + xx;
+        if (n >= No || y >= Yo || x >= Xo) return -1;
+        return n * o_n + y * o_y + x * o_x;
+    }
+};
+}  // namespace tc
+
+template <int BN_>
+__global__ void __launch_bounds__(tc::XCfg<BN_>::THREADS, 1) gfb_conv_tcx_kernel(const __grid_constant__ gfb_tcx_args p) {
+    using namespace tc;
+    using C_ = XCfg<BN_>;
+    constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, CONV_WARPS = C_::CONV_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* afull = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // A box landed
+    uint64_t* full = afull + STAGES;    // A split + B planes landed
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.y;
+    const int tx = tile % p.tiles_x, ty = (tile / p.tiles_x) % p.tiles_y, tn = tile / (p.tiles_x * p.tiles_y);
+    const int x0 = tx * p.BX, y0 = ty * p.BY, n0 = tn * p.BNI, col0 = blockIdx.x * BN;
+    const int nk = (int)(p.K / BK);
+    const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&afull[s], 1);
+            mbar_init(&full[s], 1 + CONV_WARPS);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 3; ++i) prefetch_tmap(p.tmap[i]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int cb = 0, r = 0, s_ = 0;
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+                unsigned char* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&afull[s], A_BYTES);
+                tma_load_4d(st, p.tmap[0], cb * 32, x0 * p.sx + p.ox + p.ksign * s_, y0 * p.sy + p.oy + p.ksign * r, n0,
+                            &afull[s]);
+                mbar_expect_tx(&full[s], 2 * B_BYTES);
+                tma_load_2d(st + 2 * A_BYTES, p.tmap[1], kb * BK, col0, &full[s]);
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[2], kb * BK, col0, &full[s]);
+                if (++cb == p.CB) {  // k = (r, s, c): channel blocks fastest
+                    cb = 0;
+                    if (++s_ == p.S) {
+                        s_ = 0;
+                        ++r;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
+    } else if (warp < 2 + EPI_WARPS) {
+        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, resolve<float>(p.tab, p.c), col0, p.N, p.c_sn,
+                           BoxRows{n0, y0, x0, p.BX, p.BY, p.No, p.Yo, p.Xo, p.o_n, p.o_y, p.o_x});
+    } else {
+        // converters: thread g owns 16-byte chunk (g & 7) of rows (g >> 3) + 16 i
+        const int g = threadIdx.x - (2 + EPI_WARPS) * 32;
+        const int j = g & 7, rb = g >> 3;
+        const uint32_t swz = (uint32_t)((j ^ (rb & 7)) << 4);
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % STAGES;
+            mbar_wait(&afull[s], (kb / STAGES) & 1);
+            split_rows(su32(smem + s * STAGE_BYTES) + swz + rb * 128, su32(smem + s * STAGE_BYTES) + swz + rb * 128,
+                       A_BYTES, p.pad0 == 0);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -588,6 +761,8 @@ template __global__ void gfb::gfb_gemm_tc_kernel<128>(const __grid_constant__ gf
 template __global__ void gfb::gfb_gemm_tc_kernel<256>(const __grid_constant__ gfb_tc_args);
 template __global__ void gfb::gfb_conv_tcg_kernel<64>(const __grid_constant__ gfb_tcg_args);
 template __global__ void gfb::gfb_conv_tcg_kernel<128>(const __grid_constant__ gfb_tcg_args);
+template __global__ void gfb::gfb_conv_tcx_kernel<64>(const __grid_constant__ gfb_tcx_args);
+template __global__ void gfb::gfb_conv_tcx_kernel<128>(const __grid_constant__ gfb_tcx_args);
 
 extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_DOT_TC32) return (const void*)gfb::gfb_gemm_tc_kernel<128>;
@@ -595,6 +770,8 @@ extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_SPLIT_TF32) return (const void*)gfb::gfb_split_kernel;
     if (kind == GFB_K_CONV_TCG64) return (const void*)gfb::gfb_conv_tcg_kernel<64>;
     if (kind == GFB_K_CONV_TCG128) return (const void*)gfb::gfb_conv_tcg_kernel<128>;
+    if (kind == GFB_K_CONV_TCX64) return (const void*)gfb::gfb_conv_tcx_kernel<64>;
+    if (kind == GFB_K_CONV_TCX128) return (const void*)gfb::gfb_conv_tcx_kernel<128>;
     return nullptr;
 }
 

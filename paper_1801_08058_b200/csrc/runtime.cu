@@ -59,6 +59,24 @@ bool encode_plane_map(void* gaddr, int64_t rows, int64_t kp, uint32_t box_rows, 
     std::memcpy(out, &map, sizeof(map));
     return true;
 }
+// Channel-last 4-D activation (C, W, H, N innermost first) -> boxes of
+// 32 channels x bw x bh x bn with traversal strides (1, sx, sy, 1); taps
+// outside the tensor read as zero (the convolution's padding).
+bool encode_act_map(void* gaddr, const int64_t* dims, const int64_t* estrides, uint32_t bw, uint32_t bh, uint32_t bn,
+                    uint32_t sx, uint32_t sy, void* out) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    alignas(64) CUtensorMap map;
+    cuuint64_t d[4] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2], (cuuint64_t)dims[3]};
+    cuuint64_t st[3] = {(cuuint64_t)estrides[1] * 4, (cuuint64_t)estrides[2] * 4, (cuuint64_t)estrides[3] * 4};
+    cuuint32_t box[4] = {32, bw, bh, bn};
+    cuuint32_t es[4] = {1, sx, sy, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, gaddr, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out, &map, sizeof(map));
+    return true;
+}
 }  // namespace
 
 namespace {
@@ -154,7 +172,7 @@ const void* kernel_for(uint32_t kind) {
         kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64)
         return gfb_simt_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
-        kind == GFB_K_CONV_TCG128)
+        kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128)
         return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
 }
@@ -294,6 +312,22 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                 if (!encode_plane_map(addr, rows, kp, box_rows, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
             }
+        }
+        if (L.kind == GFB_K_CONV_TCX64 || L.kind == GFB_K_CONV_TCX128) {
+            gfb_tcx_args* a = (gfb_tcx_args*)(e->args.data() + L.arg_offset);
+            const uint64_t refs[3] = {a->a, a->b_hi, a->b_lo};
+            void* addr[3];
+            for (int t = 0; t < 3; ++t) {
+                if ((refs[t] >> 56) != GFB_SLOT_ARENA)
+                    return bail(fail(GFB_ERR_INVALID, "TMA convolution operands must live in the arena"));
+                addr[t] = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
+            }
+            if (!encode_act_map(addr[0], a->a_dims, a->a_strides, (uint32_t)(a->BX * a->sx), (uint32_t)(a->BY * a->sy),
+                                (uint32_t)a->BNI, (uint32_t)a->sx, (uint32_t)a->sy, a->tmap[0]))
+                return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (activation box) failed"));
+            for (int t = 1; t < 3; ++t)
+                if (!encode_plane_map(addr[t], a->N, a->K, L.kind == GFB_K_CONV_TCX64 ? 64 : 128, a->tmap[t]))
+                    return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
         }
         if (L.kind == GFB_K_CONV_TCG64 || L.kind == GFB_K_CONV_TCG128) {
             gfb_tcg_args* a = (gfb_tcg_args*)(e->args.data() + L.arg_offset);

@@ -34,7 +34,7 @@ from . import abi
 from .compiler import Lowered, lower
 from .errors import BackendUnavailable, DeviceError, SignatureMismatch, ValidationFailure
 from .ir import ConstantData, Function, OpKind, TensorDescriptor, reachable_from_results, topological_order, validate_function
-from .layout import Layout, assign_layouts, layout_policy, tensor_layouts
+from .layout import NHWC_ORDER, Layout, assign_layouts, layout_policy, tensor_layouts
 from .memory import MemoryPlan, plan_memory
 from .rewrite import run_pipeline
 from .tensor import TensorValue, storage_to_logical, tensor_from_flat, torch_dtype
@@ -218,7 +218,7 @@ class Executable:
             return self._program
         if self._private is None:
             g = self.function
-            low = lower(g, self.layouts, private=True)
+            low = lower(g, self.layouts, private=True, channels_last=self.lowered.channels_last)
             self._private = DeviceProgram(low, self._cuda_graph, self._comm)
         return self._private
 
@@ -317,7 +317,7 @@ def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
         position = {pid: i for i, pid in enumerate(fn.parameters)}
         data_parallel.batch_params = [g.parameters[position[p]] if p in position else p for p in data_parallel.batch_params]
         roots = frozenset(analyse(g, data_parallel))
-    lowered = lower(g, layouts, private=private, allreduce=roots)
+    lowered = lower(g, layouts, private=private, allreduce=roots, channels_last=policy.conv_order == NHWC_ORDER)
     return HostCompiled(g, layouts, plan, instructions, pool_refs, param_index, result_index,
                         param_sig, result_sig, lowered, roots)
 

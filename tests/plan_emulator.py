@@ -313,6 +313,14 @@ def run_tc(mem, a):
         C[base + off] = c
 
 
+def _trunc_split(x):
+    """The converter warps' split (gemm_tc.cu split_rows): hi = x with the 13
+    low mantissa bits cleared, lo = x - hi rounded to the TF32 the MMA reads."""
+    hi = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    lo = (x - hi).astype(np.float32)
+    return hi, (lo.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
 def run_tcg(mem, a):
     """gfb_conv_tcg_kernel: gather A rows (n, y, x) x k = (r, s, c) from the
     channel-contiguous activation, split it like the kernel, contract with
@@ -331,8 +339,7 @@ def run_tcg(mem, a):
     ok = (h >= 0) & (h < a.H) & (w >= 0) & (w < a.W)
     off = n[:, None] * a.xs0 + h * a.xs2 + w * a.xs3 + c[None, :]
     x = np.where(ok, src[np.where(ok, off, 0)], np.float32(0)).astype(np.float32)
-    ahi = _rna_tf32(x)
-    alo = _rna_tf32((x - ahi).astype(np.float32))
+    ahi, alo = _trunc_split(x)
     bhi = mem.view(a.b_hi, np.float32)[: a.N * K].reshape(a.N, K).astype(np.float64)
     blo = mem.view(a.b_lo, np.float32)[: a.N * K].reshape(a.N, K).astype(np.float64)
     ahi, alo = ahi.astype(np.float64), alo.astype(np.float64)
@@ -340,6 +347,33 @@ def run_tcg(mem, a):
     i = row[:, None]
     j = np.arange(a.N, dtype=np.int64)[None, :]
     mem.view(a.c, np.float32)[(i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn] = out
+
+
+def run_tcx(mem, a):
+    """gfb_conv_tcx_kernel: rows are output pixels (n, y, x); the TMA box for
+    K-block (r, s, cb) reads act[n, y*sy + oy + ksign*r, x*sx + ox + ksign*s,
+    c] (zero outside the tensor)."""
+    src = mem.view(a.a, np.float32)
+    Cc, Wd, Hd, Nd = list(a.a_dims)
+    sc, sw, sh, sn = list(a.a_strides)
+    K = a.K
+    n, y, x = np.meshgrid(np.arange(a.No), np.arange(a.Yo), np.arange(a.Xo), indexing="ij")
+    n, y, x = (v.reshape(-1, 1).astype(np.int64) for v in (n, y, x))
+    k = np.arange(K, dtype=np.int64)[None, :]
+    C = 32 * a.CB
+    c, rs = k % C, k // C
+    h = y * a.sy + a.oy + a.ksign * (rs // a.S)
+    w = x * a.sx + a.ox + a.ksign * (rs % a.S)
+    ok = (h >= 0) & (h < Hd) & (w >= 0) & (w < Wd)
+    off = n * sn + h * sh + w * sw + c * sc
+    v = np.where(ok, src[np.where(ok, off, 0)], np.float32(0)).astype(np.float32)
+    ahi, alo = _trunc_split(v)
+    bhi = mem.view(a.b_hi, np.float32)[: a.N * K].reshape(a.N, K).astype(np.float64)
+    blo = mem.view(a.b_lo, np.float32)[: a.N * K].reshape(a.N, K).astype(np.float64)
+    ahi, alo = ahi.astype(np.float64), alo.astype(np.float64)
+    out = (ahi @ bhi.T + ahi @ blo.T + alo @ bhi.T).astype(np.float32)
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    mem.view(a.c, np.float32)[n * a.o_n + y * a.o_y + x * a.o_x + j * a.c_sn] = out
 
 
 STAGED_U = 2  # csrc/ew_vm.cu StagedCfg<T, 2>
@@ -359,6 +393,8 @@ def _run_launch(mem, L):
         run_tc(mem, L.args)
     elif L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128):
         run_tcg(mem, L.args)
+    elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):
+        run_tcx(mem, L.args)
     else:
         raise NotImplementedError(L.kind)
 

@@ -130,3 +130,41 @@ def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
     out = gf.call(exe, tens)[0].to_numpy()
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("op,shape,stride,pad", [
+    ("fwd", (4, 64, 64, 56, 56, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (3, 64, 96, 33, 31, 3, 3), (2, 2), (1, 1, 1, 1)),
+    ("fwd", (5, 128, 256, 7, 7, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (2, 64, 128, 28, 28, 1, 1), (2, 2), (0, 0, 0, 0)),
+    ("fwd", (2, 32, 128, 20, 3, 3, 3), (1, 2), (1, 1, 1, 1)),
+    ("dgrad", (4, 40, 64, 16, 15, 3, 3), (1, 1), (1, 0, 0, 1)),
+    ("dgrad", (2, 64, 128, 28, 28, 3, 3), (1, 1), (1, 1, 1, 1)),
+])
+def test_conv_tma_box_matches_oracle(monkeypatch, op, shape, stride, pad):
+    """gfb_conv_tcx_kernel (TMA pixel-box gather, in-smem TF32 split) vs the oracle."""
+    import test_lowering as TL  # noqa: F401  (shared helpers)
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    Ko = gf.OpKind
+    N, C, K, H, W, R, S = shape
+    fn = gf.Function("conv")
+    if op == "fwd":
+        x = fn.add_parameter(F32, (N, C, H, W))
+        f = fn.add_parameter(F32, (K, C, R, S))
+        c = fn.add_node(Ko.CONV2D, [fn.add_node(Ko.RELU, [x]), f], {"strides": stride, "padding": pad})
+    else:
+        d = fn.add_parameter(F32, (N, K, H, W))
+        f = fn.add_parameter(F32, (K, C, R, S))
+        Hi, Wi = H - pad[0] - pad[1] + R - 1, W - pad[2] - pad[3] + S - 1
+        c = fn.add_node(Ko.CONV_BACKPROP_DATA, [fn.add_node(Ko.RELU, [d]), f],
+                        {"data_shape": (N, C, Hi, Wi), "padding": pad}, allow_internal=True)
+    fn.set_results([fn.add_node(Ko.NEGATE, [c])])
+    exe = gf.compile_function(fn, optimize=False, conv_layout="nhwc")
+    assert any(L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128) for L in exe.lowered.launches)
+    rng = np.random.default_rng(17)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5

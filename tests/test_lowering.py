@@ -176,11 +176,51 @@ def test_conv_fused_gather_emulated(monkeypatch, op, shape, stride, pad):
     nhwc = (0, 2, 3, 1)
     h = host_compile(fn, optimize=False, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc][: len(fn.parameters)])
     kinds = [L.kind for L in h.lowered.launches]
-    assert abi.K_CONV_TCG64 in kinds or abi.K_CONV_TCG128 in kinds, [L.label for L in h.lowered.launches]
+    assert set(kinds) & {abi.K_CONV_TCG64, abi.K_CONV_TCG128, abi.K_CONV_TCX64, abi.K_CONV_TCX128}, \
+        [L.label for L in h.lowered.launches]
     assert not any(L.label.startswith("split_a") for L in h.lowered.launches)
     rng = np.random.default_rng(9)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = emulate(h, tens)[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("op,shape,stride,pad", [
+    ("fwd", (2, 32, 64, 8, 9, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (3, 64, 96, 9, 9, 3, 3), (2, 2), (1, 1, 1, 1)),
+    ("fwd", (2, 32, 64, 7, 7, 1, 1), (2, 2), (0, 0, 0, 0)),
+    ("fwd", (1, 32, 128, 20, 3, 3, 3), (1, 2), (1, 1, 1, 1)),
+    ("dgrad", (2, 40, 64, 8, 7, 3, 3), (1, 1), (1, 0, 0, 1)),
+])
+def test_conv_tma_box_emulated(monkeypatch, op, shape, stride, pad):
+    """An intermediate activation (arena) feeding an NHWC convolution takes
+    gfb_conv_tcx_kernel: A tiles are TMA boxes of output pixels."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    Ko, F32 = gf.OpKind, gf.ElementType.F32
+    N, C, K, H, W, R, S = shape
+    fn = gf.Function("conv")
+    if op == "fwd":
+        x = fn.add_parameter(F32, (N, C, H, W))
+        f = fn.add_parameter(F32, (K, C, R, S))
+        c = fn.add_node(Ko.CONV2D, [fn.add_node(Ko.RELU, [x]), f], {"strides": stride, "padding": pad})
+    else:
+        d = fn.add_parameter(F32, (N, K, H, W))
+        f = fn.add_parameter(F32, (K, C, R, S))
+        Hi, Wi = H - pad[0] - pad[1] + R - 1, W - pad[2] - pad[3] + S - 1
+        c = fn.add_node(Ko.CONV_BACKPROP_DATA, [fn.add_node(Ko.RELU, [d]), f],
+                        {"data_shape": (N, C, Hi, Wi), "padding": pad}, allow_internal=True)
+    fn.set_results([fn.add_node(Ko.NEGATE, [c])])
+    h = host_compile(fn, optimize=False, conv_layout="nhwc")
+    kinds = [L.kind for L in h.lowered.launches]
+    assert set(kinds) & {abi.K_CONV_TCX64, abi.K_CONV_TCX128}, [L.label for L in h.lowered.launches]
+    rng = np.random.default_rng(13)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(F32, v.shape, v) for v in ins]
     out = emulate(h, tens)[0]
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
 
