@@ -78,7 +78,7 @@ enum {
 
 #define GFB_MAX_LEAVES 16
 #define GFB_MAX_DIGITS 6
-#define GFB_MAX_INSTR 64
+#define GFB_MAX_INSTR 128
 
 /* One mixed-radix digit of an index map: coord = (idx / div) % mod,
  * offset += coord * stride, idx being the output (src 0) or reduced (src 1)

@@ -20,7 +20,7 @@ K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
 
 SLOT_ARENA, SLOT_CONST, SLOT_IO = 0, 1, 2
-MAX_LEAVES, MAX_DIGITS, MAX_INSTR = 16, 6, 64
+MAX_LEAVES, MAX_DIGITS, MAX_INSTR = 16, 6, 128
 PLAN_CUDA_GRAPH = 1
 
 

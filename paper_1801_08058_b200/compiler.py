@@ -56,6 +56,7 @@ NUM_SMS = 148
 HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER})
 INDEX_OPS = frozenset({OpKind.BROADCAST, OpKind.RESHAPE, OpKind.CONVERT_LAYOUT})
 MAX_STACK = 3
+TINY_DOT_K = 4  # Dots contracting over at most this many terms fuse as light ops
 MAX_PRELOAD = 4
 
 # Program construction opcodes (internal), encoded to the kernel's flat
@@ -192,6 +193,8 @@ class Buffer:
     slot: int = abi.SLOT_ARENA
     offset: int = 0
     splat: object = None  # python scalar for splat constants (no memory)
+    base: object = None   # a strided view of this Buffer (shares its storage and final offset)
+    elem_off: int = 0     # view origin, in elements from the base's origin
 
     @property
     def nbytes(self) -> int:
@@ -213,33 +216,151 @@ class Unexpressible(Exception):
     pass
 
 
+class _TooManyDigits(Exception):
+    """An operand's index map needs more than GFB_MAX_DIGITS digits."""
+
+
+class Lin:
+    """A composite axis coordinate: const + sum of mul * ((idx[src] // div) % mod).
+
+    Plain digits stay (src, div, mod) tuples; Lin appears where a Reshape
+    merges several iteration digits into one input axis (a pool window's
+    h = 2*h2 + dy) or where a coordinate is a compile-time constant (a tiny
+    Dot's contraction index)."""
+
+    __slots__ = ("terms", "const")
+
+    def __init__(self, terms=(), const=0):
+        self.terms = tuple(terms)
+        self.const = int(const)
+
+    def __repr__(self):
+        return f"Lin({self.terms}, {self.const})"
+
+
+def axis_terms(e):
+    """(terms, const) of an axis expression; terms are (src, div, mod, mul)."""
+    if e is None:
+        return (), 0
+    if isinstance(e, Lin):
+        return e.terms, e.const
+    return ((e[0], e[1], e[2], 1),), 0
+
+
+def _mk_axis(terms, const):
+    terms = tuple(t for t in terms)
+    if not terms and const == 0:
+        return None
+    if len(terms) == 1 and const == 0 and terms[0][3] == 1:
+        return terms[0][:3]
+    return Lin(terms, const)
+
+
+def _split_expr(e, dims):
+    """Coordinates over `dims` (row-major) of an out axis holding e."""
+    if e is None:
+        return [None] * len(dims)
+    if isinstance(e, Lin):
+        if e.terms:
+            if len(e.terms) == 1 and e.const == 0 and e.terms[0][3] == 1:
+                e = e.terms[0][:3]
+            else:
+                raise Unexpressible()
+        else:
+            out, c = [], e.const
+            for i, d in enumerate(dims):
+                out.append(_mk_axis((), (c // _prod(dims[i + 1:])) % d))
+            return out
+    src, div, mod = e
+    out = []
+    for i, d in enumerate(dims):
+        out.append(None if d == 1 else (src, div * _prod(dims[i + 1:]), d))
+    return out
+
+
+def _reshape_groups(out_shape, perm_dims):
+    """Minimal aligned groups (out axes, perm axes) with equal extents."""
+    groups, i, j = [], 0, 0
+    no, npm = len(out_shape), len(perm_dims)
+    while i < no or j < npm:
+        go, gp, po, pp = [], [], 1, 1
+        while True:
+            if po == pp and (go or gp):
+                # absorb trailing unit axes into this group
+                while i < no and out_shape[i] == 1:
+                    go.append(i)
+                    i += 1
+                while j < npm and perm_dims[j] == 1:
+                    gp.append(j)
+                    j += 1
+                break
+            if (po <= pp and i < no) or j >= npm:
+                po *= out_shape[i]
+                go.append(i)
+                i += 1
+            else:
+                pp *= perm_dims[j]
+                gp.append(j)
+                j += 1
+            if i >= no and j >= npm:
+                break
+        groups.append((go, gp))
+    return groups
+
+
 def through_reshape(node, out_axes) -> list:
     """Axis expressions of a Reshape's input given those of its output."""
     in_shape = node.inputs_shape
     order = node.attrs["input_order"]
-    out_shape = node.output.shape
+    out_shape = tuple(node.output.shape)
     perm_dims = tuple(in_shape[a] for a in order)
     in_axes = [None] * len(in_shape)
-    if perm_dims == tuple(out_shape):
+    if perm_dims == out_shape:
         for i, a in enumerate(order):
             in_axes[a] = out_axes[i]
         return in_axes
-    # General re-split: the output's axes must be one contiguous digit block.
-    live = [(a, e) for a, e in enumerate(out_axes) if e is not None and out_shape[a] > 1]
-    if not live:
-        return in_axes  # single element
-    srcs = {e[0] for _, e in live}
-    if len(srcs) != 1:
-        raise Unexpressible()
-    src = srcs.pop()
-    last_axis, last = live[-1]
-    base = last[1] // _prod(out_shape[last_axis + 1:])
-    for a, e in live:
-        if e[2] != out_shape[a] or e[1] != base * _prod(out_shape[a + 1:]):
+    simple = all(e is None or not isinstance(e, Lin) for e in out_axes)
+    if simple:
+        # The output's axes as one contiguous digit block re-split as a whole.
+        live = [(a, e) for a, e in enumerate(out_axes) if e is not None and out_shape[a] > 1]
+        if not live:
+            return in_axes  # single element
+        srcs = {e[0] for _, e in live}
+        ok = len(srcs) == 1
+        if ok:
+            src = srcs.pop()
+            last_axis, last = live[-1]
+            base = last[1] // _prod(out_shape[last_axis + 1:])
+            ok = all(e[2] == out_shape[a] and e[1] == base * _prod(out_shape[a + 1:]) for a, e in live)
+        if ok:
+            for i, a in enumerate(order):
+                d = perm_dims[i]
+                in_axes[a] = None if d == 1 else (src, base * _prod(perm_dims[i + 1:]), d)
+            return in_axes
+    # Aligned groups: merges become linear combinations, splits sub-digits.
+    perm_axes = [None] * len(perm_dims)
+    for go, gp in _reshape_groups(out_shape, perm_dims):
+        outs = [a for a in go if out_shape[a] > 1]
+        perms = [i for i in gp if perm_dims[i] > 1]
+        if not perms:
+            continue
+        if len(perms) == 1:
+            terms, const = [], 0
+            for a in outs:
+                w = _prod(out_shape[b] for b in outs if b > a)
+                t, c = axis_terms(out_axes[a])
+                terms += [(src, div, mod, mul * w) for src, div, mod, mul in t]
+                const += c * w
+            perm_axes[perms[0]] = _mk_axis(terms, const)
+        elif len(outs) == 1:
+            for i, e in zip(perms, _split_expr(out_axes[outs[0]], [perm_dims[i] for i in perms])):
+                perm_axes[i] = e
+        elif not outs:
+            continue
+        else:
             raise Unexpressible()
     for i, a in enumerate(order):
-        d = perm_dims[i]
-        in_axes[a] = None if d == 1 else (src, base * _prod(perm_dims[i + 1:]), d)
+        in_axes[a] = perm_axes[i]
     return in_axes
 
 
@@ -252,14 +373,32 @@ def through_index_op(node, out_axes) -> list:
     return through_reshape(node, out_axes)
 
 
+def axes_offset(buf: Buffer, axes) -> int:
+    """Element offset contributed by the constant parts of `axes`."""
+    off = 0
+    for a, e in enumerate(axes):
+        if isinstance(e, Lin) and buf.shape[a] > 1:
+            off += e.const * buf.strides[a]
+    return off
+
+
 def make_digits(buf: Buffer, axes, extents) -> list:
-    """Mixed-radix digits (src, div, mod, stride) addressing `buf` at `axes`."""
+    """Mixed-radix digits (src, div, mod, stride) addressing `buf` at `axes`
+    (constant parts excluded: see axes_offset)."""
     digs = []
     for a, e in enumerate(axes):
         if e is None or buf.strides[a] == 0 or buf.shape[a] <= 1:
             continue
-        digs.append([e[0], e[1], e[2], buf.strides[a]])
-    digs.sort(key=lambda d: (d[0], d[1]))
+        for src, div, mod, mul in axis_terms(e)[0]:
+            digs.append([src, div, mod, buf.strides[a] * mul])
+    digs.sort(key=lambda d: (d[0], d[1], d[2] or 0))
+    same = []
+    for d in digs:  # the same digit on two axes: one digit with the summed stride
+        if same and same[-1][:3] == d[:3]:
+            same[-1][3] += d[3]
+        else:
+            same.append(d)
+    digs = [d for d in same if d[3] != 0]
     merged = []
     for d in digs:
         if merged:
@@ -411,6 +550,11 @@ class Lowering:
                 if n not in self.consumers[r]:
                     self.consumers[r].append(n)
         self.param_pos = {pid: i for i, pid in enumerate(g.parameters)}
+        # Dots with a tiny contraction (the pool composite's one-hot selections
+        # [1,4]x[4,M] and their [4,1]x[1,M] gradients) are elementwise work:
+        # they fuse into VM programs as exact-order multiply-add chains.
+        self.tiny = {n for n in self.order if g.nodes[n].op is OpKind.DOT and g.nodes[n].output.element_type.is_float
+                     and g.nodes[g.nodes[n].inputs[0][0]].output.shape[1] <= TINY_DOT_K}
         # NHWC layout policy in force: 4-D intermediates are stored channel-last
         self.channels_last = channels_last
         self.buf: dict = {}
@@ -425,7 +569,11 @@ class Lowering:
 
     def is_light(self, n) -> bool:
         op = self.nodes[n].op
-        return op in ELEMENTWISE_BINARY or op in ELEMENTWISE_UNARY or op in INDEX_OPS or op is OpKind.SUM
+        return (op in ELEMENTWISE_BINARY or op in ELEMENTWISE_UNARY or op in INDEX_OPS or op is OpKind.SUM
+                or n in self.tiny)
+
+    def is_heavy(self, n) -> bool:
+        return self.nodes[n].op in HEAVY and n not in self.tiny
 
     def strides_of(self, n) -> tuple:
         return self.layouts[(n, 0)].strides(self.nodes[n].output.shape)
@@ -438,11 +586,11 @@ class Lowering:
             node = self.nodes[n]
             if not self.is_light(n):
                 continue
-            if node.op is OpKind.SUM or n in results:
+            if node.op is OpKind.SUM or n in results or n in self.allreduce:
                 M.add(n)
                 continue
             cons = self.consumers[n]
-            heavy = [c for c in cons if self.nodes[c].op in HEAVY]
+            heavy = [c for c in cons if self.is_heavy(c)]
             light = [c for c in cons if c not in heavy]
             if heavy and not self.viewable(n):
                 M.add(n)
@@ -454,7 +602,7 @@ class Lowering:
     def is_source(self, n) -> bool:
         """Materialised already: parameter, constant, heavy output or member of M."""
         op = self.nodes[n].op
-        return op in (OpKind.PARAMETER, OpKind.CONSTANT) or op in HEAVY or n in self.M
+        return op in (OpKind.PARAMETER, OpKind.CONSTANT) or self.is_heavy(n) or n in self.M
 
     def free_view(self, n) -> bool:
         """Index ops over materialised sources cost nothing to recompute."""
@@ -519,6 +667,8 @@ class Lowering:
         g = self.g
         self.buf: dict = {}
         self.launches: list = []
+        self.const_values: dict = {}  # small constants' row-major values, by buffer key
+        self._splats: dict = {}
         const_blob = bytearray()
         results = list(g.results)
         result_slot = {}  # node -> output index written directly by its producer
@@ -541,12 +691,14 @@ class Lowering:
                 if data.is_splat and self._splat_ok(n):
                     b.splat = data.splat_value()
                 else:
+                    if element_count(d.shape) <= 4096:
+                        self.const_values[b.key] = np.ascontiguousarray(data.to_numpy()).reshape(-1)
                     off = align_up(len(const_blob), DEVICE_ALIGNMENT)
                     const_blob.extend(b"\0" * (off - len(const_blob)))
                     const_blob.extend(np.ascontiguousarray(data.to_numpy()).tobytes())
                     b.offset = off
                 self.buf[n] = b
-            elif n in self.M or node.op in HEAVY:
+            elif n in self.M or self.is_heavy(n):
                 slot = abi.SLOT_ARENA
                 strides = self.strides_of(n)
                 if n in result_slot:
@@ -569,7 +721,7 @@ class Lowering:
 
         for n in self.order:
             node = self.nodes[n]
-            if node.op in HEAVY:
+            if self.is_heavy(n):
                 self.emit_heavy(n)
             elif n in self.M and n not in merged:
                 if node.op is OpKind.SUM:
@@ -604,16 +756,24 @@ class Lowering:
         return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
                        {b.key: b for b in self.buf.values()}, arena_offsets=plan.offsets)
 
+    def splat_buffer(self, et: ElementType, value) -> Buffer:
+        """A memory-less scalar operand (one per distinct bit pattern)."""
+        v = value.item() if hasattr(value, "item") else value
+        key = (et, struct.pack("<d", float(v)) if et.is_float else int(v))
+        if key not in self._splats:
+            self._splats[key] = Buffer(self.new_key(), et, (), (), abi.SLOT_CONST, 0, v)
+        return self._splats[key]
+
     def _splat_ok(self, n) -> bool:
         """Splat constants stay scalars unless a heavy op or a result reads memory."""
         results = {r for r, _ in self.g.results}
         if n in results:
             return False
         for c in self.consumers[n]:
-            if self.nodes[c].op in HEAVY:
+            if self.is_heavy(c):
                 return False
             # an index view feeding a heavy op also needs memory
-            if self.nodes[c].op in INDEX_OPS and any(self.nodes[cc].op in HEAVY for cc in self.consumers[c]):
+            if self.nodes[c].op in INDEX_OPS and any(self.is_heavy(cc) for cc in self.consumers[c]):
                 return False
         return True
 
@@ -1146,6 +1306,8 @@ def _rowmajor(shape) -> tuple:
 
 
 def _buf_ref(b: Buffer) -> int:
+    if b.base is not None:
+        return abi.ref(b.base.slot, b.base.offset + b.elem_off * b.et.byte_size)
     return abi.ref(b.slot, b.offset)
 
 
@@ -1179,6 +1341,13 @@ def _splat_bits(b: Buffer) -> int:
     return int(bool(v))
 
 
+def _dot_term_axes(node, axes, low):
+    """Operand axes of each term t of a tiny Dot at output axes (i, j)."""
+    k = low.g.nodes[node.inputs[0][0]].output.shape[1]
+    ei, ej = axes
+    return [([ei, _mk_axis((), t)], [_mk_axis((), t), ej]) for t in range(k)]
+
+
 class Program:
     def __init__(self, low: Lowering, extents, vec_src: int, et: ElementType, dry: bool = False):
         self.low = low
@@ -1191,16 +1360,29 @@ class Program:
         self.leaf_index: dict = {}
         self.code: list = []  # (cls, op, k, swap) with k = leaf spec index
         self.red_out = None
+        self.spans: dict = {}  # inlined node -> instructions it emitted
+        self._inline: set = set()
 
     # -- leaves
     def leaf(self, buf: Buffer, axes) -> int:
+        if buf.splat is None and buf.slot == abi.SLOT_CONST and self.low.const_values.get(buf.key) is not None \
+                and all(e is None or (isinstance(e, Lin) and not e.terms) for e in axes):
+            # one element of a constant at a compile-time coordinate: an immediate
+            buf = self.low.splat_buffer(buf.et, self.low.const_values[buf.key][buf.elem_off + axes_offset(buf, axes)])
         digits = make_digits(buf, axes, self.extents) if buf.splat is None else []
-        key = (buf.key, tuple(digits), False)
+        off = axes_offset(buf, axes) if buf.splat is None else 0
+        if off:
+            root = buf.base if buf.base is not None else buf
+            buf = Buffer(buf.key, buf.et, buf.shape, buf.strides, buf.slot, buf.offset, None, base=root,
+                         elem_off=buf.elem_off + off)
+        key = (buf.key, buf.elem_off, tuple(digits), False)
         if key not in self.leaf_index:
             if len(digits) > abi.MAX_DIGITS:
-                raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
+                raise _TooManyDigits()
             spec = LeafSpec(buf, digits, False)
             spec.vec = 2 if buf.splat is not None else vec_class(digits, self.vec_src, False, self.V, buf.et.byte_size)
+            if spec.vec == 1 and (buf.elem_off * buf.et.byte_size) % 16:
+                spec.vec = 0  # a constant offset breaks the vector alignment
             self.leaf_index[key] = len(self.leaf_specs)
             self.leaf_specs.append(spec)
         return self.leaf_index[key]
@@ -1221,6 +1403,25 @@ class Program:
         self.code.append((cls, op, k, swap))
 
     # -- expression evaluation
+    def view_of(self, n):
+        """A strided view Buffer for index node `n` over a materialised buffer
+        (a re-split Reshape of a row-major buffer is free even when the
+        iteration digits cannot follow it), or None."""
+        low = self.low
+        if os.environ.get("GFB_NO_VIEW"):
+            return None
+        try:
+            hv = low.heavy_operand(n)
+        except Unexpressible:
+            return None
+        if hv is None or hv[1] is None:
+            return None
+        b, st = hv
+        node = low.nodes[n]
+        root = b.base if b.base is not None else b
+        return Buffer(b.key, b.et, tuple(node.output.shape), tuple(st), b.slot, b.offset, b.splat, base=root,
+                      elem_off=b.elem_off)
+
     def need(self, n, axes) -> int:
         low = self.low
         if n in low.buf:
@@ -1230,9 +1431,19 @@ class Program:
             try:
                 return self.need(node.inputs[0][0], through_index_op(node, axes))
             except Unexpressible:
+                if self.view_of(n) is not None:
+                    return 0
                 raise _Retry(n)
         if node.op in ELEMENTWISE_UNARY:
             return self.need(node.inputs[0][0], axes)
+        if n in low.tiny:
+            a, b = node.inputs[0][0], node.inputs[1][0]
+            worst = 0
+            for t, (aa, ba) in enumerate(_dot_term_axes(node, axes, low)):
+                na, nb = self.need(a, aa), self.need(b, ba)
+                term = max(na, nb) if (self.is_plain(a, aa) or self.is_plain(b, ba)) else min(max(na, 1 + nb), max(nb, 1 + na))
+                worst = max(worst, term + (1 if t else 0))
+            return worst
         if node.op in ELEMENTWISE_BINARY:
             a, b = node.inputs[0][0], node.inputs[1][0]
             if a == b:
@@ -1248,12 +1459,30 @@ class Program:
         low = self.low
         while n not in low.buf and low.nodes[n].op in INDEX_OPS:
             node = low.nodes[n]
-            axes = through_index_op(node, axes)
+            try:
+                axes = through_index_op(node, axes)
+            except Unexpressible:
+                return self.view_of(n) is not None
             n = node.inputs[0][0]
         return n in low.buf
 
     def value(self, n, axes):
         """Emit code leaving node `n` at `axes` in acc; returns ('leaf', k) or ('acc',)."""
+        start = len(self.code)
+        r = self._value(n, axes)
+        if r[0] == "acc" and n not in self._inline:
+            self.spans[n] = max(self.spans.get(n, 0), len(self.code) - start)
+        return r
+
+    def _too_big(self, what):
+        """A fused program over the VM limits: materialise its largest inlined
+        sub-expression and lower again."""
+        cands = [(size, n) for n, size in self.spans.items() if n not in self.low.M]
+        if cands:
+            raise _Retry(max(cands)[1])
+        raise UnsupportedOp(what)
+
+    def _value(self, n, axes):
         low = self.low
         node = low.nodes[n]
         if n in low.buf and n not in self._inline:
@@ -1262,11 +1491,46 @@ class Program:
             try:
                 inner = through_index_op(node, axes)
             except Unexpressible:
-                raise _Retry(n)
-            return self.value(node.inputs[0][0], inner)
+                inner = None
+            try:
+                if inner is not None:
+                    return self.value(node.inputs[0][0], inner)
+                view = self.view_of(n)
+                if view is None:
+                    raise _Retry(n)
+                return ("leaf", self.leaf(view, axes))
+            except _TooManyDigits:
+                raise _Retry(n)  # materialise the index op: its consumers then read it plainly
         if node.op in ELEMENTWISE_UNARY:
             self.to_acc(self.value(node.inputs[0][0], axes))
             self.emit(I_UN, VM_OP[node.op])
+            return ("acc",)
+        if n in low.tiny:
+            # kernels.py:123-133: acc = 0; acc = rn(acc + rn(a*b)) for k ascending
+            a, b = node.inputs[0][0], node.inputs[1][0]
+            mul, add = VM_OP[OpKind.MULTIPLY], VM_OP[OpKind.ADD]
+            terms = _dot_term_axes(node, axes, low)
+            if not terms:  # empty contraction: the reference's 0.0
+                self.emit(I_LOAD, k=self.leaf(low.splat_buffer(node.output.element_type, 0.0), []))
+            for t, (aa, ba) in enumerate(terms):
+                if t:
+                    self.emit(I_PUSH)  # running sum
+                if self.is_plain(b, ba):
+                    self.to_acc(self.value(a, aa))
+                    self.emit(I_BIN_LEAF, mul, self.value(b, ba)[1], 0)
+                elif self.is_plain(a, aa):
+                    self.to_acc(self.value(b, ba))
+                    self.emit(I_BIN_LEAF, mul, self.value(a, aa)[1], 1)
+                else:
+                    self.to_acc(self.value(a, aa))
+                    self.emit(I_PUSH)
+                    self.to_acc(self.value(b, ba))
+                    self.emit(I_BIN_POP, mul, 0, 0)
+                if t:
+                    self.emit(I_BIN_POP, add, 0, 0)  # acc = sum + term
+                else:
+                    zero = self.leaf(low.splat_buffer(node.output.element_type, 0.0), [])
+                    self.emit(I_BIN_LEAF, add, zero, 1)  # acc = 0 + term
             return ("acc",)
         if node.op in ELEMENTWISE_BINARY:
             a, b = node.inputs[0][0], node.inputs[1][0]
@@ -1322,9 +1586,19 @@ class Program:
             try:
                 inner = through_index_op(node, axes)
             except Unexpressible:
-                raise _Retry(n)
+                inner = None
             self._inline = set()
-            r = self.value(node.inputs[0][0], inner)
+            if inner is not None:
+                r = self.value(node.inputs[0][0], inner)
+            else:
+                saved = self.low.buf.pop(n)
+                try:
+                    view = self.view_of(n)
+                finally:
+                    self.low.buf[n] = saved
+                if view is None:
+                    raise _Retry(n)
+                r = ("leaf", self.leaf(view, axes))
         else:
             if self.need_root(n, axes) > MAX_STACK:
                 raise _Retry(self._deepest_child(n, axes))
@@ -1361,7 +1635,7 @@ class Program:
         rest = [i for i in loads if i not in pre]
         new_order = pre + rest + stores
         if len(new_order) > abi.MAX_LEAVES:
-            raise UnsupportedOp(f"fused group needs {len(new_order)} leaves (> {abi.MAX_LEAVES})")
+            self._too_big(f"fused group needs {len(new_order)} leaves (> {abi.MAX_LEAVES})")
         remap = {old: new for new, old in enumerate(new_order)}
         self.leaf_specs = [self.leaf_specs[i] for i in new_order]
         code = []
@@ -1371,7 +1645,7 @@ class Program:
             code.append((cls, op, k, swap))
         self.code = code
         if len(self.code) > abi.MAX_INSTR:
-            raise UnsupportedOp(f"fused program of {len(self.code)} instructions (> {abi.MAX_INSTR})")
+            self._too_big(f"fused program of {len(self.code)} instructions (> {abi.MAX_INSTR})")
         return len(pre)
 
     def depth(self) -> int:
@@ -1394,7 +1668,7 @@ class Program:
         a.npre, a.depth, a.wpr = npre, self.depth(), wpr
         words = encode_flat(self.code, npre)
         if len(words) > abi.MAX_INSTR:
-            raise UnsupportedOp(f"fused program of {len(words)} instructions (> {abi.MAX_INSTR})")
+            self._too_big(f"fused program of {len(words)} instructions (> {abi.MAX_INSTR})")
         a.ninstr = len(words)
         for i, w in enumerate(words):
             a.prog[i] = w

@@ -45,14 +45,14 @@ def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
 
 
 @pytest.mark.parametrize("m,k,n,ta,tb,et", [
-    (1, 4, 5000, False, False, "F32"),
-    (4, 1, 3001, False, False, "F32"),
+    (1, 5, 5000, False, False, "F32"),
+    (4, 6, 3001, False, False, "F32"),
     (8, 9, 700, True, False, "F32"),
     (3, 17, 1025, False, True, "F64"),
 ])
 def test_small_m_dot_bit_exact(m, k, n, ta, tb, et):
-    """Few-row Dots (the maxpool one-hot selections) take the thread-per-
-    column SIMT kernel and keep the reference k order: bit-exact."""
+    """Few-row Dots with k > TINY_DOT_K take the thread-per-column SIMT
+    kernel and keep the reference k order: bit-exact."""
     et = getattr(gf.ElementType, et)
     fn = gf.Function("dot")
     a = fn.add_parameter(et, (k, m) if ta else (m, k))
@@ -168,3 +168,20 @@ def test_conv_tma_box_matches_oracle(monkeypatch, op, shape, stride, pad):
     out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("m,k,n,et", [(2, 2, 2, "F64"), (1, 4, 4099, "F32"), (4, 1, 3001, "F32"), (2, 0, 3, "F64")])
+def test_tiny_dot_fused_bit_exact_on_device(m, k, n, et):
+    """Dots with k <= 4 run inside the VM kernel, bit-exact with the oracle."""
+    et = getattr(gf.ElementType, et)
+    fn = gf.Function("tiny")
+    a = fn.add_parameter(et, (m, k))
+    b = fn.add_parameter(et, (k, n))
+    fn.set_results([fn.add_node(K.DOT, [a, b])])
+    exe = gf.compile_function(fn, optimize=False)
+    assert all(L.label.startswith("map:") for L in exe.lowered.launches)
+    rng = np.random.default_rng(m + k + n)
+    A = rng.uniform(-1, 1, size=(m, k)).astype(et.numpy_dtype)
+    B = rng.uniform(-1, 1, size=(k, n)).astype(et.numpy_dtype)
+    out = gf.call(exe, [gf.tensor_from_flat(et, A.shape, A), gf.tensor_from_flat(et, B.shape, B)])[0].to_numpy()
+    assert G.same_bits(out, interp.run_function(fn, [A, B])[0])
