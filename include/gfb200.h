@@ -55,6 +55,7 @@ enum {
     GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot on split planes (gfb_tc_args) */
     GFB_K_SPLIT_TF32 = 13, /* F32 -> TF32 hi/lo K-major planes (gfb_split_args) */
     GFB_K_DOT_TC32W = 14,  /* as GFB_K_DOT_TC32 with 128x256 tiles (gfb_tc_args) */
+    GFB_K_DOT_TC32P = 19,  /* as GFB_K_DOT_TC32 on a 2-SM CTA pair (cta_group::2), 256x256 tiles; grid.x = 2 * column tiles */
     GFB_K_DOT_SM_F32 = 15, /* SIMT Dot for m <= 8, thread per column, bit-exact (gfb_dot_args) */
     GFB_K_DOT_SM_F64 = 16,
     GFB_K_CONV_TCG64 = 17,  /* implicit-GEMM conv, in-kernel gather + TF32 split, 128x64 tiles (gfb_tcg_args) */

@@ -1058,12 +1058,19 @@ class Lowering:
             for k_, v_ in addr.items():
                 setattr(ta, k_, v_)
         wide = ncols >= 256 and os.environ.get("GFB_TC_WIDE", "1") == "1"
-        bn = 256 if wide else TC_TILE
-        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, splits)
+        pair = wide and m >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1"
+        if pair:  # 2-SM CTA pair, 256x256 tile (gfb_gemm_tc2_kernel)
+            kind, block, smem = abi.K_DOT_TC32P, 320, TC_SMEM
+            grid = (2 * ((ncols + 255) // 256), (m + 255) // 256, splits)
+        elif wide:
+            kind, block, smem = abi.K_DOT_TC32W, 320, TC_SMEM_W
+            grid = ((ncols + 255) // 256, (m + TC_TILE - 1) // TC_TILE, splits)
+        else:
+            kind, block, smem = abi.K_DOT_TC32, 192, TC_SMEM
+            grid = ((ncols + TC_TILE - 1) // TC_TILE, (m + TC_TILE - 1) // TC_TILE, splits)
         if grid[1] > 65535:
             raise UnsupportedOp(f"tensor-core GEMM with {m} rows exceeds the 65535-tile grid")
-        rec = LaunchRec(abi.K_DOT_TC32W if wide else abi.K_DOT_TC32, grid, (320 if wide else 192, 1, 1),
-                        TC_SMEM_W if wide else TC_SMEM, ta, [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
+        rec = LaunchRec(kind, grid, (block, 1, 1), smem, ta, [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
         rec.flops = 2 * m * ncols * kdim
         rec.finalize = _finalize_refs(ta, {"c": target, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
         self.launches.append(rec)

@@ -754,6 +754,223 @@ __global__ void __launch_bounds__(tc::XCfg<BN_>::THREADS, 1) gfb_conv_tcx_kernel
     }
 }
 
+// ---------------------------------------------------------------------------
+// 2-SM GEMM: a CTA pair (cluster of 2, cta_group::2) computes a 256 x 256
+// tile.  CTA r loads A rows [m0 + 128 r, +128) and B rows [n0 + 128 r, +128)
+// (hi and lo planes) into its own shared memory; the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 with M = 256, N = 256, which reads each CTA's
+// half of A and B from that CTA's shared memory and accumulates rows
+// [128 r, +128) in CTA r's TMEM.  Per SM this halves the shared-memory
+// operand reads per flop relative to a 128 x 256 single-SM tile (the
+// single-SM kernel is smem-bandwidth bound).  Barriers: the leader's full[s]
+// counts both CTAs' TMA bytes (the peer's loads signal it across the pair);
+// the leader's commits multicast to both CTAs' empty[s] / tfull[b]; both
+// CTAs' epilogue warps arrive on the leader's tempty[b].
+namespace tc {
+struct PCfg {
+    static constexpr int BM = 128, BN = 128, BK = 32;  // per-CTA rows of A and of B
+    static constexpr int STAGES = 3;
+    static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int CHUNK_KB = 4, NBUF = 2, NT = 256;  // accumulator columns per buffer
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, int c0, int c1, uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     su32(bar)),
+                 "h"((uint16_t)3)
+                 : "memory");
+}
+}  // namespace tc
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1)
+    gfb_gemm_tc2_kernel(const __grid_constant__ gfb_tc_args p) {
+    using namespace tc;
+    using C_ = PCfg;
+    constexpr int BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, NT = C_::NT;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int n0 = (blockIdx.x >> 1) * 256, m0 = blockIdx.y * 256;
+    const int64_t k_begin = p.k_splits > 1 ? (int64_t)blockIdx.z * p.k_per_split : 0;
+    const int64_t k_end = p.k_splits > 1 ? min(p.K, k_begin + p.k_per_split) : p.K;
+    const int nk = k_end > k_begin ? (int)((k_end - k_begin + BK - 1) / BK) : 0;
+    const int nchunk = nk > 0 ? (nk + CHUNK_KB - 1) / CHUNK_KB : 0;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 4; ++i) prefetch_tmap(p.tmap[i]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t full0 = peer_addr(full, 0);  // the leader's full barriers
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+                unsigned char* st = smem + s * STAGE_BYTES;
+                if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);  // both CTAs' bytes land on it
+                const uint32_t bar = full0 + s * 8;
+                const int kc = (int)k_begin + kb * BK;
+                const int am = m0 + 128 * rank, bn = n0 + 128 * rank;
+                tma_load_2d_pair(st, p.tmap[0], kc, am, bar);
+                tma_load_2d_pair(st + A_BYTES, p.tmap[1], kc, am, bar);
+                tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
+                tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = idesc_tf32(256, 256);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                const int chunk = kb / CHUNK_KB, b = chunk % NBUF;
+                const bool chunk_start = kb % CHUNK_KB == 0;
+                if (chunk_start) {
+                    mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                mbar_wait(&full[s], (kb / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                unsigned char* st = smem + s * STAGE_BYTES;
+                const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                const uint32_t d = tmem + (uint32_t)(b * NT);
+#pragma unroll
+                for (int j = 0; j < BK / 8; ++j) {
+                    const uint64_t adv = (uint64_t)(j * 32) >> 4;
+                    const uint32_t acc = !(chunk_start && j == 0);
+                    mma_tf32_pair(d, ah + adv, bh + adv, idesc, acc);
+                    mma_tf32_pair(d, ah + adv, bl + adv, idesc, 1);
+                    mma_tf32_pair(d, al + adv, bh + adv, idesc, 1);
+                }
+                mma_commit_pair(&empty[s]);
+                if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);
+            }
+        }
+    } else {
+        // epilogue: warp w owns TMEM lanes [32 (w % 4), +32) = this CTA's tile
+        // rows, and 128 of the 256 columns (cg); promotion as in the 1-SM kernel
+        constexpr int EC = 128;
+        const int q = warp & 3, cg = (warp - 2) >> 2;
+        const uint32_t tempty0 = peer_addr(tempty, 0);
+        float acc[EC];
+#pragma unroll
+        for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+        for (int chunk = 0; chunk < nchunk; ++chunk) {
+            const int b = chunk % NBUF;
+            mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int c = 0; c < EC / 32; ++c) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT + cg * EC + c * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+        }
+        float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
+        const LinearRows rows{m0 + 128 * (int64_t)rank, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
+        const int64_t roff = rows(q * 32 + lane);
+        if (roff >= 0) {
+            float* dst = C + roff;
+#pragma unroll
+            for (int c = 0; c < EC / 32; ++c) {
+                const int col0 = n0 + cg * EC + c * 32;
+                if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dst + col0 + j) =
+                            make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // the peer's epilogue and the leader's MMAs are done
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 }  // namespace gfb
 
 
@@ -767,6 +984,7 @@ template __global__ void gfb::gfb_conv_tcx_kernel<128>(const __grid_constant__ g
 extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_DOT_TC32) return (const void*)gfb::gfb_gemm_tc_kernel<128>;
     if (kind == GFB_K_DOT_TC32W) return (const void*)gfb::gfb_gemm_tc_kernel<256>;
+    if (kind == GFB_K_DOT_TC32P) return (const void*)gfb::gfb_gemm_tc2_kernel;
     if (kind == GFB_K_SPLIT_TF32) return (const void*)gfb::gfb_split_kernel;
     if (kind == GFB_K_CONV_TCG64) return (const void*)gfb::gfb_conv_tcg_kernel<64>;
     if (kind == GFB_K_CONV_TCG128) return (const void*)gfb::gfb_conv_tcg_kernel<128>;

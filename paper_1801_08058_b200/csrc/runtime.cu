@@ -171,7 +171,7 @@ const void* kernel_for(uint32_t kind) {
     if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64 ||
         kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64)
         return gfb_simt_kernel_ptr((int)kind);
-    if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
+    if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_DOT_TC32P || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
         kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128)
         return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
@@ -299,7 +299,7 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
         }
         e->fns[i] = kernel_for(L.kind);
         if (!e->fns[i]) return bail(fail(GFB_ERR_INVALID, "unknown kernel kind " + std::to_string(L.kind)));
-        if (L.kind == GFB_K_DOT_TC32 || L.kind == GFB_K_DOT_TC32W) {
+        if (L.kind == GFB_K_DOT_TC32 || L.kind == GFB_K_DOT_TC32W || L.kind == GFB_K_DOT_TC32P) {
             // Tensor maps need fixed addresses: the split planes live in the arena.
             gfb_tc_args* a = (gfb_tc_args*)(e->args.data() + L.arg_offset);
             const uint64_t refs[4] = {a->a_hi, a->a_lo, a->b_hi, a->b_lo};

@@ -389,7 +389,7 @@ def _run_launch(mem, L):
         run_conv(mem, L.args, dt)
     elif L.kind == abi.K_SPLIT_TF32:
         run_split(mem, L.args)
-    elif L.kind in (abi.K_DOT_TC32, abi.K_DOT_TC32W):
+    elif L.kind in (abi.K_DOT_TC32, abi.K_DOT_TC32W, abi.K_DOT_TC32P):
         run_tc(mem, L.args)
     elif L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128):
         run_tcg(mem, L.args)

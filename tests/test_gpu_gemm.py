@@ -30,6 +30,9 @@ def _dot_graph(m, k, n, ta=False, tb=False):
     (257, 64, 511, False, True),
     (200, 301, 190, True, True),
     (1, 40, 3, False, False),
+    (300, 600, 520, False, False),   # 2-SM pair kernel, ragged tiles
+    (513, 4096, 256, False, True),   # pair kernel, long K (promotion chunks)
+    (256, 20000, 256, True, False),  # pair kernel under split-K
 ])
 def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
     monkeypatch.setenv("GFB_DOT", "tc")
