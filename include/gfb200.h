@@ -62,6 +62,8 @@ enum {
     GFB_K_CONV_TCG128 = 18, /* as GFB_K_CONV_TCG64 with 128x128 tiles */
     GFB_K_CONV_TCX64 = 22,  /* implicit-GEMM conv, TMA box gather + in-smem TF32 split, 128x64 (gfb_tcx_args) */
     GFB_K_CONV_TCX128 = 23, /* as GFB_K_CONV_TCX64 with 128x128 tiles */
+    GFB_K_CONV_TCGG64 = 24, /* implicit-GEMM conv, generic k-table gather (any layout, wgrad too), 128x64 (gfb_tcgg_args) */
+    GFB_K_CONV_TCGG128 = 25,
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
@@ -250,6 +252,29 @@ typedef struct GFB_ALIGN64 {
     int64_t pad[5];
     uint64_t tmap[3][16];
 } gfb_tcx_args;
+
+/* Implicit-GEMM convolution with a generic gather.  Row `row` = (i0, i1, i2)
+ * over (*, E1, E2) starts at rowoff = i0*ro0 + i1*ro1 + i2*ro2 with spatial
+ * origin (h, w) = (i1*hm + h0, i2*wm + w0).  K index k < K = (k0, k1, k2)
+ * over (*, Ke1, Ke2) adds koff = kbase + k0*ko0 + k1*ko1 + k2*ko2 and
+ * (dh, dw) = (k1*kh + dh0, k2*kw + dw0).  A[row, k] = a[rowoff + koff] when
+ * 0 <= h + dh < H and 0 <= w + dw < W (and k < K), else 0.  Kp = K rounded
+ * up to 32.  B is a TF32 hi/lo plane pair [N, >= K] (tensor maps encoded by
+ * gfb_exe_create; columns past the plane read as zero); output as
+ * gfb_tc_args; split-K over blockIdx.z (kb_per_split K-blocks each) into
+ * c + z * split_stride. */
+typedef struct GFB_ALIGN64 {
+    const void* const* tab;
+    uint64_t c, a, b_hi, b_lo;
+    int64_t M, N, K, Kp, kp_b;
+    int64_t c_sm, c_sn, c_rdiv, c_s_hi, c_s_lo;
+    int64_t ro0, ro1, ro2;
+    int64_t ko0, ko1, ko2, kbase;
+    int64_t k_splits, split_stride;
+    int32_t E1, E2, hm, wm, h0, w0, H, W;
+    int32_t Ke1, Ke2, kh, kw, dh0, dw0, kb_per_split, pad0;
+    uint64_t tmap[2][16]; /* offset 256 */
+} gfb_tcgg_args;
 
 typedef struct {
     const void* const* tab;

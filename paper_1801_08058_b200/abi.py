@@ -17,6 +17,7 @@ K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
 K_DOT_TC32P = 19
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
+K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
 
@@ -122,6 +123,23 @@ class TcxArgs(C.Structure):
     ]
 
 
+class TcggArgs(C.Structure):
+    # 64-byte aligned in C: tmap sits at offset 256, size 512.
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64), ("a", C.c_uint64), ("b_hi", C.c_uint64), ("b_lo", C.c_uint64),
+        ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("Kp", C.c_int64), ("kp_b", C.c_int64),
+        ("c_sm", C.c_int64), ("c_sn", C.c_int64), ("c_rdiv", C.c_int64), ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64),
+        ("ro0", C.c_int64), ("ro1", C.c_int64), ("ro2", C.c_int64),
+        ("ko0", C.c_int64), ("ko1", C.c_int64), ("ko2", C.c_int64), ("kbase", C.c_int64),
+        ("k_splits", C.c_int64), ("split_stride", C.c_int64),
+        ("E1", C.c_int32), ("E2", C.c_int32), ("hm", C.c_int32), ("wm", C.c_int32), ("h0", C.c_int32),
+        ("w0", C.c_int32), ("H", C.c_int32), ("W", C.c_int32),
+        ("Ke1", C.c_int32), ("Ke2", C.c_int32), ("kh", C.c_int32), ("kw", C.c_int32), ("dh0", C.c_int32),
+        ("dw0", C.c_int32), ("kb_per_split", C.c_int32), ("pad0", C.c_int32),
+        ("tmap", (C.c_uint64 * 16) * 2),
+    ]
+
+
 class ConvArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p),
@@ -161,5 +179,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

@@ -1094,6 +1094,12 @@ class Lowering:
                 and max(abs(v) for v in xs) * 4 < 2 ** 62)
 
     @staticmethod
+    def _generic_gather_ok(xb, xs) -> bool:
+        """Element-gather conv kernel: 32-bit element offsets and a real buffer."""
+        return (os.environ.get("GFB_CONV_GATHER", "1") == "1" and xb.splat is None
+                and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 30 and element_count(xb.shape) < 2 ** 31)
+
+    @staticmethod
     def _tma_box_ok(xb, shape, sx, sy) -> bool:
         """TMA box gather: the activation needs a fixed (arena) address for
         its tensor map, and the strided box must fit the 256-element limit."""
@@ -1142,6 +1148,49 @@ class Lowering:
         rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "b_hi": bhi, "b_lo": blo})
         self.launches.append(rec)
 
+    def _conv_tcgg(self, n, xb, b, out, m, ncols, kdim, geo, addr, yb, label):
+        """Implicit-GEMM convolution whose A operand is gathered element-wise
+        inside the tensor-core kernel (gemm_tc.cu, gfb_conv_tcgg_kernel):
+        any channel count, any layout, and weight gradients (split-K)."""
+        bhi, blo, kpb = b
+        bn = 64 if ncols <= 64 else 128
+        kblocks = (kdim + 31) // 32
+        tiles = ((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE)
+        splits = 1
+        if tiles < NUM_SMS and kblocks >= 64:
+            splits = max(1, min((2 * NUM_SMS) // tiles, kblocks // 16))
+        per = (kblocks + splits - 1) // splits
+        splits = (kblocks + per - 1) // per
+        ta = abi.TcggArgs(M=m, N=ncols, K=kdim, Kp=kblocks * 32, kp_b=kpb, **geo)
+        target = out
+        if splits > 1:
+            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
+            self.buf[("splitk", n)] = scratch
+            ta.k_splits, ta.kb_per_split, ta.split_stride = splits, per, m * ncols
+            ta.c_sm, ta.c_sn = ncols, 1
+            target = scratch
+        else:
+            ta.k_splits, ta.kb_per_split = 1, kblocks
+            for k_, v_ in addr.items():
+                setattr(ta, k_, v_)
+        kind = abi.K_CONV_TCGG64 if bn == 64 else abi.K_CONV_TCGG128
+        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, splits)
+        if grid[1] > 65535:
+            raise UnsupportedOp(f"convolution GEMM with {m} rows exceeds the 65535-tile grid")
+        rec = LaunchRec(kind, grid, (320, 1, 1), TCG_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [target.key], label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": target, "a": xb, "b_hi": bhi, "b_lo": blo})
+        self.launches.append(rec)
+        if splits > 1:
+            p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
+            p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+            self._col_launch(p2, m * ncols, splits, 1, label + ":splitk", ElementType.F32)
+        return rec
+
     def emit_conv_tc(self, n) -> bool:
         """Conv2D / ConvBackpropData / ConvBackpropFilter as implicit GEMMs on
         the tensor cores; returns False when the shape or layout does not fit
@@ -1178,10 +1227,17 @@ class Lowering:
                                CB=Cc // 32, ksign=1), {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
                                yb, f"{node.op.wire_name}_tcg#{n}")
                 return True
+            addr = {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
+            if self._generic_gather_ok(xb, xs):
+                b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (Cc, R, S), st=ys[1:])
+                geo = dict(E1=Ho, E2=Wo, ro0=xs[0], ro1=sh * xs[2], ro2=sw * xs[3], hm=sh, wm=sw, h0=0, w0=0, H=H, W=W,
+                           Ke1=R, Ke2=S, ko0=xs[1], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
+                           kh=1, kw=1, dh0=-pt, dw0=-pl)
+                self._conv_tcgg(n, xb, b, out, m, ncols, kdim, geo, addr, yb, f"{node.op.wire_name}_tcgg#{n}")
+                return True
             geo = (N, Cc, H, W, R, S, Ho, Wo, sh, sw, pt, pl)
             a = self._split(n, "a", xb, m, kdim, 1, geo=geo, st=xs)
             b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (Cc, R, S), st=ys[1:])
-            addr = {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
         elif node.op is OpKind.CONV_BACKPROP_DATA:
             N, K, Ho, Wo = xshape
             _, Cc, R, S = yshape
@@ -1200,10 +1256,17 @@ class Lowering:
                                CB=K // 32, ksign=-1), {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
                                yb, f"{node.op.wire_name}_tcg#{n}")
                 return True
+            addr = {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
+            if self._generic_gather_ok(xb, xs):
+                b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (K, R, S), st=(ys[0], ys[2], ys[3]))
+                geo = dict(E1=H, E2=W, ro0=xs[0], ro1=xs[2], ro2=xs[3], hm=1, wm=1, h0=0, w0=0, H=Ho, W=Wo,
+                           Ke1=R, Ke2=S, ko0=xs[1], ko1=-xs[2], ko2=-xs[3], kbase=pt * xs[2] + pl * xs[3],
+                           kh=-1, kw=-1, dh0=pt, dw0=pl)
+                self._conv_tcgg(n, xb, b, out, m, ncols, kdim, geo, addr, yb, f"{node.op.wire_name}_tcgg#{n}")
+                return True
             geo = (N, K, H, W, R, S, Ho, Wo, 1, 1, pt, pl)
             a = self._split(n, "a", xb, m, kdim, 2, geo=geo, st=xs)
             b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (K, R, S), st=(ys[0], ys[2], ys[3]))
-            addr = {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
         else:
             N, Cc, H, W = xshape
             _, K, Ho, Wo = yshape
@@ -1211,6 +1274,15 @@ class Lowering:
             m, ncols, kdim = K, Cc * R * S, N * Ho * Wo
             if os_[1] != R * S * os_[3] or os_[2] != S * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if self._generic_gather_ok(xb, xs):
+                # rows (c, r, s) of the gathered data, columns = output channels
+                b = self._split(n, "b", yb, K, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
+                geo = dict(E1=R, E2=S, ro0=xs[1], ro1=xs[2], ro2=xs[3], hm=1, wm=1, h0=-pt, w0=-pl, H=H, W=W,
+                           Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
+                           kh=1, kw=1, dh0=0, dw0=0)
+                self._conv_tcgg(n, xb, b, out, Cc * R * S, K, kdim, geo, {"c_sm": os_[3], "c_sn": os_[0]}, yb,
+                                f"{node.op.wire_name}_tcgg#{n}")
+                return True
             a = self._split(n, "a", yb, m, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
             geo = (N, Cc, H, W, R, S, Ho, Wo, 1, 1, pt, pl)
             b = self._split(n, "b", xb, ncols, kdim, 4, geo=geo, st=xs)

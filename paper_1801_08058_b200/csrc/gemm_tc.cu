@@ -971,6 +971,165 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
     }
 }
 
+// ---------------------------------------------------------------------------
+// Implicit-GEMM convolution with a generic element gather (any channel count,
+// any layout, weight gradients included).  A[row, k] = a[rowoff(row) +
+// koff(k)] when 0 <= h(row) + dh(k) < H and 0 <= w(row) + dw(k) < W, else 0.
+// Rows are (i0, i1, i2) over (*, E1, E2): rowoff = i0*ro0 + i1*ro1 + i2*ro2,
+// h = i1*hm + h0, w = i2*wm + w0; the K index decomposes the same way into
+// (koff, dh, dw) (gfb_tcgg_args in gfb200.h):
+//   Conv2D:             rows (n, p, q), k = (c, r, s): dh = r - pt, dw = s - pl
+//   ConvBackpropData:   rows (n, h, w), k = (kk, r, s): dh = pt - r, dw = pl - s
+//   ConvBackpropFilter: rows (c, r, s) with h0 = -pt, w0 = -pl, k = (n, p, q):
+//                       dh = p, dw = q
+// Gather warps map lanes to 32 consecutive rows (coalesced along the
+// activation's fastest spatial axis) and walk the 32 k of a K-block with
+// 4-byte zero-filling cp.async into a 4-deep raw ring; each thread then
+// splits its own row into TF32 hi/lo.  B (filter or δ planes) by TMA.
+// Split-K over blockIdx.z as in the plane GEMM.
+template <int BN_>
+__global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kernel(const __grid_constant__ gfb_tcgg_args p) {
+    using namespace tc;
+    using C_ = GCfg<BN_>;
+    constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, RAW = C_::RAW;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GATHER_WARPS = C_::GATHER_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* raw = smem + STAGES * STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + RAW * A_BYTES + C_::ROWTAB);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
+    const int kb_total = (int)((p.K + BK - 1) / BK);
+    const int kb_begin = p.k_splits > 1 ? (int)blockIdx.z * p.kb_per_split : 0;
+    const int kb_end = p.k_splits > 1 ? min(kb_total, kb_begin + p.kb_per_split) : kb_total;
+    const int nk = max(0, kb_end - kb_begin);
+    const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1 + GATHER_WARPS);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(p.tmap[0]);
+        prefetch_tmap(p.tmap[1]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                unsigned char* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], 2 * B_BYTES);
+                tma_load_2d(st + 2 * A_BYTES, p.tmap[0], (kb_begin + i) * BK, n0, &full[s]);
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[1], (kb_begin + i) * BK, n0, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
+    } else if (warp < 2 + EPI_WARPS) {
+        float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
+        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, C, n0, p.N, p.c_sn,
+                           LinearRows{m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo});
+    } else {
+        // gather thread: one row of the tile, lanes over 32 consecutive rows
+        const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127 = tile row
+        const float* A = resolve<const float>(p.tab, p.a);
+        const int64_t row = m0 + g;
+        int64_t rowoff = 0;
+        int hr = -(1 << 28), wr = 0;
+        if (row < p.M) {
+            const int64_t e12 = (int64_t)p.E1 * p.E2;
+            const int64_t i0 = row / e12, rem = row - i0 * e12, i1 = rem / p.E2, i2 = rem - i1 * p.E2;
+            rowoff = i0 * p.ro0 + i1 * p.ro1 + i2 * p.ro2;
+            hr = (int)(i1 * p.hm + p.h0);
+            wr = (int)(i2 * p.wm + p.w0);
+        }
+        const float* arow = A + rowoff;
+        const uint32_t rbase = (uint32_t)g * 128u, rsw = (uint32_t)(g & 7);
+        const int ke12 = p.Ke1 * p.Ke2;
+        auto issue = [&](int i) {
+            // lane's K index of this block -> (koff, dh, dw), broadcast by shuffles
+            const int64_t k = (int64_t)(kb_begin + i) * BK + lane;
+            int koff = 0, dh = -(1 << 28), dw = 0;
+            if (k < p.K) {
+                const int kk = (int)k, k0 = kk / ke12, kr = kk - k0 * ke12, k1 = kr / p.Ke2, k2 = kr - k1 * p.Ke2;
+                koff = (int)(p.kbase + k0 * p.ko0 + k1 * p.ko1 + k2 * p.ko2);
+                dh = k1 * p.kh + p.dh0;
+                dw = k2 * p.kw + p.dw0;
+            }
+            const uint32_t dst0 = su32(raw + (i % RAW) * A_BYTES) + rbase;
+#pragma unroll 8
+            for (int t = 0; t < 32; ++t) {
+                const int ko = __shfl_sync(0xffffffffu, koff, t);
+                const int h = hr + __shfl_sync(0xffffffffu, dh, t), w = wr + __shfl_sync(0xffffffffu, dw, t);
+                const bool ok = (uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W;
+                const float* src = ok ? arow + ko : A;
+                const uint32_t dst = dst0 + ((((uint32_t)t >> 2) ^ rsw) << 4) + ((uint32_t)t & 3u) * 4u;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4u : 0u) : "memory");
+            }
+        };
+#pragma unroll
+        for (int i = 0; i < RAW; ++i) {
+            if (i < nk) issue(i);
+            cp_async_commit();
+        }
+        for (int i = 0; i < nk; ++i) {
+            cp_async_wait<RAW - 1>();  // this thread's row of K-block i has landed
+            const int s = i % STAGES;
+            mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            const uint32_t src = su32(raw + (i % RAW) * A_BYTES) + rbase;
+            const uint32_t dst = su32(smem + s * STAGE_BYTES) + rbase;
+            // the split is elementwise, so chunks are visited in a per-lane
+            // rotated order: 32 lanes = 32 rows 128 B apart then spread over
+            // all 32 banks instead of 4
+            float4 x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = lds128(src + (((uint32_t)(j + g) & 7u) << 4));
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t o = ((uint32_t)(j + g) & 7u) << 4;
+                const float4 h = trunc_tf32(x[j]);
+                const float4 l = make_float4(__fsub_rn(x[j].x, h.x), __fsub_rn(x[j].y, h.y), __fsub_rn(x[j].z, h.z),
+                                             __fsub_rn(x[j].w, h.w));
+                sts128(dst + o, h);
+                sts128(dst + A_BYTES + o, l);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+            if (i + RAW < nk) issue(i + RAW);
+            cp_async_commit();
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 }  // namespace gfb
 
 
@@ -979,6 +1138,8 @@ template __global__ void gfb::gfb_gemm_tc_kernel<256>(const __grid_constant__ gf
 template __global__ void gfb::gfb_conv_tcg_kernel<64>(const __grid_constant__ gfb_tcg_args);
 template __global__ void gfb::gfb_conv_tcg_kernel<128>(const __grid_constant__ gfb_tcg_args);
 template __global__ void gfb::gfb_conv_tcx_kernel<64>(const __grid_constant__ gfb_tcx_args);
+template __global__ void gfb::gfb_conv_tcgg_kernel<64>(const __grid_constant__ gfb_tcgg_args);
+template __global__ void gfb::gfb_conv_tcgg_kernel<128>(const __grid_constant__ gfb_tcgg_args);
 template __global__ void gfb::gfb_conv_tcx_kernel<128>(const __grid_constant__ gfb_tcx_args);
 
 extern "C" const void* gfb_tc_kernel_ptr(int kind) {
@@ -989,6 +1150,8 @@ extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_CONV_TCG64) return (const void*)gfb::gfb_conv_tcg_kernel<64>;
     if (kind == GFB_K_CONV_TCG128) return (const void*)gfb::gfb_conv_tcg_kernel<128>;
     if (kind == GFB_K_CONV_TCX64) return (const void*)gfb::gfb_conv_tcx_kernel<64>;
+    if (kind == GFB_K_CONV_TCGG64) return (const void*)gfb::gfb_conv_tcgg_kernel<64>;
+    if (kind == GFB_K_CONV_TCGG128) return (const void*)gfb::gfb_conv_tcgg_kernel<128>;
     if (kind == GFB_K_CONV_TCX128) return (const void*)gfb::gfb_conv_tcx_kernel<128>;
     return nullptr;
 }

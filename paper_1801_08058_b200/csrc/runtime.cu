@@ -172,7 +172,8 @@ const void* kernel_for(uint32_t kind) {
         kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64)
         return gfb_simt_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_DOT_TC32P || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
-        kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128)
+        kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128 || kind == GFB_K_CONV_TCGG64 ||
+        kind == GFB_K_CONV_TCGG128)
         return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
 }
@@ -328,6 +329,17 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
             for (int t = 1; t < 3; ++t)
                 if (!encode_plane_map(addr[t], a->N, a->K, L.kind == GFB_K_CONV_TCX64 ? 64 : 128, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
+        }
+        if (L.kind == GFB_K_CONV_TCGG64 || L.kind == GFB_K_CONV_TCGG128) {
+            gfb_tcgg_args* a = (gfb_tcgg_args*)(e->args.data() + L.arg_offset);
+            const uint64_t refs[2] = {a->b_hi, a->b_lo};
+            for (int t = 0; t < 2; ++t) {
+                if ((refs[t] >> 56) != GFB_SLOT_ARENA)
+                    return bail(fail(GFB_ERR_INVALID, "tensor-core operand planes must live in the arena"));
+                void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
+                if (!encode_plane_map(addr, a->N, a->kp_b, L.kind == GFB_K_CONV_TCGG64 ? 64 : 128, a->tmap[t]))
+                    return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
+            }
         }
         if (L.kind == GFB_K_CONV_TCG64 || L.kind == GFB_K_CONV_TCG128) {
             gfb_tcg_args* a = (gfb_tcg_args*)(e->args.data() + L.arg_offset);

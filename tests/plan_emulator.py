@@ -376,6 +376,46 @@ def run_tcx(mem, a):
     mem.view(a.c, np.float32)[n * a.o_n + y * a.o_y + x * a.o_x + j * a.c_sn] = out
 
 
+def run_tcgg(mem, a):
+    """gfb_conv_tcgg_kernel: generic row / K decompositions (gfb_tcgg_args)."""
+    src = mem.view(a.a, np.float32)
+    row = np.arange(a.M, dtype=np.int64)
+    e12 = a.E1 * a.E2
+    i0, rem = row // e12, row % e12
+    i1, i2 = rem // a.E2, rem % a.E2
+    rowoff = i0 * a.ro0 + i1 * a.ro1 + i2 * a.ro2
+    hr, wr = i1 * a.hm + a.h0, i2 * a.wm + a.w0
+    k = np.arange(a.K, dtype=np.int64)
+    ke12 = a.Ke1 * a.Ke2
+    k0, kr = k // ke12, k % ke12
+    k1, k2 = kr // a.Ke2, kr % a.Ke2
+    koff = a.kbase + k0 * a.ko0 + k1 * a.ko1 + k2 * a.ko2
+    h = hr[:, None] + (k1 * a.kh + a.dh0)[None, :]
+    w = wr[:, None] + (k2 * a.kw + a.dw0)[None, :]
+    ok = (h >= 0) & (h < a.H) & (w >= 0) & (w < a.W)
+    off = rowoff[:, None] + koff[None, :]
+    x = np.where(ok, src[np.where(ok, off, 0)], np.float32(0)).astype(np.float32)
+    ahi, alo = _trunc_split(x)
+    ahi, alo = ahi.astype(np.float64), alo.astype(np.float64)
+    bhi = mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b)[:, : a.K].astype(np.float64)
+    blo = mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b)[:, : a.K].astype(np.float64)
+    C = mem.view(a.c, np.float32)
+    i = row[:, None]
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    kblocks = (a.K + 31) // 32
+    for z in range(max(1, a.k_splits)):
+        b0 = z * a.kb_per_split if a.k_splits > 1 else 0
+        b1 = min(kblocks, b0 + a.kb_per_split) if a.k_splits > 1 else kblocks
+        sl = slice(32 * b0, min(a.K, 32 * b1))
+        c = (ahi[:, sl] @ bhi[:, sl].T + ahi[:, sl] @ blo[:, sl].T + alo[:, sl] @ bhi[:, sl].T).astype(np.float32)
+        base = z * a.split_stride if a.k_splits > 1 else 0
+        if a.c_rdiv > 0:
+            off = (i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn
+        else:
+            off = i * a.c_sm + j * a.c_sn
+        C[base + off] = c
+
+
 STAGED_U = 2  # csrc/ew_vm.cu StagedCfg<T, 2>
 
 
@@ -395,6 +435,8 @@ def _run_launch(mem, L):
         run_tcg(mem, L.args)
     elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):
         run_tcx(mem, L.args)
+    elif L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128):
+        run_tcgg(mem, L.args)
     else:
         raise NotImplementedError(L.kind)
 

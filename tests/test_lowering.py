@@ -134,6 +134,9 @@ def _conv_graph(op, N, C, K, H, W, R, S, stride=(1, 1), pad=(1, 1, 1, 1)):
     ("fwd", (2, 3, 8, 9, 10, 3, 3), (1, 1), (1, 1, 1, 1), "nhwc"),
     ("dgrad", (2, 5, 6, 7, 9, 3, 3), (1, 1), (1, 0, 0, 1), "identity"),
     ("wgrad", (2, 4, 6, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
+    ("fwd", (2, 3, 16, 12, 12, 7, 7), (1, 1), (3, 3, 3, 3), "identity"),    # stem-like, generic gather
+    ("wgrad", (2, 3, 16, 12, 12, 7, 7), (1, 1), (3, 3, 3, 3), "identity"),
+    ("dgrad", (2, 6, 16, 9, 9, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
 ])
 def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad, layout):
     """Implicit-GEMM convolutions (gather-split planes + 3xTF32 GEMM, split-K
@@ -146,8 +149,8 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     fn = _conv_graph(op, N, C, K, H, W, R, S, stride, pad)
     h = host_compile(fn, optimize=False, conv_layout=layout) if op == "fwd" else host_compile(fn, optimize=False)
     labels = [L.label for L in h.lowered.launches]
-    assert any("_tc#" in l for l in labels), labels
-    if op == "wgrad":
+    assert any("_tc" in l for l in labels), labels
+    if op == "wgrad" and N * H * W >= 2048:  # long K: split-K with a deterministic second pass
         assert any(":splitk" in l for l in labels), labels
     rng = np.random.default_rng(5)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
