@@ -52,7 +52,8 @@ class EwArgs(C.Structure):
         ("tab", C.c_void_p),
         ("n_o", C.c_uint32), ("n_r", C.c_uint32), ("ninstr", C.c_uint32), ("nleaves", C.c_uint32),
         ("mode", C.c_int32), ("red_kind", C.c_int32), ("vec_axis", C.c_int32), ("split", C.c_int32),
-        ("npre", C.c_int32), ("depth", C.c_int32), ("wpr", C.c_int32), ("pad", C.c_int32),
+        ("npre", C.c_int32), ("depth", C.c_int32), ("wpr", C.c_int32),
+        ("ty_ext", C.c_int32), ("ty_div", C.c_int32), ("pad", C.c_int32),
         ("prog", C.c_uint32 * MAX_INSTR),
         ("leaves", Leaf * MAX_LEAVES),
         ("red_out", Leaf),

@@ -437,8 +437,11 @@ def vec_class(digits, vec_src: int, is_store: bool, V: int, esize: int) -> int:
     if len(unit) != 1:
         return 0
     _, _, mod, stride = unit[0]
-    if stride != 1 or (mod is not None and mod % V):
+    if mod is not None and mod % V:
         return 0
+    if stride != 1:
+        # a V-aligned vector stays inside the unit digit: element v at base + v*stride
+        return 3 if abs(stride) * V < 2 ** 30 else 0
     if any(d[3] % align for d in digits if d is not unit[0]):
         return 0
     return 1
@@ -867,6 +870,11 @@ class Lowering:
         per_row = 256 // split
         grid = max(1, min((vectors + per_row - 1) // per_row, NUM_SMS * 16))
         args = prog.args(mode=2, n_o=n_o, n_r=n_r, red_kind=red_kind, split=split)
+        if red_kind == 0 and split == 1 and n_r == 1:
+            ty = _transpose_order(prog, n_o, V)
+            if ty is not None:
+                args.ty_ext, args.ty_div = ty
+                label += ":T"
         self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
 
     def emit_map(self, root: int, stores: list):
@@ -1407,6 +1415,7 @@ class LeafSpec:
     digits: list
     is_store: bool
     vec: int = 0
+    vec_src: int = 0  # the index source vectors run along (0 = o, 1 = r)
 
 
 def _splat_bits(b: Buffer) -> int:
@@ -1418,6 +1427,31 @@ def _splat_bits(b: Buffer) -> int:
     if b.et is ElementType.I64:
         return int(v) & ((1 << 64) - 1)
     return int(bool(v))
+
+
+def _transpose_order(prog, n_o: int, V: int):
+    """(ty_ext, ty_div) for a COL map whose stores are vector-contiguous but
+    whose biggest operand is contiguous along another o-digit (a layout
+    transposition): threads then walk that digit, so the operand's loads
+    coalesce across lanes while each thread still stores whole vectors."""
+    if os.environ.get("GFB_TRANSPOSE_ORDER", "1") != "1" or n_o % V:
+        return None
+    stores = [l for l in prog.leaf_specs if l.is_store]
+    if not stores or any(l.vec != 1 for l in stores):
+        return None
+    loads = [l for l in prog.leaf_specs if not l.is_store and l.buf.splat is None and l.vec == 0]
+    if not loads:
+        return None
+    big = max(loads, key=lambda l: l.buf.nbytes)
+    if 2 * big.buf.nbytes < max(l.buf.nbytes for l in prog.leaf_specs if l.buf.splat is None):
+        return None
+    for src, div, mod, stride in big.digits:
+        if src != 0 or abs(stride) != 1 or div < V or div % V:
+            continue
+        ext = mod if mod is not None else n_o // div
+        if ext >= 8 and n_o % (div * ext) == 0 and ext * div <= n_o:
+            return ext, div
+    return None
 
 
 def _dot_term_axes(node, axes, low):
@@ -1458,7 +1492,7 @@ class Program:
         if key not in self.leaf_index:
             if len(digits) > abi.MAX_DIGITS:
                 raise _TooManyDigits()
-            spec = LeafSpec(buf, digits, False)
+            spec = LeafSpec(buf, digits, False, vec_src=self.vec_src)
             spec.vec = 2 if buf.splat is not None else vec_class(digits, self.vec_src, False, self.V, buf.et.byte_size)
             if spec.vec == 1 and (buf.elem_off * buf.et.byte_size) % 16:
                 spec.vec = 0  # a constant offset breaks the vector alignment
@@ -1470,7 +1504,7 @@ class Program:
         digits = make_digits(buf, axes, self.extents)
         if len(digits) > abi.MAX_DIGITS:
             raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
-        spec = LeafSpec(buf, digits, True, vec_class(digits, self.vec_src, True, self.V, buf.et.byte_size))
+        spec = LeafSpec(buf, digits, True, vec_class(digits, self.vec_src, True, self.V, buf.et.byte_size), self.vec_src)
         self.leaf_specs.append(spec)
         return len(self.leaf_specs) - 1
 
@@ -1804,7 +1838,10 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
     L.ndig = len(s.digits)
     L.vec = s.vec
     L.rlin = r_linear(s.digits)
-    for i, (src, div, mod, stride) in enumerate(s.digits):
+    digits = list(s.digits)
+    if s.vec == 3:  # the kernel reads the unit digit's stride from dig[0]
+        digits.sort(key=lambda d: 0 if d[1] == 1 and d[0] == s.vec_src else 1)
+    for i, (src, div, mod, stride) in enumerate(digits):
         d = L.dig[i]
         d.src = src
         d.div_mul, d.div_sh = magic_u31(div)

@@ -155,6 +155,10 @@ struct Ctx {
             const uint32_t off = ob[k * obs] + r_offset(L, r);
             if (L.vec == 1) {
                 loadV<T, V>(bp + off, out);
+            } else if (L.vec == 3) {  // strided vector: element v at off + v * (stride of the unit digit)
+                const int32_t s1 = L.dig[0].stride;
+#pragma unroll
+                for (int v = 0; v < V; ++v) out[v] = __ldg(bp + (int32_t)off + v * s1);
             } else {
                 const T s = __ldg(bp + off);
 #pragma unroll
@@ -172,6 +176,12 @@ struct Ctx {
         T* bp = reinterpret_cast<T*>(const_cast<char*>(base[k]));
         if (nvalid == V && L.vec == 1) {
             storeV<T, V>(bp + ob[k * obs] + r_offset(L, r), val);
+            return;
+        }
+        if (nvalid == V && L.vec == 3) {
+            const int32_t off = (int32_t)(ob[k * obs] + r_offset(L, r)), s1 = L.dig[0].stride;
+#pragma unroll
+            for (int v = 0; v < V; ++v) bp[off + v * s1] = val[v];
             return;
         }
 #pragma unroll
@@ -283,7 +293,7 @@ __device__ __forceinline__ void setup_pre(const Ctx<T, V>& c, Pre<T> (&pr)[4]) {
             const gfb_leaf& L = c.p.leaves[k];
             pr[k].ptr = reinterpret_cast<const T*>(c.base[k]) + c.ob[k * c.obs];
             pr[k].rl = L.rlin;
-            pr[k].vec = L.mode == 1 ? 0 : L.vec;  // splats take the generic (register) path
+            pr[k].vec = (L.mode == 1 || L.vec == 3) ? 0 : L.vec;  // splats / strided vectors: generic path
         }
     }
 }
@@ -459,9 +469,16 @@ __global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ 
     const uint32_t per_row = nthr / split;
     const uint32_t lane_o = tid % per_row, rs = tid / per_row;
     const uint32_t o_stride = gridDim.x * per_row * V;
+    const uint32_t ty_ext = (uint32_t)p.ty_ext, ty_div = (uint32_t)p.ty_div;
     for (uint32_t o0 = (blockIdx.x * per_row) * V; o0 < p.n_o; o0 += o_stride) {
-        const uint32_t o = o0 + lane_o * V;
-        const bool active = o < p.n_o;
+        const uint32_t olin = o0 + lane_o * V;
+        const bool active = olin < p.n_o;
+        uint32_t o = olin;
+        if (ty_ext && active) {  // transposing order: vector w -> (rest, x block, y) with y fastest
+            const uint32_t w = olin / V, xblocks = ty_div / V;
+            const uint32_t y = w % ty_ext, t = w / ty_ext, xb = t % xblocks, rest = t / xblocks;
+            o = (rest * ty_ext + y) * ty_div + xb * V;
+        }
         const int nvalid = active ? (int)min((uint32_t)V, p.n_o - o) : 0;
         T part[V];
 #pragma unroll
