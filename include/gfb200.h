@@ -130,11 +130,12 @@ typedef struct {
     int32_t npre;     /* leaves 0..npre-1 (<= 4) are loaded up front, all in flight at once */
     int32_t depth;    /* max stack depth of the program (stack lives in shared memory) */
     int32_t wpr;      /* ROW: warps cooperating on one o */
-    /* COL maps, transposing order: when ty_ext > 0, consecutive threads take
-     * vectors at consecutive values of the o-digit (o / ty_div) % ty_ext (an
-     * operand's unit-stride axis) instead of consecutive vectors, so both that
-     * operand's loads and the vector stores use whole sectors.  n_o is a
-     * multiple of ty_div * ty_ext and ty_div of the vector width. */
+    /* Maps in transposing order: when ty_ext > 0, consecutive lanes take
+     * vectors at consecutive values of the digit (i / ty_div) % ty_ext of the
+     * vector index i (o in COL, r in ROW; an operand's unit-stride axis)
+     * instead of consecutive vectors, so that operand's loads coalesce while
+     * every vector store stays whole.  The index extent is a multiple of
+     * ty_div * ty_ext and ty_div of the vector width. */
     int32_t ty_ext;
     int32_t ty_div;
     int32_t pad;

@@ -832,6 +832,11 @@ class Lowering:
             return
         grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)
+        if red_kind == 0:
+            ty = _transpose_order(prog, n_r, vec_width(et), src=1)
+            if ty is not None:
+                args.ty_ext, args.ty_div = ty
+                label += ":T"
         self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
 
     def _staged_ok(self, prog, n_o, n_r, et) -> bool:
@@ -1429,24 +1434,25 @@ def _splat_bits(b: Buffer) -> int:
     return int(bool(v))
 
 
-def _transpose_order(prog, n_o: int, V: int):
-    """(ty_ext, ty_div) for a COL map whose stores are vector-contiguous but
-    whose biggest operand is contiguous along another o-digit (a layout
-    transposition): threads then walk that digit, so the operand's loads
-    coalesce across lanes while each thread still stores whole vectors."""
+def _transpose_order(prog, n_o: int, V: int, src: int = 0):
+    """(ty_ext, ty_div) for a map whose stores are vector-contiguous but
+    whose biggest operand is contiguous along another digit of the vector
+    index (`src`: o for COL, r for ROW) — a layout transposition: lanes then
+    walk that digit, so the operand's loads coalesce across lanes while each
+    thread still stores whole vectors."""
     if os.environ.get("GFB_TRANSPOSE_ORDER", "1") != "1" or n_o % V:
         return None
     stores = [l for l in prog.leaf_specs if l.is_store]
     if not stores or any(l.vec != 1 for l in stores):
         return None
-    loads = [l for l in prog.leaf_specs if not l.is_store and l.buf.splat is None and l.vec == 0]
+    loads = [l for l in prog.leaf_specs if not l.is_store and l.buf.splat is None and l.vec in (0, 3)]
     if not loads:
         return None
-    big = max(loads, key=lambda l: l.buf.nbytes)
-    if 2 * big.buf.nbytes < max(l.buf.nbytes for l in prog.leaf_specs if l.buf.splat is None):
-        return None
-    for src, div, mod, stride in big.digits:
-        if src != 0 or abs(stride) != 1 or div < V or div % V:
+    # the strided operand with the most bytes decides (vector-contiguous ones
+    # keep whole-sector accesses either way)
+    big = max(loads, key=lambda l: (any(d[0] == src and abs(d[3]) == 1 and d[1] >= V for d in l.digits), l.buf.nbytes))
+    for dsrc, div, mod, stride in big.digits:
+        if dsrc != src or abs(stride) != 1 or div < V or div % V:
             continue
         ext = mod if mod is not None else n_o // div
         if ext >= 8 and n_o % (div * ext) == 0 and ext * div <= n_o:

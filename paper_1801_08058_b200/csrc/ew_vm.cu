@@ -432,7 +432,13 @@ __global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ 
                 Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, V, 1};
                 Pre<T> pr[4];
                 setup_pre<T, V>(c, pr);
-                for (uint32_t r = (sub * 32u + lane) * V; r < nr; r += rstep) {
+                for (uint32_t rl = (sub * 32u + lane) * V; rl < nr; rl += rstep) {
+                    uint32_t r = rl;
+                    if (p.ty_ext) {  // transposing order along r (see gfb_ew_args)
+                        const uint32_t w = rl / V, xblocks = (uint32_t)p.ty_div / V;
+                        const uint32_t y = w % (uint32_t)p.ty_ext, t = w / (uint32_t)p.ty_ext;
+                        r = ((t / xblocks) * (uint32_t)p.ty_ext + y) * (uint32_t)p.ty_div + (t % xblocks) * V;
+                    }
                     c.r = r;
                     c.nvalid = (int)min((uint32_t)V, nr - r);
                     T acc[V];
