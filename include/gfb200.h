@@ -105,9 +105,11 @@ typedef struct {
     uint64_t splat; /* raw value bits when mode == 1 */
     int32_t mode;   /* 0 = memory, 1 = splat constant (no memory access) */
     int32_t ndig;
-    int32_t vec;    /* along the launch's vector axis: 0 gather, 1 contiguous, 2 uniform */
+    int32_t vec;    /* along the launch's vector axis: 0 gather, 1 contiguous, 2 uniform,
+                       3 patterned: element v of an aligned vector at offset(v0) + dv[v] */
     int32_t rlin;   /* r-part of the offset is r * rlin (0: no r digits); -1: general digits */
     gfb_digit dig[GFB_MAX_DIGITS];
+    int32_t dv[8];  /* vec == 3: per-element offsets inside a vector (elements) */
 } gfb_leaf;
 
 /* Fused elementwise / broadcast / reduce launch (one VM program).

@@ -44,6 +44,7 @@ class Leaf(C.Structure):
         ("ref", C.c_uint64), ("splat", C.c_uint64),
         ("mode", C.c_int32), ("ndig", C.c_int32), ("vec", C.c_int32), ("rlin", C.c_int32),
         ("dig", Digit * MAX_DIGITS),
+        ("dv", C.c_int32 * 8),
     ]
 
 

@@ -430,21 +430,34 @@ def vec_class(digits, vec_src: int, is_store: bool, V: int, esize: int) -> int:
     align = max(1, (8 if esize == 1 else 16) // esize)
     own = [d for d in digits if d[0] == vec_src]
     unit = [d for d in own if d[1] == 1]
-    if any(d[1] % V for d in own if d[1] != 1):
-        return 0
-    if not unit:
-        return 0 if is_store else 2
-    if len(unit) != 1:
-        return 0
-    _, _, mod, stride = unit[0]
-    if mod is not None and mod % V:
-        return 0
-    if stride != 1:
-        # a V-aligned vector stays inside the unit digit: element v at base + v*stride
-        return 3 if abs(stride) * V < 2 ** 30 else 0
-    if any(d[3] % align for d in digits if d is not unit[0]):
-        return 0
-    return 1
+    if not any(d[1] % V for d in own if d[1] != 1):
+        if not unit:
+            return 0 if is_store else 2
+        if len(unit) == 1:
+            _, _, mod, stride = unit[0]
+            if stride == 1 and (mod is None or mod % V == 0) and not any(d[3] % align for d in digits if d is not unit[0]):
+                return 1
+    return 3 if vec_pattern(digits, vec_src, V) is not None else 0
+
+
+def vec_pattern(digits, vec_src: int, V: int):
+    """Per-element offsets inside a V-aligned vector when they do not depend
+    on the vector's position: digits with div % V == 0 are constant across
+    it, digits with V % div == 0 and (div*mod) % V == 0 advance by
+    (v // div) * stride without wrapping.  None when neither holds."""
+    dv = [0] * V
+    for src, div, mod, stride in digits:
+        if src != vec_src:
+            continue
+        if div % V == 0:
+            continue
+        if V % div or (mod is not None and (div * mod) % V):
+            return None
+        for v in range(V):
+            dv[v] += (v // div) * stride
+    if max(abs(x) for x in dv) >= 2 ** 30:
+        return None
+    return dv
 
 
 def r_linear(digits) -> int:
@@ -1845,8 +1858,10 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
     L.vec = s.vec
     L.rlin = r_linear(s.digits)
     digits = list(s.digits)
-    if s.vec == 3:  # the kernel reads the unit digit's stride from dig[0]
-        digits.sort(key=lambda d: 0 if d[1] == 1 and d[0] == s.vec_src else 1)
+    if s.vec == 3:
+        dv = vec_pattern(digits, s.vec_src, vec_width(b.et))
+        for v in range(len(L.dv)):
+            L.dv[v] = dv[v] if v < len(dv) else 0
     for i, (src, div, mod, stride) in enumerate(digits):
         d = L.dig[i]
         d.src = src

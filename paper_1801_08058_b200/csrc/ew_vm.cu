@@ -155,10 +155,9 @@ struct Ctx {
             const uint32_t off = ob[k * obs] + r_offset(L, r);
             if (L.vec == 1) {
                 loadV<T, V>(bp + off, out);
-            } else if (L.vec == 3) {  // strided vector: element v at off + v * (stride of the unit digit)
-                const int32_t s1 = L.dig[0].stride;
+            } else if (L.vec == 3) {  // patterned vector: element v at off + dv[v]
 #pragma unroll
-                for (int v = 0; v < V; ++v) out[v] = __ldg(bp + (int32_t)off + v * s1);
+                for (int v = 0; v < V; ++v) out[v] = __ldg(bp + (int32_t)off + L.dv[v]);
             } else {
                 const T s = __ldg(bp + off);
 #pragma unroll
@@ -179,9 +178,9 @@ struct Ctx {
             return;
         }
         if (nvalid == V && L.vec == 3) {
-            const int32_t off = (int32_t)(ob[k * obs] + r_offset(L, r)), s1 = L.dig[0].stride;
+            const int32_t off = (int32_t)(ob[k * obs] + r_offset(L, r));
 #pragma unroll
-            for (int v = 0; v < V; ++v) bp[off + v * s1] = val[v];
+            for (int v = 0; v < V; ++v) bp[off + L.dv[v]] = val[v];
             return;
         }
 #pragma unroll
