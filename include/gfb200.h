@@ -50,6 +50,8 @@ enum {
     GFB_K_EW_U8 = 4,
     GFB_K_EWS_F32 = 5, /* staged ROW variant: cp.async.bulk double-buffered stages (gfb_ew_args, mode 3) */
     GFB_K_EWS_F64 = 6,
+    GFB_K_EW1_F32 = 7, /* VM kernel with one element per thread (small, latency-bound launches) */
+    GFB_K_EW1_F64 = 8,
     GFB_K_DOT_F32 = 10, /* SIMT Dot, sequential k, bit-exact (gfb_dot_args) */
     GFB_K_DOT_F64 = 11,
     GFB_K_DOT_TC32 = 12, /* tcgen05 3xTF32 Dot on split planes (gfb_tc_args) */
@@ -64,6 +66,8 @@ enum {
     GFB_K_CONV_TCX128 = 23, /* as GFB_K_CONV_TCX64 with 128x128 tiles */
     GFB_K_CONV_TCGG64 = 24, /* implicit-GEMM conv, generic k-table gather (any layout, wgrad too), 128x64 (gfb_tcgg_args) */
     GFB_K_CONV_TCGG128 = 25,
+    GFB_K_DOT_TH_F32 = 26, /* SIMT Dot, one thread per output, bit-exact (gfb_dot_args) */
+    GFB_K_DOT_TH_F64 = 27,
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */

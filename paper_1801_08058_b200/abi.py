@@ -12,12 +12,14 @@ GFB_OK = 0
 
 K_EW_F32, K_EW_F64, K_EW_I64, K_EW_U8 = 1, 2, 3, 4
 K_EWS_F32, K_EWS_F64 = 5, 6
+K_EW1_F32, K_EW1_F64 = 7, 8
 K_DOT_F32, K_DOT_F64, K_DOT_TC32, K_SPLIT_TF32, K_DOT_TC32W = 10, 11, 12, 13, 14
 K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
 K_DOT_TC32P = 19
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
+K_DOT_TH_F32, K_DOT_TH_F64 = 26, 27
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
 

@@ -115,6 +115,8 @@ VM_OP = {
     OpKind.NEGATE: 5, OpKind.EXP: 6, OpKind.LOG: 7, OpKind.TANH: 8, OpKind.SIGMOID: 9, OpKind.RELU: 10,
 }
 EW_KIND = {ElementType.F32: abi.K_EW_F32, ElementType.F64: abi.K_EW_F64, ElementType.I64: abi.K_EW_I64, ElementType.BOOL: abi.K_EW_U8}
+EW1_KIND = {ElementType.F32: abi.K_EW1_F32, ElementType.F64: abi.K_EW1_F64}
+SCALAR_VM_MAX = 1 << 17  # launches of at most this many (o, r) elements use one element per thread
 INDEX_LIMIT = 1 << 31
 
 # tcgen05 Dot (csrc/gemm_tc.cu): 128x128 tiles (3 stages of 64 KB) or, for
@@ -843,14 +845,18 @@ class Lowering:
                 else:
                     self._col_launch(p2, n_o, nch, red_kind, label + ":pass2", et)
             return
+        scalar = self._scalar_ok(prog, n_o, n_r, et)
+        if scalar:
+            prog.set_vector_width(1)
         grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)
-        if red_kind == 0:
+        if red_kind == 0 and not scalar:
             ty = _transpose_order(prog, n_r, vec_width(et), src=1)
             if ty is not None:
                 args.ty_ext, args.ty_div = ty
                 label += ":T"
-        self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
+        kind = EW1_KIND[et] if scalar else EW_KIND[et]
+        self.add_launch(kind, (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label + (":s" if scalar else ""))
 
     def _staged_ok(self, prog, n_o, n_r, et) -> bool:
         if et not in (ElementType.F32, ElementType.F64) or n_r < 256:
@@ -877,9 +883,19 @@ class Lowering:
                 return False
         return True
 
+    @staticmethod
+    def _scalar_ok(prog, n_o, n_r, et) -> bool:
+        """Small launches are latency-bound: one element per thread (8x the
+        threads of the vector kernel for the same work)."""
+        return (et in (ElementType.F32, ElementType.F64) and n_o * n_r <= SCALAR_VM_MAX
+                and os.environ.get("GFB_SCALAR_VM", "1") == "1")
+
     def _col_launch(self, prog, n_o, n_r, red_kind, label, et):
         """COL: one thread per V-vector of o, r looped (split when o is short)."""
-        V = vec_width(et)
+        scalar = self._scalar_ok(prog, n_o, n_r, et)
+        if scalar:
+            prog.set_vector_width(1)
+        V = prog.V
         vectors = (n_o + V - 1) // V
         split = 1
         if red_kind and n_r > 16:
@@ -888,12 +904,13 @@ class Lowering:
         per_row = 256 // split
         grid = max(1, min((vectors + per_row - 1) // per_row, NUM_SMS * 16))
         args = prog.args(mode=2, n_o=n_o, n_r=n_r, red_kind=red_kind, split=split)
-        if red_kind == 0 and split == 1 and n_r == 1:
+        if red_kind == 0 and split == 1 and n_r == 1 and not scalar:
             ty = _transpose_order(prog, n_o, V)
             if ty is not None:
                 args.ty_ext, args.ty_div = ty
                 label += ":T"
-        self.add_launch(EW_KIND[et], (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label)
+        kind = EW1_KIND[et] if scalar else EW_KIND[et]
+        self.add_launch(kind, (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label + (":s" if scalar else ""))
 
     def emit_map(self, root: int, stores: list):
         node = self.nodes[root]
@@ -1070,6 +1087,9 @@ class Lowering:
         splits = 1
         if tiles < NUM_SMS and kblocks >= 64:
             splits = max(1, min((2 * NUM_SMS) // tiles, kblocks // 16))
+        elif tiles <= 8 and kblocks >= 16:
+            # a handful of tiles over a medium K (an MLP's first layer): spread K
+            splits = max(1, min(NUM_SMS // tiles, kblocks // 4))
         ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb)
         target = out
         if splits > 1:
@@ -1337,6 +1357,10 @@ class Lowering:
             if m <= 8 and nn >= 256:
                 kind = abi.K_DOT_SM_F32 if et is ElementType.F32 else abi.K_DOT_SM_F64
                 grid = (max(1, min((nn + 255) // 256, NUM_SMS * 16)), 1, 1)
+            elif m * nn <= 1 << 16 and (m < 64 or nn < 64):
+                # few outputs: a 64x64 tile would idle most threads
+                kind = abi.K_DOT_TH_F32 if et is ElementType.F32 else abi.K_DOT_TH_F64
+                grid = (max(1, (m * nn + 255) // 256), 1, 1)
             else:
                 kind = abi.K_DOT_F32 if et is ElementType.F32 else abi.K_DOT_F64
                 grid = ((nn + 63) // 64, (m + 63) // 64, 1)
@@ -1434,6 +1458,7 @@ class LeafSpec:
     is_store: bool
     vec: int = 0
     vec_src: int = 0  # the index source vectors run along (0 = o, 1 = r)
+    dv: list = None   # vec == 3: per-element offsets inside a vector
 
 
 def _splat_bits(b: Buffer) -> int:
@@ -1515,6 +1540,8 @@ class Program:
             spec.vec = 2 if buf.splat is not None else vec_class(digits, self.vec_src, False, self.V, buf.et.byte_size)
             if spec.vec == 1 and (buf.elem_off * buf.et.byte_size) % 16:
                 spec.vec = 0  # a constant offset breaks the vector alignment
+            if spec.vec == 3:
+                spec.dv = vec_pattern(digits, self.vec_src, self.V)
             self.leaf_index[key] = len(self.leaf_specs)
             self.leaf_specs.append(spec)
         return self.leaf_index[key]
@@ -1524,12 +1551,27 @@ class Program:
         if len(digits) > abi.MAX_DIGITS:
             raise UnsupportedOp(f"index map needs {len(digits)} digits (> {abi.MAX_DIGITS})")
         spec = LeafSpec(buf, digits, True, vec_class(digits, self.vec_src, True, self.V, buf.et.byte_size), self.vec_src)
+        if spec.vec == 3:
+            spec.dv = vec_pattern(digits, self.vec_src, self.V)
         self.leaf_specs.append(spec)
         return len(self.leaf_specs) - 1
 
     def set_red_out(self, buf: Buffer, axes):
         digits = make_digits(buf, axes, self.extents)
         self.red_out = LeafSpec(buf, digits, True, vec_class(digits, 0, True, self.V, buf.et.byte_size))
+
+    def set_vector_width(self, V: int):
+        """Re-derive every leaf's access class for a kernel variant with V
+        elements per thread-vector (the scalar VM uses V = 1)."""
+        self.V = V
+        for spec in self.leaf_specs + ([self.red_out] if self.red_out is not None else []):
+            if spec.buf.splat is not None:
+                spec.vec = 2
+                continue
+            spec.vec = vec_class(spec.digits, spec.vec_src, spec.is_store, V, spec.buf.et.byte_size)
+            if spec.vec == 1 and (spec.buf.elem_off * spec.buf.et.byte_size) % 16:
+                spec.vec = 0
+            spec.dv = vec_pattern(spec.digits, spec.vec_src, V) if spec.vec == 3 else None
 
     def emit(self, cls, op=0, k=0, swap=0):
         self.code.append((cls, op, k, swap))
@@ -1858,10 +1900,10 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
     L.vec = s.vec
     L.rlin = r_linear(s.digits)
     digits = list(s.digits)
-    if s.vec == 3:
-        dv = vec_pattern(digits, s.vec_src, vec_width(b.et))
-        for v in range(len(L.dv)):
-            L.dv[v] = dv[v] if v < len(dv) else 0
+    for v in range(len(L.dv)):
+        L.dv[v] = s.dv[v] if s.vec == 3 and s.dv is not None and v < len(s.dv) else 0
+    if s.vec == 3 and s.dv is None:
+        L.vec = 0
     for i, (src, div, mod, stride) in enumerate(digits):
         d = L.dig[i]
         d.src = src

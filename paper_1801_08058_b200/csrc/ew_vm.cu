@@ -66,8 +66,10 @@ __device__ __forceinline__ T from_bits(uint64_t b) {
 // ---- V consecutive elements, one or two 128-bit (or one 64-bit) accesses
 template <typename T, int V>
 __device__ __forceinline__ void loadV(const T* p, T (&v)[V]) {
-    static_assert(V * sizeof(T) == 32 || V * sizeof(T) == 8, "vector width");
-    if constexpr (V * sizeof(T) == 32) {
+    static_assert(V == 1 || V * sizeof(T) == 32 || V * sizeof(T) == 8, "vector width");
+    if constexpr (V == 1) {
+        v[0] = __ldg(p);
+    } else if constexpr (V * sizeof(T) == 32) {
         const int4* q = reinterpret_cast<const int4*>(p);
         int4 a = __ldg(q), b = __ldg(q + 1);
         const T* pa = reinterpret_cast<const T*>(&a);
@@ -87,7 +89,9 @@ __device__ __forceinline__ void loadV(const T* p, T (&v)[V]) {
 
 template <typename T, int V>
 __device__ __forceinline__ void storeV(T* p, const T (&v)[V]) {
-    if constexpr (V * sizeof(T) == 32) {
+    if constexpr (V == 1) {
+        *p = v[0];
+    } else if constexpr (V * sizeof(T) == 32) {
         int4 a, b;
         T* pa = reinterpret_cast<T*>(&a);
         T* pb = reinterpret_cast<T*>(&b);
@@ -847,6 +851,8 @@ template __global__ void gfb_ew_kernel<float, 8>(const __grid_constant__ gfb_ew_
 template __global__ void gfb_ew_kernel<double, 4>(const __grid_constant__ gfb_ew_args);
 template __global__ void gfb_ew_kernel<long long, 4>(const __grid_constant__ gfb_ew_args);
 template __global__ void gfb_ew_kernel<unsigned char, 8>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_kernel<float, 1>(const __grid_constant__ gfb_ew_args);
+template __global__ void gfb_ew_kernel<double, 1>(const __grid_constant__ gfb_ew_args);
 
 }  // namespace gfb
 
@@ -858,6 +864,8 @@ extern "C" const void* gfb_ew_kernel_ptr(int kind) {
         case GFB_K_EW_U8: return (const void*)gfb::gfb_ew_kernel<unsigned char, 8>;
         case GFB_K_EWS_F32: return (const void*)gfb::gfb_ew_staged_kernel<float, 2, 2>;
         case GFB_K_EWS_F64: return (const void*)gfb::gfb_ew_staged_kernel<double, 2, 2>;
+        case GFB_K_EW1_F32: return (const void*)gfb::gfb_ew_kernel<float, 1>;
+        case GFB_K_EW1_F64: return (const void*)gfb::gfb_ew_kernel<double, 1>;
     }
     return nullptr;
 }

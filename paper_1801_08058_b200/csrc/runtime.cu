@@ -167,9 +167,9 @@ struct gfb_exe {
 namespace {
 
 const void* kernel_for(uint32_t kind) {
-    if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EWS_F64) return gfb_ew_kernel_ptr((int)kind);
+    if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64) return gfb_ew_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64 ||
-        kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64)
+        kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64 || kind == GFB_K_DOT_TH_F32 || kind == GFB_K_DOT_TH_F64)
         return gfb_simt_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_DOT_TC32P || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
         kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128 || kind == GFB_K_CONV_TCGG64 ||

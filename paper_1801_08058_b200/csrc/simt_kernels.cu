@@ -113,6 +113,55 @@ __global__ void __launch_bounds__(256) gfb_dot_small_m_kernel(const __grid_const
     }
 }
 
+// Dot with few outputs (a narrow classifier layer, its gradients): one
+// thread per output element, k ascending — the reference order, bit-exact.
+// Consecutive threads take consecutive columns, so B loads coalesce and A
+// loads broadcast; the add chain runs in registers (no tile barriers).
+template <typename T>
+__global__ void __launch_bounds__(256) gfb_dot_thread_kernel(const __grid_constant__ gfb_dot_args p) {
+    const T* A = resolve<const T>(p.tab, p.a);
+    const T* B = resolve<const T>(p.tab, p.b);
+    T* C = resolve<T>(p.tab, p.c);
+    const int64_t total = p.m * p.n;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx / p.n, j = idx - i * p.n;
+        const T* a = A + i * p.a_sm;
+        const T* b = B + j * p.b_sn;
+        T acc = T(0);
+        // 16 products' operands in flight per step: the add chain is the
+        // only serial part (software-pipelined against the loads)
+        constexpr int D = 16;
+        T av[D], bv[D];
+        int64_t t = 0;
+        const int64_t kfull = p.k - p.k % D;
+        if (kfull > 0) {
+#pragma unroll
+            for (int u = 0; u < D; ++u) {
+                av[u] = __ldg(a + (int64_t)u * p.a_sk);
+                bv[u] = __ldg(b + (int64_t)u * p.b_sk);
+            }
+        }
+        for (; t < kfull; t += D) {
+            T an[D], bn[D];
+            const bool more = t + D < kfull;
+#pragma unroll
+            for (int u = 0; u < D; ++u) {
+                an[u] = more ? __ldg(a + (t + D + u) * p.a_sk) : T(0);
+                bn[u] = more ? __ldg(b + (t + D + u) * p.b_sk) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < D; ++u) acc = add_rn(acc, mul_rn(av[u], bv[u]));
+#pragma unroll
+            for (int u = 0; u < D; ++u) {
+                av[u] = an[u];
+                bv[u] = bn[u];
+            }
+        }
+        for (; t < p.k; ++t) acc = add_rn(acc, mul_rn(__ldg(a + t * p.a_sk), __ldg(b + t * p.b_sk)));
+        C[i * p.c_sm + j * p.c_sn] = acc;
+    }
+}
+
 // One thread per output element, the reference loop nest verbatim.
 template <typename T>
 __global__ void __launch_bounds__(256) gfb_conv_kernel(const __grid_constant__ gfb_conv_args p) {
@@ -182,6 +231,8 @@ template __global__ void gfb_dot_kernel<float>(const __grid_constant__ gfb_dot_a
 template __global__ void gfb_dot_kernel<double>(const __grid_constant__ gfb_dot_args);
 template __global__ void gfb_dot_small_m_kernel<float>(const __grid_constant__ gfb_dot_args);
 template __global__ void gfb_dot_small_m_kernel<double>(const __grid_constant__ gfb_dot_args);
+template __global__ void gfb_dot_thread_kernel<float>(const __grid_constant__ gfb_dot_args);
+template __global__ void gfb_dot_thread_kernel<double>(const __grid_constant__ gfb_dot_args);
 template __global__ void gfb_conv_kernel<float>(const __grid_constant__ gfb_conv_args);
 template __global__ void gfb_conv_kernel<double>(const __grid_constant__ gfb_conv_args);
 
@@ -193,6 +244,8 @@ extern "C" const void* gfb_simt_kernel_ptr(int kind) {
         case GFB_K_DOT_F64: return (const void*)gfb::gfb_dot_kernel<double>;
         case GFB_K_DOT_SM_F32: return (const void*)gfb::gfb_dot_small_m_kernel<float>;
         case GFB_K_DOT_SM_F64: return (const void*)gfb::gfb_dot_small_m_kernel<double>;
+        case GFB_K_DOT_TH_F32: return (const void*)gfb::gfb_dot_thread_kernel<float>;
+        case GFB_K_DOT_TH_F64: return (const void*)gfb::gfb_dot_thread_kernel<double>;
         case GFB_K_CONV_F32: return (const void*)gfb::gfb_conv_kernel<float>;
         case GFB_K_CONV_F64: return (const void*)gfb::gfb_conv_kernel<double>;
     }

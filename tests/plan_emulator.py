@@ -15,8 +15,8 @@ import numpy as np
 from paper_1801_08058_b200 import abi
 from paper_1801_08058_b200.compiler import decode_flat
 
-DT = {abi.K_EWS_F32: np.float32, abi.K_EWS_F64: np.float64, abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
-      abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_DOT_SM_F32: np.float32, abi.K_DOT_SM_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
+DT = {abi.K_EW1_F32: np.float32, abi.K_EW1_F64: np.float64, abi.K_EWS_F32: np.float32, abi.K_EWS_F64: np.float64, abi.K_EW_F32: np.float32, abi.K_EW_F64: np.float64, abi.K_EW_I64: np.int64, abi.K_EW_U8: np.uint8,
+      abi.K_DOT_F32: np.float32, abi.K_DOT_F64: np.float64, abi.K_DOT_SM_F32: np.float32, abi.K_DOT_SM_F64: np.float64, abi.K_DOT_TH_F32: np.float32, abi.K_DOT_TH_F64: np.float64, abi.K_CONV_F32: np.float32, abi.K_CONV_F64: np.float64}
 
 
 def _fdiv(n, mul, sh):
@@ -421,9 +421,10 @@ STAGED_U = 2  # csrc/ew_vm.cu StagedCfg<T, 2>
 
 def _run_launch(mem, L):
     dt = DT.get(L.kind)
-    if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8, abi.K_EWS_F32, abi.K_EWS_F64):
+    if L.kind in (abi.K_EW_F32, abi.K_EW_F64, abi.K_EW_I64, abi.K_EW_U8, abi.K_EWS_F32, abi.K_EWS_F64, abi.K_EW1_F32,
+                  abi.K_EW1_F64):
         run_ew(mem, L.args, dt)
-    elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64, abi.K_DOT_SM_F32, abi.K_DOT_SM_F64):
+    elif L.kind in (abi.K_DOT_F32, abi.K_DOT_F64, abi.K_DOT_SM_F32, abi.K_DOT_SM_F64, abi.K_DOT_TH_F32, abi.K_DOT_TH_F64):
         run_dot(mem, L.args, dt)
     elif L.kind in (abi.K_CONV_F32, abi.K_CONV_F64):
         run_conv(mem, L.args, dt)

@@ -52,6 +52,8 @@ def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
     (4, 6, 3001, False, False, "F32"),
     (8, 9, 700, True, False, "F32"),
     (3, 17, 1025, False, True, "F64"),
+    (128, 512, 10, False, False, "F32"),   # thread-per-output kernel
+    (40, 33, 70, True, True, "F64"),
 ])
 def test_small_m_dot_bit_exact(m, k, n, ta, tb, et):
     """Few-row Dots with k > TINY_DOT_K take the thread-per-column SIMT
@@ -67,7 +69,7 @@ def test_small_m_dot_bit_exact(m, k, n, ta, tb, et):
     dt = et.numpy_dtype
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(dt) for p in fn.parameters]
     exe = gf.compile_function(fn)
-    assert any(L.kind in (15, 16) for L in exe.lowered.launches)
+    assert any(L.kind in (15, 16, 26, 27) for L in exe.lowered.launches)
     out = gf.call(exe, [gf.tensor_from_flat(et, v.shape, v) for v in ins])[0].to_numpy()
     assert G.same_bits(out, interp.run_function(fn, ins)[0])
 
