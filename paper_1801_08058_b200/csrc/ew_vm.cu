@@ -591,8 +591,10 @@ __device__ __forceinline__ int sidx(int u, int h, int lane, int j) {
 // U = sub-vectors per thread per dispatch (a 512-float chunk per warp item;
 // smaller chunks measured 1.7x slower: per-item issue/wait overhead), NS =
 // depth of each warp's stage ring (2 measured best: deeper rings cost warps).
+// __launch_bounds__(256, 3): the shared-memory budget fits three blocks per
+// SM; the hint (62 registers) measured 150.7 -> 137.5 us on config B.
 template <typename T, int U_, int NS_>
-__global__ void __launch_bounds__(256) gfb_ew_staged_kernel(const __grid_constant__ gfb_ew_args p) {
+__global__ void __launch_bounds__(256, 3) gfb_ew_staged_kernel(const __grid_constant__ gfb_ew_args p) {
     using Cfg = StagedCfg<T, U_>;
     constexpr int HV = Cfg::HV, V = Cfg::V, U = Cfg::U, CH = Cfg::CH;
     extern __shared__ __align__(128) unsigned char dyn[];
