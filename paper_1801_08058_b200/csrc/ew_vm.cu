@@ -402,8 +402,11 @@ __device__ __forceinline__ T fold_init(int kind) {
 }
 
 // Dynamic shared memory: [ob: nleaves x blockDim u32][stack: depth*V x blockDim T][fold: V x blockDim T]
+// __launch_bounds__(256, 4): occupancy over registers.  The V-wide variants
+// spill a little at 64 registers and still measured faster on configs A, C
+// and D than at 80 / 110 registers (the general VM is latency bound).
 template <typename T, int V>
-__global__ void __launch_bounds__(256, 2) gfb_ew_kernel(const __grid_constant__ gfb_ew_args p) {
+__global__ void __launch_bounds__(256, 4) gfb_ew_kernel(const __grid_constant__ gfb_ew_args p) {
     __shared__ Shared sh;
     extern __shared__ __align__(128) unsigned char dyn[];
     const int nthr = blockDim.x, tid = threadIdx.x;
