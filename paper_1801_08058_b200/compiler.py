@@ -1065,13 +1065,25 @@ class Lowering:
         lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
         self.buf[("tc", n, name, "hi")] = hi
         self.buf[("tc", n, name, "lo")] = lo
+        if mode == 3 and len(geo) >= 15 and len(st) >= 3:
+            e0, e1, e2 = geo[12:15]
+            t0, t1, t2 = st[:3]
+            if (e1 <= 1 or t1 == e2 * t2) and (e0 <= 1 or t0 == e1 * e2 * t2):
+                mode, s_k = 0, t2  # the K digits collapse to one linear stride (e.g. NHWC pixels)
         if mode == 0 and s_k == 1 and kdim == kp and s_r % 4 == 0 and src.splat is None:
             mode = 5  # streaming, 128-bit
+        elif (mode == 0 and s_r == 1 and s_k % 4 == 0 and src.splat is None and (src.offset + src.elem_off * 4) % 16 == 0
+              and os.environ.get("GFB_SPLIT_T", "1") == "1"):
+            mode = 6  # transposing, 64x64 tiles with 128-bit loads and stores
         sa = abi.SplitArgs(rows=rows, k=kdim, kp=kp, s_r=s_r, s_k=s_k, mode=mode)
         sa.geo[:len(geo)] = list(geo)
         sa.st[:len(st)] = list(st)
-        grid = (max(1, min((rows * kp // 4 + 255) // 256, NUM_SMS * 16)), 1, 1) if mode == 5 else \
-               (((rows + 31) // 32) * ((kp + 31) // 32), 1, 1)
+        if mode == 5:
+            grid = (max(1, min((rows * kp // 4 + 255) // 256, NUM_SMS * 16)), 1, 1)
+        elif mode == 6:
+            grid = (max(1, min(((rows + 63) // 64) * ((kp + 63) // 64), NUM_SMS * 8)), 1, 1)
+        else:
+            grid = (((rows + 31) // 32) * ((kp + 31) // 32), 1, 1)
         rec = LaunchRec(abi.K_SPLIT_TF32, grid, (256, 1, 1), 0, sa, [src.key], [hi.key, lo.key], f"split_{name}#{n}")
         rec.algo_bytes = rows * kdim * 4 + 2 * rows * kp * 4
         rec.finalize = _finalize_refs(sa, {"src": src, "hi": hi, "lo": lo})

@@ -411,6 +411,55 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
         }
         return;
     }
+    if (p.mode == 6) {
+        // Transposing split of a row-contiguous source (s_r == 1, s_k % 4 == 0):
+        // 64 x 64 tiles, 128-bit loads along rows, smem transpose, 128-bit hi/lo
+        // stores along K; grid-stride over the tiles.
+        __shared__ float tt[64][65];
+        const int64_t rt = (p.rows + 63) / 64, ntiles = rt * ((p.kp + 63) / 64);
+        const int t = threadIdx.x;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t r0 = (tile % rt) * 64, k0 = (tile / rt) * 64;
+            // load: thread t covers rows r0 + 4*(t % 16) .. +3 at k0 + t / 16 + 16 i
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int kk = t / 16 + 16 * i, rr = 4 * (t % 16);
+                const int64_t k = k0 + kk, r = r0 + rr;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (k < p.k) {
+                    const float* q = src + k * p.s_k + r;
+                    if (r + 3 < p.rows) v = __ldg(reinterpret_cast<const float4*>(q));
+                    else {
+                        if (r < p.rows) v.x = q[0];
+                        if (r + 1 < p.rows) v.y = q[1];
+                        if (r + 2 < p.rows) v.z = q[2];
+                    }
+                }
+                tt[rr][kk] = v.x;
+                tt[rr + 1][kk] = v.y;
+                tt[rr + 2][kk] = v.z;
+                tt[rr + 3][kk] = v.w;
+            }
+            __syncthreads();
+            // store: thread t covers k0 + 4*(t % 16) .. +3 of rows r0 + t / 16 + 16 i
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int rr = t / 16 + 16 * i, kk = 4 * (t % 16);
+                const int64_t r = r0 + rr, k = k0 + kk;
+                if (r < p.rows && k < p.kp) {
+                    float4 h, l;
+                    split_tf32(tt[rr][kk], h.x, l.x);
+                    split_tf32(tt[rr][kk + 1], h.y, l.y);
+                    split_tf32(tt[rr][kk + 2], h.z, l.z);
+                    split_tf32(tt[rr][kk + 3], h.w, l.w);
+                    *reinterpret_cast<float4*>(hi + r * p.kp + k) = h;  // kp % 4 == 0, k % 4 == 0
+                    *reinterpret_cast<float4*>(lo + r * p.kp + k) = l;
+                }
+            }
+            __syncthreads();
+        }
+        return;
+    }
     // 1-D grid over (row tile, k tile): either extent can exceed 65535 (the
     // N*H*W rows of a 224x224 batch, or the K of a weight gradient)
     const int64_t row_tiles = (p.rows + 31) / 32;

@@ -273,7 +273,7 @@ def _gather_offsets(a, r, k):
         h, w = pp + rr - g[10], q + ss - g[11]
         valid = (h >= 0) & (h < g[2]) & (w >= 0) & (w < g[3])
         off = n * st[0] + c * st[1] + h * st[2] + w * st[3]
-    else:  # 0 plain, 5 streaming (row-contiguous)
+    else:  # 0 plain, 5 streaming (row-contiguous), 6 transposing (column-contiguous)
         off = r * a.s_r + k * a.s_k
     return np.where(valid, off, -1)
 
