@@ -269,7 +269,9 @@ typedef struct GFB_ALIGN64 {
 
 /* Implicit-GEMM convolution with a generic gather.  Row `row` = (i0, i1, i2)
  * over (*, E1, E2) starts at rowoff = i0*ro0 + i1*ro1 + i2*ro2 with spatial
- * origin (h, w) = (i1*hm + h0, i2*wm + w0).  K index k < K = (k0, k1, k2)
+ * origin (h, w) = (i1*hm + h0, i2*wm + w0), or (i0*hm + h0, i1*wm + w0) when
+ * pad0 == 1 (weight-gradient rows (r, s, c) over channel-last data, lanes
+ * along the contiguous channels).  K index k < K = (k0, k1, k2)
  * over (*, Ke1, Ke2) adds koff = kbase + k0*ko0 + k1*ko1 + k2*ko2 and
  * (dh, dw) = (k1*kh + dh0, k2*kw + dw0).  A[row, k] = a[rowoff + koff] when
  * 0 <= h + dh < H and 0 <= w + dw < W (and k < K), else 0.  Kp = K rounded

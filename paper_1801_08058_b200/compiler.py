@@ -1335,11 +1335,17 @@ class Lowering:
             if self._generic_gather_ok(xb, xs):
                 # rows (c, r, s) of the gathered data, columns = output channels
                 b = self._split(n, "b", yb, K, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
-                geo = dict(E1=R, E2=S, ro0=xs[1], ro1=xs[2], ro2=xs[3], hm=1, wm=1, h0=-pt, w0=-pl, H=H, W=W,
-                           Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
-                           kh=1, kw=1, dh0=0, dw0=0)
-                self._conv_tcgg(n, xb, b, out, Cc * R * S, K, kdim, geo, {"c_sm": os_[3], "c_sn": os_[0]}, yb,
-                                f"{node.op.wire_name}_tcgg#{n}")
+                kgeo = dict(Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
+                            kh=1, kw=1, dh0=0, dw0=0)
+                if xs[1] == 1 and Cc > 1:
+                    # channel-last data: rows (r, s, c) so lanes read contiguous channels
+                    geo = dict(E1=S, E2=Cc, ro0=xs[2], ro1=xs[3], ro2=xs[1], hm=1, wm=1, h0=-pt, w0=-pl, H=H, W=W,
+                               pad0=1, **kgeo)
+                    addr = {"c_rdiv": Cc, "c_s_hi": os_[3], "c_s_lo": os_[1], "c_sn": os_[0]}
+                else:
+                    geo = dict(E1=R, E2=S, ro0=xs[1], ro1=xs[2], ro2=xs[3], hm=1, wm=1, h0=-pt, w0=-pl, H=H, W=W, **kgeo)
+                    addr = {"c_sm": os_[3], "c_sn": os_[0]}
+                self._conv_tcgg(n, xb, b, out, Cc * R * S, K, kdim, geo, addr, yb, f"{node.op.wire_name}_tcgg#{n}")
                 return True
             a = self._split(n, "a", yb, m, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
             geo = (N, Cc, H, W, R, S, Ho, Wo, 1, 1, pt, pl)

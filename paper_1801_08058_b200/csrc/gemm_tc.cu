@@ -1025,7 +1025,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
 // any layout, weight gradients included).  A[row, k] = a[rowoff(row) +
 // koff(k)] when 0 <= h(row) + dh(k) < H and 0 <= w(row) + dw(k) < W, else 0.
 // Rows are (i0, i1, i2) over (*, E1, E2): rowoff = i0*ro0 + i1*ro1 + i2*ro2,
-// h = i1*hm + h0, w = i2*wm + w0; the K index decomposes the same way into
+// h = i1*hm + h0, w = i2*wm + w0 (rows (r, s, c), pad0 == 1: h from i0, w
+// from i1, so lanes walk contiguous channels); the K index decomposes into
 // (koff, dh, dw) (gfb_tcgg_args in gfb200.h):
 //   Conv2D:             rows (n, p, q), k = (c, r, s): dh = r - pt, dw = s - pl
 //   ConvBackpropData:   rows (n, h, w), k = (kk, r, s): dh = pt - r, dw = pl - s
@@ -1111,8 +1112,13 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
             const int64_t e12 = (int64_t)p.E1 * p.E2;
             const int64_t i0 = row / e12, rem = row - i0 * e12, i1 = rem / p.E2, i2 = rem - i1 * p.E2;
             rowoff = i0 * p.ro0 + i1 * p.ro1 + i2 * p.ro2;
-            hr = (int)(i1 * p.hm + p.h0);
-            wr = (int)(i2 * p.wm + p.w0);
+            if (p.pad0 == 1) {  // rows (r, s, c): the spatial offsets come from the two outer digits
+                hr = (int)(i0 * p.hm + p.h0);
+                wr = (int)(i1 * p.wm + p.w0);
+            } else {
+                hr = (int)(i1 * p.hm + p.h0);
+                wr = (int)(i2 * p.wm + p.w0);
+            }
         }
         const float* arow = A + rowoff;
         const uint32_t rbase = (uint32_t)g * 128u, rsw = (uint32_t)(g & 7);

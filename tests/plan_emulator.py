@@ -384,7 +384,10 @@ def run_tcgg(mem, a):
     i0, rem = row // e12, row % e12
     i1, i2 = rem // a.E2, rem % a.E2
     rowoff = i0 * a.ro0 + i1 * a.ro1 + i2 * a.ro2
-    hr, wr = i1 * a.hm + a.h0, i2 * a.wm + a.w0
+    if a.pad0 == 1:
+        hr, wr = i0 * a.hm + a.h0, i1 * a.wm + a.w0
+    else:
+        hr, wr = i1 * a.hm + a.h0, i2 * a.wm + a.w0
     k = np.arange(a.K, dtype=np.int64)
     ke12 = a.Ke1 * a.Ke2
     k0, kr = k // ke12, k % ke12

@@ -194,3 +194,21 @@ def test_tiny_dot_fused_bit_exact_on_device(m, k, n, et):
     B = rng.uniform(-1, 1, size=(k, n)).astype(et.numpy_dtype)
     out = gf.call(exe, [gf.tensor_from_flat(et, A.shape, A), gf.tensor_from_flat(et, B.shape, B)])[0].to_numpy()
     assert G.same_bits(out, interp.run_function(fn, [A, B])[0])
+
+
+@pytest.mark.parametrize("shape,pad", [((4, 64, 64, 28, 28, 3, 3), (1, 1, 1, 1)), ((2, 5, 16, 17, 15, 3, 3), (1, 0, 0, 1))])
+def test_wgrad_channel_last_matches_oracle(monkeypatch, shape, pad):
+    """Weight gradient over channel-last data on the generic-gather kernel."""
+    import test_lowering as TL
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, Ko, H, W, R, S = shape
+    fn = TL._conv_graph("wgrad", N, C, Ko, H, W, R, S, (1, 1), pad)
+    nhwc = gf.Layout((0, 2, 3, 1))
+    exe = gf.compile_function(fn, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc])
+    rng = np.random.default_rng(23)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = gf.call(exe, tens)[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5

@@ -266,3 +266,25 @@ def test_tiny_dot_fused_bit_exact(m, k, n, et):
         B.reshape(-1)[2] = np.nan
     out = emulate(h, [gf.tensor_from_flat(et, A.shape, A), gf.tensor_from_flat(et, B.shape, B)])[0]
     assert G.same_bits(out, interp.run_function(fn, [A, B])[0])
+
+
+@pytest.mark.parametrize("shape,pad", [((2, 32, 16, 9, 8, 3, 3), (1, 1, 1, 1)), ((2, 5, 8, 7, 7, 3, 3), (1, 0, 0, 1))])
+def test_wgrad_channel_last_rows_emulated(monkeypatch, shape, pad):
+    """ConvBackpropFilter over channel-last data walks rows (r, s, c) so lanes
+    read contiguous channels (gfb_tcgg_args.pad0 == 1)."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, K, H, W, R, S = shape
+    fn = _conv_graph("wgrad", N, C, K, H, W, R, S, (1, 1), pad)
+    nhwc = (0, 2, 3, 1)
+    h = host_compile(fn, optimize=False, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc])
+    tg = [L for L in h.lowered.launches if L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128)]
+    assert tg and tg[0].args.pad0 == 1, [L.label for L in h.lowered.launches]
+    rng = np.random.default_rng(21)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = emulate(h, tens)[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
