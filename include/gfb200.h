@@ -114,6 +114,8 @@ typedef struct {
     int32_t rlin;   /* r-part of the offset is r * rlin (0: no r digits); -1: general digits */
     gfb_digit dig[GFB_MAX_DIGITS];
     int32_t dv[8];  /* vec == 3: per-element offsets inside a vector (elements) */
+    int32_t same;   /* index of an earlier leaf with the same digits (its offsets are reused), or -1 */
+    int32_t pad;
 } gfb_leaf;
 
 /* Fused elementwise / broadcast / reduce launch (one VM program).

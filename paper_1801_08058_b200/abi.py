@@ -47,6 +47,7 @@ class Leaf(C.Structure):
         ("mode", C.c_int32), ("ndig", C.c_int32), ("vec", C.c_int32), ("rlin", C.c_int32),
         ("dig", Digit * MAX_DIGITS),
         ("dv", C.c_int32 * 8),
+        ("same", C.c_int32), ("pad", C.c_int32),
     ]
 
 

@@ -607,6 +607,14 @@ class Lowering:
             if node.op is OpKind.SUM or n in results or n in self.allreduce:
                 M.add(n)
                 continue
+            if (self.channels_last and node.op is OpKind.RESHAPE and len(node.output.shape) == 4
+                    and len(node.inputs_shape) != 4 and os.environ.get("GFB_RELAYOUT", "1") == "1"):
+                # a rank-changing Reshape back to 4-D (the pool composite's window
+                # merge) is where NCHW-ordered flat data meets channel-last
+                # storage: one transposing map writes it channel-last, instead
+                # of every consumer gathering across the layouts
+                M.add(n)
+                continue
             cons = self.consumers[n]
             heavy = [c for c in cons if self.is_heavy(c)]
             light = [c for c in cons if c not in heavy]
@@ -1875,10 +1883,16 @@ class Program:
         red = self.red_out
 
         def fin():
+            first = {}
             for i, s in enumerate(specs):
                 _encode_leaf(a.leaves[i], s)
+                key = tuple(s.digits) if s.buf.splat is None else None
+                a.leaves[i].same = first.get(key, -1) if key is not None else -1
+                if key is not None:
+                    first.setdefault(key, i)
             if red is not None:
                 _encode_leaf(a.red_out, red)
+                a.red_out.same = -1
         return fin
 
     def reads(self):

@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(256, 4) gfb_ew_kernel(const __grid_constant__ 
             const bool active = o < p.n_o;
             T part = fold_init<T>(kind);
             if (active) {
-                for (int k = 0; k < nleaves; ++k) ob[k * nthr] = part_offset(p.leaves[k], o, 0);
+                for (int k = 0; k < nleaves; ++k) {
+                    const int sm = p.leaves[k].same;
+                    ob[k * nthr] = sm >= 0 ? ob[sm * nthr] : part_offset(p.leaves[k], o, 0);
+                }
                 Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, V, 1};
                 Pre<T> pr[4];
                 setup_pre<T, V>(c, pr);
@@ -496,7 +499,10 @@ __global__ void __launch_bounds__(256, 4) gfb_ew_kernel(const __grid_constant__ 
 #pragma unroll
         for (int v = 0; v < V; ++v) part[v] = fold_init<T>(kind);
         if (active) {
-            for (int k = 0; k < nleaves; ++k) ob[k * nthr] = part_offset(p.leaves[k], o, 0);
+            for (int k = 0; k < nleaves; ++k) {
+                const int sm = p.leaves[k].same;  // operands sharing an index map share its offset
+                ob[k * nthr] = sm >= 0 ? ob[sm * nthr] : part_offset(p.leaves[k], o, 0);
+            }
             Ctx<T, V> c{p, sh.base, ob, nthr, stack, o, 0, nvalid, 0};
             Pre<T> pr[4];
             setup_pre<T, V>(c, pr);
