@@ -1240,9 +1240,9 @@ class Lowering:
             for k_, v_ in addr.items():
                 setattr(ta, k_, v_)
         kind = abi.K_CONV_TCGG64 if bn == 64 else abi.K_CONV_TCGG128
-        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, splits)
-        if grid[1] > 65535:
-            raise UnsupportedOp(f"convolution GEMM with {m} rows exceeds the 65535-tile grid")
+        # persistent: one CTA per SM walks the (n tile, m tile, split) items
+        items = ((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE) * splits
+        grid = (max(1, min(items, NUM_SMS)), 1, 1)
         rec = LaunchRec(kind, grid, (320, 1, 1), TCG_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [target.key], label)
         rec.flops = 2 * m * ncols * kdim
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes

@@ -1039,6 +1039,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
 // Split-K over blockIdx.z as in the plane GEMM.
 template <int BN_>
 __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kernel(const __grid_constant__ gfb_tcgg_args p) {
+    // Persistent: CTA b walks work items b, b + gridDim.x, ... over (n tile,
+    // m tile, K split); the stage ring, the raw ring and the TMEM accumulator
+    // buffers keep their counters across items, so one item's epilogue and
+    // stores overlap the next item's gather and MMAs, and TMEM allocation,
+    // barrier setup and tensor-map prefetch happen once per CTA.
     using namespace tc;
     using C_ = GCfg<BN_>;
     constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, RAW = C_::RAW;
@@ -1054,12 +1059,24 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
     const int kb_total = (int)((p.K + BK - 1) / BK);
-    const int kb_begin = p.k_splits > 1 ? (int)blockIdx.z * p.kb_per_split : 0;
-    const int kb_end = p.k_splits > 1 ? min(kb_total, kb_begin + p.kb_per_split) : kb_total;
-    const int nk = max(0, kb_end - kb_begin);
-    const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    const int ntn = (int)((p.N + BN - 1) / BN), ntm = (int)((p.M + 127) / 128);
+    const int nsplit = p.k_splits > 1 ? (int)p.k_splits : 1;
+    const int nitems = ntn * ntm * nsplit;
+    struct Item {
+        int m0, n0, z, kb_begin, nk;
+    };
+    auto item_at = [&](int it) {
+        Item r;
+        const int nt = it % ntn, mt = (it / ntn) % ntm;
+        r.z = it / (ntn * ntm);
+        r.m0 = mt * 128;
+        r.n0 = nt * BN;
+        r.kb_begin = nsplit > 1 ? r.z * p.kb_per_split : 0;
+        const int kb_end = nsplit > 1 ? min(kb_total, r.kb_begin + p.kb_per_split) : kb_total;
+        r.nk = max(0, kb_end - r.kb_begin);
+        return r;
+    };
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -1086,95 +1103,194 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int i = 0; i < nk; ++i) {
-                const int s = i % STAGES;
-                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-                unsigned char* st = smem + s * STAGE_BYTES;
-                mbar_expect_tx(&full[s], 2 * B_BYTES);
-                tma_load_2d(st + 2 * A_BYTES, p.tmap[0], (kb_begin + i) * BK, n0, &full[s]);
-                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[1], (kb_begin + i) * BK, n0, &full[s]);
+            uint32_t gk = 0;  // K-blocks issued by this CTA so far
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const Item I = item_at(it);
+                for (int i = 0; i < I.nk; ++i, ++gk) {
+                    const int s = gk % STAGES;
+                    mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], 2 * B_BYTES);
+                    tma_load_2d(st + 2 * A_BYTES, p.tmap[0], (I.kb_begin + i) * BK, I.n0, &full[s]);
+                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[1], (I.kb_begin + i) * BK, I.n0, &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, BN);
+            uint32_t gk = 0, gc = 0;  // K-blocks and accumulator chunks so far
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const Item I = item_at(it);
+                for (int i = 0; i < I.nk; ++i, ++gk) {
+                    const int s = gk % STAGES;
+                    const uint32_t chunk = gc + i / CHUNK_KB;
+                    const int b = chunk % NBUF;
+                    const bool chunk_start = i % CHUNK_KB == 0;
+                    if (chunk_start) {
+                        mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                    const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t adv = (uint64_t)(j * 32) >> 4;
+                        const uint32_t acc = !(chunk_start && j == 0);
+                        mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+                        mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+                        mma_tf32(d, al + adv, bh + adv, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                    if (i % CHUNK_KB == CHUNK_KB - 1 || i == I.nk - 1) mma_commit(&tfull[b]);
+                }
+                gc += (I.nk + CHUNK_KB - 1) / CHUNK_KB;
+            }
+        }
     } else if (warp < 2 + EPI_WARPS) {
-        float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
-        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, C, n0, p.N, p.c_sn,
-                           LinearRows{m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo});
+        // epilogue: drain each item's chunks, then store its rows
+        constexpr int EC = BN < 128 ? BN : 128;
+        const int q = warp & 3;
+        uint32_t gc = 0;
+        float* C0 = resolve<float>(p.tab, p.c);
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const Item I = item_at(it);
+            const int nchunk = (I.nk + CHUNK_KB - 1) / CHUNK_KB;
+            float acc[EC];
+#pragma unroll
+            for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            for (int c0 = 0; c0 < nchunk; ++c0) {
+                const uint32_t chunk = gc + c0;
+                const int b = chunk % NBUF;
+                mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    uint32_t r[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            }
+            gc += nchunk;
+            float* C = C0 + (nsplit > 1 ? (int64_t)I.z * p.split_stride : 0);
+            const LinearRows rows{I.m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
+            const int64_t roff = rows(q * 32 + lane);
+            if (roff >= 0) {
+                float* dst = C + roff;
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    const int col0 = I.n0 + c * 32;
+                    if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + col0 + j) =
+                                make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                    }
+                }
+            }
+        }
     } else {
-        // gather thread: one row of the tile, lanes over 32 consecutive rows
+        // gather thread: one row of the item's tile, lanes over 32 consecutive rows
         const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127 = tile row
         const float* A = resolve<const float>(p.tab, p.a);
-        const int64_t row = m0 + g;
-        int64_t rowoff = 0;
-        int hr = -(1 << 28), wr = 0;
-        if (row < p.M) {
-            const int64_t e12 = (int64_t)p.E1 * p.E2;
-            const int64_t i0 = row / e12, rem = row - i0 * e12, i1 = rem / p.E2, i2 = rem - i1 * p.E2;
-            rowoff = i0 * p.ro0 + i1 * p.ro1 + i2 * p.ro2;
-            if (p.pad0 == 1) {  // rows (r, s, c): the spatial offsets come from the two outer digits
-                hr = (int)(i0 * p.hm + p.h0);
-                wr = (int)(i1 * p.wm + p.w0);
-            } else {
-                hr = (int)(i1 * p.hm + p.h0);
-                wr = (int)(i2 * p.wm + p.w0);
-            }
-        }
-        const float* arow = A + rowoff;
         const uint32_t rbase = (uint32_t)g * 128u, rsw = (uint32_t)(g & 7);
         const int ke12 = p.Ke1 * p.Ke2;
-        auto issue = [&](int i) {
-            // lane's K index of this block -> (koff, dh, dw), broadcast by shuffles
-            const int64_t k = (int64_t)(kb_begin + i) * BK + lane;
-            int koff = 0, dh = -(1 << 28), dw = 0;
-            if (k < p.K) {
-                const int kk = (int)k, k0 = kk / ke12, kr = kk - k0 * ke12, k1 = kr / p.Ke2, k2 = kr - k1 * p.Ke2;
-                koff = (int)(p.kbase + k0 * p.ko0 + k1 * p.ko1 + k2 * p.ko2);
-                dh = k1 * p.kh + p.dh0;
-                dw = k2 * p.kw + p.dw0;
+        uint32_t gk = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const Item I = item_at(it);
+            const int64_t row = I.m0 + g;
+            int64_t rowoff = 0;
+            int hr = -(1 << 28), wr = 0;
+            if (row < p.M) {
+                const int64_t e12 = (int64_t)p.E1 * p.E2;
+                const int64_t i0 = row / e12, rem = row - i0 * e12, i1 = rem / p.E2, i2 = rem - i1 * p.E2;
+                rowoff = i0 * p.ro0 + i1 * p.ro1 + i2 * p.ro2;
+                if (p.pad0 == 1) {  // rows (r, s, c): the spatial offsets come from the two outer digits
+                    hr = (int)(i0 * p.hm + p.h0);
+                    wr = (int)(i1 * p.wm + p.w0);
+                } else {
+                    hr = (int)(i1 * p.hm + p.h0);
+                    wr = (int)(i2 * p.wm + p.w0);
+                }
             }
-            const uint32_t dst0 = su32(raw + (i % RAW) * A_BYTES) + rbase;
+            const float* arow = A + rowoff;
+            auto issue = [&](int i) {
+                // lane's K index of this block -> (koff, dh, dw), broadcast by shuffles
+                const int64_t k = (int64_t)(I.kb_begin + i) * BK + lane;
+                int koff = 0, dh = -(1 << 28), dw = 0;
+                if (k < p.K) {
+                    const int kk = (int)k, k0 = kk / ke12, kr = kk - k0 * ke12, k1 = kr / p.Ke2, k2 = kr - k1 * p.Ke2;
+                    koff = (int)(p.kbase + k0 * p.ko0 + k1 * p.ko1 + k2 * p.ko2);
+                    dh = k1 * p.kh + p.dh0;
+                    dw = k2 * p.kw + p.dw0;
+                }
+                const uint32_t dst0 = su32(raw + ((gk + i) % RAW) * A_BYTES) + rbase;
 #pragma unroll 8
-            for (int t = 0; t < 32; ++t) {
-                const int ko = __shfl_sync(0xffffffffu, koff, t);
-                const int h = hr + __shfl_sync(0xffffffffu, dh, t), w = wr + __shfl_sync(0xffffffffu, dw, t);
-                const bool ok = (uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W;
-                const float* src = ok ? arow + ko : A;
-                const uint32_t dst = dst0 + ((((uint32_t)t >> 2) ^ rsw) << 4) + ((uint32_t)t & 3u) * 4u;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4u : 0u) : "memory");
+                for (int t = 0; t < 32; ++t) {
+                    const int ko = __shfl_sync(0xffffffffu, koff, t);
+                    const int h = hr + __shfl_sync(0xffffffffu, dh, t), w = wr + __shfl_sync(0xffffffffu, dw, t);
+                    const bool ok = (uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W;
+                    const float* src = ok ? arow + ko : A;
+                    const uint32_t dst = dst0 + ((((uint32_t)t >> 2) ^ rsw) << 4) + ((uint32_t)t & 3u) * 4u;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4u : 0u) : "memory");
+                }
+            };
+#pragma unroll
+            for (int i = 0; i < RAW; ++i) {
+                if (i < I.nk) issue(i);
+                cp_async_commit();
             }
-        };
+            for (int i = 0; i < I.nk; ++i) {
+                cp_async_wait<RAW - 1>();  // this thread's row of K-block i has landed
+                const uint32_t g2 = gk + i;
+                const int s = g2 % STAGES;
+                mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
+                const uint32_t src = su32(raw + (g2 % RAW) * A_BYTES) + rbase;
+                const uint32_t dst = su32(smem + s * STAGE_BYTES) + rbase;
+                // the split is elementwise, so chunks are visited in a per-lane
+                // rotated order: 32 lanes = 32 rows 128 B apart then spread over
+                // all 32 banks instead of 4
+                float4 x[8];
 #pragma unroll
-        for (int i = 0; i < RAW; ++i) {
-            if (i < nk) issue(i);
-            cp_async_commit();
-        }
-        for (int i = 0; i < nk; ++i) {
-            cp_async_wait<RAW - 1>();  // this thread's row of K-block i has landed
-            const int s = i % STAGES;
-            mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-            const uint32_t src = su32(raw + (i % RAW) * A_BYTES) + rbase;
-            const uint32_t dst = su32(smem + s * STAGE_BYTES) + rbase;
-            // the split is elementwise, so chunks are visited in a per-lane
-            // rotated order: 32 lanes = 32 rows 128 B apart then spread over
-            // all 32 banks instead of 4
-            float4 x[8];
+                for (int j = 0; j < 8; ++j) x[j] = lds128(src + (((uint32_t)(j + g) & 7u) << 4));
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = lds128(src + (((uint32_t)(j + g) & 7u) << 4));
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t o = ((uint32_t)(j + g) & 7u) << 4;
-                const float4 h = trunc_tf32(x[j]);
-                const float4 l = make_float4(__fsub_rn(x[j].x, h.x), __fsub_rn(x[j].y, h.y), __fsub_rn(x[j].z, h.z),
-                                             __fsub_rn(x[j].w, h.w));
-                sts128(dst + o, h);
-                sts128(dst + A_BYTES + o, l);
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t o = ((uint32_t)(j + g) & 7u) << 4;
+                    const float4 h = trunc_tf32(x[j]);
+                    const float4 l = make_float4(__fsub_rn(x[j].x, h.x), __fsub_rn(x[j].y, h.y), __fsub_rn(x[j].z, h.z),
+                                                 __fsub_rn(x[j].w, h.w));
+                    sts128(dst + o, h);
+                    sts128(dst + A_BYTES + o, l);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+                if (i + RAW < I.nk) issue(i + RAW);  // reuses the raw slot just consumed
+                cp_async_commit();
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
-            if (i + RAW < nk) issue(i + RAW);
-            cp_async_commit();
+            gk += I.nk;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
