@@ -1191,9 +1191,8 @@ class Lowering:
         ta.a_strides[:] = [xs[1], xs[3], xs[2], xs[0]]
         bn = 64 if ncols <= 64 else 128
         kind = abi.K_CONV_TCX64 if bn == 64 else abi.K_CONV_TCX128
-        if tiles > 65535:
-            raise UnsupportedOp(f"TMA convolution with {tiles} pixel tiles exceeds the 65535-tile grid")
-        grid = ((ncols + bn - 1) // bn, tiles, 1)
+        # persistent: one CTA per SM walks the (column tile, pixel tile) items
+        grid = (max(1, min(tiles * ((ncols + bn - 1) // bn), NUM_SMS)), 1, 1)
         rec = LaunchRec(kind, grid, (320, 1, 1), TCX_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [out.key], label)
         rec.flops = 2 * No * Yo * Xo * ncols * kdim
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes

@@ -709,6 +709,9 @@ struct BoxRows {
 
 template <int BN_>
 __global__ void __launch_bounds__(tc::XCfg<BN_>::THREADS, 1) gfb_conv_tcx_kernel(const __grid_constant__ gfb_tcx_args p) {
+    // Persistent like gfb_conv_tcgg_kernel: CTA b walks items b, b + gridDim.x,
+    // ... over (column tile, pixel tile); ring and TMEM-buffer counters carry
+    // across items.
     using namespace tc;
     using C_ = XCfg<BN_>;
     constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF;
@@ -724,11 +727,24 @@ __global__ void __launch_bounds__(tc::XCfg<BN_>::THREADS, 1) gfb_conv_tcx_kernel
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.y;
-    const int tx = tile % p.tiles_x, ty = (tile / p.tiles_x) % p.tiles_y, tn = tile / (p.tiles_x * p.tiles_y);
-    const int x0 = tx * p.BX, y0 = ty * p.BY, n0 = tn * p.BNI, col0 = blockIdx.x * BN;
     const int nk = (int)(p.K / BK);
     const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    const int ntn = (int)((p.N + BN - 1) / BN);
+    const int npix = p.tiles_x * p.tiles_y * ((p.No + p.BNI - 1) / p.BNI);
+    const int nitems = ntn * npix;
+    struct Item {
+        int x0, y0, n0, col0;
+    };
+    auto item_at = [&](int it) {
+        Item r;
+        const int tile = it / ntn;
+        const int tx = tile % p.tiles_x, ty = (tile / p.tiles_x) % p.tiles_y, tn = tile / (p.tiles_x * p.tiles_y);
+        r.x0 = tx * p.BX;
+        r.y0 = ty * p.BY;
+        r.n0 = tn * p.BNI;
+        r.col0 = (it % ntn) * BN;
+        return r;
+    };
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -755,44 +771,137 @@ __global__ void __launch_bounds__(tc::XCfg<BN_>::THREADS, 1) gfb_conv_tcx_kernel
 
     if (warp == 0) {
         if (lane == 0) {
-            int cb = 0, r = 0, s_ = 0;
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                unsigned char* st = smem + s * STAGE_BYTES;
-                mbar_expect_tx(&afull[s], A_BYTES);
-                tma_load_4d(st, p.tmap[0], cb * 32, x0 * p.sx + p.ox + p.ksign * s_, y0 * p.sy + p.oy + p.ksign * r, n0,
-                            &afull[s]);
-                mbar_expect_tx(&full[s], 2 * B_BYTES);
-                tma_load_2d(st + 2 * A_BYTES, p.tmap[1], kb * BK, col0, &full[s]);
-                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[2], kb * BK, col0, &full[s]);
-                if (++cb == p.CB) {  // k = (r, s, c): channel blocks fastest
-                    cb = 0;
-                    if (++s_ == p.S) {
-                        s_ = 0;
-                        ++r;
+            uint32_t gk = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const Item I = item_at(it);
+                int cb = 0, r = 0, s_ = 0;
+                for (int kb = 0; kb < nk; ++kb, ++gk) {
+                    const int s = gk % STAGES;
+                    mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&afull[s], A_BYTES);
+                    tma_load_4d(st, p.tmap[0], cb * 32, I.x0 * p.sx + p.ox + p.ksign * s_, I.y0 * p.sy + p.oy + p.ksign * r,
+                                I.n0, &afull[s]);
+                    mbar_expect_tx(&full[s], 2 * B_BYTES);
+                    tma_load_2d(st + 2 * A_BYTES, p.tmap[1], kb * BK, I.col0, &full[s]);
+                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[2], kb * BK, I.col0, &full[s]);
+                    if (++cb == p.CB) {  // k = (r, s, c): channel blocks fastest
+                        cb = 0;
+                        if (++s_ == p.S) {
+                            s_ = 0;
+                            ++r;
+                        }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, BN);
+            uint32_t gk = 0, gc = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                for (int i = 0; i < nk; ++i, ++gk) {
+                    const int s = gk % STAGES;
+                    const uint32_t chunk = gc + i / CHUNK_KB;
+                    const int b = chunk % NBUF;
+                    const bool chunk_start = i % CHUNK_KB == 0;
+                    if (chunk_start) {
+                        mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                    const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t adv = (uint64_t)(j * 32) >> 4;
+                        const uint32_t acc = !(chunk_start && j == 0);
+                        mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+                        mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+                        mma_tf32(d, al + adv, bh + adv, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                    if (i % CHUNK_KB == CHUNK_KB - 1 || i == nk - 1) mma_commit(&tfull[b]);
+                }
+                gc += nchunk;
+            }
+        }
     } else if (warp < 2 + EPI_WARPS) {
-        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, resolve<float>(p.tab, p.c), col0, p.N, p.c_sn,
-                           BoxRows{n0, y0, x0, p.BX, p.BY, p.No, p.Yo, p.Xo, p.o_n, p.o_y, p.o_x});
+        constexpr int EC = BN < 128 ? BN : 128;
+        const int q = warp & 3;
+        uint32_t gc = 0;
+        float* C = resolve<float>(p.tab, p.c);
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const Item I = item_at(it);
+            float acc[EC];
+#pragma unroll
+            for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            for (int c0 = 0; c0 < nchunk; ++c0) {
+                const uint32_t chunk = gc + c0;
+                const int b = chunk % NBUF;
+                mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    uint32_t r[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            }
+            gc += nchunk;
+            const BoxRows rows{I.n0, I.y0, I.x0, p.BX, p.BY, p.No, p.Yo, p.Xo, p.o_n, p.o_y, p.o_x};
+            const int64_t roff = rows(q * 32 + lane);
+            if (roff >= 0) {
+                float* dst = C + roff;
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    const int col0 = I.col0 + c * 32;
+                    if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + col0 + j) =
+                                make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                    }
+                }
+            }
+        }
     } else {
         // converters: thread g owns 16-byte chunk (g & 7) of rows (g >> 3) + 16 i
         const int g = threadIdx.x - (2 + EPI_WARPS) * 32;
         const int j = g & 7, rb = g >> 3;
         const uint32_t swz = (uint32_t)((j ^ (rb & 7)) << 4);
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(&afull[s], (kb / STAGES) & 1);
-            split_rows(su32(smem + s * STAGE_BYTES) + swz + rb * 128, su32(smem + s * STAGE_BYTES) + swz + rb * 128,
-                       A_BYTES, p.pad0 == 0);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+        uint32_t gk = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            for (int kb = 0; kb < nk; ++kb, ++gk) {
+                const int s = gk % STAGES;
+                mbar_wait(&afull[s], (gk / STAGES) & 1);
+                split_rows(su32(smem + s * STAGE_BYTES) + swz + rb * 128, su32(smem + s * STAGE_BYTES) + swz + rb * 128,
+                           A_BYTES, p.pad0 == 0);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
