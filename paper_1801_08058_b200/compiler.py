@@ -197,6 +197,7 @@ class Buffer:
     splat: object = None  # python scalar for splat constants (no memory)
     base: object = None   # a strided view of this Buffer (shares its storage and final offset)
     elem_off: int = 0     # view origin, in elements from the base's origin
+    subaxes: dict = None  # axis -> [(extent, stride), ...] outer to inner: a flattened axis stored permuted
 
     @property
     def nbytes(self) -> int:
@@ -259,25 +260,42 @@ def _mk_axis(terms, const):
 
 
 def _split_expr(e, dims):
-    """Coordinates over `dims` (row-major) of an out axis holding e."""
+    """Coordinates over `dims` (row-major) of an out axis holding e.
+
+    A plain digit splits into sub-digits; a composite coordinate splits when
+    each of its terms lands inside one dim without carrying into the next
+    (term mul = P_i * m with m * mod <= dims[i], P_i the inner product), and
+    its constant decomposes likewise."""
     if e is None:
         return [None] * len(dims)
-    if isinstance(e, Lin):
-        if e.terms:
-            if len(e.terms) == 1 and e.const == 0 and e.terms[0][3] == 1:
-                e = e.terms[0][:3]
-            else:
-                raise Unexpressible()
+    if not isinstance(e, Lin):
+        src, div, mod = e
+        return [None if d == 1 else (src, div * _prod(dims[i + 1:]), d) for i, d in enumerate(dims)]
+    if len(e.terms) == 1 and e.const == 0 and e.terms[0][3] == 1 and e.terms[0][2] is not None \
+            and e.terms[0][2] == _prod(dims):
+        return _split_expr(e.terms[0][:3], dims)
+    inner = [_prod(dims[i + 1:]) for i in range(len(dims))]
+    per_terms = [[] for _ in dims]
+    per_max = [0] * len(dims)
+    c = e.const
+    consts = [(c // inner[i]) % d for i, d in enumerate(dims)]
+    if sum(consts[i] * inner[i] for i in range(len(dims))) != c:
+        raise Unexpressible()
+    for src, div, mod, mul in e.terms:
+        if mod is None:
+            raise Unexpressible()
+        for i in range(len(dims)):
+            if mul % inner[i] == 0 and (mul // inner[i]) * (mod - 1) < dims[i]:
+                m = mul // inner[i]
+                per_terms[i].append((src, div, mod, m))
+                per_max[i] += m * (mod - 1)
+                break
         else:
-            out, c = [], e.const
-            for i, d in enumerate(dims):
-                out.append(_mk_axis((), (c // _prod(dims[i + 1:])) % d))
-            return out
-    src, div, mod = e
-    out = []
+            raise Unexpressible()
     for i, d in enumerate(dims):
-        out.append(None if d == 1 else (src, div * _prod(dims[i + 1:]), d))
-    return out
+        if consts[i] + per_max[i] >= d:
+            raise Unexpressible()  # would carry into the next dim
+    return [_mk_axis(per_terms[i], consts[i]) for i in range(len(dims))]
 
 
 def _reshape_groups(out_shape, perm_dims):
@@ -375,12 +393,27 @@ def through_index_op(node, out_axes) -> list:
     return through_reshape(node, out_axes)
 
 
+def _axis_parts(buf: Buffer, a: int, e):
+    """(terms (src, div, mod, stride), constant element offset) of axis a at e."""
+    sub = buf.subaxes.get(a) if buf.subaxes else None
+    if sub is None:
+        terms, const = axis_terms(e)
+        return [(src, div, mod, buf.strides[a] * mul) for src, div, mod, mul in terms], const * buf.strides[a]
+    parts = _split_expr(e, [x for x, _ in sub])
+    terms, off = [], 0
+    for (x, stride), pe in zip(sub, parts):
+        t, c = axis_terms(pe)
+        terms += [(src, div, mod, stride * mul) for src, div, mod, mul in t]
+        off += c * stride
+    return terms, off
+
+
 def axes_offset(buf: Buffer, axes) -> int:
     """Element offset contributed by the constant parts of `axes`."""
     off = 0
     for a, e in enumerate(axes):
-        if isinstance(e, Lin) and buf.shape[a] > 1:
-            off += e.const * buf.strides[a]
+        if e is not None and buf.shape[a] > 1 and (isinstance(e, Lin) or (buf.subaxes and a in buf.subaxes)):
+            off += _axis_parts(buf, a, e)[1]
     return off
 
 
@@ -389,10 +422,10 @@ def make_digits(buf: Buffer, axes, extents) -> list:
     (constant parts excluded: see axes_offset)."""
     digs = []
     for a, e in enumerate(axes):
-        if e is None or buf.strides[a] == 0 or buf.shape[a] <= 1:
+        if e is None or buf.shape[a] <= 1 or (buf.strides[a] == 0 and not (buf.subaxes and a in buf.subaxes)):
             continue
-        for src, div, mod, mul in axis_terms(e)[0]:
-            digs.append([src, div, mod, buf.strides[a] * mul])
+        for src, div, mod, stride in _axis_parts(buf, a, e)[0]:
+            digs.append([src, div, mod, stride])
     digs.sort(key=lambda d: (d[0], d[1], d[2] or 0))
     same = []
     for d in digs:  # the same digit on two axes: one digit with the summed stride
@@ -695,6 +728,7 @@ class Lowering:
         self.launches: list = []
         self.const_values: dict = {}  # small constants' row-major values, by buffer key
         self._splats: dict = {}
+        self._window_factors = None
         const_blob = bytearray()
         results = list(g.results)
         result_slot = {}  # node -> output index written directly by its producer
@@ -734,7 +768,10 @@ class Lowering:
                     # kernel reads through strides, and the convolutions' gathers then
                     # find 32-channel runs contiguous (gfb_conv_tcg_kernel)
                     strides = Layout(NHWC_ORDER).strides(d.shape)
-                self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, strides, slot)
+                subaxes = self._flat_channel_last(n) if slot == abi.SLOT_ARENA else None
+                if subaxes is not None:
+                    strides = (d.shape[1], 1)
+                self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, strides, slot, subaxes=subaxes)
 
         # merge rule: a materialised node consumed only by one Sum is that Sum's side output
         side_of = {}
@@ -781,6 +818,48 @@ class Lowering:
             L.finalize()
         return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
                        {b.key: b for b in self.buf.values()}, arena_offsets=plan.offsets)
+
+    def _flat_channel_last(self, n):
+        """Sub-axis storage for a flattened pool-window matrix [k, M] under the
+        NHWC policy: M enumerates (n, c, h2, w2) (the composite's window
+        Reshape); stored as (n, h2, w2, c) it lines up with the channel-last
+        activations it is computed from and scattered back to, so neither
+        side transposes.  Only for matrices read exclusively by fused maps
+        (every access goes through index maps, never raw strides)."""
+        if not self.channels_last or os.environ.get("GFB_SUBAXES", "1") != "1":
+            return None
+        node = self.nodes[n]
+        shape = node.output.shape
+        if len(shape) != 2 or self.is_heavy(n) or n in self.allreduce:
+            return None
+        if getattr(self, "_window_factors", None) is None:
+            wf = {}
+            for x in self.order:
+                nd = self.nodes[x]
+                if nd.op is not OpKind.RESHAPE:
+                    continue
+                for shp in (tuple(nd.output.shape), tuple(nd.inputs_shape)):
+                    if len(shp) == 6 and shp[3] == 2 and shp[5] == 2:  # (n, c, h2, 2, w2, 2)
+                        wf[shp[0] * shp[1] * shp[2] * shp[4]] = (shp[0], shp[1], shp[2], shp[4])
+                    if len(shp) == 6 and shp[0] == 2 and shp[1] == 2:  # (2, 2, n, c, h2, w2)
+                        wf[shp[2] * shp[3] * shp[4] * shp[5]] = shp[2:]
+            self._window_factors = wf
+        f = self._window_factors.get(shape[1])
+        if f is None or f[1] == 1:
+            return None
+        stack, seen = [n], {n}
+        while stack:  # every reader is a fused map (possibly through index ops)
+            x = stack.pop()
+            for c in self.consumers[x]:
+                if not self.is_light(c) or c in seen:
+                    if not self.is_light(c):
+                        return None
+                    continue
+                if self.nodes[c].op in INDEX_OPS:
+                    seen.add(c)
+                    stack.append(c)
+        N_, C_, H2, W2 = f
+        return {1: [(N_, H2 * W2 * C_), (C_, 1), (H2, W2 * C_), (W2, C_)]}
 
     def splat_buffer(self, et: ElementType, value) -> Buffer:
         """A memory-less scalar operand (one per distinct bit pattern)."""
@@ -930,24 +1009,41 @@ class Lowering:
         # Iterate in the output's storage order so stores coalesce (channel-last
         # intermediates); fall back to logical order when an index op on the
         # way down cannot follow the permuted digits.
-        perm = _storage_perm(self.buf[root])
-        if perm != list(range(len(shape))):
+        buf = self.buf[root]
+        if buf.subaxes:
+            # flattened axes stored permuted: iterate their sub-digits in storage order
+            cand = []
+            for a, d in enumerate(shape):
+                if a in buf.subaxes:
+                    sub = buf.subaxes[a]
+                    for i, (x, st) in enumerate(sub):
+                        cand.append((st, a, _prod(x2 for x2, _ in sub[i + 1:]), x))
+                else:
+                    cand.append((buf.strides[a], a, 1, d))
+            dims = [(a, mul, x) for _, a, mul, x in sorted(cand, key=lambda t: -t[0])]
+        else:
+            dims = [(a, 1, shape[a]) for a in _storage_perm(buf)]
+        if [d[0] for d in dims] != list(range(len(shape))) or any(d[1] != 1 for d in dims):
             mark = len(self.launches)
             try:
-                self._emit_map_in(root, shape, perm, et, total, node)
+                self._emit_map_in(root, shape, dims, et, total, node)
                 return
             except (_Retry, Unexpressible):
                 del self.launches[mark:]
-        self._emit_map_in(root, shape, list(range(len(shape))), et, total, node)
+        self._emit_map_in(root, shape, [(a, 1, shape[a]) for a in range(len(shape))], et, total, node)
 
-    def _emit_map_in(self, root, shape, perm, et, total, node):
-        pshape = tuple(shape[a] for a in perm)
+    def _emit_map_in(self, root, shape, dims, et, total, node):
+        """One map launch iterating `dims` = [(logical axis, multiplier,
+        extent)] outer to inner (a permutation of the axes, or of the
+        sub-digits of flattened axes)."""
+        pshape = tuple(x for _, _, x in dims)
 
         def logical(axes_p):
-            ax = [None] * len(shape)
-            for i, a in enumerate(perm):
-                ax[a] = axes_p[i]
-            return ax
+            terms = [[] for _ in shape]
+            for (a, mul, _), e in zip(dims, axes_p):
+                if e is not None:
+                    terms[a] += [(t[0], t[1], t[2], t[3] * mul) for t in axis_terms(e)[0]]
+            return [_mk_axis(t, 0) for t in terms]
 
         # Split the iteration space into rows (o) x contiguous columns (r)
         # when the trailing extent is long enough for warp-wide vectors.
@@ -1698,7 +1794,7 @@ class Program:
                 if view is None:
                     raise _Retry(n)
                 return ("leaf", self.leaf(view, axes))
-            except _TooManyDigits:
+            except (_TooManyDigits, Unexpressible):
                 raise _Retry(n)  # materialise the index op: its consumers then read it plainly
         if node.op in ELEMENTWISE_UNARY:
             self.to_acc(self.value(node.inputs[0][0], axes))
