@@ -782,15 +782,17 @@ class Lowering:
                     side_of[cons[0]] = n
         merged = set(side_of.values())
 
+        groups = self._sibling_groups(merged)
+        grouped = {m for g in groups.values() for m in g[1:]}
         for n in self.order:
             node = self.nodes[n]
             if self.is_heavy(n):
                 self.emit_heavy(n)
-            elif n in self.M and n not in merged:
+            elif n in self.M and n not in merged and n not in grouped:
                 if node.op is OpKind.SUM:
                     self.emit_reduce(n, side_of.get(n))
                 else:
-                    self.emit_map(n, [n])
+                    self.emit_map(n, groups.get(n, [n]))
             if n in self.allreduce:
                 self.emit_allreduce(n)
 
@@ -999,7 +1001,66 @@ class Lowering:
         kind = EW1_KIND[et] if scalar else EW_KIND[et]
         self.add_launch(kind, (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label + (":s" if scalar else ""))
 
+    def _sibling_groups(self, merged) -> dict:
+        """Materialised maps over the same iteration space whose inputs are
+        ready when the first of them is emitted run as one launch with several
+        stores (e.g. the pool composite's four one-hot selections of one
+        window tensor: the window is read once instead of four times)."""
+        if os.environ.get("GFB_SIBLINGS", "1") != "1":
+            return {}
+        pos = {n: i for i, n in enumerate(self.order)}
+
+        def sources(n):  # nearest materialised inputs of n's fused expression
+            out, stack, seen = set(), [r for r, _ in self.g.nodes[n].inputs], set()
+            while stack:
+                x = stack.pop()
+                if x in seen:
+                    continue
+                seen.add(x)
+                if self.is_source(x):
+                    out.add(x)
+                else:
+                    stack += [r for r, _ in self.g.nodes[x].inputs]
+            return out
+
+        cands = [n for n in self.order if n in self.M and n not in merged and self.is_light(n)
+                 and self.nodes[n].op is not OpKind.SUM and n in self.buf and self.buf[n].slot == abi.SLOT_ARENA]
+        groups, taken = {}, set()
+        for i, n in enumerate(cands):
+            if n in taken:
+                continue
+            b0 = self.buf[n]
+            src0 = sources(n)
+            g = [n]
+            for m in cands[i + 1:]:
+                if m in taken or len(g) >= 4:
+                    continue
+                bm = self.buf[m]
+                if (bm.shape != b0.shape or bm.et != b0.et or bm.strides != b0.strides or bm.subaxes != b0.subaxes):
+                    continue
+                sm = sources(m)
+                # ready at n's position, and sharing an input (the point of fusing)
+                if any(pos[x] > pos[n] for x in sm if x in pos and x not in (n,)) or not (sm & src0):
+                    continue
+                if any(x in sm for x in g):
+                    continue
+                g.append(m)
+            if len(g) > 1:
+                groups[n] = g
+                taken.update(g)
+        return groups
+
     def emit_map(self, root: int, stores: list):
+        if len(stores) > 1:
+            mark = len(self.launches)
+            try:
+                self._emit_group(stores)
+                return
+            except (_Retry, UnsupportedOp, Unexpressible):
+                del self.launches[mark:]
+            for m in stores:  # too big together: one launch each
+                self.emit_map(m, [m])
+            return
         node = self.nodes[root]
         shape = tuple(node.output.shape)
         et = node.output.element_type
@@ -1031,6 +1092,35 @@ class Lowering:
             except (_Retry, Unexpressible):
                 del self.launches[mark:]
         self._emit_map_in(root, shape, [(a, 1, shape[a]) for a in range(len(shape))], et, total, node)
+
+    def _emit_group(self, roots):
+        """One flat (COL) launch storing several same-shaped maps."""
+        node = self.nodes[roots[0]]
+        shape = tuple(node.output.shape)
+        et = node.output.element_type
+        total = element_count(shape)
+        buf = self.buf[roots[0]]
+        if buf.subaxes:
+            cand = []
+            for a, d in enumerate(shape):
+                if a in buf.subaxes:
+                    sub = buf.subaxes[a]
+                    for i, (x, st) in enumerate(sub):
+                        cand.append((st, a, _prod(x2 for x2, _ in sub[i + 1:]), x))
+                else:
+                    cand.append((buf.strides[a], a, 1, d))
+            dims = [(a, mul, x) for _, a, mul, x in sorted(cand, key=lambda t: -t[0])]
+        else:
+            dims = [(a, 1, shape[a]) for a in _storage_perm(buf)]
+        pshape = tuple(x for _, _, x in dims)
+        terms_of = lambda axes_p: [_mk_axis([(t[0], t[1], t[2], t[3] * mul) for (a2, mul, _), e in zip(dims, axes_p)
+                                             if a2 == a and e is not None for t in axis_terms(e)[0]], 0)
+                                   for a in range(len(shape))]
+        prog = Program(self, extents=(total, 1), vec_src=0, et=et)
+        axes = terms_of(iteration_axes(pshape))
+        for r in roots:
+            prog.eval_store(r, axes, self.buf[r])
+        self._col_launch(prog, total, 1, 0, "map:" + "+".join(f"{self.nodes[r].op.wire_name}#{r}" for r in roots), et)
 
     def _emit_map_in(self, root, shape, dims, et, total, node):
         """One map launch iterating `dims` = [(logical axis, multiplier,
