@@ -146,7 +146,9 @@ typedef struct {
      * ty_div * ty_ext and ty_div of the vector width. */
     int32_t ty_ext;
     int32_t ty_div;
-    int32_t pad;
+    int32_t pad;      /* ROW: nonzero = cache every leaf's r-part offset once per vector
+                         (shared between leaves with equal maps); the dynamic shared
+                         memory then holds 2 x nleaves offset arrays */
     uint32_t prog[GFB_MAX_INSTR];
     gfb_leaf leaves[GFB_MAX_LEAVES];
     gfb_leaf red_out;

@@ -939,7 +939,9 @@ class Lowering:
             prog.set_vector_width(1)
         grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)
-        if red_kind == 0 and not scalar:
+        general_r = [l.digits for l in prog.leaf_specs if l.buf.splat is None and r_linear(l.digits) < 0]
+        if len(general_r) >= 2 and len(set(map(tuple, general_r))) < len(general_r):
+            args.pad = 1  # cache_r: leaves sharing an r map compute it once per vector
             ty = _transpose_order(prog, n_r, vec_width(et), src=1)
             if ty is not None:
                 args.ty_ext, args.ty_div = ty
@@ -2061,7 +2063,8 @@ class Program:
 
     def smem_bytes(self, a: abi.EwArgs, threads: int = 256) -> int:
         es = self.et.byte_size
-        return 4 * a.nleaves * threads + es * a.depth * self.V * threads + es * max(self.V * threads, 8)
+        nofs = a.nleaves * (2 if a.pad else 1)
+        return 4 * nofs * threads + es * a.depth * self.V * threads + es * max(self.V * threads, 8)
 
     def finalize_fn(self, a: abi.EwArgs):
         specs = list(self.leaf_specs)

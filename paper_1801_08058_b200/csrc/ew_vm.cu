@@ -145,6 +145,9 @@ struct Ctx {
     T* stack;                 // per-thread stack, element stride `obs`
     uint32_t o, r;
     int nvalid, vaxis;
+    const uint32_t* rb = nullptr;  // ROW with cache_r: r-part offsets of the current vector, stride `obs`
+
+    __device__ __forceinline__ uint32_t roff(const gfb_leaf& L, int k) const { return rb ? rb[k * obs] : r_offset(L, r); }
 
     __device__ __forceinline__ void load(int k, T (&out)[V]) const {
         const gfb_leaf& L = p.leaves[k];
@@ -156,7 +159,7 @@ struct Ctx {
         }
         const T* bp = reinterpret_cast<const T*>(base[k]);
         if (nvalid == V && L.vec != 0) {
-            const uint32_t off = ob[k * obs] + r_offset(L, r);
+            const uint32_t off = ob[k * obs] + roff(L, k);
             if (L.vec == 1) {
                 loadV<T, V>(bp + off, out);
             } else if (L.vec == 3) {  // patterned vector: element v at off + dv[v]
@@ -178,11 +181,11 @@ struct Ctx {
         const gfb_leaf& L = p.leaves[k];
         T* bp = reinterpret_cast<T*>(const_cast<char*>(base[k]));
         if (nvalid == V && L.vec == 1) {
-            storeV<T, V>(bp + ob[k * obs] + r_offset(L, r), val);
+            storeV<T, V>(bp + ob[k * obs] + roff(L, k), val);
             return;
         }
         if (nvalid == V && L.vec == 3) {
-            const int32_t off = (int32_t)(ob[k * obs] + r_offset(L, r));
+            const int32_t off = (int32_t)(ob[k * obs] + roff(L, k));
 #pragma unroll
             for (int v = 0; v < V; ++v) bp[off + L.dv[v]] = val[v];
             return;
@@ -412,8 +415,9 @@ __global__ void __launch_bounds__(256, 4) gfb_ew_kernel(const __grid_constant__ 
     const int nthr = blockDim.x, tid = threadIdx.x;
     const int nleaves = p.nleaves;
     uint32_t* ob = reinterpret_cast<uint32_t*>(dyn) + tid;
-    T* stack = reinterpret_cast<T*>(dyn + sizeof(uint32_t) * nleaves * nthr) + tid;
-    T* scratch = reinterpret_cast<T*>(dyn + sizeof(uint32_t) * nleaves * nthr + sizeof(T) * p.depth * V * nthr);
+    const int nofs = p.pad ? 2 * nleaves : nleaves;  // o-part (+ cached r-part) offsets
+    T* stack = reinterpret_cast<T*>(dyn + sizeof(uint32_t) * nofs * nthr) + tid;
+    T* scratch = reinterpret_cast<T*>(dyn + sizeof(uint32_t) * nofs * nthr + sizeof(T) * p.depth * V * nthr);
     if (tid < nleaves) {
         const gfb_leaf& L = p.leaves[tid];
         sh.base[tid] = L.mode == 1 ? nullptr : reinterpret_cast<const char*>(p.tab[L.ref >> 56]) + (L.ref & kOffsetMask);
@@ -450,6 +454,15 @@ __global__ void __launch_bounds__(256, 4) gfb_ew_kernel(const __grid_constant__ 
                     }
                     c.r = r;
                     c.nvalid = (int)min((uint32_t)V, nr - r);
+                    if (p.pad) {  // cache_r: general r-part offsets once per vector, shared by equal maps
+                        uint32_t* rbw = ob + nleaves * nthr;
+                        for (int k = 0; k < nleaves; ++k) {
+                            const gfb_leaf& L = p.leaves[k];
+                            const int sm = L.same;
+                            rbw[k * nthr] = sm >= 0 ? rbw[sm * nthr] : r_offset(L, r);
+                        }
+                        c.rb = rbw;
+                    }
                     T acc[V];
                     vm_run<T, V>(c, pr, acc);
                     if (kind) {
