@@ -239,6 +239,10 @@ def test_resnet_nhwc_layout_assignment_emulated():
     # ConvertLayout costs no launch of its own; channel-last storage may keep
     # a pool-window Reshape materialised that the identity plan reads as a view
     assert len(nhwc.lowered.launches) <= len(ident.lowered.launches) + 4
+    # the pool composite's flattened window matrices are stored channel-last
+    # (sub-axis storage) and its one-hot selections share one launch
+    assert any(b.subaxes for b in nhwc.lowered.buffers.values())
+    assert any("+" in L.label for L in nhwc.lowered.launches)
     _compare(emulate(nhwc, [G.tensor_of(d) for d in case["inputs"]]), case["outputs"], "resnet nhwc")
 
 
