@@ -62,7 +62,9 @@ MAX_PRELOAD = 4
 # Program construction opcodes (internal), encoded to the kernel's flat
 # jump-table opcodes by `encode_flat` (csrc/ew_vm.cu, "Flat opcodes").
 I_LOAD, I_UN, I_BIN_LEAF, I_BIN_POP, I_BIN_SELF, I_PUSH, I_STORE, I_PUSH_LOAD = 1, 2, 3, 4, 5, 6, 7, 8
+I_DOT = 9  # acc = acc + leaf[k] * leaf[k2] (two roundings): one tiny-Dot term, no operand stack
 F_LOADP, F_LOADM, F_PUSH, F_STORE, F_UN, F_BIN = 1, 5, 6, 7, 8, 16
+F_DOT = 14
 SRC_MEM, SRC_POP, SRC_SELF = 4, 5, 6
 
 
@@ -73,6 +75,9 @@ def encode_flat(code, npre: int) -> list:
         if cls == I_PUSH_LOAD:
             out.append(F_PUSH)
             cls = I_LOAD
+        if cls == I_DOT:
+            out.append(F_DOT | (k << 8) | (swap << 16))  # swap holds the second leaf
+            continue
         if cls == I_LOAD:
             out.append(F_LOADP + k if k < npre else F_LOADM | (k << 8))
         elif cls == I_PUSH:
@@ -104,6 +109,8 @@ def decode_flat(word: int):
         return ("push",)
     if code == F_STORE:
         return ("store", k)
+    if code == F_DOT:
+        return ("dot", k, (word >> 16) & 0xFF)
     if F_UN <= code < F_UN + 6:
         return ("un", code - F_UN + 5)
     rel = code - F_BIN
@@ -955,7 +962,7 @@ class Lowering:
         es = et.byte_size
         if (n_r * es) % 16:
             return False
-        if any(c[0] in (I_PUSH, I_PUSH_LOAD, I_BIN_POP) for c in prog.code):
+        if any(c[0] in (I_PUSH, I_PUSH_LOAD, I_BIN_POP, I_DOT) for c in prog.code):
             return False
         if sum(1 for l in prog.leaf_specs if not l.is_store) > MAX_PRELOAD:
             return False  # every operand must be a preloaded leaf
@@ -1825,12 +1832,19 @@ class Program:
             return self.need(node.inputs[0][0], axes)
         if n in low.tiny:
             a, b = node.inputs[0][0], node.inputs[1][0]
+            terms = _dot_term_axes(node, axes, low)
+            if terms and all(self.is_plain(a, aa) and self.is_plain(b, ba) for aa, ba in terms):
+                return 0
             worst = 0
             for t, (aa, ba) in enumerate(_dot_term_axes(node, axes, low)):
                 na, nb = self.need(a, aa), self.need(b, ba)
                 term = max(na, nb) if (self.is_plain(a, aa) or self.is_plain(b, ba)) else min(max(na, 1 + nb), max(nb, 1 + na))
                 worst = max(worst, term + (1 if t else 0))
             return worst
+        if node.op is OpKind.ADD:
+            fold = self._add_dot1(n, axes)
+            if fold is not None:
+                return self.need(fold[0], axes)
         if node.op in ELEMENTWISE_BINARY:
             a, b = node.inputs[0][0], node.inputs[1][0]
             if a == b:
@@ -1897,6 +1911,12 @@ class Program:
             a, b = node.inputs[0][0], node.inputs[1][0]
             mul, add = VM_OP[OpKind.MULTIPLY], VM_OP[OpKind.ADD]
             terms = _dot_term_axes(node, axes, low)
+            if terms and all(self.is_plain(a, aa) and self.is_plain(b, ba) for aa, ba in terms):
+                # every operand a plain leaf: one two-operand multiply-add per term
+                self.emit(I_LOAD, k=self.leaf(low.splat_buffer(node.output.element_type, 0.0), []))
+                for aa, ba in terms:
+                    self.emit(I_DOT, 0, self.value(a, aa)[1], self.value(b, ba)[1])
+                return ("acc",)
             if not terms:  # empty contraction: the reference's 0.0
                 self.emit(I_LOAD, k=self.leaf(low.splat_buffer(node.output.element_type, 0.0), []))
             for t, (aa, ba) in enumerate(terms):
@@ -1919,6 +1939,16 @@ class Program:
                     zero = self.leaf(low.splat_buffer(node.output.element_type, 0.0), [])
                     self.emit(I_BIN_LEAF, add, zero, 1)  # acc = 0 + term
             return ("acc",)
+        if node.op is OpKind.ADD:
+            fold = self._add_dot1(n, axes)
+            if fold is not None:
+                # x + (0 + p) == x + p when x can never be -0: append the term
+                other, t = fold
+                self.to_acc(self.value(other, axes))
+                (aa, ba) = t
+                d = low.nodes[t[2]]
+                self.emit(I_DOT, 0, self.value(d.inputs[0][0], aa)[1], self.value(d.inputs[1][0], ba)[1])
+                return ("acc",)
         if node.op in ELEMENTWISE_BINARY:
             a, b = node.inputs[0][0], node.inputs[1][0]
             op = VM_OP[node.op]
@@ -1954,6 +1984,37 @@ class Program:
                 self.emit(I_BIN_POP, op, 0, 1)  # acc = op(acc=a, pop=b)
             return ("acc",)
         raise _Retry(n)
+
+    def _never_neg_zero(self, n, depth=0) -> bool:
+        """Values of n are never -0: a tiny Dot starts its sum at +0, and a sum
+        is -0 only when both addends are."""
+        low = self.low
+        node = low.nodes[n]
+        if n in low.tiny:
+            return True
+        if node.op is OpKind.ADD and depth < 8:
+            return any(self._never_neg_zero(r, depth + 1) for r, _ in node.inputs)
+        return False
+
+    def _add_dot1(self, n, axes):
+        """(other operand, (a axes, b axes, dot node)) when Add n has a k = 1
+        tiny-Dot operand computed inline from plain leaves and the other
+        operand can never be -0, else None."""
+        low = self.low
+        if n in low.buf and n not in self._inline:
+            return None
+        x, y = (r for r, _ in low.nodes[n].inputs)
+        for d, other in ((y, x), (x, y)):
+            if d == other or d not in low.tiny or d in low.buf:
+                continue
+            dn = low.nodes[d]
+            if low.g.nodes[dn.inputs[0][0]].output.shape[1] != 1:
+                continue
+            (aa, ba), = _dot_term_axes(dn, axes, low)
+            if self.is_plain(dn.inputs[0][0], aa) and self.is_plain(dn.inputs[1][0], ba) \
+                    and self._never_neg_zero(other):
+                return other, (aa, ba, d)
+        return None
 
     def to_acc(self, r):
         if r[0] == "leaf":
@@ -2012,13 +2073,25 @@ class Program:
         loads = [i for i, s in enumerate(self.leaf_specs) if not s.is_store]
         stores = [i for i, s in enumerate(self.leaf_specs) if s.is_store]
         uses = {i: 0 for i in loads}
-        for cls, _, k, _ in self.code:
+        for cls, _, k, k2 in self.code:
             if cls in (I_LOAD, I_BIN_LEAF, I_PUSH_LOAD) and k in uses:
                 uses[k] += 1
-        mem = [i for i in loads if self.leaf_specs[i].buf.splat is None]
+            if cls == I_DOT:
+                for x in (k, k2):
+                    if x in uses:
+                        uses[x] += 1
+        dot_only = set()
+        other = set()
+        for cls, _, k, k2 in self.code:
+            if cls == I_DOT:
+                dot_only.update((k, k2))
+            elif cls in (I_LOAD, I_BIN_LEAF, I_PUSH_LOAD):
+                other.add(k)
+        dot_only -= other  # read only by multiply-adds: loaded there, never preloaded
+        mem = [i for i in loads if self.leaf_specs[i].buf.splat is None and i not in dot_only]
         mem.sort(key=lambda i: -self.leaf_specs[i].buf.nbytes)
         pre = mem[:MAX_PRELOAD]
-        pre += [i for i in loads if i not in pre][: MAX_PRELOAD - len(pre)]  # splats ride along
+        pre += [i for i in loads if i not in pre and i not in dot_only][: MAX_PRELOAD - len(pre)]  # splats ride along
         rest = [i for i in loads if i not in pre]
         new_order = pre + rest + stores
         if len(new_order) > abi.MAX_LEAVES:
@@ -2029,6 +2102,8 @@ class Program:
         for cls, op, k, swap in self.code:
             if cls in (I_LOAD, I_BIN_LEAF, I_STORE, I_PUSH_LOAD):
                 k = remap[k]
+            elif cls == I_DOT:
+                k, swap = remap[k], remap[swap]
             code.append((cls, op, k, swap))
         self.code = code
         if len(self.code) > abi.MAX_INSTR:

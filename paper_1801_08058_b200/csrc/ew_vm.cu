@@ -45,7 +45,7 @@ namespace gfb {
 //   8..13  acc = unary(acc)         (Negate, Exp, Log, Tanh, Sigmoid, Relu)
 //   16 + ((src * 5 + op) * 2 + s)   acc = s ? op(B, acc) : op(acc, B),
 //          src 0..3 = pre[src], 4 = load(leaf), 5 = pop, 6 = acc itself
-enum : uint32_t { F_LOADP = 1, F_LOADM = 5, F_PUSH = 6, F_STORE = 7, F_UN = 8, F_BIN = 16 };
+enum : uint32_t { F_LOADP = 1, F_LOADM = 5, F_PUSH = 6, F_STORE = 7, F_UN = 8, F_DOT = 14, F_BIN = 16 };
 enum : uint32_t {
     OP_ADD = 0, OP_SUB, OP_MUL, OP_DIV, OP_MAX, OP_NEG, OP_EXP, OP_LOG, OP_TANH, OP_SIGMOID, OP_RELU,
 };
@@ -370,6 +370,15 @@ __device__ __forceinline__ void vm_run(const Ctx<T, V>& c, const Pre<T> (&pr)[4]
                 ++sp;
                 break;
             case F_STORE: c.store(k, acc); break;
+            case F_DOT: {  // acc = acc + leaf[k] * leaf[k2]: one tiny-Dot term (two roundings)
+                const int k2 = (int)((ins >> 16) & 0xffu);
+                T a[V], b[V];  // the compiler keeps multiply-add operands out of the preload set
+                c.load(k, a);
+                c.load(k2, b);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = bin1<T>(OP_ADD, acc[v], bin1<T>(OP_MUL, a[v], b[v]));
+                break;
+            }
             GFB_UN(OP_NEG) GFB_UN(OP_EXP) GFB_UN(OP_LOG) GFB_UN(OP_TANH) GFB_UN(OP_SIGMOID) GFB_UN(OP_RELU)
             GFB_OPS(0, GFB_PREP_NONE, p0)
             GFB_OPS(1, GFB_PREP_NONE, p1)

@@ -138,6 +138,9 @@ def run_ew(mem, a, dt):
             mem.view(L.ref, dt)[leaf_offsets(L, o, r)] = acc
         elif ins[0] == "un":
             acc = _un(ins[1], acc, dt)
+        elif ins[0] == "dot":  # acc = acc + a * b, two roundings
+            va, vb = load(ins[1]), load(ins[2])
+            acc = _bin(0, acc, _bin(2, va, vb, dt), dt)
         else:
             _, src, op, sw, k = ins
             if src < 4:
