@@ -28,7 +28,16 @@
 #ifndef GFB200_H
 #define GFB200_H
 
+#ifdef __CUDACC_RTC__ /* runtime-compiled kernels (jit.py): fixed-width types from libcu++ */
+#include <cuda/std/cstdint>
+typedef cuda::std::int32_t int32_t;
+typedef cuda::std::int64_t int64_t;
+typedef cuda::std::uint8_t uint8_t;
+typedef cuda::std::uint32_t uint32_t;
+typedef cuda::std::uint64_t uint64_t;
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -345,6 +354,14 @@ int gfb_exe_destroy(gfb_exe* exe);
 int gfb_exe_num_launches(const gfb_exe* exe);
 /* Launch only record `index` of the plan (profiling / per-kernel timing). */
 int gfb_exe_run_one(gfb_exe* exe, uint32_t index, void* const* inputs, void* const* outputs, void* stream);
+
+/* Runtime-compiled kernels (paper_1801_08058_b200/jit.py).  gfb_kernel_load
+ * loads an sm_100a cubin and returns the handle of its kernel `name`;
+ * gfb_exe_set_kernel makes launch `index` (a GFB_K_EW* record, same grid,
+ * block and argument block) use that kernel with `smem` bytes of dynamic
+ * shared memory.  The executable's CUDA graph is re-captured on its next run. */
+int gfb_kernel_load(const void* cubin, const char* name, const void** kernel);
+int gfb_exe_set_kernel(gfb_exe* exe, uint32_t index, const void* kernel, uint32_t smem);
 
 /* NCCL communicator, one per process / GPU.  `unique_id` is the 128-byte
  * ncclUniqueId created by rank 0 with gfb_comm_unique_id and shared by the

@@ -1,9 +1,19 @@
 // Shared device helpers for the gfb200 kernels (sm_100a).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 #include "gfb200.h"
+
+// Loops over digits / program words: kept rolled in the generic kernels,
+// unrolled (and folded) when the structure is a compile-time constant.
+#ifdef __CUDACC_RTC__
+#define GFB_LOOP _Pragma("unroll")
+#else
+#define GFB_LOOP _Pragma("unroll 1")
+#endif
 
 namespace gfb {
 
@@ -31,7 +41,7 @@ __device__ __forceinline__ uint32_t digit_coord(const gfb_digit& d, uint32_t o, 
 __device__ __forceinline__ uint32_t leaf_offset(const gfb_leaf& L, uint32_t o, uint32_t r) {
     uint32_t off = 0;
     const int n = L.ndig;
-#pragma unroll 1
+    GFB_LOOP
     for (int i = 0; i < n; ++i) off += digit_coord(L.dig[i], o, r) * (uint32_t)L.dig[i].stride;
     return off;
 }

@@ -407,6 +407,32 @@ int gfb_exe_run_one(gfb_exe* e, uint32_t index, void* const* inputs, void* const
 
 int gfb_exe_num_launches(const gfb_exe* e) { return e ? (int)e->launches.size() : 0; }
 
+int gfb_kernel_load(const void* cubin, const char* name, const void** kernel) {
+    if (!cubin || !name || !kernel) return fail(GFB_ERR_INVALID, "null argument");
+    cudaLibrary_t lib = nullptr;
+    CUDA_TRY(cudaLibraryLoadData(&lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0));
+    cudaKernel_t k = nullptr;
+    CUDA_TRY(cudaLibraryGetKernel(&k, lib, name));
+    *kernel = (const void*)k;  // the library stays loaded for the life of the process
+    return GFB_OK;
+}
+
+int gfb_exe_set_kernel(gfb_exe* e, uint32_t index, const void* kernel, uint32_t smem) {
+    if (!e || index >= e->launches.size() || !kernel) return fail(GFB_ERR_INVALID, "bad launch index or kernel");
+    std::lock_guard<std::mutex> lk(e->mu);
+    const uint32_t kind = e->launches[index].kind;
+    if (!(kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64))
+        return fail(GFB_ERR_INVALID, "only fused elementwise launches take a runtime-compiled kernel");
+    if (smem >= 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    e->fns[index] = kernel;
+    e->launches[index].smem = smem;
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    return GFB_OK;
+}
+
 int gfb_exe_destroy(gfb_exe* e) {
     if (!e) return GFB_OK;
     cudaStreamSynchronize(cudaStreamPerThread);

@@ -30,7 +30,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import abi
+from . import abi, jit
 from .compiler import Lowered, lower
 from .errors import BackendUnavailable, DeviceError, SignatureMismatch, ValidationFailure
 from .ir import ConstantData, Function, OpKind, TensorDescriptor, reachable_from_results, topological_order, validate_function
@@ -77,6 +77,8 @@ def lib():
         L.gfb_comm_unique_id.argtypes = [vp]
         L.gfb_comm_create.argtypes = [i32, i32, vp, C.POINTER(vp)]
         L.gfb_comm_destroy.argtypes = [vp]
+        L.gfb_kernel_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
+        L.gfb_exe_set_kernel.argtypes = [vp, u32, vp, u32]
         _LIB = L
         return L
 
@@ -157,6 +159,8 @@ class DeviceProgram:
         ensure_device()
         check(lib().gfb_exe_create(C.byref(plan), C.byref(handle)), "gfb_exe_create")
         self.handle = handle
+        # launches running a runtime-specialised kernel (jit.py) instead of the generic VM
+        self.jit_launches = jit.specialise(lib(), handle, lowered.launches, blob, recs) if jit.enabled() else []
 
     def run(self, in_ptrs: list, out_ptrs: list, stream=None):
         ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
