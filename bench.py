@@ -280,7 +280,8 @@ def bench_chain(args, ws, rank, local):
                 "call_value": ws * nbytes / call_s / 1e9, "call_ms_per_step": call_s * 1e3,
                 "call_api": "paper_1801_08058_b200.call(exe, pinned host tensors, out=pinned host tensors)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": _traffic("B"), "kernel": exe.lowered.launches[dom].label, "kernel_ms": kernel_ms,
+                     "traffic": _traffic("B"), "kernel": exe.lowered.launches[dom].label + (":jit" if dom in prog.jit_launches else ""),
+                     "kernel_ms": kernel_ms,
                      "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),

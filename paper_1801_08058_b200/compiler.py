@@ -98,6 +98,14 @@ def encode_flat(code, npre: int) -> list:
     return out
 
 
+def _staged_policy() -> str:
+    """GFB_STAGED: "1" staged kernel wherever it applies, "0" never, "auto"
+    (default with runtime specialisation) only for few long rows."""
+    from . import jit
+
+    return os.environ.get("GFB_STAGED", "auto" if jit.enabled() else "1")
+
+
 def decode_flat(word: int):
     """Kernel word -> (kind, arg...) for the host emulator."""
     code, k = word & 0xFF, (word >> 8) & 0xFF
@@ -957,7 +965,14 @@ class Lowering:
         self.add_launch(kind, (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label + (":s" if scalar else ""))
 
     def _staged_ok(self, prog, n_o, n_r, et) -> bool:
-        if et not in (ElementType.F32, ElementType.F64) or n_r < 256:
+        # With runtime specialisation (jit.py) a generated ROW kernel beats the
+        # staged interpreter on every measured workload (B, A, C, D); the
+        # staged kernel keeps the few-long-rows case, where its chunk-wise
+        # split fills the GPU and warps-per-row cannot.
+        policy = _staged_policy()
+        if et not in (ElementType.F32, ElementType.F64) or n_r < 256 or policy == "0":
+            return False
+        if policy == "auto" and not (n_o < 2 * NUM_SMS and n_r >= 4096):
             return False
         es = et.byte_size
         if (n_r * es) % 16:

@@ -50,8 +50,8 @@ KINDS = {
 }
 OPTIONS = ["-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo"]
 ENTRY = b"gfb_jit_ew"
-# launches moving fewer bytes than this stay on the generic kernel (not worth a compile)
-MIN_BYTES = int(os.environ.get("GFB_JIT_MIN_BYTES", 1 << 20))
+# launches moving fewer bytes than this stay on the generic kernel
+MIN_BYTES = int(os.environ.get("GFB_JIT_MIN_BYTES", 0))
 
 _lock = threading.Lock()
 _nvrtc = None

@@ -11,7 +11,7 @@ for w in A C D E G H; do
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_B.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gfb_ew_staged -s 3 -c 1 -o $OUT/prof_B \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gfb_jit_ew -s 3 -c 1 -o $OUT/prof_B \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_B.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gfb_gemm_tc -s 1 -c 1 -o $OUT/prof_G \
   python bench.py --workload G --steps 2 --warmup 3 > $OUT/ncu_G.log 2>&1

@@ -82,6 +82,7 @@ def test_workload_jit_bit_identical(name, monkeypatch):
     fn = G.fn_of(case["fn"])
     tensors = [G.tensor_of(d) for d in case["inputs"]]
     layout = "nhwc" if name.startswith("resnet") else "identity"
+    monkeypatch.setenv("GFB_STAGED", "auto")  # the same plan with and without specialisation
     monkeypatch.setattr(jit, "MIN_BYTES", 0)
     exe, spec = _run(fn, tensors, layout)
     assert exe.program().jit_launches, "no launch was specialised"
@@ -94,6 +95,7 @@ def test_workload_jit_bit_identical(name, monkeypatch):
 
 @pytest.mark.gpu
 def test_corpus_jit_bit_identical(monkeypatch):
+    monkeypatch.setenv("GFB_STAGED", "auto")
     monkeypatch.setattr(jit, "MIN_BYTES", 0)
     cases = G.load("corpus.json.gz")[::4]
     spec = [_run(G.fn_of(c["fn"]), [G.tensor_of(d) for d in c["inputs"]])[1] for c in cases]
