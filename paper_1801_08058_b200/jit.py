@@ -493,10 +493,10 @@ def _kernel(lib, cubin: bytes):
 
 def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = None) -> int:
     """Compile and install specialised kernels for the eligible launches of
-    one executable; returns how many were replaced."""
+    one executable; returns the indices of the launches replaced."""
     todo = [i for i, L in enumerate(launches) if eligible(L)]
     if not todo:
-        return 0
+        return []
 
     def build(i):
         r = recs[i]
