@@ -142,6 +142,7 @@ TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
+TCGG_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu GCfg::THREADS_GG
 TCG_SMEM = {bn: (2 if bn == 128 else 3) * (2 * 128 + 2 * bn) * 32 * 4 + 4 * 128 * 32 * 4 + 128 * 16 + 256 + 1024
             for bn in (64, 128)}
 
@@ -1452,7 +1453,7 @@ class Lowering:
         # persistent: one CTA per SM walks the (n tile, m tile, split) items
         items = ((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE) * splits
         grid = (max(1, min(items, NUM_SMS)), 1, 1)
-        rec = LaunchRec(kind, grid, (320, 1, 1), TCG_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [target.key], label)
+        rec = LaunchRec(kind, grid, (TCGG_THREADS[bn], 1, 1), TCG_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [target.key], label)
         rec.flops = 2 * m * ncols * kdim
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
         rec.finalize = _finalize_refs(ta, {"c": target, "a": xb, "b_hi": bhi, "b_lo": blo})

@@ -522,6 +522,11 @@ struct GCfg {
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int EPI_WARPS = 4, GATHER_WARPS = 4;
     static constexpr int THREADS = 64 + 32 * (EPI_WARPS + GATHER_WARPS);
+    // generic gather (tcgg) at BN = 64: two warps per 32 rows, each taking 16
+    // of a K-block's 32 columns (the 4-byte gather is latency bound; at
+    // BN = 128 the epilogue's registers leave room for one warp per 32 rows)
+    static constexpr int GATHER_WARPS_GG = BN_ == 64 ? 8 : 4;
+    static constexpr int THREADS_GG = 64 + 32 * (EPI_WARPS + GATHER_WARPS_GG);
     static constexpr int ROWTAB = BM * 16;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RAW * A_BYTES + ROWTAB + 256 + 1024;
 };
@@ -1147,7 +1152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
 // splits its own row into TF32 hi/lo.  B (filter or δ planes) by TMA.
 // Split-K over blockIdx.z as in the plane GEMM.
 template <int BN_>
-__global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kernel(const __grid_constant__ gfb_tcgg_args p) {
+__global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS_GG, 1) gfb_conv_tcgg_kernel(const __grid_constant__ gfb_tcgg_args p) {
     // Persistent: CTA b walks work items b, b + gridDim.x, ... over (n tile,
     // m tile, K split); the stage ring, the raw ring and the TMEM accumulator
     // buffers keep their counters across items, so one item's epilogue and
@@ -1157,7 +1162,7 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
     using C_ = GCfg<BN_>;
     constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, RAW = C_::RAW;
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
-    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GATHER_WARPS = C_::GATHER_WARPS;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GATHER_WARPS = C_::GATHER_WARPS_GG;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* raw = smem + STAGES * STAGE_BYTES;
@@ -1321,8 +1326,11 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
             }
         }
     } else {
-        // gather thread: one row of the item's tile, lanes over 32 consecutive rows
-        const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127 = tile row
+        // gather thread: one row of the item's tile, lanes over 32 consecutive
+        // rows; `half` picks the 16 columns of each K-block it gathers and splits
+        constexpr int NH = GATHER_WARPS / 4, CW = 32 / NH, CCH = 8 / NH;  // column groups, columns / chunks each
+        const int gt = threadIdx.x - (2 + EPI_WARPS) * 32;
+        const int g = gt & 127, half = gt >> 7;  // tile row, column group
         const float* A = resolve<const float>(p.tab, p.a);
         const uint32_t rbase = (uint32_t)g * 128u, rsw = (uint32_t)(g & 7);
         const int ke12 = p.Ke1 * p.Ke2;
@@ -1357,7 +1365,7 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
                 }
                 const uint32_t dst0 = su32(raw + ((gk + i) % RAW) * A_BYTES) + rbase;
 #pragma unroll 8
-                for (int t = 0; t < 32; ++t) {
+                for (int t = half * CW; t < half * CW + CW; ++t) {
                     const int ko = __shfl_sync(0xffffffffu, koff, t);
                     const int h = hr + __shfl_sync(0xffffffffu, dh, t), w = wr + __shfl_sync(0xffffffffu, dw, t);
                     const bool ok = (uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W;
@@ -1378,15 +1386,16 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcgg_kerne
                 mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
                 const uint32_t src = su32(raw + (g2 % RAW) * A_BYTES) + rbase;
                 const uint32_t dst = su32(smem + s * STAGE_BYTES) + rbase;
-                // the split is elementwise, so chunks are visited in a per-lane
-                // rotated order: 32 lanes = 32 rows 128 B apart then spread over
-                // all 32 banks instead of 4
-                float4 x[8];
+                // the split is elementwise and the raw ring has the stage's
+                // swizzle, so each half splits the physical 16-byte slots of its
+                // logical chunks in place: for fixed j the 32 lanes (rows 128 B
+                // apart) hit 8 distinct slots, the 4-wavefront minimum
+                float4 x[CCH];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[j] = lds128(src + (((uint32_t)(j + g) & 7u) << 4));
+                for (int j = 0; j < CCH; ++j) x[j] = lds128(src + (((uint32_t)(half * CCH + j) ^ rsw) << 4));
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t o = ((uint32_t)(j + g) & 7u) << 4;
+                for (int j = 0; j < CCH; ++j) {
+                    const uint32_t o = ((uint32_t)(half * CCH + j) ^ rsw) << 4;
                     const float4 h = trunc_tf32(x[j]);
                     const float4 l = make_float4(__fsub_rn(x[j].x, h.x), __fsub_rn(x[j].y, h.y), __fsub_rn(x[j].z, h.z),
                                                  __fsub_rn(x[j].w, h.w));
