@@ -75,6 +75,8 @@ enum {
     GFB_K_CONV_TCX128 = 23, /* as GFB_K_CONV_TCX64 with 128x128 tiles */
     GFB_K_CONV_TCGG64 = 24, /* implicit-GEMM conv, generic k-table gather (any layout, wgrad too), 128x64 (gfb_tcgg_args) */
     GFB_K_CONV_TCGG128 = 25,
+    GFB_K_CONV_TCGW64 = 28,  /* weight gradient over channel-last data, MN-major 16-byte gathers, in-kernel TF32 split of both operands, 128x64 (gfb_tcgw_args) */
+    GFB_K_CONV_TCGW128 = 29,
     GFB_K_DOT_TH_F32 = 26, /* SIMT Dot, one thread per output, bit-exact (gfb_dot_args) */
     GFB_K_DOT_TH_F64 = 27,
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
@@ -304,6 +306,27 @@ typedef struct GFB_ALIGN64 {
     int32_t Ke1, Ke2, kh, kw, dh0, dw0, kb_per_split, pad0;
     uint64_t tmap[2][16]; /* offset 256 */
 } gfb_tcgg_args;
+
+/* Weight gradient dW[(r, s, c), k] = sum over pixels (n, p, q) of
+ * x[n, p + r - pt, q + s - pl, c] * dy[(n, p, q), k] for channel-last x and
+ * dy (c and k contiguous, C and K multiples of 4).  Rows (r, s, c) over
+ * (*, E1 = S, E2 = C): rowoff = i0*ro0 + i1*ro1 + i2*ro2, spatial origin
+ * (i0 + h0, i1 + w0).  Pixel k = (k0, k1, k2) over (*, Ke1, Ke2): x offset
+ * kbase + k0*ko0 + k1*ko1 + k2*ko2 at (dh, dw) = (k1, k2); dy offset
+ * k0*yo0 + k1*yo1 + k2*yo2 (+ column).  Both operands are loaded raw with
+ * 16-byte cp.async into MN-major tiles and split into TF32 hi/lo in shared
+ * memory.  Output and split-K as gfb_tcgg_args. */
+typedef struct {
+    const void* const* tab;
+    uint64_t c, a, b;
+    int64_t M, N, K;
+    int64_t c_sm, c_sn, c_rdiv, c_s_hi, c_s_lo;
+    int64_t ro0, ro1, ro2;
+    int64_t ko0, ko1, ko2, kbase;
+    int64_t yo0, yo1, yo2;
+    int64_t k_splits, split_stride;
+    int32_t E1, E2, h0, w0, H, W, Ke1, Ke2, kb_per_split, pad;
+} gfb_tcgw_args;
 
 typedef struct {
     const void* const* tab;

@@ -19,6 +19,7 @@ K_DOT_TC32P = 19
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
+K_CONV_TCGW64, K_CONV_TCGW128 = 28, 29
 K_DOT_TH_F32, K_DOT_TH_F64 = 26, 27
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
@@ -145,6 +146,20 @@ class TcggArgs(C.Structure):
     ]
 
 
+class TcgwArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64), ("a", C.c_uint64), ("b", C.c_uint64),
+        ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
+        ("c_sm", C.c_int64), ("c_sn", C.c_int64), ("c_rdiv", C.c_int64), ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64),
+        ("ro0", C.c_int64), ("ro1", C.c_int64), ("ro2", C.c_int64),
+        ("ko0", C.c_int64), ("ko1", C.c_int64), ("ko2", C.c_int64), ("kbase", C.c_int64),
+        ("yo0", C.c_int64), ("yo1", C.c_int64), ("yo2", C.c_int64),
+        ("k_splits", C.c_int64), ("split_stride", C.c_int64),
+        ("E1", C.c_int32), ("E2", C.c_int32), ("h0", C.c_int32), ("w0", C.c_int32), ("H", C.c_int32), ("W", C.c_int32),
+        ("Ke1", C.c_int32), ("Ke2", C.c_int32), ("kb_per_split", C.c_int32), ("pad", C.c_int32),
+    ]
+
+
 class ConvArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p),
@@ -184,5 +199,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

@@ -142,6 +142,9 @@ TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
+TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
+TCGW_SMEM = {64: 3 * (2 * 16384 + 2 * 8192) + 3 * (16384 + 8192) + 1280,
+             128: 2 * (2 * 16384 + 2 * 16384) + 2 * (16384 + 16384) + 1280}  # WCfg::SMEM_BYTES
 TCGG_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu GCfg::THREADS_GG
 TCG_SMEM = {bn: (2 if bn == 128 else 3) * (2 * 128 + 2 * bn) * 32 * 4 + 4 * 128 * 32 * 4 + 128 * 16 + 256 + 1024
             for bn in (64, 128)}
@@ -1377,6 +1380,56 @@ class Lowering:
                 and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 30 and element_count(xb.shape) < 2 ** 31)
 
     @staticmethod
+    def _wgrad_mn_ok(xb, xs, yb, ys, Cc, K) -> bool:
+        """MN-major weight-gradient kernel: channel-last x and dy with channel
+        counts and every stride multiples of 4 (16-byte pieces)."""
+        return (os.environ.get("GFB_TCGW", "1") == "1" and xb.splat is None and yb.splat is None
+                and xs[1] == 1 and ys[1] == 1 and Cc % 4 == 0 and K % 4 == 0
+                and all(v % 4 == 0 for v in (xs[0], xs[2], xs[3], ys[0], ys[2], ys[3]))
+                and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 30 and element_count(xb.shape) < 2 ** 31
+                and max(abs(v) for v in ys) * max(yb.shape) < 2 ** 30 and element_count(yb.shape) < 2 ** 31)
+
+    def _conv_tcgw(self, n, xb, yb, out, m, ncols, kdim, geo, addr, label):
+        """Weight gradient on gemm_tc.cu gfb_conv_tcgw_kernel (split-K over
+        the pixels when the (r, s, c) x k tiles do not fill the GPU)."""
+        bn = 64 if ncols <= 64 else 128
+        kblocks = (kdim + 31) // 32
+        tiles = ((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE)
+        splits = 1
+        if tiles < NUM_SMS and kblocks >= 64:
+            splits = max(1, min((2 * NUM_SMS) // tiles, kblocks // 16))
+        per = (kblocks + splits - 1) // splits
+        splits = (kblocks + per - 1) // per
+        ta = abi.TcgwArgs(M=m, N=ncols, K=kdim, **geo)
+        target = out
+        if splits > 1:
+            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
+            self.buf[("splitk", n)] = scratch
+            ta.k_splits, ta.kb_per_split, ta.split_stride = splits, per, m * ncols
+            ta.c_sm, ta.c_sn = ncols, 1
+            target = scratch
+        else:
+            ta.k_splits, ta.kb_per_split = 1, kblocks
+            for k_, v_ in addr.items():
+                setattr(ta, k_, v_)
+        kind = abi.K_CONV_TCGW64 if bn == 64 else abi.K_CONV_TCGW128
+        items = ((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE) * splits
+        grid = (max(1, min(items, NUM_SMS)), 1, 1)
+        rec = LaunchRec(kind, grid, (TCGW_THREADS[bn], 1, 1), TCGW_SMEM[bn], ta, [xb.key, yb.key], [target.key], label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": target, "a": xb, "b": yb})
+        self.launches.append(rec)
+        if splits > 1:
+            p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
+            p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+            self._col_launch(p2, m * ncols, splits, 1, label + ":splitk", ElementType.F32)
+        return rec
+
+    @staticmethod
     def _tma_box_ok(xb, shape, sx, sy) -> bool:
         """TMA box gather: the activation needs a fixed (arena) address for
         its tensor map, and the strided box must fit the 256-element limit."""
@@ -1552,9 +1605,19 @@ class Lowering:
                 return False
             if self._generic_gather_ok(xb, xs):
                 # rows (c, r, s) of the gathered data, columns = output channels
-                b = self._split(n, "b", yb, K, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
+                b = None if self._wgrad_mn_ok(xb, xs, yb, ys, Cc, K) else self._split(
+                    n, "b", yb, K, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
                 kgeo = dict(Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
                             kh=1, kw=1, dh0=0, dw0=0)
+                if self._wgrad_mn_ok(xb, xs, yb, ys, Cc, K):
+                    # channel-last x and dy: 16-byte MN-major loads of both raw
+                    # operands, split to TF32 in the kernel (no dy planes)
+                    geo = dict(E1=S, E2=Cc, ro0=xs[2], ro1=xs[3], ro2=xs[1], h0=-pt, w0=-pl, H=H, W=W,
+                               Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
+                               yo0=ys[0], yo1=ys[2], yo2=ys[3])
+                    addr = {"c_rdiv": Cc, "c_s_hi": os_[3], "c_s_lo": os_[1], "c_sn": os_[0]}
+                    self._conv_tcgw(n, xb, yb, out, Cc * R * S, K, kdim, geo, addr, f"{node.op.wire_name}_tcgw#{n}")
+                    return True
                 if xs[1] == 1 and Cc > 1:
                     # channel-last data: rows (r, s, c) so lanes read contiguous channels
                     geo = dict(E1=S, E2=Cc, ro0=xs[2], ro1=xs[3], ro2=xs[1], hm=1, wm=1, h0=-pt, w0=-pl, H=H, W=W,

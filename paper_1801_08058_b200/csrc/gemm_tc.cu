@@ -1419,9 +1419,309 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS_GG, 1) gfb_conv_tcgg_ke
     }
 }
 
+// ---------------------------------------------------------------------------
+// Weight gradient over channel-last data (gfb_tcgw_args): both operands are
+// loaded raw with 16-byte cp.async straight into MN-major tiles -- A rows
+// (r, s, c) are contiguous channels of x, B columns contiguous channels of
+// dy -- and split into TF32 hi/lo in place.  tcgen05 kind::tf32 reads
+// MN-major operands only in the SWIZZLE_128B_BASE32B layout: atoms of 4 K
+// rows x 128 B (32 MN elements) with 32-byte chunks XOR-swizzled by the row
+// (verified by scripts/mn_probe.cu); atoms along K are SBO = 512 B apart,
+// along MN LBO = 4096 B (one K-block of 8 atoms).  This replaces tcgg's
+// 4-byte element gather (latency bound) and the separate TF32 split pass
+// over dy that the plane form needs.
+namespace tc {
+template <int BN_>
+struct WCfg {
+    static constexpr int BM = 128, BN = BN_, BK = 32;
+    static constexpr int STAGES = BN_ == 128 ? 2 : 3, RAW = BN_ == 128 ? 2 : 3;
+    static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES, RAW_BYTES = A_BYTES + B_BYTES;
+    static constexpr int CHUNK_KB = 4, NBUF = 512 / BN;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4, GATHER_WARPS = BN_ == 64 ? 8 : 4;
+    static constexpr int THREADS = 64 + 32 * (EPI_WARPS + GATHER_WARPS);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RAW * RAW_BYTES + 256 + 1024;
+};
+
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;          // start address
+    d |= (uint64_t)(4096 >> 4) << 16;      // LBO: MN atoms
+    d |= (uint64_t)(512 >> 4) << 32;       // SBO: 4-row K atoms
+    d |= (uint64_t)1 << 46;                // version (sm100)
+    d |= (uint64_t)1 << 61;                // SWIZZLE_128B_BASE32B
+    return d;
+}
+// byte offset of the 16-byte piece holding MN elements mn..mn+3 (mn % 4 == 0) at K row kl
+__device__ __forceinline__ uint32_t mn_piece(int mn, int kl) {
+    const int mi = mn & 31;
+    return (uint32_t)(mn >> 5) * 4096u + (uint32_t)(kl >> 2) * 512u + (uint32_t)(kl & 3) * 128u +
+           ((uint32_t)((mi >> 3) ^ (kl & 3)) << 5) + (uint32_t)((mi >> 2) & 1) * 16u;
+}
+}  // namespace tc
+
+template <int BN_>
+__global__ void __launch_bounds__(tc::WCfg<BN_>::THREADS, 1) gfb_conv_tcgw_kernel(const __grid_constant__ gfb_tcgw_args p) {
+    using namespace tc;
+    using C_ = WCfg<BN_>;
+    constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, RAW = C_::RAW;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES, RAW_BYTES = C_::RAW_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GW = C_::GATHER_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* raw = smem + STAGES * STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + RAW * RAW_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kb_total = (int)((p.K + BK - 1) / BK);
+    const int ntn = (int)((p.N + BN - 1) / BN), ntm = (int)((p.M + 127) / 128);
+    const int nsplit = p.k_splits > 1 ? (int)p.k_splits : 1;
+    const int nitems = ntn * ntm * nsplit;
+    struct Item {
+        int m0, n0, z, kb_begin, nk;
+    };
+    auto item_at = [&](int it) {
+        Item r;
+        const int nt = it % ntn, mt = (it / ntn) % ntm;
+        r.z = it / (ntn * ntm);
+        r.m0 = mt * 128;
+        r.n0 = nt * BN;
+        r.kb_begin = nsplit > 1 ? r.z * p.kb_per_split : 0;
+        const int kb_end = nsplit > 1 ? min(kb_total, r.kb_begin + p.kb_per_split) : kb_total;
+        r.nk = max(0, kb_end - r.kb_begin);
+        return r;
+    };
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], GW);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, BN) | (1u << 15) | (1u << 16);  // MN-major A and B
+            uint32_t gk = 0, gc = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const Item I = item_at(it);
+                for (int i = 0; i < I.nk; ++i, ++gk) {
+                    const int s = gk % STAGES;
+                    const uint32_t chunk = gc + i / CHUNK_KB;
+                    const int b = chunk % NBUF;
+                    const bool chunk_start = i % CHUNK_KB == 0;
+                    if (chunk_start) {
+                        mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t st = su32(smem + s * STAGE_BYTES);
+                    const uint64_t ah = smem_desc_mn(st), al = smem_desc_mn(st + A_BYTES);
+                    const uint64_t bh = smem_desc_mn(st + 2 * A_BYTES), bl = smem_desc_mn(st + 2 * A_BYTES + B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t adv = (uint64_t)(j * 1024) >> 4;  // two 4-row K atoms per K = 8 step
+                        const uint32_t acc = !(chunk_start && j == 0);
+                        mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+                        mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+                        mma_tf32(d, al + adv, bh + adv, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                    if (i % CHUNK_KB == CHUNK_KB - 1 || i == I.nk - 1) mma_commit(&tfull[b]);
+                }
+                gc += (I.nk + CHUNK_KB - 1) / CHUNK_KB;
+            }
+        }
+    } else if (warp >= 2 && warp < 2 + EPI_WARPS) {
+        constexpr int EC = BN < 128 ? BN : 128;
+        const int q = warp & 3;
+        uint32_t gc = 0;
+        float* C0 = resolve<float>(p.tab, p.c);
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const Item I = item_at(it);
+            const int nchunk = (I.nk + CHUNK_KB - 1) / CHUNK_KB;
+            float acc[EC];
+#pragma unroll
+            for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            for (int c0 = 0; c0 < nchunk; ++c0) {
+                const uint32_t chunk = gc + c0;
+                const int b = chunk % NBUF;
+                mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    uint32_t r[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            }
+            gc += nchunk;
+            float* C = C0 + (nsplit > 1 ? (int64_t)I.z * p.split_stride : 0);
+            const LinearRows rows{I.m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
+            const int64_t roff = rows(q * 32 + lane);
+            if (roff >= 0) {
+                float* dst = C + roff;
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    const int col0 = I.n0 + c * 32;
+                    if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + col0 + j) =
+                                make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                    }
+                }
+            }
+        }
+    } else if (warp >= 2 + EPI_WARPS) {
+        // loaders: lane = 4-row group of the tile (rows 4*rg..4*rg+3 are four
+        // contiguous channels of one tap), each warp KPW of a K-block's 32
+        // pixels for A; B pieces (four contiguous dy channels of one pixel)
+        // striped over all loader threads
+        constexpr int KPW = 32 / GW, NQ = BN / 4, BPT = (32 * NQ) / (32 * GW);
+        const int gt = threadIdx.x - (2 + EPI_WARPS) * 32;
+        const int rg = gt & 31, gw = gt >> 5;
+        const float* X = resolve<const float>(p.tab, p.a);
+        const float* Y = resolve<const float>(p.tab, p.b);
+        const int ke2 = p.Ke2, ke12 = p.Ke1 * p.Ke2, e12 = p.E1 * p.E2;
+        uint32_t gk = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const Item I = item_at(it);
+            const int row = I.m0 + 4 * rg;
+            int64_t rowoff = 0;
+            int hr = -(1 << 28), wr = 0;
+            if (row < p.M) {
+                const int i0 = row / e12, rem = row - i0 * e12, i1 = rem / p.E2, i2 = rem - i1 * p.E2;
+                rowoff = i0 * p.ro0 + i1 * p.ro1 + i2 * p.ro2 + p.kbase;
+                hr = i0 + p.h0;
+                wr = i1 + p.w0;
+            }
+            const float* arow = X + rowoff;
+            auto issue = [&](int i) {
+                const int kb = I.kb_begin + i;
+                const uint32_t slot = su32(raw + ((gk + i) % RAW) * RAW_BYTES);
+                // lane l decomposes pixel kb*32 + l once; pieces fetch it by shuffle
+                int koff = 0, yoff = -1, k1 = -(1 << 28), k2 = 0;
+                {
+                    const int k = kb * BK + lane;
+                    if (k < p.K) {
+                        const int k0 = k / ke12, kr = k - k0 * ke12;
+                        k1 = kr / ke2;
+                        k2 = kr - k1 * ke2;
+                        koff = (int)(k0 * p.ko0 + k1 * p.ko1 + k2 * p.ko2);
+                        yoff = (int)(k0 * p.yo0 + k1 * p.yo1 + k2 * p.yo2);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < KPW; ++t) {
+                    const int kl = gw * KPW + t;
+                    const int ko = __shfl_sync(0xffffffffu, koff, kl);
+                    const int h = hr + __shfl_sync(0xffffffffu, k1, kl), w = wr + __shfl_sync(0xffffffffu, k2, kl);
+                    const bool ok = (uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(slot + mn_piece(4 * rg, kl)),
+                                 "l"(ok ? arow + ko : X), "r"(ok ? 16u : 0u) : "memory");
+                }
+#pragma unroll
+                for (int u = 0; u < BPT; ++u) {
+                    const int pc = gt + u * 32 * GW, kl = pc / NQ, nq = pc - kl * NQ;
+                    const int yo = __shfl_sync(0xffffffffu, yoff, kl);
+                    const int n = I.n0 + 4 * nq;
+                    const bool ok = yo >= 0 && n < p.N;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(slot + A_BYTES + mn_piece(4 * nq, kl)),
+                                 "l"(ok ? Y + yo + n : Y), "r"(ok ? 16u : 0u) : "memory");
+                }
+            };
+#pragma unroll
+            for (int i = 0; i < RAW; ++i) {
+                if (i < I.nk) issue(i);
+                cp_async_commit();
+            }
+            for (int i = 0; i < I.nk; ++i) {
+                cp_async_wait<RAW - 1>();  // this thread's pieces of K-block i have landed
+                const uint32_t g2 = gk + i;
+                const int s = g2 % STAGES;
+                mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
+                const uint32_t src = su32(raw + (g2 % RAW) * RAW_BYTES);
+                const uint32_t dst = su32(smem + s * STAGE_BYTES);
+                // the split is elementwise: each thread converts exactly the pieces it loaded
+#pragma unroll
+                for (int t = 0; t < KPW; ++t) {
+                    const uint32_t o = mn_piece(4 * rg, gw * KPW + t);
+                    const float4 x = lds128(src + o), h = trunc_tf32(x);
+                    sts128(dst + o, h);
+                    sts128(dst + A_BYTES + o, make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
+                                                          __fsub_rn(x.w, h.w)));
+                }
+#pragma unroll
+                for (int u = 0; u < BPT; ++u) {
+                    const int pc = gt + u * 32 * GW, kl = pc / NQ, nq = pc - kl * NQ;
+                    const uint32_t o = mn_piece(4 * nq, kl);
+                    const float4 x = lds128(src + A_BYTES + o), h = trunc_tf32(x);
+                    sts128(dst + 2 * A_BYTES + o, h);
+                    sts128(dst + 2 * A_BYTES + B_BYTES + o, make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y),
+                                                                        __fsub_rn(x.z, h.z), __fsub_rn(x.w, h.w)));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+                if (i + RAW < I.nk) issue(i + RAW);  // reuses the raw slot just consumed
+                cp_async_commit();
+            }
+            gk += I.nk;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 }  // namespace gfb
 
 
+template __global__ void gfb::gfb_conv_tcgw_kernel<64>(const __grid_constant__ gfb_tcgw_args);
+template __global__ void gfb::gfb_conv_tcgw_kernel<128>(const __grid_constant__ gfb_tcgw_args);
 template __global__ void gfb::gfb_gemm_tc_kernel<128>(const __grid_constant__ gfb_tc_args);
 template __global__ void gfb::gfb_gemm_tc_kernel<256>(const __grid_constant__ gfb_tc_args);
 template __global__ void gfb::gfb_conv_tcg_kernel<64>(const __grid_constant__ gfb_tcg_args);
@@ -1442,8 +1742,11 @@ extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_CONV_TCGG64) return (const void*)gfb::gfb_conv_tcgg_kernel<64>;
     if (kind == GFB_K_CONV_TCGG128) return (const void*)gfb::gfb_conv_tcgg_kernel<128>;
     if (kind == GFB_K_CONV_TCX128) return (const void*)gfb::gfb_conv_tcx_kernel<128>;
+    if (kind == GFB_K_CONV_TCGW64) return (const void*)gfb::gfb_conv_tcgw_kernel<64>;
+    if (kind == GFB_K_CONV_TCGW128) return (const void*)gfb::gfb_conv_tcgw_kernel<128>;
     return nullptr;
 }
 
 extern "C" int gfb_tc_smem_bytes(int wide) { return wide ? gfb::tc::Cfg<256>::SMEM_BYTES : gfb::tc::Cfg<128>::SMEM_BYTES; }
+extern "C" int gfb_tcgw_smem_bytes(int bn) { return bn == 64 ? gfb::tc::WCfg<64>::SMEM_BYTES : gfb::tc::WCfg<128>::SMEM_BYTES; }
 extern "C" int gfb_tcg_smem_bytes(int bn) { return bn == 64 ? gfb::tc::GCfg<64>::SMEM_BYTES : gfb::tc::GCfg<128>::SMEM_BYTES; }

@@ -173,7 +173,7 @@ const void* kernel_for(uint32_t kind) {
         return gfb_simt_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_DOT_TC32P || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
         kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128 || kind == GFB_K_CONV_TCGG64 ||
-        kind == GFB_K_CONV_TCGG128)
+        kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128)
         return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
 }

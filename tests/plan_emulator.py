@@ -422,6 +422,46 @@ def run_tcgg(mem, a):
         C[base + off] = c
 
 
+def run_tcgw(mem, a):
+    """gfb_conv_tcgw_kernel: MN-major weight gradient over channel-last x and
+    dy, both operands split to TF32 hi/lo in the kernel (gfb_tcgw_args)."""
+    X = mem.view(a.a, np.float32)
+    Y = mem.view(a.b, np.float32)
+    row = np.arange(a.M, dtype=np.int64)
+    e12 = a.E1 * a.E2
+    i0, rem = row // e12, row % e12
+    i1, i2 = rem // a.E2, rem % a.E2
+    rowoff = i0 * a.ro0 + i1 * a.ro1 + i2 * a.ro2 + a.kbase
+    hr, wr = i0 + a.h0, i1 + a.w0
+    k = np.arange(a.K, dtype=np.int64)
+    ke12 = a.Ke1 * a.Ke2
+    k0, kr = k // ke12, k % ke12
+    k1, k2 = kr // a.Ke2, kr % a.Ke2
+    h = hr[:, None] + k1[None, :]
+    w = wr[:, None] + k2[None, :]
+    ok = (h >= 0) & (h < a.H) & (w >= 0) & (w < a.W)
+    off = rowoff[:, None] + (k0 * a.ko0 + k1 * a.ko1 + k2 * a.ko2)[None, :]
+    x = np.where(ok, X[np.where(ok, off, 0)], np.float32(0)).astype(np.float32)
+    ahi, alo = (v.astype(np.float64) for v in _trunc_split(x))
+    yoff = (k0 * a.yo0 + k1 * a.yo1 + k2 * a.yo2)[None, :] + np.arange(a.N, dtype=np.int64)[:, None]
+    bhi, blo = (v.astype(np.float64) for v in _trunc_split(Y[yoff].astype(np.float32)))
+    C = mem.view(a.c, np.float32)
+    i = row[:, None]
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    kblocks = (a.K + 31) // 32
+    for z in range(max(1, a.k_splits)):
+        b0 = z * a.kb_per_split if a.k_splits > 1 else 0
+        b1 = min(kblocks, b0 + a.kb_per_split) if a.k_splits > 1 else kblocks
+        sl = slice(32 * b0, min(a.K, 32 * b1))
+        c = (ahi[:, sl] @ bhi[:, sl].T + ahi[:, sl] @ blo[:, sl].T + alo[:, sl] @ bhi[:, sl].T).astype(np.float32)
+        base = z * a.split_stride if a.k_splits > 1 else 0
+        if a.c_rdiv > 0:
+            o = (i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn
+        else:
+            o = i * a.c_sm + j * a.c_sn
+        C[base + o] = c
+
+
 STAGED_U = 2  # csrc/ew_vm.cu StagedCfg<T, 2>
 
 
@@ -442,6 +482,8 @@ def _run_launch(mem, L):
         run_tcg(mem, L.args)
     elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):
         run_tcx(mem, L.args)
+    elif L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128):
+        run_tcgw(mem, L.args)
     elif L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128):
         run_tcgg(mem, L.args)
     else:

@@ -272,21 +272,31 @@ def test_tiny_dot_fused_bit_exact(m, k, n, et):
     assert G.same_bits(out, interp.run_function(fn, [A, B])[0])
 
 
-@pytest.mark.parametrize("shape,pad", [((2, 32, 16, 9, 8, 3, 3), (1, 1, 1, 1)), ((2, 5, 8, 7, 7, 3, 3), (1, 0, 0, 1))])
-def test_wgrad_channel_last_rows_emulated(monkeypatch, shape, pad):
-    """ConvBackpropFilter over channel-last data walks rows (r, s, c) so lanes
-    read contiguous channels (gfb_tcgg_args.pad0 == 1)."""
+@pytest.mark.parametrize("mn", [True, False])
+@pytest.mark.parametrize("shape,pad", [((2, 32, 16, 9, 8, 3, 3), (1, 1, 1, 1)), ((2, 5, 8, 7, 7, 3, 3), (1, 0, 0, 1)),
+                                       ((3, 12, 132, 6, 5, 3, 3), (1, 1, 0, 2))])
+def test_wgrad_channel_last_rows_emulated(monkeypatch, shape, pad, mn):
+    """ConvBackpropFilter over channel-last data: the MN-major kernel
+    (gfb_tcgw_args: 16-byte loads of x and dy, split in the kernel) when the
+    channel counts are multiples of 4, else rows (r, s, c) on the element
+    gather so lanes read contiguous channels (gfb_tcgg_args.pad0 == 1)."""
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import abi
     from oracle import interp
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_TCGW", "1" if mn else "0")
     N, C, K, H, W, R, S = shape
     fn = _conv_graph("wgrad", N, C, K, H, W, R, S, (1, 1), pad)
     nhwc = (0, 2, 3, 1)
     h = host_compile(fn, optimize=False, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc])
-    tg = [L for L in h.lowered.launches if L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128)]
-    assert tg and tg[0].args.pad0 == 1, [L.label for L in h.lowered.launches]
+    labels = [L.label for L in h.lowered.launches]
+    if mn and C % 4 == 0 and K % 4 == 0:
+        assert any(L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128) for L in h.lowered.launches), labels
+        assert not any(L.kind == abi.K_SPLIT_TF32 for L in h.lowered.launches), labels  # no dy planes
+    else:
+        tg = [L for L in h.lowered.launches if L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128)]
+        assert tg and tg[0].args.pad0 == 1, labels
     rng = np.random.default_rng(21)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
