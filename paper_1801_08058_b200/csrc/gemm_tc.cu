@@ -1636,20 +1636,32 @@ __global__ void __launch_bounds__(tc::WCfg<BN_>::THREADS, 1) gfb_conv_tcgw_kerne
                 wr = i1 + p.w0;
             }
             const float* arow = X + rowoff;
+            // lane l tracks pixel kb*32 + l as (c0, c1, c2) over (*, Ke1, Ke2):
+            // one division at the item's first K-block, then carries (K-blocks
+            // are issued in order, 32 pixels apart)
+            int c0 = 0, c1 = 0, c2 = 0, ckb = -1;
             auto issue = [&](int i) {
                 const int kb = I.kb_begin + i;
                 const uint32_t slot = su32(raw + ((gk + i) % RAW) * RAW_BYTES);
-                // lane l decomposes pixel kb*32 + l once; pieces fetch it by shuffle
-                int koff = 0, yoff = -1, k1 = -(1 << 28), k2 = 0;
-                {
-                    const int k = kb * BK + lane;
-                    if (k < p.K) {
-                        const int k0 = k / ke12, kr = k - k0 * ke12;
-                        k1 = kr / ke2;
-                        k2 = kr - k1 * ke2;
-                        koff = (int)(k0 * p.ko0 + k1 * p.ko1 + k2 * p.ko2);
-                        yoff = (int)(k0 * p.yo0 + k1 * p.yo1 + k2 * p.yo2);
+                const int k = kb * BK + lane;
+                if (ckb < 0) {
+                    c0 = k / ke12;
+                    const int kr = k - c0 * ke12;
+                    c1 = kr / ke2;
+                    c2 = kr - c1 * ke2;
+                } else {
+                    for (c2 += (kb - ckb) * BK; c2 >= ke2;) {
+                        c2 -= ke2;
+                        if (++c1 == p.Ke1) c1 = 0, ++c0;
                     }
+                }
+                ckb = kb;
+                int koff = 0, yoff = -1, k1 = -(1 << 28), k2 = 0;
+                if (k < p.K) {
+                    k1 = c1;
+                    k2 = c2;
+                    koff = (int)(c0 * p.ko0 + c1 * p.ko1 + c2 * p.ko2);
+                    yoff = (int)(c0 * p.yo0 + c1 * p.yo1 + c2 * p.yo2);
                 }
 #pragma unroll
                 for (int t = 0; t < KPW; ++t) {
