@@ -238,7 +238,8 @@ typedef struct GFB_ALIGN64 {
 /* Implicit-GEMM convolution with the A gather fused into the tensor-core
  * kernel.  A is a 4-D activation with unit channel stride (NHWC storage):
  * GEMM row `row` = (n, y, x) over extents (*, Y, X) has spatial origin
- * h = y*sy + oy, w = x*sx + ox; K index k = (r, s, c) over (R, S, C = 32*CB)
+ * h = y*sy + oy, w = x*sx + ox; K index k = (r, s, c) over (R, S, C), C a
+ * multiple of 4 (16-byte pieces of 4 channels; K-blocks may span taps)
  * reads a[n, h + ksign*r, w + ksign*s, c] (element strides xs0, xs2, xs3
  * along n, h, w), zero outside [0, H) x [0, W).  Conv2D: (Y, X) = (Ho, Wo),
  * (sy, sx) = strides, (oy, ox) = -(pt, pl), ksign = +1.  ConvBackpropData:
@@ -253,7 +254,7 @@ typedef struct GFB_ALIGN64 {
     int64_t c_sm, c_sn, c_rdiv, c_s_hi, c_s_lo;
     uint64_t a, b_hi, b_lo;
     int64_t xs0, xs2, xs3;
-    int32_t Y, X, sy, sx, oy, ox, H, W, S, CB, ksign, pad0;
+    int32_t Y, X, sy, sx, oy, ox, H, W, S, CB, ksign, C; /* C: channel count (multiple of 4; 0 = 32*CB) */
     int64_t pad[2];
     uint64_t tmap[2][16];
 } gfb_tcg_args;

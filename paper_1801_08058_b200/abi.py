@@ -107,7 +107,7 @@ class TcgArgs(C.Structure):
         ("a", C.c_uint64), ("b_hi", C.c_uint64), ("b_lo", C.c_uint64),
         ("xs0", C.c_int64), ("xs2", C.c_int64), ("xs3", C.c_int64),
         ("Y", C.c_int32), ("X", C.c_int32), ("sy", C.c_int32), ("sx", C.c_int32), ("oy", C.c_int32), ("ox", C.c_int32),
-        ("H", C.c_int32), ("W", C.c_int32), ("S", C.c_int32), ("CB", C.c_int32), ("ksign", C.c_int32), ("pad0", C.c_int32),
+        ("H", C.c_int32), ("W", C.c_int32), ("S", C.c_int32), ("CB", C.c_int32), ("ksign", C.c_int32), ("C", C.c_int32),
         ("pad", C.c_int64 * 2),
         ("tmap", (C.c_uint64 * 16) * 2),
     ]

@@ -1367,9 +1367,9 @@ class Lowering:
     @staticmethod
     def _gather_ok(xb, xs, channels, m) -> bool:
         """The fused-gather conv kernel needs unit channel stride (NHWC
-        storage), whole 32-channel K-blocks and 16-byte aligned runs."""
+        storage) and 16-byte aligned runs of 4 channels."""
         return (os.environ.get("GFB_CONV_GATHER", "1") == "1" and xb.splat is None and xs[1] == 1
-                and channels % 32 == 0 and all(v % 4 == 0 for v in (xs[0], xs[2], xs[3]))
+                and channels % 4 == 0 and all(v % 4 == 0 for v in (xs[0], xs[2], xs[3]))
                 and xb.offset % 16 == 0 and (m + TC_TILE - 1) // TC_TILE <= 65535
                 and max(abs(v) for v in xs) * 4 < 2 ** 62)
 
@@ -1547,13 +1547,13 @@ class Lowering:
                 return False
             if self._gather_ok(xb, xs, Cc, m):
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (R, S, Cc), st=(ys[2], ys[3], ys[1]))
-                if self._tma_box_ok(xb, (N, Cc, H, W), sw, sh):
+                if Cc % 32 == 0 and self._tma_box_ok(xb, (N, Cc, H, W), sw, sh):
                     self._conv_tcx(n, xb, xs, (N, Cc, H, W), b, out, (N, Ho, Wo), ncols, kdim,
                                    dict(sx=sw, sy=sh, ox=-pl, oy=-pt, S=S, CB=Cc // 32, ksign=1), yb,
                                    f"{node.op.wire_name}_tcx#{n}")
                     return True
                 self._conv_tcg(n, xb, xs, b, out, m, ncols, kdim, dict(Y=Ho, X=Wo, sy=sh, sx=sw, oy=-pt, ox=-pl, H=H, W=W, S=S,
-                               CB=Cc // 32, ksign=1), {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
+                               CB=Cc // 32, C=Cc, ksign=1), {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
                                yb, f"{node.op.wire_name}_tcg#{n}")
                 return True
             addr = {"c_rdiv": Ho * Wo, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}
@@ -1576,13 +1576,13 @@ class Lowering:
                 return False
             if self._gather_ok(xb, xs, K, m):
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (R, S, K), st=(ys[2], ys[3], ys[0]))
-                if self._tma_box_ok(xb, (N, K, Ho, Wo), 1, 1):
+                if K % 32 == 0 and self._tma_box_ok(xb, (N, K, Ho, Wo), 1, 1):
                     self._conv_tcx(n, xb, xs, (N, K, Ho, Wo), b, out, (N, H, W), ncols, kdim,
                                    dict(sx=1, sy=1, ox=pl, oy=pt, S=S, CB=K // 32, ksign=-1), yb,
                                    f"{node.op.wire_name}_tcx#{n}")
                     return True
                 self._conv_tcg(n, xb, xs, b, out, m, ncols, kdim, dict(Y=H, X=W, sy=1, sx=1, oy=pt, ox=pl, H=Ho, W=Wo, S=S,
-                               CB=K // 32, ksign=-1), {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
+                               CB=K // 32, C=K, ksign=-1), {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]},
                                yb, f"{node.op.wire_name}_tcg#{n}")
                 return True
             addr = {"c_rdiv": H * W, "c_s_hi": os_[0], "c_s_lo": os_[3], "c_sn": os_[1]}

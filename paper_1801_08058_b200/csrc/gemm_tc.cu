@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
-    const int nk = (int)(p.K / BK);
+    const int nk = (int)((p.K + BK - 1) / BK);
     const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
 
     if (warp == 0 && lane == 0) {
@@ -627,16 +627,19 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
         const float* A = resolve<const float>(p.tab, p.a);
         const int j = g & 7, rb = g >> 3;
         const uint32_t swz = (uint32_t)((j ^ (rb & 7)) << 4);  // row & 7 == rb & 7 for every row rb + 16 i
+        const int Cc = p.C ? p.C : 32 * p.CB;
         auto issue = [&](int kb) {
-            const int cb = kb % p.CB, rs = kb / p.CB, r = rs / p.S, s = rs - r * p.S;
+            // this thread's 16-byte piece: channels c..c+3 of tap (r, s), k = kb*32 + 4j
+            const int k = kb * BK + j * 4, tap = k / Cc, c = k - tap * Cc, r = tap / p.S, s = tap - r * p.S;
+            const bool kok = k < p.K;
             const int dh = p.ksign * r, dw = p.ksign * s;
-            const int64_t koff = (int64_t)dh * p.xs2 + (int64_t)dw * p.xs3 + cb * 32 + j * 4;
+            const int64_t koff = (int64_t)dh * p.xs2 + (int64_t)dw * p.xs3 + c;
             unsigned char* dst = raw + (kb % RAW) * A_BYTES + swz;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int row = rb + 16 * i;
                 const RowInfo ri = rowtab[row];
-                const bool ok = (uint32_t)(ri.h + dh) < (uint32_t)p.H && (uint32_t)(ri.w + dw) < (uint32_t)p.W;
+                const bool ok = kok && (uint32_t)(ri.h + dh) < (uint32_t)p.H && (uint32_t)(ri.w + dw) < (uint32_t)p.W;
                 cp_async16(dst + row * 128, ok ? (const void*)(A + ri.off + koff) : (const void*)A, ok ? 16u : 0u);
             }
         };

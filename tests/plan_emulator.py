@@ -329,7 +329,7 @@ def run_tcg(mem, a):
     channel-contiguous activation, split it like the kernel, contract with
     the B planes."""
     src = mem.view(a.a, np.float32)
-    M, K, C = a.M, a.K, 32 * a.CB
+    M, K, C = a.M, a.K, (a.C or 32 * a.CB)
     row = np.arange(M, dtype=np.int64)
     n, rem = row // (a.Y * a.X), row % (a.Y * a.X)
     h0 = (rem // a.X) * a.sy + a.oy

@@ -121,6 +121,11 @@ def test_conv_tensor_cores_match_oracle(monkeypatch, op, shape, stride, pad, lay
     ("fwd", (2, 64, 128, 28, 28, 1, 1), (2, 2), (0, 0, 0, 0)),
     ("dgrad", (4, 40, 64, 16, 15, 3, 3), (1, 1), (1, 0, 0, 1)),
     ("dgrad", (2, 64, 128, 28, 28, 3, 3), (1, 1), (1, 1, 1, 1)),
+    # channel counts that are multiples of 4 but not 32: K-blocks span taps
+    ("fwd", (8, 16, 32, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (3, 4, 64, 30, 29, 7, 7), (1, 1), (3, 3, 3, 3)),
+    ("fwd", (2, 12, 40, 17, 19, 3, 3), (2, 1), (0, 1, 1, 0)),
+    ("dgrad", (4, 20, 16, 16, 15, 3, 3), (1, 1), (1, 0, 0, 1)),
 ])
 def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
     """gfb_conv_tcg_kernel (in-kernel NHWC gather + TF32 split) vs the oracle."""
