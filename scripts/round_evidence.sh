@@ -15,4 +15,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gfb_
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_B.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gfb_gemm_tc -s 1 -c 1 -o $OUT/prof_G \
   python bench.py --workload G --steps 2 --warmup 3 > $OUT/ncu_G.log 2>&1
+
+bash scripts/ncu_top.sh D gfb_conv_tcgw 0 > /dev/null 2>&1
 echo done
