@@ -253,7 +253,8 @@ def bench_chain(args, ws, rank, local):
     # plain call(): H2D, run, D2H back to back
     call_s = timed(lambda: gf.call(exe, host_in, out=host_out))
     # call_streamed(): row chunks with H2D / compute / D2H overlapped on 3 streams
-    e2e_s = timed(lambda: gf.call_streamed(exe, host_in, host_out, chunks=16))
+    chunks = int(os.environ.get("GFB_BENCH_CHUNKS", 16))
+    e2e_s = timed(lambda: gf.call_streamed(exe, host_in, host_out, chunks=chunks))
     h2d = sum(a.nbytes for a in arrays)
     d2h = sum(t.buffer.nbytes for t in host_out)
 
@@ -276,7 +277,7 @@ def bench_chain(args, ws, rank, local):
                    "l2": "inputs 805 MB > 126 MB L2, no flush needed", "parallelism": f"replicas x{ws} (row shards, no collective)"},
         "e2e": {"value": ws * nbytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3,
-                "api": "paper_1801_08058_b200.call_streamed(exe, pinned host inputs, pinned host results, chunks=16)",
+                "api": f"paper_1801_08058_b200.call_streamed(exe, pinned host inputs, pinned host results, chunks={chunks})",
                 "call_value": ws * nbytes / call_s / 1e9, "call_ms_per_step": call_s * 1e3,
                 "call_api": "paper_1801_08058_b200.call(exe, pinned host tensors, out=pinned host tensors)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

@@ -21,6 +21,9 @@ check that.
 
 Compiled cubins are cached on disk (key: source + options + kernel headers);
 the cache only saves compile time.  `GFB_JIT=0` disables specialisation.
+If NVRTC is missing or a generated kernel fails to compile, the launch keeps
+the generic CUDA kernel and a RuntimeWarning says so (`GFB_JIT_STRICT=1`,
+set by the test suite, raises instead).
 """
 
 from __future__ import annotations
@@ -57,6 +60,17 @@ _lock = threading.Lock()
 _nvrtc = None
 _kernels: dict = {}  # cubin digest -> kernel handle (libraries stay loaded for the process)
 _header_digest = None
+
+
+_warned: set = set()
+
+
+def _warn_once(msg: str):
+    import warnings
+
+    if msg not in _warned:
+        _warned.add(msg)
+        warnings.warn(msg, RuntimeWarning, stacklevel=3)
 
 
 def enabled() -> bool:
@@ -497,12 +511,28 @@ def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = N
     todo = [i for i, L in enumerate(launches) if eligible(L)]
     if not todo:
         return []
+    strict = os.environ.get("GFB_JIT_STRICT", "0") == "1"
+    try:
+        _lib_nvrtc()
+    except RuntimeError as exc:
+        if strict:
+            raise
+        _warn_once(f"runtime specialisation off ({exc}); the generic VM kernel runs every elementwise launch")
+        return []
 
     def build(i):
         r = recs[i]
         args = abi.EwArgs.from_buffer_copy(blob[r.arg_offset:r.arg_offset + r.arg_size])
         g = generate(launches[i].kind, args, r.block[0])
-        return None if g is None else (i, compile_cubin(g[0]), g[1])
+        if g is None:
+            return None
+        try:
+            return i, compile_cubin(g[0]), g[1]
+        except RuntimeError as exc:  # a generator bug: keep the generic kernel for this launch, loudly
+            if strict:
+                raise
+            _warn_once(f"{launches[i].label}: specialised kernel failed to compile, generic kernel kept: {exc}")
+            return None
 
     workers = workers or min(len(todo), max(1, (os.cpu_count() or 4)))
     with ThreadPoolExecutor(workers) as ex:
