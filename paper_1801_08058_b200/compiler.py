@@ -747,6 +747,7 @@ class Lowering:
         self.launches: list = []
         self.const_values: dict = {}  # small constants' row-major values, by buffer key
         self._splats: dict = {}
+        self._pads: dict = {}  # channel-padded channel-last copies of conv inputs
         self._window_factors = None
         const_blob = bytearray()
         results = list(g.results)
@@ -1243,6 +1244,32 @@ class Lowering:
         self._col_launch(prog, n_o, 1, 0, "copy", dst.et)
         self.buf[("copy", dst.key)] = dst
 
+    def _pad_channels(self, xb, xs, shape, cp):
+        """Channel-last copy of activation (xb, strides xs) with its channel
+        count padded to `cp` (zeros), for the 16-byte conv kernels; one copy
+        per source, shared by the convolutions that read it."""
+        key = (xb.key, xb.elem_off, tuple(xs), cp)
+        if key in self._pads:
+            return self._pads[key]
+        N, Cc, H, W = shape
+        P = Buffer(self.new_key(), ElementType.F32, (N, cp, H, W), (H * W * cp, 1, W * cp, cp))
+        self.buf[("padc", P.key)] = P
+        root = xb.base if xb.base is not None else xb
+        src = Buffer(xb.key, xb.et, shape, tuple(xs), xb.slot, xb.offset, xb.splat, base=root, elem_off=xb.elem_off)
+        parts = [(src, Buffer(P.key, P.et, shape, P.strides, P.slot, P.offset, None, base=P, elem_off=0))]
+        zshape = (N, cp - Cc, H, W)
+        parts.append((self.splat_buffer(ElementType.F32, 0.0),
+                      Buffer(P.key, P.et, zshape, P.strides, P.slot, P.offset, None, base=P, elem_off=Cc)))
+        for s_, d_ in parts:
+            n_o = element_count(d_.shape)
+            prog = Program(self, extents=(n_o, 1), vec_src=0, et=ElementType.F32)
+            axes = iteration_axes(d_.shape)
+            prog.emit(I_LOAD, k=prog.leaf(s_, axes))
+            prog.emit(I_STORE, k=prog.store_leaf(d_, axes))
+            self._col_launch(prog, n_o, 1, 0, f"padc#{P.key}", ElementType.F32)
+        self._pads[key] = (P, P.strides)
+        return self._pads[key]
+
     def add_launch(self, kind, grid, block, smem, args, prog, label):
         rec = LaunchRec(kind, grid, block, smem, args, prog.reads(), prog.writes(), label)
         rec.algo_bytes = prog.algo_bytes()
@@ -1389,9 +1416,11 @@ class Lowering:
                 and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 30 and element_count(xb.shape) < 2 ** 31
                 and max(abs(v) for v in ys) * max(yb.shape) < 2 ** 30 and element_count(yb.shape) < 2 ** 31)
 
-    def _conv_tcgw(self, n, xb, yb, out, m, ncols, kdim, geo, addr, label):
+    def _conv_tcgw(self, n, xb, yb, out, m, ncols, kdim, geo, addr, label, real_c=None):
         """Weight gradient on gemm_tc.cu gfb_conv_tcgw_kernel (split-K over
-        the pixels when the (r, s, c) x k tiles do not fill the GPU)."""
+        the pixels when the (r, s, c) x k tiles do not fill the GPU).  With
+        `real_c`, the kernel's rows have zero-padded channels (geo E2) and the
+        reduction pass writes only the first real_c of each tap."""
         bn = 64 if ncols <= 64 else 128
         kblocks = (kdim + 31) // 32
         tiles = ((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE)
@@ -1402,7 +1431,7 @@ class Lowering:
         splits = (kblocks + per - 1) // per
         ta = abi.TcgwArgs(M=m, N=ncols, K=kdim, **geo)
         target = out
-        if splits > 1:
+        if splits > 1 or real_c is not None:
             scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
             self.buf[("splitk", n)] = scratch
             ta.k_splits, ta.kb_per_split, ta.split_stride = splits, per, m * ncols
@@ -1420,7 +1449,19 @@ class Lowering:
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
         rec.finalize = _finalize_refs(ta, {"c": target, "a": xb, "b": yb})
         self.launches.append(rec)
-        if splits > 1:
+        if real_c is not None:
+            cp = geo["E2"]
+            taps = m // cp
+            mo = taps * real_c
+            view = Buffer(scratch.key, ElementType.F32, (splits, taps, cp, ncols), (m * ncols, cp * ncols, ncols, 1),
+                          scratch.slot, scratch.offset, None, base=scratch, elem_off=0)
+            p2 = Program(self, extents=(mo * ncols, splits), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(view, [(1, 1, splits), (0, real_c * ncols, taps), (0, ncols, real_c), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.red_out = LeafSpec(out, _conv_out_digits(addr, mo, ncols), True)
+            p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+            self._col_launch(p2, mo * ncols, splits, 1, label + ":splitk", ElementType.F32)
+        elif splits > 1:
             p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
             k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
             p2.emit(I_LOAD, k=k)
@@ -1603,6 +1644,14 @@ class Lowering:
             m, ncols, kdim = K, Cc * R * S, N * Ho * Wo
             if os_[1] != R * S * os_[3] or os_[2] != S * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            real_c = None
+            if (Cc % 4 and Cc < 32 and xb.splat is None and os.environ.get("GFB_PAD_CHANNELS", "1") == "1"
+                    and self._wgrad_mn_ok(xb, (4 * H * W, 1, 4 * W, 4), yb, ys, 4, K)):
+                # few channels (the 3-channel stem): a zero-padded channel-last copy of x
+                # lets the MN-major kernel run; the padded rows of dW are dropped
+                real_c = Cc
+                xb, xs = self._pad_channels(xb, xs, (N, Cc, H, W), align_up(Cc, 4))
+                Cc = align_up(Cc, 4)
             if self._generic_gather_ok(xb, xs):
                 # rows (c, r, s) of the gathered data, columns = output channels
                 b = None if self._wgrad_mn_ok(xb, xs, yb, ys, Cc, K) else self._split(
@@ -1615,8 +1664,9 @@ class Lowering:
                     geo = dict(E1=S, E2=Cc, ro0=xs[2], ro1=xs[3], ro2=xs[1], h0=-pt, w0=-pl, H=H, W=W,
                                Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
                                yo0=ys[0], yo1=ys[2], yo2=ys[3])
-                    addr = {"c_rdiv": Cc, "c_s_hi": os_[3], "c_s_lo": os_[1], "c_sn": os_[0]}
-                    self._conv_tcgw(n, xb, yb, out, Cc * R * S, K, kdim, geo, addr, f"{node.op.wire_name}_tcgw#{n}")
+                    addr = {"c_rdiv": real_c or Cc, "c_s_hi": os_[3], "c_s_lo": os_[1], "c_sn": os_[0]}
+                    self._conv_tcgw(n, xb, yb, out, Cc * R * S, K, kdim, geo, addr, f"{node.op.wire_name}_tcgw#{n}",
+                                    real_c=real_c)
                     return True
                 if xs[1] == 1 and Cc > 1:
                     # channel-last data: rows (r, s, c) so lanes read contiguous channels

@@ -274,7 +274,7 @@ def test_tiny_dot_fused_bit_exact(m, k, n, et):
 
 @pytest.mark.parametrize("mn", [True, False])
 @pytest.mark.parametrize("shape,pad", [((2, 32, 16, 9, 8, 3, 3), (1, 1, 1, 1)), ((2, 5, 8, 7, 7, 3, 3), (1, 0, 0, 1)),
-                                       ((3, 12, 132, 6, 5, 3, 3), (1, 1, 0, 2))])
+                                       ((3, 12, 132, 6, 5, 3, 3), (1, 1, 0, 2)), ((2, 3, 64, 12, 11, 7, 7), (3, 3, 3, 3))])
 def test_wgrad_channel_last_rows_emulated(monkeypatch, shape, pad, mn):
     """ConvBackpropFilter over channel-last data: the MN-major kernel
     (gfb_tcgw_args: 16-byte loads of x and dy, split in the kernel) when the
@@ -291,7 +291,7 @@ def test_wgrad_channel_last_rows_emulated(monkeypatch, shape, pad, mn):
     nhwc = (0, 2, 3, 1)
     h = host_compile(fn, optimize=False, conv_layout="nhwc", parameter_layouts=[nhwc, None, nhwc])
     labels = [L.label for L in h.lowered.launches]
-    if mn and C % 4 == 0 and K % 4 == 0:
+    if mn and K % 4 == 0 and (C % 4 == 0 or C < 32):  # few channels: zero-padded copy of x
         assert any(L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128) for L in h.lowered.launches), labels
         assert not any(L.kind == abi.K_SPLIT_TF32 for L in h.lowered.launches), labels  # no dy planes
     else:
