@@ -1511,7 +1511,8 @@ class Lowering:
         bn = 64 if ncols <= 64 else 128
         ta = abi.TcgArgs(M=m, N=ncols, K=kdim, xs0=xs[0], xs2=xs[2], xs3=xs[3], c_sm=0, **addr, **geo)
         kind = abi.K_CONV_TCG64 if bn == 64 else abi.K_CONV_TCG128
-        grid = ((ncols + bn - 1) // bn, (m + TC_TILE - 1) // TC_TILE, 1)
+        # persistent: one CTA per SM walks the (column tile, row tile) items
+        grid = (max(1, min(((ncols + bn - 1) // bn) * ((m + TC_TILE - 1) // TC_TILE), NUM_SMS)), 1, 1)
         rec = LaunchRec(kind, grid, (320, 1, 1), TCG_SMEM[bn], ta, [xb.key, bhi.key, blo.key], [out.key], label)
         rec.flops = 2 * m * ncols * kdim
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
@@ -1586,6 +1587,15 @@ class Lowering:
             m, ncols, kdim = N * Ho * Wo, K, Cc * R * S
             if os_[2] != Wo * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if (Cc % 4 and Cc < 32 and xb.splat is None and yb.splat is None and ncols >= 32
+                    and os.environ.get("GFB_PAD_CHANNELS_FWD", "0") == "1"):
+                # (measured no faster than the element gather for the 3-channel stem: off by default)
+                # few channels (the 3-channel stem): zero-padded channel-last copies of the
+                # input (shared with its weight gradient) and of the filter feed the 16-byte gather
+                cp = align_up(Cc, 4)
+                xb, xs = self._pad_channels(xb, xs, (N, Cc, H, W), cp)
+                yb, ys = self._pad_channels(yb, ys, (K, Cc, R, S), cp)
+                Cc, kdim = cp, cp * R * S
             if self._gather_ok(xb, xs, Cc, m):
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (R, S, Cc), st=(ys[2], ys[3], ys[1]))
                 if Cc % 32 == 0 and self._tma_box_ok(xb, (N, Cc, H, W), sw, sh):

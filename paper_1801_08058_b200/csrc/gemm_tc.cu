@@ -546,6 +546,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int BN_>
 __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel(const __grid_constant__ gfb_tcg_args p) {
+    // Persistent: CTA b walks (column tile, row tile) items b, b + gridDim.x,
+    // ...; the stage ring, raw ring and TMEM accumulator buffers keep their
+    // counters across items, so one item's epilogue overlaps the next item's
+    // gather and MMAs (small-K convolutions are a few K-blocks per tile).
     using namespace tc;
     using C_ = GCfg<BN_>;
     constexpr int BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NBUF = C_::NBUF, RAW = C_::RAW;
@@ -554,17 +558,17 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* raw = smem + STAGES * STAGE_BYTES;
-    RowInfo* rowtab = reinterpret_cast<RowInfo*>(raw + RAW * A_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(rowtab) + C_::ROWTAB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + RAW * A_BYTES + C_::ROWTAB);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + NBUF;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
     const int nk = (int)((p.K + BK - 1) / BK);
     const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    const int ntn = (int)((p.N + BN - 1) / BN), ntm = (int)((p.M + 127) / 128);
+    const int nitems = ntn * ntm;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -591,74 +595,170 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                unsigned char* st = smem + s * STAGE_BYTES;
-                mbar_expect_tx(&full[s], 2 * B_BYTES);
-                tma_load_2d(st + 2 * A_BYTES, p.tmap[0], kb * BK, n0, &full[s]);
-                tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[1], kb * BK, n0, &full[s]);
+            uint32_t gk = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int n0 = (it % ntn) * BN;
+                for (int kb = 0; kb < nk; ++kb, ++gk) {
+                    const int s = gk % STAGES;
+                    mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], 2 * B_BYTES);
+                    tma_load_2d(st + 2 * A_BYTES, p.tmap[0], kb * BK, n0, &full[s]);
+                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, p.tmap[1], kb * BK, n0, &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) mma_loop<BN, STAGES, STAGE_BYTES, A_BYTES, B_BYTES, CHUNK_KB, NBUF>(smem, full, empty, tfull, tempty, tmem, nk);
-    } else if (warp < 2 + EPI_WARPS) {
-        epilogue<BN, NBUF>(warp, lane, tfull, tempty, tmem, nchunk, resolve<float>(p.tab, p.c), n0, p.N, p.c_sn,
-                           LinearRows{m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo});
-    } else {
-        const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127
-        {
-            const int64_t row = m0 + g;
-            RowInfo ri;
-            if (row < p.M) {
-                const int64_t yx = (int64_t)p.Y * p.X;
-                const int64_t n = row / yx, rem = row - n * yx, y = rem / p.X, x = rem - y * p.X;
-                ri.h = (int32_t)(y * p.sy + p.oy);
-                ri.w = (int32_t)(x * p.sx + p.ox);
-                ri.off = n * p.xs0 + (int64_t)ri.h * p.xs2 + (int64_t)ri.w * p.xs3;
-            } else {
-                ri.off = 0;
-                ri.h = -(1 << 30);
-                ri.w = 0;
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, BN);
+            uint32_t gk = 0, gc = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                for (int i = 0; i < nk; ++i, ++gk) {
+                    const int s = gk % STAGES;
+                    const uint32_t chunk = gc + i / CHUNK_KB;
+                    const int b = chunk % NBUF;
+                    const bool chunk_start = i % CHUNK_KB == 0;
+                    if (chunk_start) {
+                        mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                    const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t adv = (uint64_t)(j * 32) >> 4;
+                        const uint32_t acc = !(chunk_start && j == 0);
+                        mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+                        mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+                        mma_tf32(d, al + adv, bh + adv, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                    if (i % CHUNK_KB == CHUNK_KB - 1 || i == nk - 1) mma_commit(&tfull[b]);
+                }
+                gc += nchunk;
             }
-            rowtab[g] = ri;
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(GATHER_WARPS * 32) : "memory");
+    } else if (warp < 2 + EPI_WARPS) {
+        constexpr int EC = BN < 128 ? BN : 128;
+        const int q = warp & 3;
+        uint32_t gc = 0;
+        float* C = resolve<float>(p.tab, p.c);
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int n0 = (it % ntn) * BN, m0 = (it / ntn) * 128;
+            float acc[EC];
+#pragma unroll
+            for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            for (int c0 = 0; c0 < nchunk; ++c0) {
+                const uint32_t chunk = gc + c0;
+                const int b = chunk % NBUF;
+                mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    uint32_t r[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            }
+            gc += nchunk;
+            const LinearRows rows{m0, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
+            const int64_t roff = rows(q * 32 + lane);
+            if (roff >= 0) {
+                float* dst = C + roff;
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    const int col0 = n0 + c * 32;
+                    if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + col0 + j) =
+                                make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                    }
+                }
+            }
+        }
+    } else {
+        // gather thread: 16-byte piece j (channels 4j..4j+3 of the K-block) of rows rb + 16 i
+        const int g = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..127
         const float* A = resolve<const float>(p.tab, p.a);
         const int j = g & 7, rb = g >> 3;
         const uint32_t swz = (uint32_t)((j ^ (rb & 7)) << 4);  // row & 7 == rb & 7 for every row rb + 16 i
         const int Cc = p.C ? p.C : 32 * p.CB;
-        auto issue = [&](int kb) {
-            // this thread's 16-byte piece: channels c..c+3 of tap (r, s), k = kb*32 + 4j
-            const int k = kb * BK + j * 4, tap = k / Cc, c = k - tap * Cc, r = tap / p.S, s = tap - r * p.S;
-            const bool kok = k < p.K;
-            const int dh = p.ksign * r, dw = p.ksign * s;
-            const int64_t koff = (int64_t)dh * p.xs2 + (int64_t)dw * p.xs3 + c;
-            unsigned char* dst = raw + (kb % RAW) * A_BYTES + swz;
+        uint32_t gk = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int m0 = (it / ntn) * 128;
+            int64_t roff[8];
+            int rh[8], rw[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int row = rb + 16 * i;
-                const RowInfo ri = rowtab[row];
-                const bool ok = kok && (uint32_t)(ri.h + dh) < (uint32_t)p.H && (uint32_t)(ri.w + dw) < (uint32_t)p.W;
-                cp_async16(dst + row * 128, ok ? (const void*)(A + ri.off + koff) : (const void*)A, ok ? 16u : 0u);
+                const int64_t row = m0 + rb + 16 * i;
+                if (row < p.M) {
+                    const int64_t yx = (int64_t)p.Y * p.X;
+                    const int64_t n = row / yx, rem = row - n * yx, y = rem / p.X, x = rem - y * p.X;
+                    rh[i] = (int)(y * p.sy + p.oy);
+                    rw[i] = (int)(x * p.sx + p.ox);
+                    roff[i] = n * p.xs0 + (int64_t)rh[i] * p.xs2 + (int64_t)rw[i] * p.xs3;
+                } else {
+                    roff[i] = 0;
+                    rh[i] = -(1 << 30);
+                    rw[i] = 0;
+                }
             }
-        };
+            auto issue = [&](int kb) {
+                // this thread's 16-byte piece: channels c..c+3 of tap (r, s), k = kb*32 + 4j
+                const int k = kb * BK + j * 4, tap = k / Cc, c = k - tap * Cc, r = tap / p.S, s = tap - r * p.S;
+                const bool kok = k < p.K;
+                const int dh = p.ksign * r, dw = p.ksign * s;
+                const int64_t koff = (int64_t)dh * p.xs2 + (int64_t)dw * p.xs3 + c;
+                unsigned char* dst = raw + ((gk + kb) % RAW) * A_BYTES + swz;
 #pragma unroll
-        for (int kb = 0; kb < RAW; ++kb) {
-            if (kb < nk) issue(kb);
-            cp_async_commit();
-        }
-        for (int kb = 0; kb < nk; ++kb) {
-            cp_async_wait<RAW - 1>();  // this thread's copies of K-block kb have landed
-            const int s = kb % STAGES;
-            mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-            split_rows(su32(raw + (kb % RAW) * A_BYTES) + swz + rb * 128, su32(smem + s * STAGE_BYTES) + swz + rb * 128,
-                       A_BYTES);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
-            if (kb + RAW < nk) issue(kb + RAW);  // reuses the raw slot just consumed (own chunks only)
-            cp_async_commit();
+                for (int i = 0; i < 8; ++i) {
+                    const int row = rb + 16 * i;
+                    const bool ok = kok && (uint32_t)(rh[i] + dh) < (uint32_t)p.H && (uint32_t)(rw[i] + dw) < (uint32_t)p.W;
+                    cp_async16(dst + row * 128, ok ? (const void*)(A + roff[i] + koff) : (const void*)A, ok ? 16u : 0u);
+                }
+            };
+#pragma unroll
+            for (int kb = 0; kb < RAW; ++kb) {
+                if (kb < nk) issue(kb);
+                cp_async_commit();
+            }
+            for (int kb = 0; kb < nk; ++kb) {
+                cp_async_wait<RAW - 1>();  // this thread's copies of K-block kb have landed
+                const uint32_t g2 = gk + kb;
+                const int s = g2 % STAGES;
+                mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
+                split_rows(su32(raw + (g2 % RAW) * A_BYTES) + swz + rb * 128, su32(smem + s * STAGE_BYTES) + swz + rb * 128,
+                           A_BYTES);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+                if (kb + RAW < nk) issue(kb + RAW);  // reuses the raw slot just consumed (own chunks only)
+                cp_async_commit();
+            }
+            gk += nk;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");

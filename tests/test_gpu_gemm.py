@@ -126,6 +126,7 @@ def test_conv_tensor_cores_match_oracle(monkeypatch, op, shape, stride, pad, lay
     ("fwd", (3, 4, 64, 30, 29, 7, 7), (1, 1), (3, 3, 3, 3)),
     ("fwd", (2, 12, 40, 17, 19, 3, 3), (2, 1), (0, 1, 1, 0)),
     ("dgrad", (4, 20, 16, 16, 15, 3, 3), (1, 1), (1, 0, 0, 1)),
+    ("fwd", (4, 3, 64, 40, 36, 7, 7), (1, 1), (3, 3, 3, 3)),  # the stem: zero-padded to 4 channels
 ])
 def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
     """gfb_conv_tcg_kernel (in-kernel NHWC gather + TF32 split) vs the oracle."""
@@ -133,6 +134,7 @@ def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
     from paper_1801_08058_b200 import abi
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_PAD_CHANNELS_FWD", "1")
     N, C, Ko, H, W, R, S = shape
     fn = TL._conv_graph(op, N, C, Ko, H, W, R, S, stride, pad)
     nhwc = gf.Layout((0, 2, 3, 1))

@@ -165,10 +165,14 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     ("fwd", (1, 32, 64, 7, 7, 1, 1), (2, 2), (0, 0, 0, 0)),
     ("dgrad", (2, 40, 64, 8, 7, 3, 3), (1, 1), (1, 0, 0, 1)),
     ("dgrad", (2, 16, 128, 6, 6, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (2, 12, 40, 9, 8, 3, 3), (2, 1), (0, 1, 1, 0)),    # 4-channel pieces, K-blocks span taps
+    ("fwd", (2, 3, 64, 12, 11, 7, 7), (1, 1), (3, 3, 3, 3)),   # 3 channels: zero-padded copies
 ])
 def test_conv_fused_gather_emulated(monkeypatch, op, shape, stride, pad):
-    """NHWC convolutions whose gathered channels come in whole 32-blocks take
-    gfb_conv_tcg_kernel (gather + split inside the GEMM): no im2col planes."""
+    """NHWC convolutions whose gathered channels come in 16-byte pieces take
+    gfb_conv_tcg_kernel (gather + split inside the GEMM): no im2col planes.
+    A 3-channel input is zero-padded to 4 channels first (GFB_PAD_CHANNELS_FWD)."""
+    monkeypatch.setenv("GFB_PAD_CHANNELS_FWD", "1")
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import abi
     from oracle import interp
