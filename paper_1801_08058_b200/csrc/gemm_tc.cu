@@ -711,15 +711,15 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
             const int m0 = (it / ntn) * 128;
             int64_t roff[8];
             int rh[8], rw[8];
+            const uint32_t yx = (uint32_t)p.Y * (uint32_t)p.X;  // rows < 2^31 (lowering checks the tile count)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int64_t row = m0 + rb + 16 * i;
-                if (row < p.M) {
-                    const int64_t yx = (int64_t)p.Y * p.X;
-                    const int64_t n = row / yx, rem = row - n * yx, y = rem / p.X, x = rem - y * p.X;
-                    rh[i] = (int)(y * p.sy + p.oy);
-                    rw[i] = (int)(x * p.sx + p.ox);
-                    roff[i] = n * p.xs0 + (int64_t)rh[i] * p.xs2 + (int64_t)rw[i] * p.xs3;
+                const uint32_t row = (uint32_t)(m0 + rb + 16 * i);
+                if (row < (uint32_t)p.M) {
+                    const uint32_t n = row / yx, rem = row - n * yx, y = rem / (uint32_t)p.X, x = rem - y * (uint32_t)p.X;
+                    rh[i] = (int)y * p.sy + p.oy;
+                    rw[i] = (int)x * p.sx + p.ox;
+                    roff[i] = (int64_t)n * p.xs0 + (int64_t)rh[i] * p.xs2 + (int64_t)rw[i] * p.xs3;
                 } else {
                     roff[i] = 0;
                     rh[i] = -(1 << 30);
@@ -1443,10 +1443,10 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS_GG, 1) gfb_conv_tcgg_ke
             const int64_t row = I.m0 + g;
             int64_t rowoff = 0;
             int hr = -(1 << 28), wr = 0;
-            if (row < p.M) {
-                const int64_t e12 = (int64_t)p.E1 * p.E2;
-                const int64_t i0 = row / e12, rem = row - i0 * e12, i1 = rem / p.E2, i2 = rem - i1 * p.E2;
-                rowoff = i0 * p.ro0 + i1 * p.ro1 + i2 * p.ro2;
+            if (row < p.M) {  // M < 2^31
+                const uint32_t e12 = (uint32_t)p.E1 * (uint32_t)p.E2, r32 = (uint32_t)row;
+                const uint32_t i0 = r32 / e12, rem = r32 - i0 * e12, i1 = rem / (uint32_t)p.E2, i2 = rem - i1 * (uint32_t)p.E2;
+                rowoff = (int64_t)i0 * p.ro0 + (int64_t)i1 * p.ro1 + (int64_t)i2 * p.ro2;
                 if (p.pad0 == 1) {  // rows (r, s, c): the spatial offsets come from the two outer digits
                     hr = (int)(i0 * p.hm + p.h0);
                     wr = (int)(i1 * p.wm + p.w0);
