@@ -319,10 +319,11 @@ def launch_times(exe, dev_in, outs, stream, reps=3):
     total = sum(r[0] for r in rows)
     sys.stderr.write(f"# per-launch times (ms), total {total:.3f}\n")
     jitted = set(getattr(prog, "jit_launches", ()))
+    merged = set(getattr(prog, "skipped", ()))
     for t, i, L in sorted(rows, key=lambda r: -r[0]):
         gbs = L.algo_bytes / (t * 1e-3) / 1e9 if t else 0
         tfs = L.flops / (t * 1e-3) / 1e12 if t else 0
-        label = L.label + (":jit" if i in jitted else "")
+        label = L.label + (":jit" if i in jitted else "") + (":merged-above" if i in merged else "")
         sys.stderr.write(f"{t:9.3f} {100 * t / total:5.1f}% #{i:3d} {label:28s} grid={L.grid} {gbs:8.1f} GB/s {tfs:7.1f} TF/s\n")
 
 

@@ -383,7 +383,9 @@ int gfb_exe_run_one(gfb_exe* exe, uint32_t index, void* const* inputs, void* con
  * loads an sm_100a cubin and returns the handle of its kernel `name`;
  * gfb_exe_set_kernel makes launch `index` (a GFB_K_EW* record, same grid,
  * block and argument block) use that kernel with `smem` bytes of dynamic
- * shared memory.  The executable's CUDA graph is re-captured on its next run. */
+ * shared memory; a NULL kernel skips the launch (its work was merged into
+ * an earlier specialised kernel).  The executable's CUDA graph is
+ * re-captured on its next run. */
 int gfb_kernel_load(const void* cubin, const char* name, const void** kernel);
 int gfb_exe_set_kernel(gfb_exe* exe, uint32_t index, const void* kernel, uint32_t smem);
 

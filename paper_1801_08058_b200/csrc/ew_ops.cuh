@@ -88,6 +88,30 @@ __device__ __forceinline__ void loadV(const T* p, T (&v)[V]) {
     }
 }
 
+// loadV without the read-only (non-coherent) path: for data written earlier
+// in the same kernel (runtime-merged launches, jit.py)
+template <typename T, int V>
+__device__ __forceinline__ void loadV_plain(const T* p, T (&v)[V]) {
+    if constexpr (V == 1) {
+        v[0] = *p;
+    } else if constexpr (V * sizeof(T) == 32) {
+        const int4* q = reinterpret_cast<const int4*>(p);
+        int4 a = q[0], b = q[1];
+        const T* pa = reinterpret_cast<const T*>(&a);
+        const T* pb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+        for (int i = 0; i < V / 2; ++i) {
+            v[i] = pa[i];
+            v[i + V / 2] = pb[i];
+        }
+    } else {
+        uint2 a = *reinterpret_cast<const uint2*>(p);
+        const T* pa = reinterpret_cast<const T*>(&a);
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = pa[i];
+    }
+}
+
 template <typename T, int V>
 __device__ __forceinline__ void storeV(T* p, const T (&v)[V]) {
     if constexpr (V == 1) {

@@ -191,6 +191,7 @@ int launch_one(gfb_exe* e, size_t i, cudaStream_t s) {
         if (r != 0) return nccl_fail(r, "ncclAllReduce");
         return GFB_OK;
     }
+    if (!e->fns[i]) return GFB_OK;  // folded into a preceding merged kernel (gfb_exe_set_kernel with NULL)
     void* kargs[1] = {blob};
     dim3 grid(L.grid[0], L.grid[1], L.grid[2]), block(L.block[0], L.block[1], L.block[2]);
     cudaError_t err = cudaLaunchKernel(e->fns[i], grid, block, kargs, L.smem, s);
@@ -418,12 +419,13 @@ int gfb_kernel_load(const void* cubin, const char* name, const void** kernel) {
 }
 
 int gfb_exe_set_kernel(gfb_exe* e, uint32_t index, const void* kernel, uint32_t smem) {
-    if (!e || index >= e->launches.size() || !kernel) return fail(GFB_ERR_INVALID, "bad launch index or kernel");
+    if (!e || index >= e->launches.size()) return fail(GFB_ERR_INVALID, "bad launch index");
     std::lock_guard<std::mutex> lk(e->mu);
     const uint32_t kind = e->launches[index].kind;
     if (!(kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64))
         return fail(GFB_ERR_INVALID, "only fused elementwise launches take a runtime-compiled kernel");
-    if (smem >= 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (kernel && smem >= 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     e->fns[index] = kernel;
     e->launches[index].smem = smem;
     if (e->graph) {

@@ -131,6 +131,43 @@ def generate(kind: int, args: "abi.EwArgs", block: int = 256):
     return src, g.smem
 
 
+def generate_merged(members, block: int):
+    """One kernel running several single-block launches in order, a block
+    barrier between them (their global writes are then visible to the whole
+    block, and every load is a plain coherent load, never the read-only
+    path).  `members`: [(kind, args)].  Returns (source, smem) or None."""
+    gens = []
+    for kind, args in members:
+        if kind not in KINDS or args.mode not in (1, 2):
+            return None
+        gens.append(_Gen(kind, args, block))
+    src = _kernel_source(gens)
+    return src, max(g.smem for g in gens)
+
+
+def _kernel_source(gens) -> str:
+    block = gens[0].block
+    merged = len(gens) > 1
+    L = ['#include "ew_ops.cuh"', "using namespace gfb;",
+         "__device__ __forceinline__ uint32_t mod_of(uint32_t q, uint32_t mul, uint32_t sh, uint32_t m) {"
+         " return q - fast_div(q, mul, sh) * m; }"]
+    if merged:  # later members read what earlier ones wrote in this kernel: coherent loads only
+        L += ["#define GFB_LD(p) (*(p))", "#define GFB_LOADV(p, x) loadV_plain<T, V>((p), (x))"]
+    else:
+        L += ["#define GFB_LD(p) __ldg(p)", "#define GFB_LOADV(p, x) loadV<T, V>((p), (x))"]
+    bodies = [g.member(i) for i, g in enumerate(gens)]
+    L += bodies
+    L.append(f'extern "C" __global__ void __launch_bounds__({block}, {max(1, 1024 // block)}) '
+             "gfb_jit_ew(const __grid_constant__ gfb_ew_args pa) {")
+    L.append("extern __shared__ __align__(16) unsigned char dyn[];")
+    for i in range(len(gens)):
+        if i:
+            L.append("__syncthreads();")
+        L.append(f"m{i}::run(pa, dyn);")
+    L.append("}")
+    return "\n".join(L) + "\n"
+
+
 def _u32(x: int) -> str:
     return f"{x & 0xFFFFFFFF}u"
 
@@ -206,15 +243,15 @@ class _Gen:
         if full and L.vec != 0:
             off = f"(ob{m} + rp{m})"
             if L.vec == 1:
-                out.append(f"loadV<T, V>(B{k} + {off}, {x});")
+                out.append(f"GFB_LOADV(B{k} + {off}, {x});")
             elif L.vec == 3:
                 for v in range(V):
-                    out.append(f"{x}[{v}] = __ldg(B{k} + (int32_t){off} + {L.dv[v]});")
+                    out.append(f"{x}[{v}] = GFB_LD(B{k} + (int32_t){off} + {L.dv[v]});")
             else:
-                out.append(f"{{ const T s = __ldg(B{k} + {off}); _Pragma(\"unroll\") for (int v = 0; v < V; ++v) {x}[v] = s; }}")
+                out.append(f"{{ const T s = GFB_LD(B{k} + {off}); _Pragma(\"unroll\") for (int v = 0; v < V; ++v) {x}[v] = s; }}")
             return x
         for v in range(V):
-            e = f"__ldg(B{k} + ({self._elem(k, v)}))"
+            e = f"GFB_LD(B{k} + ({self._elem(k, v)}))"
             out.append(f"{x}[{v}] = {e};" if full else f"{x}[{v}] = {v} < nvalid ? {e} : T(0);")
         return x
 
@@ -282,20 +319,17 @@ class _Gen:
 
     # ---- kernel ------------------------------------------------------------
     def emit(self):
+        """The full translation unit of this launch alone."""
+        return _kernel_source([self])
+
+    def member(self, idx):
+        """This launch as `namespace m<idx> { run(pa, dyn) }`."""
         a, V = self.a, self.V
         row = a.mode == 1
         n_o, n_r = a.n_o, a.n_r
-        L = []
-        L.append('#include "ew_ops.cuh"')
-        L.append("using namespace gfb;")
-        L.append("__device__ __forceinline__ uint32_t mod_of(uint32_t q, uint32_t mul, uint32_t sh, uint32_t m) {"
-                 " return q - fast_div(q, mul, sh) * m; }")
-        L.append(f"typedef {self.t} T;")
-        L.append(f"constexpr int V = {V};")
-        L.append(f'extern "C" __global__ void __launch_bounds__({self.block}, {max(1, 1024 // self.block)}) '
-                 f"gfb_jit_ew(const __grid_constant__ gfb_ew_args pa) {{")
+        L = [f"namespace m{idx} {{", f"typedef {self.t} T;", f"constexpr int V = {V};",
+             "__device__ __forceinline__ void run(const gfb_ew_args& pa, unsigned char* dyn) {"]
         L.append("const int nthr = blockDim.x, tid = threadIdx.x;")
-        L.append("extern __shared__ __align__(16) unsigned char dyn[];")
         L.append("T* scratch = reinterpret_cast<T*>(dyn); (void)scratch;")
         for k, lf in enumerate(self.leaves):
             if lf.mode == 1:
@@ -425,7 +459,8 @@ class _Gen:
                 L.append("}")
             L.append("}")  # o loop
             smem = V * self.block * self.esize if (kind and a.split > 1) else 0
-        L.append("}")
+        L.append("}")  # run
+        L.append("}")  # namespace
         self.smem = smem
         return "\n".join(L) + "\n"
 
@@ -505,12 +540,40 @@ def _kernel(lib, cubin: bytes):
     return k
 
 
-def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = None) -> int:
+MERGE = os.environ.get("GFB_JIT_MERGE", "1") == "1"
+
+
+def _groups(launches, recs, todo):
+    """Eligible launches in program order, consecutive single-block ones with
+    the same block size merged into one group (they then run as one kernel
+    with block barriers between them)."""
+    groups, run = [], []
+    prev = None
+    for i in todo:
+        r = recs[i]
+        single = MERGE and tuple(r.grid) == (1, 1, 1)
+        if single and run and prev == i - 1 and recs[run[0]].block[0] == r.block[0]:
+            run.append(i)
+        else:
+            if run:
+                groups.append(run)
+            run = [i]
+            if not single:
+                groups.append(run)
+                run = []
+        prev = i
+    if run:
+        groups.append(run)
+    return groups
+
+
+def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = None):
     """Compile and install specialised kernels for the eligible launches of
-    one executable; returns the indices of the launches replaced."""
+    one executable.  Returns (indices of the launches replaced, indices of
+    launches folded into a preceding merged kernel and skipped)."""
     todo = [i for i, L in enumerate(launches) if eligible(L)]
     if not todo:
-        return []
+        return [], []
     strict = os.environ.get("GFB_JIT_STRICT", "0") == "1"
     try:
         _lib_nvrtc()
@@ -518,27 +581,48 @@ def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = N
         if strict:
             raise
         _warn_once(f"runtime specialisation off ({exc}); the generic VM kernel runs every elementwise launch")
-        return []
+        return [], []
 
-    def build(i):
+    def args_of(i):
         r = recs[i]
-        args = abi.EwArgs.from_buffer_copy(blob[r.arg_offset:r.arg_offset + r.arg_size])
-        g = generate(launches[i].kind, args, r.block[0])
+        return abi.EwArgs.from_buffer_copy(blob[r.arg_offset:r.arg_offset + r.arg_size])
+
+    def build(group):
+        if len(group) == 1:
+            g = generate(launches[group[0]].kind, args_of(group[0]), recs[group[0]].block[0])
+        else:
+            g = generate_merged([(launches[i].kind, args_of(i)) for i in group], recs[group[0]].block[0])
         if g is None:
             return None
         try:
-            return i, compile_cubin(g[0]), g[1]
-        except RuntimeError as exc:  # a generator bug: keep the generic kernel for this launch, loudly
+            return group, compile_cubin(g[0]), g[1]
+        except RuntimeError as exc:  # a generator bug: keep the generic kernel, loudly
             if strict:
                 raise
-            _warn_once(f"{launches[i].label}: specialised kernel failed to compile, generic kernel kept: {exc}")
+            _warn_once(f"{launches[group[0]].label}: specialised kernel failed to compile, generic kernel kept: {exc}")
             return None
 
-    workers = workers or min(len(todo), max(1, (os.cpu_count() or 4)))
+    groups = _groups(launches, recs, todo)
+    # a merged group that fails to generate falls back to its members one by one
+    workers = workers or min(len(groups), max(1, (os.cpu_count() or 4)))
     with ThreadPoolExecutor(workers) as ex:
-        built = [b for b in ex.map(build, todo) if b is not None]
-    for i, cubin, smem in built:
-        rc = lib.gfb_exe_set_kernel(handle, i, C.c_void_p(_kernel(lib, cubin)), smem)
+        built = list(ex.map(build, groups))
+    retry = [[i] for grp, b in zip(groups, built) if b is None and len(grp) > 1 for i in grp]
+    if retry:
+        with ThreadPoolExecutor(workers) as ex:
+            built += list(ex.map(build, retry))
+    replaced, skipped = [], []
+    for b in built:
+        if b is None:
+            continue
+        group, cubin, smem = b
+        rc = lib.gfb_exe_set_kernel(handle, group[0], C.c_void_p(_kernel(lib, cubin)), smem)
         if rc:
-            raise RuntimeError(f"gfb_exe_set_kernel({i}) failed: {lib.gfb_last_error().decode()}")
-    return [i for i, _, _ in built]
+            raise RuntimeError(f"gfb_exe_set_kernel({group[0]}) failed: {lib.gfb_last_error().decode()}")
+        replaced.append(group[0])
+        for i in group[1:]:
+            rc = lib.gfb_exe_set_kernel(handle, i, None, 0)  # runs inside the merged kernel
+            if rc:
+                raise RuntimeError(f"gfb_exe_set_kernel({i}, skip) failed: {lib.gfb_last_error().decode()}")
+            skipped.append(i)
+    return sorted(replaced), sorted(skipped)

@@ -159,8 +159,10 @@ class DeviceProgram:
         ensure_device()
         check(lib().gfb_exe_create(C.byref(plan), C.byref(handle)), "gfb_exe_create")
         self.handle = handle
-        # launches running a runtime-specialised kernel (jit.py) instead of the generic VM
-        self.jit_launches = jit.specialise(lib(), handle, lowered.launches, blob, recs) if jit.enabled() else []
+        # launches running a runtime-specialised kernel (jit.py) instead of the generic VM,
+        # and launches folded into a preceding merged kernel (not launched at all)
+        self.jit_launches, self.skipped = (jit.specialise(lib(), handle, lowered.launches, blob, recs)
+                                           if jit.enabled() else ([], []))
 
     def run(self, in_ptrs: list, out_ptrs: list, stream=None):
         ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
@@ -215,7 +217,8 @@ class Executable:
 
     @property
     def num_launches(self) -> int:
-        return len(self.lowered.launches)
+        """Kernels one run launches (merged single-block launches count once)."""
+        return len(self.lowered.launches) - len(self._program.skipped)
 
     def program(self, private: bool = False) -> DeviceProgram:
         if not private:

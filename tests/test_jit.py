@@ -66,6 +66,30 @@ def test_nvrtc_compiles_sample(tmp_path, monkeypatch):
         assert cubin[:4] == b"\x7fELF"
 
 
+def test_single_block_launches_merge(tmp_path, monkeypatch):
+    """Consecutive single-block launches (config A's softmax / loss chain)
+    form one group, generate one kernel with block barriers between the
+    members and plain (coherent) loads, and compile."""
+    case = next(c for c in G.load("workloads.json.gz") if c["name"] == "mlp_A_small")
+    h = host_compile(G.fn_of(case["fn"]))
+    recs, blob = h.lowered.pack()
+    todo = [i for i, L in enumerate(h.lowered.launches) if L.kind in jit.KINDS]
+    groups = jit._groups(h.lowered.launches, recs, todo)
+    big = max(groups, key=len)
+    assert len(big) >= 3 and all(tuple(recs[i].grid) == (1, 1, 1) for i in big)
+    assert sorted(i for g in groups for i in g) == todo
+    members = [(h.lowered.launches[i].kind, abi.EwArgs.from_buffer_copy(blob[recs[i].arg_offset:recs[i].arg_offset + recs[i].arg_size]))
+               for i in big]
+    src, smem = jit.generate_merged(members, recs[big[0]].block[0])
+    assert src.count("__syncthreads();\nm") == len(big) - 1 and "__ldg" not in src.split("#define GFB_LOADV")[1]
+    try:
+        jit._lib_nvrtc()
+    except RuntimeError as exc:
+        pytest.skip(str(exc))
+    monkeypatch.setenv("GFB_JIT_CACHE", str(tmp_path))
+    assert jit.compile_cubin(src)[:4] == b"\x7fELF"
+
+
 # ---------------------------------------------------------------- GPU
 gf = pytest.importorskip("paper_1801_08058_b200")
 
@@ -86,6 +110,8 @@ def test_workload_jit_bit_identical(name, monkeypatch):
     monkeypatch.setattr(jit, "MIN_BYTES", 0)
     exe, spec = _run(fn, tensors, layout)
     assert exe.program().jit_launches, "no launch was specialised"
+    if name.startswith("mlp_A"):
+        assert exe.program().skipped, "no single-block launches were merged"
     monkeypatch.setenv("GFB_JIT", "0")
     exe0, gen = _run(fn, tensors, layout)
     assert not exe0.program().jit_launches
