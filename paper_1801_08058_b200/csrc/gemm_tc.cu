@@ -1797,23 +1797,35 @@ __global__ void __launch_bounds__(tc::WCfg<BN_>::THREADS, 1) gfb_conv_tcgw_kerne
                 mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
                 const uint32_t src = su32(raw + (g2 % RAW) * RAW_BYTES);
                 const uint32_t dst = su32(smem + s * STAGE_BYTES);
-                // the split is elementwise: each thread converts exactly the pieces it loaded
+                // the split is elementwise: each thread converts exactly the pieces it
+                // loaded; all shared loads first (the stores' memory clobbers would
+                // otherwise serialise load -> convert -> store per piece)
+                float4 xa[KPW], xb[BPT];
+                uint32_t oa[KPW], ob[BPT];
 #pragma unroll
                 for (int t = 0; t < KPW; ++t) {
-                    const uint32_t o = mn_piece(4 * rg, gw * KPW + t);
-                    const float4 x = lds128(src + o), h = trunc_tf32(x);
-                    sts128(dst + o, h);
-                    sts128(dst + A_BYTES + o, make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
-                                                          __fsub_rn(x.w, h.w)));
+                    oa[t] = mn_piece(4 * rg, gw * KPW + t);
+                    xa[t] = lds128(src + oa[t]);
                 }
 #pragma unroll
                 for (int u = 0; u < BPT; ++u) {
                     const int pc = gt + u * 32 * GW, kl = pc / NQ, nq = pc - kl * NQ;
-                    const uint32_t o = mn_piece(4 * nq, kl);
-                    const float4 x = lds128(src + A_BYTES + o), h = trunc_tf32(x);
-                    sts128(dst + 2 * A_BYTES + o, h);
-                    sts128(dst + 2 * A_BYTES + B_BYTES + o, make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y),
-                                                                        __fsub_rn(x.z, h.z), __fsub_rn(x.w, h.w)));
+                    ob[u] = 2 * A_BYTES + mn_piece(4 * nq, kl);
+                    xb[u] = lds128(src + ob[u] - A_BYTES);
+                }
+#pragma unroll
+                for (int t = 0; t < KPW; ++t) {
+                    const float4 x = xa[t], h = trunc_tf32(x);
+                    sts128(dst + oa[t], h);
+                    sts128(dst + A_BYTES + oa[t], make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
+                                                              __fsub_rn(x.w, h.w)));
+                }
+#pragma unroll
+                for (int u = 0; u < BPT; ++u) {
+                    const float4 x = xb[u], h = trunc_tf32(x);
+                    sts128(dst + ob[u], h);
+                    sts128(dst + B_BYTES + ob[u], make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
+                                                              __fsub_rn(x.w, h.w)));
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();

@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <vector>
+#include <cmath>
+#include <cstring>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -156,14 +158,30 @@ __global__ void mma_rate(int var, int iters, long long* cycles) {
     if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-int main() {
+static float trunc_tf32_h(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    u &= 0xffffe000u;
+    memcpy(&x, &u, 4);
+    return x;
+}
+
+int main(int argc, char** argv) {
+    const bool raw = argc > 1;  // operands with full fp32 mantissas: does the MMA truncate them to TF32?
     std::vector<float> A(128 * 32), B(64 * 32), D(128 * 64), R(128 * 64, 0.f);
     srand(1);
-    for (auto& x : A) x = (float)(rand() % 7 - 3);
-    for (auto& x : B) x = (float)(rand() % 5 - 2);
+    for (auto& x : A) x = raw ? (float)(rand() % 7 - 3) * (1.0f + (float)(rand() % 8191) / 8192.0f / 1024.0f) : (float)(rand() % 7 - 3);
+    for (auto& x : B) x = raw ? (float)(rand() % 5 - 2) * (1.0f + (float)(rand() % 8191) / 8192.0f / 1024.0f) : (float)(rand() % 5 - 2);
+    double maxdiff_trunc = 0, maxdiff_full = 0;
     for (int m = 0; m < 128; ++m)
-        for (int n = 0; n < 64; ++n)
-            for (int k = 0; k < 32; ++k) R[m * 64 + n] += A[m * 32 + k] * B[n * 32 + k];
+        for (int n = 0; n < 64; ++n) {
+            double rt = 0, rf = 0;
+            for (int k = 0; k < 32; ++k) {
+                rt += (double)trunc_tf32_h(A[m * 32 + k]) * (double)trunc_tf32_h(B[n * 32 + k]);
+                rf += (double)A[m * 32 + k] * (double)B[n * 32 + k];
+            }
+            R[m * 64 + n] = raw ? (float)rt : (float)rf;
+        }
     float *dA, *dB, *dD;
     cudaMalloc(&dA, A.size() * 4);
     cudaMalloc(&dB, B.size() * 4);
@@ -184,6 +202,20 @@ int main() {
                 if (bad < 3) printf("  var %d mismatch m=%d n=%d got %g want %g\n", var, i / 64, i % 64, D[i], R[i]);
                 ++bad;
             }
+        }
+        if (raw) {  // compare against the truncated-operand and the full-precision products
+            double dt = 0, df = 0;
+            for (int m = 0; m < 128; ++m)
+                for (int n = 0; n < 64; ++n) {
+                    double rt = 0, rf = 0;
+                    for (int k = 0; k < 32; ++k) {
+                        rt += (double)trunc_tf32_h(A[m * 32 + k]) * (double)trunc_tf32_h(B[n * 32 + k]);
+                        rf += (double)A[m * 32 + k] * (double)B[n * 32 + k];
+                    }
+                    dt = fmax(dt, fabs(D[m * 64 + n] - rt));
+                    df = fmax(df, fabs(D[m * 64 + n] - rf));
+                }
+            printf("variant %d raw operands: max |D - trunc product| = %.3g, max |D - full product| = %.3g\n", var, dt, df);
         }
         printf("variant %d: %s, %d mismatches, %d zeros (%s)\n", var, bad ? "FAIL" : "OK", bad, zeros, cudaGetErrorString(e));
         fails += bad != 0;
