@@ -63,3 +63,16 @@ def test_magic_division(d):
     n = n.astype(np.uint64)
     q = n if mul == 0 else (n * np.uint64(mul)) >> np.uint64(32 + sh)
     assert np.array_equal(q, n // np.uint64(d))
+
+
+def test_launch_shared_memory_matches_kernels():
+    """The lowering's dynamic shared-memory sizes equal the kernels' own
+    configurations (host-only entry points of libgfb200.so; no GPU)."""
+    from paper_1801_08058_b200 import compiler as Cm
+
+    lib = ctypes.CDLL(library_path())
+    assert lib.gfb_tc_smem_bytes(0) == Cm.TC_SMEM
+    assert lib.gfb_tc_smem_bytes(1) == Cm.TC_SMEM_W
+    for bn in (64, 128):
+        assert lib.gfb_tcg_smem_bytes(bn) == Cm.TCG_SMEM[bn]
+        assert lib.gfb_tcgw_smem_bytes(bn) == Cm.TCGW_SMEM[bn]
