@@ -804,11 +804,13 @@ class Lowering:
 
         groups = self._sibling_groups(merged)
         grouped = {m for g in groups.values() for m in g[1:]}
+        self._map_side = self._chains(merged | grouped | set(groups))
+        chained = set(self._map_side.values())
         for n in self.order:
             node = self.nodes[n]
             if self.is_heavy(n):
                 self.emit_heavy(n)
-            elif n in self.M and n not in merged and n not in grouped:
+            elif n in self.M and n not in merged and n not in grouped and n not in chained:
                 if node.op is OpKind.SUM:
                     self.emit_reduce(n, side_of.get(n))
                 else:
@@ -1030,6 +1032,36 @@ class Lowering:
         kind = EW1_KIND[et] if scalar else EW_KIND[et]
         self.add_launch(kind, (grid, 1, 1), (256, 1, 1), prog.smem_bytes(args), args, prog, label + (":s" if scalar else ""))
 
+    def _chains(self, taken) -> dict:
+        """consumer -> producer: a materialised map whose first consumer is an
+        elementwise map over the same storage is written as a side output of
+        that consumer's launch (e.g. E's bias Add and the ReLU after it: the
+        pre-activation is still stored for the backward pass, but read once
+        less and one launch fewer)."""
+        if os.environ.get("GFB_CHAINS", "1") != "1":
+            return {}
+        pos = {n: i for i, n in enumerate(self.order)}
+        out, used = {}, set()
+        for n in self.order:
+            if (n not in self.M or n in taken or n in used or n in self.allreduce or not self.is_light(n)
+                    or self.nodes[n].op is OpKind.SUM or n not in self.buf):
+                continue
+            cons = sorted(set(self.consumers[n]), key=lambda c: pos.get(c, 1 << 30))
+            if not cons:
+                continue
+            c = cons[0]
+            if (c in taken or c in out or c in used or c not in self.M or not self.is_light(c) or c in self.allreduce
+                    or self.nodes[c].op is OpKind.SUM or self.nodes[c].op in INDEX_OPS or c not in self.buf
+                    or pos.get(c) is None):
+                continue
+            bn, bc = self.buf[n], self.buf[c]
+            if (bn.shape != bc.shape or bn.et != bc.et or bn.strides != bc.strides or bn.subaxes != bc.subaxes
+                    or bn.splat is not None or bc.splat is not None):
+                continue
+            out[c] = n
+            used |= {n, c}
+        return out
+
     def _sibling_groups(self, merged) -> dict:
         """Materialised maps over the same iteration space whose inputs are
         ready when the first of them is emitted run as one launch with several
@@ -1154,7 +1186,22 @@ class Lowering:
     def _emit_map_in(self, root, shape, dims, et, total, node):
         """One map launch iterating `dims` = [(logical axis, multiplier,
         extent)] outer to inner (a permutation of the axes, or of the
-        sub-digits of flattened axes)."""
+        sub-digits of flattened axes).  A chained producer (`_chains`) is
+        stored by the same launch; if the pair does not fit one program the
+        producer gets its own launch first."""
+        side = getattr(self, "_map_side", {}).get(root)
+        if side is None:
+            return self._emit_map_in1(root, shape, dims, et, total, node)
+        mark = len(self.launches)
+        try:
+            return self._emit_map_in1(root, shape, dims, et, total, node)
+        except (UnsupportedOp, _TooManyDigits):
+            del self.launches[mark:]
+            del self._map_side[root]
+            self.emit_map(side, [side])
+            return self._emit_map_in1(root, shape, dims, et, total, node)
+
+    def _emit_map_in1(self, root, shape, dims, et, total, node):
         pshape = tuple(x for _, _, x in dims)
 
         def logical(axes_p):
@@ -1173,19 +1220,31 @@ class Lowering:
         # rows x columns only when there are enough rows to fill the GPU;
         # a map has no reason to run few, very long rows (flat mode instead)
         few_rows = total // max(n_r, 1) < NUM_SMS * 8 and n_r > 8192
+        side = getattr(self, "_map_side", {}).get(root)
+        label = f"map:{node.op.wire_name}#{root}"
+        if side is not None:
+            label += f"+side:{self.nodes[side].op.wire_name}#{side}"
+
+        def stores(prog, axes):
+            if side is not None:  # the producer first, then the consumer recomputing it inline
+                prog.eval_store(side, axes, self.buf[side])
+                prog.eval_store(root, axes, self.buf[root], also_inline=(side,))
+            else:
+                prog.eval_store(root, axes, self.buf[root])
+
         if n_r >= 128 and inner_from < len(pshape) and not few_rows:
             n_o = total // n_r
             prog = Program(self, extents=(max(n_o, 1), n_r), vec_src=1, et=et)
             try:
-                prog.eval_store(root, logical(split_axes(pshape, inner_from)), self.buf[root])
+                stores(prog, logical(split_axes(pshape, inner_from)))
             except _Retry:
                 prog = None  # a Reshape straddles the row split: use the flat form
             if prog is not None:
-                self._row_launch(prog, n_o, n_r, 0, f"map:{node.op.wire_name}#{root}", et)
+                self._row_launch(prog, n_o, n_r, 0, label, et)
                 return
         prog = Program(self, extents=(total, 1), vec_src=0, et=et)
-        prog.eval_store(root, logical(iteration_axes(pshape)), self.buf[root])
-        self._col_launch(prog, total, 1, 0, f"map:{node.op.wire_name}#{root}", et)
+        stores(prog, logical(iteration_axes(pshape)))
+        self._col_launch(prog, total, 1, 0, label, et)
 
     def emit_reduce(self, s: int, side: int | None):
         node = self.nodes[s]
@@ -2165,8 +2224,9 @@ class Program:
             raise _Retry(self._deepest_child(n, axes))
         self.to_acc(self.value(n, axes))
 
-    def eval_store(self, n, axes, out_buf: Buffer):
-        """Compute node `n` itself (even though it is materialised) and store it."""
+    def eval_store(self, n, axes, out_buf: Buffer, also_inline=()):
+        """Compute node `n` itself (even though it is materialised) and store it
+        (`also_inline`: materialised inputs recomputed rather than loaded)."""
         self._inline = {n}
         node = self.low.nodes[n]
         if node.op in INDEX_OPS:
@@ -2187,14 +2247,19 @@ class Program:
                     raise _Retry(n)
                 r = ("leaf", self.leaf(view, axes))
         else:
-            if self.need_root(n, axes) > MAX_STACK:
-                raise _Retry(self._deepest_child(n, axes))
-            r = self.value(n, axes)
+            # also_inline: those inputs' buffers are hidden while n is evaluated, so
+            # every query (need, is_plain, value) recomputes them
+            hidden = {x: self.low.buf.pop(x) for x in also_inline if x in self.low.buf}
+            try:
+                if self.need_root(n, axes) > MAX_STACK:
+                    raise _Retry(self._deepest_child(n, axes))
+                r = self.value(n, axes)
+            finally:
+                self.low.buf.update(hidden)
         self.to_acc(r)
         self.emit(I_STORE, k=self.store_leaf(out_buf, axes))
 
     def need_root(self, n, axes) -> int:
-        node = self.low.nodes[n]
         saved = self.low.buf.pop(n)
         try:
             return self.need(n, axes)
