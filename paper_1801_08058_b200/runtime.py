@@ -327,9 +327,8 @@ def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     # Intermediate 4-D activations are stored channel-last whatever the
     # caller's layout policy (parameters and results keep theirs): the conv
     # kernels then gather 16-byte runs of channels.  GFB_CHANNELS_LAST=0
-    # keeps the policy's order for intermediates too.
-    cl = os.environ.get("GFB_CHANNELS_LAST", "1")
-    channels_last = policy.conv_order == NHWC_ORDER if cl == "auto" else cl == "1"
+    # stores intermediates in the policy's order instead.
+    channels_last = os.environ.get("GFB_CHANNELS_LAST", "1") == "1" or policy.conv_order == NHWC_ORDER
     lowered = lower(g, layouts, private=private, allreduce=roots, channels_last=channels_last)
     return HostCompiled(g, layouts, plan, instructions, pool_refs, param_index, result_index,
                         param_sig, result_sig, lowered, roots)
