@@ -77,6 +77,7 @@ enum {
     GFB_K_CONV_TCGG128 = 25,
     GFB_K_CONV_TCGW64 = 28,  /* weight gradient over channel-last data, MN-major 16-byte gathers, in-kernel TF32 split of both operands, 128x64 (gfb_tcgw_args) */
     GFB_K_CONV_TCGW128 = 29,
+    GFB_K_CONV_STEM64 = 32, /* few-channel forward conv: 8x16 pixel tiles built from a shared-memory input patch, resident filter planes (gfb_tcg_args) */
     GFB_K_DOT_TH_F32 = 26, /* SIMT Dot, one thread per output, bit-exact (gfb_dot_args) */
     GFB_K_DOT_TH_F64 = 27,
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */

@@ -20,6 +20,7 @@ K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
 K_CONV_TCGW64, K_CONV_TCGW128 = 28, 29
+K_CONV_STEM64 = 32
 K_DOT_TH_F32, K_DOT_TH_F64 = 26, 27
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30

@@ -142,6 +142,8 @@ TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
+STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
+STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
 TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
 TCGW_SMEM = {64: 3 * (2 * 16384 + 2 * 8192) + 3 * (16384 + 8192) + 1280,
              128: 2 * (2 * 16384 + 2 * 16384) + 2 * (16384 + 16384) + 1280}  # WCfg::SMEM_BYTES
@@ -1563,6 +1565,21 @@ class Lowering:
         rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "b_hi": bhi, "b_lo": blo})
         self.launches.append(rec)
 
+    def _conv_stem(self, n, xb, xs, b, out, m, ncols, kdim, geo, yb, label):
+        """Few-channel forward convolution on gemm_tc.cu gfb_conv_stem_kernel
+        (persistent over 8x16 output-pixel tiles)."""
+        bhi, blo, kp = b
+        ta = abi.TcgArgs(M=m, N=ncols, K=kdim, xs0=xs[0], xs2=xs[2], xs3=xs[3], **geo)
+        ta.pad[0], ta.pad[1] = xs[1], kp  # channel stride of x, filter-plane pitch
+        tiles = (m // (geo["Y"] * geo["X"])) * ((geo["Y"] + 7) // 8) * ((geo["X"] + 15) // 16)
+        grid = (max(1, min(tiles, NUM_SMS)), 1, 1)
+        rec = LaunchRec(abi.K_CONV_STEM64, grid, (STEM_THREADS, 1, 1), STEM_SMEM, ta, [xb.key, bhi.key, blo.key],
+                        [out.key], label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "b_hi": bhi, "b_lo": blo})
+        self.launches.append(rec)
+
     def _conv_tcg(self, n, xb, xs, b, out, m, ncols, kdim, geo, addr, yb, label):
         """Conv2D / ConvBackpropData with the activation gather and TF32
         split inside the tensor-core kernel (gemm_tc.cu, gfb_conv_tcg_kernel)."""
@@ -1646,6 +1663,17 @@ class Lowering:
             m, ncols, kdim = N * Ho * Wo, K, Cc * R * S
             if os_[2] != Wo * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if (Cc < 16 and ncols <= 64 and kdim <= 160 and (sh, sw) == (1, 1) and xb.splat is None
+                    and (8 + R - 1) * (16 + S - 1) * Cc <= 1536 and os.environ.get("GFB_CONV_STEM", "1") == "1"
+                    and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 62):
+                # few input channels (the ResNet stem): 8x16 pixel tiles built from a
+                # shared-memory input patch, the filter resident (gemm_tc.cu gfb_conv_stem_kernel)
+                b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (R, S, Cc), st=(ys[2], ys[3], ys[1]))
+                self._conv_stem(n, xb, xs, b, out, m, ncols, kdim,
+                                dict(Y=Ho, X=Wo, sy=1, sx=1, oy=-pt, ox=-pl, H=H, W=W, S=S, C=Cc, ksign=1,
+                                     c_s_hi=os_[0], c_sm=os_[2], c_s_lo=os_[3], c_sn=os_[1]),
+                                yb, f"{node.op.wire_name}_stem#{n}")
+                return True
             if (Cc % 4 and Cc < 32 and xb.splat is None and yb.splat is None and ncols >= 32
                     and os.environ.get("GFB_PAD_CHANNELS_FWD", "0") == "1"):
                 # (measured no faster than the element gather for the 3-channel stem: off by default)

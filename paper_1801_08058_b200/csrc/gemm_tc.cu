@@ -1844,6 +1844,241 @@ __global__ void __launch_bounds__(tc::WCfg<BN_>::THREADS, 1) gfb_conv_tcgw_kerne
     }
 }
 
+// ---------------------------------------------------------------------------
+// Few-channel forward convolution (the 3-channel ResNet stem): a persistent
+// implicit GEMM whose 128 rows are an 8 x 16 block of output pixels.  The
+// block's input patch ((8 + R - 1) x (16 + S - 1) x C, zero outside the
+// image) is staged once per tile in shared memory with plain loads; loader
+// warps then build each K-block's A tile (K order (r, s, c), the filter
+// planes' order) from the patch through a per-K offset table, splitting
+// into TF32 hi/lo as they write.  The filter planes (K <= 160) stay
+// resident in shared memory for the whole kernel (one TMA load per CTA).
+// Arguments: gfb_tcg_args with C the channel count, pad[0] the channel
+// stride of x, unit strides; the output row (n, y, x) is written at
+// n * c_s_hi + y * c_sm + x * c_s_lo, column j at j * c_sn.
+namespace tc {
+struct SCfg {
+    static constexpr int BM = 128, BN = 64, BK = 32, TH = 8, TW = 16;
+    static constexpr int MAXKB = 5;  // K <= 160 (the filter stays resident)
+    static constexpr int STAGES = 4;
+    static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES;
+    static constexpr int BRES_BYTES = MAXKB * 2 * B_BYTES;  // resident filter hi/lo planes
+    static constexpr int PATCH_FLOATS = 1536;              // (8 + R - 1)(16 + S - 1) C <= 1536
+    static constexpr int NBUF = 8;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4, LOAD_WARPS = 8;
+    static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LOAD_WARPS);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BRES_BYTES + 2 * PATCH_FLOATS * 4 + MAXKB * 32 * 4 + 256 + 1024;
+};
+}  // namespace tc
+
+__global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(const __grid_constant__ gfb_tcg_args p) {
+    using namespace tc;
+    using C_ = SCfg;
+    constexpr int BN = C_::BN, BK = C_::BK, TH = C_::TH, TW = C_::TW, STAGES = C_::STAGES, NBUF = C_::NBUF;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int EPI_WARPS = C_::EPI_WARPS, LW = C_::LOAD_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* bres = smem + STAGES * STAGE_BYTES;  // K-block kb: hi at kb * 2 * B_BYTES, lo after it
+    float* patch = reinterpret_cast<float*>(bres + C_::BRES_BYTES);  // two buffers of PATCH_FLOATS
+    int* ktab = reinterpret_cast<int*>(patch + 2 * C_::PATCH_FLOATS);  // patch offset of every k (-1: k >= K)
+    uint64_t* full = reinterpret_cast<uint64_t*>(ktab + C_::MAXKB * 32);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint64_t* bbar = tempty + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bbar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nk = (int)((p.K + BK - 1) / BK);
+    const int Cc = p.C, S = p.S, R = (int)(p.K / ((int64_t)Cc * S));
+    const int PH = TH + R - 1, PW = TW + S - 1, PSZ = PH * PW * Cc;
+    const int tiles_x = (p.X + TW - 1) / TW, tiles_y = (p.Y + TH - 1) / TH;
+    const int nitems = (int)(p.M / ((int64_t)p.Y * p.X)) * tiles_y * tiles_x;  // M = N * Y * X
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], LW);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        mbar_init(bbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // K -> patch offset table: k = (r, s, c), c fastest; patch layout [c][py][px]
+    for (int k = threadIdx.x; k < C_::MAXKB * 32; k += blockDim.x) {
+        int off = -1;
+        if (k < p.K) {
+            const int tap = k / Cc, c = k - tap * Cc, r = tap / S, s = tap - r * S;
+            off = (c * PH + r) * PW + s;
+        }
+        ktab[k] = off;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    auto item_at = [&](int it, int& n, int& y0, int& x0) {
+        const int tx = it % tiles_x, t = it / tiles_x, ty = t % tiles_y;
+        n = t / tiles_y;
+        y0 = ty * TH;
+        x0 = tx * TW;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // the filter planes, once
+            prefetch_tmap(p.tmap[0]);
+            prefetch_tmap(p.tmap[1]);
+            mbar_expect_tx(bbar, (uint32_t)(nk * 2 * B_BYTES));
+            for (int kb = 0; kb < nk; ++kb) {
+                tma_load_2d(bres + kb * 2 * B_BYTES, p.tmap[0], kb * BK, 0, bbar);
+                tma_load_2d(bres + kb * 2 * B_BYTES + B_BYTES, p.tmap[1], kb * BK, 0, bbar);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_wait(bbar, 0);
+            constexpr uint32_t idesc = idesc_tf32(128, BN);
+            uint32_t gk = 0, gt = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
+                const int b = gt % NBUF;
+                mbar_wait(&tempty[b], ((gt / NBUF) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(b * BN);
+                for (int kb = 0; kb < nk; ++kb, ++gk) {
+                    const int s = gk % STAGES;
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                    const uint64_t bh = smem_desc(bres + kb * 2 * B_BYTES), bl = smem_desc(bres + kb * 2 * B_BYTES + B_BYTES);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t adv = (uint64_t)(j * 32) >> 4;
+                        const uint32_t acc = !(kb == 0 && j == 0);
+                        mma_tf32(d, ah + adv, bh + adv, idesc, acc);
+                        mma_tf32(d, ah + adv, bl + adv, idesc, 1);
+                        mma_tf32(d, al + adv, bh + adv, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[b]);
+            }
+        }
+    } else if (warp < 2 + EPI_WARPS) {
+        const int q = warp & 3;
+        float* C = resolve<float>(p.tab, p.c);
+        uint32_t gt = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
+            int n, y0, x0;
+            item_at(it, n, y0, x0);
+            const int b = gt % NBUF;
+            mbar_wait(&tfull[b], (gt / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float acc[BN];
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __uint_as_float(r[j]);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            const int m = q * 32 + lane, y = y0 + m / TW, x = x0 + m % TW;
+            if (y < p.Y && x < p.X) {
+                float* dst = C + (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm + (int64_t)x * p.c_s_lo;
+                if (p.c_sn == 1 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && p.N == BN) {
+#pragma unroll
+                    for (int j = 0; j < BN; j += 4)
+                        *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BN; ++j)
+                        if (j < p.N) dst[(int64_t)j * p.c_sn] = acc[j];
+                }
+            }
+        }
+    } else {
+        // loaders: stage the tile's input patch, then build its A tiles.
+        // Thread t builds row m = t & 127 of each K-block, 16-byte chunks
+        // 4 (t >> 7) .. 4 (t >> 7) + 3 (half of the row's 32 columns).
+        const int t = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0 .. 32 * LW - 1
+        const int m = t & 127, hf = t >> 7;
+        const int py = m / TW, px = m % TW;
+        const uint32_t rsw = (uint32_t)(m & 7);
+        const float* X = resolve<const float>(p.tab, p.a);
+        const int64_t xs1 = p.pad[0];
+        uint32_t gk = 0, gt = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
+            int n, y0, x0;
+            item_at(it, n, y0, x0);
+            float* pt = patch + (gt & 1) * C_::PATCH_FLOATS;
+            for (int i = t; i < PSZ; i += 32 * LW) {
+                const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
+                const int h = y0 + yy + p.oy, w = x0 + xx + p.ox;
+                float v = 0.0f;
+                if ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W)
+                    v = __ldg(X + (int64_t)n * p.xs0 + (int64_t)c * xs1 + (int64_t)h * p.xs2 + (int64_t)w * p.xs3);
+                pt[i] = v;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");  // patch complete
+            const float* prow = pt + py * PW + px;
+            for (int kb = 0; kb < nk; ++kb, ++gk) {
+                const int s = gk % STAGES;
+                mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
+                const uint32_t st = su32(smem + s * STAGE_BYTES) + (uint32_t)m * 128u;
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int j = hf * 4 + jj, k0 = kb * BK + 4 * j;
+                    const int o0 = ktab[k0], o1 = ktab[k0 + 1], o2 = ktab[k0 + 2], o3 = ktab[k0 + 3];
+                    float4 x;
+                    x.x = o0 >= 0 ? prow[o0] : 0.0f;
+                    x.y = o1 >= 0 ? prow[o1] : 0.0f;
+                    x.z = o2 >= 0 ? prow[o2] : 0.0f;
+                    x.w = o3 >= 0 ? prow[o3] : 0.0f;
+                    const float4 h = trunc_tf32(x);
+                    const uint32_t o = ((uint32_t)j ^ rsw) << 4;
+                    sts128(st + o, h);
+                    sts128(st + A_BYTES + o, make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
+                                                         __fsub_rn(x.w, h.w)));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 }  // namespace gfb
 
 
@@ -1870,10 +2105,12 @@ extern "C" const void* gfb_tc_kernel_ptr(int kind) {
     if (kind == GFB_K_CONV_TCGG128) return (const void*)gfb::gfb_conv_tcgg_kernel<128>;
     if (kind == GFB_K_CONV_TCX128) return (const void*)gfb::gfb_conv_tcx_kernel<128>;
     if (kind == GFB_K_CONV_TCGW64) return (const void*)gfb::gfb_conv_tcgw_kernel<64>;
+    if (kind == GFB_K_CONV_STEM64) return (const void*)gfb::gfb_conv_stem_kernel;
     if (kind == GFB_K_CONV_TCGW128) return (const void*)gfb::gfb_conv_tcgw_kernel<128>;
     return nullptr;
 }
 
 extern "C" int gfb_tc_smem_bytes(int wide) { return wide ? gfb::tc::Cfg<256>::SMEM_BYTES : gfb::tc::Cfg<128>::SMEM_BYTES; }
 extern "C" int gfb_tcgw_smem_bytes(int bn) { return bn == 64 ? gfb::tc::WCfg<64>::SMEM_BYTES : gfb::tc::WCfg<128>::SMEM_BYTES; }
+extern "C" int gfb_stem_smem_bytes(void) { return gfb::tc::SCfg::SMEM_BYTES; }
 extern "C" int gfb_tcg_smem_bytes(int bn) { return bn == 64 ? gfb::tc::GCfg<64>::SMEM_BYTES : gfb::tc::GCfg<128>::SMEM_BYTES; }

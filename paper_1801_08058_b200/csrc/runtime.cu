@@ -173,7 +173,7 @@ const void* kernel_for(uint32_t kind) {
         return gfb_simt_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_TC32 || kind == GFB_K_DOT_TC32W || kind == GFB_K_DOT_TC32P || kind == GFB_K_SPLIT_TF32 || kind == GFB_K_CONV_TCG64 ||
         kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128 || kind == GFB_K_CONV_TCGG64 ||
-        kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128)
+        kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128 || kind == GFB_K_CONV_STEM64)
         return gfb_tc_kernel_ptr((int)kind);
     return nullptr;
 }
@@ -342,14 +342,15 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
             }
         }
-        if (L.kind == GFB_K_CONV_TCG64 || L.kind == GFB_K_CONV_TCG128) {
+        if (L.kind == GFB_K_CONV_TCG64 || L.kind == GFB_K_CONV_TCG128 || L.kind == GFB_K_CONV_STEM64) {
             gfb_tcg_args* a = (gfb_tcg_args*)(e->args.data() + L.arg_offset);
             const uint64_t refs[2] = {a->b_hi, a->b_lo};
             for (int t = 0; t < 2; ++t) {
                 if ((refs[t] >> 56) != GFB_SLOT_ARENA)
                     return bail(fail(GFB_ERR_INVALID, "tensor-core operand planes must live in the arena"));
                 void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
-                if (!encode_plane_map(addr, a->N, a->K, L.kind == GFB_K_CONV_TCG64 ? 64 : 128, a->tmap[t]))
+                const int64_t kp = L.kind == GFB_K_CONV_STEM64 ? a->pad[1] : a->K;  // stem: plane pitch in pad[1]
+                if (!encode_plane_map(addr, a->N, kp, L.kind == GFB_K_CONV_TCG128 ? 128 : 64, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
             }
         }

@@ -352,6 +352,33 @@ def run_tcg(mem, a):
     mem.view(a.c, np.float32)[(i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn] = out
 
 
+def run_stem(mem, a):
+    """gfb_conv_stem_kernel: rows (n, y, x), k = (r, s, c) over (R, S, C) reads
+    x[n, c, y + oy + r, x + ox + s] through strides (xs0, pad[0], xs2, xs3),
+    zero outside; output row (n, y, x) at n*c_s_hi + y*c_sm + x*c_s_lo."""
+    src = mem.view(a.a, np.float32)
+    M, K, C = a.M, a.K, a.C
+    R = K // (C * a.S)
+    row = np.arange(M, dtype=np.int64)
+    n, rem = row // (a.Y * a.X), row % (a.Y * a.X)
+    y, x = rem // a.X, rem % a.X
+    k = np.arange(K, dtype=np.int64)
+    c, tap = k % C, k // C
+    r, s = tap // a.S, tap % a.S
+    h = (y + a.oy)[:, None] + r[None, :]
+    w = (x + a.ox)[:, None] + s[None, :]
+    ok = (h >= 0) & (h < a.H) & (w >= 0) & (w < a.W)
+    off = n[:, None] * a.xs0 + c[None, :] * a.pad[0] + h * a.xs2 + w * a.xs3
+    xv = np.where(ok, src[np.where(ok, off, 0)], np.float32(0)).astype(np.float32)
+    ahi, alo = (v.astype(np.float64) for v in _trunc_split(xv))
+    kp = a.pad[1]
+    bhi = mem.view(a.b_hi, np.float32)[: a.N * kp].reshape(a.N, kp)[:, :K].astype(np.float64)
+    blo = mem.view(a.b_lo, np.float32)[: a.N * kp].reshape(a.N, kp)[:, :K].astype(np.float64)
+    out = (ahi @ bhi.T + ahi @ blo.T + alo @ bhi.T).astype(np.float32)
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    mem.view(a.c, np.float32)[(n * a.c_s_hi + y * a.c_sm + x * a.c_s_lo)[:, None] + j * a.c_sn] = out
+
+
 def run_tcx(mem, a):
     """gfb_conv_tcx_kernel: rows are output pixels (n, y, x); the TMA box for
     K-block (r, s, cb) reads act[n, y*sy + oy + ksign*r, x*sx + ox + ksign*s,
@@ -482,6 +509,8 @@ def _run_launch(mem, L):
         run_tcg(mem, L.args)
     elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):
         run_tcx(mem, L.args)
+    elif L.kind == abi.K_CONV_STEM64:
+        run_stem(mem, L.args)
     elif L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128):
         run_tcgw(mem, L.args)
     elif L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128):

@@ -93,7 +93,7 @@ def test_tc_dot_large_config_E_layer():
     ("dgrad", (4, 16, 32, 32, 32, 3, 3), (1, 1), (1, 0, 0, 1), "identity"),
     ("wgrad", (8, 16, 32, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
     ("wgrad", (8, 3, 16, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
-    ("fwd", (4, 3, 64, 40, 40, 7, 7), (1, 1), (3, 3, 3, 3), "identity"),   # the config-D stem shape, generic gather
+    ("fwd", (4, 3, 64, 40, 40, 7, 7), (1, 1), (3, 3, 3, 3), "identity"),   # the config-D stem shape (stem kernel)
     ("wgrad", (4, 3, 64, 40, 40, 7, 7), (1, 1), (3, 3, 3, 3), "identity"),
     ("fwd", (2, 16, 32, 33, 31, 3, 3), (2, 1), (0, 1, 1, 0), "nhwc"),
     ("dgrad", (4, 16, 40, 20, 20, 3, 3), (1, 1), (1, 1, 1, 1), "identity"),
@@ -105,7 +105,7 @@ def test_conv_tensor_cores_match_oracle(monkeypatch, op, shape, stride, pad, lay
     N, C, Ko, H, W, R, S = shape
     fn = TL._conv_graph(op, N, C, Ko, H, W, R, S, stride, pad)
     exe = gf.compile_function(fn, conv_layout=layout) if op == "fwd" else gf.compile_function(fn)
-    assert any("_tc" in L.label for L in exe.lowered.launches)
+    assert any("_tc" in L.label or "_stem#" in L.label for L in exe.lowered.launches)
     rng = np.random.default_rng(7)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
@@ -135,6 +135,7 @@ def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
 
     monkeypatch.setenv("GFB_CONV", "tc")
     monkeypatch.setenv("GFB_PAD_CHANNELS_FWD", "1")
+    monkeypatch.setenv("GFB_CONV_STEM", "0")
     N, C, Ko, H, W, R, S = shape
     fn = TL._conv_graph(op, N, C, Ko, H, W, R, S, stride, pad)
     nhwc = gf.Layout((0, 2, 3, 1))
@@ -223,6 +224,32 @@ def test_wgrad_channel_last_matches_oracle(monkeypatch, shape, pad, mn):
     used = any(L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128) for L in exe.lowered.launches)
     assert used == (mn and Ko % 4 == 0 and (C % 4 == 0 or C < 32)), [L.label for L in exe.lowered.launches]
     rng = np.random.default_rng(23)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = gf.call(exe, tens)[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("shape,pad,layout", [
+    ((4, 3, 64, 40, 36, 7, 7), (3, 3, 3, 3), "identity"),   # the ResNet stem, NCHW input
+    ((2, 3, 16, 32, 32, 3, 3), (1, 1, 1, 1), "identity"),   # config C's first layer (16 < 64 columns)
+    ((3, 4, 64, 17, 23, 5, 5), (2, 1, 0, 3), "nhwc"),       # channel-last input, partial tiles
+    ((2, 1, 40, 9, 11, 3, 3), (0, 0, 1, 1), "identity"),    # one channel, no padding rows
+])
+def test_conv_stem_kernel_matches_oracle(monkeypatch, shape, pad, layout):
+    """gfb_conv_stem_kernel (8x16 pixel tiles from a shared-memory input
+    patch, resident filter planes) vs the oracle."""
+    import test_lowering as TL
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, Ko, H, W, R, S = shape
+    fn = TL._conv_graph("fwd", N, C, Ko, H, W, R, S, (1, 1), pad)
+    lay = [gf.Layout((0, 2, 3, 1)), None] if layout == "nhwc" else None
+    exe = gf.compile_function(fn, conv_layout=layout, parameter_layouts=lay)
+    assert any(L.kind == abi.K_CONV_STEM64 for L in exe.lowered.launches), [L.label for L in exe.lowered.launches]
+    rng = np.random.default_rng(31)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
     out = gf.call(exe, tens)[0].to_numpy()

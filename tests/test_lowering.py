@@ -149,7 +149,9 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     fn = _conv_graph(op, N, C, K, H, W, R, S, stride, pad)
     h = host_compile(fn, optimize=False, conv_layout=layout) if op == "fwd" else host_compile(fn, optimize=False)
     labels = [L.label for L in h.lowered.launches]
-    assert any("_tc" in l for l in labels), labels
+    assert any("_tc" in l or "_stem" in l for l in labels), labels
+    if op == "fwd" and C < 16 and stride == (1, 1):  # few channels: the patch-staged stem kernel
+        assert any("_stem#" in l for l in labels), labels
     if op == "wgrad" and N * H * W >= 2048:  # long K: split-K with a deterministic second pass
         assert any(":splitk" in l for l in labels), labels
     rng = np.random.default_rng(5)
@@ -171,8 +173,10 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
 def test_conv_fused_gather_emulated(monkeypatch, op, shape, stride, pad):
     """NHWC convolutions whose gathered channels come in 16-byte pieces take
     gfb_conv_tcg_kernel (gather + split inside the GEMM): no im2col planes.
-    A 3-channel input is zero-padded to 4 channels first (GFB_PAD_CHANNELS_FWD)."""
+    A 3-channel input is zero-padded to 4 channels first (GFB_PAD_CHANNELS_FWD,
+    with the patch-staged stem kernel off)."""
     monkeypatch.setenv("GFB_PAD_CHANNELS_FWD", "1")
+    monkeypatch.setenv("GFB_CONV_STEM", "0")
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import abi
     from oracle import interp
