@@ -2031,20 +2031,41 @@ __global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(con
         const uint32_t rsw = (uint32_t)(m & 7);
         const float* X = resolve<const float>(p.tab, p.a);
         const int64_t xs1 = p.pad[0];
+        // the next tile's patch is loaded into registers while this tile's A
+        // tiles are built, so the global-load latency stays off the critical path
+        constexpr int PPT = (C_::PATCH_FLOATS + 32 * LW - 1) / (32 * LW);  // patch elements per thread
+        float pre[PPT];
+        auto fetch = [&](int it2) {
+            int n2, ya, xa;
+            item_at(it2, n2, ya, xa);
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) {
+                const int i = t + u * 32 * LW;
+                float v = 0.0f;
+                if (i < PSZ) {
+                    const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
+                    const int h = ya + yy + p.oy, w = xa + xx + p.ox;
+                    if ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W)
+                        v = __ldg(X + (int64_t)n2 * p.xs0 + (int64_t)c * xs1 + (int64_t)h * p.xs2 + (int64_t)w * p.xs3);
+                }
+                pre[u] = v;
+            }
+        };
+        auto park = [&](float* pt) {
+#pragma unroll
+            for (int u = 0; u < PPT; ++u)
+                if (t + u * 32 * LW < PSZ) pt[t + u * 32 * LW] = pre[u];
+        };
+        if ((int)blockIdx.x < nitems) {
+            fetch(blockIdx.x);
+            park(patch);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
         uint32_t gk = 0, gt = 0;
         for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
-            int n, y0, x0;
-            item_at(it, n, y0, x0);
-            float* pt = patch + (gt & 1) * C_::PATCH_FLOATS;
-            for (int i = t; i < PSZ; i += 32 * LW) {
-                const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
-                const int h = y0 + yy + p.oy, w = x0 + xx + p.ox;
-                float v = 0.0f;
-                if ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W)
-                    v = __ldg(X + (int64_t)n * p.xs0 + (int64_t)c * xs1 + (int64_t)h * p.xs2 + (int64_t)w * p.xs3);
-                pt[i] = v;
-            }
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");  // patch complete
+            const bool more = it + (int)gridDim.x < nitems;
+            if (more) fetch(it + gridDim.x);
+            const float* pt = patch + (gt & 1) * C_::PATCH_FLOATS;
             const float* prow = pt + py * PW + px;
             for (int kb = 0; kb < nk; ++kb, ++gk) {
                 const int s = gk % STAGES;
@@ -2069,6 +2090,9 @@ __global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(con
                 __syncwarp();
                 if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
             }
+            // the other buffer's last readers (tile it - gridDim.x) passed the previous barrier
+            if (more) park(patch + ((gt + 1) & 1) * C_::PATCH_FLOATS);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
