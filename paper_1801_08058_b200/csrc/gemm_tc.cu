@@ -2035,20 +2035,25 @@ __global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(con
         // tiles are built, so the global-load latency stays off the critical path
         constexpr int PPT = (C_::PATCH_FLOATS + 32 * LW - 1) / (32 * LW);  // patch elements per thread
         float pre[PPT];
+        // this thread's patch elements (c, yy, xx) are the same for every tile
+        int pyy[PPT], pxx[PPT];
+        int64_t poff[PPT];
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int i = t + u * 32 * LW;
+            const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
+            pyy[u] = i < PSZ ? yy + p.oy : -(1 << 28);
+            pxx[u] = xx + p.ox;
+            poff[u] = (int64_t)c * xs1 + (int64_t)(yy + p.oy) * p.xs2 + (int64_t)(xx + p.ox) * p.xs3;
+        }
         auto fetch = [&](int it2) {
             int n2, ya, xa;
             item_at(it2, n2, ya, xa);
+            const float* base = X + (int64_t)n2 * p.xs0 + (int64_t)ya * p.xs2 + (int64_t)xa * p.xs3;
 #pragma unroll
             for (int u = 0; u < PPT; ++u) {
-                const int i = t + u * 32 * LW;
-                float v = 0.0f;
-                if (i < PSZ) {
-                    const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
-                    const int h = ya + yy + p.oy, w = xa + xx + p.ox;
-                    if ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W)
-                        v = __ldg(X + (int64_t)n2 * p.xs0 + (int64_t)c * xs1 + (int64_t)h * p.xs2 + (int64_t)w * p.xs3);
-                }
-                pre[u] = v;
+                const int h = ya + pyy[u], w = xa + pxx[u];
+                pre[u] = ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W) ? __ldg(base + poff[u]) : 0.0f;
             }
         };
         auto park = [&](float* pt) {
@@ -2071,16 +2076,23 @@ __global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(con
                 const int s = gk % STAGES;
                 mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
                 const uint32_t st = su32(smem + s * STAGE_BYTES) + (uint32_t)m * 128u;
+                // all 16 offsets, then all 16 patch reads, then the split (no
+                // load -> dependent load -> store chain per element)
+                int4 ko[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) ko[jj] = *reinterpret_cast<const int4*>(ktab + kb * BK + 4 * (hf * 4 + jj));
+                float4 xv[4];
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
-                    const int j = hf * 4 + jj, k0 = kb * BK + 4 * j;
-                    const int o0 = ktab[k0], o1 = ktab[k0 + 1], o2 = ktab[k0 + 2], o3 = ktab[k0 + 3];
-                    float4 x;
-                    x.x = o0 >= 0 ? prow[o0] : 0.0f;
-                    x.y = o1 >= 0 ? prow[o1] : 0.0f;
-                    x.z = o2 >= 0 ? prow[o2] : 0.0f;
-                    x.w = o3 >= 0 ? prow[o3] : 0.0f;
-                    const float4 h = trunc_tf32(x);
+                    xv[jj].x = ko[jj].x >= 0 ? prow[ko[jj].x] : 0.0f;
+                    xv[jj].y = ko[jj].y >= 0 ? prow[ko[jj].y] : 0.0f;
+                    xv[jj].z = ko[jj].z >= 0 ? prow[ko[jj].z] : 0.0f;
+                    xv[jj].w = ko[jj].w >= 0 ? prow[ko[jj].w] : 0.0f;
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int j = hf * 4 + jj;
+                    const float4 x = xv[jj], h = trunc_tf32(x);
                     const uint32_t o = ((uint32_t)j ^ rsw) << 4;
                     sts128(st + o, h);
                     sts128(st + A_BYTES + o, make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
