@@ -1929,9 +1929,19 @@ __global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(con
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
+    // item -> (image, tile row, tile column) with float-reciprocal divisions
+    // (item indices < 2^24 are exact in float; one correction step each)
+    const float inv_tx = 1.0f / (float)tiles_x, inv_ty = 1.0f / (float)tiles_y;
+    auto divmod = [](int a, int d, float inv, int& q) {
+        q = (int)((float)a * inv);
+        if (q * d > a) --q;
+        else if ((q + 1) * d <= a) ++q;
+        return a - q * d;
+    };
     auto item_at = [&](int it, int& n, int& y0, int& x0) {
-        const int tx = it % tiles_x, t = it / tiles_x, ty = t % tiles_y;
-        n = t / tiles_y;
+        int t;
+        const int tx = divmod(it, tiles_x, inv_tx, t);
+        const int ty = divmod(t, tiles_y, inv_ty, n);
         y0 = ty * TH;
         x0 = tx * TW;
     };
