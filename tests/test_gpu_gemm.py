@@ -52,8 +52,11 @@ def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
     (4, 6, 3001, False, False, "F32"),
     (8, 9, 700, True, False, "F32"),
     (3, 17, 1025, False, True, "F64"),
-    (128, 512, 10, False, False, "F32"),   # thread-per-output kernel
+    (128, 512, 10, False, False, "F32"),   # thread-per-output kernel, A rows and B staged in shared memory
     (40, 33, 70, True, True, "F64"),
+    (512, 128, 10, True, False, "F32"),    # the classifier's weight gradient (transposed A)
+    (33, 300, 7, False, True, "F64"),
+    (50, 4000, 8, False, False, "F32"),    # too big to stage: the register-pipelined form
 ])
 def test_small_m_dot_bit_exact(m, k, n, ta, tb, et):
     """Few-row Dots with k > TINY_DOT_K take the thread-per-column SIMT
