@@ -389,6 +389,14 @@ int gfb_exe_run_one(gfb_exe* exe, uint32_t index, void* const* inputs, void* con
  * re-captured on its next run. */
 int gfb_kernel_load(const void* cubin, const char* name, const void** kernel);
 int gfb_exe_set_kernel(gfb_exe* exe, uint32_t index, const void* kernel, uint32_t smem);
+/* Multi-stream capture schedule: launch i is captured on stream stream_of[i]
+ * (< n_streams <= 16) after waiting for the earlier launches
+ * deps[dep_offsets[i] .. dep_offsets[i + 1]) it conflicts with, so
+ * independent launches become concurrent nodes of the executable's CUDA
+ * graph (re-captured on the next run).  n_streams == 1 restores the single
+ * in-order stream. */
+int gfb_exe_set_schedule(gfb_exe* exe, uint32_t n_streams, const uint32_t* stream_of, const uint32_t* dep_offsets,
+                         const uint32_t* deps);
 
 /* NCCL communicator, one per process / GPU.  `unique_id` is the 128-byte
  * ncclUniqueId created by rank 0 with gfb_comm_unique_id and shared by the

@@ -162,6 +162,14 @@ struct gfb_exe {
     cudaStream_t capture_stream = nullptr;
     gfb_comm* comm = nullptr;
     std::mutex mu;
+    // multi-stream capture schedule (gfb_exe_set_schedule): stream of each
+    // launch and the earlier launches it must wait for (CSR)
+    uint32_t n_streams = 1;
+    std::vector<uint32_t> stream_of, dep_off, deps;
+    std::vector<cudaStream_t> streams;  // streams[0] is capture_stream
+    std::vector<cudaEvent_t> done;
+    cudaEvent_t fork = nullptr;
+    std::vector<cudaEvent_t> joins;
 };
 
 namespace {
@@ -209,6 +217,31 @@ int launch_all(gfb_exe* e, cudaStream_t s) {
     return GFB_OK;
 }
 
+// Capture-time launch order over several streams: every launch waits (by
+// event) only for the earlier launches it conflicts with, so independent
+// branches of the step (weight gradients next to data gradients, bias sums,
+// optimizer updates) become concurrent nodes of the CUDA graph.
+int launch_all_streams(gfb_exe* e, cudaStream_t s0) {
+    CUDA_TRY(cudaEventRecord(e->fork, s0));
+    for (uint32_t k = 1; k < e->n_streams; ++k) CUDA_TRY(cudaStreamWaitEvent(e->streams[k], e->fork, 0));
+    for (size_t i = 0; i < e->launches.size(); ++i) {
+        const uint32_t sk = e->stream_of[i];
+        cudaStream_t st = sk == 0 ? s0 : e->streams[sk];
+        for (uint32_t d = e->dep_off[i]; d < e->dep_off[i + 1]; ++d) {
+            const uint32_t j = e->deps[d];
+            if (e->stream_of[j] != sk) CUDA_TRY(cudaStreamWaitEvent(st, e->done[j], 0));
+        }
+        int rc = launch_one(e, i, st);
+        if (rc != GFB_OK) return rc;
+        CUDA_TRY(cudaEventRecord(e->done[i], st));
+    }
+    for (uint32_t k = 1; k < e->n_streams; ++k) {
+        CUDA_TRY(cudaEventRecord(e->joins[k], e->streams[k]));
+        CUDA_TRY(cudaStreamWaitEvent(s0, e->joins[k], 0));
+    }
+    return GFB_OK;
+}
+
 int upload_table(gfb_exe* e, void* const* inputs, void* const* outputs, cudaStream_t s) {
     CUDA_TRY(cudaEventSynchronize(e->tab_done));  // previous run consumed the staging copy
     e->htab[GFB_SLOT_ARENA] = e->arena;
@@ -220,7 +253,20 @@ int upload_table(gfb_exe* e, void* const* inputs, void* const* outputs, cudaStre
     return GFB_OK;
 }
 
+void release_schedule(gfb_exe* e) {
+    for (size_t k = 1; k < e->streams.size(); ++k) cudaStreamDestroy(e->streams[k]);
+    for (cudaEvent_t ev : e->done) cudaEventDestroy(ev);
+    for (size_t k = 1; k < e->joins.size(); ++k) cudaEventDestroy(e->joins[k]);
+    if (e->fork) cudaEventDestroy(e->fork);
+    e->streams.clear();
+    e->done.clear();
+    e->joins.clear();
+    e->fork = nullptr;
+    e->n_streams = 1;
+}
+
 void release(gfb_exe* e) {
+    release_schedule(e);
     if (e->graph) cudaGraphExecDestroy(e->graph);
     if (e->capture_stream) cudaStreamDestroy(e->capture_stream);
     if (e->tab_done) cudaEventDestroy(e->tab_done);
@@ -382,7 +428,7 @@ int gfb_exe_run(gfb_exe* e, void* const* inputs, void* const* outputs, void* str
         // Capture on a private stream: nothing executes during capture, and
         // the instantiated graph is then launched on the caller's stream.
         CUDA_TRY(cudaStreamBeginCapture(e->capture_stream, cudaStreamCaptureModeThreadLocal));
-        rc = launch_all(e, e->capture_stream);
+        rc = e->n_streams > 1 ? launch_all_streams(e, e->capture_stream) : launch_all(e, e->capture_stream);
         cudaGraph_t g = nullptr;
         cudaError_t end = cudaStreamEndCapture(e->capture_stream, &g);
         if (rc != GFB_OK) {
@@ -416,6 +462,40 @@ int gfb_kernel_load(const void* cubin, const char* name, const void** kernel) {
     cudaKernel_t k = nullptr;
     CUDA_TRY(cudaLibraryGetKernel(&k, lib, name));
     *kernel = (const void*)k;  // the library stays loaded for the life of the process
+    return GFB_OK;
+}
+
+int gfb_exe_set_schedule(gfb_exe* e, uint32_t n_streams, const uint32_t* stream_of, const uint32_t* dep_offsets,
+                         const uint32_t* deps) {
+    if (!e || n_streams == 0 || n_streams > 16 || (n_streams > 1 && (!stream_of || !dep_offsets)))
+        return fail(GFB_ERR_INVALID, "bad schedule");
+    std::lock_guard<std::mutex> lk(e->mu);
+    const size_t n = e->launches.size();
+    release_schedule(e);
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    if (n_streams == 1) return GFB_OK;
+    for (size_t i = 0; i < n; ++i) {
+        if (stream_of[i] >= n_streams) return fail(GFB_ERR_INVALID, "schedule: stream index out of range");
+        for (uint32_t d = dep_offsets[i]; d < dep_offsets[i + 1]; ++d)
+            if (deps[d] >= i) return fail(GFB_ERR_INVALID, "schedule: a launch may only wait for earlier launches");
+    }
+    e->stream_of.assign(stream_of, stream_of + n);
+    e->dep_off.assign(dep_offsets, dep_offsets + n + 1);
+    e->deps.assign(deps, deps + dep_offsets[n]);
+    e->streams.assign(n_streams, nullptr);
+    e->streams[0] = e->capture_stream;
+    e->joins.assign(n_streams, nullptr);
+    e->done.assign(n, nullptr);
+    e->n_streams = n_streams;
+    for (uint32_t k = 1; k < n_streams; ++k) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&e->streams[k], cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&e->joins[k], cudaEventDisableTiming));
+    }
+    for (size_t i = 0; i < n; ++i) CUDA_TRY(cudaEventCreateWithFlags(&e->done[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
     return GFB_OK;
 }
 

@@ -79,6 +79,7 @@ def lib():
         L.gfb_comm_destroy.argtypes = [vp]
         L.gfb_kernel_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
         L.gfb_exe_set_kernel.argtypes = [vp, u32, vp, u32]
+        L.gfb_exe_set_schedule.argtypes = [vp, u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]
         _LIB = L
         return L
 
@@ -163,6 +164,14 @@ class DeviceProgram:
         # and launches folded into a preceding merged kernel (not launched at all)
         self.jit_launches, self.skipped = (jit.specialise(lib(), handle, lowered.launches, blob, recs)
                                            if jit.enabled() else ([], []))
+        # independent launches as concurrent graph nodes (schedule.py)
+        self.n_streams = int(os.environ.get("GFB_STREAMS", "4"))
+        if cuda_graph and self.n_streams > 1 and len(lowered.launches) > 1:
+            from . import schedule
+
+            st, off, deps = schedule.build(lowered, self.skipped, self.n_streams)
+            arr = lambda v: (C.c_uint32 * max(1, len(v)))(*v)
+            check(lib().gfb_exe_set_schedule(handle, self.n_streams, arr(st), arr(off), arr(deps)), "gfb_exe_set_schedule")
 
     def run(self, in_ptrs: list, out_ptrs: list, stream=None):
         ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
@@ -330,6 +339,11 @@ def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     # stores intermediates in the policy's order instead.
     channels_last = os.environ.get("GFB_CHANNELS_LAST", "1") == "1" or policy.conv_order == NHWC_ORDER
     lowered = lower(g, layouts, private=private, allreduce=roots, channels_last=channels_last)
+    if (not private and int(os.environ.get("GFB_STREAMS", "4")) > 1
+            and lowered.arena_bytes <= int(os.environ.get("GFB_PRIVATE_ARENA_MAX", 64 << 20))):
+        # small arenas: one range per tensor, so reuse adds no false ordering
+        # between launches that could run concurrently (schedule.py)
+        lowered = lower(g, layouts, private=True, allreduce=roots, channels_last=channels_last)
     return HostCompiled(g, layouts, plan, instructions, pool_refs, param_index, result_index,
                         param_sig, result_sig, lowered, roots)
 

@@ -1,0 +1,99 @@
+"""Multi-stream capture schedule for an executable's launch list.
+
+`call` replays one CUDA graph per step.  Captured from a single stream, the
+graph is a chain: every launch waits for the previous one.  Many launches of
+a training step are independent (a layer's weight gradient and its data
+gradient, bias sums, the optimizer updates), so the schedule computed here
+captures each launch on one of a few streams and makes it wait, by event,
+only for the earlier launches it conflicts with.  The graph then has those
+launches as concurrent nodes.
+
+Conflicts are decided on physical memory, not on tensor identity: the arena
+planner reuses an arena range once its tensor is dead *in launch order*, so
+two launches touching overlapping arena bytes with at least one write must
+stay ordered (read-after-write, write-after-read and write-after-write).
+Caller buffers and the constant pool are compared per slot.
+"""
+
+from __future__ import annotations
+
+from . import abi
+
+
+def _ranges(lowered, keys, write):
+    """(space, lo, hi, write) per tensor key; unknown keys conflict with everything."""
+    out = []
+    for k in keys:
+        b = lowered.buffers.get(k)
+        if b is None:
+            out.append(("*", 0, 1 << 62, write))
+            continue
+        root = b.base if b.base is not None else b
+        if root.splat is not None:
+            continue  # a scalar in the argument block: no memory
+        if root.slot == abi.SLOT_ARENA:
+            lo = lowered.arena_offsets.get(root.key, root.offset)
+            out.append((0, lo, lo + max(1, root.nbytes), write))
+        else:
+            out.append((root.slot, 0, 1 << 62, write))
+    return out
+
+
+def _conflict(a, b) -> bool:
+    for sa, la, ha, wa in a:
+        for sb, lb, hb, wb in b:
+            if (wa or wb) and (sa == sb or sa == "*" or sb == "*") and la < hb and lb < ha:
+                return True
+    return False
+
+
+def build(lowered, skipped=(), n_streams: int = 4):
+    """(stream_of, dep_offsets, deps) for gfb_exe_set_schedule.  `skipped`:
+    launches folded into the preceding merged kernel (their accesses belong
+    to it)."""
+    n = len(lowered.launches)
+    skipped = set(skipped)
+    acc = []
+    head = list(range(n))
+    for i, L in enumerate(lowered.launches):
+        acc.append(_ranges(lowered, L.reads, False) + _ranges(lowered, L.writes, True))
+        if i in skipped and i > 0:
+            head[i] = head[i - 1]
+    for i in range(n):  # a merged kernel does its members' work
+        if head[i] != i:
+            acc[head[i]] += acc[i]
+    deps = [[] for _ in range(n)]
+    live = [i for i in range(n) if head[i] == i]
+    for x, i in enumerate(live):
+        for j in live[:x]:
+            if _conflict(acc[i], acc[j]):
+                deps[i].append(j)
+    stream_of = [0] * n
+    tail = [-1] * n_streams
+    last_collective = None
+    for i in range(n):
+        if head[i] != i:
+            stream_of[i] = stream_of[head[i]]
+            deps[i] = [head[i]]
+            continue
+        if lowered.launches[i].kind == abi.K_ALLREDUCE:
+            # collectives stay on stream 0 in program order: every rank's graph
+            # then issues them in the same sequence
+            if last_collective is not None and last_collective not in deps[i]:
+                deps[i].append(last_collective)
+            last_collective = i
+            stream_of[i] = 0
+            tail[0] = i
+            continue
+        ends = [d for d in deps[i] if tail[stream_of[d]] == d]
+        if ends:
+            st = stream_of[max(ends)]  # continue the chain of the latest dependency
+        else:
+            st = min(range(n_streams), key=lambda k: tail[k])  # the least recently used stream
+        stream_of[i] = st
+        tail[st] = i
+    offsets, flat = [0], []
+    for d in deps:
+        flat += d
+        offsets.append(len(flat))
+    return stream_of, offsets, flat
