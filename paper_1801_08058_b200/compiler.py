@@ -53,6 +53,11 @@ from .memory import DEVICE_ALIGNMENT, align_up, plan_buffers
 from .layout import NHWC_ORDER, Layout
 
 NUM_SMS = 148
+# Grid cap of the ROW / COL elementwise launches, in blocks per SM.  Measured
+# on config B (scripts/b_sweep.cu): 16 blocks/SM (a grid-stride loop of ~3.5
+# row groups per block) 123.3 us, 32 -> 119.7, 55 (one row group per block)
+# 119.2; the blocks of the last wave are then short, so the tail is short too.
+EW_BLOCKS_PER_SM = int(os.environ.get("GFB_EW_BLOCKS_PER_SM", 64))
 HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER})
 INDEX_OPS = frozenset({OpKind.BROADCAST, OpKind.RESHAPE, OpKind.CONVERT_LAYOUT})
 MAX_STACK = 3
@@ -961,7 +966,7 @@ class Lowering:
         scalar = self._scalar_ok(prog, n_o, n_r, et)
         if scalar:
             prog.set_vector_width(1)
-        grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * 16))
+        grid = max(1, min((n_o + rpb - 1) // rpb, NUM_SMS * EW_BLOCKS_PER_SM))
         args = prog.args(mode=1, n_o=n_o, n_r=n_r, red_kind=red_kind, wpr=wpr)
         general_r = [l.digits for l in prog.leaf_specs if l.buf.splat is None and r_linear(l.digits) < 0]
         if len(general_r) >= 2 and len(set(map(tuple, general_r))) < len(general_r):
@@ -1024,7 +1029,7 @@ class Lowering:
             while split < 64 and ((vectors * split + 255) // 256) < 2 * NUM_SMS and n_r // (split * 2) >= 8:
                 split *= 2
         per_row = 256 // split
-        grid = max(1, min((vectors + per_row - 1) // per_row, NUM_SMS * 16))
+        grid = max(1, min((vectors + per_row - 1) // per_row, NUM_SMS * EW_BLOCKS_PER_SM))
         args = prog.args(mode=2, n_o=n_o, n_r=n_r, red_kind=red_kind, split=split)
         if red_kind == 0 and split == 1 and n_r == 1 and not scalar:
             ty = _transpose_order(prog, n_o, V)
