@@ -58,6 +58,9 @@ NUM_SMS = 148
 # row groups per block) 123.3 us, 32 -> 119.7, 55 (one row group per block)
 # 119.2; the blocks of the last wave are then short, so the tail is short too.
 EW_BLOCKS_PER_SM = int(os.environ.get("GFB_EW_BLOCKS_PER_SM", 64))
+# ROW launches add warps per row (up to 8) while the grid has fewer than this
+# many 8-warp blocks per SM.
+ROW_BLOCKS_PER_SM = int(os.environ.get("GFB_EW_ROW_BLOCKS_PER_SM", 32))
 HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER})
 INDEX_OPS = frozenset({OpKind.BROADCAST, OpKind.RESHAPE, OpKind.CONVERT_LAYOUT})
 MAX_STACK = 3
@@ -923,7 +926,7 @@ class Lowering:
         V = vec_width(et)
         staged = self._staged_ok(prog, n_o, n_r, et)
         wpr = 1
-        while not staged and wpr < 8 and n_o * wpr < 2 * NUM_SMS * 8 and n_r >= 32 * V * wpr * 2:
+        while not staged and wpr < 8 and n_o * wpr < ROW_BLOCKS_PER_SM * NUM_SMS * 8 and n_r >= 32 * V * wpr * 2:
             wpr *= 2
         rpb = 8 // wpr
         if staged:
