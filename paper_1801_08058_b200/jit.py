@@ -50,6 +50,8 @@ KINDS = {
     abi.K_EW_F64: ("double", 4, 4),
     abi.K_EW1_F32: ("float", 1, 4),
     abi.K_EW1_F64: ("double", 1, 4),
+    abi.K_EWS_F32: ("float", 8, 4),  # chunk-wise staged launches (mode 3, split 1) only
+    abi.K_EWS_F64: ("double", 4, 4),
 }
 OPTIONS = ["-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo"]
 ENTRY = b"gfb_jit_ew"
@@ -121,10 +123,16 @@ def _c_init(v) -> str:
     raise TypeError(f"cannot initialise from {type(v)}")
 
 
+def _mode_ok(args) -> bool:
+    """ROW (1), COL (2) and the chunk-wise staged mode (3 with split 1: few
+    long rows cut into chunks, one partial per (row, chunk))."""
+    return args.mode in (1, 2) or (args.mode == 3 and args.split == 1)
+
+
 def generate(kind: int, args: "abi.EwArgs", block: int = 256):
     """(CUDA C of one launch's specialised kernel, its dynamic shared memory
     bytes), or None when the generic kernel keeps the launch."""
-    if kind not in KINDS or args.mode not in (1, 2):
+    if kind not in KINDS or not _mode_ok(args):
         return None
     g = _Gen(kind, args, block)
     src = g.emit()
@@ -138,7 +146,7 @@ def generate_merged(members, block: int):
     path).  `members`: [(kind, args)].  Returns (source, smem) or None."""
     gens = []
     for kind, args in members:
-        if kind not in KINDS or args.mode not in (1, 2):
+        if kind not in KINDS or not _mode_ok(args):
             return None
         gens.append(_Gen(kind, args, block))
     src = _kernel_source(gens)
@@ -226,7 +234,7 @@ class _Gen:
         return f"t{self.n}"
 
     def _elem(self, k, v):
-        vaxis = self.a.mode == 1
+        vaxis = self.a.mode in (1, 3)
         o = "o" if vaxis else f"o + {v}u"
         r = f"r + {v}u" if vaxis else "r"
         return self._full_off(k, o, r)
@@ -325,7 +333,7 @@ class _Gen:
     def member(self, idx):
         """This launch as `namespace m<idx> { run(pa, dyn) }`."""
         a, V = self.a, self.V
-        row = a.mode == 1
+        row = a.mode in (1, 3)
         n_o, n_r = a.n_o, a.n_r
         L = [f"namespace m{idx} {{", f"typedef {self.t} T;", f"constexpr int V = {V};",
              "__device__ __forceinline__ void run(const gfb_ew_args& pa, unsigned char* dyn) {"]
@@ -354,7 +362,35 @@ class _Gen:
                 lines += ["if (nvalid == V) {", *body_full, "} else {", *body_part, "}"]
 
         ob = [f"const uint32_t ob{m} = {self._expr(self.maps[m][1], 'o', '0u', src=0)};" for m in range(len(self.maps))]
-        if row:
+        if a.mode == 3:
+            # chunk-wise (csrc/ew_vm.cu gfb_ew_staged_kernel, split == 1): a warp
+            # per (o, chunk) item of CH elements; partial -> red[o * nch + chunk]
+            ch = 32 * 2 * (16 // self.esize) * 2  # StagedCfg<T, 2>::CH
+            L += [
+                "const int lane = tid & 31, warp = tid >> 5;",
+                f"constexpr uint32_t CH = {ch}u, nr = {n_r}u, no = {n_o}u, nch = (nr + CH - 1) / CH;",
+                "const uint32_t items = no * nch, wpb = nthr >> 5;",
+                "for (uint32_t g = blockIdx.x * wpb + warp; g < items; g += gridDim.x * wpb) {",
+                "const uint32_t o = g / nch, c = g % nch, rend = min(nr, (c + 1u) * CH);",
+                f"T part = fold_init<T>({kind});",
+                *ob,
+                "for (uint32_t r = c * CH + lane * V; r < rend; r += 32u * V) {",
+                "const int nvalid = (int)min((uint32_t)V, nr - r);",
+            ]
+            if kind:
+                L.append("T acc[V];")
+            run(L)
+            if kind:
+                L.append(f"_Pragma(\"unroll\") for (int v = 0; v < V; ++v) if (v < nvalid) part = fold<T>({kind}, part, acc[v]);")
+            L.append("}")  # r loop
+            if kind:
+                L += [
+                    f"_Pragma(\"unroll\") for (int off = 16; off > 0; off >>= 1) part = fold<T>({kind}, part, __shfl_xor_sync(0xffffffffu, part, off));",
+                    "if (lane == 0) red[(size_t)o * nch + c] = part;",
+                ]
+            L.append("}")  # item loop
+            smem = 0
+        elif row:
             L += [
                 "const int lane = tid & 31, warp = tid >> 5;",
                 f"constexpr int wpr = {a.wpr};",
