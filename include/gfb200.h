@@ -21,9 +21,13 @@
  * `void*` (a cudaStream_t, NULL = the per-thread default stream).  The
  * caller owns input/output buffers ("results and parameters are
  * caller-allocated"); the library owns the arena, the constant pool, the
- * device pointer table and the captured CUDA graph.  Runs of one executable
- * are serialised by an internal mutex (the reference allows concurrent
- * calls on one Executable).
+ * device pointer table and the captured CUDA graph.  Concurrent runs of one
+ * executable are safe (the reference allows concurrent calls on one
+ * Executable): submission is serialised by an internal mutex,
+ * and on the device each run waits for the previous run's completion event
+ * before it rewrites the pointer table or touches the arena, whatever
+ * streams the two runs were issued on.  gfb_exe_destroy waits for the last
+ * run.
  */
 #ifndef GFB200_H
 #define GFB200_H
@@ -335,7 +339,7 @@ typedef struct {
     uint64_t buf;   /* GFB_REF of the contiguous gradient bucket */
     uint64_t count; /* elements */
     int32_t dtype;  /* 0 f32, 1 f64 */
-    int32_t pad;
+    int32_t op;     /* 0 sum (partial gradients), 1 max (a max-reduction over the sharded batch axis) */
 } gfb_allreduce_args;
 
 /* One kernel launch of the plan; its argument block is args[arg_offset, +arg_size). */

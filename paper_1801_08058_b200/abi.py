@@ -176,7 +176,7 @@ class ConvArgs(C.Structure):
 class AllReduceArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p), ("buf", C.c_uint64), ("count", C.c_uint64),
-        ("dtype", C.c_int32), ("pad", C.c_int32),
+        ("dtype", C.c_int32), ("op", C.c_int32),
     ]
 
 

@@ -227,6 +227,7 @@ class Buffer:
     base: object = None   # a strided view of this Buffer (shares its storage and final offset)
     elem_off: int = 0     # view origin, in elements from the base's origin
     subaxes: dict = None  # axis -> [(extent, stride), ...] outer to inner: a flattened axis stored permuted
+    bucket: object = None  # (gradient region, is_max) for a data-parallel partial root
 
     @property
     def nbytes(self) -> int:
@@ -616,11 +617,12 @@ class _Node:
 
 class Lowering:
     def __init__(self, g: Function, layouts: dict, private: bool = False, allreduce=frozenset(),
-                 channels_last: bool = False):
+                 channels_last: bool = False, allreduce_max=frozenset()):
         self.g = g
         self.layouts = layouts
         self.private = private
         self.allreduce = set(allreduce)  # data-parallel partial roots (dp.analyse)
+        self.allreduce_max = set(allreduce_max)  # the roots reduced with max (a max over the batch shard)
         self.order = [n for n in topological_order(g) if n in reachable_from_results(g)]
         self.topo = {n: i for i, n in enumerate(self.order)}
         self.nodes = {n: _Node(g.nodes[n], g) for n in self.order}
@@ -803,6 +805,8 @@ class Lowering:
                     strides = (d.shape[1], 1)
                 self.buf[n] = Buffer(self.new_key(), d.element_type, d.shape, strides, slot, subaxes=subaxes)
 
+        self._grad_regions = self._gradient_regions() if self.allreduce else []
+
         # merge rule: a materialised node consumed only by one Sum is that Sum's side output
         side_of = {}
         for n in self.order:
@@ -825,8 +829,9 @@ class Lowering:
                     self.emit_reduce(n, side_of.get(n))
                 else:
                     self.emit_map(n, groups.get(n, [n]))
-            if n in self.allreduce:
-                self.emit_allreduce(n)
+
+        if self.allreduce:
+            self._bucket_allreduces()
 
         # results that are parameters / constants / repeated: copy launches
         for j, (r, _) in enumerate(results):
@@ -843,15 +848,23 @@ class Lowering:
             for k in L.writes + L.reads:
                 lo, hi = live.get(k, (i, i))
                 live[k] = (min(lo, i), max(hi, i))
-        arena_bufs = {b.key: b for b in self.buf.values() if b.slot == abi.SLOT_ARENA}
+        arena_bufs = {b.key: b for b in self.buf.values() if b.slot == abi.SLOT_ARENA and b.base is None}
         items = {k: (b.nbytes, live.get(k, (0, 0))[0], live.get(k, (0, 0))[1]) for k, b in arena_bufs.items()}
+        for region, members in self._grad_regions:
+            # the gradient region lives from its first member's producer to its last reader
+            spans = [live[m.key] for m in members if m.key in live] or [(0, 0)]
+            arena_bufs[region.key] = region
+            items[region.key] = (region.nbytes, min(a for a, _ in spans), max(b for _, b in spans))
         plan = plan_buffers(items, private=self.private)
         for k, b in arena_bufs.items():
             b.offset = plan.offsets[k]
         for L in self.launches:
             L.finalize()
+        buffers = {b.key: b for b in self.buf.values()}
+        for region, _ in self._grad_regions:
+            buffers[region.key] = region
         return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
-                       {b.key: b for b in self.buf.values()}, arena_offsets=plan.offsets)
+                       buffers, arena_offsets=plan.offsets)
 
     def _flat_channel_last(self, n):
         """Sub-axis storage for a flattened pool-window matrix [k, M] under the
@@ -1345,19 +1358,103 @@ class Lowering:
         rec.finalize = prog.finalize_fn(args)
         self.launches.append(rec)
 
-    def emit_allreduce(self, n: int):
-        """In-place NCCL sum of a data-parallel partial root across ranks."""
-        b = self.buf.get(n)
-        if b is None or b.slot != abi.SLOT_ARENA:
-            raise UnsupportedOp(f"data parallel: partial root {n} is not materialised in the arena")
-        d = self.nodes[n].output
-        if d.element_type not in (ElementType.F32, ElementType.F64):
-            raise UnsupportedOp("data parallel all-reduce needs a float tensor")
-        args = abi.AllReduceArgs(count=element_count(d.shape), dtype=0 if d.element_type is ElementType.F32 else 1)
-        rec = LaunchRec(abi.K_ALLREDUCE, (1, 1, 1), (1, 1, 1), 0, args, [b.key], [b.key], f"allreduce#{n}")
-        rec.algo_bytes = b.nbytes
-        rec.finalize = _finalize_refs(args, {"buf": b})
-        self.launches.append(rec)
+    def _gradient_regions(self):
+        """Place the data-parallel partial roots contiguously, in production
+        order (for a training step: the loss, then the gradients in reverse
+        layer order), one arena region per (element type, reduction op).
+        Each root becomes a dense view into its region, so a run of
+        consecutive roots is one all-reduce bucket."""
+        groups: dict = {}
+        for n in self.order:
+            if n not in self.allreduce:
+                continue
+            b = self.buf.get(n)
+            if b is None or b.slot != abi.SLOT_ARENA or b.base is not None:
+                raise UnsupportedOp(f"data parallel: partial root {n} is not materialised in the arena")
+            if b.et not in (ElementType.F32, ElementType.F64):
+                raise UnsupportedOp("data parallel all-reduce needs a float tensor")
+            groups.setdefault((b.et, n in self.allreduce_max), []).append(n)
+        regions = []
+        for (et, is_max), ns in groups.items():
+            region = Buffer(self.new_key(), et, (0,), (1,), abi.SLOT_ARENA)
+            off, members = 0, []
+            for n in ns:
+                b = self.buf[n]
+                b.base, b.elem_off = region, off // et.byte_size
+                b.bucket = (region, is_max)
+                members.append(b)
+                off = align_up(off + b.nbytes, DEVICE_ALIGNMENT)
+            region.shape = (max(1, off // et.byte_size),)
+            regions.append((region, members))
+        return regions
+
+    def _bucket_allreduces(self):
+        """Insert the all-reduce launches over the gradient regions.
+
+        A bucket is a run of consecutive roots of one region; it is reduced
+        right after the launch that finishes its last member once it holds
+        GFB_BUCKET_MB (default 32) MiB, or earlier if a later launch reads
+        one of its members before that (the SGD update of that parameter).
+        Buckets are issued in the order their members were produced, so a
+        layer's gradients are summed while the earlier layers' backward
+        GEMMs still run (the schedule keeps collectives in program order on
+        stream 0; everything else may overlap them)."""
+        cap = int(float(os.environ.get("GFB_BUCKET_MB", "32")) * (1 << 20))
+        member_of = {}
+        for region, members in self._grad_regions:
+            for b in members:
+                member_of[b.key] = b
+        last_write = {}
+        for i, L in enumerate(self.launches):
+            for k in L.writes:
+                if k in member_of:
+                    last_write[k] = i
+        out = []
+        pending: list = []  # members fully produced, not yet reduced
+
+        def flush():
+            runs = []
+            for b in sorted(pending, key=lambda b: (id(b.bucket[0]), b.elem_off)):
+                if runs and runs[-1][-1].bucket[0] is b.bucket[0] and \
+                        align_up(runs[-1][-1].elem_off * b.et.byte_size + runs[-1][-1].nbytes, DEVICE_ALIGNMENT) \
+                        == b.elem_off * b.et.byte_size:
+                    runs[-1].append(b)
+                else:
+                    runs.append([b])
+            for run in runs:
+                out.append(self._allreduce_rec(run))
+            pending.clear()
+
+        for i, L in enumerate(self.launches):
+            if L.kind != abi.K_ALLREDUCE and any(k in member_of and last_write.get(k, -1) < i and
+                                                 member_of[k] in pending for k in L.reads):
+                flush()
+            out.append(L)
+            done = [member_of[k] for k, j in last_write.items() if j == i]
+            pending.extend(b for b in done if b not in pending)
+            if pending and sum(b.nbytes for b in pending) >= cap:
+                flush()
+        if pending:
+            flush()
+        self.launches = out
+
+    def _allreduce_rec(self, run):
+        """One in-place NCCL all-reduce over consecutive members of a region."""
+        region, is_max = run[0].bucket
+        et = run[0].et
+        first, last = run[0], run[-1]
+        count = last.elem_off + element_count(last.shape) - first.elem_off
+        args = abi.AllReduceArgs(count=count, dtype=0 if et is ElementType.F32 else 1, op=1 if is_max else 0)
+        keys = [b.key for b in run]
+        label = "allreduce#" + ",".join(str(n) for n in self._nodes_of(keys))
+        rec = LaunchRec(abi.K_ALLREDUCE, (1, 1, 1), (1, 1, 1), 0, args, keys, keys, label)
+        rec.algo_bytes = count * et.byte_size
+        rec.finalize = _finalize_refs(args, {"buf": first})
+        return rec
+
+    def _nodes_of(self, keys):
+        ks = set(keys)
+        return [n for n, b in self.buf.items() if b.key in ks]
 
     # -- heavy ops
     def operand(self, ref_node):
@@ -2451,7 +2548,8 @@ def _encode_leaf(L: abi.Leaf, s: LeafSpec):
         d.stride = stride
 
 
-def lower(g: Function, layouts: dict, private: bool = False, allreduce=frozenset(), channels_last: bool = False) -> Lowered:
-    low = Lowering(g, layouts, private, allreduce, channels_last).run()
+def lower(g: Function, layouts: dict, private: bool = False, allreduce=frozenset(), channels_last: bool = False,
+          allreduce_max=frozenset()) -> Lowered:
+    low = Lowering(g, layouts, private, allreduce, channels_last, allreduce_max).run()
     low.channels_last = channels_last
     return low

@@ -67,9 +67,14 @@ __device__ __forceinline__ T from_bits(uint64_t b) {
 // ---- V consecutive elements, one or two 128-bit (or one 64-bit) accesses
 template <typename T, int V>
 __device__ __forceinline__ void loadV(const T* p, T (&v)[V]) {
-    static_assert(V == 1 || V * sizeof(T) == 32 || V * sizeof(T) == 8, "vector width");
+    static_assert(V == 1 || V * sizeof(T) == 32 || V * sizeof(T) == 16 || V * sizeof(T) == 8, "vector width");
     if constexpr (V == 1) {
         v[0] = __ldg(p);
+    } else if constexpr (V * sizeof(T) == 16) {
+        int4 a = __ldg(reinterpret_cast<const int4*>(p));
+        const T* pa = reinterpret_cast<const T*>(&a);
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = pa[i];
     } else if constexpr (V * sizeof(T) == 32) {
         const int4* q = reinterpret_cast<const int4*>(p);
         int4 a = __ldg(q), b = __ldg(q + 1);
@@ -94,6 +99,11 @@ template <typename T, int V>
 __device__ __forceinline__ void loadV_plain(const T* p, T (&v)[V]) {
     if constexpr (V == 1) {
         v[0] = *p;
+    } else if constexpr (V * sizeof(T) == 16) {
+        int4 a = *reinterpret_cast<const int4*>(p);
+        const T* pa = reinterpret_cast<const T*>(&a);
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = pa[i];
     } else if constexpr (V * sizeof(T) == 32) {
         const int4* q = reinterpret_cast<const int4*>(p);
         int4 a = q[0], b = q[1];
@@ -116,6 +126,12 @@ template <typename T, int V>
 __device__ __forceinline__ void storeV(T* p, const T (&v)[V]) {
     if constexpr (V == 1) {
         *p = v[0];
+    } else if constexpr (V * sizeof(T) == 16) {
+        int4 a;
+        T* pa = reinterpret_cast<T*>(&a);
+#pragma unroll
+        for (int i = 0; i < V; ++i) pa[i] = v[i];
+        *reinterpret_cast<int4*>(p) = a;
     } else if constexpr (V * sizeof(T) == 32) {
         int4 a, b;
         T* pa = reinterpret_cast<T*>(&a);

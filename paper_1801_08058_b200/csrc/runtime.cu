@@ -105,6 +105,8 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommRegister)(ncclComm_t, void*, size_t, void**) = nullptr;  // NCCL >= 2.19, optional
+    ncclResult_t (*CommDeregister)(ncclComm_t, void*) = nullptr;
 };
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
@@ -127,6 +129,8 @@ int load_nccl() {
     g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
     g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    g_nccl.CommRegister = (decltype(g_nccl.CommRegister))dlsym(h, "ncclCommRegister");
+    g_nccl.CommDeregister = (decltype(g_nccl.CommDeregister))dlsym(h, "ncclCommDeregister");
     if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
         return fail(GFB_ERR_NCCL, "libnccl is missing required symbols");
     g_nccl.loaded = true;
@@ -153,6 +157,12 @@ struct gfb_exe {
     void** dtab = nullptr;  // device pointer table
     void** htab = nullptr;  // pinned staging copy of the table
     cudaEvent_t tab_done = nullptr;
+    // completion of the previous run: the next run (on any stream) waits for
+    // it before rewriting the pointer table or touching the arena, so runs
+    // of one executable never overlap on the device
+    cudaEvent_t run_done = nullptr;
+    bool ran = false;
+    void* nccl_reg = nullptr;  // ncclCommRegister handle of the arena (GFB_NCCL_REGISTER=1)
     uint32_t n_in = 0, n_out = 0, n_slots = 0;
     std::vector<gfb_launch> launches;
     std::vector<const void*> fns;
@@ -195,7 +205,7 @@ int launch_one(gfb_exe* e, size_t i, cudaStream_t s) {
         void* ptr = (char*)((a->buf >> 56) == GFB_SLOT_ARENA ? e->arena : nullptr) + (a->buf & ((1ull << 56) - 1));
         if ((a->buf >> 56) != GFB_SLOT_ARENA) return fail(GFB_ERR_INVALID, "all-reduce bucket must live in the arena");
         ncclResult_t r = g_nccl.AllReduce(ptr, ptr, (size_t)a->count, a->dtype == 0 ? 7 /*ncclFloat32*/ : 8 /*ncclFloat64*/,
-                                          0 /*ncclSum*/, e->comm->comm, s);
+                                          a->op == 1 ? 2 /*ncclMax*/ : 0 /*ncclSum*/, e->comm->comm, s);
         if (r != 0) return nccl_fail(r, "ncclAllReduce");
         return GFB_OK;
     }
@@ -244,12 +254,21 @@ int launch_all_streams(gfb_exe* e, cudaStream_t s0) {
 
 int upload_table(gfb_exe* e, void* const* inputs, void* const* outputs, cudaStream_t s) {
     CUDA_TRY(cudaEventSynchronize(e->tab_done));  // previous run consumed the staging copy
+    // the previous run may be in flight on another stream: its kernels still
+    // read the device table and the arena this run is about to reuse
+    if (e->ran) CUDA_TRY(cudaStreamWaitEvent(s, e->run_done, 0));
     e->htab[GFB_SLOT_ARENA] = e->arena;
     e->htab[GFB_SLOT_CONST] = e->consts;
     for (uint32_t i = 0; i < e->n_in; ++i) e->htab[GFB_SLOT_IO + i] = inputs[i];
     for (uint32_t j = 0; j < e->n_out; ++j) e->htab[GFB_SLOT_IO + e->n_in + j] = outputs[j];
     CUDA_TRY(cudaMemcpyAsync(e->dtab, e->htab, sizeof(void*) * e->n_slots, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaEventRecord(e->tab_done, s));
+    return GFB_OK;
+}
+
+int mark_done(gfb_exe* e, cudaStream_t s) {
+    CUDA_TRY(cudaEventRecord(e->run_done, s));
+    e->ran = true;
     return GFB_OK;
 }
 
@@ -266,7 +285,10 @@ void release_schedule(gfb_exe* e) {
 }
 
 void release(gfb_exe* e) {
+    if (e->ran && e->run_done) cudaEventSynchronize(e->run_done);
+    if (e->nccl_reg && e->comm && g_nccl.CommDeregister) g_nccl.CommDeregister(e->comm->comm, e->nccl_reg);
     release_schedule(e);
+    if (e->run_done) cudaEventDestroy(e->run_done);
     if (e->graph) cudaGraphExecDestroy(e->graph);
     if (e->capture_stream) cudaStreamDestroy(e->capture_stream);
     if (e->tab_done) cudaEventDestroy(e->tab_done);
@@ -330,6 +352,7 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
     if ((err = cudaMalloc(&e->dtab, sizeof(void*) * e->n_slots)) != cudaSuccess ||
         (err = cudaMallocHost(&e->htab, sizeof(void*) * e->n_slots)) != cudaSuccess ||
         (err = cudaEventCreateWithFlags(&e->tab_done, cudaEventDisableTiming)) != cudaSuccess ||
+        (err = cudaEventCreateWithFlags(&e->run_done, cudaEventDisableTiming)) != cudaSuccess ||
         (err = cudaStreamCreateWithFlags(&e->capture_stream, cudaStreamNonBlocking)) != cudaSuccess)
         return bail(fail(GFB_ERR_CUDA, std::string("executable setup: ") + cudaGetErrorString(err)));
     e->launches.assign(plan->launches, plan->launches + plan->n_launches);
@@ -413,6 +436,15 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
         err = cudaFuncSetAttribute(e->fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
         if (err != cudaSuccess) return bail(fail(GFB_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(err)));
     }
+    // Optional NCCL user-buffer registration of the arena (every all-reduce
+    // bucket lives there), so collectives can skip the internal staging copy.
+    if (e->comm && e->arena && g_nccl.CommRegister) {
+        const char* reg = getenv("GFB_NCCL_REGISTER");
+        if (reg && reg[0] == '1') {
+            ncclResult_t r = g_nccl.CommRegister(e->comm->comm, e->arena, plan->arena_bytes, &e->nccl_reg);
+            if (r != 0) return bail(nccl_fail(r, "ncclCommRegister"));
+        }
+    }
     *out = e;
     return GFB_OK;
 }
@@ -423,7 +455,10 @@ int gfb_exe_run(gfb_exe* e, void* const* inputs, void* const* outputs, void* str
     cudaStream_t s = stream ? (cudaStream_t)stream : cudaStreamPerThread;
     int rc = upload_table(e, inputs, outputs, s);
     if (rc != GFB_OK) return rc;
-    if (!e->use_graph) return launch_all(e, s);
+    if (!e->use_graph) {
+        rc = launch_all(e, s);
+        return rc != GFB_OK ? rc : mark_done(e, s);
+    }
     if (!e->graph) {
         // Capture on a private stream: nothing executes during capture, and
         // the instantiated graph is then launched on the caller's stream.
@@ -441,7 +476,7 @@ int gfb_exe_run(gfb_exe* e, void* const* inputs, void* const* outputs, void* str
         if (inst != cudaSuccess) return fail(GFB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(inst));
     }
     CUDA_TRY(cudaGraphLaunch(e->graph, s));
-    return GFB_OK;
+    return mark_done(e, s);
 }
 
 int gfb_exe_run_one(gfb_exe* e, uint32_t index, void* const* inputs, void* const* outputs, void* stream) {
@@ -450,7 +485,8 @@ int gfb_exe_run_one(gfb_exe* e, uint32_t index, void* const* inputs, void* const
     cudaStream_t s = stream ? (cudaStream_t)stream : cudaStreamPerThread;
     int rc = upload_table(e, inputs, outputs, s);
     if (rc != GFB_OK) return rc;
-    return launch_one(e, index, s);
+    rc = launch_one(e, index, s);
+    return rc != GFB_OK ? rc : mark_done(e, s);
 }
 
 int gfb_exe_num_launches(const gfb_exe* e) { return e ? (int)e->launches.size() : 0; }
@@ -518,8 +554,7 @@ int gfb_exe_set_kernel(gfb_exe* e, uint32_t index, const void* kernel, uint32_t 
 
 int gfb_exe_destroy(gfb_exe* e) {
     if (!e) return GFB_OK;
-    cudaStreamSynchronize(cudaStreamPerThread);
-    release(e);
+    release(e);  // waits for the last run, whatever stream it was launched on
     return GFB_OK;
 }
 

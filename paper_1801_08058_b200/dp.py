@@ -28,6 +28,9 @@ from .errors import UnsupportedOp
 from .ir import ELEMENTWISE_BINARY, ELEMENTWISE_UNARY, Function, OpKind, reachable_from_results, topological_order
 
 REPL, PART = "replicated", "partial"
+# per-rank max over the batch shard (a max-reduction along the sharded axis):
+# nothing is linear in it, so its first consumer needs the max across ranks
+PMAX = "partial_max"
 
 
 def sharded(axis: int):
@@ -42,6 +45,7 @@ class DataParallel:
     axis: int = 0
     world_size: int = 1
     allreduce: set = field(default_factory=set)  # filled by analyse()
+    allreduce_max: set = field(default_factory=set)  # the roots among them reduced with max, not sum
 
 
 def _reshape_axis(node, in_shape, axis: int):
@@ -92,6 +96,11 @@ def _propagate(g: Function, dp: DataParallel):
         if n in dp.allreduce:
             st[n] = REPL  # summed across ranks right after it is produced
             continue
+        pmax = [r for (r, _), s in zip(node.inputs, ins) if s == PMAX]
+        if pmax:
+            for r in pmax:
+                demand.append((n, r))
+            ins = [REPL if s == PMAX else s for s in ins]
         parts = [r for (r, _), s in zip(node.inputs, ins) if s == PART]
         shards = [s for s in ins if isinstance(s, tuple)]
 
@@ -148,7 +157,7 @@ def _propagate(g: Function, dp: DataParallel):
             axes = node.attrs["reduction_axes"]
             if isinstance(s, tuple):
                 if s[1] in axes:
-                    st[n] = PART
+                    st[n] = PMAX if node.attrs["reduction_kind"] == "max" else PART
                 else:
                     st[n] = sharded(s[1] - sum(1 for a in axes if a < s[1]))
             elif s == PART and node.attrs["reduction_kind"] == "max":
@@ -192,7 +201,7 @@ def _propagate(g: Function, dp: DataParallel):
         else:
             raise UnsupportedOp(f"data parallel: no rule for {op.wire_name}")
     for r, _ in g.results:
-        if st[r] == PART:
+        if st[r] in (PART, PMAX):
             demand.append((None, r))
     return st, demand
 
@@ -201,6 +210,8 @@ def _root_of(g: Function, st: dict, n: int):
     """Walk back through linear ops to the materialised node that created the partial."""
     node = g.nodes[n]
     op = node.op
+    if st[n] == PMAX:
+        return [n]
     if op in (OpKind.DOT, OpKind.CONV_BACKPROP_FILTER):
         ins = [st[r] for r, _ in node.inputs]
         if PART not in ins:
@@ -217,11 +228,15 @@ def _root_of(g: Function, st: dict, n: int):
 def analyse(g: Function, dp: DataParallel) -> set:
     """Fill `dp.allreduce` with the partial roots that must be summed."""
     dp.allreduce = set()
+    dp.allreduce_max = set()
     for _ in range(len(g.nodes) + 1):
         st, demand = _propagate(g, dp)
         if not demand:
             dp.states = st
             return dp.allreduce
         for _, r in demand:
-            dp.allreduce.update(_root_of(g, st, r))
+            for root in _root_of(g, st, r):
+                dp.allreduce.add(root)
+                if st[root] == PMAX:
+                    dp.allreduce_max.add(root)
     raise UnsupportedOp("data parallel analysis did not converge")

@@ -187,6 +187,11 @@ class _Gen:
 
     def __init__(self, kind, a, block):
         self.t, self.V, self.minb = KINDS[kind]
+        if a.mode == 3:
+            # the chunk-wise staged kernel hands each lane 16-byte pieces
+            # (csrc/ew_vm.cu sidx): generate over 16-byte vectors so the
+            # lane-to-element map, and with it the fold order, is the same
+            self.V //= 2
         self.a, self.block = a, block
         self.nl = a.nleaves
         self.leaves = [a.leaves[k] for k in range(self.nl)]
@@ -365,6 +370,9 @@ class _Gen:
         if a.mode == 3:
             # chunk-wise (csrc/ew_vm.cu gfb_ew_staged_kernel, split == 1): a warp
             # per (o, chunk) item of CH elements; partial -> red[o * nch + chunk]
+            # V here is one 16-byte piece (HV); the lane's pieces of a chunk are
+            # (u, h) = 0..3 at chunk + (2u + h) * 32 * HV + lane * HV, folded in
+            # (u, h, j) order exactly like the VM's sidx(u, h, lane, j)
             ch = 32 * 2 * (16 // self.esize) * 2  # StagedCfg<T, 2>::CH
             L += [
                 "const int lane = tid & 31, warp = tid >> 5;",
@@ -374,7 +382,9 @@ class _Gen:
                 "const uint32_t o = g / nch, c = g % nch, rend = min(nr, (c + 1u) * CH);",
                 f"T part = fold_init<T>({kind});",
                 *ob,
-                "for (uint32_t r = c * CH + lane * V; r < rend; r += 32u * V) {",
+                "_Pragma(\"unroll\") for (uint32_t piece = 0; piece < 4u; ++piece) {",
+                "const uint32_t r = c * CH + piece * 32u * V + lane * V;",
+                "if (r >= rend) continue;",
                 "const int nvalid = (int)min((uint32_t)V, nr - r);",
             ]
             if kind:

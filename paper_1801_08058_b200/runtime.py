@@ -338,12 +338,16 @@ def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     # kernels then gather 16-byte runs of channels.  GFB_CHANNELS_LAST=0
     # stores intermediates in the policy's order instead.
     channels_last = os.environ.get("GFB_CHANNELS_LAST", "1") == "1" or policy.conv_order == NHWC_ORDER
-    lowered = lower(g, layouts, private=private, allreduce=roots, channels_last=channels_last)
-    if (not private and int(os.environ.get("GFB_STREAMS", "4")) > 1
-            and lowered.arena_bytes <= int(os.environ.get("GFB_PRIVATE_ARENA_MAX", 64 << 20))):
+    rmax = frozenset(getattr(data_parallel, "allreduce_max", ()) or ())
+    lowered = lower(g, layouts, private=private, allreduce=roots, channels_last=channels_last, allreduce_max=rmax)
+    cap = int(os.environ.get("GFB_PRIVATE_ARENA_MAX", 64 << 20))
+    if not private and int(os.environ.get("GFB_STREAMS", "4")) > 1 and lowered.arena_bytes <= cap:
         # small arenas: one range per tensor, so reuse adds no false ordering
-        # between launches that could run concurrently (schedule.py)
-        lowered = lower(g, layouts, private=True, allreduce=roots, channels_last=channels_last)
+        # between launches that could run concurrently (schedule.py) -- kept
+        # only if the no-reuse plan itself stays within the cap
+        private_plan = lower(g, layouts, private=True, allreduce=roots, channels_last=channels_last, allreduce_max=rmax)
+        if private_plan.arena_bytes <= cap:
+            lowered = private_plan
     return HostCompiled(g, layouts, plan, instructions, pool_refs, param_index, result_index,
                         param_sig, result_sig, lowered, roots)
 

@@ -31,6 +31,11 @@ def _ranges(lowered, keys, write):
         root = b.base if b.base is not None else b
         if root.splat is not None:
             continue  # a scalar in the argument block: no memory
+        if getattr(b, "bucket", None) is not None:
+            # a partial root inside the gradient region: exactly its own bytes
+            lo = lowered.arena_offsets.get(root.key, root.offset) + b.elem_off * b.et.byte_size
+            out.append((0, lo, lo + max(1, b.nbytes), write))
+            continue
         if root.slot == abi.SLOT_ARENA:
             lo = lowered.arena_offsets.get(root.key, root.offset)
             out.append((0, lo, lo + max(1, root.nbytes), write))

@@ -538,11 +538,11 @@ def execute_ranks(lowered, inputs_per_rank: list, out_specs: list, allreduce=Non
         if L.kind == abi.K_ALLREDUCE:
             views = [allreduce_view(m, L.args) for m in mems]
             if allreduce is not None:
-                allreduce(views)
+                allreduce(views, L.args.op)
             else:
                 total = views[0].copy()
                 for v in views[1:]:
-                    total = total + v
+                    total = np.maximum(total, v) if L.args.op == 1 else total + v
                 for v in views:
                     v[:] = total
             continue

@@ -14,6 +14,7 @@ from hostcompile import host_compile
 from oracle import interp
 
 import paper_1801_08058_b200 as gf
+from paper_1801_08058_b200 import abi
 from paper_1801_08058_b200 import workloads as W
 from paper_1801_08058_b200.dp import DataParallel
 
@@ -56,7 +57,60 @@ def test_partial_roots(kind):
         assert ops == ["Dot", "Dot", "Sum", "Sum", "Sum"]  # dW1, dW2, db1, db2, loss
     else:
         assert ops == ["ConvBackpropFilter", "ConvBackpropFilter", "Dot", "Sum"]
-    assert sum(1 for L in h.lowered.launches if L.label.startswith("allreduce")) == len(h.allreduce)
+    # the roots share one contiguous gradient region; buckets cover each root exactly once
+    ar = [L for L in h.lowered.launches if L.kind == abi.K_ALLREDUCE]
+    covered = [k for L in ar for k in L.reads]
+    assert len(covered) == len(set(covered)) == len(h.allreduce)
+    assert 1 <= len(ar) <= len(h.allreduce)
+
+
+def test_small_roots_share_one_bucket():
+    """A, C-sized steps: the loss sum is reduced where the forward divides it;
+    the four gradients fit one 32 MiB bucket -> one all-reduce, issued after
+    the last gradient and before the first SGD update reads one."""
+    loc, h, _, _ = _dp_case("mlp", 2)
+    launches = h.lowered.launches
+    ar = [i for i, L in enumerate(launches) if L.kind == abi.K_ALLREDUCE]
+    assert len(ar) == 2 and len(launches[ar[0]].reads) == 1 and len(launches[ar[1]].reads) == 4
+    a = launches[ar[1]].args
+    assert a.op == 0 and a.count >= sum(h.graph.nodes[r].output.element_count for r in h.allreduce) - 1
+    first_sgd = min(i for i, L in enumerate(launches) if "Subtract" in L.label)
+    assert ar[1] < first_sgd
+
+
+def test_bucket_cap_splits_and_orders(monkeypatch):
+    monkeypatch.setenv("GFB_BUCKET_MB", "0")  # every root its own bucket, reduced right after it lands
+    loc, h, arrays, want = _dp_case("mlp", 2)
+    ar = [L for L in h.lowered.launches if L.kind == abi.K_ALLREDUCE]
+    assert len(ar) == len(h.allreduce)
+    outs = plan_emulator.execute_ranks(h.lowered, _split_inputs(loc, arrays, 2),
+                                       [(d.element_type.numpy_dtype, d.element_count) for d, _ in h.result_signature])
+    for o, w in zip(outs[0], want):
+        assert G.normwise(o, w.reshape(-1)) <= 1e-5
+
+
+def test_max_over_batch_is_a_max_allreduce():
+    """A max-reduction over the sharded axis is reduced with ncclMax, not summed."""
+    def build(batch):
+        fn = gf.Function("maxbatch")
+        x = fn.add_parameter(gf.ElementType.F32, (batch, 5))
+        w = fn.add_parameter(gf.ElementType.F32, (5,))
+        m = fn.add_node(gf.OpKind.SUM, [x], {"reduction_axes": (0,), "reduction_kind": "max"})
+        fn.set_results([fn.add_node(gf.OpKind.MULTIPLY, [m, w])])
+        return fn, x
+
+    fn, _ = build(8)
+    loc, x = build(4)
+    dp = DataParallel([x], world_size=2)
+    h = host_compile(loc, data_parallel=dp)
+    ar = [L for L in h.lowered.launches if L.kind == abi.K_ALLREDUCE]
+    assert len(ar) == 1 and ar[0].args.op == 1
+    rng = np.random.default_rng(0)
+    xs, ws = rng.uniform(-1, 1, (8, 5)).astype(np.float32), rng.uniform(-1, 1, 5).astype(np.float32)
+    want = interp.run_function(fn, [xs, ws])[0]
+    outs = plan_emulator.execute_ranks(h.lowered, [[xs[:4], ws], [xs[4:], ws]], [(np.float32, 5)])
+    for r in range(2):
+        assert G.same_bits(outs[r][0], want.reshape(-1))
 
 
 @pytest.mark.parametrize("kind,world", [("mlp", 2), ("mlp", 4), ("cnn", 2)])
@@ -82,9 +136,9 @@ def _gloo_worker(rank, world, port, q):
         loc, h, arrays, want = _dp_case("mlp", world)
         specs = [(d.element_type.numpy_dtype, d.element_count) for d, _ in h.result_signature]
 
-        def allreduce(views):
+        def allreduce(views, op=0):
             t = torch.from_numpy(views[0])
-            dist.all_reduce(t)  # the real collective, over processes
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)  # the real collective
 
         mine = _split_inputs(loc, arrays, world)[rank]
         outs = plan_emulator.execute_ranks(h.lowered, [mine], specs, allreduce=allreduce)[0]
