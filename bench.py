@@ -1,21 +1,25 @@
 """Benchmark driver (one JSON line on rank 0).
 
-Default workload = BASELINE.json configs[1] (config B): the fused
-elementwise / Broadcast / Sum chain over 64 Mi-element fp32 tensors,
-`t3 = Relu(a + Broadcast(c)) * b`, results t3 and its row sums, executed
-through `compile_function` / the C ABI as ONE fused launch per step.
-Metric: fused-op HBM GB/s = algorithmic bytes per step (SURVEY.md §8(d):
-805,572,608 B) / step time.  Inputs (805 MB) exceed the 126 MB L2, so no
-flush is needed between steps.
+Headline (BASELINE.json metric "training-step samples/sec per graph ...
+at 1/2/4/8 B200"): config E, the wide-MLP (4096 x 8 layers) training step
+-- forward, autodiff backward and SGD as ONE Function -- at global batch
+65536, batch-sharded over the N GPUs (strong scaling) with the partial
+gradients summed by NCCL all-reduces captured inside the step's CUDA graph.
+Metric: samples/s = 65536 / step time (max over ranks).  Inputs (x alone is
+1 GiB at N=1) exceed the 126 MB L2, so no flush is needed between steps.
+
+The same line carries config B (BASELINE.json's "fused-op HBM GB/s": the
+fused Relu(a + Broadcast(c)) * b + row Sum chain over 64 Mi fp32) as the
+`secondary` block, with its own roofline.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload B|A]
+                  [--workload E|B|A|C|D|G|H]
 
-N > 1 (torchrun): config B shards by rows with no collective, each rank
-processing its own 64 Mi-element chain (weak scaling); value = all ranks'
-bytes / max-over-ranks time.  `--impl reference` times the reference
-semantics on the host CPU (the C oracle port, all host threads) on the same
-config; under torchrun only rank 0 runs it.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU, rendezvous on 127.0.0.1).  `--impl reference`
+times the reference semantics on the host CPU (the C oracle port, all host
+threads) on the same workload and metric, at a bounded sample batch; under
+torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -142,14 +146,170 @@ def dist_setup():
     return ws, rank, local
 
 
-def cpu_reference(rows, cols, steps, warmup, budget_s=120.0):
-    """Reference semantics on the host: the oracle (C restatement of the
-    reference kernels) over the fused chain, all host threads."""
+def maybe_relaunch(args):
+    """`--gpus N` outside torchrun: re-exec this script under
+    torch.distributed.run with N local ranks (rendezvous on 127.0.0.1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def tf32_peak():
+    """Measured tcgen05 kind::tf32 dense TFLOP/s (scripts/mma_probe.cu on a
+    B200 of this pool, profiles/tf32_peak.json), else the nominal 1,100."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "tf32_peak.json")) as fh:
+            p = json.load(fh)
+        return float(p["tf32_dense_tflops"]), float(p.get("tf32_dense_tflops_sustained", p["tf32_dense_tflops"])), \
+            "measured (profiles/tf32_peak.json, scripts/mma_probe.cu)"
+    except Exception:
+        return 1100.0, 1100.0, "nominal (no profiles/tf32_peak.json)"
+
+
+def _traffic(workload):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(workload)
+    except Exception:
+        return None
+
+
+E_DESC = ("E: wide MLP 4096 x 8 layers (+bias, Relu), softmax cross-entropy loss, fwd + autodiff bwd + SGD "
+          "as one Function, global batch 65536")
+
+
+def step_config(workload, ws, batch=None):
+    """The `config` dict of a training-step line (identical in both arms)."""
+    g = {"A": 128, "C": 256, "D": 128 * ws, "E": 65536}[workload] if batch is None else batch
+    desc = {"A": "A: MLP 784-512-10", "C": "C: CNN 32x32x3, conv 3->16->32, maxpool, fc 8192->10",
+            "D": "D: ResNet-18-style 224x224, NHWC layout assignment", "E": E_DESC}[workload]
+    return {"workload": desc, "global_batch": g, "batch_per_gpu": g // ws, "parallelism": f"dp{ws}",
+            "scaling": "weak" if workload == "D" else "strong",
+            "l2": "per-step inputs exceed the 126 MB L2 (E: x alone is 1 GiB per GPU at N=1); no flush needed"
+            if workload in ("D", "E") else "small step: inputs L2-resident between steps (latency-bound config)"}
+
+
+def _step_for(workload, batch=None, ws=1):
+    """(step graph, per-GPU batch); `batch` is the GLOBAL batch."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import workloads as W
+
+    g = step_config(workload, ws, batch)["global_batch"]
+    if workload == "A":
+        return W.mlp_step(gf, batch=g // ws, loss_batch=g), g // ws
+    if workload == "C":
+        return W.cnn_step(gf, batch=g // ws, loss_batch=g), g // ws
+    if workload == "D":
+        return W.resnet_step(gf, batch=g // ws, loss_batch=g), g // ws
+    if workload == "E":
+        return W.wide_mlp_step(gf, batch=g // ws, loss_batch=g), g // ws
+    raise ValueError(workload)
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port of the reference interpreter
+
+
+def _oracle_step_seconds(workload, batch, threads, global_batch):
     import paper_1801_08058_b200 as gf
     from oracle import interp
     from paper_1801_08058_b200 import workloads as W
 
+    interp.set_threads(threads)
+    if workload == "E":
+        step = W.wide_mlp_step(gf, batch=batch, loss_batch=global_batch)
+    else:
+        step, _ = _step_for(workload, batch, 1)
+    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=0, x_range=W.x_range_of(workload))
+    t0 = time.perf_counter()
+    interp.run_function(step.fn, arrays)
+    return time.perf_counter() - t0
+
+
+def cpu_step_sample(workload, per_step_budget, threads, global_batch):
+    """Largest power-of-two sample batch whose oracle step fits the budget:
+    two probes give the fixed cost (SGD over every parameter, which does not
+    shrink with the batch) and the per-sample cost."""
+    t16 = _oracle_step_seconds(workload, 16, threads, global_batch)
+    t64 = _oracle_step_seconds(workload, 64, threads, global_batch)
+    per = max(1e-6, (t64 - t16) / 48.0)
+    fixed = max(0.0, t16 - 16 * per)
+    b = 16
+    while b * 2 <= min(global_batch, 512) and fixed + 2 * b * per <= per_step_budget:
+        b *= 2
+    return b
+
+
+def reference_arm(args, ws):
+    """The reference interpreter's semantics timed on the host cores (the C
+    oracle port, all threads), on our arm's workload, metric and config."""
+    from oracle import interp
+
     threads = interp.max_threads()
+    wl = args.workload
+    if wl == "B":
+        value, _, sample = cpu_reference_chain(ROWS, COLS, args.steps, min(args.warmup, 1), threads)
+        line = {"impl": "reference", "metric": CHAIN_METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": chain_config(ws)}
+        unit = "GB/s"
+    else:
+        cfg = step_config(wl, ws, args.batch)
+        g = cfg["global_batch"]
+        budget = float(os.environ.get("GFB_REF_BUDGET_S", 120.0)) / max(1, args.steps + 1)
+        b = cpu_step_sample(wl, budget, threads, g) if wl == "E" else min(g, 2)
+        _oracle_step_seconds(wl, b, threads, g)  # warm-up
+        times = [_oracle_step_seconds(wl, b, threads, g) for _ in range(args.steps)]
+        t = float(np.mean(times))
+        value = b / t
+        sample = f"oracle step at batch {b} (of {g}), loss divided by {g}, {args.steps} steps, mean {t:.2f} s/step"
+        line = {"impl": "reference", "metric": step_metric(wl), "value": value, "unit": "samples/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg}
+        unit = "samples/s"
+    line["cpu_baseline"] = {"value": value, "unit": unit, "cores": threads, "kind": "port", "sample": sample,
+                            "cpu": _cpu_model()}
+    line["e2e"] = {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    return line
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+CHAIN_METRIC = "fused-op HBM GB/s (config B: Relu(a+Broadcast(c))*b + row Sum, 64Mi fp32)"
+
+
+def chain_config(ws):
+    return {"workload": "B: fused_chain rows=65536 cols=1024 per GPU",
+            "l2": "inputs 805 MB > 126 MB L2, no flush needed", "parallelism": f"replicas x{ws} (row shards, no collective)"}
+
+
+def step_metric(workload):
+    return f"training-step samples/sec per graph (config {step_config(workload, 1)['workload'].split(':')[0]})"
+
+
+def cpu_reference_chain(rows, cols, steps, warmup, threads, budget_s=120.0):
+    """Config B on the oracle (C restatement of the reference kernels)."""
+    import paper_1801_08058_b200 as gf
+    from oracle import interp
+    from paper_1801_08058_b200 import workloads as W
+
     interp.set_threads(threads)
     sample_rows = rows
 
@@ -171,18 +331,78 @@ def cpu_reference(rows, cols, steps, warmup, budget_s=120.0):
     return chain_bytes(sample_rows, cols) / t / 1e9, threads, f"config B sample [{sample_rows},{cols}] per step, {steps} steps"
 
 
-def bench_chain(args, ws, rank, local):
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def _barrier(ws):
+    import torch
+
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(x, ws):
+    import torch
+
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _own_launches(exe) -> int:
+    """Kernels of ours one run launches (NCCL's all-reduce kernels excluded)."""
+    from paper_1801_08058_b200 import abi
+
+    return exe.num_launches - sum(1 for L in exe.lowered.launches if L.kind == abi.K_ALLREDUCE)
+
+
+def _time_launch(exe, idx, dev_in, outs, stream, reps):
+    """Average duration of launch `idx` alone, CUDA events on its stream."""
+    import torch
+
+    prog = exe.program()
+    pin = [t.data_ptr() for t in dev_in]
+    pout = [t.data_ptr() for t in outs]
+    for _ in range(2):
+        prog.run_one(idx, pin, pout, stream.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        prog.run_one(idx, pin, pout, stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def launch_times(exe, dev_in, outs, stream, reps=3, to_stderr=True):
+    """Each launch alone (CUDA events on the launch stream); worst first."""
+    prog = exe.program()
+    rows = []
+    for i, L in enumerate(exe.lowered.launches):
+        rows.append((_time_launch(exe, i, dev_in, outs, stream, reps), i, L))
+    total = sum(r[0] for r in rows)
+    if to_stderr:
+        sys.stderr.write(f"# per-launch times (ms), total {total:.3f}\n")
+        jitted = set(getattr(prog, "jit_launches", ()))
+        merged = set(getattr(prog, "skipped", ()))
+        for t, i, L in sorted(rows, key=lambda r: -r[0]):
+            gbs = L.algo_bytes / (t * 1e-3) / 1e9 if t else 0
+            tfs = L.flops / (t * 1e-3) / 1e12 if t else 0
+            label = L.label + (":jit" if i in jitted else "") + (":merged-above" if i in merged else "")
+            sys.stderr.write(f"{t:9.3f} {100 * t / total:5.1f}% #{i:3d} {label:28s} grid={L.grid} {gbs:8.1f} GB/s {tfs:7.1f} TF/s\n")
+    return rows, total
+
+
+def bench_chain(args, ws, rank, local, e2e=True):
     import torch
 
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import workloads as W
     from paper_1801_08058_b200.runtime import pinned_tensor
 
-    torch.cuda.set_device(local)
-    if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fn = W.fused_chain(gf, rows=ROWS, cols=COLS)
     exe = gf.compile_function(fn)
     arrays = W.chain_inputs(ROWS, COLS, seed=1 + rank)
@@ -191,140 +411,178 @@ def bench_chain(args, ws, rank, local):
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     nbytes = chain_bytes(ROWS, COLS)
-    launches_per_step = exe.num_launches
-
-    def barrier():
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
+    steps = args.steps if args.workload == "B" else max(20, min(args.steps, 200))
 
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
             exe.run_device(dev_in, outs, stream=sh)
-        barrier()
+        _barrier(ws)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(steps):
+            exe.run_device(dev_in, outs, stream=sh)
+        t1.record(stream)
+        _barrier(ws)
+    ms = _max_over_ranks(t0.elapsed_time(t1) / steps, ws)
+    dom = max(range(len(exe.lowered.launches)), key=lambda i: exe.lowered.launches[i].algo_bytes)
+    kernel_ms = _time_launch(exe, dom, dev_in, outs, stream, max(10, steps))
+    hbm, _, peak_src = peaks()
+    achieved = nbytes / (kernel_ms * 1e-3) / 1e9
+    prog = exe.program()
+    line = {
+        "metric": CHAIN_METRIC, "value": ws * nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": ws,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (numpy PCG64 seeded U(-1,1))",
+        "config": dict(chain_config(ws), bytes_per_step_per_gpu=nbytes),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": _traffic("B"), "kernel": exe.lowered.launches[dom].label + (":jit" if dom in prog.jit_launches else ""),
+                     "kernel_ms": kernel_ms, "algorithmic_bytes": nbytes,
+                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
+        "gpu_launches": _own_launches(exe) * steps, "clocks": clk.summary(),
+    }
+    if e2e:
+        host_in = []
+        for a in arrays:
+            t = pinned_tensor(gf.ElementType.F32, a.shape)
+            t.buffer[:] = a.reshape(-1)
+            host_in.append(t)
+        host_out = [pinned_tensor(d.element_type, d.shape) for d, _ in exe.result_signature]
+        n = max(3, min(20, steps))
+
+        def timed(call):
+            for _ in range(2):
+                call()
+            _barrier(ws)
+            e0 = time.perf_counter()
+            for _ in range(n):
+                call()
+            return _max_over_ranks((time.perf_counter() - e0) / n, ws)
+
+        call_s = timed(lambda: gf.call(exe, host_in, out=host_out))
+        chunks = int(os.environ.get("GFB_BENCH_CHUNKS", 16))
+        e2e_s = timed(lambda: gf.call_streamed(exe, host_in, host_out, chunks=chunks))
+        line["e2e"] = {"value": ws * nbytes / e2e_s / 1e9, "unit": "GB/s",
+                       "h2d_bytes_per_step": sum(a.nbytes for a in arrays),
+                       "d2h_bytes_per_step": sum(t.buffer.nbytes for t in host_out), "ms_per_step": e2e_s * 1e3,
+                       "api": f"paper_1801_08058_b200.call_streamed(exe, pinned host inputs, pinned host results, chunks={chunks})",
+                       "call_value": ws * nbytes / call_s / 1e9, "call_ms_per_step": call_s * 1e3,
+                       "call_api": "paper_1801_08058_b200.call(exe, pinned host tensors, out=pinned host tensors)"}
+    return line
+
+
+def bench_step(args, ws, rank, local):
+    """Training step (fwd + autodiff bwd + SGD as one Function), samples/s.
+
+    At N > 1 the global batch is sharded over the ranks: each rank runs the
+    graph specialised to batch/N with the loss still divided by the global
+    batch, and the partial gradients are summed by NCCL all-reduces captured
+    inside the step's CUDA graph (dp.py; gradient buckets in compiler.py)."""
+    import torch
+
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import workloads as W
+    from paper_1801_08058_b200.runtime import pinned_tensor
+
+    wl = args.workload
+    cfg = step_config(wl, ws, args.batch)
+    step, batch = _step_for(wl, args.batch, ws)
+    t_compile = time.perf_counter()
+    dp = None
+    if ws > 1 or args.dp:
+        names = step.param_names
+        dp = gf.DataParallel([step.fn.parameters[names.index("x")], step.fn.parameters[names.index("t")]], world_size=ws)
+    exe = gf.compile_function(step.fn, data_parallel=dp, conv_layout="nhwc" if wl == "D" else "identity")
+    t_compile = time.perf_counter() - t_compile
+    shapes = W.parameter_shapes(step)
+    arrays = W.step_inputs(step, shapes, seed=rank, x_range=W.x_range_of(wl))
+    dev_in = [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for a in arrays]
+    outs = exe.allocate_outputs()
+    stream = torch.cuda.current_stream()
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            exe.run_device(dev_in, outs, stream=stream.cuda_stream)
+        _barrier(ws)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            exe.run_device(dev_in, outs, stream=sh)
+            exe.run_device(dev_in, outs, stream=stream.cuda_stream)
         t1.record(stream)
-        barrier()
-        ms = t0.elapsed_time(t1) / args.steps
-        # dominant kernel alone, same stream, for the roofline
-        dom = max(range(launches_per_step), key=lambda i: exe.lowered.launches[i].algo_bytes)
-        prog = exe.program()
-        ptr_in = [t.data_ptr() for t in dev_in]
-        ptr_out = [t.data_ptr() for t in outs]
-        for _ in range(3):
-            prog.run_one(dom, ptr_in, ptr_out, sh)
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k0.record(stream)
-        kreps = max(10, args.steps)
-        for _ in range(kreps):
-            prog.run_one(dom, ptr_in, ptr_out, sh)
-        k1.record(stream)
-        torch.cuda.synchronize()
-        kernel_ms = k0.elapsed_time(k1) / kreps
-    ms_t = torch.tensor([ms], device="cuda")
-    if ws > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(ms_t.item())
+        _barrier(ws)
+    ms = _max_over_ranks(t0.elapsed_time(t1) / args.steps, ws)
+    gbatch = cfg["global_batch"]
+    flops = sum(L.flops for L in exe.lowered.launches)
+
+    # dominant kernel (the largest-flop launch: a tcgen05 GEMM / conv) alone,
+    # same stream; and every launch alone for its share of the step
+    rows, total = launch_times(exe, dev_in, outs, stream, reps=2, to_stderr=args.launch_times)
+    dom = max(range(len(exe.lowered.launches)), key=lambda i: exe.lowered.launches[i].flops)
+    Ld = exe.lowered.launches[dom]
+    kernel_ms = _time_launch(exe, dom, dev_in, outs, stream, 5 if wl in ("D", "E") else 50)
+    tf32, tf32_sus, tf_src = tf32_peak()
+    useful_peak = tf32_sus / 3.0  # 3xTF32: three kind::tf32 MMAs per useful product
+    achieved = Ld.flops / (kernel_ms * 1e-3) / 1e12
+    gemm_ms = sum(t for t, i, L in rows if L.flops)
+    line = {
+        "metric": step_metric(wl), "value": gbatch / (ms * 1e-3), "unit": "samples/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (numpy PCG64 seeded; random-init weights of the config's architecture)",
+        "config": cfg,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
+                     "frac": achieved / useful_peak, "traffic": _traffic(wl),
+                     "kernel": Ld.label, "kernel_ms": kernel_ms, "algorithmic_flops": Ld.flops,
+                     "step_share": kernel_ms / total if total else None,
+                     "peak_source": f"3xTF32 useful ceiling = kind::tf32 dense {tf32_sus:.0f} TFLOP/s / 3, {tf_src}",
+                     "tensor_pipe_frac": 3 * achieved / tf32_sus,
+                     "frac_of_measured_bf16": achieved / peaks()[1]},
+        "step_detail": {"launches": exe.num_launches, "allreduces": sum(1 for L in exe.lowered.launches if L.label.startswith("allreduce")),
+                        "flops_per_step_per_gpu": flops, "achieved_tflops_step": ws * flops / (ms * 1e-3) / 1e12,
+                        "gemm_launch_ms_sum": gemm_ms, "launch_ms_sum": total,
+                        "arena_bytes": exe.lowered.arena_bytes, "compile_s": t_compile},
+        "gpu_launches": _own_launches(exe) * args.steps, "clocks": clk.summary(),
+    }
 
     # end to end through the public API: pinned host inputs -> call() -> pinned host results
     host_in = []
     for a in arrays:
         t = pinned_tensor(gf.ElementType.F32, a.shape)
-        t.buffer[:] = a.reshape(-1)
+        t.buffer[:] = np.ascontiguousarray(a).reshape(-1)
         host_in.append(t)
     host_out = [pinned_tensor(d.element_type, d.shape) for d, _ in exe.result_signature]
-    e2e_steps = max(3, min(20, args.steps))
-
-    def timed(fn_call):
-        for _ in range(2):
-            fn_call()
-        barrier()
-        e0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            fn_call()
-        t = torch.tensor([(time.perf_counter() - e0) / e2e_steps], device="cuda")
-        if ws > 1:
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
-
-    # plain call(): H2D, run, D2H back to back
-    call_s = timed(lambda: gf.call(exe, host_in, out=host_out))
-    # call_streamed(): row chunks with H2D / compute / D2H overlapped on 3 streams
-    chunks = int(os.environ.get("GFB_BENCH_CHUNKS", 16))
-    e2e_s = timed(lambda: gf.call_streamed(exe, host_in, host_out, chunks=chunks))
-    h2d = sum(a.nbytes for a in arrays)
-    d2h = sum(t.buffer.nbytes for t in host_out)
-
-    hbm, _, peak_src = peaks()
-    achieved = nbytes / (kernel_ms * 1e-3) / 1e9
-    line = {
-        "metric": "fused-op HBM GB/s (config B: Relu(a+Broadcast(c))*b + row Sum, 64Mi fp32)",
-        "value": ws * nbytes / (ms * 1e-3) / 1e9,
-        "unit": "GB/s",
-        "n_gpus": ws,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ms,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic (numpy PCG64 seeded U(-1,1))",
-        "config": {"workload": "B: fused_chain rows=65536 cols=1024 per GPU", "bytes_per_step_per_gpu": nbytes,
-                   "l2": "inputs 805 MB > 126 MB L2, no flush needed", "parallelism": f"replicas x{ws} (row shards, no collective)"},
-        "e2e": {"value": ws * nbytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_s * 1e3,
-                "api": f"paper_1801_08058_b200.call_streamed(exe, pinned host inputs, pinned host results, chunks={chunks})",
-                "call_value": ws * nbytes / call_s / 1e9, "call_ms_per_step": call_s * 1e3,
-                "call_api": "paper_1801_08058_b200.call(exe, pinned host tensors, out=pinned host tensors)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": _traffic("B"), "kernel": exe.lowered.launches[dom].label + (":jit" if dom in prog.jit_launches else ""),
-                     "kernel_ms": kernel_ms,
-                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
-    }
+    n = max(3, min(10, args.steps))
+    for _ in range(2):
+        gf.call(exe, host_in, out=host_out)
+    _barrier(ws)
+    e0 = time.perf_counter()
+    for _ in range(n):
+        gf.call(exe, host_in, out=host_out)
+    e2e_s = _max_over_ranks((time.perf_counter() - e0) / n, ws)
+    line["e2e"] = {"value": gbatch / e2e_s, "unit": "samples/s", "ms_per_step": e2e_s * 1e3,
+                   "h2d_bytes_per_step": ws * sum(a.nbytes for a in arrays),
+                   "d2h_bytes_per_step": ws * sum(t.buffer.nbytes for t in host_out),
+                   "api": "paper_1801_08058_b200.call(exe, pinned host TensorValues, out=pinned host TensorValues) "
+                          "on every rank (its batch shard; replicated parameters), wall clock, max over ranks"}
     return line
 
 
-def _traffic(workload):
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(workload)
-    except Exception:
-        return None
+def cpu_baseline_step(wl):
+    """Oracle port on the host cores, bounded samples (about 15-25 s): all
+    threads at batch 64, and one thread at batch 4 (labelled)."""
+    from oracle import interp
 
-
-def launch_times(exe, dev_in, outs, stream, reps=3):
-    """Each launch alone (CUDA events on the launch stream), worst first, to stderr."""
-    import torch
-
-    prog = exe.program()
-    pin = [t.data_ptr() for t in dev_in]
-    pout = [t.data_ptr() for t in outs]
-    rows = []
-    for i, L in enumerate(exe.lowered.launches):
-        prog.run_one(i, pin, pout, stream.cuda_stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            prog.run_one(i, pin, pout, stream.cuda_stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) / reps
-        rows.append((t, i, L))
-    total = sum(r[0] for r in rows)
-    sys.stderr.write(f"# per-launch times (ms), total {total:.3f}\n")
-    jitted = set(getattr(prog, "jit_launches", ()))
-    merged = set(getattr(prog, "skipped", ()))
-    for t, i, L in sorted(rows, key=lambda r: -r[0]):
-        gbs = L.algo_bytes / (t * 1e-3) / 1e9 if t else 0
-        tfs = L.flops / (t * 1e-3) / 1e12 if t else 0
-        label = L.label + (":jit" if i in jitted else "") + (":merged-above" if i in merged else "")
-        sys.stderr.write(f"{t:9.3f} {100 * t / total:5.1f}% #{i:3d} {label:28s} grid={L.grid} {gbs:8.1f} GB/s {tfs:7.1f} TF/s\n")
+    threads = interp.max_threads()
+    g = step_config(wl, 1)["global_batch"]
+    b_all = 64 if wl == "E" else 2
+    t_all = _oracle_step_seconds(wl, b_all, threads, g)
+    b_one = 4 if wl == "E" else 1
+    t_one = _oracle_step_seconds(wl, b_one, 1, g)
+    return {"value": b_all / t_all, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"one oracle step at batch {b_all} of {g} (loss / {g}) on {threads} threads: {t_all:.2f} s",
+            "single_core": {"value": b_one / t_one, "cores": 1,
+                            "sample": f"one oracle step at batch {b_one} on 1 thread: {t_one:.2f} s"},
+            "cpu": _cpu_model(),
+            "note": "the step has a batch-independent part (SGD over all 134 M parameters), so samples/s grows with the sample batch"}
 
 
 def bench_gemm(args, local):
@@ -415,144 +673,62 @@ def bench_conv(args, local):
                        "launches": exe.num_launches}}
 
 
-def _step_for(workload, batch=None, ws=1):
-    """(step graph, per-GPU batch, description); `batch` is the GLOBAL batch."""
-    import paper_1801_08058_b200 as gf
-    from paper_1801_08058_b200 import workloads as W
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="E", choices=["E", "B", "A", "C", "D", "G", "H"])
+    ap.add_argument("--batch", type=int, default=None, help="global batch (training steps)")
+    ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
+    ap.add_argument("--dp", action="store_true", help="data-parallel plan even at one GPU (NCCL all-reduces)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-B block of the E line")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    maybe_relaunch(args)
+    ws, rank, local = dist_setup()
 
-    if workload == "A":
-        g = batch or 128
-        return W.mlp_step(gf, batch=g // ws, loss_batch=g), g // ws, "A: MLP 784-512-10"
-    if workload == "C":
-        g = batch or 256
-        return (W.cnn_step(gf, batch=g // ws, loss_batch=g), g // ws,
-                "C: CNN 32x32x3, conv 3->16->32, maxpool, fc 8192->10")
-    if workload == "D":
-        g = batch or 128 * ws  # config D is weak-scaled: 128 images per GPU
-        return (W.resnet_step(gf, batch=g // ws, loss_batch=g), g // ws,
-                "D: ResNet-18-style 224x224, NHWC layout assignment")
-    if workload == "E":
-        g = batch or 65536
-        return (W.mlp_step(gf, batch=g // ws, in_dim=4096, hidden=(4096,) * 7, out_dim=4096, loss_batch=g), g // ws,
-                "E: wide MLP 4096 x 8 layers")
-    raise ValueError(workload)
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(reference_arm(args, ws)), flush=True)
+        return
 
-
-def bench_step(args, ws, rank, local):
-    """Training step (fwd + autodiff bwd + SGD as one Function), samples/s.
-
-    Under torchrun the global batch is sharded over the ranks (strong
-    scaling): each rank runs the graph specialised to batch/ws with the loss
-    still divided by the global batch, and the partial gradients are summed
-    by NCCL all-reduces captured inside the step's CUDA graph."""
     import torch
-
-    import paper_1801_08058_b200 as gf
-    from paper_1801_08058_b200 import workloads as W
 
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    step, batch, desc = _step_for(args.workload, args.batch, ws)
-    t_compile = time.perf_counter()
-    dp = None
-    if ws > 1 or args.dp:
-        names = step.param_names
-        dp = gf.DataParallel([step.fn.parameters[names.index("x")], step.fn.parameters[names.index("t")]], world_size=ws)
-    exe = gf.compile_function(step.fn, data_parallel=dp, conv_layout="nhwc" if args.workload == "D" else "identity")
-    t_compile = time.perf_counter() - t_compile
-    shapes = W.parameter_shapes(step)
-    arrays = W.step_inputs(step, shapes, seed=rank)
-    dev_in = [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for a in arrays]
-    del arrays
-    outs = exe.allocate_outputs()
-    stream = torch.cuda.current_stream()
-    def barrier():
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-
-    with ClockSampler(local) as clk:
-        for _ in range(args.warmup):
-            exe.run_device(dev_in, outs, stream=stream.cuda_stream)
-        barrier()
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.steps):
-            exe.run_device(dev_in, outs, stream=stream.cuda_stream)
-        t1.record(stream)
-        barrier()
-    ms = t0.elapsed_time(t1) / args.steps
-    if ws > 1:
-        ms_t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(ms_t.item())
-    if args.launch_times:
-        launch_times(exe, dev_in, outs, stream)
-    flops = sum(L.flops for L in exe.lowered.launches)
-    _, tf_peak, _ = peaks()
-    gbatch = batch * ws
-    return {
-        "metric": f"training-step samples/sec (config {desc}, global batch {gbatch}, fwd+autodiff bwd+SGD)",
-        "value": gbatch / (ms * 1e-3), "unit": "samples/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if args.workload == "D" else "strong",
-        "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": desc, "global_batch": gbatch, "batch_per_gpu": batch,
-                                        "parallelism": f"dp{ws}", "launches": exe.num_launches,
-                                        "allreduces": len(getattr(exe, "allreduce", ()) or ()),
-                                        "flops_per_step_per_gpu": flops, "arena_bytes": exe.lowered.arena_bytes,
-                                        "compile_s": t_compile},
-        "achieved_tflops": ws * flops / (ms * 1e-3) / 1e12,
-        "gpu_launches": exe.num_launches * args.steps, "clocks": clk.summary(),
-    }
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="B", choices=["B", "A", "C", "D", "E", "G", "H"])
-    ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--launch-times", action="store_true", help="per-launch timing table to stderr")
-    ap.add_argument("--dp", action="store_true", help="data-parallel plan even at one GPU (NCCL all-reduces)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    ws, rank, local = dist_setup()
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        value, threads, sample = cpu_reference(ROWS, COLS, args.steps, args.warmup)
-        line = {
-            "impl": "reference", "metric": "fused-op HBM GB/s (config B: Relu(a+Broadcast(c))*b + row Sum, 64Mi fp32)",
-            "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "B: fused_chain rows=65536 cols=1024 per GPU"},
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line))
-        return
-
     if args.workload == "G":
         line = bench_gemm(args, local)
     elif args.workload == "H":
         line = bench_conv(args, local)
+    elif args.workload == "B":
+        line = bench_chain(args, ws, rank, local)
+        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+            from oracle import interp
+
+            value, threads, sample = cpu_reference_chain(ROWS, COLS, 2, 1, interp.max_threads(), budget_s=30.0)
+            line["cpu_baseline"] = {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
+                                    "cpu": _cpu_model()}
     else:
-        line = bench_chain(args, ws, rank, local) if args.workload == "B" else bench_step(args, ws, rank, local)
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "B":
-        value, threads, sample = cpu_reference(ROWS, COLS, 2, 1, budget_s=30.0)
-        line["cpu_baseline"] = {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}
+        line = bench_step(args, ws, rank, local)
+        if args.workload == "E" and not args.no_secondary:
+            torch.cuda.empty_cache()
+            b = bench_chain(args, ws, rank, local)
+            line["secondary"] = {k: b[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "config",
+                                                   "roofline", "e2e", "gpu_launches", "clocks") if k in b}
+        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_step(args.workload)
     if rank == 0:
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
 
+        dist.barrier()
         dist.destroy_process_group()
 
 

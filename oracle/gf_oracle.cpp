@@ -21,6 +21,7 @@
  * All buffers are logical row-major; layouts are value-transparent in the
  * reference (layout.py:1-12) and are not modelled here.
  */
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <thread>
@@ -153,16 +154,58 @@ void orc_elementwise(int op, int et, const void* a, const void* b, void* out, in
     }
 }
 
+/* kernels.py:143-153 for the 2-D transpose Reshape(x, (1, 0)) (autodiff's
+ * dW / dX operands): out[c, r] = in[r, c], a pure copy (bit-exact), in
+ * 64 x 64 tiles over all threads */
+void orc_transpose2d(int esize, const void* in, void* out, int64_t rows, int64_t cols) {
+    const int64_t TB = 64, nbr = (rows + TB - 1) / TB, nbc = (cols + TB - 1) / TB;
+    parfor(nbr * nbc, [&](int64_t blk) {
+        const int64_t r0 = (blk / nbc) * TB, c0 = (blk % nbc) * TB;
+        const int64_t r1 = std::min(rows, r0 + TB), c1 = std::min(cols, c0 + TB);
+        if (esize == 4) {
+            const uint32_t* x = (const uint32_t*)in;
+            uint32_t* y = (uint32_t*)out;
+            for (int64_t c = c0; c < c1; c++)
+                for (int64_t r = r0; r < r1; r++) y[c * rows + r] = x[r * cols + c];
+        } else if (esize == 8) {
+            const uint64_t* x = (const uint64_t*)in;
+            uint64_t* y = (uint64_t*)out;
+            for (int64_t c = c0; c < c1; c++)
+                for (int64_t r = r0; r < r1; r++) y[c * rows + r] = x[r * cols + c];
+        } else {
+            const uint8_t* x = (const uint8_t*)in;
+            uint8_t* y = (uint8_t*)out;
+            for (int64_t c = c0; c < c1; c++)
+                for (int64_t r = r0; r < r1; r++) y[c * rows + r] = x[r * cols + c];
+        }
+    });
+}
+
 /* kernels.py:123-133: acc = add(acc, mul(a[i,k], b[k,j])), k ascending */
 void orc_dot(int et, const void* a, const void* b, void* out, int64_t m, int64_t k, int64_t n) {
     if (et == ET_F32) {
         const float *A = (const float*)a, *B = (const float*)b;
         float* C = (float*)out;
-        parfor(m * n, [&](int64_t ij) {
-            int64_t i = ij / n, j = ij % n;
-            float acc = 0.0f;
-            for (int64_t t = 0; t < k; t++) acc = mac32(acc, A[i * k + t], B[t * n + j]);
-            C[ij] = acc;
+        // Work item = 8 rows x 256 columns of C: the accumulators stay in
+        // registers / L1 while k ascends and B streams row by row (no
+        // transpose).  Every output is still its own k-ascending chain.
+        constexpr int64_t RI = 8, CJ = 256;
+        const int64_t ni = (m + RI - 1) / RI, nj = (n + CJ - 1) / CJ;
+        parfor(ni * nj, [&](int64_t item) {
+            const int64_t i0 = (item / nj) * RI, j0 = (item % nj) * CJ;
+            const int64_t ri = std::min(RI, m - i0), cj = std::min(CJ, n - j0);
+            float acc[RI][CJ];
+            for (int64_t ii = 0; ii < ri; ii++)
+                for (int64_t jj = 0; jj < cj; jj++) acc[ii][jj] = 0.0f;
+            for (int64_t t = 0; t < k; t++) {
+                const float* br = B + t * n + j0;
+                for (int64_t ii = 0; ii < ri; ii++) {
+                    const float av = A[(i0 + ii) * k + t];
+                    for (int64_t jj = 0; jj < cj; jj++) acc[ii][jj] = mac32(acc[ii][jj], av, br[jj]);
+                }
+            }
+            for (int64_t ii = 0; ii < ri; ii++)
+                for (int64_t jj = 0; jj < cj; jj++) C[(i0 + ii) * n + j0 + jj] = acc[ii][jj];
         });
     } else {
         const double *A = (const double*)a, *B = (const double*)b;

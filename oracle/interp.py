@@ -64,6 +64,7 @@ def lib():
         _lib.orc_conv_bwd_data.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 11
         _lib.orc_conv_bwd_filter.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 11
         _lib.orc_set_threads.argtypes = [ctypes.c_int]
+        _lib.orc_transpose2d.argtypes = [ctypes.c_int, vp, vp, i64, i64]
     return _lib
 
 
@@ -107,7 +108,13 @@ def eval_node(node, args: list) -> np.ndarray:
         axes = node.attrs["broadcast_axes"]
         return np.broadcast_to(np.expand_dims(args[0], axes), desc.shape).copy()
     if kind is OpKind.RESHAPE:
-        return _c(args[0].transpose(node.attrs["input_order"])).reshape(desc.shape).copy()
+        x = args[0]
+        if tuple(node.attrs["input_order"]) == (1, 0) and x.ndim == 2 and x.size >= 65536:
+            x = _c(x)
+            out = np.empty((x.shape[1], x.shape[0]), dtype=x.dtype)
+            L.orc_transpose2d(x.itemsize, _ptr(x), _ptr(out), x.shape[0], x.shape[1])
+            return out.reshape(desc.shape)
+        return _c(x.transpose(node.attrs["input_order"])).reshape(desc.shape).copy()
     if kind is OpKind.CONVERT_LAYOUT:
         return args[0].copy()
     if kind is OpKind.SUM:

@@ -112,6 +112,19 @@ def mlp_step(api, batch=128, in_dim=784, hidden=(512,), out_dim=10, lr=0.01, bia
     return _training_step(api, fn, loss, names, weights, lr, et)
 
 
+def wide_mlp_step(api, batch=65536, width=4096, layers=8, loss_batch=None, lr=0.01) -> StepGraph:
+    """Config E: `layers` Dot+bias layers of width x width with Relu between
+    them, softmax cross-entropy over `width` classes, SGD."""
+    return mlp_step(api, batch=batch, in_dim=width, hidden=(width,) * (layers - 1), out_dim=width, lr=lr,
+                    loss_batch=loss_batch)
+
+
+def x_range_of(workload: str) -> tuple:
+    """Input distribution of x per config: U(-1, 1) for
+    config E, U(0, 1) (image-like) for the others."""
+    return (-1.0, 1.0) if workload == "E" else (0.0, 1.0)
+
+
 def maxpool2x2(api, fn, x, shape):
     """Differentiable 2x2/2 max-pool composite (SURVEY.md §7 hard part 8)."""
     K = api.OpKind
@@ -241,7 +254,7 @@ def _one_hot(rng, batch, classes, dtype):
     return t
 
 
-def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True) -> list:
+def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True, x_range=(0.0, 1.0)) -> list:
     """Arrays for every parameter of a training step, in parameter order."""
     dtype = np.float32 if f32 else np.float64
     rng = np.random.default_rng(seed)
@@ -249,7 +262,7 @@ def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True) -> list:
     for name in step.param_names:
         shape = fn_shapes[name]
         if name == "x":
-            out.append(_uniform(rng, shape, 0.0, 1.0, dtype))
+            out.append(_uniform(rng, shape, x_range[0], x_range[1], dtype))
         elif name == "t":
             out.append(_one_hot(rng, shape[0], shape[1], dtype))
         elif name == "seed":

@@ -3,6 +3,7 @@
 // in shared memory, no loads).  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mma_probe scripts/mma_probe.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -13,10 +14,11 @@ __device__ __forceinline__ uint64_t desc(const void* p) {
     d |= (uint64_t)2 << 61;
     return d;
 }
-template <int KIND>  // 0 tf32, 1 f16 (bf16)
+template <int KIND>  // 0 tf32, 1 f16 (bf16), 2 i8 (s8 x s8 -> s32)
 __host__ __device__ constexpr uint32_t idesc(int M, int N) {
-    return KIND == 0 ? ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24))
-                     : ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24));
+    return KIND == 0   ? ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24))
+           : KIND == 1 ? ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24))
+                       : ((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24));
 }
 
 template <int N, int NACC, int KIND>
@@ -48,6 +50,8 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* o
                 const uint64_t adv = (uint64_t)((j & 3) * 32) >> 4;
                 if (KIND == 0)
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(a + adv), "l"(b + adv), "r"(id));
+                else if (KIND == 2)
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\ttcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(a + adv), "l"(b + adv), "r"(id));
                 else
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(a + adv), "l"(b + adv), "r"(id));
             }
@@ -64,13 +68,15 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* o
     if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+static int g_iters = 2000;
+
 template <int N, int NACC, int KIND>
 void run(const char* name) {
     unsigned long long* d;
     cudaMalloc(&d, 8);
     int smem = (128 + 256) * 128 + 1024;
     cudaFuncSetAttribute(probe<N, NACC, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int iters = 2000;
+    const int iters = g_iters;
     probe<N, NACC, KIND><<<148, 128, smem>>>(iters, d);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -84,14 +90,16 @@ void run(const char* name) {
     unsigned long long cyc;
     cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
     const double mmas = 12.0 * iters;
-    const double k = KIND == 0 ? 8 : 16;
+    const double k = KIND == 0 ? 8 : KIND == 1 ? 16 : 32;
     const double flops = mmas * 2.0 * 128 * N * k * 148;
-    printf("%-6s N=%3d acc=%d: %7.1f cyc/mma  %8.1f TFLOP/s  (%s)\n", KIND == 0 ? "tf32" : "bf16", N, NACC, cyc / mmas,
-           flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    printf("%-6s N=%3d acc=%d iters=%6d: %7.1f cyc/mma  %8.1f TFLOP/s  %6.0f MHz  %.2f ms  (%s)\n",
+           KIND == 0 ? "tf32" : KIND == 1 ? "bf16" : "i8", N, NACC, iters, cyc / mmas, flops / (ms * 1e-3) / 1e12,
+           cyc / (ms * 1e3), ms, cudaGetErrorString(cudaGetLastError()));
     cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) g_iters = atoi(argv[1]);
     run<64, 1, 0>("");
     run<64, 3, 0>("");
     run<128, 1, 0>("");
@@ -100,5 +108,13 @@ int main() {
     run<256, 2, 0>("");
     run<128, 1, 1>("");
     run<256, 1, 1>("");
+    run<128, 1, 2>("");
+    run<256, 1, 2>("");
+    run<256, 2, 2>("");
+    // sustained (seconds-long, under the power cap): tf32 N=256, the 3xTF32 GEMM's shape
+    g_iters *= 200;
+    run<256, 2, 0>("");
+    run<256, 2, 1>("");
+    run<256, 2, 2>("");
     return 0;
 }
