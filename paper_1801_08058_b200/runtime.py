@@ -359,6 +359,11 @@ def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     the launch list once), `data_parallel` (a `dp.DataParallel`: batch-shard
     the listed parameters and all-reduce the partial gradients) with the
     NCCL communicator `comm` from `init_distributed()`."""
+    from .refcompat import as_function, as_layout
+
+    fn = as_function(fn)  # a reference-built graphforge.Function is mirrored node for node
+    if parameter_layouts is not None:
+        parameter_layouts = [as_layout(lay) for lay in parameter_layouts]
     h = prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=parameter_layouts,
                          data_parallel=data_parallel)
     if h.allreduce and comm is None:
@@ -455,6 +460,9 @@ def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device
     """
     import torch
 
+    from .refcompat import as_tensor
+
+    inputs = [as_tensor(t) for t in inputs]  # reference-built TensorValues are accepted as they are
     _check_signature(exe, inputs)
     ensure_device()
     dev_in = [to_device(t) for t in inputs]

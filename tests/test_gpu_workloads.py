@@ -83,7 +83,8 @@ def test_data_parallel_plan_single_rank_nccl():
     names = step.param_names
     dp = gf.DataParallel([step.fn.parameters[names.index("x")], step.fn.parameters[names.index("t")]])
     exe = gf.compile_function(step.fn, data_parallel=dp)
-    assert sum(1 for L in exe.lowered.launches if L.label.startswith("allreduce")) == 5
+    ar = [L for L in exe.lowered.launches if L.label.startswith("allreduce")]
+    assert 1 <= len(ar) <= 5 and sum(len(L.reads) for L in ar) == 5  # 5 roots in gradient buckets
     tens = [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays]
     got = [t.to_numpy() for t in gf.call(exe, tens)]
     plain = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
