@@ -228,7 +228,8 @@ def _oracle_step_seconds(workload, batch, threads, global_batch):
         step = W.wide_mlp_step(gf, batch=batch, loss_batch=global_batch)
     else:
         step, _ = _step_for(workload, batch, 1)
-    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=0, x_range=W.x_range_of(workload))
+    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=0, x_range=W.x_range_of(workload),
+                           conv_gain=W.conv_gain_of(workload))
     t0 = time.perf_counter()
     interp.run_function(step.fn, arrays)
     return time.perf_counter() - t0
@@ -494,7 +495,7 @@ def bench_step(args, ws, rank, local):
     exe = gf.compile_function(step.fn, data_parallel=dp, conv_layout="nhwc" if wl == "D" else "identity")
     t_compile = time.perf_counter() - t_compile
     shapes = W.parameter_shapes(step)
-    arrays = W.step_inputs(step, shapes, seed=rank, x_range=W.x_range_of(wl))
+    arrays = W.step_inputs(step, shapes, seed=rank, x_range=W.x_range_of(wl), conv_gain=W.conv_gain_of(wl))
     dev_in = [torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).cuda() for a in arrays]
     outs = exe.allocate_outputs()
     stream = torch.cuda.current_stream()
@@ -566,23 +567,26 @@ def bench_step(args, ws, rank, local):
     return line
 
 
+# sample batches of the CPU baseline per config: (all threads, one thread)
+CPU_SAMPLE = {"E": (64, 4), "A": (128, 128), "C": (16, 2), "D": (1, 1)}
+
+
 def cpu_baseline_step(wl):
-    """Oracle port on the host cores, bounded samples (about 15-25 s): all
-    threads at batch 64, and one thread at batch 4 (labelled)."""
+    """Oracle port on the host cores, bounded samples (a few to ~20 s): all
+    threads at a sample batch, and one thread at a smaller one (labelled)."""
     from oracle import interp
 
     threads = interp.max_threads()
     g = step_config(wl, 1)["global_batch"]
-    b_all = 64 if wl == "E" else 2
+    b_all, b_one = CPU_SAMPLE[wl]
     t_all = _oracle_step_seconds(wl, b_all, threads, g)
-    b_one = 4 if wl == "E" else 1
-    t_one = _oracle_step_seconds(wl, b_one, 1, g)
+    t_one = _oracle_step_seconds(wl, b_one, 1, g) if wl != "D" else None
     return {"value": b_all / t_all, "unit": "samples/s", "cores": threads, "kind": "port",
             "sample": f"one oracle step at batch {b_all} of {g} (loss / {g}) on {threads} threads: {t_all:.2f} s",
-            "single_core": {"value": b_one / t_one, "cores": 1,
-                            "sample": f"one oracle step at batch {b_one} on 1 thread: {t_one:.2f} s"},
+            "single_core": None if t_one is None else {"value": b_one / t_one, "cores": 1,
+                                                       "sample": f"one oracle step at batch {b_one} on 1 thread: {t_one:.2f} s"},
             "cpu": _cpu_model(),
-            "note": "the step has a batch-independent part (SGD over all 134 M parameters), so samples/s grows with the sample batch"}
+            "note": "the step has a batch-independent part (SGD over every parameter), so samples/s grows with the sample batch"}
 
 
 def bench_gemm(args, local):
@@ -716,13 +720,24 @@ def main():
                                     "cpu": _cpu_model()}
     else:
         line = bench_step(args, ws, rank, local)
-        if args.workload == "E" and not args.no_secondary:
-            torch.cuda.empty_cache()
-            b = bench_chain(args, ws, rank, local)
-            line["secondary"] = {k: b[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "config",
-                                                   "roofline", "e2e", "gpu_launches", "clocks") if k in b}
         if rank == 0 and ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_step(args.workload)
+        if args.workload == "E" and not args.no_secondary:
+            # the other BASELINE.json configs, each measured the same way (own
+            # roofline, e2e through call(), CPU baseline at N = 1)
+            keys = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "scaling", "config", "roofline", "e2e",
+                    "gpu_launches", "clocks", "step_detail", "cpu_baseline")
+            torch.cuda.empty_cache()
+            b = bench_chain(args, ws, rank, local)
+            line["secondary"] = {k: b[k] for k in keys if k in b}
+            line["configs"] = {}
+            for wl, steps in (("A", 200), ("C", 50), ("D", 10)):
+                torch.cuda.empty_cache()
+                sub = argparse.Namespace(**dict(vars(args), workload=wl, steps=steps, batch=None, launch_times=False))
+                r = bench_step(sub, ws, rank, local)
+                if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+                    r["cpu_baseline"] = cpu_baseline_step(wl)
+                line["configs"][wl] = {k: r[k] for k in keys if k in r}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -10,10 +10,19 @@ value (same descriptor, layout order and logical contents; `tensor.py:27-102`),
 without a print/parse round trip.  Detection is duck-typed on the objects'
 structure and their defining module, never on an import of the reference
 (which this package must not depend on).
+
+Errors keep the caller's taxonomy: when the objects came from the
+reference package, a `GraphError` raised here is re-raised as the
+reference's class of the same name (`errors.py:6-84`), so `except
+graphforge.errors.SignatureMismatch` keeps working after the swap.
 """
 
 from __future__ import annotations
 
+import contextlib
+import sys
+
+from .errors import GraphError
 from .ir import ElementType, Function, Node, OpKind, infer_output, normalize_attrs
 from .layout import Layout
 from .tensor import TensorValue, tensor_from_flat
@@ -69,3 +78,34 @@ def as_tensor(t):
         return t
     d = t.descriptor
     return tensor_from_flat(_enum(d.element_type, ElementType), tuple(d.shape), t.to_flat(), as_layout(t.layout))
+
+
+def foreign_errors(*objs):
+    """The reference package's `errors` module if any of `objs` (or, for a
+    list, its first element) was built by it, else None."""
+    ours = __name__.split(".")[0]
+    for obj in objs:
+        if isinstance(obj, (list, tuple)):
+            obj = obj[0] if obj else None
+        if obj is None:
+            continue
+        top = type(obj).__module__.split(".")[0]
+        if top not in (ours, "builtins"):
+            return sys.modules.get(top + ".errors")
+    return None
+
+
+@contextlib.contextmanager
+def caller_errors(errors_mod):
+    """Re-raise our GraphError subclasses as `errors_mod`'s same-named class."""
+    try:
+        yield
+    except GraphError as exc:
+        cls = getattr(errors_mod, type(exc).__name__, None) if errors_mod is not None else None
+        if not (isinstance(cls, type) and issubclass(cls, Exception)):
+            raise
+        try:
+            new = cls(*exc.args)
+        except TypeError:
+            raise exc
+        raise new from exc

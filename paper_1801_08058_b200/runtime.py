@@ -359,13 +359,15 @@ def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     the launch list once), `data_parallel` (a `dp.DataParallel`: batch-shard
     the listed parameters and all-reduce the partial gradients) with the
     NCCL communicator `comm` from `init_distributed()`."""
-    from .refcompat import as_function, as_layout
+    from .refcompat import as_function, as_layout, caller_errors, foreign_errors
 
-    fn = as_function(fn)  # a reference-built graphforge.Function is mirrored node for node
-    if parameter_layouts is not None:
-        parameter_layouts = [as_layout(lay) for lay in parameter_layouts]
-    h = prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=parameter_layouts,
-                         data_parallel=data_parallel)
+    errors_mod = foreign_errors(fn)
+    with caller_errors(errors_mod):
+        fn = as_function(fn)  # a reference-built graphforge.Function is mirrored node for node
+        if parameter_layouts is not None:
+            parameter_layouts = [as_layout(lay) for lay in parameter_layouts]
+        h = prepare_function(fn, optimize=optimize, conv_layout=conv_layout, parameter_layouts=parameter_layouts,
+                             data_parallel=data_parallel)
     if h.allreduce and comm is None:
         comm = init_distributed()
     handle = comm.handle if comm is not None else None
@@ -374,6 +376,7 @@ def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
                      h.lowered, cuda_graph, handle)
     exe.comm = comm
     exe.allreduce = h.allreduce
+    exe.caller_errors = errors_mod
     return exe
 
 
@@ -460,10 +463,11 @@ def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device
     """
     import torch
 
-    from .refcompat import as_tensor
+    from .refcompat import as_tensor, caller_errors, foreign_errors
 
-    inputs = [as_tensor(t) for t in inputs]  # reference-built TensorValues are accepted as they are
-    _check_signature(exe, inputs)
+    with caller_errors(getattr(exe, "caller_errors", None) or foreign_errors(inputs)):
+        inputs = [as_tensor(t) for t in inputs]  # reference-built TensorValues are accepted as they are
+        _check_signature(exe, inputs)
     ensure_device()
     dev_in = [to_device(t) for t in inputs]
     outs = exe.allocate_outputs()

@@ -119,6 +119,15 @@ def wide_mlp_step(api, batch=65536, width=4096, layers=8, loss_batch=None, lr=0.
                     loss_batch=loss_batch)
 
 
+def conv_gain_of(workload: str) -> float:
+    """Scale of the He-style conv filter bound per config.  Config D (no
+    normalisation, 8 residual additions) at gain 1 drives the logits so far
+    apart that softmax probabilities underflow to 0 and the reference loss
+    t * log(p) becomes 0 * -inf = NaN; at 0.5 the 224x224 step stays finite
+    (loss ~2.2, near log 10)."""
+    return 0.5 if workload == "D" else 1.0
+
+
 def x_range_of(workload: str) -> tuple:
     """Input distribution of x per config: U(-1, 1) for
     config E, U(0, 1) (image-like) for the others."""
@@ -254,7 +263,7 @@ def _one_hot(rng, batch, classes, dtype):
     return t
 
 
-def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True, x_range=(0.0, 1.0)) -> list:
+def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True, x_range=(0.0, 1.0), conv_gain=1.0) -> list:
     """Arrays for every parameter of a training step, in parameter order."""
     dtype = np.float32 if f32 else np.float64
     rng = np.random.default_rng(seed)
@@ -268,7 +277,7 @@ def step_inputs(step: StepGraph, fn_shapes: dict, seed=0, f32=True, x_range=(0.0
         elif name == "seed":
             out.append(np.ones(shape, dtype=dtype))
         elif len(shape) == 4:  # conv filter [K, C, R, S]: He-style fan-in bound
-            bound = float(np.sqrt(6.0 / (shape[1] * shape[2] * shape[3])))
+            bound = conv_gain * float(np.sqrt(6.0 / (shape[1] * shape[2] * shape[3])))
             out.append(_uniform(rng, shape, -bound, bound, dtype))
         else:
             fan = shape[0] if len(shape) >= 2 else 10

@@ -50,3 +50,18 @@ def test_tensor_and_layout_mirror():
     assert o.layout.order == (1, 0) and o.to_flat() == t.to_flat()
     assert np.asarray(o.to_flat()).dtype == np.float64
     assert as_layout(graphforge.Layout((0, 2, 1))).order == (0, 2, 1)
+
+
+def test_errors_keep_the_callers_taxonomy():
+    from paper_1801_08058_b200.errors import SignatureMismatch
+    from paper_1801_08058_b200.refcompat import caller_errors, foreign_errors
+
+    fn, _ = _mlp_ref()
+    mod = foreign_errors(fn)
+    assert mod is graphforge.errors
+    with pytest.raises(graphforge.errors.SignatureMismatch):
+        with caller_errors(mod):
+            raise SignatureMismatch("x")
+    with pytest.raises(SignatureMismatch):  # our own objects: our own classes
+        with caller_errors(foreign_errors(as_function(fn))):
+            raise SignatureMismatch("x")
