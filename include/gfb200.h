@@ -87,6 +87,9 @@ enum {
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
+    GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
+                             always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
+                             entry only traps */
 };
 
 /* ---- tensor references inside kernel arguments ------------------------- */
@@ -341,6 +344,16 @@ typedef struct {
     int32_t dtype;  /* 0 f32, 1 f64 */
     int32_t op;     /* 0 sum (partial gradients), 1 max (a max-reduction over the sharded batch axis) */
 } gfb_allreduce_args;
+
+/* Row-fused launch: the generated kernel's tensors, by position (inputs,
+ * outputs, per-team partials of cross-row reductions; rowfuse.py). */
+#define GFB_ROW_MAX_REFS 30
+typedef struct {
+    const void* const* tab;
+    uint32_t n_refs;
+    uint32_t pad;
+    uint64_t refs[GFB_ROW_MAX_REFS]; /* GFB_REF */
+} gfb_row_args;
 
 /* One kernel launch of the plan; its argument block is args[arg_offset, +arg_size). */
 typedef struct {

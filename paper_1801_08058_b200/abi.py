@@ -24,6 +24,8 @@ K_CONV_STEM64 = 32
 K_DOT_TH_F32, K_DOT_TH_F64 = 26, 27
 K_CONV_F32, K_CONV_F64 = 20, 21
 K_ALLREDUCE = 30
+K_ROWJIT = 33
+ROW_MAX_REFS = 30
 
 SLOT_ARENA, SLOT_CONST, SLOT_IO = 0, 1, 2
 MAX_LEAVES, MAX_DIGITS, MAX_INSTR = 16, 6, 128
@@ -180,6 +182,12 @@ class AllReduceArgs(C.Structure):
     ]
 
 
+class RowArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("n_refs", C.c_uint32), ("pad", C.c_uint32), ("refs", C.c_uint64 * 30),
+    ]
+
+
 class Launch(C.Structure):
     _fields_ = [
         ("kind", C.c_uint32), ("grid", C.c_uint32 * 3), ("block", C.c_uint32 * 3),
@@ -200,5 +208,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

@@ -597,6 +597,13 @@ class Lowered:
         return recs, bytes(blob)
 
 
+class _DropRowGroup(Exception):
+    """A row group turned out not to be expressible: lower without it."""
+
+    def __init__(self, group):
+        self.group = group
+
+
 class _Retry(Exception):
     def __init__(self, nid):
         self.nid = nid
@@ -742,16 +749,54 @@ class Lowering:
 
     # -- main entry
     def run(self) -> Lowered:
+        self._topo_order = list(self.order)
         self.M = set()
         self.initial_materialised()
+        self.row_groups = []
+        from . import rowfuse
+
+        if rowfuse.enabled():
+            self.row_groups = rowfuse.find_groups(self)
+        self._apply_row_groups()
         for _ in range(1000):
             try:
                 return self._lower()
             except _Retry as r:
+                g = self._row_of.get(r.nid)
+                if g is not None:  # a member someone must read from memory: store it too
+                    if r.nid in g.outputs:
+                        raise UnsupportedOp(f"cannot lower node {r.nid} ({self.nodes[r.nid].op.wire_name})")
+                    g.outputs.append(r.nid)
+                    self.M.add(r.nid)
+                    continue
                 if r.nid in self.M:
                     raise UnsupportedOp(f"cannot lower node {r.nid} ({self.nodes[r.nid].op.wire_name})")
                 self.M.add(r.nid)
+            except _DropRowGroup as d:
+                self.row_groups.remove(d.group)
+                self.M = set()
+                self.initial_materialised()
+                self._apply_row_groups()
         raise UnsupportedOp("lowering did not converge")
+
+    def _apply_row_groups(self):
+        """Materialisation and order for the row-fused groups (rowfuse.py):
+        internal members live in registers, outputs and forced inputs in
+        memory, and each group's members become contiguous in the order."""
+        from . import rowfuse
+
+        self._row_of, self._row_nodes = {}, set()
+        for g in self.row_groups:
+            for m in g.members:
+                self._row_of[m] = g
+                if m not in g.outputs:
+                    self.M.discard(m)
+            self.M.update(g.outputs)
+            self.M.update(g.force)
+            self._row_nodes |= set(g.members)
+        self.order = rowfuse.reorder(self._topo_order, self.consumers, lambda n: [r for r, _ in self.nodes[n].inputs],
+                                     self.row_groups) if self.row_groups else list(self._topo_order)
+        self.topo = {n: i for i, n in enumerate(self.order)}
 
     def _lower(self) -> Lowered:
         g = self.g
@@ -810,9 +855,9 @@ class Lowering:
         # merge rule: a materialised node consumed only by one Sum is that Sum's side output
         side_of = {}
         for n in self.order:
-            if n in self.M and self.nodes[n].op is not OpKind.SUM and self.is_light(n):
+            if n in self.M and self.nodes[n].op is not OpKind.SUM and self.is_light(n) and n not in self._row_nodes:
                 cons = self.consumers[n]
-                if len(cons) == 1 and self.nodes[cons[0]].op is OpKind.SUM:
+                if len(cons) == 1 and self.nodes[cons[0]].op is OpKind.SUM and cons[0] not in self._row_nodes:
                     side_of[cons[0]] = n
         merged = set(side_of.values())
 
@@ -822,6 +867,11 @@ class Lowering:
         chained = set(self._map_side.values())
         for n in self.order:
             node = self.nodes[n]
+            rg = self._row_of.get(n)
+            if rg is not None:
+                if n == rg.anchor:
+                    self.emit_row_group(rg)
+                continue
             if self.is_heavy(n):
                 self.emit_heavy(n)
             elif n in self.M and n not in merged and n not in grouped and n not in chained:
@@ -1067,13 +1117,14 @@ class Lowering:
         out, used = {}, set()
         for n in self.order:
             if (n not in self.M or n in taken or n in used or n in self.allreduce or not self.is_light(n)
-                    or self.nodes[n].op is OpKind.SUM or n not in self.buf):
+                    or self.nodes[n].op is OpKind.SUM or n not in self.buf or n in self._row_nodes):
                 continue
             cons = sorted(set(self.consumers[n]), key=lambda c: pos.get(c, 1 << 30))
             if not cons:
                 continue
             c = cons[0]
             if (c in taken or c in out or c in used or c not in self.M or not self.is_light(c) or c in self.allreduce
+                    or c in self._row_nodes
                     or self.nodes[c].op is OpKind.SUM or self.nodes[c].op in INDEX_OPS or c not in self.buf
                     or pos.get(c) is None):
                 continue
@@ -1107,7 +1158,7 @@ class Lowering:
                     stack += [r for r, _ in self.g.nodes[x].inputs]
             return out
 
-        cands = [n for n in self.order if n in self.M and n not in merged and self.is_light(n)
+        cands = [n for n in self.order if n in self.M and n not in merged and self.is_light(n) and n not in self._row_nodes
                  and self.nodes[n].op is not OpKind.SUM and n in self.buf and self.buf[n].slot == abi.SLOT_ARENA]
         groups, taken = {}, set()
         for i, n in enumerate(cands):
@@ -1357,6 +1408,142 @@ class Lowering:
         rec.algo_bytes = prog.algo_bytes()
         rec.finalize = prog.finalize_fn(args)
         self.launches.append(rec)
+
+    def emit_row_group(self, g):
+        """One row-fused launch for a group (rowfuse.py) plus a short second
+        pass per cross-row reduction over the per-team partials."""
+        from . import rowfuse as RF
+
+        et, esize = g.et, g.et.byte_size
+        refs, reads, writes = [], [], []
+        vals, index, ext_val = [], {}, {}
+        full_access = []  # (s0, s1, buffer) of every FULL load / store: decides the vector width
+
+        def ref_of(b):
+            for i, x in enumerate(refs):
+                if x is b:
+                    return i
+            refs.append(b)
+            return len(refs) - 1
+
+        def access(x):
+            b = self.buf.get(x)
+            if b is not None:
+                return b, b.strides
+            hv = self.heavy_operand(x)
+            if hv is None or hv[1] is None:
+                raise _DropRowGroup(g)
+            return hv
+
+        def ext(x, cls):
+            key = (x, cls)
+            if key in ext_val:
+                return ext_val[key]
+            if cls == RF.UNI:
+                b = self.buf.get(x)
+                if b is not None and b.splat is not None:
+                    vals.append((RF.UNI, ("imm", RF.splat_bits(et, b.splat))))
+                else:
+                    b, _ = access(x)
+                    vals.append((RF.UNI, ("loadu", ref_of(b))))
+                    reads.append(b.key)
+            else:
+                b, st = access(x)
+                if b.subaxes or b.splat is not None:
+                    raise _DropRowGroup(g)
+                reads.append(b.key)
+                if cls == RF.FULL:
+                    vals.append((RF.FULL, ("load", ref_of(b), int(st[0]), int(st[1]))))
+                    full_access.append((int(st[0]), int(st[1]), b))
+                elif cls == RF.ROWV:
+                    vals.append((RF.ROWV, ("loadr", ref_of(b), int(st[0]))))
+                else:  # COLV: only as the operand of a Broadcast along rows
+                    vals.append((RF.FULL, ("colv", ref_of(b), int(st[0]))))
+            ext_val[key] = len(vals) - 1
+            return ext_val[key]
+
+        def operand(r, cls):
+            return index[r] if r in index else ext(r, g.externals[r])
+
+        for n in g.members:
+            node = self.nodes[n]
+            c = g.cls[n]
+            ins = [r for r, _ in node.inputs]
+            if node.op in ELEMENTWISE_UNARY:
+                e = ("un", RF.UNARY_CODE[node.op], operand(ins[0], c))
+            elif node.op in ELEMENTWISE_BINARY:
+                e = ("bin", RF.BINARY_CODE[node.op], operand(ins[0], c), operand(ins[1], c))
+            elif node.op is OpKind.BROADCAST:
+                r = ins[0]
+                if r not in index and g.externals[r] == RF.COLV:
+                    index[n] = ext(r, RF.COLV)
+                    continue
+                e = ("bcast", operand(r, None))
+            else:  # Sum: a row reduction or a cross-row one
+                kind = 2 if node.attrs["reduction_kind"] == "max" else 1
+                a = operand(ins[0], None)
+                e = ("rred", kind, a) if c == RF.ROWV else ("xred", kind, a, vals[a][0])
+            vals.append((c, e))
+            index[n] = len(vals) - 1
+        stores, xrow, pass2 = [], [], []
+        for o in g.outputs:
+            b = self.buf[o]
+            if b.subaxes:
+                raise _DropRowGroup(g)
+            writes.append(b.key)
+            if g.cls[o] == RF.XROW:
+                continue
+            st = b.strides
+            if g.cls[o] == RF.FULL:
+                stores.append((index[o], ref_of(b), int(st[0]), int(st[1])))
+                full_access.append((int(st[0]), int(st[1]), b))
+            else:
+                stores.append((index[o], ref_of(b), int(st[0]), 0))
+        vec_ok = all(s1 == 1 and s0 % (16 // esize) == 0 and (b.elem_off * esize) % 16 == 0 for s0, s1, b in full_access)
+        team, block, vec = RF.geometry(g.C, esize, vec_ok)
+        per_block = block // team
+        blocks = max(1, min((g.R + per_block - 1) // per_block, NUM_SMS * max(1, 2048 // block)))
+        n_teams = blocks * per_block
+        for o in g.outputs:
+            if g.cls[o] != RF.XROW:
+                continue
+            kind = vals[index[o]][1][1]
+            partial = Buffer(self.new_key(), et, (n_teams,), (1,))
+            self.buf[("rowpart", partial.key)] = partial
+            writes.append(partial.key)
+            xrow.append((index[o], kind, ref_of(partial)))
+            pass2.append((o, kind, partial))
+        if len(refs) > abi.ROW_MAX_REFS:
+            raise _DropRowGroup(g)
+        live = sum(1 for c, _ in vals if c == RF.FULL)
+        if live > 4 * RF.MAX_FULL_LIVE:
+            raise _DropRowGroup(g)
+        spec = RF.RowSpec(g.R, g.C, "float" if et is ElementType.F32 else "double", team, block, vec, vals, stores, xrow,
+                          n_teams)
+        args = abi.RowArgs(n_refs=len(refs))
+        label = f"row:{self.nodes[g.members[0]].op.wire_name}#{g.members[0]}..{self.nodes[g.anchor].op.wire_name}#{g.anchor}"
+        rec = LaunchRec(abi.K_ROWJIT, (blocks, 1, 1), (block, 1, 1), 0, args, sorted(set(reads)), sorted(set(writes)), label)
+        ext_bytes = {RF.FULL: g.R * g.C, RF.ROWV: g.R, RF.COLV: g.C, RF.UNI: 1}
+        rec.algo_bytes = esize * (sum(ext_bytes[c] for c in g.externals.values())
+                                  + sum(ext_bytes.get(g.cls[o], 1) for o in g.outputs))
+        bufs = list(refs)
+
+        def fin():
+            for i, b in enumerate(bufs):
+                args.refs[i] = _buf_ref(b)
+        rec.finalize = fin
+        rec.row_spec = spec
+        self.launches.append(rec)
+        for o, kind, partial in pass2:
+            rowwise = n_teams >= 256
+            p2 = Program(self, extents=(1, n_teams), vec_src=1 if rowwise else 0, et=et)
+            k = p2.leaf(partial, [(1, 1, n_teams)])
+            p2.emit(I_LOAD, k=k)
+            p2.set_red_out(self.buf[o], iteration_axes(self.nodes[o].output.shape))
+            if rowwise:
+                self._row_launch(p2, 1, n_teams, kind, f"rowsum#{o}:teams", et)
+            else:
+                self._col_launch(p2, 1, n_teams, kind, f"rowsum#{o}:teams", et)
 
     def _gradient_regions(self):
         """Place the data-parallel partial roots contiguously, in production

@@ -698,6 +698,11 @@ __global__ void __launch_bounds__(256, 3) gfb_ew_staged_kernel(const __grid_cons
 }
 
 template __global__ void gfb_ew_staged_kernel<float, 2, 2>(const __grid_constant__ gfb_ew_args);
+
+// A row-fused launch (GFB_K_ROWJIT) only ever runs its runtime-generated
+// kernel (rowfuse.py via jit.py); reaching this entry means the kernel was
+// never installed, which must fail loudly rather than compute nothing.
+__global__ void gfb_row_unspecialised(const __grid_constant__ gfb_row_args) { __trap(); }
 template __global__ void gfb_ew_staged_kernel<double, 2, 2>(const __grid_constant__ gfb_ew_args);
 
 template __global__ void gfb_ew_kernel<float, 8>(const __grid_constant__ gfb_ew_args);
@@ -715,6 +720,7 @@ extern "C" const void* gfb_ew_kernel_ptr(int kind) {
         case GFB_K_EW_F64: return (const void*)gfb::gfb_ew_kernel<double, 4>;
         case GFB_K_EW_I64: return (const void*)gfb::gfb_ew_kernel<long long, 4>;
         case GFB_K_EW_U8: return (const void*)gfb::gfb_ew_kernel<unsigned char, 8>;
+        case GFB_K_ROWJIT: return (const void*)gfb::gfb_row_unspecialised;
         case GFB_K_EWS_F32: return (const void*)gfb::gfb_ew_staged_kernel<float, 2, 2>;
         case GFB_K_EWS_F64: return (const void*)gfb::gfb_ew_staged_kernel<double, 2, 2>;
         case GFB_K_EW1_F32: return (const void*)gfb::gfb_ew_kernel<float, 1>;

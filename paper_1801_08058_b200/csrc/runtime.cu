@@ -185,7 +185,7 @@ struct gfb_exe {
 namespace {
 
 const void* kernel_for(uint32_t kind) {
-    if (kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64) return gfb_ew_kernel_ptr((int)kind);
+    if ((kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64) || kind == GFB_K_ROWJIT) return gfb_ew_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F32 || kind == GFB_K_DOT_F64 || kind == GFB_K_CONV_F32 || kind == GFB_K_CONV_F64 ||
         kind == GFB_K_DOT_SM_F32 || kind == GFB_K_DOT_SM_F64 || kind == GFB_K_DOT_TH_F32 || kind == GFB_K_DOT_TH_F64)
         return gfb_simt_kernel_ptr((int)kind);
@@ -539,8 +539,8 @@ int gfb_exe_set_kernel(gfb_exe* e, uint32_t index, const void* kernel, uint32_t 
     if (!e || index >= e->launches.size()) return fail(GFB_ERR_INVALID, "bad launch index");
     std::lock_guard<std::mutex> lk(e->mu);
     const uint32_t kind = e->launches[index].kind;
-    if (!(kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64))
-        return fail(GFB_ERR_INVALID, "only fused elementwise launches take a runtime-compiled kernel");
+    if (!((kind >= GFB_K_EW_F32 && kind <= GFB_K_EW1_F64) || kind == GFB_K_ROWJIT))
+        return fail(GFB_ERR_INVALID, "only fused elementwise / row launches take a runtime-compiled kernel");
     if (kernel && smem >= 48 * 1024)
         CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     e->fns[index] = kernel;

@@ -569,7 +569,7 @@ def compile_cubin(src: str) -> bytes:
 
 
 def eligible(L) -> bool:
-    return L.kind in KINDS and (L.algo_bytes or 0) >= MIN_BYTES
+    return L.kind == abi.K_ROWJIT or (L.kind in KINDS and (L.algo_bytes or 0) >= MIN_BYTES)
 
 
 def _kernel(lib, cubin: bytes):
@@ -597,7 +597,7 @@ def _groups(launches, recs, todo):
     prev = None
     for i in todo:
         r = recs[i]
-        single = MERGE and tuple(r.grid) == (1, 1, 1)
+        single = MERGE and tuple(r.grid) == (1, 1, 1) and launches[i].kind != abi.K_ROWJIT
         if single and run and prev == i - 1 and recs[run[0]].block[0] == r.block[0]:
             run.append(i)
         else:
@@ -624,7 +624,7 @@ def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = N
     try:
         _lib_nvrtc()
     except RuntimeError as exc:
-        if strict:
+        if strict or any(launches[i].kind == abi.K_ROWJIT for i in todo):
             raise
         _warn_once(f"runtime specialisation off ({exc}); the generic VM kernel runs every elementwise launch")
         return [], []
@@ -634,6 +634,10 @@ def specialise(lib, handle, launches, blob: bytes, recs, workers: int | None = N
         return abi.EwArgs.from_buffer_copy(blob[r.arg_offset:r.arg_offset + r.arg_size])
 
     def build(group):
+        if launches[group[0]].kind == abi.K_ROWJIT:  # row-fused launch: generated or nothing (rowfuse.py)
+            from .rowfuse import generate_source
+
+            return group, compile_cubin(generate_source(launches[group[0]].row_spec)), 0
         if len(group) == 1:
             g = generate(launches[group[0]].kind, args_of(group[0]), recs[group[0]].block[0])
         else:

@@ -515,8 +515,71 @@ def _run_launch(mem, L):
         run_tcgw(mem, L.args)
     elif L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128):
         run_tcgg(mem, L.args)
+    elif L.kind == abi.K_ROWJIT:
+        run_row(mem, L)
     else:
         raise NotImplementedError(L.kind)
+
+
+def run_row(mem, L):
+    """A row-fused launch (paper_1801_08058_b200/rowfuse.py) in reference
+    semantics: its value program over whole [R, C] arrays, row reductions
+    folded sequentially along the row, cross-row reductions sequentially in
+    row-major order.  The kernel's per-team partials are emulated as
+    (that full fold, then fold identities), so the second pass reproduces
+    the reference's single sequential fold exactly."""
+    spec, a = L.row_spec, L.args
+    dt = np.float32 if spec.dtype == "float" else np.float64
+    R, C = spec.R, spec.C
+    rows = np.arange(R, dtype=np.int64)[:, None]
+    cols = np.arange(C, dtype=np.int64)[None, :]
+
+    def fold_seq(kind, vals):  # vals [..., n]: fold along the last axis from the identity
+        acc = np.full(vals.shape[:-1], -np.inf if kind == 2 else 0.0, dtype=dt)
+        with np.errstate(all="ignore"):
+            for j in range(vals.shape[-1]):
+                v = vals[..., j]
+                acc = (np.where(acc >= v, acc, v) if kind == 2 else acc + v).astype(dt)
+        return acc
+
+    v = []
+    for cls, e in spec.values:
+        op = e[0]
+        if op == "imm":
+            raw = np.array([e[1]], dtype=np.uint64)
+            x = raw.astype(np.uint32).view(np.float32)[0] if dt == np.float32 else raw.view(np.float64)[0]
+            v.append(dt(x))
+        elif op == "loadu":
+            v.append(mem.view(a.refs[e[1]], dt)[0])
+        elif op == "load":
+            v.append(mem.view(a.refs[e[1]], dt)[rows * e[2] + cols * e[3]].copy())
+        elif op == "loadr":
+            v.append(mem.view(a.refs[e[1]], dt)[np.arange(R) * e[2]].copy())
+        elif op == "colv":
+            v.append(np.broadcast_to(mem.view(a.refs[e[1]], dt)[np.arange(C) * e[2]], (R, C)).copy())
+        elif op == "bcast":
+            x = v[e[1]]
+            v.append(np.broadcast_to(np.asarray(x)[:, None] if np.ndim(x) == 1 else x, (R, C) if cls == "full" else (R,)).astype(dt))
+        elif op == "un":
+            v.append(_un(e[1], np.asarray(v[e[2]], dtype=dt), dt))
+        elif op == "bin":
+            v.append(_bin(e[1], np.asarray(v[e[2]], dtype=dt), np.asarray(v[e[3]], dtype=dt), dt))
+        elif op == "rred":
+            v.append(fold_seq(e[1], v[e[2]]))
+        elif op == "xred":
+            v.append(fold_seq(e[1], np.asarray(v[e[2]]).reshape(1, -1))[0])
+        else:
+            raise ValueError(e)
+    for k, ref, s0, s1 in spec.stores:
+        x = v[k]
+        if np.ndim(x) == 2:
+            mem.view(a.refs[ref], dt)[rows * s0 + cols * s1] = x
+        else:
+            mem.view(a.refs[ref], dt)[np.arange(R) * s0] = x
+    for k, kind, ref in spec.xrow:
+        part = np.full(spec.n_teams, -np.inf if kind == 2 else 0.0, dtype=dt)
+        part[0] = v[k]
+        mem.view(a.refs[ref], dt)[: spec.n_teams] = part
 
 
 def allreduce_view(mem, a):

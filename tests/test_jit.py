@@ -32,7 +32,8 @@ def _plans():
         yield (host_compile(fn, conv_layout="nhwc" if case["name"].startswith("resnet") else "identity"),)
 
 
-def test_every_ew_launch_generates():
+def test_every_ew_launch_generates(monkeypatch):
+    monkeypatch.setenv("GFB_ROWFUSE", "0")  # the unfused plans: every VM mode appears
     n = modes = 0
     seen = set()
     for plans in _plans():
@@ -54,6 +55,7 @@ def test_nvrtc_compiles_sample(tmp_path, monkeypatch):
     except RuntimeError as exc:
         pytest.skip(str(exc))
     monkeypatch.setenv("GFB_JIT_CACHE", str(tmp_path))
+    monkeypatch.setenv("GFB_ROWFUSE", "0")
     picked = {}
     for plans in _plans():
         for h in plans:
@@ -107,6 +109,7 @@ def test_workload_jit_bit_identical(name, monkeypatch):
     tensors = [G.tensor_of(d) for d in case["inputs"]]
     layout = "nhwc" if name.startswith("resnet") else "identity"
     monkeypatch.setenv("GFB_JIT", "1")
+    monkeypatch.setenv("GFB_ROWFUSE", "0")  # row fusion changes the plan; it is tested in test_rowfuse.py
     monkeypatch.setenv("GFB_STAGED", "auto")  # the same plan with and without specialisation
     monkeypatch.setattr(jit, "MIN_BYTES", 0)
     exe, spec = _run(fn, tensors, layout)
@@ -123,6 +126,7 @@ def test_workload_jit_bit_identical(name, monkeypatch):
 @pytest.mark.gpu
 def test_corpus_jit_bit_identical(monkeypatch):
     monkeypatch.setenv("GFB_JIT", "1")
+    monkeypatch.setenv("GFB_ROWFUSE", "0")
     monkeypatch.setenv("GFB_STAGED", "auto")
     monkeypatch.setattr(jit, "MIN_BYTES", 0)
     cases = G.load("corpus.json.gz")[::4]

@@ -88,8 +88,10 @@ def test_tensor_core_lowering_emulated(monkeypatch, ta, tb):
 
 
 @pytest.mark.parametrize("shape,axes", [((3, 5000), (1,)), ((2, 300, 40), (1, 2)), ((70000,), (0,))])
-def test_chunkwise_reduction_emulated(shape, axes):
-    """Few long rows: staged chunk-wise partials + a second pass."""
+def test_chunkwise_reduction_emulated(shape, axes, monkeypatch):
+    """Few long rows: staged chunk-wise partials + a second pass (the row
+    fusion would otherwise take [3, 5000]: a small graph)."""
+    monkeypatch.setenv("GFB_ROWFUSE", "0")
     import paper_1801_08058_b200 as gf
     from oracle import interp
 
