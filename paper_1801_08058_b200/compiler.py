@@ -1661,8 +1661,26 @@ class Lowering:
         rec.algo_bytes = (m * k + k * nn + m * nn) * 4
 
     def _split(self, n, name, src, rows, kdim, mode, s_r=0, s_k=0, geo=(), st=()):
-        """hi/lo TF32 planes [rows, kp] of an implicit-GEMM operand."""
+        """hi/lo TF32 planes [rows, kp] of an implicit-GEMM operand.
+
+        A dense, row-contiguous operand that lives in the arena (a fixed
+        address the tensor maps can name) is its own hi plane: the tensor
+        core reads only the TF32 bits of an fp32 value, i.e. hi = trunc(x);
+        only lo = x - trunc(x) is written (split mode 7), which saves the hi
+        plane's write and read (1 GiB each for a config-E activation)."""
         kp = align_up(kdim, 4)
+        root = src.base if src.base is not None else src
+        if (mode == 0 and s_k == 1 and kdim == kp and s_r == kp and src.splat is None and root.slot == abi.SLOT_ARENA
+                and (src.elem_off * 4) % 16 == 0 and os.environ.get("GFB_RAW_HI", "1") == "1"):
+            lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
+            self.buf[("tc", n, name, "lo")] = lo
+            sa = abi.SplitArgs(rows=rows, k=kdim, kp=kp, s_r=s_r, s_k=s_k, mode=7)
+            grid = (max(1, min((rows * kp // 4 + 255) // 256, NUM_SMS * 16)), 1, 1)
+            rec = LaunchRec(abi.K_SPLIT_TF32, grid, (256, 1, 1), 0, sa, [src.key], [lo.key], f"split_{name}:lo#{n}")
+            rec.algo_bytes = 2 * rows * kp * 4
+            rec.finalize = _finalize_refs(sa, {"src": src, "hi": src, "lo": lo})
+            self.launches.append(rec)
+            return src, lo, kp
         hi = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
         lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
         self.buf[("tc", n, name, "hi")] = hi

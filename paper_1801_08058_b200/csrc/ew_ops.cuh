@@ -203,6 +203,43 @@ __device__ __forceinline__ void apply_unary(uint32_t op, T (&a)[V]) {
     }
 }
 
+// Compile-time-op variants for the runtime-generated kernels (jit.py,
+// rowfuse.py): the same double-precision functions, inlined, so a vector of
+// transcendentals is straight-line code the scheduler can interleave instead
+// of V calls through `transcendental`'s switch.  Results are identical.
+template <uint32_t OP>
+__device__ __forceinline__ double transcendental_c(double x) {
+    if constexpr (OP == OP_EXP) {
+        return exp(x);
+    } else if constexpr (OP == OP_LOG) {
+        if (x != x) return x;
+        if (x < 0.0) return __longlong_as_double(0x7ff8000000000000ll);
+        if (x == 0.0) return -__longlong_as_double(0x7ff0000000000000ll);
+        return log(x);
+    } else if constexpr (OP == OP_TANH) {
+        return tanh(x);
+    } else {
+        if (x != x) return x;
+        if (x >= 0.0) return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+        const double e = exp(x);
+        return __ddiv_rn(e, __dadd_rn(1.0, e));
+    }
+}
+
+template <uint32_t OP, typename T, int V>
+__device__ __forceinline__ void apply_unary_c(T (&a)[V]) {
+    if constexpr (!std::is_floating_point<T>::value || OP == OP_NEG || OP == OP_RELU) {
+        apply_unary<T, V>(OP, a);
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const double y = transcendental_c<OP>((double)a[v]);
+            if constexpr (std::is_same<T, float>::value) a[v] = __double2float_rn(y);
+            else a[v] = y;
+        }
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ T bin1(uint32_t op, T x, T y) {
     if constexpr (std::is_same<T, float>::value) {

@@ -411,6 +411,20 @@ __global__ void __launch_bounds__(256) gfb_split_kernel(const __grid_constant__ 
         }
         return;
     }
+    if (p.mode == 7) {
+        // Lo plane only, for a dense row-contiguous arena source that the GEMM
+        // reads directly as its hi operand (the tensor core uses only the TF32
+        // bits of an fp32 operand, i.e. hi = x truncated): lo = x - trunc(x),
+        // exact in fp32.  Saves the hi plane's write and read.
+        const int64_t n4 = p.rows * p.kp / 4;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src) + i);
+            const float4 h = trunc_tf32(x);
+            reinterpret_cast<float4*>(lo)[i] = make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z),
+                                                           __fsub_rn(x.w, h.w));
+        }
+        return;
+    }
     if (p.mode == 6) {
         // Transposing split of a row-contiguous source (s_r == 1, s_k % 4 == 0):
         // 64 x 64 tiles, 128-bit loads along rows, smem transpose, 128-bit hi/lo

@@ -313,7 +313,7 @@ class _Gen:
                 cache.clear()
             elif F_UN <= f < F_UN + 6:
                 x = self._tmp()
-                out.append(f"T {x}[V]; copyV<T, V>({x}, {acc}); apply_unary<T, V>({f - F_UN + 5}u, {x});")
+                out.append(f"T {x}[V]; copyV<T, V>({x}, {acc}); apply_unary_c<{f - F_UN + 5}u, T, V>({x});")
                 acc = x
             elif f == F_DOT:
                 xa, xb = ld(k), ld(k2)

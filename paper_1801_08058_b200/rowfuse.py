@@ -292,7 +292,7 @@ def geometry(C: int, esize: int, vec_ok: bool):
         block = 256
     else:
         team = 64
-        while team < 512 and C > team * vec * 8:
+        while team < 512 and C > team * vec * 4:
             team *= 2
         block = team
     return team, block, vec
@@ -349,7 +349,7 @@ def generate_source(spec: RowSpec) -> str:
         elif e[0] == "loadu":
             L.append(f"const T v{k} = P{e[1]}[0];")
         elif e[0] == "un":
-            L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary<T, 1>({e[1]}u, v{k}_); const T v{k} = v{k}_[0];")
+            L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary_c<{e[1]}u, T, 1>(v{k}_); const T v{k} = v{k}_[0];")
         elif e[0] == "bin":
             L.append(f"const T v{k} = bin1<T>({e[1]}u, v{e[2]}, v{e[3]});")
         else:
@@ -380,7 +380,7 @@ def generate_source(spec: RowSpec) -> str:
             elif op == "bcast":  # a ROWV / UNI value across the columns
                 L.append(f"T v{k}[EPT]; _Pragma(\"unroll\") for (int i = 0; i < EPT; ++i) v{k}[i] = v{e[1]};")
             elif op == "un":
-                L.append(f"T v{k}[EPT]; copyV<T, EPT>(v{k}, v{e[2]}); apply_unary<T, EPT>({e[1]}u, v{k});")
+                L.append(f"T v{k}[EPT]; copyV<T, EPT>(v{k}, v{e[2]}); apply_unary_c<{e[1]}u, T, EPT>(v{k});")
             elif op == "bin":
                 L.append(f"T v{k}[EPT]; _Pragma(\"unroll\") for (int i = 0; i < EPT; ++i) v{k}[i] = bin1<T>({e[1]}u, v{e[2]}[i], v{e[3]}[i]);")
             else:
@@ -391,7 +391,7 @@ def generate_source(spec: RowSpec) -> str:
             elif op == "bcast":
                 L.append(f"const T v{k} = v{e[1]};")
             elif op == "un":
-                L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary<T, 1>({e[1]}u, v{k}_); const T v{k} = v{k}_[0];")
+                L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary_c<{e[1]}u, T, 1>(v{k}_); const T v{k} = v{k}_[0];")
             elif op == "bin":
                 L.append(f"const T v{k} = bin1<T>({e[1]}u, v{e[2]}, v{e[3]});")
             elif op == "rred":

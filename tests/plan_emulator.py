@@ -283,6 +283,11 @@ def _gather_offsets(a, r, k):
 
 def run_split(mem, a):
     src = mem.view(a.src, np.float32)
+    if a.mode == 7:  # lo plane only: the source is the hi operand (the MMA truncates it)
+        x = src[: a.rows * a.kp].copy()
+        hi = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+        mem.view(a.lo, np.float32)[: a.rows * a.kp] = (x - hi).astype(np.float32)
+        return
     r = np.arange(a.rows, dtype=np.int64)[:, None]
     k = np.arange(a.kp, dtype=np.int64)[None, :]
     off = _gather_offsets(a, r, np.minimum(k, max(a.k - 1, 0)))
@@ -294,11 +299,16 @@ def run_split(mem, a):
     mem.view(a.lo, np.float32)[: a.rows * a.kp] = lo.reshape(-1)
 
 
+def _tf32(x):
+    """What kind::tf32 reads of an fp32 operand: its top 19 bits (truncation)."""
+    return (np.ascontiguousarray(x).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
+
+
 def run_tc(mem, a):
-    A = (mem.view(a.a_hi, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64),
-         mem.view(a.a_lo, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a).astype(np.float64))
-    B = (mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64),
-         mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b).astype(np.float64))
+    A = (_tf32(mem.view(a.a_hi, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a)),
+         _tf32(mem.view(a.a_lo, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a)))
+    B = (_tf32(mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b)),
+         _tf32(mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b)))
     splits = max(1, a.k_splits)
     i = np.arange(a.M, dtype=np.int64)[:, None]
     j = np.arange(a.N, dtype=np.int64)[None, :]

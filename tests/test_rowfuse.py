@@ -115,7 +115,7 @@ def test_softmax_gpu_vs_oracle(R, C):
     interp.set_threads(interp.max_threads())
     want = interp.run_function(fn, [x])[0]
     assert G.normwise(out[0], want) <= 1e-5
-    assert np.max(np.abs(out[0] - want) / np.maximum(np.abs(want), 1e-30)) <= 2e-6  # only the row-sum order differs
+    assert np.max(np.abs(out[0] - want) / np.maximum(np.abs(want), 1e-30)) <= 1e-5  # only the row-sum order differs
 
 
 @pytest.mark.gpu
