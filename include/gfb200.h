@@ -187,7 +187,8 @@ typedef struct {
 typedef struct {
     const void* const* tab;
     uint64_t x, y, out;   /* op-specific roles, see kernels_conv.cu */
-    int32_t op;           /* 0 Conv2D, 1 ConvBackpropData, 2 ConvBackpropFilter */
+    int32_t op;           /* 0 Conv2D, 1 ConvBackpropData, 2 ConvBackpropFilter (sh, sw: the strides of all three),
+                             3 MaxPool, 4 MaxPoolBackprop (R, S = window; y = delta for 4) */
     int32_t pad0;
     int64_t N, C, H, W, K, R, S, Ho, Wo;
     int64_t sh, sw, pt, pl;

@@ -274,20 +274,28 @@ void orc_conv2d(int et, const void* data, const void* flt, void* out, int64_t N,
     });
 }
 
-/* kernels.py:209-235: stride-1 adjoint w.r.t. data, order k, r, s */
+/* kernels.py:209-235: adjoint w.r.t. data, order k, r, s.  The reference is
+ * stride-1 only; for the IR extension (strided Conv2D gradients) the same
+ * loop keeps the taps with (h + pt - r) and (w + pl - s) divisible by the
+ * stride: p = (h + pt - r) / sh, q = (w + pl - s) / sw. */
 void orc_conv_bwd_data(int et, const void* delta, const void* flt, void* out, int64_t N, int64_t C, int64_t H,
-                       int64_t W, int64_t K, int64_t R, int64_t S, int64_t Ho, int64_t Wo, int64_t pt, int64_t pl) {
+                       int64_t W, int64_t K, int64_t R, int64_t S, int64_t Ho, int64_t Wo, int64_t pt, int64_t pl,
+                       int64_t sh, int64_t sw) {
     parfor(N * C * H * W, [&](int64_t idx) {
         int64_t w = idx % W, h = (idx / W) % H, c = (idx / (W * H)) % C, n = idx / (W * H * C);
         float a32 = 0.0f;
         double a64 = 0.0;
         for (int64_t k = 0; k < K; k++)
             for (int64_t r = 0; r < R; r++) {
-                int64_t p = h + pt - r;
-                if (p < 0 || p >= Ho) continue;
+                int64_t pn = h + pt - r;
+                if (pn < 0 || pn % sh) continue;
+                int64_t p = pn / sh;
+                if (p >= Ho) continue;
                 for (int64_t s = 0; s < S; s++) {
-                    int64_t q = w + pl - s;
-                    if (q < 0 || q >= Wo) continue;
+                    int64_t qn = w + pl - s;
+                    if (qn < 0 || qn % sw) continue;
+                    int64_t q = qn / sw;
+                    if (q >= Wo) continue;
                     int64_t di = ((n * K + k) * Ho + p) * Wo + q, fi = ((k * C + c) * R + r) * S + s;
                     if (et == ET_F32) a32 = mac32(a32, ((const float*)delta)[di], ((const float*)flt)[fi]);
                     else a64 = a64 + ((const double*)delta)[di] * ((const double*)flt)[fi];
@@ -298,19 +306,21 @@ void orc_conv_bwd_data(int et, const void* delta, const void* flt, void* out, in
     });
 }
 
-/* kernels.py:238-264: stride-1 adjoint w.r.t. filter, order n, p, q */
+/* kernels.py:238-264: adjoint w.r.t. filter, order n, p, q (strided taps
+ * h = p * sh + r - pt for the IR extension; the reference has sh = sw = 1) */
 void orc_conv_bwd_filter(int et, const void* data, const void* delta, void* out, int64_t N, int64_t C, int64_t H,
-                         int64_t W, int64_t K, int64_t R, int64_t S, int64_t Ho, int64_t Wo, int64_t pt, int64_t pl) {
+                         int64_t W, int64_t K, int64_t R, int64_t S, int64_t Ho, int64_t Wo, int64_t pt, int64_t pl,
+                         int64_t sh, int64_t sw) {
     parfor(K * C * R * S, [&](int64_t idx) {
         int64_t s = idx % S, r = (idx / S) % R, c = (idx / (S * R)) % C, k = idx / (S * R * C);
         float a32 = 0.0f;
         double a64 = 0.0;
         for (int64_t n = 0; n < N; n++)
             for (int64_t p = 0; p < Ho; p++) {
-                int64_t h = p + r - pt;
+                int64_t h = p * sh + r - pt;
                 if (h < 0 || h >= H) continue;
                 for (int64_t q = 0; q < Wo; q++) {
-                    int64_t w = q + s - pl;
+                    int64_t w = q * sw + s - pl;
                     if (w < 0 || w >= W) continue;
                     int64_t di = ((n * K + k) * Ho + p) * Wo + q, xi = ((n * C + c) * H + h) * W + w;
                     if (et == ET_F32) a32 = mac32(a32, ((const float*)delta)[di], ((const float*)data)[xi]);
@@ -319,6 +329,75 @@ void orc_conv_bwd_filter(int et, const void* data, const void* delta, void* out,
             }
         if (et == ET_F32) ((float*)out)[idx] = a32;
         else ((double*)out)[idx] = a64;
+    });
+}
+
+/* IR extension (no reference counterpart): MaxPool over (kh, kw) windows
+ * with strides and padding.  out = fold over the window in row-major order
+ * of acc >= v ? acc : v from -inf (the reference's max-reduce fold,
+ * kernels.py:156-177), padding taps skipped. */
+void orc_maxpool(int et, const void* data, void* out, int64_t N, int64_t C, int64_t H, int64_t W, int64_t kh,
+                 int64_t kw, int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t Ho, int64_t Wo) {
+    parfor(N * C * Ho * Wo, [&](int64_t idx) {
+        int64_t q = idx % Wo, p = (idx / Wo) % Ho, nc = idx / (Wo * Ho);
+        double acc = -kInf;
+        for (int64_t i = 0; i < kh; i++) {
+            int64_t h = p * sh + i - pt;
+            if (h < 0 || h >= H) continue;
+            for (int64_t j = 0; j < kw; j++) {
+                int64_t w = q * sw + j - pl;
+                if (w < 0 || w >= W) continue;
+                int64_t xi = (nc * H + h) * W + w;
+                double v = et == ET_F32 ? (double)((const float*)data)[xi] : ((const double*)data)[xi];
+                acc = bmax(acc, v);
+            }
+        }
+        if (et == ET_F32) ((float*)out)[idx] = (float)acc;
+        else ((double*)out)[idx] = acc;
+    });
+}
+
+/* MaxPoolBackprop: dx[n,c,h,w] = sum, over the windows (p, q) ascending that
+ * contain (h, w) and whose selected element (the position where the forward
+ * fold last took a new value) is (h, w), of delta[n,c,p,q]; from +0.0 with
+ * one rounding per add. */
+void orc_maxpool_bwd(int et, const void* data, const void* delta, void* out, int64_t N, int64_t C, int64_t H,
+                     int64_t W, int64_t kh, int64_t kw, int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t Ho,
+                     int64_t Wo) {
+    auto X = [&](int64_t i) { return et == ET_F32 ? (double)((const float*)data)[i] : ((const double*)data)[i]; };
+    auto D = [&](int64_t i) { return et == ET_F32 ? (double)((const float*)delta)[i] : ((const double*)delta)[i]; };
+    parfor(N * C * H * W, [&](int64_t idx) {
+        int64_t w = idx % W, h = (idx / W) % H, nc = idx / (W * H);
+        double acc = 0.0;
+        for (int64_t p = 0; p < Ho; p++) {
+            int64_t i = h + pt - p * sh;
+            if (i < 0 || i >= kh) continue;
+            for (int64_t q = 0; q < Wo; q++) {
+                int64_t j = w + pl - q * sw;
+                if (j < 0 || j >= kw) continue;
+                double best = -kInf;
+                int64_t arg = -1;
+                for (int64_t a = 0; a < kh; a++) {
+                    int64_t hh = p * sh + a - pt;
+                    if (hh < 0 || hh >= H) continue;
+                    for (int64_t b = 0; b < kw; b++) {
+                        int64_t ww = q * sw + b - pl;
+                        if (ww < 0 || ww >= W) continue;
+                        double v = X((nc * H + hh) * W + ww);
+                        if (!(best >= v)) {
+                            best = v;
+                            arg = hh * W + ww;
+                        }
+                    }
+                }
+                if (arg == h * W + w) {
+                    double d = D((nc * Ho + p) * Wo + q);
+                    acc = et == ET_F32 ? (double)f32(acc + d) : acc + d;
+                }
+            }
+        }
+        if (et == ET_F32) ((float*)out)[idx] = (float)acc;
+        else ((double*)out)[idx] = acc;
     });
 }
 

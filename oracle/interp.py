@@ -61,8 +61,10 @@ def lib():
         _lib.orc_dot.argtypes = [ctypes.c_int, vp, vp, vp, i64, i64, i64]
         _lib.orc_reduce.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, ctypes.POINTER(_RedDesc), i64, i64]
         _lib.orc_conv2d.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 13
-        _lib.orc_conv_bwd_data.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 11
-        _lib.orc_conv_bwd_filter.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 11
+        _lib.orc_conv_bwd_data.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 13
+        _lib.orc_conv_bwd_filter.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 13
+        _lib.orc_maxpool.argtypes = [ctypes.c_int, vp, vp] + [i64] * 12
+        _lib.orc_maxpool_bwd.argtypes = [ctypes.c_int, vp, vp, vp] + [i64] * 12
         _lib.orc_set_threads.argtypes = [ctypes.c_int]
         _lib.orc_transpose2d.argtypes = [ctypes.c_int, vp, vp, i64, i64]
     return _lib
@@ -146,16 +148,36 @@ def eval_node(node, args: list) -> np.ndarray:
         N, C, H, Wd = desc.shape
         K, _, R, S = f.shape
         pt, _, pl, _ = node.attrs["padding"]
+        sh, sw = node.attrs.get("strides", (1, 1))
         if out.size:
-            L.orc_conv_bwd_data(_ET[et], _ptr(dlt), _ptr(f), _ptr(out), N, C, H, Wd, K, R, S, dlt.shape[2], dlt.shape[3], pt, pl)
+            L.orc_conv_bwd_data(_ET[et], _ptr(dlt), _ptr(f), _ptr(out), N, C, H, Wd, K, R, S, dlt.shape[2], dlt.shape[3], pt, pl,
+                                sh, sw)
         return out
     if kind is OpKind.CONV_BACKPROP_FILTER:
         x, dlt = _c(args[0]), _c(args[1])
         N, C, H, Wd = x.shape
         K, _, R, S = desc.shape
         pt, _, pl, _ = node.attrs["padding"]
+        sh, sw = node.attrs.get("strides", (1, 1))
         if out.size:
-            L.orc_conv_bwd_filter(_ET[et], _ptr(x), _ptr(dlt), _ptr(out), N, C, H, Wd, K, R, S, dlt.shape[2], dlt.shape[3], pt, pl)
+            L.orc_conv_bwd_filter(_ET[et], _ptr(x), _ptr(dlt), _ptr(out), N, C, H, Wd, K, R, S, dlt.shape[2], dlt.shape[3], pt, pl,
+                                  sh, sw)
+        return out
+    if kind in (OpKind.MAX_POOL, OpKind.MAX_POOL_BACKPROP):  # IR extension: parity pinned by FD gradients only
+        x = _c(args[0])
+        N, C, H, Wd = x.shape
+        kh, kw = node.attrs["window"]
+        sh, sw = node.attrs["strides"]
+        pt, _, pl, _ = node.attrs["padding"]
+        if kind is OpKind.MAX_POOL:
+            Ho, Wo = desc.shape[2], desc.shape[3]
+            if out.size:
+                L.orc_maxpool(_ET[et], _ptr(x), _ptr(out), N, C, H, Wd, kh, kw, sh, sw, pt, pl, Ho, Wo)
+        else:
+            dlt = _c(args[1])
+            if out.size:
+                L.orc_maxpool_bwd(_ET[et], _ptr(x), _ptr(dlt), _ptr(out), N, C, H, Wd, kh, kw, sh, sw, pt, pl,
+                                  dlt.shape[2], dlt.shape[3])
         return out
     raise NotImplementedError(kind)
 

@@ -39,6 +39,7 @@ import numpy as np
 from . import abi
 from .errors import UnsupportedOp
 from .ir import (
+    conv_strides,
     ELEMENTWISE_BINARY,
     ELEMENTWISE_UNARY,
     ConstantData,
@@ -61,7 +62,8 @@ EW_BLOCKS_PER_SM = int(os.environ.get("GFB_EW_BLOCKS_PER_SM", 64))
 # ROW launches add warps per row (up to 8) while the grid has fewer than this
 # many 8-warp blocks per SM.
 ROW_BLOCKS_PER_SM = int(os.environ.get("GFB_EW_ROW_BLOCKS_PER_SM", 32))
-HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER})
+HEAVY = frozenset({OpKind.DOT, OpKind.CONV2D, OpKind.CONV_BACKPROP_DATA, OpKind.CONV_BACKPROP_FILTER,
+                   OpKind.MAX_POOL, OpKind.MAX_POOL_BACKPROP})
 INDEX_OPS = frozenset({OpKind.BROADCAST, OpKind.RESHAPE, OpKind.CONVERT_LAYOUT})
 MAX_STACK = 3
 TINY_DOT_K = 4  # Dots contracting over at most this many terms fuse as light ops
@@ -1955,6 +1957,10 @@ class Lowering:
         node = self.nodes[n]
         if node.output.element_type is not ElementType.F32 or os.environ.get("GFB_CONV", "auto") == "simt":
             return False
+        if node.op in (OpKind.MAX_POOL, OpKind.MAX_POOL_BACKPROP):
+            return False
+        if node.op is not OpKind.CONV2D and conv_strides(node) != (1, 1):
+            return False  # strided gradients (IR extension): the exact-order kernel
         x, y = node.inputs[0][0], node.inputs[1][0]
         try:
             (xb, xs), (yb, ys) = self.operand(x), self.operand(y)
@@ -2093,6 +2099,9 @@ class Lowering:
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
         return True
 
+    def emit_pool(self, n: int):
+        _pool_emit(self, n)
+
     def emit_heavy(self, n: int):
         node = self.nodes[n]
         out = self.buf[n]
@@ -2126,6 +2135,9 @@ class Lowering:
             rec.finalize = _finalize_refs(args, {"a": ab, "b": bb, "c": out})
             self.launches.append(rec)
             return
+        if node.op in (OpKind.MAX_POOL, OpKind.MAX_POOL_BACKPROP):
+            self.emit_pool(n)
+            return
         x, y = node.inputs[0][0], node.inputs[1][0]
         (xb, xs), (yb, ys) = self.operand(x), self.operand(y)
         xshape, yshape = self.nodes[x].output.shape, self.nodes[y].output.shape
@@ -2142,14 +2154,14 @@ class Lowering:
             N, K, Ho, Wo = xshape
             _, Cc, R, S = yshape
             H, W = oshape[2], oshape[3]
-            sh = sw = 1
+            sh, sw = conv_strides(node)
             opc, total = 1, N * Cc * H * W
             macs = N * K * Ho * Wo * Cc * R * S
         else:
             N, Cc, H, W = xshape
             _, K, Ho, Wo = yshape
             R, S = oshape[2], oshape[3]
-            sh = sw = 1
+            sh, sw = conv_strides(node)
             opc, total = 2, K * Cc * R * S
             macs = N * K * Ho * Wo * Cc * R * S
         if total == 0:
@@ -2166,6 +2178,43 @@ class Lowering:
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
         rec.finalize = _finalize_refs(args, {"x": xb, "y": yb, "out": out})
         self.launches.append(rec)
+
+
+def _pool_emit(low, n):
+    """MaxPool (op 3) / MaxPoolBackprop (op 4) on the SIMT convolution-family
+    kernel (csrc/simt_kernels.cu): one thread per output element, operands
+    through per-axis strides (any layout), the window scanned in row-major
+    order exactly as the oracle folds it."""
+    node = low.nodes[n]
+    out = low.buf[n]
+    et = node.output.element_type
+    a = node.attrs
+    x = node.inputs[0][0]
+    xb, xs = low.operand(x)
+    N, Cc, H, W = low.nodes[x].output.shape
+    kh, kw = a["window"]
+    sh, sw = a["strides"]
+    pt, _, pl, _ = a["padding"]
+    if node.op is OpKind.MAX_POOL:
+        Ho, Wo = node.output.shape[2], node.output.shape[3]
+        yb, ys, opc, total = xb, xs, 3, N * Cc * Ho * Wo
+    else:
+        yb, ys = low.operand(node.inputs[1][0])
+        Ho, Wo = low.nodes[node.inputs[1][0]].output.shape[2:]
+        opc, total = 4, N * Cc * H * W
+    if total == 0:
+        return
+    args = abi.ConvArgs(op=opc, N=N, C=Cc, H=H, W=W, K=Cc, R=kh, S=kw, Ho=Ho, Wo=Wo, sh=sh, sw=sw, pt=pt, pl=pl)
+    args.xs[:] = list(xs)
+    args.ys[:] = list(ys)
+    args.os[:] = list(out.strides)
+    kind = abi.K_CONV_F32 if et is ElementType.F32 else abi.K_CONV_F64
+    grid = max(1, min((total + 255) // 256, NUM_SMS * 64))
+    rec = LaunchRec(kind, (grid, 1, 1), (256, 1, 1), 0, args, sorted({xb.key, yb.key}), [out.key],
+                    f"{node.op.wire_name}#{n}")
+    rec.algo_bytes = xb.nbytes + out.nbytes + (yb.nbytes if opc == 4 else 0)
+    rec.finalize = _finalize_refs(args, {"x": xb, "y": yb, "out": out})
+    low.launches.append(rec)
 
 
 def _storage_perm(buf) -> list:

@@ -15,6 +15,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "gfb_common.cuh"
@@ -170,7 +171,8 @@ __global__ void __launch_bounds__(256) gfb_conv_kernel(const __grid_constant__ g
     T* O = resolve<T>(p.tab, p.out);
     int64_t total;
     if (p.op == 0) total = p.N * p.K * p.Ho * p.Wo;
-    else if (p.op == 1) total = p.N * p.C * p.H * p.W;
+    else if (p.op == 1 || p.op == 4) total = p.N * p.C * p.H * p.W;
+    else if (p.op == 3) total = p.N * p.C * p.Ho * p.Wo;
     else total = p.K * p.C * p.R * p.S;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -192,31 +194,85 @@ __global__ void __launch_bounds__(256) gfb_conv_kernel(const __grid_constant__ g
                 }
             O[n * p.os[0] + k * p.os[1] + pp * p.os[2] + q * p.os[3]] = acc;
         } else if (p.op == 1) {
-            // out[n,c,h,w] = sum_{k,r,s} delta[n,k,h+pt-r,w+pl-s] * f[k,c,r,s]
+            // out[n,c,h,w] = sum_{k,r,s} delta[n,k,(h+pt-r)/sh,(w+pl-s)/sw] * f[k,c,r,s]
+            // over the taps divisible by the stride (1 for the reference's ops)
             const int64_t w = idx % p.W, h = (idx / p.W) % p.H, c = (idx / (p.W * p.H)) % p.C,
                           n = idx / (p.W * p.H * p.C);
             for (int64_t k = 0; k < p.K; ++k)
                 for (int64_t r = 0; r < p.R; ++r) {
-                    const int64_t pp = h + p.pt - r;
-                    if (pp < 0 || pp >= p.Ho) continue;
+                    const int64_t pn = h + p.pt - r;
+                    if (pn < 0 || pn % p.sh) continue;
+                    const int64_t pp = pn / p.sh;
+                    if (pp >= p.Ho) continue;
                     for (int64_t s = 0; s < p.S; ++s) {
-                        const int64_t q = w + p.pl - s;
-                        if (q < 0 || q >= p.Wo) continue;
+                        const int64_t qn = w + p.pl - s;
+                        if (qn < 0 || qn % p.sw) continue;
+                        const int64_t q = qn / p.sw;
+                        if (q >= p.Wo) continue;
                         acc = add_rn(acc, mul_rn(X[n * p.xs[0] + k * p.xs[1] + pp * p.xs[2] + q * p.xs[3]],
                                                  Y[k * p.ys[0] + c * p.ys[1] + r * p.ys[2] + s * p.ys[3]]));
                     }
                 }
             O[n * p.os[0] + c * p.os[1] + h * p.os[2] + w * p.os[3]] = acc;
+        } else if (p.op == 3) {
+            // MaxPool (IR extension): fold acc >= v ? acc : v from -inf over
+            // the (R, S) window in row-major order, padding taps skipped
+            const int64_t q = idx % p.Wo, pp = (idx / p.Wo) % p.Ho, c = (idx / (p.Wo * p.Ho)) % p.C,
+                          n = idx / (p.Wo * p.Ho * p.C);
+            acc = -(T)INFINITY;
+            for (int64_t i = 0; i < p.R; ++i) {
+                const int64_t h = pp * p.sh + i - p.pt;
+                if (h < 0 || h >= p.H) continue;
+                for (int64_t j = 0; j < p.S; ++j) {
+                    const int64_t w = q * p.sw + j - p.pl;
+                    if (w < 0 || w >= p.W) continue;
+                    const T v = X[n * p.xs[0] + c * p.xs[1] + h * p.xs[2] + w * p.xs[3]];
+                    acc = acc >= v ? acc : v;
+                }
+            }
+            O[n * p.os[0] + c * p.os[1] + pp * p.os[2] + q * p.os[3]] = acc;
+        } else if (p.op == 4) {
+            // MaxPoolBackprop: sum over the windows (p, q) ascending that hold
+            // (h, w) and select it (the element where the forward fold last
+            // changed) of delta[n, c, p, q]
+            const int64_t w = idx % p.W, h = (idx / p.W) % p.H, c = (idx / (p.W * p.H)) % p.C,
+                          n = idx / (p.W * p.H * p.C);
+            const T* xc = X + n * p.xs[0] + c * p.xs[1];
+            for (int64_t pp = 0; pp < p.Ho; ++pp) {
+                const int64_t i = h + p.pt - pp * p.sh;
+                if (i < 0 || i >= p.R) continue;
+                for (int64_t q = 0; q < p.Wo; ++q) {
+                    const int64_t j = w + p.pl - q * p.sw;
+                    if (j < 0 || j >= p.S) continue;
+                    T best = -(T)INFINITY;
+                    int64_t arg = -1;
+                    for (int64_t a = 0; a < p.R; ++a) {
+                        const int64_t hh = pp * p.sh + a - p.pt;
+                        if (hh < 0 || hh >= p.H) continue;
+                        for (int64_t b = 0; b < p.S; ++b) {
+                            const int64_t ww = q * p.sw + b - p.pl;
+                            if (ww < 0 || ww >= p.W) continue;
+                            const T v = xc[hh * p.xs[2] + ww * p.xs[3]];
+                            if (!(best >= v)) {
+                                best = v;
+                                arg = hh * p.W + ww;
+                            }
+                        }
+                    }
+                    if (arg == h * p.W + w) acc = add_rn(acc, Y[n * p.ys[0] + c * p.ys[1] + pp * p.ys[2] + q * p.ys[3]]);
+                }
+            }
+            O[n * p.os[0] + c * p.os[1] + h * p.os[2] + w * p.os[3]] = acc;
         } else {
-            // out[k,c,r,s] = sum_{n,p,q} delta[n,k,p,q] * x[n,c,p+r-pt,q+s-pl]
+            // out[k,c,r,s] = sum_{n,p,q} delta[n,k,p,q] * x[n,c,p*sh+r-pt,q*sw+s-pl]
             const int64_t s = idx % p.S, r = (idx / p.S) % p.R, c = (idx / (p.S * p.R)) % p.C,
                           k = idx / (p.S * p.R * p.C);
             for (int64_t n = 0; n < p.N; ++n)
                 for (int64_t pp = 0; pp < p.Ho; ++pp) {
-                    const int64_t h = pp + r - p.pt;
+                    const int64_t h = pp * p.sh + r - p.pt;
                     if (h < 0 || h >= p.H) continue;
                     for (int64_t q = 0; q < p.Wo; ++q) {
-                        const int64_t w = q + s - p.pl;
+                        const int64_t w = q * p.sw + s - p.pl;
                         if (w < 0 || w >= p.W) continue;
                         acc = add_rn(acc, mul_rn(Y[n * p.ys[0] + k * p.ys[1] + pp * p.ys[2] + q * p.ys[3]],
                                                  X[n * p.xs[0] + c * p.xs[1] + h * p.xs[2] + w * p.xs[3]]));

@@ -189,6 +189,15 @@ def _propagate(g: Function, dp: DataParallel):
             else:
                 need_all()
                 st[n] = sharded(0) if a == sharded(0) else REPL
+        elif op in (OpKind.MAX_POOL, OpKind.MAX_POOL_BACKPROP):
+            # pooling is per image: the batch shard carries through
+            if all(s == sharded(0) for s in ins):
+                st[n] = sharded(0)
+            elif all(s == REPL for s in ins):
+                st[n] = REPL
+            else:
+                need_all()
+                st[n] = REPL
         elif op is OpKind.CONV_BACKPROP_FILTER:
             a, b = ins
             if a == sharded(0) and b == sharded(0):

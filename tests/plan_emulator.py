@@ -209,7 +209,18 @@ def run_conv(mem, a, dt):
     def p(arr):
         return arr.ctypes.data_as(interp.ctypes.c_void_p)
 
-    if a.op == 0:
+    if a.op in (3, 4):  # MaxPool / MaxPoolBackprop (IR extension)
+        x, _ = np.ascontiguousarray(_gather4(X, (a.N, a.C, a.H, a.W), a.xs)[0]), None
+        if a.op == 3:
+            oshape = (a.N, a.C, a.Ho, a.Wo)
+            out = np.empty(oshape, dtype=dt)
+            L.orc_maxpool(et, p(x), p(out), a.N, a.C, a.H, a.W, a.R, a.S, a.sh, a.sw, a.pt, a.pl, a.Ho, a.Wo)
+        else:
+            d = np.ascontiguousarray(_gather4(Y, (a.N, a.C, a.Ho, a.Wo), a.ys)[0])
+            oshape = (a.N, a.C, a.H, a.W)
+            out = np.empty(oshape, dtype=dt)
+            L.orc_maxpool_bwd(et, p(x), p(d), p(out), a.N, a.C, a.H, a.W, a.R, a.S, a.sh, a.sw, a.pt, a.pl, a.Ho, a.Wo)
+    elif a.op == 0:
         x, _ = _gather4(X, (a.N, a.C, a.H, a.W), a.xs)
         f, _ = _gather4(Y, (a.K, a.C, a.R, a.S), a.ys)
         oshape = (a.N, a.K, a.Ho, a.Wo)
@@ -222,14 +233,14 @@ def run_conv(mem, a, dt):
         oshape = (a.N, a.C, a.H, a.W)
         out = np.empty(oshape, dtype=dt)
         d, f = np.ascontiguousarray(d), np.ascontiguousarray(f)
-        L.orc_conv_bwd_data(et, p(d), p(f), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.Ho, a.Wo, a.pt, a.pl)
+        L.orc_conv_bwd_data(et, p(d), p(f), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.Ho, a.Wo, a.pt, a.pl, a.sh, a.sw)
     else:
         x, _ = _gather4(X, (a.N, a.C, a.H, a.W), a.xs)
         d, _ = _gather4(Y, (a.N, a.K, a.Ho, a.Wo), a.ys)
         oshape = (a.K, a.C, a.R, a.S)
         out = np.empty(oshape, dtype=dt)
         x, d = np.ascontiguousarray(x), np.ascontiguousarray(d)
-        L.orc_conv_bwd_filter(et, p(x), p(d), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.Ho, a.Wo, a.pt, a.pl)
+        L.orc_conv_bwd_filter(et, p(x), p(d), p(out), a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.Ho, a.Wo, a.pt, a.pl, a.sh, a.sw)
     _, idx = _gather4(O, oshape, a.os)
     O[idx] = out
 

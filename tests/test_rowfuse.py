@@ -114,8 +114,14 @@ def test_softmax_gpu_vs_oracle(R, C):
     assert any(L.kind == abi.K_ROWJIT for L in exe.lowered.launches)
     interp.set_threads(interp.max_threads())
     want = interp.run_function(fn, [x])[0]
-    assert G.normwise(out[0], want) <= 1e-5
-    assert np.max(np.abs(out[0] - want) / np.maximum(np.abs(want), 1e-30)) <= 1e-5  # only the row-sum order differs
+    # the reference's sequential fp32 row sums carry ~sqrt(C) * 2^-24 of error
+    # themselves: compare both against the exact softmax (float64)
+    x64 = x.astype(np.float64)
+    e = np.exp(x64 - x64.max(axis=1, keepdims=True))
+    exact = e / e.sum(axis=1, keepdims=True)
+    assert G.normwise(out[0], exact) <= 1e-5
+    assert G.normwise(out[0], exact) <= G.normwise(want, exact) + 1e-6
+    assert np.max(np.abs(out[0] - exact) / exact) <= 1e-5  # elementwise, not only normwise
 
 
 @pytest.mark.gpu
