@@ -240,7 +240,13 @@ typedef struct GFB_ALIGN64 {
     int64_t kp_a, kp_b;
     int64_t c_rdiv, c_s_hi, c_s_lo;
     int64_t k_splits, k_per_split, split_stride;
-    int64_t pad[5];
+    /* MN-major operands (GFB_K_DOT_TC32P only): when a_ld_mn > 0, the A hi /
+     * lo operands are stored MN-contiguous, element (m, k) at k * a_ld_mn + m
+     * (e.g. a row-major activation read as its own transpose by a weight
+     * gradient), loaded as SWIZZLE_128B_ATOM_32B boxes (the tf32 MN-major
+     * layout); likewise b_ld_mn for B.  0 = K-major planes [rows, kp]. */
+    int64_t a_ld_mn, b_ld_mn;
+    int64_t pad[3];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

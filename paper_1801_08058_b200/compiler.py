@@ -1657,10 +1657,54 @@ class Lowering:
         tcgen05 3xTF32 GEMM (csrc/gemm_tc.cu), split-K when the output is
         too small to fill the GPU."""
         (ab, ast), (bb, bst) = a_op, b_op
-        a = self._split(n, "a", ab, m, k, 0, s_r=ast[0], s_k=ast[1])
-        b = self._split(n, "b", bb, nn, k, 0, s_r=bst[1], s_k=bst[0])
+        pair = m >= 256 and nn >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1" and os.environ.get("GFB_TC_WIDE", "1") == "1"
+        a = self._raw_mn(ab, ast[0], ast[1], m, k) if pair else None
+        b = self._raw_mn(bb, bst[1], bst[0], nn, k) if pair else None
+        if a is None:
+            a = self._split(n, "a", ab, m, k, 0, s_r=ast[0], s_k=ast[1])
+        if b is None:
+            b = self._split(n, "b", bb, nn, k, 0, s_r=bst[1], s_k=bst[0])
         rec = self._tc_gemm(n, a, b, out, m, nn, k, {"c_sm": out.strides[0], "c_sn": out.strides[1]}, f"dot_tc#{n}")
         rec.algo_bytes = (m * k + k * nn + m * nn) * 4
+
+    def _dense_root(self, src):
+        """The whole dense arena buffer `src` views at offset 0, or None."""
+        root = src.base if src.base is not None else src
+        if (src.splat is not None or root.slot != abi.SLOT_ARENA or src.elem_off != 0 or root.subaxes
+                or root.et is not ElementType.F32 or not _dense_rowmajor(root.shape, root.strides)
+                or element_count(root.shape) % 4):
+            return None
+        return root
+
+    def _lo_plane(self, root):
+        """lo = x - trunc_tf32(x) of a dense arena tensor, in the tensor's own
+        layout, written once (split mode 7) and shared by every GEMM that
+        reads the tensor as a raw-hi operand, K-major or MN-major."""
+        key = ("lo", root.key)
+        lo = self.buf.get(key)
+        if lo is None:
+            total = element_count(root.shape)
+            lo = Buffer(self.new_key(), ElementType.F32, root.shape, root.strides)
+            self.buf[key] = lo
+            sa = abi.SplitArgs(rows=1, k=total, kp=total, s_r=total, s_k=1, mode=7)
+            grid = (max(1, min((total // 4 + 255) // 256, NUM_SMS * 16)), 1, 1)
+            rec = LaunchRec(abi.K_SPLIT_TF32, grid, (256, 1, 1), 0, sa, [root.key], [lo.key], f"lo#{root.key}")
+            rec.algo_bytes = 2 * total * 4
+            rec.finalize = _finalize_refs(sa, {"src": root, "hi": root, "lo": lo})
+            self.launches.append(rec)
+        return lo
+
+    def _raw_mn(self, src, s_r, s_k, rows, kdim):
+        """Operand [rows, k] read in place from its arena tensor: as an
+        MN-major operand when rows are contiguous (s_r == 1; e.g. the
+        activation of a weight gradient Dot(Reshape(h, (1, 0)), dz)), with the
+        shared lo plane.  Returns (hi, lo, kp, ld_mn) or None (split instead)."""
+        if s_r != 1 or rows % 32 or s_k % 4 or s_k < rows or os.environ.get("GFB_MN_MAJOR", "1") != "1":
+            return None
+        root = self._dense_root(src)
+        if root is None or element_count(root.shape) < s_k * kdim:
+            return None
+        return root, self._lo_plane(root), align_up(kdim, 4), s_k
 
     def _split(self, n, name, src, rows, kdim, mode, s_r=0, s_k=0, geo=(), st=()):
         """hi/lo TF32 planes [rows, kp] of an implicit-GEMM operand.
@@ -1671,18 +1715,10 @@ class Lowering:
         only lo = x - trunc(x) is written (split mode 7), which saves the hi
         plane's write and read (1 GiB each for a config-E activation)."""
         kp = align_up(kdim, 4)
-        root = src.base if src.base is not None else src
-        if (mode == 0 and s_k == 1 and kdim == kp and s_r == kp and src.splat is None and root.slot == abi.SLOT_ARENA
-                and (src.elem_off * 4) % 16 == 0 and os.environ.get("GFB_RAW_HI", "1") == "1"):
-            lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
-            self.buf[("tc", n, name, "lo")] = lo
-            sa = abi.SplitArgs(rows=rows, k=kdim, kp=kp, s_r=s_r, s_k=s_k, mode=7)
-            grid = (max(1, min((rows * kp // 4 + 255) // 256, NUM_SMS * 16)), 1, 1)
-            rec = LaunchRec(abi.K_SPLIT_TF32, grid, (256, 1, 1), 0, sa, [src.key], [lo.key], f"split_{name}:lo#{n}")
-            rec.algo_bytes = 2 * rows * kp * 4
-            rec.finalize = _finalize_refs(sa, {"src": src, "hi": src, "lo": lo})
-            self.launches.append(rec)
-            return src, lo, kp
+        root = self._dense_root(src) if mode == 0 else None
+        if (root is not None and s_k == 1 and kdim == kp and s_r == kp and element_count(root.shape) == rows * kp
+                and os.environ.get("GFB_RAW_HI", "1") == "1"):
+            return root, self._lo_plane(root), kp
         hi = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
         lo = Buffer(self.new_key(), ElementType.F32, (rows, kp), (kp, 1))
         self.buf[("tc", n, name, "hi")] = hi
@@ -1715,7 +1751,9 @@ class Lowering:
     def _tc_gemm(self, n, a, b, out, m, ncols, kdim, addr, label):
         """tcgen05 GEMM over split planes; split-K (+ a reduce pass) when the
         output has too few tiles to fill the GPU for a long K."""
-        (ahi, alo, kpa), (bhi, blo, kpb) = a, b
+        (ahi, alo, kpa), (bhi, blo, kpb) = a[:3], b[:3]
+        a_mn = a[3] if len(a) > 3 else 0
+        b_mn = b[3] if len(b) > 3 else 0
         tiles = ((ncols + TC_TILE - 1) // TC_TILE) * ((m + TC_TILE - 1) // TC_TILE)
         kblocks = (kdim + 31) // 32
         splits = 1
@@ -1724,7 +1762,7 @@ class Lowering:
         elif tiles <= 8 and kblocks >= 16:
             # a handful of tiles over a medium K (an MLP's first layer): spread K
             splits = max(1, min(NUM_SMS // tiles, kblocks // 4))
-        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb)
+        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn)
         target = out
         if splits > 1:
             per = ((kblocks + splits - 1) // splits) * 32
@@ -1739,6 +1777,8 @@ class Lowering:
                 setattr(ta, k_, v_)
         wide = ncols >= 256 and os.environ.get("GFB_TC_WIDE", "1") == "1"
         pair = wide and m >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1"
+        if (a_mn or b_mn) and not pair:
+            raise UnsupportedOp("MN-major tensor-core operands need the CTA-pair kernel")
         if pair:  # 2-SM CTA pair, 256x256 tile (gfb_gemm_tc2_kernel)
             kind, block, smem = abi.K_DOT_TC32P, 320, TC_SMEM
             grid = (2 * ((ncols + 255) // 256), (m + 255) // 256, splits)

@@ -1080,6 +1080,24 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, in
         "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, int c0, int c1, int c2, uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+        : "memory");
+}
+// MN-major SWIZZLE_128B_BASE32B operand (see the tcgw kernel below): MN atoms
+// 4096 B apart (LBO), 4-row K groups 512 B apart (SBO)
+__device__ __forceinline__ uint64_t smem_desc_mn_at(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)(4096 >> 4) << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;
+    return d;
+}
 __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -1152,15 +1170,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                 const uint32_t bar = full0 + s * 8;
                 const int kc = (int)k_begin + kb * BK;
                 const int am = m0 + 128 * rank, bn = n0 + 128 * rank;
-                tma_load_2d_pair(st, p.tmap[0], kc, am, bar);
-                tma_load_2d_pair(st + A_BYTES, p.tmap[1], kc, am, bar);
-                tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
-                tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+                if (p.a_ld_mn > 0) {  // MN-major: (32 MN, 32 K, 4 MN atoms) boxes
+                    tma_load_3d_pair(st, p.tmap[0], 0, kc, am >> 5, bar);
+                    tma_load_3d_pair(st + A_BYTES, p.tmap[1], 0, kc, am >> 5, bar);
+                } else {
+                    tma_load_2d_pair(st, p.tmap[0], kc, am, bar);
+                    tma_load_2d_pair(st + A_BYTES, p.tmap[1], kc, am, bar);
+                }
+                if (p.b_ld_mn > 0) {
+                    tma_load_3d_pair(st + 2 * A_BYTES, p.tmap[2], 0, kc, bn >> 5, bar);
+                    tma_load_3d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], 0, kc, bn >> 5, bar);
+                } else {
+                    tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
+                    tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0 && leader) {
-            constexpr uint32_t idesc = idesc_tf32(256, 256);
+            const bool a_mn = p.a_ld_mn > 0, b_mn = p.b_ld_mn > 0;
+            const uint32_t idesc = idesc_tf32(256, 256) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % STAGES;
                 const int chunk = kb / CHUNK_KB, b = chunk % NBUF;
@@ -1172,16 +1201,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                 mbar_wait(&full[s], (kb / STAGES) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 unsigned char* st = smem + s * STAGE_BYTES;
-                const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
-                const uint64_t bh = smem_desc(st + 2 * A_BYTES), bl = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                const uint32_t sa = su32(st), sb = sa + 2 * A_BYTES;
                 const uint32_t d = tmem + (uint32_t)(b * NT);
 #pragma unroll
                 for (int j = 0; j < BK / 8; ++j) {
-                    const uint64_t adv = (uint64_t)(j * 32) >> 4;
+                    // K-major SW128: 8 tf32 = 32 B along K inside the atom; MN-major:
+                    // 8 K rows = two 4-row groups = 1024 B further
+                    const uint64_t ah = a_mn ? smem_desc_mn_at(sa + j * 1024) : smem_desc(st) + ((uint64_t)(j * 32) >> 4);
+                    const uint64_t al = a_mn ? smem_desc_mn_at(sa + A_BYTES + j * 1024)
+                                             : smem_desc(st + A_BYTES) + ((uint64_t)(j * 32) >> 4);
+                    const uint64_t bh = b_mn ? smem_desc_mn_at(sb + j * 1024) : smem_desc(st + 2 * A_BYTES) + ((uint64_t)(j * 32) >> 4);
+                    const uint64_t bl = b_mn ? smem_desc_mn_at(sb + B_BYTES + j * 1024)
+                                             : smem_desc(st + 2 * A_BYTES + B_BYTES) + ((uint64_t)(j * 32) >> 4);
                     const uint32_t acc = !(chunk_start && j == 0);
-                    mma_tf32_pair(d, ah + adv, bh + adv, idesc, acc);
-                    mma_tf32_pair(d, ah + adv, bl + adv, idesc, 1);
-                    mma_tf32_pair(d, al + adv, bh + adv, idesc, 1);
+                    mma_tf32_pair(d, ah, bh, idesc, acc);
+                    mma_tf32_pair(d, ah, bl, idesc, 1);
+                    mma_tf32_pair(d, al, bh, idesc, 1);
                 }
                 mma_commit_pair(&empty[s]);
                 if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);

@@ -59,6 +59,25 @@ bool encode_plane_map(void* gaddr, int64_t rows, int64_t kp, uint32_t box_rows, 
     std::memcpy(out, &map, sizeof(map));
     return true;
 }
+// MN-major operand (element (mn, k) at k * ld + mn): 3-D view (32 MN, K,
+// MN / 32) whose box (32, 32, 4) lands as four 4 KB MN atoms in the
+// SWIZZLE_128B_BASE32B layout tcgen05 reads MN-major tf32 operands in
+// (SWIZZLE_128B_ATOM_32B; scripts/tma_mn_probe.cu checks it against a host
+// product, profiles/r02_tma_mn_probe.txt).
+bool encode_mn_map(void* gaddr, int64_t mn, int64_t k, int64_t ld, void* out) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || mn % 32) return false;
+    alignas(64) CUtensorMap map;
+    cuuint64_t dims[3] = {32, (cuuint64_t)k, (cuuint64_t)(mn / 32)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+    cuuint32_t box[3] = {32, 32, 4};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, gaddr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out, &map, sizeof(map));
+    return true;
+}
 // Channel-last 4-D activation (C, W, H, N innermost first) -> boxes of
 // 32 channels x bw x bh x bn with traversal strides (1, sx, sy, 1); taps
 // outside the tensor read as zero (the convolution's padding).
@@ -379,8 +398,14 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                     return bail(fail(GFB_ERR_INVALID, "tensor-core operand planes must live in the arena"));
                 void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
                 const int64_t rows = t < 2 ? a->M : a->N, kp = t < 2 ? a->kp_a : a->kp_b;
+                const int64_t ld_mn = t < 2 ? a->a_ld_mn : a->b_ld_mn;
                 const uint32_t box_rows = (t >= 2 && L.kind == GFB_K_DOT_TC32W) ? 256 : 128;
-                if (!encode_plane_map(addr, rows, kp, box_rows, a->tmap[t]))
+                if (ld_mn > 0) {
+                    if (L.kind != GFB_K_DOT_TC32P)
+                        return bail(fail(GFB_ERR_INVALID, "MN-major operands need the CTA-pair GEMM"));
+                    if (!encode_mn_map(addr, rows, a->K, ld_mn, a->tmap[t]))
+                        return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (MN-major operand) failed"));
+                } else if (!encode_plane_map(addr, rows, kp, box_rows, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
             }
         }

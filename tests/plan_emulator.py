@@ -315,11 +315,20 @@ def _tf32(x):
     return (np.ascontiguousarray(x).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
 
 
+def _plane(mem, ref, rows, kp, k, ld_mn):
+    """[rows, kp] operand: a K-major plane, or an MN-major tensor (element
+    (r, k) at k * ld_mn + r, columns past K zero)."""
+    v = mem.view(ref, np.float32)
+    if ld_mn > 0:
+        out = np.zeros((rows, kp), dtype=np.float32)
+        out[:, :k] = v[np.arange(k)[None, :] * ld_mn + np.arange(rows)[:, None]]
+        return _tf32(out)
+    return _tf32(v[: rows * kp].reshape(rows, kp))
+
+
 def run_tc(mem, a):
-    A = (_tf32(mem.view(a.a_hi, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a)),
-         _tf32(mem.view(a.a_lo, np.float32)[: a.M * a.kp_a].reshape(a.M, a.kp_a)))
-    B = (_tf32(mem.view(a.b_hi, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b)),
-         _tf32(mem.view(a.b_lo, np.float32)[: a.N * a.kp_b].reshape(a.N, a.kp_b)))
+    A = (_plane(mem, a.a_hi, a.M, a.kp_a, a.K, a.a_ld_mn), _plane(mem, a.a_lo, a.M, a.kp_a, a.K, a.a_ld_mn))
+    B = (_plane(mem, a.b_hi, a.N, a.kp_b, a.K, a.b_ld_mn), _plane(mem, a.b_lo, a.N, a.kp_b, a.K, a.b_ld_mn))
     splits = max(1, a.k_splits)
     i = np.arange(a.M, dtype=np.int64)[:, None]
     j = np.arange(a.N, dtype=np.int64)[None, :]

@@ -258,3 +258,40 @@ def test_conv_stem_kernel_matches_oracle(monkeypatch, shape, pad, layout):
     out = gf.call(exe, tens)[0].to_numpy()
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("m,k,n", [(512, 4096, 256), (288, 1000, 352), (4096, 2048, 4096)])
+@pytest.mark.parametrize("raw", ["mn", "kmajor", "split"])
+def test_raw_hi_operands(monkeypatch, m, k, n, raw):
+    """Arena-resident operands read in place as the tf32 hi operand (the MMA
+    truncates), with one shared lo plane: K-major (Dot(h, W)) and MN-major
+    via TMA SWIZZLE_128B_ATOM_32B (the weight gradient Dot(h^T, dz)),
+    against the plane-split form and the oracle."""
+    if raw == "split":
+        monkeypatch.setenv("GFB_RAW_HI", "0")
+        monkeypatch.setenv("GFB_MN_MAJOR", "0")
+    fn = gf.Function("raw")
+    h = fn.add_parameter(F32, (k, m))
+    dz = fn.add_parameter(F32, (k, n))
+    rh, rd = fn.add_node(K.RELU, [h]), fn.add_node(K.NEGATE, [dz])  # arena-resident producers
+    if raw == "kmajor":
+        w = fn.add_parameter(F32, (m, n))
+        out = fn.add_node(K.DOT, [rh, w])  # [k, m] x [m, n]: A K-major
+    else:
+        ht = fn.add_node(K.RESHAPE, [rh], {"input_order": (1, 0), "output_shape": (m, k)})
+        out = fn.add_node(K.DOT, [ht, rd])  # [m, k] x [k, n]: both MN-major
+    fn.set_results([out, rh])
+    rng = np.random.default_rng(m + k + n)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    exe = gf.compile_function(fn)
+    tc = [L for L in exe.lowered.launches if L.label.startswith("dot_tc")]
+    assert tc
+    if raw == "mn":
+        assert tc[0].args.a_ld_mn == m and tc[0].args.b_ld_mn == n
+        assert not any(L.label.startswith("split") for L in exe.lowered.launches)
+    out = gf.call(exe, [gf.tensor_from_flat(F32, a.shape, a) for a in ins])[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    want = interp.run_function(fn, ins)[0]
+    exact = np.maximum(ins[0].astype(np.float64), 0).T @ (-ins[1].astype(np.float64)) if raw != "kmajor" else \
+        np.maximum(ins[0].astype(np.float64), 0) @ ins[2].astype(np.float64)
+    assert G.normwise(out, exact) <= 1e-5 and G.normwise(out, want) <= 1e-5
