@@ -408,6 +408,13 @@ def init_distributed(rank: int | None = None, world: int | None = None) -> Comm:
         world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     if _COMM is not None and (_COMM.rank, _COMM.world) == (rank, world):
         return _COMM
+    # Collective pinning for the gradient buckets: single-node
+    # NVSwitch all-reduces of 1-64 MiB buckets -- NVLS (in-switch reduction)
+    # or Ring, Simple / LL128 protocols; Tree and LL do not pay at these sizes.
+    # Callers' own settings win; GFB_NCCL_PIN=0 leaves NCCL to choose.
+    if os.environ.get("GFB_NCCL_PIN", "1") == "1":
+        os.environ.setdefault("NCCL_ALGO", "NVLS,Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple,LL128")
     uid = C.create_string_buffer(128)
     if rank == 0:
         check(lib().gfb_comm_unique_id(uid), "gfb_comm_unique_id")

@@ -280,7 +280,10 @@ def test_raw_hi_operands(monkeypatch, m, k, n, raw):
     else:
         ht = fn.add_node(K.RESHAPE, [rh], {"input_order": (1, 0), "output_shape": (m, k)})
         out = fn.add_node(K.DOT, [ht, rd])  # [m, k] x [k, n]: both MN-major
-    fn.set_results([out, rh])
+    # rh's second reader keeps it materialised in the arena (as in config E,
+    # where an activation feeds the next layer's Dot and this layer's weight
+    # gradient); the transposing Reshape is then a free view
+    fn.set_results([out, fn.add_node(K.SUM, [rh], {"reduction_axes": (0,)})])
     rng = np.random.default_rng(m + k + n)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     exe = gf.compile_function(fn)
