@@ -1094,7 +1094,7 @@ class Lowering:
         vectors = (n_o + V - 1) // V
         split = 1
         if red_kind and n_r > 16:
-            while split < 64 and ((vectors * split + 255) // 256) < 2 * NUM_SMS and n_r // (split * 2) >= 8:
+            while split < 256 and ((vectors * split + 255) // 256) < 3 * NUM_SMS and n_r // (split * 2) >= 8:
                 split *= 2
         per_row = 256 // split
         grid = max(1, min((vectors + per_row - 1) // per_row, NUM_SMS * EW_BLOCKS_PER_SM))
