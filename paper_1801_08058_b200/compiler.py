@@ -1779,9 +1779,10 @@ class Lowering:
         pair = wide and m >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1"
         if (a_mn or b_mn) and not pair:
             raise UnsupportedOp("MN-major tensor-core operands need the CTA-pair kernel")
-        if pair:  # 2-SM CTA pair, 256x256 tile (gfb_gemm_tc2_kernel)
+        if pair:  # 2-SM CTA pairs, 256x256 tiles, persistent (gfb_gemm_tc2_kernel)
             kind, block, smem = abi.K_DOT_TC32P, 320, TC_SMEM
-            grid = (2 * ((ncols + 255) // 256), (m + 255) // 256, splits)
+            ntiles = ((ncols + 255) // 256) * ((m + 255) // 256) * splits
+            grid = (2 * min(ntiles, NUM_SMS // 2), 1, 1)
         elif wide:
             kind, block, smem = abi.K_DOT_TC32W, 320, TC_SMEM_W
             grid = ((ncols + 255) // 256, (m + TC_TILE - 1) // TC_TILE, splits)

@@ -1113,6 +1113,34 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
 }
 }  // namespace tc
 
+// Persistent: the grid is at most one CTA pair per two SMs, and each pair
+// walks the output tiles (and K splits) in a grouped raster -- GROUP_M
+// row-tiles by every column tile -- so that concurrently running pairs share
+// their A row strips and B column strips in L2.  The stage ring, the TMEM
+// accumulator ring and the epilogue's promotion protocol all run across tile
+// boundaries: one tile's last chunks and its stores overlap the next tile's
+// loads and MMAs, and the barrier / TMEM setup is paid once per kernel.
+namespace tc {
+struct PTile {
+    int m0, n0, z, nk;
+};
+__device__ __forceinline__ PTile pair_tile(const gfb_tc_args& p, int t, int ntm, int ntn) {
+    constexpr int GROUP_M = 8;
+    const int per_z = ntm * ntn;
+    const int z = t / per_z, r = t % per_z;
+    const int g = r / (GROUP_M * ntn), gr = r % (GROUP_M * ntn);
+    const int gm = min(GROUP_M, ntm - g * GROUP_M);
+    PTile o;
+    o.m0 = (g * GROUP_M + gr % gm) * 256;
+    o.n0 = (gr / gm) * 256;
+    o.z = z;
+    const int64_t k_begin = p.k_splits > 1 ? (int64_t)z * p.k_per_split : 0;
+    const int64_t k_end = p.k_splits > 1 ? min(p.K, k_begin + p.k_per_split) : p.K;
+    o.nk = k_end > k_begin ? (int)((k_end - k_begin + PCfg::BK - 1) / PCfg::BK) : 0;
+    return o;
+}
+}  // namespace tc
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1)
     gfb_gemm_tc2_kernel(const __grid_constant__ gfb_tc_args p) {
     using namespace tc;
@@ -1131,11 +1159,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    const int n0 = (blockIdx.x >> 1) * 256, m0 = blockIdx.y * 256;
-    const int64_t k_begin = p.k_splits > 1 ? (int64_t)blockIdx.z * p.k_per_split : 0;
-    const int64_t k_end = p.k_splits > 1 ? min(p.K, k_begin + p.k_per_split) : p.K;
-    const int nk = k_end > k_begin ? (int)((k_end - k_begin + BK - 1) / BK) : 0;
-    const int nchunk = nk > 0 ? (nk + CHUNK_KB - 1) / CHUNK_KB : 0;
+    const int ntn = (int)((p.N + 255) / 256), ntm = (int)((p.M + 255) / 256);
+    const int ntiles = ntn * ntm * (p.k_splits > 1 ? (int)p.k_splits : 1);
+    const int pair_id = (int)(blockIdx.x >> 1), npairs = (int)(gridDim.x >> 1);
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -1162,27 +1188,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
     if (warp == 0) {
         if (lane == 0) {
             const uint32_t full0 = peer_addr(full, 0);  // the leader's full barriers
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                unsigned char* st = smem + s * STAGE_BYTES;
-                if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);  // both CTAs' bytes land on it
-                const uint32_t bar = full0 + s * 8;
-                const int kc = (int)k_begin + kb * BK;
-                const int am = m0 + 128 * rank, bn = n0 + 128 * rank;
-                if (p.a_ld_mn > 0) {  // MN-major: (32 MN, 32 K, 4 MN atoms) boxes
-                    tma_load_3d_pair(st, p.tmap[0], 0, kc, am >> 5, bar);
-                    tma_load_3d_pair(st + A_BYTES, p.tmap[1], 0, kc, am >> 5, bar);
-                } else {
-                    tma_load_2d_pair(st, p.tmap[0], kc, am, bar);
-                    tma_load_2d_pair(st + A_BYTES, p.tmap[1], kc, am, bar);
-                }
-                if (p.b_ld_mn > 0) {
-                    tma_load_3d_pair(st + 2 * A_BYTES, p.tmap[2], 0, kc, bn >> 5, bar);
-                    tma_load_3d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], 0, kc, bn >> 5, bar);
-                } else {
-                    tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
-                    tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+            int g = 0;                                   // K-blocks issued so far (the ring position)
+            for (int t = pair_id; t < ntiles; t += npairs) {
+                const PTile T = pair_tile(p, t, ntm, ntn);
+                const int64_t k_begin = p.k_splits > 1 ? (int64_t)T.z * p.k_per_split : 0;
+                const int am = T.m0 + 128 * rank, bn = T.n0 + 128 * rank;
+                for (int kb = 0; kb < T.nk; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);  // both CTAs' bytes land on it
+                    const uint32_t bar = full0 + s * 8;
+                    const int kc = (int)k_begin + kb * BK;
+                    if (p.a_ld_mn > 0) {  // MN-major: (32 MN, 32 K, 4 MN atoms) boxes
+                        tma_load_3d_pair(st, p.tmap[0], 0, kc, am >> 5, bar);
+                        tma_load_3d_pair(st + A_BYTES, p.tmap[1], 0, kc, am >> 5, bar);
+                    } else {
+                        tma_load_2d_pair(st, p.tmap[0], kc, am, bar);
+                        tma_load_2d_pair(st + A_BYTES, p.tmap[1], kc, am, bar);
+                    }
+                    if (p.b_ld_mn > 0) {
+                        tma_load_3d_pair(st + 2 * A_BYTES, p.tmap[2], 0, kc, bn >> 5, bar);
+                        tma_load_3d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], 0, kc, bn >> 5, bar);
+                    } else {
+                        tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
+                        tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+                    }
                 }
             }
         }
@@ -1190,36 +1221,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
         if (lane == 0 && leader) {
             const bool a_mn = p.a_ld_mn > 0, b_mn = p.b_ld_mn > 0;
             const uint32_t idesc = idesc_tf32(256, 256) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const int chunk = kb / CHUNK_KB, b = chunk % NBUF;
-                const bool chunk_start = kb % CHUNK_KB == 0;
-                if (chunk_start) {
-                    mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+            int g = 0, gchunk = 0;  // ring positions across tiles
+            for (int t = pair_id; t < ntiles; t += npairs) {
+                const PTile T = pair_tile(p, t, ntm, ntn);
+                for (int kb = 0; kb < T.nk; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const int chunk = gchunk + kb / CHUNK_KB, b = chunk % NBUF;
+                    const bool chunk_start = kb % CHUNK_KB == 0;
+                    if (chunk_start) {
+                        mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    mbar_wait(&full[s], (g / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                mbar_wait(&full[s], (kb / STAGES) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                unsigned char* st = smem + s * STAGE_BYTES;
-                const uint32_t sa = su32(st), sb = sa + 2 * A_BYTES;
-                const uint32_t d = tmem + (uint32_t)(b * NT);
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    const uint32_t sa = su32(st), sb = sa + 2 * A_BYTES;
+                    const uint32_t d = tmem + (uint32_t)(b * NT);
 #pragma unroll
-                for (int j = 0; j < BK / 8; ++j) {
-                    // K-major SW128: 8 tf32 = 32 B along K inside the atom; MN-major:
-                    // 8 K rows = two 4-row groups = 1024 B further
-                    const uint64_t ah = a_mn ? smem_desc_mn_at(sa + j * 1024) : smem_desc(st) + ((uint64_t)(j * 32) >> 4);
-                    const uint64_t al = a_mn ? smem_desc_mn_at(sa + A_BYTES + j * 1024)
-                                             : smem_desc(st + A_BYTES) + ((uint64_t)(j * 32) >> 4);
-                    const uint64_t bh = b_mn ? smem_desc_mn_at(sb + j * 1024) : smem_desc(st + 2 * A_BYTES) + ((uint64_t)(j * 32) >> 4);
-                    const uint64_t bl = b_mn ? smem_desc_mn_at(sb + B_BYTES + j * 1024)
-                                             : smem_desc(st + 2 * A_BYTES + B_BYTES) + ((uint64_t)(j * 32) >> 4);
-                    const uint32_t acc = !(chunk_start && j == 0);
-                    mma_tf32_pair(d, ah, bh, idesc, acc);
-                    mma_tf32_pair(d, ah, bl, idesc, 1);
-                    mma_tf32_pair(d, al, bh, idesc, 1);
+                    for (int j = 0; j < BK / 8; ++j) {
+                        // K-major SW128: 8 tf32 = 32 B along K inside the atom; MN-major:
+                        // 8 K rows = two 4-row groups = 1024 B further
+                        const uint64_t ah = a_mn ? smem_desc_mn_at(sa + j * 1024) : smem_desc(st) + ((uint64_t)(j * 32) >> 4);
+                        const uint64_t al = a_mn ? smem_desc_mn_at(sa + A_BYTES + j * 1024)
+                                                 : smem_desc(st + A_BYTES) + ((uint64_t)(j * 32) >> 4);
+                        const uint64_t bh = b_mn ? smem_desc_mn_at(sb + j * 1024)
+                                                 : smem_desc(st + 2 * A_BYTES) + ((uint64_t)(j * 32) >> 4);
+                        const uint64_t bl = b_mn ? smem_desc_mn_at(sb + B_BYTES + j * 1024)
+                                                 : smem_desc(st + 2 * A_BYTES + B_BYTES) + ((uint64_t)(j * 32) >> 4);
+                        const uint32_t acc = !(chunk_start && j == 0);
+                        mma_tf32_pair(d, ah, bh, idesc, acc);
+                        mma_tf32_pair(d, ah, bl, idesc, 1);
+                        mma_tf32_pair(d, al, bh, idesc, 1);
+                    }
+                    mma_commit_pair(&empty[s]);
+                    if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == T.nk - 1) mma_commit_pair(&tfull[b]);
                 }
-                mma_commit_pair(&empty[s]);
-                if (kb % CHUNK_KB == CHUNK_KB - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);
+                gchunk += (T.nk + CHUNK_KB - 1) / CHUNK_KB;
             }
         }
     } else {
@@ -1228,52 +1265,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
         constexpr int EC = 128;
         const int q = warp & 3, cg = (warp - 2) >> 2;
         const uint32_t tempty0 = peer_addr(tempty, 0);
-        float acc[EC];
+        int gchunk = 0;
+        for (int t = pair_id; t < ntiles; t += npairs) {
+            const PTile T = pair_tile(p, t, ntm, ntn);
+            const int nchunk = (T.nk + CHUNK_KB - 1) / CHUNK_KB;
+            float acc[EC];
 #pragma unroll
-        for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
-        for (int chunk = 0; chunk < nchunk; ++chunk) {
-            const int b = chunk % NBUF;
-            mbar_wait(&tfull[b], (chunk / NBUF) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            for (int c0 = 0; c0 < nchunk; ++c0) {
+                const int chunk = gchunk + c0, b = chunk % NBUF;
+                mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-            for (int c = 0; c < EC / 32; ++c) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT + cg * EC + c * 32);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                for (int c = 0; c < EC / 32; ++c) {
+                    uint32_t r[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT + cg * EC + c * 32);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+                    for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
             }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
-        }
-        float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)blockIdx.z * p.split_stride : 0);
-        const LinearRows rows{m0 + 128 * (int64_t)rank, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
-        const int64_t roff = rows(q * 32 + lane);
-        if (roff >= 0) {
-            float* dst = C + roff;
+            gchunk += nchunk;
+            float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)T.z * p.split_stride : 0);
+            const LinearRows rows{T.m0 + 128 * (int64_t)rank, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
+            const int64_t roff = rows(q * 32 + lane);
+            if (roff >= 0) {
+                float* dst = C + roff;
 #pragma unroll
-            for (int c = 0; c < EC / 32; ++c) {
-                const int col0 = n0 + cg * EC + c * 32;
-                if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
+                for (int c = 0; c < EC / 32; ++c) {
+                    const int col0 = T.n0 + cg * EC + c * 32;
+                    if (p.c_sn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst + col0) & 15) == 0)) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(dst + col0 + j) =
-                            make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
-                } else {
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + col0 + j) =
+                                make_float4(acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) dst[(int64_t)(col0 + j) * p.c_sn] = acc[c * 32 + j];
+                    }
                 }
             }
         }
