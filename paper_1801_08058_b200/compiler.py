@@ -1757,7 +1757,19 @@ class Lowering:
         tiles = ((ncols + TC_TILE - 1) // TC_TILE) * ((m + TC_TILE - 1) // TC_TILE)
         kblocks = (kdim + 31) // 32
         splits = 1
-        if tiles < NUM_SMS and kblocks >= 64:
+        pair_tiles = ((ncols + 255) // 256) * ((m + 255) // 256)
+        pairs = NUM_SMS // 2
+        if (ncols >= 256 and m >= 256 and pair_tiles >= pairs and kblocks >= 64
+                and os.environ.get("GFB_TC_PAIR", "1") == "1" and os.environ.get("GFB_TC_QSPLIT", "1") == "1"):
+            # the persistent pair kernel runs pair_tiles / 74 waves; a weight
+            # gradient (16 x 16 tiles of 256, K = the batch) is 3.46 waves, i.e.
+            # 13 % idle in the last one: split K where that fills the waves
+            # (the partials cost one extra pass over the output, ~1 % here)
+            def fill(sp):
+                w = pair_tiles * sp / pairs
+                return w / -(-w // 1)
+            splits = max((sp for sp in range(1, 5) if kblocks // sp >= 32), key=lambda sp: fill(sp) - 0.02 * (sp - 1))
+        elif tiles < NUM_SMS and kblocks >= 64:
             splits = max(1, min((2 * NUM_SMS) // tiles, kblocks // 16))
         elif tiles <= 8 and kblocks >= 16:
             # a handful of tiles over a medium K (an MLP's first layer): spread K
@@ -1782,7 +1794,8 @@ class Lowering:
         if pair:  # 2-SM CTA pairs, 256x256 tiles, persistent (gfb_gemm_tc2_kernel)
             kind, block, smem = abi.K_DOT_TC32P, 320, TC_SMEM
             ntiles = ((ncols + 255) // 256) * ((m + 255) // 256) * splits
-            grid = (2 * min(ntiles, NUM_SMS // 2), 1, 1)
+            pairs = NUM_SMS // 2 if os.environ.get("GFB_TC_PERSIST", "1") == "1" else ntiles
+            grid = (2 * min(ntiles, pairs), 1, 1)
         elif wide:
             kind, block, smem = abi.K_DOT_TC32W, 320, TC_SMEM_W
             grid = ((ncols + 255) // 256, (m + TC_TILE - 1) // TC_TILE, splits)
