@@ -246,7 +246,8 @@ typedef struct GFB_ALIGN64 {
      * gradient), loaded as SWIZZLE_128B_ATOM_32B boxes (the tf32 MN-major
      * layout); likewise b_ld_mn for B.  0 = K-major planes [rows, kp]. */
     int64_t a_ld_mn, b_ld_mn;
-    int64_t pad[3];
+    int64_t group_m; /* persistent pair kernel: tile raster grouped by this many tile rows (<= 1: row-major) */
+    int64_t pad[2];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

@@ -96,8 +96,8 @@ class TcArgs(C.Structure):
         ("kp_a", C.c_int64), ("kp_b", C.c_int64),
         ("c_rdiv", C.c_int64), ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64),
         ("k_splits", C.c_int64), ("k_per_split", C.c_int64), ("split_stride", C.c_int64),
-        ("a_ld_mn", C.c_int64), ("b_ld_mn", C.c_int64),
-        ("pad", C.c_int64 * 3),
+        ("a_ld_mn", C.c_int64), ("b_ld_mn", C.c_int64), ("group_m", C.c_int64),
+        ("pad", C.c_int64 * 2),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
 

@@ -1774,7 +1774,8 @@ class Lowering:
         elif tiles <= 8 and kblocks >= 16:
             # a handful of tiles over a medium K (an MLP's first layer): spread K
             splits = max(1, min(NUM_SMS // tiles, kblocks // 4))
-        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn)
+        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn,
+                        group_m=int(os.environ.get("GFB_TC_GROUP_M", "1")))
         target = out
         if splits > 1:
             per = ((kblocks + splits - 1) // splits) * 32

@@ -1125,7 +1125,7 @@ struct PTile {
     int m0, n0, z, nk;
 };
 __device__ __forceinline__ PTile pair_tile(const gfb_tc_args& p, int t, int ntm, int ntn) {
-    constexpr int GROUP_M = 8;
+    const int GROUP_M = p.group_m > 1 ? (int)p.group_m : 1;  // 1: row-major, column tiles fastest
     const int per_z = ntm * ntn;
     const int z = t / per_z, r = t % per_z;
     const int g = r / (GROUP_M * ntn), gr = r % (GROUP_M * ntn);
