@@ -247,7 +247,19 @@ typedef struct GFB_ALIGN64 {
      * layout); likewise b_ld_mn for B.  0 = K-major planes [rows, kp]. */
     int64_t a_ld_mn, b_ld_mn;
     int64_t group_m; /* persistent pair kernel: tile raster grouped by this many tile rows (<= 1: row-major) */
-    int64_t pad[2];
+    /* Fused epilogue (pair kernel, no split-K; every [M, N] operand dense
+     * row-major with row pitch N, bias unit stride), element (m, n), z = the
+     * promoted fp32 accumulator:
+     *   epi_kind 1 (Dot -> Add(Broadcast(bias)) -> Relu): C = x = z + bias[n];
+     *              e_out2[m, n] = x > 0 ? x : 0
+     *   epi_kind 2 (Dot -> Multiply(Maximum(Divide(h, x), 0))): C = z * r,
+     *              r = h / x >= 0 ? h / x : 0 with h = e_aux1, x = e_aux2
+     * and when e_lo != 0, e_lo[m, n] = y - trunc_tf32(y) for the tensor a
+     * later GEMM reads as its TF32 hi operand (y = e_out2 for kind 1, C for
+     * kind 2).  Each op is the unfused plan's IEEE op: bit-identical. */
+    int64_t epi_kind;
+    uint64_t e_bias, e_aux1, e_aux2, e_out2, e_lo; /* GFB_REF */
+    int64_t pad[4];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

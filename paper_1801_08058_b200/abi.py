@@ -88,7 +88,7 @@ class SplitArgs(C.Structure):
 
 
 class TcArgs(C.Structure):
-    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 192, size 704.
+    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 256, size 768.
     _fields_ = [
         ("tab", C.c_void_p), ("c", C.c_uint64),
         ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("c_sm", C.c_int64), ("c_sn", C.c_int64),
@@ -97,7 +97,9 @@ class TcArgs(C.Structure):
         ("c_rdiv", C.c_int64), ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64),
         ("k_splits", C.c_int64), ("k_per_split", C.c_int64), ("split_stride", C.c_int64),
         ("a_ld_mn", C.c_int64), ("b_ld_mn", C.c_int64), ("group_m", C.c_int64),
-        ("pad", C.c_int64 * 2),
+        ("epi_kind", C.c_int64), ("e_bias", C.c_uint64), ("e_aux1", C.c_uint64), ("e_aux2", C.c_uint64),
+        ("e_out2", C.c_uint64), ("e_lo", C.c_uint64),
+        ("pad", C.c_int64 * 4),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
 

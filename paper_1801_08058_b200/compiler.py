@@ -817,9 +817,13 @@ class Lowering:
             if node.op not in (OpKind.PARAMETER, OpKind.CONSTANT) and r not in result_slot and r not in self.allreduce:
                 result_slot[r] = j
 
+        self._epi = self._plan_epilogues()
+        self._epi_nodes = {m for sp in self._epi.values() for m in sp["absorbed"]}
         for n in self.order:
             node = self.nodes[n]
             d = node.output
+            if n in self._epi:
+                continue  # a Dot whose consumer map runs in its epilogue: never materialised
             if element_count(d.shape) >= INDEX_LIMIT:
                 raise UnsupportedOp(f"tensor of {element_count(d.shape)} elements exceeds the 2^31 index limit")
             if node.op is OpKind.PARAMETER:
@@ -857,7 +861,8 @@ class Lowering:
         # merge rule: a materialised node consumed only by one Sum is that Sum's side output
         side_of = {}
         for n in self.order:
-            if n in self.M and self.nodes[n].op is not OpKind.SUM and self.is_light(n) and n not in self._row_nodes:
+            if (n in self.M and self.nodes[n].op is not OpKind.SUM and self.is_light(n) and n not in self._row_nodes
+                    and n not in self._epi_nodes):
                 cons = self.consumers[n]
                 if len(cons) == 1 and self.nodes[cons[0]].op is OpKind.SUM and cons[0] not in self._row_nodes:
                     side_of[cons[0]] = n
@@ -874,6 +879,8 @@ class Lowering:
                 if n == rg.anchor:
                     self.emit_row_group(rg)
                 continue
+            if n in self._epi_nodes:
+                continue  # written by the epilogue of the Dot it consumes
             if self.is_heavy(n):
                 self.emit_heavy(n)
             elif n in self.M and n not in merged and n not in grouped and n not in chained:
@@ -1119,14 +1126,14 @@ class Lowering:
         out, used = {}, set()
         for n in self.order:
             if (n not in self.M or n in taken or n in used or n in self.allreduce or not self.is_light(n)
-                    or self.nodes[n].op is OpKind.SUM or n not in self.buf or n in self._row_nodes):
+                    or self.nodes[n].op is OpKind.SUM or n not in self.buf or n in self._row_nodes or n in self._epi_nodes):
                 continue
             cons = sorted(set(self.consumers[n]), key=lambda c: pos.get(c, 1 << 30))
             if not cons:
                 continue
             c = cons[0]
             if (c in taken or c in out or c in used or c not in self.M or not self.is_light(c) or c in self.allreduce
-                    or c in self._row_nodes
+                    or c in self._row_nodes or c in self._epi_nodes
                     or self.nodes[c].op is OpKind.SUM or self.nodes[c].op in INDEX_OPS or c not in self.buf
                     or pos.get(c) is None):
                 continue
@@ -1161,6 +1168,7 @@ class Lowering:
             return out
 
         cands = [n for n in self.order if n in self.M and n not in merged and self.is_light(n) and n not in self._row_nodes
+                 and n not in self._epi_nodes
                  and self.nodes[n].op is not OpKind.SUM and n in self.buf and self.buf[n].slot == abi.SLOT_ARENA]
         groups, taken = {}, set()
         for i, n in enumerate(cands):
@@ -1667,6 +1675,95 @@ class Lowering:
         rec = self._tc_gemm(n, a, b, out, m, nn, k, {"c_sm": out.strides[0], "c_sn": out.strides[1]}, f"dot_tc#{n}")
         rec.algo_bytes = (m * k + k * nn + m * nn) * 4
 
+    def _plan_epilogues(self) -> dict:
+        """Dots whose only consumer is an elementwise map the pair GEMM can
+        apply in its epilogue (gfb_tc_args.epi_kind): config E's forward
+        Dot -> Add(Broadcast(bias)) -> Relu, and its backward
+        Dot -> Multiply(Maximum(Divide(relu, x), 0)) (the Relu gradient,
+        autodiff.py:143-148).  The maps' nodes are then written by the GEMM
+        (every op the same IEEE op, so bit-identical) and the Dot's own
+        [M, N] output never touches memory."""
+        if os.environ.get("GFB_TC_EPILOGUE", "1") != "1" or os.environ.get("GFB_TC_PAIR", "1") != "1":
+            return {}
+        out = {}
+        results = {r for r, _ in self.g.results}
+        nodes = self.nodes
+
+        def dense2(n, M, N):
+            return (tuple(nodes[n].output.shape) == (M, N) and self.layouts[(n, 0)].order == (0, 1)
+                    and nodes[n].output.element_type is ElementType.F32)
+
+        def plain(n):  # a node the epilogue may write: materialised, not claimed by other fusions
+            return (n in self.M and n not in self._row_nodes and n not in self.allreduce
+                    and n not in results and n not in self.tiny)
+
+        def splat_zero(n):
+            nd = nodes[n]
+            if nd.op is not OpKind.CONSTANT or not nd.attrs["data"].is_splat:
+                return False
+            v = nd.attrs["data"].splat_value()
+            return float(v) == 0.0 and not np.signbit(v)
+
+        for d in self.order:
+            nd = nodes[d]
+            if nd.op is not OpKind.DOT or not self.is_heavy(d) or nd.output.element_type is not ElementType.F32:
+                continue
+            M, N = nd.output.shape
+            Kd = nodes[nd.inputs[0][0]].output.shape[1]
+            if M < 256 or N < 256 or not use_tensor_cores(M, N, Kd) or len(self.consumers[d]) != 1 or d in results:
+                continue
+            c = self.consumers[d][0]
+            cn = nodes[c]
+            if cn.op is OpKind.ADD and plain(c) and dense2(c, M, N):
+                other = [r for r, _ in cn.inputs if r != d]
+                if len(other) != 1:
+                    continue
+                bc = nodes[other[0]]
+                if not (bc.op is OpKind.BROADCAST and tuple(bc.attrs["broadcast_axes"]) == (0,)
+                        and tuple(bc.inputs_shape) == (N,) and bc.id not in self.M):
+                    continue
+                bias = bc.inputs[0][0]
+                if not (self.is_source(bias) and nodes[bias].output.element_type is ElementType.F32):
+                    continue
+                relus = [r for r in self.consumers[c] if nodes[r].op is OpKind.RELU and plain(r) and dense2(r, M, N)]
+                if not relus:
+                    continue
+                out[d] = {"kind": 1, "out": c, "out2": relus[0], "bias": bias, "absorbed": {c, relus[0]},
+                          "lo_of": relus[0]}
+            elif cn.op is OpKind.MULTIPLY and plain(c) and dense2(c, M, N):
+                other = [r for r, _ in cn.inputs if r != d]
+                if len(other) != 1:
+                    continue
+                mk = nodes[other[0]]
+                if mk.op is not OpKind.MAXIMUM or mk.id in self.M or not splat_zero(mk.inputs[1][0]):
+                    continue
+                dv = nodes[mk.inputs[0][0]]
+                if dv.op is not OpKind.DIVIDE or dv.id in self.M:
+                    continue
+                h, x = dv.inputs[0][0], dv.inputs[1][0]
+                if not (self.is_source(h) and self.is_source(x) and dense2(h, M, N) and dense2(x, M, N)):
+                    continue
+                out[d] = {"kind": 2, "out": c, "aux1": h, "aux2": x, "absorbed": {c}, "lo_of": c}
+        return out
+
+    def _feeds_tc(self, n) -> bool:
+        """Some Dot reads `n` (directly or through index views) on the tensor cores."""
+        stack, seen = [n], set()
+        while stack:
+            x = stack.pop()
+            for c in self.consumers[x]:
+                if c in seen:
+                    continue
+                seen.add(c)
+                cn = self.nodes[c]
+                if cn.op in INDEX_OPS:
+                    stack.append(c)
+                elif cn.op is OpKind.DOT and self.is_heavy(c) and cn.output.element_type is ElementType.F32:
+                    m, k = self.nodes[cn.inputs[0][0]].output.shape
+                    if use_tensor_cores(m, cn.output.shape[1], k):
+                        return True
+        return False
+
     def _dense_root(self, src):
         """The whole dense arena buffer `src` views at offset 0, or None."""
         root = src.base if src.base is not None else src
@@ -1805,9 +1902,29 @@ class Lowering:
             grid = ((ncols + TC_TILE - 1) // TC_TILE, (m + TC_TILE - 1) // TC_TILE, splits)
         if grid[1] > 65535:
             raise UnsupportedOp(f"tensor-core GEMM with {m} rows exceeds the 65535-tile grid")
-        rec = LaunchRec(kind, grid, (block, 1, 1), smem, ta, [ahi.key, alo.key, bhi.key, blo.key], [target.key], label)
+        reads, writes = [ahi.key, alo.key, bhi.key, blo.key], [target.key]
+        refs = {"c": target, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo}
+        epi = self._epi.get(n) if hasattr(self, "_epi") else None
+        if epi is not None:
+            if not pair or splits > 1 or target.strides != (ncols, 1) or target.elem_off:
+                raise UnsupportedOp(f"fused epilogue of Dot {n} needs the unsplit pair kernel and a dense output")
+            ta.epi_kind = epi["kind"]
+            for field, key in (("e_bias", "bias"), ("e_aux1", "aux1"), ("e_aux2", "aux2"), ("e_out2", "out2")):
+                if key in epi:
+                    b = self.buf[epi[key]]
+                    refs[field] = b
+                    (writes if field == "e_out2" else reads).append(b.key)
+            y = self.buf[epi["lo_of"]]
+            root = self._dense_root(y)
+            if root is not None and self._feeds_tc(epi["lo_of"]) and ("lo", root.key) not in self.buf:
+                lo = Buffer(self.new_key(), ElementType.F32, root.shape, root.strides)
+                self.buf[("lo", root.key)] = lo  # _lo_plane finds it: no separate pass
+                refs["e_lo"] = lo
+                writes.append(lo.key)
+            label += ":epi" + ("bias_relu" if epi["kind"] == 1 else "relu_grad")
+        rec = LaunchRec(kind, grid, (block, 1, 1), smem, ta, reads, writes, label)
         rec.flops = 2 * m * ncols * kdim
-        rec.finalize = _finalize_refs(ta, {"c": target, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo})
+        rec.finalize = _finalize_refs(ta, refs)
         self.launches.append(rec)
         if splits > 1:
             # deterministic second pass: out[o] = sum over splits of scratch[z, o]
@@ -2159,6 +2276,11 @@ class Lowering:
 
     def emit_heavy(self, n: int):
         node = self.nodes[n]
+        if n in self._epi:
+            (ab, ast), (bb, bst) = self.operand(node.inputs[0][0]), self.operand(node.inputs[1][0])
+            m, k = self.nodes[node.inputs[0][0]].output.shape
+            self.emit_dot_tc(n, (ab, ast), (bb, bst), self.buf[self._epi[n]["out"]], m, node.output.shape[1], k)
+            return
         out = self.buf[n]
         et = node.output.element_type
         if node.op is not OpKind.DOT and self.emit_conv_tc(n):

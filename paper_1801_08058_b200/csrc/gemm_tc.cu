@@ -1302,7 +1302,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
             float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)T.z * p.split_stride : 0);
             const LinearRows rows{T.m0 + 128 * (int64_t)rank, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
             const int64_t roff = rows(q * 32 + lane);
-            if (roff >= 0) {
+            if (roff >= 0 && p.epi_kind != 0) {
+                // fused epilogue (gfb200.h gfb_tc_args): the elementwise map that
+                // consumed this Dot, computed from the registers, in 4-wide pieces
+                const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
+                const float* hin = p.e_aux1 ? resolve<const float>(p.tab, p.e_aux1) + roff : nullptr;
+                const float* xin = p.e_aux2 ? resolve<const float>(p.tab, p.e_aux2) + roff : nullptr;
+                float* out2 = p.e_out2 ? resolve<float>(p.tab, p.e_out2) + roff : nullptr;
+                float* lo = p.e_lo ? resolve<float>(p.tab, p.e_lo) + roff : nullptr;
+                float* dst = C + roff;
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    const int col0 = T.n0 + cg * EC + c * 32;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const int n = col0 + j;
+                        if (n >= p.N) break;
+                        float v[4] = {acc[c * 32 + j], acc[c * 32 + j + 1], acc[c * 32 + j + 2], acc[c * 32 + j + 3]};
+                        float y[4];  // the tensor a later GEMM may read raw (lo plane)
+                        const int cnt = min(4, (int)(p.N - n));
+                        const bool vec = cnt == 4 && ((roff + n) & 3) == 0;  // 16-byte pieces (bias: n % 4 == 0 too)
+                        if (p.epi_kind == 1) {
+                            float b[4];
+                            if (vec) {
+                                const float4 t4 = __ldg(reinterpret_cast<const float4*>(bias + n));
+                                b[0] = t4.x, b[1] = t4.y, b[2] = t4.z, b[3] = t4.w;
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) b[e] = e < cnt ? bias[n + e] : 0.f;
+                            }
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                v[e] = __fadd_rn(v[e], b[e]);
+                                y[e] = v[e] > 0.f ? v[e] : 0.f;
+                            }
+                        } else {
+                            float hh[4], xx[4];
+                            if (vec) {
+                                const float4 h4 = __ldg(reinterpret_cast<const float4*>(hin + n));
+                                const float4 x4 = __ldg(reinterpret_cast<const float4*>(xin + n));
+                                hh[0] = h4.x, hh[1] = h4.y, hh[2] = h4.z, hh[3] = h4.w;
+                                xx[0] = x4.x, xx[1] = x4.y, xx[2] = x4.z, xx[3] = x4.w;
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    hh[e] = e < cnt ? hin[n + e] : 0.f;
+                                    xx[e] = e < cnt ? xin[n + e] : 1.f;
+                                }
+                            }
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float r = __fdiv_rn(hh[e], xx[e]);
+                                v[e] = __fmul_rn(v[e], r >= 0.f ? r : 0.f);
+                                y[e] = v[e];
+                            }
+                        }
+                        float l[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) l[e] = __fsub_rn(y[e], __uint_as_float(__float_as_uint(y[e]) & 0xffffe000u));
+                        if (vec) {
+                            *reinterpret_cast<float4*>(dst + n) = make_float4(v[0], v[1], v[2], v[3]);
+                            if (out2) *reinterpret_cast<float4*>(out2 + n) = make_float4(y[0], y[1], y[2], y[3]);
+                            if (lo) *reinterpret_cast<float4*>(lo + n) = make_float4(l[0], l[1], l[2], l[3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                if (e >= cnt) break;
+                                dst[n + e] = v[e];
+                                if (out2) out2[n + e] = y[e];
+                                if (lo) lo[n + e] = l[e];
+                            }
+                        }
+                    }
+                }
+            } else if (roff >= 0) {
                 float* dst = C + roff;
 #pragma unroll
                 for (int c = 0; c < EC / 32; ++c) {

@@ -339,6 +339,21 @@ def run_tc(mem, a):
         sl = slice(k0, k1)
         c = (A[0][:, sl] @ B[0][:, sl].T + A[0][:, sl] @ B[1][:, sl].T + A[1][:, sl] @ B[0][:, sl].T).astype(np.float32)
         base = z * a.split_stride if splits > 1 else 0
+        if a.epi_kind:  # fused epilogue (gfb200.h gfb_tc_args): dense [M, N] operands, pitch N
+            with np.errstate(all="ignore"):
+                if a.epi_kind == 1:
+                    c = (c + mem.view(a.e_bias, np.float32)[: a.N][None, :]).astype(np.float32)
+                    y = np.where(c > 0, c, np.float32(0)).astype(np.float32)
+                    mem.view(a.e_out2, np.float32)[: a.M * a.N] = y.reshape(-1)
+                else:
+                    h = mem.view(a.e_aux1, np.float32)[: a.M * a.N].reshape(a.M, a.N)
+                    x = mem.view(a.e_aux2, np.float32)[: a.M * a.N].reshape(a.M, a.N)
+                    r = (h / x).astype(np.float32)
+                    c = (c * np.where(r >= 0, r, np.float32(0))).astype(np.float32)
+                    y = c
+                if a.e_lo:
+                    hi = (np.ascontiguousarray(y).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+                    mem.view(a.e_lo, np.float32)[: a.M * a.N] = (y - hi).astype(np.float32).reshape(-1)
         if a.c_rdiv > 0:
             off = (i // a.c_rdiv) * a.c_s_hi + (i % a.c_rdiv) * a.c_s_lo + j * a.c_sn
         else:
