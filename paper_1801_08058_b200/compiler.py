@@ -149,6 +149,7 @@ INDEX_LIMIT = 1 << 31
 TC_TILE = 128
 TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
 TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
+TC_SMEM_PAIR = TC_SMEM + 8 * 32 * 32 * 4  # + the epilogue warps' transpose tiles (gemm_tc.cu PCfg::SMEM_BYTES_PAIR)
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
@@ -1890,7 +1891,7 @@ class Lowering:
         if (a_mn or b_mn) and not pair:
             raise UnsupportedOp("MN-major tensor-core operands need the CTA-pair kernel")
         if pair:  # 2-SM CTA pairs, 256x256 tiles, persistent (gfb_gemm_tc2_kernel)
-            kind, block, smem = abi.K_DOT_TC32P, 320, TC_SMEM
+            kind, block, smem = abi.K_DOT_TC32P, 320, TC_SMEM_PAIR
             ntiles = ((ncols + 255) // 256) * ((m + 255) // 256) * splits
             pairs = NUM_SMS // 2 if os.environ.get("GFB_TC_PERSIST", "1") == "1" else ntiles
             grid = (2 * min(ntiles, pairs), 1, 1)

@@ -1057,6 +1057,10 @@ struct PCfg {
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int EPI_WARPS = 8;
     static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+    // per epilogue warp, a 32 x 32 fp32 transpose tile (16-byte pieces XOR-swizzled
+    // by row): the accumulators sit one row per lane, the stores go out row-contiguous
+    static constexpr int XPOSE_BYTES = EPI_WARPS * 32 * 32 * 4;
+    static constexpr int SMEM_BYTES_PAIR = STAGES * STAGE_BYTES + 1024 + 256 + XPOSE_BYTES;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -1302,7 +1306,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
             float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)T.z * p.split_stride : 0);
             const LinearRows rows{T.m0 + 128 * (int64_t)rank, p.M, p.c_sm, p.c_rdiv, p.c_s_hi, p.c_s_lo};
             const int64_t roff = rows(q * 32 + lane);
-            if (roff >= 0 && p.epi_kind != 0) {
+            // Coalesced path: every row of the tile is a dense run of the output
+            // (and of the epilogue's operands), row pitch c_sm, 16-byte aligned.
+            const bool coalesced = p.c_rdiv <= 0 && p.c_sn == 1 && (p.c_sm & 3) == 0 && (p.N & 3) == 0;
+            if (coalesced) {
+                float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024 + 256) + (warp - 2) * 1024;
+                const int64_t row0 = T.m0 + 128 * (int64_t)rank + q * 32;  // this warp's 32 rows
+                const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
+                const float* hin = p.e_aux1 ? resolve<const float>(p.tab, p.e_aux1) : nullptr;
+                const float* xin = p.e_aux2 ? resolve<const float>(p.tab, p.e_aux2) : nullptr;
+                float* out2 = p.e_out2 ? resolve<float>(p.tab, p.e_out2) : nullptr;
+                float* lo = p.e_lo ? resolve<float>(p.tab, p.e_lo) : nullptr;
+#pragma unroll
+                for (int c = 0; c < EC / 32; ++c) {
+                    // lane r writes its row's 32 values as 8 swizzled 16-byte pieces
+#pragma unroll
+                    for (int qd = 0; qd < 8; ++qd)
+                        *reinterpret_cast<float4*>(xt + lane * 32 + ((qd ^ (lane & 7)) << 2)) =
+                            make_float4(acc[c * 32 + 4 * qd], acc[c * 32 + 4 * qd + 1], acc[c * 32 + 4 * qd + 2],
+                                        acc[c * 32 + 4 * qd + 3]);
+                    __syncwarp();
+                    const int qd = lane & 7, col = T.n0 + cg * EC + c * 32 + 4 * qd;
+                    float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (p.epi_kind == 1 && col < p.N) b4 = __ldg(reinterpret_cast<const float4*>(bias + col));
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int rr = 4 * i + (lane >> 3);  // lanes 8k..8k+7 cover one 128-byte row piece
+                        const int64_t row = row0 + rr;
+                        float4 v = *reinterpret_cast<const float4*>(xt + rr * 32 + ((qd ^ (rr & 7)) << 2));
+                        if (row >= p.M || col >= p.N) continue;
+                        const int64_t off = row * p.c_sm + col;
+                        float4 y = v;  // the tensor a later GEMM may read raw (lo plane)
+                        if (p.epi_kind == 1) {
+                            v = make_float4(__fadd_rn(v.x, b4.x), __fadd_rn(v.y, b4.y), __fadd_rn(v.z, b4.z), __fadd_rn(v.w, b4.w));
+                            y = make_float4(v.x > 0.f ? v.x : 0.f, v.y > 0.f ? v.y : 0.f, v.z > 0.f ? v.z : 0.f, v.w > 0.f ? v.w : 0.f);
+                        } else if (p.epi_kind == 2) {
+                            const float4 h4 = __ldg(reinterpret_cast<const float4*>(hin + off));
+                            const float4 x4 = __ldg(reinterpret_cast<const float4*>(xin + off));
+                            const float r0 = __fdiv_rn(h4.x, x4.x), r1 = __fdiv_rn(h4.y, x4.y), r2 = __fdiv_rn(h4.z, x4.z),
+                                        r3 = __fdiv_rn(h4.w, x4.w);
+                            v = make_float4(__fmul_rn(v.x, r0 >= 0.f ? r0 : 0.f), __fmul_rn(v.y, r1 >= 0.f ? r1 : 0.f),
+                                            __fmul_rn(v.z, r2 >= 0.f ? r2 : 0.f), __fmul_rn(v.w, r3 >= 0.f ? r3 : 0.f));
+                            y = v;
+                        }
+                        *reinterpret_cast<float4*>(C + off) = v;
+                        if (out2) *reinterpret_cast<float4*>(out2 + off) = y;
+                        if (lo)
+                            *reinterpret_cast<float4*>(lo + off) = make_float4(
+                                __fsub_rn(y.x, __uint_as_float(__float_as_uint(y.x) & 0xffffe000u)),
+                                __fsub_rn(y.y, __uint_as_float(__float_as_uint(y.y) & 0xffffe000u)),
+                                __fsub_rn(y.z, __uint_as_float(__float_as_uint(y.z) & 0xffffe000u)),
+                                __fsub_rn(y.w, __uint_as_float(__float_as_uint(y.w) & 0xffffe000u)));
+                    }
+                    __syncwarp();
+                }
+            } else if (roff >= 0 && p.epi_kind != 0) {
                 // fused epilogue (gfb200.h gfb_tc_args): the elementwise map that
                 // consumed this Dot, computed from the registers, in 4-wide pieces
                 const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
@@ -2322,6 +2380,7 @@ extern "C" const void* gfb_tc_kernel_ptr(int kind) {
 }
 
 extern "C" int gfb_tc_smem_bytes(int wide) { return wide ? gfb::tc::Cfg<256>::SMEM_BYTES : gfb::tc::Cfg<128>::SMEM_BYTES; }
+extern "C" int gfb_tc_pair_smem_bytes(void) { return gfb::tc::PCfg::SMEM_BYTES_PAIR; }
 extern "C" int gfb_tcgw_smem_bytes(int bn) { return bn == 64 ? gfb::tc::WCfg<64>::SMEM_BYTES : gfb::tc::WCfg<128>::SMEM_BYTES; }
 extern "C" int gfb_stem_smem_bytes(void) { return gfb::tc::SCfg::SMEM_BYTES; }
 extern "C" int gfb_tcg_smem_bytes(int bn) { return bn == 64 ? gfb::tc::GCfg<64>::SMEM_BYTES : gfb::tc::GCfg<128>::SMEM_BYTES; }

@@ -298,3 +298,25 @@ def test_raw_hi_operands(monkeypatch, m, k, n, raw):
     exact = np.maximum(ins[0].astype(np.float64), 0).T @ (-ins[1].astype(np.float64)) if raw != "kmajor" else \
         np.maximum(ins[0].astype(np.float64), 0) @ ins[2].astype(np.float64)
     assert G.normwise(out, exact) <= 1e-5 and G.normwise(out, want) <= 1e-5
+
+
+@pytest.mark.parametrize("width,batch", [(512, 1024), (768, 2048)])
+def test_fused_epilogues_bit_identical(monkeypatch, width, batch):
+    """Bias + Relu after the forward Dot and the Relu-gradient mask after the
+    data-gradient Dot, applied in the pair GEMM's epilogue: the same IEEE ops
+    on the same accumulator values -> every result bit-identical to the plan
+    that runs them as separate maps."""
+    from paper_1801_08058_b200 import workloads as W
+
+    step = W.wide_mlp_step(gf, batch=batch, width=width, layers=3, loss_batch=65536)
+    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=6, x_range=(-1, 1))
+    tens = [gf.tensor_from_flat(F32, a.shape, a) for a in arrays]
+    monkeypatch.setenv("GFB_TC_EPILOGUE", "1")
+    exe = gf.compile_function(step.fn)
+    kinds = {L.args.epi_kind for L in exe.lowered.launches if L.label.startswith("dot_tc")}
+    assert kinds == {0, 1, 2}
+    fused = [t.to_numpy() for t in gf.call(exe, tens)]
+    monkeypatch.setenv("GFB_TC_EPILOGUE", "0")
+    plain = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
+    for a, b in zip(fused, plain):
+        assert G.same_bits(a, b)
