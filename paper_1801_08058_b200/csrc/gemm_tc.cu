@@ -1102,6 +1102,13 @@ __device__ __forceinline__ uint64_t smem_desc_mn_at(uint32_t addr) {
     d |= (uint64_t)1 << 61;
     return d;
 }
+// The Relu gradient's mask Maximum(Divide(Relu(x), x), 0) (autodiff.py:143-148)
+// as a function of x alone, value for value: Relu(x) / x is exactly 1 for
+// 0 < x < inf, -0 for x < 0 (0 / negative, including -inf), and NaN for
+// x = +-0, +inf, NaN, which Maximum(NaN, 0) turns into +0.
+__device__ __forceinline__ float relu_grad_mask(float x) {
+    return (x > 0.f && x < INFINITY) ? 1.f : (x < 0.f ? -0.f : 0.f);
+}
 __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -1310,10 +1317,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
             // (and of the epilogue's operands), row pitch c_sm, 16-byte aligned.
             const bool coalesced = p.c_rdiv <= 0 && p.c_sn == 1 && (p.c_sm & 3) == 0 && (p.N & 3) == 0;
             if (coalesced) {
-                float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024 + 256) + (warp - 2) * 1024;
+                // after the barriers (the first 256 B past the stages); the 1024 B of
+                // slack in the allocation are the alignment of `smem`, not an offset
+                float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
                 const int64_t row0 = T.m0 + 128 * (int64_t)rank + q * 32;  // this warp's 32 rows
                 const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
-                const float* hin = p.e_aux1 ? resolve<const float>(p.tab, p.e_aux1) : nullptr;
                 const float* xin = p.e_aux2 ? resolve<const float>(p.tab, p.e_aux2) : nullptr;
                 float* out2 = p.e_out2 ? resolve<float>(p.tab, p.e_out2) : nullptr;
                 float* lo = p.e_lo ? resolve<float>(p.tab, p.e_lo) : nullptr;
@@ -1330,7 +1338,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                     float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (p.epi_kind == 1 && col < p.N) b4 = __ldg(reinterpret_cast<const float4*>(bias + col));
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
+                    for (int half = 0; half < 2; ++half) {
+                    float4 x4[4];  // kind 2: four rows' pre-activations in flight at once
+                    if (p.epi_kind == 2) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int64_t row = row0 + 4 * (4 * half + i) + (lane >> 3);
+                            x4[i] = (row < p.M && col < p.N) ? __ldg(reinterpret_cast<const float4*>(xin + row * p.c_sm + col))
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    }
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const int i = 4 * half + ii;
                         const int rr = 4 * i + (lane >> 3);  // lanes 8k..8k+7 cover one 128-byte row piece
                         const int64_t row = row0 + rr;
                         float4 v = *reinterpret_cast<const float4*>(xt + rr * 32 + ((qd ^ (rr & 7)) << 2));
@@ -1341,12 +1361,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                             v = make_float4(__fadd_rn(v.x, b4.x), __fadd_rn(v.y, b4.y), __fadd_rn(v.z, b4.z), __fadd_rn(v.w, b4.w));
                             y = make_float4(v.x > 0.f ? v.x : 0.f, v.y > 0.f ? v.y : 0.f, v.z > 0.f ? v.z : 0.f, v.w > 0.f ? v.w : 0.f);
                         } else if (p.epi_kind == 2) {
-                            const float4 h4 = __ldg(reinterpret_cast<const float4*>(hin + off));
-                            const float4 x4 = __ldg(reinterpret_cast<const float4*>(xin + off));
-                            const float r0 = __fdiv_rn(h4.x, x4.x), r1 = __fdiv_rn(h4.y, x4.y), r2 = __fdiv_rn(h4.z, x4.z),
-                                        r3 = __fdiv_rn(h4.w, x4.w);
-                            v = make_float4(__fmul_rn(v.x, r0 >= 0.f ? r0 : 0.f), __fmul_rn(v.y, r1 >= 0.f ? r1 : 0.f),
-                                            __fmul_rn(v.z, r2 >= 0.f ? r2 : 0.f), __fmul_rn(v.w, r3 >= 0.f ? r3 : 0.f));
+                            v = make_float4(__fmul_rn(v.x, relu_grad_mask(x4[ii].x)), __fmul_rn(v.y, relu_grad_mask(x4[ii].y)),
+                                            __fmul_rn(v.z, relu_grad_mask(x4[ii].z)), __fmul_rn(v.w, relu_grad_mask(x4[ii].w)));
                             y = v;
                         }
                         *reinterpret_cast<float4*>(C + off) = v;
@@ -1358,13 +1374,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                                 __fsub_rn(y.z, __uint_as_float(__float_as_uint(y.z) & 0xffffe000u)),
                                 __fsub_rn(y.w, __uint_as_float(__float_as_uint(y.w) & 0xffffe000u)));
                     }
+                    }
                     __syncwarp();
                 }
             } else if (roff >= 0 && p.epi_kind != 0) {
                 // fused epilogue (gfb200.h gfb_tc_args): the elementwise map that
                 // consumed this Dot, computed from the registers, in 4-wide pieces
                 const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
-                const float* hin = p.e_aux1 ? resolve<const float>(p.tab, p.e_aux1) + roff : nullptr;
                 const float* xin = p.e_aux2 ? resolve<const float>(p.tab, p.e_aux2) + roff : nullptr;
                 float* out2 = p.e_out2 ? resolve<float>(p.tab, p.e_out2) + roff : nullptr;
                 float* lo = p.e_lo ? resolve<float>(p.tab, p.e_lo) + roff : nullptr;
@@ -1395,23 +1411,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                                 y[e] = v[e] > 0.f ? v[e] : 0.f;
                             }
                         } else {
-                            float hh[4], xx[4];
-                            if (vec) {
-                                const float4 h4 = __ldg(reinterpret_cast<const float4*>(hin + n));
-                                const float4 x4 = __ldg(reinterpret_cast<const float4*>(xin + n));
-                                hh[0] = h4.x, hh[1] = h4.y, hh[2] = h4.z, hh[3] = h4.w;
-                                xx[0] = x4.x, xx[1] = x4.y, xx[2] = x4.z, xx[3] = x4.w;
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    hh[e] = e < cnt ? hin[n + e] : 0.f;
-                                    xx[e] = e < cnt ? xin[n + e] : 1.f;
-                                }
-                            }
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                const float r = __fdiv_rn(hh[e], xx[e]);
-                                v[e] = __fmul_rn(v[e], r >= 0.f ? r : 0.f);
+                                v[e] = __fmul_rn(v[e], relu_grad_mask(e < cnt ? xin[n + e] : 1.f));
                                 y[e] = v[e];
                             }
                         }

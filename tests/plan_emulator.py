@@ -345,10 +345,9 @@ def run_tc(mem, a):
                     c = (c + mem.view(a.e_bias, np.float32)[: a.N][None, :]).astype(np.float32)
                     y = np.where(c > 0, c, np.float32(0)).astype(np.float32)
                     mem.view(a.e_out2, np.float32)[: a.M * a.N] = y.reshape(-1)
-                else:
-                    h = mem.view(a.e_aux1, np.float32)[: a.M * a.N].reshape(a.M, a.N)
+                else:  # the Relu-gradient mask, evaluated the graph's way: Maximum(Relu(x) / x, 0)
                     x = mem.view(a.e_aux2, np.float32)[: a.M * a.N].reshape(a.M, a.N)
-                    r = (h / x).astype(np.float32)
+                    r = (np.where(x > 0, x, np.float32(0)) / x).astype(np.float32)
                     c = (c * np.where(r >= 0, r, np.float32(0))).astype(np.float32)
                     y = c
                 if a.e_lo:
