@@ -258,8 +258,9 @@ typedef struct GFB_ALIGN64 {
      * later GEMM reads as its TF32 hi operand (y = e_out2 for kind 1, C for
      * kind 2).  Each op is the unfused plan's IEEE op: bit-identical. */
     int64_t epi_kind;
-    uint64_t e_bias, e_aux1, e_aux2, e_out2, e_lo; /* GFB_REF */
-    int64_t pad[4];
+    uint64_t e_bias, e_aux1, e_aux2, e_out2, e_lo; /* GFB_REF (an arena ref may be 0: presence is in epi_flags) */
+    int64_t epi_flags; /* bit 0: e_out2 is written, bit 1: e_lo is written */
+    int64_t pad[3];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

@@ -98,8 +98,8 @@ class TcArgs(C.Structure):
         ("k_splits", C.c_int64), ("k_per_split", C.c_int64), ("split_stride", C.c_int64),
         ("a_ld_mn", C.c_int64), ("b_ld_mn", C.c_int64), ("group_m", C.c_int64),
         ("epi_kind", C.c_int64), ("e_bias", C.c_uint64), ("e_aux1", C.c_uint64), ("e_aux2", C.c_uint64),
-        ("e_out2", C.c_uint64), ("e_lo", C.c_uint64),
-        ("pad", C.c_int64 * 4),
+        ("e_out2", C.c_uint64), ("e_lo", C.c_uint64), ("epi_flags", C.c_int64),
+        ("pad", C.c_int64 * 3),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
 

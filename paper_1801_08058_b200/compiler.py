@@ -1715,7 +1715,8 @@ class Lowering:
                 continue
             c = self.consumers[d][0]
             cn = nodes[c]
-            if cn.op is OpKind.ADD and plain(c) and dense2(c, M, N):
+            kinds = os.environ.get("GFB_TC_EPILOGUE_KINDS", "1,2").split(",")
+            if cn.op is OpKind.ADD and "1" in kinds and plain(c) and dense2(c, M, N):
                 other = [r for r, _ in cn.inputs if r != d]
                 if len(other) != 1:
                     continue
@@ -1731,7 +1732,7 @@ class Lowering:
                     continue
                 out[d] = {"kind": 1, "out": c, "out2": relus[0], "bias": bias, "absorbed": {c, relus[0]},
                           "lo_of": relus[0]}
-            elif cn.op is OpKind.MULTIPLY and plain(c) and dense2(c, M, N):
+            elif cn.op is OpKind.MULTIPLY and "2" in kinds and plain(c) and dense2(c, M, N):
                 other = [r for r, _ in cn.inputs if r != d]
                 if len(other) != 1:
                     continue
@@ -1915,6 +1916,7 @@ class Lowering:
                     b = self.buf[epi[key]]
                     refs[field] = b
                     (writes if field == "e_out2" else reads).append(b.key)
+            ta.epi_flags = 1 if "out2" in epi else 0
             y = self.buf[epi["lo_of"]]
             root = self._dense_root(y)
             if root is not None and self._feeds_tc(epi["lo_of"]) and ("lo", root.key) not in self.buf:
@@ -1922,6 +1924,7 @@ class Lowering:
                 self.buf[("lo", root.key)] = lo  # _lo_plane finds it: no separate pass
                 refs["e_lo"] = lo
                 writes.append(lo.key)
+                ta.epi_flags |= 2
             label += ":epi" + ("bias_relu" if epi["kind"] == 1 else "relu_grad")
         rec = LaunchRec(kind, grid, (block, 1, 1), smem, ta, reads, writes, label)
         rec.flops = 2 * m * ncols * kdim

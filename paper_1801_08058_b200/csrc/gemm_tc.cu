@@ -1321,10 +1321,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
                 // slack in the allocation are the alignment of `smem`, not an offset
                 float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
                 const int64_t row0 = T.m0 + 128 * (int64_t)rank + q * 32;  // this warp's 32 rows
-                const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
-                const float* xin = p.e_aux2 ? resolve<const float>(p.tab, p.e_aux2) : nullptr;
-                float* out2 = p.e_out2 ? resolve<float>(p.tab, p.e_out2) : nullptr;
-                float* lo = p.e_lo ? resolve<float>(p.tab, p.e_lo) : nullptr;
+                // refs are (slot, offset): arena offset 0 encodes as 0, so presence comes from the kind / flags
+                const float* bias = p.epi_kind == 1 ? resolve<const float>(p.tab, p.e_bias) : nullptr;
+                const float* xin = p.epi_kind == 2 ? resolve<const float>(p.tab, p.e_aux2) : nullptr;
+                float* out2 = (p.epi_flags & 1) ? resolve<float>(p.tab, p.e_out2) : nullptr;
+                float* lo = (p.epi_flags & 2) ? resolve<float>(p.tab, p.e_lo) : nullptr;
 #pragma unroll
                 for (int c = 0; c < EC / 32; ++c) {
                     // lane r writes its row's 32 values as 8 swizzled 16-byte pieces
@@ -1380,10 +1381,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
             } else if (roff >= 0 && p.epi_kind != 0) {
                 // fused epilogue (gfb200.h gfb_tc_args): the elementwise map that
                 // consumed this Dot, computed from the registers, in 4-wide pieces
-                const float* bias = p.e_bias ? resolve<const float>(p.tab, p.e_bias) : nullptr;
-                const float* xin = p.e_aux2 ? resolve<const float>(p.tab, p.e_aux2) + roff : nullptr;
-                float* out2 = p.e_out2 ? resolve<float>(p.tab, p.e_out2) + roff : nullptr;
-                float* lo = p.e_lo ? resolve<float>(p.tab, p.e_lo) + roff : nullptr;
+                const float* bias = p.epi_kind == 1 ? resolve<const float>(p.tab, p.e_bias) : nullptr;
+                const float* xin = p.epi_kind == 2 ? resolve<const float>(p.tab, p.e_aux2) + roff : nullptr;
+                float* out2 = (p.epi_flags & 1) ? resolve<float>(p.tab, p.e_out2) + roff : nullptr;
+                float* lo = (p.epi_flags & 2) ? resolve<float>(p.tab, p.e_lo) + roff : nullptr;
                 float* dst = C + roff;
 #pragma unroll
                 for (int c = 0; c < EC / 32; ++c) {

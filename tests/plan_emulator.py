@@ -350,7 +350,7 @@ def run_tc(mem, a):
                     r = (np.where(x > 0, x, np.float32(0)) / x).astype(np.float32)
                     c = (c * np.where(r >= 0, r, np.float32(0))).astype(np.float32)
                     y = c
-                if a.e_lo:
+                if a.epi_flags & 2:
                     hi = (np.ascontiguousarray(y).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
                     mem.view(a.e_lo, np.float32)[: a.M * a.N] = (y - hi).astype(np.float32).reshape(-1)
         if a.c_rdiv > 0:
