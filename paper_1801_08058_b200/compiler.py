@@ -1711,8 +1711,9 @@ class Lowering:
                 continue
             M, N = nd.output.shape
             Kd = nodes[nd.inputs[0][0]].output.shape[1]
-            if M < 256 or N < 256 or not use_tensor_cores(M, N, Kd) or len(self.consumers[d]) != 1 or d in results:
-                continue
+            if (M < 256 or N < 256 or not use_tensor_cores(M, N, Kd) or len(self.consumers[d]) != 1 or d in results
+                    or self._tc_splits(M, N, Kd) > 1):
+                continue  # (a split-K GEMM writes partials: no place for an epilogue)
             c = self.consumers[d][0]
             cn = nodes[c]
             kinds = os.environ.get("GFB_TC_EPILOGUE_KINDS", "1,2").split(",")
@@ -1853,6 +1854,28 @@ class Lowering:
         (ahi, alo, kpa), (bhi, blo, kpb) = a[:3], b[:3]
         a_mn = a[3] if len(a) > 3 else 0
         b_mn = b[3] if len(b) > 3 else 0
+        splits = self._tc_splits(m, ncols, kdim)
+        tiles = ((ncols + TC_TILE - 1) // TC_TILE) * ((m + TC_TILE - 1) // TC_TILE)
+        kblocks = (kdim + 31) // 32
+        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn,
+                        group_m=int(os.environ.get("GFB_TC_GROUP_M", "1")))
+        target = out
+        if splits > 1:
+            per = ((kblocks + splits - 1) // splits) * 32
+            splits = (kdim + per - 1) // per
+            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
+            self.buf[("splitk", n)] = scratch
+            ta.k_splits, ta.k_per_split, ta.split_stride = splits, per, m * ncols
+            ta.c_sm, ta.c_sn = ncols, 1
+            target = scratch
+        else:
+            for k_, v_ in addr.items():
+                setattr(ta, k_, v_)
+        return self._tc_gemm_emit(n, ahi, alo, bhi, blo, ta, target, out, m, ncols, kdim, splits, addr, label)
+
+    @staticmethod
+    def _tc_splits(m, ncols, kdim) -> int:
+        """K splits of a tensor-core GEMM (see _tc_gemm)."""
         tiles = ((ncols + TC_TILE - 1) // TC_TILE) * ((m + TC_TILE - 1) // TC_TILE)
         kblocks = (kdim + 31) // 32
         splits = 1
@@ -1873,20 +1896,10 @@ class Lowering:
         elif tiles <= 8 and kblocks >= 16:
             # a handful of tiles over a medium K (an MLP's first layer): spread K
             splits = max(1, min(NUM_SMS // tiles, kblocks // 4))
-        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn,
-                        group_m=int(os.environ.get("GFB_TC_GROUP_M", "1")))
-        target = out
-        if splits > 1:
-            per = ((kblocks + splits - 1) // splits) * 32
-            splits = (kdim + per - 1) // per
-            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
-            self.buf[("splitk", n)] = scratch
-            ta.k_splits, ta.k_per_split, ta.split_stride = splits, per, m * ncols
-            ta.c_sm, ta.c_sn = ncols, 1
-            target = scratch
-        else:
-            for k_, v_ in addr.items():
-                setattr(ta, k_, v_)
+        return splits
+
+    def _tc_gemm_emit(self, n, ahi, alo, bhi, blo, ta, target, out, m, ncols, kdim, splits, addr, label):
+        a_mn, b_mn = ta.a_ld_mn, ta.b_ld_mn
         wide = ncols >= 256 and os.environ.get("GFB_TC_WIDE", "1") == "1"
         pair = wide and m >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1"
         if (a_mn or b_mn) and not pair:
@@ -1933,7 +1946,7 @@ class Lowering:
         if splits > 1:
             # deterministic second pass: out[o] = sum over splits of scratch[z, o]
             p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
-            k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            k = p2.leaf(target, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])  # the split-K scratch
             p2.emit(I_LOAD, k=k)
             p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
             p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
@@ -2012,7 +2025,7 @@ class Lowering:
             self._col_launch(p2, mo * ncols, splits, 1, label + ":splitk", ElementType.F32)
         elif splits > 1:
             p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
-            k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            k = p2.leaf(target, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])  # the split-K scratch
             p2.emit(I_LOAD, k=k)
             p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
             p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
@@ -2119,7 +2132,7 @@ class Lowering:
         self.launches.append(rec)
         if splits > 1:
             p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
-            k = p2.leaf(scratch, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            k = p2.leaf(target, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])  # the split-K scratch
             p2.emit(I_LOAD, k=k)
             p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
             p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)

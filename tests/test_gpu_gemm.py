@@ -313,7 +313,9 @@ def test_fused_epilogues_bit_identical(monkeypatch, width, batch):
     tens = [gf.tensor_from_flat(F32, a.shape, a) for a in arrays]
     monkeypatch.setenv("GFB_TC_EPILOGUE", "1")
     exe = gf.compile_function(step.fn)
-    kinds = {L.args.epi_kind for L in exe.lowered.launches if L.label.startswith("dot_tc")}
+    from paper_1801_08058_b200 import abi
+
+    kinds = {L.args.epi_kind for L in exe.lowered.launches if L.kind == abi.K_DOT_TC32P}
     assert kinds == {0, 1, 2}
     fused = [t.to_numpy() for t in gf.call(exe, tens)]
     monkeypatch.setenv("GFB_TC_EPILOGUE", "0")
