@@ -584,7 +584,9 @@ def bench_step(args, ws, rank, local):
                    "h2d_bytes_per_step": ws * sum(a.nbytes for a in arrays),
                    "d2h_bytes_per_step": ws * sum(t.buffer.nbytes for t in host_out),
                    "api": "paper_1801_08058_b200.call(exe, pinned host TensorValues, out=pinned host TensorValues) "
-                          "on every rank (its batch shard; replicated parameters), wall clock, max over ranks"}
+                          "on every rank (its batch shard; replicated parameters), wall clock, max over ranks; the "
+                          "copies run inside the step's CUDA graph (gfb_exe_run_host): inputs in first-use order "
+                          "under the launches that do not need them yet, each result right after its last writer"}
     return line
 
 

@@ -413,6 +413,19 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out);
 /* inputs[i] / outputs[j]: device pointers for this run (caller-owned). */
 int gfb_exe_run(gfb_exe* exe, void* const* inputs, void* const* outputs, void* stream);
 int gfb_exe_destroy(gfb_exe* exe);
+/* Host-buffer runs.  gfb_exe_set_io gives the byte size of every input and
+ * result, the inputs each launch reads (CSR over the launch list:
+ * reads[read_offsets[i] .. read_offsets[i + 1])) and the last launch writing
+ * each result, and allocates device staging buffers for them.
+ * gfb_exe_run_host then runs one step on page-locked host buffers: the H2D
+ * copies (in first-use order, one stream), the launches (each waiting only
+ * for the copies of the inputs it reads) and the D2H copies (each right
+ * after the last writer of its result) are one CUDA graph, so the copies
+ * overlap the step.  Results are in host_outputs once `stream` reaches the
+ * run's end.  Replaces interpreter.py:191-245 `call` on host TensorValues. */
+int gfb_exe_set_io(gfb_exe* exe, const uint64_t* in_bytes, const uint64_t* out_bytes, const uint32_t* read_offsets,
+                   const uint32_t* reads, const uint32_t* out_writer);
+int gfb_exe_run_host(gfb_exe* exe, const void* const* host_inputs, void* const* host_outputs, void* stream);
 /* Number of kernels one run launches (for bench accounting). */
 int gfb_exe_num_launches(const gfb_exe* exe);
 /* Launch only record `index` of the plan (profiling / per-kernel timing). */

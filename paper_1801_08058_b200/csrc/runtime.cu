@@ -199,6 +199,22 @@ struct gfb_exe {
     std::vector<cudaEvent_t> done;
     cudaEvent_t fork = nullptr;
     std::vector<cudaEvent_t> joins;
+    // host-buffer runs (gfb_exe_set_io / gfb_exe_run_host): device staging
+    // buffers of the inputs and results, the inputs each launch reads (CSR)
+    // and the last launch writing each result; a second CUDA graph holds the
+    // H2D / D2H copies next to the launches
+    bool io_set = false;
+    std::vector<uint64_t> in_bytes, out_bytes;
+    std::vector<void*> dev_in, dev_out;
+    std::vector<uint32_t> rd_off, rd, out_writer, in_order;
+    cudaGraph_t hgraph = nullptr;
+    cudaGraphExec_t hexec = nullptr;
+    std::vector<cudaGraphNode_t> h2d_node, d2h_node;
+    std::vector<const void*> cur_hin;
+    std::vector<void*> cur_hout;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> in_ev, wr_ev;
+    cudaEvent_t io_fork = nullptr, h2d_join = nullptr, d2h_join = nullptr;
 };
 
 namespace {
@@ -291,6 +307,119 @@ int mark_done(gfb_exe* e, cudaStream_t s) {
     return GFB_OK;
 }
 
+void drop_host_graph(gfb_exe* e) {
+    if (e->hexec) cudaGraphExecDestroy(e->hexec);
+    if (e->hgraph) cudaGraphDestroy(e->hgraph);
+    e->hexec = nullptr;
+    e->hgraph = nullptr;
+}
+
+void drop_graphs(gfb_exe* e) {
+    if (e->graph) cudaGraphExecDestroy(e->graph);
+    e->graph = nullptr;
+    drop_host_graph(e);
+}
+
+void release_io(gfb_exe* e) {
+    for (void* p : e->dev_in) cudaFree(p);
+    for (void* p : e->dev_out) cudaFree(p);
+    for (cudaEvent_t ev : e->in_ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->wr_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->io_fork) cudaEventDestroy(e->io_fork);
+    if (e->h2d_join) cudaEventDestroy(e->h2d_join);
+    if (e->d2h_join) cudaEventDestroy(e->d2h_join);
+    if (e->h2d) cudaStreamDestroy(e->h2d);
+    if (e->d2h) cudaStreamDestroy(e->d2h);
+    e->dev_in.clear();
+    e->dev_out.clear();
+    e->in_ev.clear();
+    e->wr_ev.clear();
+    e->io_fork = e->h2d_join = e->d2h_join = nullptr;
+    e->h2d = e->d2h = nullptr;
+    e->io_set = false;
+}
+
+// Capture of a host-buffer run: the inputs' H2D copies run on their own
+// stream in first-use order, and each launch waits only for the copies of
+// the inputs it reads, so the step starts as soon as its first operand has
+// arrived and later inputs (weights, targets) cross PCIe under the forward
+// pass; each result's D2H copy runs on a third stream right after the last
+// launch writing it, under the rest of the step.
+int launch_all_io(gfb_exe* e, cudaStream_t s0, const void* const* hin, void* const* hout) {
+    const bool multi = e->n_streams > 1;
+    CUDA_TRY(cudaEventRecord(e->io_fork, s0));
+    CUDA_TRY(cudaStreamWaitEvent(e->h2d, e->io_fork, 0));
+    CUDA_TRY(cudaStreamWaitEvent(e->d2h, e->io_fork, 0));
+    if (multi)
+        for (uint32_t k = 1; k < e->n_streams; ++k) CUDA_TRY(cudaStreamWaitEvent(e->streams[k], e->io_fork, 0));
+    for (uint32_t i : e->in_order) {
+        CUDA_TRY(cudaMemcpyAsync(e->dev_in[i], hin[i], e->in_bytes[i], cudaMemcpyHostToDevice, e->h2d));
+        CUDA_TRY(cudaEventRecord(e->in_ev[i], e->h2d));
+    }
+    std::vector<char> waited(e->n_in * (size_t)(multi ? e->n_streams : 1), 0);
+    for (size_t i = 0; i < e->launches.size(); ++i) {
+        const uint32_t sk = multi ? e->stream_of[i] : 0;
+        cudaStream_t st = sk == 0 ? s0 : e->streams[sk];
+        if (multi)
+            for (uint32_t d = e->dep_off[i]; d < e->dep_off[i + 1]; ++d) {
+                const uint32_t j = e->deps[d];
+                if (e->stream_of[j] != sk) CUDA_TRY(cudaStreamWaitEvent(st, e->done[j], 0));
+            }
+        for (uint32_t r = e->rd_off[i]; r < e->rd_off[i + 1]; ++r) {
+            char& w = waited[(size_t)sk * e->n_in + e->rd[r]];
+            if (!w) CUDA_TRY(cudaStreamWaitEvent(st, e->in_ev[e->rd[r]], 0));
+            w = 1;
+        }
+        int rc = launch_one(e, i, st);
+        if (rc != GFB_OK) return rc;
+        if (multi) CUDA_TRY(cudaEventRecord(e->done[i], st));
+        if (e->wr_ev[i]) {
+            CUDA_TRY(cudaEventRecord(e->wr_ev[i], st));
+            CUDA_TRY(cudaStreamWaitEvent(e->d2h, e->wr_ev[i], 0));
+            for (uint32_t j = 0; j < e->n_out; ++j)
+                if (e->out_writer[j] == i)
+                    CUDA_TRY(cudaMemcpyAsync(hout[j], e->dev_out[j], e->out_bytes[j], cudaMemcpyDeviceToHost, e->d2h));
+        }
+    }
+    if (multi)
+        for (uint32_t k = 1; k < e->n_streams; ++k) {
+            CUDA_TRY(cudaEventRecord(e->joins[k], e->streams[k]));
+            CUDA_TRY(cudaStreamWaitEvent(s0, e->joins[k], 0));
+        }
+    CUDA_TRY(cudaEventRecord(e->h2d_join, e->h2d));
+    CUDA_TRY(cudaStreamWaitEvent(s0, e->h2d_join, 0));
+    CUDA_TRY(cudaEventRecord(e->d2h_join, e->d2h));
+    CUDA_TRY(cudaStreamWaitEvent(s0, e->d2h_join, 0));
+    return GFB_OK;
+}
+
+// The memcpy nodes of a captured host-buffer graph, found by their device
+// staging address, so later runs retarget them at new host buffers.
+bool find_copy_nodes(gfb_exe* e) {
+    size_t n = 0;
+    if (cudaGraphGetNodes(e->hgraph, nullptr, &n) != cudaSuccess) return false;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (cudaGraphGetNodes(e->hgraph, nodes.data(), &n) != cudaSuccess) return false;
+    e->h2d_node.assign(e->n_in, nullptr);
+    e->d2h_node.assign(e->n_out, nullptr);
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeMemcpy) continue;
+        cudaMemcpy3DParms p;
+        if (cudaGraphMemcpyNodeGetParams(nd, &p) != cudaSuccess) return false;
+        for (uint32_t i = 0; i < e->n_in; ++i)
+            if (p.dstPtr.ptr == e->dev_in[i]) e->h2d_node[i] = nd;
+        for (uint32_t j = 0; j < e->n_out; ++j)
+            if (p.srcPtr.ptr == e->dev_out[j]) e->d2h_node[j] = nd;
+    }
+    for (uint32_t i : e->in_order)
+        if (!e->h2d_node[i]) return false;
+    for (uint32_t j = 0; j < e->n_out; ++j)
+        if (!e->d2h_node[j]) return false;
+    return true;
+}
+
 void release_schedule(gfb_exe* e) {
     for (size_t k = 1; k < e->streams.size(); ++k) cudaStreamDestroy(e->streams[k]);
     for (cudaEvent_t ev : e->done) cudaEventDestroy(ev);
@@ -307,8 +436,9 @@ void release(gfb_exe* e) {
     if (e->ran && e->run_done) cudaEventSynchronize(e->run_done);
     if (e->nccl_reg && e->comm && g_nccl.CommDeregister) g_nccl.CommDeregister(e->comm->comm, e->nccl_reg);
     release_schedule(e);
+    drop_graphs(e);
+    release_io(e);
     if (e->run_done) cudaEventDestroy(e->run_done);
-    if (e->graph) cudaGraphExecDestroy(e->graph);
     if (e->capture_stream) cudaStreamDestroy(e->capture_stream);
     if (e->tab_done) cudaEventDestroy(e->tab_done);
     if (e->htab) cudaFreeHost(e->htab);
@@ -514,6 +644,133 @@ int gfb_exe_run_one(gfb_exe* e, uint32_t index, void* const* inputs, void* const
     return rc != GFB_OK ? rc : mark_done(e, s);
 }
 
+int gfb_exe_set_io(gfb_exe* e, const uint64_t* in_bytes, const uint64_t* out_bytes, const uint32_t* read_offsets,
+                   const uint32_t* reads, const uint32_t* out_writer) {
+    if (!e || (e->n_in && !in_bytes) || (e->n_out && (!out_bytes || !out_writer)) || !read_offsets)
+        return fail(GFB_ERR_INVALID, "gfb_exe_set_io: null argument");
+    std::lock_guard<std::mutex> lk(e->mu);
+    const size_t n = e->launches.size();
+    if (read_offsets[0] != 0) return fail(GFB_ERR_INVALID, "gfb_exe_set_io: read_offsets[0] must be 0");
+    for (size_t i = 0; i < n; ++i) {
+        if (read_offsets[i + 1] < read_offsets[i]) return fail(GFB_ERR_INVALID, "gfb_exe_set_io: offsets not monotone");
+        for (uint32_t r = read_offsets[i]; r < read_offsets[i + 1]; ++r)
+            if (reads[r] >= e->n_in) return fail(GFB_ERR_INVALID, "gfb_exe_set_io: input index out of range");
+    }
+    for (uint32_t j = 0; j < e->n_out; ++j)
+        if (out_writer[j] >= n) return fail(GFB_ERR_INVALID, "gfb_exe_set_io: every result needs a writing launch");
+    if (e->ran) CUDA_TRY(cudaEventSynchronize(e->run_done));  // a host-buffer run may still use the old buffers
+    drop_graphs(e);
+    release_io(e);
+    e->in_bytes.assign(in_bytes, in_bytes + e->n_in);
+    e->out_bytes.assign(out_bytes, out_bytes + e->n_out);
+    e->rd_off.assign(read_offsets, read_offsets + n + 1);
+    e->rd.assign(reads, reads + read_offsets[n]);
+    e->out_writer.assign(out_writer, out_writer + e->n_out);
+    // inputs in order of their first reader; unread inputs are never copied
+    std::vector<uint32_t> first(e->n_in, UINT32_MAX);
+    for (size_t i = n; i-- > 0;)
+        for (uint32_t r = e->rd_off[i]; r < e->rd_off[i + 1]; ++r) first[e->rd[r]] = (uint32_t)i;
+    e->in_order.clear();
+    for (size_t i = 0; i < n; ++i)
+        for (uint32_t k = 0; k < e->n_in; ++k)
+            if (first[k] == i) e->in_order.push_back(k);
+    e->dev_in.assign(e->n_in, nullptr);
+    e->dev_out.assign(e->n_out, nullptr);
+    e->in_ev.assign(e->n_in, nullptr);
+    e->wr_ev.assign(n, nullptr);
+    auto bail = [&](cudaError_t err) {
+        release_io(e);
+        return fail(GFB_ERR_CUDA, std::string("gfb_exe_set_io: ") + cudaGetErrorString(err));
+    };
+    cudaError_t err;
+    for (uint32_t i = 0; i < e->n_in; ++i)
+        if ((err = cudaMalloc(&e->dev_in[i], e->in_bytes[i] ? e->in_bytes[i] : 1)) != cudaSuccess ||
+            (err = cudaEventCreateWithFlags(&e->in_ev[i], cudaEventDisableTiming)) != cudaSuccess)
+            return bail(err);
+    for (uint32_t j = 0; j < e->n_out; ++j) {
+        if ((err = cudaMalloc(&e->dev_out[j], e->out_bytes[j] ? e->out_bytes[j] : 1)) != cudaSuccess) return bail(err);
+        if (!e->wr_ev[e->out_writer[j]] &&
+            (err = cudaEventCreateWithFlags(&e->wr_ev[e->out_writer[j]], cudaEventDisableTiming)) != cudaSuccess)
+            return bail(err);
+    }
+    if ((err = cudaEventCreateWithFlags(&e->io_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (err = cudaEventCreateWithFlags(&e->h2d_join, cudaEventDisableTiming)) != cudaSuccess ||
+        (err = cudaEventCreateWithFlags(&e->d2h_join, cudaEventDisableTiming)) != cudaSuccess ||
+        (err = cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (err = cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(err);
+    e->io_set = true;
+    return GFB_OK;
+}
+
+int gfb_exe_run_host(gfb_exe* e, const void* const* host_inputs, void* const* host_outputs, void* stream) {
+    if (!e) return fail(GFB_ERR_INVALID, "null executable");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (!e->io_set) return fail(GFB_ERR_INVALID, "gfb_exe_run_host before gfb_exe_set_io");
+    for (uint32_t i = 0; i < e->n_in + e->n_out; ++i) {
+        const void* p = i < e->n_in ? host_inputs[i] : host_outputs[i - e->n_in];
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            return fail(GFB_ERR_INVALID, "gfb_exe_run_host: host buffer " + std::to_string(i) + " is not page-locked");
+        }
+    }
+    cudaStream_t s = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    int rc = upload_table(e, e->dev_in.data(), e->dev_out.data(), s);
+    if (rc != GFB_OK) return rc;
+    if (!e->use_graph) {  // in order on one stream
+        for (uint32_t i = 0; i < e->n_in; ++i)
+            CUDA_TRY(cudaMemcpyAsync(e->dev_in[i], host_inputs[i], e->in_bytes[i], cudaMemcpyHostToDevice, s));
+        rc = launch_all(e, s);
+        if (rc != GFB_OK) return rc;
+        for (uint32_t j = 0; j < e->n_out; ++j)
+            CUDA_TRY(cudaMemcpyAsync(host_outputs[j], e->dev_out[j], e->out_bytes[j], cudaMemcpyDeviceToHost, s));
+        return mark_done(e, s);
+    }
+    bool same = e->hexec != nullptr;
+    for (uint32_t i = 0; same && i < e->n_in; ++i) same = e->cur_hin[i] == host_inputs[i];
+    for (uint32_t j = 0; same && j < e->n_out; ++j) same = e->cur_hout[j] == host_outputs[j];
+    if (e->hexec && !same) {
+        // retarget the copy nodes at this call's host buffers (once the
+        // previous launch of the graph has finished with the old ones)
+        CUDA_TRY(cudaEventSynchronize(e->run_done));
+        for (uint32_t i : e->in_order)
+            if (e->cur_hin[i] != host_inputs[i])
+                CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(e->hexec, e->h2d_node[i], e->dev_in[i], host_inputs[i],
+                                                            e->in_bytes[i], cudaMemcpyHostToDevice));
+        for (uint32_t j = 0; j < e->n_out; ++j)
+            if (e->cur_hout[j] != host_outputs[j])
+                CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(e->hexec, e->d2h_node[j], host_outputs[j], e->dev_out[j],
+                                                            e->out_bytes[j], cudaMemcpyDeviceToHost));
+    }
+    if (!e->hexec) {
+        CUDA_TRY(cudaStreamBeginCapture(e->capture_stream, cudaStreamCaptureModeThreadLocal));
+        rc = launch_all_io(e, e->capture_stream, host_inputs, host_outputs);
+        cudaGraph_t g = nullptr;
+        cudaError_t end = cudaStreamEndCapture(e->capture_stream, &g);
+        if (rc != GFB_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (end != cudaSuccess) return fail(GFB_ERR_CUDA, std::string("host-run graph capture: ") + cudaGetErrorString(end));
+        e->hgraph = g;
+        if (!find_copy_nodes(e)) {
+            drop_host_graph(e);
+            return fail(GFB_ERR_CUDA, "host-run graph: copy nodes not found");
+        }
+        cudaError_t inst = cudaGraphInstantiate(&e->hexec, g, 0);
+        if (inst != cudaSuccess) {
+            e->hexec = nullptr;
+            drop_host_graph(e);
+            return fail(GFB_ERR_CUDA, std::string("host-run graph instantiate: ") + cudaGetErrorString(inst));
+        }
+    }
+    e->cur_hin.assign(host_inputs, host_inputs + e->n_in);
+    e->cur_hout.assign(host_outputs, host_outputs + e->n_out);
+    CUDA_TRY(cudaGraphLaunch(e->hexec, s));
+    return mark_done(e, s);
+}
+
 int gfb_exe_num_launches(const gfb_exe* e) { return e ? (int)e->launches.size() : 0; }
 
 int gfb_kernel_load(const void* cubin, const char* name, const void** kernel) {
@@ -533,10 +790,7 @@ int gfb_exe_set_schedule(gfb_exe* e, uint32_t n_streams, const uint32_t* stream_
     std::lock_guard<std::mutex> lk(e->mu);
     const size_t n = e->launches.size();
     release_schedule(e);
-    if (e->graph) {
-        cudaGraphExecDestroy(e->graph);
-        e->graph = nullptr;
-    }
+    drop_graphs(e);
     if (n_streams == 1) return GFB_OK;
     for (size_t i = 0; i < n; ++i) {
         if (stream_of[i] >= n_streams) return fail(GFB_ERR_INVALID, "schedule: stream index out of range");
@@ -570,10 +824,7 @@ int gfb_exe_set_kernel(gfb_exe* e, uint32_t index, const void* kernel, uint32_t 
         CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     e->fns[index] = kernel;
     e->launches[index].smem = smem;
-    if (e->graph) {
-        cudaGraphExecDestroy(e->graph);
-        e->graph = nullptr;
-    }
+    drop_graphs(e);
     return GFB_OK;
 }
 

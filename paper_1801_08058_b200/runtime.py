@@ -33,7 +33,8 @@ import numpy as np
 from . import abi, jit
 from .compiler import Lowered, lower
 from .errors import BackendUnavailable, DeviceError, SignatureMismatch, ValidationFailure
-from .ir import ConstantData, Function, OpKind, TensorDescriptor, reachable_from_results, topological_order, validate_function
+from .ir import (ConstantData, Function, OpKind, TensorDescriptor, element_count, reachable_from_results, topological_order,
+                 validate_function)
 from .layout import NHWC_ORDER, Layout, assign_layouts, layout_policy, tensor_layouts
 from .memory import MemoryPlan, plan_memory
 from .rewrite import run_pipeline
@@ -80,6 +81,9 @@ def lib():
         L.gfb_kernel_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
         L.gfb_exe_set_kernel.argtypes = [vp, u32, vp, u32]
         L.gfb_exe_set_schedule.argtypes = [vp, u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]
+        u64 = C.c_uint64
+        L.gfb_exe_set_io.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]
+        L.gfb_exe_run_host.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), vp]
         _LIB = L
         return L
 
@@ -160,6 +164,7 @@ class DeviceProgram:
         ensure_device()
         check(lib().gfb_exe_create(C.byref(plan), C.byref(handle)), "gfb_exe_create")
         self.handle = handle
+        self._io = None  # host-buffer runs: None = not set up yet
         # launches running a runtime-specialised kernel (jit.py) instead of the generic VM,
         # and launches folded into a preceding merged kernel (not launched at all)
         self.jit_launches, self.skipped = (jit.specialise(lib(), handle, lowered.launches, blob, recs)
@@ -177,6 +182,29 @@ class DeviceProgram:
         ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
         outs = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
         check(lib().gfb_exe_run(self.handle, ins, outs, stream), "gfb_exe_run")
+
+    def host_io(self, in_bytes: list, out_bytes: list) -> bool:
+        """Set up host-buffer runs once (device staging buffers, copy
+        schedule); False when the plan does not support them."""
+        if self._io is None:
+            from . import schedule
+
+            acc = schedule.io_access(self.lowered, self.skipped)
+            if acc is None:
+                self._io = False
+                return False
+            off, reads, writer = acc
+            u32 = lambda v: (C.c_uint32 * max(1, len(v)))(*v)
+            u64 = lambda v: (C.c_uint64 * max(1, len(v)))(*v)
+            check(lib().gfb_exe_set_io(self.handle, u64(in_bytes), u64(out_bytes), u32(off), u32(reads), u32(writer)),
+                  "gfb_exe_set_io")
+            self._io = True
+        return self._io
+
+    def run_host(self, in_ptrs: list, out_ptrs: list, stream=None):
+        ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
+        outs = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
+        check(lib().gfb_exe_run_host(self.handle, ins, outs, stream), "gfb_exe_run_host")
 
     def run_one(self, index: int, in_ptrs: list, out_ptrs: list, stream=None):
         ins = (C.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
@@ -462,6 +490,35 @@ def pinned_tensor(et, shape) -> TensorValue:
     return TensorValue(TensorDescriptor(et, tuple(shape)), identity_layout(len(shape)), buf)
 
 
+def _pinned_host(t: TensorValue, desc) -> bool:
+    import torch
+
+    b = t.buffer
+    return (not t.is_device and isinstance(b, np.ndarray) and b.flags.c_contiguous and b.size > 0
+            and t.descriptor == desc and b.nbytes == element_count(desc.shape) * desc.element_type.byte_size
+            and torch.from_numpy(b).is_pinned())
+
+
+def _host_run(exe: Executable, inputs: list, out: list, stream) -> bool:
+    """One step on page-locked host buffers with the copies inside the
+    step's CUDA graph (gfb_exe_run_host): inputs cross PCIe in first-use
+    order under the launches that do not need them yet, and each result
+    leaves as soon as its last writer finishes.  False (nothing done) when a
+    buffer is not page-locked or the plan has no host-run schedule."""
+    if os.environ.get("GFB_HOST_GRAPH", "1") == "0" or len(out) != len(exe.result_signature):
+        return False
+    if not all(_pinned_host(t, d) for t, (d, _) in zip(inputs, exe.parameter_signature)):
+        return False
+    if not all(_pinned_host(t, d) and t.layout.order == lay.order for t, (d, lay) in zip(out, exe.result_signature)):
+        return False
+    prog = exe.program(False)
+    if not prog.host_io([t.buffer.nbytes for t in inputs], [t.buffer.nbytes for t in out]):
+        return False
+    prog.run_host([t.buffer.ctypes.data for t in inputs], [t.buffer.ctypes.data for t in out], stream.cuda_stream)
+    stream.synchronize()
+    return True
+
+
 def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device: bool = False, out=None) -> list:
     """Execute on the B200; one fresh result tensor per result.
 
@@ -476,9 +533,11 @@ def call(exe: Executable, inputs: list, *, private_buffers: bool = False, device
         inputs = [as_tensor(t) for t in inputs]  # reference-built TensorValues are accepted as they are
         _check_signature(exe, inputs)
     ensure_device()
+    cur = torch.cuda.current_stream()
+    if out is not None and not private_buffers and not device and _host_run(exe, inputs, out, cur):
+        return list(out)
     dev_in = [to_device(t) for t in inputs]
     outs = exe.allocate_outputs()
-    cur = torch.cuda.current_stream()
     exe.run_device(dev_in, outs, stream=cur.cuda_stream, private=private_buffers)
     if device:
         return [TensorValue(desc, layout, buf) for (desc, layout), buf in zip(exe.result_signature, outs)]

@@ -102,3 +102,47 @@ def build(lowered, skipped=(), n_streams: int = 4):
         flat += d
         offsets.append(len(flat))
     return stream_of, offsets, flat
+
+
+def io_access(lowered, skipped=()):
+    """(read_offsets, reads, out_writer) for gfb_exe_set_io: the caller inputs
+    each launch reads and the last launch writing each result (None if some
+    result is written by no launch).  A launch
+    folded into a preceding merged kernel counts as that kernel's access."""
+    n = len(lowered.launches)
+    skipped = set(skipped)
+    head = list(range(n))
+    for i in range(1, n):
+        if i in skipped:
+            head[i] = head[i - 1]
+    n_in = lowered.n_inputs
+    reads = [set() for _ in range(n)]
+    writer = [None] * lowered.n_outputs
+
+    def slots(keys):
+        for k in keys:
+            b = lowered.buffers.get(k)
+            if b is None:
+                yield None
+                continue
+            root = b.base if b.base is not None else b
+            if root.splat is None:
+                yield root.slot
+
+    for i, L in enumerate(lowered.launches):
+        h = head[i]
+        for s in slots(L.reads):
+            if s is None:  # unknown access: wait for every input
+                reads[h].update(range(n_in))
+            elif abi.SLOT_IO <= s < abi.SLOT_IO + n_in:
+                reads[h].add(s - abi.SLOT_IO)
+        for s in slots(L.writes):
+            if s is not None and s >= abi.SLOT_IO + n_in:
+                writer[s - abi.SLOT_IO - n_in] = h
+    if any(w is None for w in writer):
+        return None  # a result no launch writes: host-buffer runs are not offered
+    offsets, flat = [0], []
+    for r in reads:
+        flat += sorted(r)
+        offsets.append(len(flat))
+    return offsets, flat, writer

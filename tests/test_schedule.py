@@ -75,3 +75,30 @@ def test_schedule_keeps_collectives_in_order():
     assert all(st[i] == 0 for i in coll)
     for a, b in zip(coll, coll[1:]):
         assert a in deps_of[b]
+
+
+@pytest.mark.parametrize("name", ["mlp_A_small", "cnn_C_small", "resnet_D_small", "mlp_E_small"])
+def test_io_access_covers_every_input_and_result(name):
+    """Host-buffer runs wait for an input's copy only at the launches that
+    read it: every launch touching an input slot must be listed, and every
+    result's D2H follows its last writer."""
+    case = next(c for c in G.load("workloads.json.gz") if c["name"] == name)
+    h = host_compile(G.fn_of(case["fn"]), conv_layout="nhwc" if name.startswith("resnet") else "identity")
+    low = h.lowered
+    off, reads, writer = schedule.io_access(low)
+    n, n_in = len(low.launches), low.n_inputs
+    assert len(off) == n + 1 and off[-1] == len(reads) and len(writer) == low.n_outputs
+    for i, L in enumerate(low.launches):
+        mine = set(reads[off[i]:off[i + 1]])
+        for k in L.reads:
+            b = low.buffers[k]
+            root = b.base if b.base is not None else b
+            if root.splat is None and abi.SLOT_IO <= root.slot < abi.SLOT_IO + n_in:
+                assert root.slot - abi.SLOT_IO in mine
+        for k in L.writes:
+            b = low.buffers[k]
+            root = b.base if b.base is not None else b
+            if root.slot >= abi.SLOT_IO + n_in:
+                assert writer[root.slot - abi.SLOT_IO - n_in] >= i
+    assert set(reads) == set(range(n_in)) - {i for i in range(n_in) if not any(
+        (low.buffers[k].base or low.buffers[k]).slot == abi.SLOT_IO + i for L in low.launches for k in L.reads)}
