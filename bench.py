@@ -174,6 +174,15 @@ def tf32_peak():
         return 1100.0, 1100.0, "nominal (no profiles/tf32_peak.json)"
 
 
+def f16_peak():
+    """Measured tcgen05 kind::f16 dense TFLOP/s, sustained (same probe)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "tf32_peak.json")) as fh:
+            return float(json.load(fh)["f16_dense_tflops_sustained"])
+    except Exception:
+        return 2 * tf32_peak()[1]
+
+
 def _traffic(workload):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -378,7 +387,7 @@ def _time_launch(exe, idx, dev_in, outs, stream, reps):
     return e0.elapsed_time(e1) / reps
 
 
-_KIND_NAMES = {19: "gfb_gemm_tc2_kernel", 12: "gfb_gemm_tc_kernel<128>", 14: "gfb_gemm_tc_kernel<256>",
+_KIND_NAMES = {34: "gfb_gemm_f16p_kernel", 19: "gfb_gemm_tc2_kernel", 12: "gfb_gemm_tc_kernel<128>", 14: "gfb_gemm_tc_kernel<256>",
                22: "gfb_conv_tcx_kernel<64>", 23: "gfb_conv_tcx_kernel<128>", 17: "gfb_conv_tcg_kernel<64>",
                18: "gfb_conv_tcg_kernel<128>", 24: "gfb_conv_tcgg_kernel<64>", 25: "gfb_conv_tcgg_kernel<128>",
                28: "gfb_conv_tcgw_kernel<64>", 29: "gfb_conv_tcgw_kernel<128>", 32: "gfb_conv_stem_kernel",
@@ -538,7 +547,11 @@ def bench_step(args, ws, rank, local):
     dom_flops = sum(L.flops for _, _, L in dom_rows)
     kernel_ms = dom_ms / len(dom_rows)
     tf32, tf32_sus, tf_src = tf32_peak()
-    useful_peak = tf32_sus / 3.0  # 3xTF32: three kind::tf32 MMAs per useful product
+    if dom_kind == 34:  # 2xFP16: three kind::f16 MMAs per useful product
+        mma_sus, mma_name = f16_peak(), "2xFP16 useful ceiling = kind::f16"
+    else:  # 3xTF32: three kind::tf32 MMAs per useful product
+        mma_sus, mma_name = tf32_sus, "3xTF32 useful ceiling = kind::tf32"
+    useful_peak = mma_sus / 3.0
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12
     gemm_ms = sum(t for t, i, L in rows if L.flops)
     best = max(dom_rows, key=lambda r: r[2].flops / r[0])
@@ -555,8 +568,8 @@ def bench_step(args, ws, rank, local):
                      "kernel_ms": kernel_ms, "algorithmic_flops": dom_flops // len(dom_rows),
                      "step_share": dom_ms / total if total else None,
                      "best_launch": {"label": best[2].label, "ms": best[0], "tflops": best[2].flops / (best[0] * 1e-3) / 1e12},
-                     "peak_source": f"3xTF32 useful ceiling = kind::tf32 dense {tf32_sus:.0f} TFLOP/s / 3, {tf_src}",
-                     "tensor_pipe_frac": 3 * achieved / tf32_sus,
+                     "peak_source": f"{mma_name} dense {mma_sus:.0f} TFLOP/s / 3, {tf_src}",
+                     "tensor_pipe_frac": 3 * achieved / mma_sus,
                      "frac_of_measured_bf16": achieved / peaks()[1]},
         "step_detail": {"launches": exe.num_launches, "allreduces": sum(1 for L in exe.lowered.launches if L.label.startswith("allreduce")),
                         "flops_per_step_per_gpu": flops, "achieved_tflops_step": ws * flops / (ms * 1e-3) / 1e12,

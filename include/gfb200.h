@@ -87,6 +87,9 @@ enum {
     GFB_K_CONV_F32 = 20, /* direct Conv2D / ConvBackpropData / ConvBackpropFilter (gfb_conv_args) */
     GFB_K_CONV_F64 = 21,
     GFB_K_ALLREDUCE = 30, /* NCCL sum all-reduce over a byte range (gfb_allreduce_args) */
+    GFB_K_DOT_F16P = 34,  /* 2xFP16 block-scaled Dot on a 2-SM CTA pair (kind::f16, 256x256 tiles; gfb_tc_args
+                             with the fp16 plane fields): the fp32 accuracy of the 3xTF32 kernel at the f16 rate */
+    GFB_K_SPLIT_F16 = 35, /* F32 -> fp16 hi / lo planes + per-128x128-tile power-of-two scales (gfb_split16_args) */
     GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
                              always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
                              entry only traps */
@@ -259,10 +262,31 @@ typedef struct GFB_ALIGN64 {
      * kind 2).  Each op is the unfused plan's IEEE op: bit-identical. */
     int64_t epi_kind;
     uint64_t e_bias, e_aux1, e_aux2, e_out2, e_lo; /* GFB_REF (an arena ref may be 0: presence is in epi_flags) */
-    int64_t epi_flags; /* bit 0: e_out2 is written, bit 1: e_lo is written */
+    int64_t epi_flags; /* bit 0: e_out2 is written, bit 1: e_lo is written, bit 2: the fp16 planes
+                          e_hi / e_lo / e_sc of y are written (GFB_K_DOT_F16P) */
+    /* GFB_K_DOT_F16P: a_hi / a_lo / b_hi / b_lo are fp16 planes (K-major: element (r, k)
+     * at r * kp + k; MN-major: at k * ld_mn + r) holding x * s rounded to fp16 (hi) and
+     * the rounded remainder (lo), s a power of two per 128 x 128 tile of the plane's
+     * storage: s(r, k) = sc[(r / 128) * sc_r + (k / 128) * sc_k].  Every 128-K chunk of
+     * the three products is promoted into fp32 registers times 1 / (s_a s_b). */
+    uint64_t a_sc, b_sc;
+    int64_t a_sc_r, a_sc_k, b_sc_r, b_sc_k;
+    /* epi_flags bit 2: fp16 planes of y (e_hi, e_lo: [M, N], pitch N) and their scale
+     * grid e_sc ([ceil(M / 128), ceil(N / 128)], row-major) */
+    uint64_t e_hi, e_sc;
     int64_t pad[3];
     uint64_t tmap[4][16];
 } gfb_tc_args;
+
+/* fp16 split of a dense F32 matrix [rows, cols] (row pitch ld elements, cols % 8 == 0):
+ * per 128 x 128 tile, s = 2^(14 - floor(log2(max |x|))) (1 for an all-zero tile),
+ * hi = fp16_rn(x s), lo = fp16_rn(x s - hi); sc[tile] = s over the row-major tile grid
+ * [ceil(rows / 128), ceil(cols / 128)].  The planes are [rows, cols] dense. */
+typedef struct {
+    const void* const* tab;
+    uint64_t src, hi, lo, sc; /* GFB_REF */
+    int64_t rows, cols, ld;
+} gfb_split16_args;
 
 /* Implicit-GEMM convolution with the A gather fused into the tensor-core
  * kernel.  A is a 4-D activation with unit channel stride (NHWC storage):

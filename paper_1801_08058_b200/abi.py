@@ -16,6 +16,7 @@ K_EW1_F32, K_EW1_F64 = 7, 8
 K_DOT_F32, K_DOT_F64, K_DOT_TC32, K_SPLIT_TF32, K_DOT_TC32W = 10, 11, 12, 13, 14
 K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
 K_DOT_TC32P = 19
+K_DOT_F16P, K_SPLIT_F16 = 34, 35
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
@@ -87,8 +88,15 @@ class SplitArgs(C.Structure):
     ]
 
 
+class Split16Args(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("src", C.c_uint64), ("hi", C.c_uint64), ("lo", C.c_uint64), ("sc", C.c_uint64),
+        ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64),
+    ]
+
+
 class TcArgs(C.Structure):
-    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 256, size 768.
+    # 64-byte aligned in C (GFB_ALIGN64): tmap sits at offset 320, size 832.
     _fields_ = [
         ("tab", C.c_void_p), ("c", C.c_uint64),
         ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("c_sm", C.c_int64), ("c_sn", C.c_int64),
@@ -99,6 +107,9 @@ class TcArgs(C.Structure):
         ("a_ld_mn", C.c_int64), ("b_ld_mn", C.c_int64), ("group_m", C.c_int64),
         ("epi_kind", C.c_int64), ("e_bias", C.c_uint64), ("e_aux1", C.c_uint64), ("e_aux2", C.c_uint64),
         ("e_out2", C.c_uint64), ("e_lo", C.c_uint64), ("epi_flags", C.c_int64),
+        ("a_sc", C.c_uint64), ("b_sc", C.c_uint64),
+        ("a_sc_r", C.c_int64), ("a_sc_k", C.c_int64), ("b_sc_r", C.c_int64), ("b_sc_k", C.c_int64),
+        ("e_hi", C.c_uint64), ("e_sc", C.c_uint64),
         ("pad", C.c_int64 * 3),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
@@ -211,5 +222,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

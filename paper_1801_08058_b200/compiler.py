@@ -150,6 +150,7 @@ TC_TILE = 128
 TC_SMEM = 3 * 4 * 128 * 32 * 4 + 1024 + 256
 TC_SMEM_W = 2 * (2 * 128 + 2 * 256) * 32 * 4 + 1024 + 256
 TC_SMEM_PAIR = TC_SMEM + 8 * 32 * 32 * 4  # + the epilogue warps' transpose tiles (gemm_tc.cu PCfg::SMEM_BYTES_PAIR)
+F16_SMEM_PAIR = TC_SMEM_PAIR  # gemm_f16.cu HCfg::SMEM_BYTES: same 64 KB stages (64 fp16 K instead of 32 fp32 K)
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
@@ -177,6 +178,14 @@ def _conv_out_digits(addr: dict, m: int, ncols: int) -> list:
     else:
         digs = [(0, ncols, None, addr["c_sm"]), (0, 1, ncols, addr["c_sn"])]
     return [d for d in digs if d[3] != 0]
+
+
+def use_f16() -> bool:
+    """Large dense F32 Dots on the 2xFP16 block-scaled pair GEMM (kind::f16,
+    csrc/gemm_f16.cu) instead of 3xTF32; GFB_F16=0 selects 3xTF32."""
+    import os
+
+    return os.environ.get("GFB_F16", "1") == "1"
 
 
 def use_tensor_cores(m: int, n: int, k: int) -> bool:
@@ -1667,6 +1676,13 @@ class Lowering:
         too small to fill the GPU."""
         (ab, ast), (bb, bst) = a_op, b_op
         pair = m >= 256 and nn >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1" and os.environ.get("GFB_TC_WIDE", "1") == "1"
+        if pair and use_f16():
+            a16 = self._f16_operand(ab, ast[0], ast[1], m, k)
+            b16 = self._f16_operand(bb, bst[1], bst[0], nn, k) if a16 is not None else None
+            if b16 is not None:
+                rec = self._f16_gemm(n, a16, b16, out, m, nn, k, {"c_sm": out.strides[0], "c_sn": out.strides[1]}, f"dot_f16#{n}")
+                rec.algo_bytes = (m * k + k * nn + m * nn) * 4
+                return
         a = self._raw_mn(ab, ast[0], ast[1], m, k) if pair else None
         b = self._raw_mn(bb, bst[1], bst[0], nn, k) if pair else None
         if a is None:
@@ -1793,6 +1809,118 @@ class Lowering:
             rec.finalize = _finalize_refs(sa, {"src": root, "hi": root, "lo": lo})
             self.launches.append(rec)
         return lo
+
+    # -- 2xFP16 block-scaled GEMM (csrc/gemm_f16.cu)
+    def _f16_operand(self, src, s_r, s_k, rows, kdim):
+        """Operand [rows, k] of the fp16 pair GEMM: a dense row-major F32
+        tensor read K-major (s_k == 1) or MN-major (s_r == 1), with its fp16
+        planes and tile scales (shared by every GEMM that reads the tensor,
+        either way).  Returns (hi, lo, sc, kp, ld_mn, sc_r, sc_k) or None."""
+        root = src.base if src.base is not None else src
+        if (src.splat is not None or src.elem_off or root.subaxes or root.et is not ElementType.F32
+                or not _dense_rowmajor(root.shape, root.strides) or element_count(root.shape) != rows * kdim):
+            return None
+        if s_k == 1 and s_r == kdim and kdim % 8 == 0:
+            hi, lo, sc = self._f16_planes(root, rows, kdim)
+            return hi, lo, sc, kdim, 0, (kdim + 127) // 128, 1
+        if s_r == 1 and s_k == rows and rows % 64 == 0:
+            hi, lo, sc = self._f16_planes(root, kdim, rows)
+            return hi, lo, sc, align_up(kdim, 8), rows, 1, (rows + 127) // 128
+        return None
+
+    def _f16_planes(self, root, R, Cc):
+        """fp16 hi / lo planes of the dense tensor `root` viewed as [R, Cc]
+        and its 128 x 128 tile scales: written by the epilogue of the GEMM
+        producing `root` when there is one (epi_flags bit 2), else by one
+        split pass (gfb_split16_kernel, 8 B of traffic per element)."""
+        got = self._f16_get(root)
+        if got is not None:
+            return got
+        planes = self._f16_buffers(root, R, Cc)
+        hi, lo, sc = planes
+        sa = abi.Split16Args(rows=R, cols=Cc, ld=Cc)
+        tiles = ((R + 127) // 128) * ((Cc + 127) // 128)
+        rec = LaunchRec(abi.K_SPLIT_F16, (max(1, min(tiles, NUM_SMS * 4)), 1, 1), (256, 1, 1), 0, sa, [root.key],
+                        [hi.key, lo.key, sc.key], f"split16#{root.key}")
+        rec.algo_bytes = R * Cc * 8
+        rec.finalize = _finalize_refs(sa, {"src": root, "hi": hi, "lo": lo, "sc": sc})
+        self.launches.append(rec)
+        return planes
+
+    def _f16_get(self, root):
+        parts = [self.buf.get(("f16", root.key, p)) for p in ("hi", "lo", "sc")]
+        return None if parts[0] is None else tuple(parts)
+
+    def _f16_buffers(self, root, R, Cc):
+        """Register the planes of `root` (fp16 planes are sized as F32
+        buffers of half the element count)."""
+        hi = Buffer(self.new_key(), ElementType.F32, ((R * Cc + 1) // 2,), (1,))
+        lo = Buffer(self.new_key(), ElementType.F32, ((R * Cc + 1) // 2,), (1,))
+        sc = Buffer(self.new_key(), ElementType.F32, (((R + 127) // 128) * ((Cc + 127) // 128),), (1,))
+        for p, b in (("hi", hi), ("lo", lo), ("sc", sc)):
+            self.buf[("f16", root.key, p)] = b
+        return hi, lo, sc
+
+    def _f16_gemm(self, n, a, b, out, m, ncols, kdim, addr, label):
+        """The fp16 pair GEMM over planes (split-K on 128-K boundaries, the
+        scale blocks, + the deterministic reduce pass)."""
+        (ahi, alo, asc, kpa, a_mn, a_r, a_k), (bhi, blo, bsc, kpb, b_mn, b_r, b_k) = a, b
+        splits = self._tc_splits(m, ncols, kdim)
+        ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn,
+                        a_sc_r=a_r, a_sc_k=a_k, b_sc_r=b_r, b_sc_k=b_k,
+                        group_m=int(os.environ.get("GFB_TC_GROUP_M", "1")))
+        target = out
+        if splits > 1:
+            kchunks = (kdim + 127) // 128
+            per = ((kchunks + splits - 1) // splits) * 128
+            splits = (kdim + per - 1) // per
+        if splits > 1:
+            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
+            self.buf[("splitk", n)] = scratch
+            ta.k_splits, ta.k_per_split, ta.split_stride = splits, per, m * ncols
+            ta.c_sm, ta.c_sn = ncols, 1
+            target = scratch
+        else:
+            for k_, v_ in addr.items():
+                setattr(ta, k_, v_)
+        ntiles = ((ncols + 255) // 256) * ((m + 255) // 256) * max(1, splits)
+        pairs = NUM_SMS // 2 if os.environ.get("GFB_TC_PERSIST", "1") == "1" else ntiles
+        grid = (2 * min(ntiles, pairs), 1, 1)
+        reads, writes = [ahi.key, alo.key, asc.key, bhi.key, blo.key, bsc.key], [target.key]
+        refs = {"c": target, "a_hi": ahi, "a_lo": alo, "a_sc": asc, "b_hi": bhi, "b_lo": blo, "b_sc": bsc}
+        epi = self._epi.get(n) if hasattr(self, "_epi") else None
+        if epi is not None:
+            if splits > 1 or target.strides != (ncols, 1) or target.elem_off or ncols % 4:
+                raise UnsupportedOp(f"fused epilogue of Dot {n} needs an unsplit GEMM and a dense output")
+            ta.epi_kind = epi["kind"]
+            for field, key in (("e_bias", "bias"), ("e_aux1", "aux1"), ("e_aux2", "aux2"), ("e_out2", "out2")):
+                if key in epi:
+                    bb = self.buf[epi[key]]
+                    refs[field] = bb
+                    (writes if field == "e_out2" else reads).append(bb.key)
+            ta.epi_flags = 1 if "out2" in epi else 0
+            y = self.buf[epi["lo_of"]]
+            root = y.base if y.base is not None else y
+            if (y.splat is None and not y.elem_off and not root.subaxes and _dense_rowmajor(root.shape, root.strides)
+                    and element_count(root.shape) == m * ncols and ncols % 8 == 0 and self._feeds_tc(epi["lo_of"])
+                    and self._f16_get(root) is None):
+                planes = self._f16_buffers(root, m, ncols)  # _f16_planes finds them: no split pass
+                refs["e_hi"], refs["e_lo"], refs["e_sc"] = planes
+                writes.extend(pl.key for pl in planes)
+                ta.epi_flags |= 4
+            label += ":epi" + ("bias_relu" if epi["kind"] == 1 else "relu_grad")
+        rec = LaunchRec(abi.K_DOT_F16P, grid, (320, 1, 1), F16_SMEM_PAIR, ta, reads, writes, label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.finalize = _finalize_refs(ta, refs)
+        self.launches.append(rec)
+        if splits > 1:
+            p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(target, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
+            p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+            self._col_launch(p2, m * ncols, splits, 1, label + ":splitk", ElementType.F32)
+        return rec
 
     def _raw_mn(self, src, s_r, s_k, rows, kdim):
         """Operand [rows, k] read in place from its arena tensor: as an

@@ -24,6 +24,7 @@
 extern "C" const void* gfb_ew_kernel_ptr(int kind);
 extern "C" const void* gfb_simt_kernel_ptr(int kind);
 extern "C" const void* gfb_tc_kernel_ptr(int kind);
+extern "C" const void* gfb_f16_kernel_ptr(int kind);
 
 namespace {
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -74,6 +75,39 @@ bool encode_mn_map(void* gaddr, int64_t mn, int64_t k, int64_t ld, void* out) {
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, gaddr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out, &map, sizeof(map));
+    return true;
+}
+// fp16 planes of the 2xFP16 GEMM (gemm_f16.cu).  K-major [rows, kp]:
+// 128B-swizzled boxes of 64 (K) x 128 rows.  MN-major (element (mn, k) at
+// k * ld + mn, mn % 64 == 0): 3-D view (64 MN, K, MN / 64) with (64, 64, 2)
+// boxes, i.e. two 8 KB chunks of 64 K rows x 128 B in the canonical
+// SWIZZLE_128B MN-major layout.
+bool encode_plane16_map(void* gaddr, int64_t rows, int64_t kp, void* out) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || kp % 8) return false;
+    alignas(64) CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, gaddr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out, &map, sizeof(map));
+    return true;
+}
+bool encode_mn16_map(void* gaddr, int64_t mn, int64_t k, int64_t ld, void* out) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || mn % 64 || ld % 8) return false;
+    alignas(64) CUtensorMap map;
+    cuuint64_t dims[3] = {64, (cuuint64_t)k, (cuuint64_t)(mn / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, 128};
+    cuuint32_t box[3] = {64, 64, 2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, gaddr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     std::memcpy(out, &map, sizeof(map));
     return true;
@@ -228,6 +262,7 @@ const void* kernel_for(uint32_t kind) {
         kind == GFB_K_CONV_TCG128 || kind == GFB_K_CONV_TCX64 || kind == GFB_K_CONV_TCX128 || kind == GFB_K_CONV_TCGG64 ||
         kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128 || kind == GFB_K_CONV_STEM64)
         return gfb_tc_kernel_ptr((int)kind);
+    if (kind == GFB_K_DOT_F16P || kind == GFB_K_SPLIT_F16) return gfb_f16_kernel_ptr((int)kind);
     return nullptr;
 }
 
@@ -537,6 +572,19 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                         return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (MN-major operand) failed"));
                 } else if (!encode_plane_map(addr, rows, kp, box_rows, a->tmap[t]))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
+            }
+        }
+        if (L.kind == GFB_K_DOT_F16P) {
+            gfb_tc_args* a = (gfb_tc_args*)(e->args.data() + L.arg_offset);
+            const uint64_t refs[4] = {a->a_hi, a->a_lo, a->b_hi, a->b_lo};
+            for (int t = 0; t < 4; ++t) {
+                if ((refs[t] >> 56) != GFB_SLOT_ARENA)
+                    return bail(fail(GFB_ERR_INVALID, "tensor-core operand planes must live in the arena"));
+                void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
+                const int64_t rows = t < 2 ? a->M : a->N, kp = t < 2 ? a->kp_a : a->kp_b;
+                const int64_t ld_mn = t < 2 ? a->a_ld_mn : a->b_ld_mn;
+                const bool ok = ld_mn > 0 ? encode_mn16_map(addr, rows, a->K, ld_mn, a->tmap[t]) : encode_plane16_map(addr, rows, kp, a->tmap[t]);
+                if (!ok) return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 plane) failed"));
             }
         }
         if (L.kind == GFB_K_CONV_TCX64 || L.kind == GFB_K_CONV_TCX128) {

@@ -52,7 +52,7 @@ def main():
         for name, fn in graphs().items():
             exe = gf.compile_function(fn)
             ins = [data[0], wt] if name == "fwd" else [data[0], data[1]]
-            gi = [i for i, L in enumerate(exe.lowered.launches) if L.label.startswith("dot_tc")]  # GEMM (+ split-K pass)
+            gi = [i for i, L in enumerate(exe.lowered.launches) if L.label.startswith(("dot_tc", "dot_f16"))]  # GEMM (+ split-K pass)
             per[name] = (exe, ins, exe.allocate_outputs(), gi)
         exes.append(per)
         for k, x in old.items():

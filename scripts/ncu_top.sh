@@ -8,7 +8,7 @@ NTH=${3:-0}
 OUT=gpurun_out/ncu_${W}_${RE}_${NTH}
 mkdir -p $OUT
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:$RE --csv \
-  --log-file $OUT/list.csv python bench.py --workload $W --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+  --log-file $OUT/list.csv python bench.py --workload $W --steps 1 --warmup 3 --no-cpu-baseline --no-secondary > /dev/null 2>&1
 IDX=$(python - <<PY
 import csv
 rows=[r for r in csv.reader(open("$OUT/list.csv")) if len(r)==15 and r[0]!="ID"]
@@ -18,5 +18,5 @@ PY
 )
 echo "launch index $IDX of regex $RE"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:$RE -s $IDX -c 1 -o $OUT/prof \
-  python bench.py --workload $W --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu.log 2>&1
+  python bench.py --workload $W --steps 1 --warmup 3 --no-cpu-baseline --no-secondary > $OUT/ncu.log 2>&1
 echo done

@@ -360,6 +360,89 @@ def run_tc(mem, a):
         C[base + off] = c
 
 
+def _f16_scale(mx):
+    """gemm_f16.cu / tc_prims.cuh f16_tile_scale: 2^(14 - floor(log2 mx))."""
+    if not (mx > 0) or not np.isfinite(mx):
+        return np.float32(1.0)
+    e = int(np.frexp(np.float32(mx))[1])
+    return np.float32(2.0 ** min(15 - e, 126))
+
+
+def _f16_split(y, R, Cc):
+    """fp16 hi / lo planes and the 128 x 128 tile scale grid of y [R, Cc]."""
+    tr, tc = (R + 127) // 128, (Cc + 127) // 128
+    sc = np.ones((tr, tc), dtype=np.float32)
+    full = np.empty((R, Cc), dtype=np.float32)
+    with np.errstate(all="ignore"):
+        for i in range(tr):
+            for j in range(tc):
+                blk = y[128 * i:128 * (i + 1), 128 * j:128 * (j + 1)]
+                sc[i, j] = _f16_scale(np.abs(blk).max() if blk.size else 0.0)
+                full[128 * i:128 * (i + 1), 128 * j:128 * (j + 1)] = sc[i, j]
+        v = (y * full).astype(np.float32)
+        hi = v.astype(np.float16)
+        lo = (v - hi.astype(np.float32)).astype(np.float16)
+    return hi, lo, sc
+
+
+def run_split16(mem, a):
+    src = mem.view(a.src, np.float32)
+    y = src[np.arange(a.rows)[:, None] * a.ld + np.arange(a.cols)[None, :]]
+    hi, lo, sc = _f16_split(y, a.rows, a.cols)
+    mem.view(a.hi, np.float16)[: a.rows * a.cols] = hi.reshape(-1)
+    mem.view(a.lo, np.float16)[: a.rows * a.cols] = lo.reshape(-1)
+    mem.view(a.sc, np.float32)[: sc.size] = sc.reshape(-1)
+
+
+def _plane16(mem, ref, scref, rows, kp, k, ld_mn, sc_r, sc_k):
+    """[rows, k] operand of the fp16 GEMM, unscaled (exact in float64)."""
+    v = mem.view(ref, np.float16)
+    r = np.arange(rows)[:, None]
+    kk = np.arange(k)[None, :]
+    x = v[kk * ld_mn + r] if ld_mn > 0 else v[r * kp + kk]
+    s = mem.view(scref, np.float32)[(r // 128) * sc_r + (kk // 128) * sc_k]
+    return x.astype(np.float64) / s.astype(np.float64)
+
+
+def run_f16p(mem, a):
+    """gfb_gemm_f16p_kernel: sum over 128-K chunks of (Ahi Bhi + Ahi Blo +
+    Alo Bhi) / (s_a s_b), then the fused epilogue (fp32 elementwise ops as
+    in run_tc, fp16 planes of y when epi_flags bit 2 is set)."""
+    Ah = _plane16(mem, a.a_hi, a.a_sc, a.M, a.kp_a, a.K, a.a_ld_mn, a.a_sc_r, a.a_sc_k)
+    Al = _plane16(mem, a.a_lo, a.a_sc, a.M, a.kp_a, a.K, a.a_ld_mn, a.a_sc_r, a.a_sc_k)
+    Bh = _plane16(mem, a.b_hi, a.b_sc, a.N, a.kp_b, a.K, a.b_ld_mn, a.b_sc_r, a.b_sc_k)
+    Bl = _plane16(mem, a.b_lo, a.b_sc, a.N, a.kp_b, a.K, a.b_ld_mn, a.b_sc_r, a.b_sc_k)
+    splits = max(1, a.k_splits)
+    i = np.arange(a.M, dtype=np.int64)[:, None]
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    C = mem.view(a.c, np.float32)
+    for z in range(splits):
+        k0 = z * a.k_per_split if splits > 1 else 0
+        k1 = min(a.K, k0 + a.k_per_split) if splits > 1 else a.K
+        sl = slice(k0, k1)
+        c = (Ah[:, sl] @ Bh[:, sl].T + Ah[:, sl] @ Bl[:, sl].T + Al[:, sl] @ Bh[:, sl].T).astype(np.float32)
+        base = z * a.split_stride if splits > 1 else 0
+        if a.epi_kind or a.epi_flags & 4:
+            y = c
+            with np.errstate(all="ignore"):
+                if a.epi_kind == 1:
+                    c = (c + mem.view(a.e_bias, np.float32)[: a.N][None, :]).astype(np.float32)
+                    y = np.where(c > 0, c, np.float32(0)).astype(np.float32)
+                    if a.epi_flags & 1:
+                        mem.view(a.e_out2, np.float32)[: a.M * a.N] = y.reshape(-1)
+                elif a.epi_kind == 2:
+                    x = mem.view(a.e_aux2, np.float32)[: a.M * a.N].reshape(a.M, a.N)
+                    r = (np.where(x > 0, x, np.float32(0)) / x).astype(np.float32)
+                    c = (c * np.where(r >= 0, r, np.float32(0))).astype(np.float32)
+                    y = c
+            if a.epi_flags & 4:
+                hi, lo, sc = _f16_split(y, a.M, a.N)
+                mem.view(a.e_hi, np.float16)[: a.M * a.N] = hi.reshape(-1)
+                mem.view(a.e_lo, np.float16)[: a.M * a.N] = lo.reshape(-1)
+                mem.view(a.e_sc, np.float32)[: sc.size] = sc.reshape(-1)
+        C[base + i * a.c_sm + j * a.c_sn] = c
+
+
 def _trunc_split(x):
     """The converter warps' split (gemm_tc.cu split_rows): hi = x with the 13
     low mantissa bits cleared, lo = x - hi rounded to the TF32 the MMA reads."""
@@ -549,6 +632,10 @@ def _run_launch(mem, L):
         run_split(mem, L.args)
     elif L.kind in (abi.K_DOT_TC32, abi.K_DOT_TC32W, abi.K_DOT_TC32P):
         run_tc(mem, L.args)
+    elif L.kind == abi.K_SPLIT_F16:
+        run_split16(mem, L.args)
+    elif L.kind == abi.K_DOT_F16P:
+        run_f16p(mem, L.args)
     elif L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128):
         run_tcg(mem, L.args)
     elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):

@@ -36,6 +36,7 @@ def _dot_graph(m, k, n, ta=False, tb=False):
 ])
 def test_tc_dot_matches_oracle(monkeypatch, m, k, n, ta, tb):
     monkeypatch.setenv("GFB_DOT", "tc")
+    monkeypatch.setenv("GFB_F16", "0")
     fn = _dot_graph(m, k, n, ta, tb)
     rng = np.random.default_rng(m * 7 + k + n)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
@@ -77,7 +78,8 @@ def test_small_m_dot_bit_exact(m, k, n, ta, tb, et):
     assert G.same_bits(out, interp.run_function(fn, ins)[0])
 
 
-def test_tc_dot_large_config_E_layer():
+def test_tc_dot_large_config_E_layer(monkeypatch):
+    monkeypatch.setenv("GFB_F16", "0")
     fn = _dot_graph(2048, 4096, 4096)
     rng = np.random.default_rng(0)
     a = rng.uniform(-1, 1, size=(2048, 4096)).astype(np.float32)
@@ -267,6 +269,7 @@ def test_raw_hi_operands(monkeypatch, m, k, n, raw):
     truncates), with one shared lo plane: K-major (Dot(h, W)) and MN-major
     via TMA SWIZZLE_128B_ATOM_32B (the weight gradient Dot(h^T, dz)),
     against the plane-split form and the oracle."""
+    monkeypatch.setenv("GFB_F16", "0")
     if raw == "split":
         monkeypatch.setenv("GFB_RAW_HI", "0")
         monkeypatch.setenv("GFB_MN_MAJOR", "0")
@@ -308,6 +311,7 @@ def test_fused_epilogues_bit_identical(monkeypatch, width, batch):
     that runs them as separate maps."""
     from paper_1801_08058_b200 import workloads as W
 
+    monkeypatch.setenv("GFB_F16", "0")
     step = W.wide_mlp_step(gf, batch=batch, width=width, layers=3, loss_batch=65536)
     arrays = W.step_inputs(step, W.parameter_shapes(step), seed=6, x_range=(-1, 1))
     tens = [gf.tensor_from_flat(F32, a.shape, a) for a in arrays]
@@ -322,3 +326,62 @@ def test_fused_epilogues_bit_identical(monkeypatch, width, batch):
     plain = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
     for a, b in zip(fused, plain):
         assert G.same_bits(a, b)
+
+
+# ---- 2xFP16 block-scaled pair GEMM (csrc/gemm_f16.cu) ----
+
+@pytest.mark.parametrize("m,k,n,ta,tb", [
+    (512, 1024, 512, False, False),   # A K-major, B MN-major (Dot(h, W))
+    (512, 1024, 512, True, False),    # both MN-major (the weight gradient Dot(h^T, dz))
+    (512, 1024, 512, False, True),    # both K-major (the data gradient Dot(dz, W^T))
+    (512, 1024, 512, True, True),
+    (320, 200, 256, False, False),    # ragged K (zero-filled TMA tail), ragged M tile
+    (300, 600, 520, False, True),     # ragged tiles (K-major operands only: MN-major needs rows % 64)
+    (256, 20000, 256, True, False),   # split-K on 128-K scale blocks
+    (2048, 4096, 4096, False, False), # a config-E layer
+])
+def test_f16_dot_matches_exact(m, k, n, ta, tb):
+    """fp16 hi / lo planes with 128 x 128 tile scales and three kind::f16
+    MMAs per K-step: normwise within 1e-6 of the exact product (the Dot
+    contract is 1e-5), including tiles whose magnitudes differ by 1e40."""
+    fn = _dot_graph(m, k, n, ta, tb)
+    rng = np.random.default_rng(m + 3 * k + n)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0].reshape(-1)[: 128 * 128] *= np.float32(1e-20)
+    ins[1].reshape(-1)[-1000:] *= np.float32(1e20)
+    exe = gf.compile_function(fn)
+    from paper_1801_08058_b200 import abi
+
+    assert [L.kind for L in exe.lowered.launches if L.flops] == [abi.K_DOT_F16P]
+    out = gf.call(exe, [gf.tensor_from_flat(F32, a.shape, a) for a in ins])[0].to_numpy()
+    A = ins[0].astype(np.float64).T if ta else ins[0].astype(np.float64)
+    B = ins[1].astype(np.float64).T if tb else ins[1].astype(np.float64)
+    ref = A @ B
+    assert G.normwise(out, ref) <= 1e-6, G.normwise(out, ref)
+    rows = 128 if not ta else m  # the scaled-down block's rows stand on their own
+    assert G.normwise(out[:rows], ref[:rows]) <= 1e-6
+
+
+@pytest.mark.parametrize("width,batch", [(512, 1024), (768, 2048)])
+def test_f16_epilogue_planes_bit_identical(monkeypatch, width, batch):
+    """The fp16 planes the fused epilogues write (block maximum, scale, hi /
+    lo of the Relu output and of the masked gradient) equal the split pass
+    over the unfused maps' results: every step result bit-identical."""
+    from paper_1801_08058_b200 import abi, workloads as W
+
+    step = W.wide_mlp_step(gf, batch=batch, width=width, layers=3, loss_batch=65536)
+    arrays = W.step_inputs(step, W.parameter_shapes(step), seed=6, x_range=(-1, 1))
+    tens = [gf.tensor_from_flat(F32, a.shape, a) for a in arrays]
+    monkeypatch.setenv("GFB_TC_EPILOGUE", "1")
+    exe = gf.compile_function(step.fn)
+    f16 = [L for L in exe.lowered.launches if L.kind == abi.K_DOT_F16P]
+    assert {L.args.epi_kind for L in f16} == {0, 1, 2} and any(L.args.epi_flags & 4 for L in f16)
+    fused = [t.to_numpy() for t in gf.call(exe, tens)]
+    monkeypatch.setenv("GFB_TC_EPILOGUE", "0")
+    plain = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
+    for a, b in zip(fused, plain):
+        assert G.same_bits(a, b)
+    monkeypatch.setenv("GFB_F16", "0")
+    tf32 = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
+    for a, b in zip(fused, tf32):
+        assert G.normwise(a, b) <= 1e-5

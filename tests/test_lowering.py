@@ -13,6 +13,7 @@ import pytest
 
 import golden_io as G
 from hostcompile import emulate, host_compile
+from paper_1801_08058_b200 import abi
 
 
 def _compare(outs, want_docs, label):
@@ -85,6 +86,58 @@ def test_tensor_core_lowering_emulated(monkeypatch, ta, tb):
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     out = emulate(h, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0]
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_f16_gemm_lowering_emulated(ta, tb):
+    """fp16 planes with 128 x 128 tile scales + the 2xFP16 product (K-major
+    and MN-major operands), emulated: normwise within 1e-6 of the oracle."""
+    import paper_1801_08058_b200 as gf
+    from oracle import interp
+
+    m, k, n = 320, 200, 256
+    fn = gf.Function("dot")
+    K, F32 = gf.OpKind, gf.ElementType.F32
+    a = fn.add_parameter(F32, (k, m) if ta else (m, k))
+    b = fn.add_parameter(F32, (n, k) if tb else (k, n))
+    x = fn.add_node(K.RESHAPE, [a], {"input_order": (1, 0), "output_shape": (m, k)}) if ta else a
+    y = fn.add_node(K.RESHAPE, [b], {"input_order": (1, 0), "output_shape": (k, n)}) if tb else b
+    fn.set_results([fn.add_node(K.DOT, [x, y])])
+    h = host_compile(fn)
+    labels = [L.label.split("#")[0] for L in h.lowered.launches]
+    assert labels == ["split16", "split16", "dot_f16"], labels
+    g = next(L.args for L in h.lowered.launches if L.kind == abi.K_DOT_F16P)
+    assert (g.a_ld_mn > 0, g.b_ld_mn > 0) == (ta, not tb)
+    rng = np.random.default_rng(1)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][:128, :128] *= np.float32(1e-20)  # a tile far below the others: scales are per tile
+    out = emulate(h, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0]
+    ref = interp.run_function(fn, ins)[0]
+    assert G.normwise(out, ref) <= 1e-6
+    assert G.normwise(out[:128], ref[:128]) <= 1e-6
+
+
+def test_f16_epilogue_planes_emulated():
+    """An MLP step whose hidden layers run on the fp16 GEMM: the bias + Relu
+    and Relu-gradient epilogues write the next GEMMs' fp16 planes (no split
+    pass for the activations); outputs within 1e-5 of the oracle."""
+    import paper_1801_08058_b200 as gf
+    from oracle import interp
+    from paper_1801_08058_b200 import workloads as W
+
+    st = W.mlp_step(gf, batch=256, in_dim=256, hidden=(256, 256), out_dim=256)
+    h = host_compile(st.fn)
+    labels = [L.label for L in h.lowered.launches]
+    assert sum(lb.startswith("dot_f16") for lb in labels) == 8, labels  # 3 forward, 3 weight, 2 data gradients
+    assert any("epibias_relu" in lb for lb in labels) and any("epirelu_grad" in lb for lb in labels)
+    planes_by_epi = sum(1 for L in h.lowered.launches if L.kind == abi.K_DOT_F16P and L.args.epi_flags & 4)
+    assert planes_by_epi >= 3
+    rng = np.random.default_rng(3)
+    ins = W.step_inputs(st, W.parameter_shapes(st), seed=3)
+    out = emulate(h, [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v) for v in ins])
+    ref = interp.run_function(st.fn, ins)
+    for o, r in zip(out, ref):
+        assert G.normwise(o, r) <= 1e-5
 
 
 @pytest.mark.parametrize("shape,axes", [((3, 5000), (1,)), ((2, 300, 40), (1, 2)), ((70000,), (0,))])
