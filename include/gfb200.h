@@ -274,7 +274,12 @@ typedef struct GFB_ALIGN64 {
     /* epi_flags bit 2: fp16 planes of y (e_hi, e_lo: [M, N], pitch N) and their scale
      * grid e_sc ([ceil(M / 128), ceil(N / 128)], row-major) */
     uint64_t e_hi, e_sc;
-    int64_t pad[3];
+    /* Relu-gradient mask bytes, [M, N] pitch N: 1 = 1.0, 2 = -0.0, 0 = +0.0, the value of
+     * Maximum(Divide(Relu(x), x), 0) (GFB_K_DOT_F16P).  epi_flags bit 3 (kind 1): write
+     * the mask of x = C; bit 4 (kind 2): read it instead of e_aux2; bit 5: C is not
+     * stored (no reader: the mask and the planes carry everything later launches need). */
+    uint64_t e_mask;
+    int64_t pad[2];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

@@ -911,13 +911,16 @@ class Lowering:
             dst = Buffer(self.new_key(), d.element_type, d.shape, _rowmajor(d.shape), abi.SLOT_IO + self.n_in + j)
             self.emit_copy(src, dst)
 
+        dropped = self._drop_unread_epilogue_outputs()
+
         # arena plan over launch-index live ranges
         live: dict = {}
         for i, L in enumerate(self.launches):
             for k in L.writes + L.reads:
                 lo, hi = live.get(k, (i, i))
                 live[k] = (min(lo, i), max(hi, i))
-        arena_bufs = {b.key: b for b in self.buf.values() if b.slot == abi.SLOT_ARENA and b.base is None}
+        arena_bufs = {b.key: b for b in self.buf.values() if b.slot == abi.SLOT_ARENA and b.base is None
+                      and b.key not in dropped}
         items = {k: (b.nbytes, live.get(k, (0, 0))[0], live.get(k, (0, 0))[1]) for k, b in arena_bufs.items()}
         for region, members in self._grad_regions:
             # the gradient region lives from its first member's producer to its last reader
@@ -934,6 +937,37 @@ class Lowering:
             buffers[region.key] = region
         return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
                        buffers, arena_offsets=plan.offsets)
+
+    def _drop_unread_epilogue_outputs(self) -> set:
+        """fp16 GEMM epilogues store the fp32 tensors of the maps they absorb
+        (the pre-activation C, the Relu output); when no launch reads one --
+        its consumers take the fp16 planes and the mask bytes instead -- the
+        store is dropped and the tensor gets no arena space.  Returns the
+        dropped buffer keys."""
+        read = set()
+        for L in self.launches:
+            read.update(L.reads)
+        dropped = set()
+        for L in self.launches:
+            if L.kind != abi.K_DOT_F16P or not L.args.epi_kind:
+                continue
+            a, bufs = L.args, L.epi_bufs
+            out2 = bufs.get("out2")
+            if (a.epi_flags & 1 and out2 is not None and out2.slot == abi.SLOT_ARENA and out2.base is None
+                    and out2.key not in read):
+                a.epi_flags &= ~1
+                L.writes.remove(out2.key)
+                dropped.add(out2.key)
+            c = bufs["c"]
+            if (a.epi_flags & (4 | 8) and c.slot == abi.SLOT_ARENA and c.base is None and c.key not in read
+                    and c.key not in self._region_keys()):
+                a.epi_flags |= 32
+                L.writes.remove(c.key)
+                dropped.add(c.key)
+        return dropped
+
+    def _region_keys(self) -> set:
+        return {m.key for _, members in self._grad_regions for m in members}
 
     def _flat_channel_last(self, n):
         """Sub-axis storage for a flattened pool-window matrix [k, M] under the
@@ -1763,6 +1797,16 @@ class Lowering:
                 if not (self.is_source(h) and self.is_source(x) and dense2(h, M, N) and dense2(x, M, N)):
                     continue
                 out[d] = {"kind": 2, "out": c, "aux1": h, "aux2": x, "absorbed": {c}, "lo_of": c}
+        # A Relu-gradient epilogue whose x is the pre-activation a bias + Relu
+        # epilogue writes reads that GEMM's mask bytes (1 B per element) instead
+        # of x (4 B); x and the Relu output then often have no reader left and
+        # are not stored at all (_drop_unread_epilogue_outputs).
+        if os.environ.get("GFB_TC_MASK", "1") == "1":
+            writer = {sp["out"]: d for d, sp in out.items() if sp["kind"] == 1}
+            for d, sp in out.items():
+                if sp["kind"] == 2 and sp["aux2"] in writer:
+                    sp["mask"] = sp["aux2"]
+                    out[writer[sp["aux2"]]]["mask_of"] = sp["aux2"]
         return out
 
     def _feeds_tc(self, n) -> bool:
@@ -1893,12 +1937,24 @@ class Lowering:
             if splits > 1 or target.strides != (ncols, 1) or target.elem_off or ncols % 4:
                 raise UnsupportedOp(f"fused epilogue of Dot {n} needs an unsplit GEMM and a dense output")
             ta.epi_kind = epi["kind"]
-            for field, key in (("e_bias", "bias"), ("e_aux1", "aux1"), ("e_aux2", "aux2"), ("e_out2", "out2")):
-                if key in epi:
+            ta.epi_flags = 1 if "out2" in epi else 0
+            mask = self.buf.get(("mask", epi["mask"])) if "mask" in epi else None
+            if mask is not None:
+                refs["e_mask"] = mask
+                reads.append(mask.key)
+                ta.epi_flags |= 16
+            # (the kernel derives the Relu-gradient mask from x alone: e_aux1 is never read)
+            for field, key in (("e_bias", "bias"), ("e_aux2", "aux2"), ("e_out2", "out2")):
+                if key in epi and not (field == "e_aux2" and mask is not None):
                     bb = self.buf[epi[key]]
                     refs[field] = bb
                     (writes if field == "e_out2" else reads).append(bb.key)
-            ta.epi_flags = 1 if "out2" in epi else 0
+            if "mask_of" in epi:
+                mb = Buffer(self.new_key(), ElementType.BOOL, (m * ncols,), (1,))
+                self.buf[("mask", epi["mask_of"])] = mb
+                refs["e_mask"] = mb
+                writes.append(mb.key)
+                ta.epi_flags |= 8
             y = self.buf[epi["lo_of"]]
             root = y.base if y.base is not None else y
             if (y.splat is None and not y.elem_off and not root.subaxes and _dense_rowmajor(root.shape, root.strides)
@@ -1911,6 +1967,7 @@ class Lowering:
             label += ":epi" + ("bias_relu" if epi["kind"] == 1 else "relu_grad")
         rec = LaunchRec(abi.K_DOT_F16P, grid, (320, 1, 1), F16_SMEM_PAIR, ta, reads, writes, label)
         rec.flops = 2 * m * ncols * kdim
+        rec.epi_bufs = {"c": target, "out2": refs.get("e_out2")}
         rec.finalize = _finalize_refs(ta, refs)
         self.launches.append(rec)
         if splits > 1:

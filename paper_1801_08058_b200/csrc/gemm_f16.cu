@@ -80,6 +80,35 @@ __device__ __forceinline__ void split4_f16(float4 v, uint2& hi, uint2& lo) {
 __device__ __forceinline__ float4 scale4(float4 v, float s) {
     return make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
 }
+// Relu-gradient mask bytes (gfb_tc_args.e_mask): the value of
+// Maximum(Divide(Relu(x), x), 0) -- 1 for 0 < x < inf, -0 for x < 0, +0
+// otherwise -- as 1, 2, 0 (relu_grad_mask in tc_prims.cuh).
+__device__ __forceinline__ uint32_t mask_code(float x) { return (x > 0.f && x < INFINITY) ? 1u : (x < 0.f ? 2u : 0u); }
+__device__ __forceinline__ float mask_value(uint32_t code) {
+    code &= 0xffu;
+    return code == 1u ? 1.f : (code == 2u ? -0.f : 0.f);
+}
+// 16 TMEM columns of this warp's 32 lanes (one per thread), fp32
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+          "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+}
 __device__ __forceinline__ float amax4(float m, float4 v) {
     return fmaxf(fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
 }
@@ -259,159 +288,247 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
         constexpr int EC = 128;
         const int q = warp & 3, cg = (warp - 2) >> 2;
         const uint32_t tempty0 = peer_addr(tempty, 0);
-        const float* a_sc = resolve<const float>(p.tab, p.a_sc);
-        const float* b_sc = resolve<const float>(p.tab, p.b_sc);
-        const int64_t mblocks = (p.M + 127) / 128, nblocks = (p.N + 127) / 128;
+        const int mblocks = (int)((p.M + 127) / 128), nblocks = (int)((p.N + 127) / 128);
         int gchunk = 0;
         for (int t = pair_id; t < ntiles; t += npairs) {
             const HTile T = f16_tile(p, t, ntm, ntn);
             const int nchunk = (T.nk + CHUNK_KB - 1) / CHUNK_KB;
-            const int64_t mb = (T.m0 >> 7) + rank, nb = (T.n0 >> 7) + cg;
+            const int mb = (T.m0 >> 7) + (int)rank, nb = (T.n0 >> 7) + cg;
+            // this tile's scale columns: chunk c0 reads sa[c0 * a_sc_k], sb[c0 * b_sc_k]
+            const int kb0 = (int)(T.k_begin >> 7);
+            const float* sa_p = mb < mblocks ? resolve<const float>(p.tab, p.a_sc) + (int64_t)mb * p.a_sc_r + (int64_t)kb0 * p.a_sc_k : nullptr;
+            const float* sb_p = nb < nblocks ? resolve<const float>(p.tab, p.b_sc) + (int64_t)nb * p.b_sc_r + (int64_t)kb0 * p.b_sc_k : nullptr;
+            const int pf_at = p.epi_kind == 2 ? max(0, nchunk - 3) : -1;
             float acc[EC];
 #pragma unroll
             for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            int b_last = 0;
             for (int c0 = 0; c0 < nchunk; ++c0) {
                 const int chunk = gchunk + c0, b = chunk % NBUF;
-                const int64_t kblk = (T.k_begin >> 7) + c0;
-                const float sa = mb < mblocks ? __ldg(a_sc + mb * p.a_sc_r + kblk * p.a_sc_k) : 1.f;
-                const float sb = nb < nblocks ? __ldg(b_sc + nb * p.b_sc_r + kblk * p.b_sc_k) : 1.f;
+                const float sa = sa_p ? __ldg(sa_p + (int64_t)c0 * p.a_sc_k) : 1.f;
+                const float sb = sb_p ? __ldg(sb_p + (int64_t)c0 * p.b_sc_k) : 1.f;
                 const float ia = __frcp_rn(sa), ib = __frcp_rn(sb), inv = ia * ib;  // exact powers of two
                 const bool one_step = inv >= 1.17549435e-38f && inv < INFINITY;
                 mbar_wait(&tfull[b], (chunk / NBUF) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT + cg * EC);
 #pragma unroll
-                for (int c = 0; c < EC / 32; ++c) {
-                    uint32_t r[32];
-                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT + cg * EC + c * 32);
+                for (int c = 0; c < EC / 16; ++c) {
+                    // 16 columns per load: the accumulators plus one load stay inside the
+                    // register budget (spills would go through the small L1 to L2)
+                    uint32_t r[16];
                     asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                        : "r"(taddr));
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                        : "r"(tbase + c * 16));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     if (one_step) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) acc[c * 32 + j] = fmaf(__uint_as_float(r[j]), inv, acc[c * 32 + j]);
+                        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = fmaf(__uint_as_float(r[j]), inv, acc[c * 16 + j]);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __fmul_rn(__fmul_rn(__uint_as_float(r[j]), ia), ib));
+                        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = fmaf(__fmul_rn(__uint_as_float(r[j]), ia), ib, acc[c * 16 + j]);
                     }
+                }
+                if (c0 == nchunk - 1) {
+                    // the tile's sums go back into the buffer just drained (released
+                    // after the store phase), so the stores below run from TMEM
+                    // with a few live registers instead of the 128 accumulators
+#pragma unroll
+                    for (int c = 0; c < EC / 16; ++c) tmem_st16(tbase + c * 16, &acc[c * 16]);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    b_last = b;
+                    break;
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0)
-                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+                    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+                if (c0 == pf_at) {
+                    // the store phase reads this row's 128 mask bytes (or 512 B of x): pull
+                    // them into L2 while the last chunks are still being multiplied
+                    const int64_t row = T.m0 + 128 * (int64_t)rank + q * 32 + lane, col = T.n0 + cg * EC;
+                    if (row < p.M && col < p.N) {
+                        if (p.epi_flags & 16) {
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(resolve<const uint8_t>(p.tab, p.e_mask) + row * p.N + col));
+                        } else {
+                            const float* xr = resolve<const float>(p.tab, p.e_aux2) + row * p.c_sm + col;
+#pragma unroll
+                            for (int l = 0; l < 4; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + 32 * l));
+                        }
+                    }
+                }
             }
             gchunk += nchunk;
+            if (nchunk == 0) continue;
+            const uint32_t tsum = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b_last * NT + cg * EC);
             float* C = resolve<float>(p.tab, p.c) + (p.k_splits > 1 ? (int64_t)T.z * p.split_stride : 0);
             const int64_t rowA = T.m0 + 128 * (int64_t)rank + q * 32;  // this warp's 32 rows
+            const int64_t prow = rowA + lane, colb = T.n0 + cg * EC;
+            const bool rok = prow < p.M;
             const bool coalesced = p.c_sn == 1 && (p.c_sm & 3) == 0 && (p.N & 3) == 0;
             if (!coalesced) {
                 if (p.epi_kind != 0 || (p.epi_flags & 4)) __trap();  // the lowering fuses epilogues into dense outputs only
-                const int64_t row = rowA + lane;
-                if (row < p.M) {
+#pragma unroll 1
+                for (int c = 0; c < EC / 16; ++c) {
+                    float v[16];
+                    tmem_ld16(tsum + c * 16, v);
 #pragma unroll
-                    for (int j = 0; j < EC; ++j) {
-                        const int64_t col = T.n0 + cg * EC + j;
-                        if (col < p.N) C[row * p.c_sm + col * p.c_sn] = acc[j];
+                    for (int j = 0; j < 16; ++j) {
+                        const int64_t col = colb + c * 16 + j;
+                        if (rok && col < p.N) C[prow * p.c_sm + col * p.c_sn] = v[j];
                     }
                 }
-                continue;
-            }
-            float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
-            const float* bias = p.epi_kind == 1 ? resolve<const float>(p.tab, p.e_bias) : nullptr;
-            const float* xin = p.epi_kind == 2 ? resolve<const float>(p.tab, p.e_aux2) : nullptr;
-            float* out2 = (p.epi_flags & 1) ? resolve<float>(p.tab, p.e_out2) : nullptr;
-            const bool planes = (p.epi_flags & 4) != 0;
-            float ymax = 0.f;
-            const int qd = lane & 7;
-#pragma unroll
-            for (int c = 0; c < EC / 32; ++c) {
-                // lane r writes its row's 32 values as 8 swizzled 16-byte pieces
-#pragma unroll
-                for (int d = 0; d < 8; ++d)
-                    *reinterpret_cast<float4*>(xt + lane * 32 + ((d ^ (lane & 7)) << 2)) =
-                        make_float4(acc[c * 32 + 4 * d], acc[c * 32 + 4 * d + 1], acc[c * 32 + 4 * d + 2], acc[c * 32 + 4 * d + 3]);
-                __syncwarp();
-                const int64_t col = T.n0 + cg * EC + c * 32 + 4 * qd;
-                const bool cok = col < p.N;
-                float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (p.epi_kind == 1 && cok) b4 = __ldg(reinterpret_cast<const float4*>(bias + col));
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    float4 x4[4];
-                    if (p.epi_kind == 2) {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const int64_t row = rowA + 4 * (4 * half + i) + (lane >> 3);
-                            x4[i] = (row < p.M && cok) ? __ldg(reinterpret_cast<const float4*>(xin + row * p.c_sm + col))
-                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-                    }
-#pragma unroll
-                    for (int ii = 0; ii < 4; ++ii) {
-                        const int i = 4 * half + ii;
-                        const int rr = 4 * i + (lane >> 3);  // lanes 8k..8k+7 cover one 128-byte row piece
-                        const int64_t row = rowA + rr;
-                        float4 v = *reinterpret_cast<const float4*>(xt + rr * 32 + ((qd ^ (rr & 7)) << 2));
-                        float4 y = v;
+            } else {
+                // Pass 1, row layout (lane = row prow, 16 columns per TMEM load): the
+                // absorbed elementwise maps, their row-layout side stores (the mask
+                // bytes, C / out2 of kind 1), y written back to TMEM and the block
+                // maximum.  Pass 2, through the swizzled transpose tile: C of kinds
+                // 0 / 2 (= y) and the fp16 planes with row-contiguous stores.
+                const bool store_c = (p.epi_flags & 32) == 0;
+                const bool planes = (p.epi_flags & 4) != 0;
+                float ymax = 0.f;
+                if (p.epi_kind != 0 || planes) {
+                    const float* bias = p.epi_kind == 1 ? resolve<const float>(p.tab, p.e_bias) : nullptr;
+                    const bool mask_in = p.epi_kind == 2 && (p.epi_flags & 16);
+                    uint8_t* mkout = p.epi_kind == 1 && (p.epi_flags & 8) ? resolve<uint8_t>(p.tab, p.e_mask) + prow * p.N : nullptr;
+                    const uint8_t* mkrow = mask_in ? resolve<const uint8_t>(p.tab, p.e_mask) + prow * p.N : nullptr;
+                    const float* xrow = p.epi_kind == 2 && !mask_in ? resolve<const float>(p.tab, p.e_aux2) + prow * p.c_sm : nullptr;
+                    float* crow = p.epi_kind == 1 && store_c ? C + prow * p.c_sm : nullptr;
+                    float* orow = (p.epi_flags & 1) ? resolve<float>(p.tab, p.e_out2) + prow * p.c_sm : nullptr;
+#pragma unroll 1
+                    for (int c = 0; c < EC / 16; ++c) {
+                        const int64_t col0 = colb + 16 * c;
+                        const bool full16 = rok && col0 + 16 <= p.N;
+                        float v[16];
+                        tmem_ld16(tsum + c * 16, v);
                         if (p.epi_kind == 1) {
-                            v = make_float4(__fadd_rn(v.x, b4.x), __fadd_rn(v.y, b4.y), __fadd_rn(v.z, b4.z), __fadd_rn(v.w, b4.w));
-                            y = make_float4(v.x > 0.f ? v.x : 0.f, v.y > 0.f ? v.y : 0.f, v.z > 0.f ? v.z : 0.f, v.w > 0.f ? v.w : 0.f);
+                            uint32_t code[4];
+#pragma unroll
+                            for (int d = 0; d < 4; ++d) {
+                                const int64_t col = col0 + 4 * d;
+                                const bool ok = rok && col < p.N;
+                                const float4 b4 = col < p.N ? __ldg(reinterpret_cast<const float4*>(bias + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                                const float4 z = make_float4(__fadd_rn(v[4 * d], b4.x), __fadd_rn(v[4 * d + 1], b4.y),
+                                                             __fadd_rn(v[4 * d + 2], b4.z), __fadd_rn(v[4 * d + 3], b4.w));
+                                const float4 y = make_float4(z.x > 0.f ? z.x : 0.f, z.y > 0.f ? z.y : 0.f, z.z > 0.f ? z.z : 0.f,
+                                                             z.w > 0.f ? z.w : 0.f);
+                                code[d] = mask_code(z.x) | (mask_code(z.y) << 8) | (mask_code(z.z) << 16) | (mask_code(z.w) << 24);
+                                if (ok) {
+                                    ymax = amax4(ymax, y);
+                                    if (crow) *reinterpret_cast<float4*>(crow + col) = z;
+                                    if (orow) *reinterpret_cast<float4*>(orow + col) = y;
+                                }
+                                v[4 * d] = y.x, v[4 * d + 1] = y.y, v[4 * d + 2] = y.z, v[4 * d + 3] = y.w;
+                            }
+                            if (mkout && full16) {
+                                *reinterpret_cast<uint4*>(mkout + col0) = make_uint4(code[0], code[1], code[2], code[3]);
+                            } else if (mkout && rok) {
+#pragma unroll
+                                for (int d = 0; d < 4; ++d)
+                                    if (col0 + 4 * d < p.N) *reinterpret_cast<uint32_t*>(mkout + col0 + 4 * d) = code[d];
+                            }
                         } else if (p.epi_kind == 2) {
-                            v = make_float4(__fmul_rn(v.x, relu_grad_mask(x4[ii].x)), __fmul_rn(v.y, relu_grad_mask(x4[ii].y)),
-                                            __fmul_rn(v.z, relu_grad_mask(x4[ii].z)), __fmul_rn(v.w, relu_grad_mask(x4[ii].w)));
-                            y = v;
+                            uint32_t code[4] = {0u, 0u, 0u, 0u};
+                            float4 x4[4];
+                            if (mask_in) {
+                                if (full16) {
+                                    const uint4 m = __ldg(reinterpret_cast<const uint4*>(mkrow + col0));
+                                    code[0] = m.x, code[1] = m.y, code[2] = m.z, code[3] = m.w;
+                                } else if (rok) {
+#pragma unroll
+                                    for (int d = 0; d < 4; ++d)
+                                        if (col0 + 4 * d < p.N) code[d] = __ldg(reinterpret_cast<const uint32_t*>(mkrow + col0 + 4 * d));
+                                }
+                            } else {
+#pragma unroll
+                                for (int d = 0; d < 4; ++d)
+                                    x4[d] = rok && col0 + 4 * d < p.N ? __ldg(reinterpret_cast<const float4*>(xrow + col0 + 4 * d))
+                                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+#pragma unroll
+                            for (int d = 0; d < 4; ++d) {
+                                float4 y;
+                                if (mask_in)
+                                    y = make_float4(__fmul_rn(v[4 * d], mask_value(code[d])), __fmul_rn(v[4 * d + 1], mask_value(code[d] >> 8)),
+                                                    __fmul_rn(v[4 * d + 2], mask_value(code[d] >> 16)),
+                                                    __fmul_rn(v[4 * d + 3], mask_value(code[d] >> 24)));
+                                else
+                                    y = make_float4(__fmul_rn(v[4 * d], relu_grad_mask(x4[d].x)), __fmul_rn(v[4 * d + 1], relu_grad_mask(x4[d].y)),
+                                                    __fmul_rn(v[4 * d + 2], relu_grad_mask(x4[d].z)),
+                                                    __fmul_rn(v[4 * d + 3], relu_grad_mask(x4[d].w)));
+                                if (rok && col0 + 4 * d < p.N) ymax = amax4(ymax, y);
+                                v[4 * d] = y.x, v[4 * d + 1] = y.y, v[4 * d + 2] = y.z, v[4 * d + 3] = y.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                if (rok && col0 + j < p.N) ymax = amax4(ymax, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                         }
-                        const bool ok = cok && row < p.M;
-                        // keep y for the planes in the registers this chunk came from
-                        acc[c * 32 + 4 * i] = y.x, acc[c * 32 + 4 * i + 1] = y.y;
-                        acc[c * 32 + 4 * i + 2] = y.z, acc[c * 32 + 4 * i + 3] = y.w;
-                        if (!ok) continue;
-                        if (planes) ymax = amax4(ymax, y);
-                        const int64_t off = row * p.c_sm + col;
-                        *reinterpret_cast<float4*>(C + off) = v;
-                        if (out2) *reinterpret_cast<float4*>(out2 + off) = y;
+                        if (p.epi_kind != 0) tmem_st16(tsum + c * 16, v);
+                    }
+                    if (p.epi_kind != 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                }
+                float s = 1.f;
+                __half* ehi = nullptr;
+                __half* elo = nullptr;
+                if (planes) {
+                    // block maximum over the 4 warps of this column group (one 128 x 128 block)
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+                    if (lane == 0) red[warp - 2] = ymax;
+                    asm volatile("bar.sync 1, 256;" ::: "memory");
+                    float m = red[cg * 4];
+#pragma unroll
+                    for (int i = 1; i < 4; ++i) m = fmaxf(m, red[cg * 4 + i]);
+                    asm volatile("bar.sync 1, 256;" ::: "memory");  // red[] is rewritten by the next tile
+                    s = f16_tile_scale(m);
+                    ehi = resolve<__half>(p.tab, p.e_hi);
+                    elo = resolve<__half>(p.tab, p.e_lo);
+                    if (q == 0 && lane == 0 && mb < mblocks && nb < nblocks) resolve<float>(p.tab, p.e_sc)[(int64_t)mb * nblocks + nb] = s;
+                }
+                const bool c_pass2 = store_c && p.epi_kind != 1;  // C == y
+                if (c_pass2 || planes) {
+                    float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
+                    const int qd = lane & 7;
+#pragma unroll 1
+                    for (int c = 0; c < EC / 32; ++c) {
+                        float v[16];
+                        // lane r writes its row's 32 values as 8 swizzled 16-byte pieces
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            tmem_ld16(tsum + c * 32 + 16 * h, v);
+#pragma unroll
+                            for (int d = 0; d < 4; ++d)
+                                *reinterpret_cast<float4*>(xt + lane * 32 + (((4 * h + d) ^ (lane & 7)) << 2)) =
+                                    make_float4(v[4 * d], v[4 * d + 1], v[4 * d + 2], v[4 * d + 3]);
+                        }
+                        __syncwarp();
+                        const int64_t col = colb + c * 32 + 4 * qd;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int rr = 4 * i + (lane >> 3);  // lanes 8k..8k+7 cover one 128-byte row piece
+                            const int64_t row = rowA + rr;
+                            const float4 y = *reinterpret_cast<const float4*>(xt + rr * 32 + ((qd ^ (rr & 7)) << 2));
+                            if (col >= p.N || row >= p.M) continue;
+                            if (c_pass2) *reinterpret_cast<float4*>(C + row * p.c_sm + col) = y;
+                            if (planes) {
+                                uint2 hh, ll;
+                                split4_f16(scale4(y, s), hh, ll);
+                                *reinterpret_cast<uint2*>(ehi + row * p.N + col) = hh;
+                                *reinterpret_cast<uint2*>(elo + row * p.N + col) = ll;
+                            }
+                        }
+                        __syncwarp();
                     }
                 }
-                __syncwarp();
             }
-            if (planes) {
-                // block maximum over the 4 warps of this column group (one 128 x 128 block)
-#pragma unroll
-                for (int o = 16; o; o >>= 1) ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
-                if (lane == 0) red[warp - 2] = ymax;
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                float m = red[cg * 4];
-#pragma unroll
-                for (int i = 1; i < 4; ++i) m = fmaxf(m, red[cg * 4 + i]);
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // red[] is rewritten by the next tile
-                const float s = f16_tile_scale(m);
-                __half* ehi = resolve<__half>(p.tab, p.e_hi);
-                __half* elo = resolve<__half>(p.tab, p.e_lo);
-                if (q == 0 && lane == 0 && mb < mblocks && nb < nblocks) resolve<float>(p.tab, p.e_sc)[mb * nblocks + nb] = s;
-#pragma unroll
-                for (int c = 0; c < EC / 32; ++c) {
-                    const int64_t col = T.n0 + cg * EC + c * 32 + 4 * qd;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int64_t row = rowA + 4 * i + (lane >> 3);
-                        if (col >= p.N || row >= p.M) continue;
-                        uint2 h, l;
-                        split4_f16(scale4(make_float4(acc[c * 32 + 4 * i], acc[c * 32 + 4 * i + 1], acc[c * 32 + 4 * i + 2],
-                                                      acc[c * 32 + 4 * i + 3]),
-                                          s),
-                                   h, l);
-                        *reinterpret_cast<uint2*>(ehi + row * p.N + col) = h;
-                        *reinterpret_cast<uint2*>(elo + row * p.N + col) = l;
-                    }
-                }
-            }
+            // release the staged buffer to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b_last * 8) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");

@@ -430,17 +430,26 @@ def run_f16p(mem, a):
                     y = np.where(c > 0, c, np.float32(0)).astype(np.float32)
                     if a.epi_flags & 1:
                         mem.view(a.e_out2, np.float32)[: a.M * a.N] = y.reshape(-1)
+                    if a.epi_flags & 8:  # mask bytes of x = c: 1 -> 1.0, 2 -> -0.0, 0 -> +0.0
+                        code = np.where((c > 0) & (c < np.inf), 1, np.where(c < 0, 2, 0)).astype(np.uint8)
+                        mem.view(a.e_mask, np.uint8)[: a.M * a.N] = code.reshape(-1)
                 elif a.epi_kind == 2:
-                    x = mem.view(a.e_aux2, np.float32)[: a.M * a.N].reshape(a.M, a.N)
-                    r = (np.where(x > 0, x, np.float32(0)) / x).astype(np.float32)
-                    c = (c * np.where(r >= 0, r, np.float32(0))).astype(np.float32)
+                    if a.epi_flags & 16:
+                        code = mem.view(a.e_mask, np.uint8)[: a.M * a.N].reshape(a.M, a.N)
+                        r = np.where(code == 1, np.float32(1), np.where(code == 2, np.float32(-0.0), np.float32(0)))
+                        c = (c * r.astype(np.float32)).astype(np.float32)
+                    else:
+                        x = mem.view(a.e_aux2, np.float32)[: a.M * a.N].reshape(a.M, a.N)
+                        r = (np.where(x > 0, x, np.float32(0)) / x).astype(np.float32)
+                        c = (c * np.where(r >= 0, r, np.float32(0))).astype(np.float32)
                     y = c
             if a.epi_flags & 4:
                 hi, lo, sc = _f16_split(y, a.M, a.N)
                 mem.view(a.e_hi, np.float16)[: a.M * a.N] = hi.reshape(-1)
                 mem.view(a.e_lo, np.float16)[: a.M * a.N] = lo.reshape(-1)
                 mem.view(a.e_sc, np.float32)[: sc.size] = sc.reshape(-1)
-        C[base + i * a.c_sm + j * a.c_sn] = c
+        if not a.epi_flags & 32:
+            C[base + i * a.c_sm + j * a.c_sn] = c
 
 
 def _trunc_split(x):

@@ -130,8 +130,12 @@ def test_f16_epilogue_planes_emulated():
     labels = [L.label for L in h.lowered.launches]
     assert sum(lb.startswith("dot_f16") for lb in labels) == 8, labels  # 3 forward, 3 weight, 2 data gradients
     assert any("epibias_relu" in lb for lb in labels) and any("epirelu_grad" in lb for lb in labels)
-    planes_by_epi = sum(1 for L in h.lowered.launches if L.kind == abi.K_DOT_F16P and L.args.epi_flags & 4)
-    assert planes_by_epi >= 3
+    f16 = [L for L in h.lowered.launches if L.kind == abi.K_DOT_F16P]
+    assert sum(1 for L in f16 if L.args.epi_flags & 4) >= 3
+    # the backward reads the forward's mask bytes; the pre-activations and the
+    # Relu outputs are then never stored (their readers take planes / masks)
+    assert sum(1 for L in f16 if L.args.epi_flags & 8) == 2 and sum(1 for L in f16 if L.args.epi_flags & 16) == 2
+    assert all(L.args.epi_flags & 32 and not L.args.epi_flags & 1 for L in f16 if L.args.epi_kind == 1)
     rng = np.random.default_rng(3)
     ins = W.step_inputs(st, W.parameter_shapes(st), seed=3)
     out = emulate(h, [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v) for v in ins])
