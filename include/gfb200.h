@@ -279,7 +279,11 @@ typedef struct GFB_ALIGN64 {
      * the mask of x = C; bit 4 (kind 2): read it instead of e_aux2; bit 5: C is not
      * stored (no reader: the mask and the planes carry everything later launches need). */
     uint64_t e_mask;
-    int64_t pad[2];
+    /* epi_flags bit 6: column sums of C over each 32-row block, e_csum[(m / 32) * N + n]
+     * (rows in order within a lane, then a fixed shuffle tree): the bias gradient's Sum
+     * over the batch finishes as a reduction over ceil(M / 32) rows */
+    uint64_t e_csum;
+    int64_t pad[1];
     uint64_t tmap[4][16];
 } gfb_tc_args;
 

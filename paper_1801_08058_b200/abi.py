@@ -109,8 +109,8 @@ class TcArgs(C.Structure):
         ("e_out2", C.c_uint64), ("e_lo", C.c_uint64), ("epi_flags", C.c_int64),
         ("a_sc", C.c_uint64), ("b_sc", C.c_uint64),
         ("a_sc_r", C.c_int64), ("a_sc_k", C.c_int64), ("b_sc_r", C.c_int64), ("b_sc_k", C.c_int64),
-        ("e_hi", C.c_uint64), ("e_sc", C.c_uint64), ("e_mask", C.c_uint64),
-        ("pad", C.c_int64 * 2),
+        ("e_hi", C.c_uint64), ("e_sc", C.c_uint64), ("e_mask", C.c_uint64), ("e_csum", C.c_uint64),
+        ("pad", C.c_int64 * 1),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
 

@@ -827,6 +827,7 @@ class Lowering:
             if node.op not in (OpKind.PARAMETER, OpKind.CONSTANT) and r not in result_slot and r not in self.allreduce:
                 result_slot[r] = j
 
+        self._csum_done = set()
         self._epi = self._plan_epilogues()
         self._epi_nodes = {m for sp in self._epi.values() for m in sp["absorbed"]}
         for n in self.order:
@@ -889,8 +890,8 @@ class Lowering:
                 if n == rg.anchor:
                     self.emit_row_group(rg)
                 continue
-            if n in self._epi_nodes:
-                continue  # written by the epilogue of the Dot it consumes
+            if n in self._epi_nodes or n in self._csum_done:
+                continue  # written by the epilogue of the Dot it consumes (or reduced from its partials)
             if self.is_heavy(n):
                 self.emit_heavy(n)
             elif n in self.M and n not in merged and n not in grouped and n not in chained:
@@ -1797,6 +1798,15 @@ class Lowering:
                 if not (self.is_source(h) and self.is_source(x) and dense2(h, M, N) and dense2(x, M, N)):
                     continue
                 out[d] = {"kind": 2, "out": c, "aux1": h, "aux2": x, "absorbed": {c}, "lo_of": c}
+                # the bias gradient Sum(c, axes (0,)) reads c once more: the epilogue
+                # writes 32-row column partials and the Sum reduces those instead
+                for r in self.consumers[c]:
+                    rn = nodes[r]
+                    if (rn.op is OpKind.SUM and tuple(rn.attrs["reduction_axes"]) == (0,)
+                            and rn.attrs["reduction_kind"] == "sum" and r in self.M and r not in self._row_nodes
+                            and os.environ.get("GFB_TC_COLSUM", "1") == "1"):
+                        out[d]["colsum"] = r
+                        break
         # A Relu-gradient epilogue whose x is the pre-activation a bias + Relu
         # epilogue writes reads that GEMM's mask bytes (1 B per element) instead
         # of x (4 B); x and the Relu output then often have no reader left and
@@ -1965,11 +1975,28 @@ class Lowering:
                 writes.extend(pl.key for pl in planes)
                 ta.epi_flags |= 4
             label += ":epi" + ("bias_relu" if epi["kind"] == 1 else "relu_grad")
+        colsum = None
+        if epi is not None and "colsum" in epi and ncols % 4 == 0:
+            rp = (m + 31) // 32
+            part = Buffer(self.new_key(), ElementType.F32, (rp, ncols), (ncols, 1))
+            self.buf[("csum", n)] = part
+            refs["e_csum"] = part
+            writes.append(part.key)
+            ta.epi_flags |= 64
+            colsum = (epi["colsum"], part, rp)
         rec = LaunchRec(abi.K_DOT_F16P, grid, (320, 1, 1), F16_SMEM_PAIR, ta, reads, writes, label)
         rec.flops = 2 * m * ncols * kdim
         rec.epi_bufs = {"c": target, "out2": refs.get("e_out2")}
         rec.finalize = _finalize_refs(ta, refs)
         self.launches.append(rec)
+        if colsum is not None:
+            s, part, rp = colsum
+            p2 = Program(self, extents=(ncols, rp), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(part, [(1, 1, rp), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.set_red_out(self.buf[s], iteration_axes(self.nodes[s].output.shape))
+            self._col_launch(p2, ncols, rp, 1, f"colsum#{s}:part", ElementType.F32)
+            self._csum_done.add(s)
         if splits > 1:
             p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
             k = p2.leaf(target, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])

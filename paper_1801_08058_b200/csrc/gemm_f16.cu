@@ -397,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                     const float* xrow = p.epi_kind == 2 && !mask_in ? resolve<const float>(p.tab, p.e_aux2) + prow * p.c_sm : nullptr;
                     float* crow = p.epi_kind == 1 && store_c ? C + prow * p.c_sm : nullptr;
                     float* orow = (p.epi_flags & 1) ? resolve<float>(p.tab, p.e_out2) + prow * p.c_sm : nullptr;
-#pragma unroll 1
+#pragma unroll 2
                     for (int c = 0; c < EC / 16; ++c) {
                         const int64_t col0 = colb + 16 * c;
                         const bool full16 = rok && col0 + 16 <= p.N;
@@ -489,10 +489,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                     if (q == 0 && lane == 0 && mb < mblocks && nb < nblocks) resolve<float>(p.tab, p.e_sc)[(int64_t)mb * nblocks + nb] = s;
                 }
                 const bool c_pass2 = store_c && p.epi_kind != 1;  // C == y
-                if (c_pass2 || planes) {
+                float* csum = (p.epi_flags & 64) ? resolve<float>(p.tab, p.e_csum) + (rowA >> 5) * p.N : nullptr;
+                if (c_pass2 || planes || csum) {
                     float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
                     const int qd = lane & 7;
-#pragma unroll 1
+#pragma unroll
                     for (int c = 0; c < EC / 32; ++c) {
                         float v[16];
                         // lane r writes its row's 32 values as 8 swizzled 16-byte pieces
@@ -506,12 +507,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                         }
                         __syncwarp();
                         const int64_t col = colb + c * 32 + 4 * qd;
+                        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // this lane's rows, in order
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             const int rr = 4 * i + (lane >> 3);  // lanes 8k..8k+7 cover one 128-byte row piece
                             const int64_t row = rowA + rr;
                             const float4 y = *reinterpret_cast<const float4*>(xt + rr * 32 + ((qd ^ (rr & 7)) << 2));
                             if (col >= p.N || row >= p.M) continue;
+                            if (csum) cs = make_float4(__fadd_rn(cs.x, y.x), __fadd_rn(cs.y, y.y), __fadd_rn(cs.z, y.z), __fadd_rn(cs.w, y.w));
                             if (c_pass2) *reinterpret_cast<float4*>(C + row * p.c_sm + col) = y;
                             if (planes) {
                                 uint2 hh, ll;
@@ -519,6 +522,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                                 *reinterpret_cast<uint2*>(ehi + row * p.N + col) = hh;
                                 *reinterpret_cast<uint2*>(elo + row * p.N + col) = ll;
                             }
+                        }
+                        if (csum) {
+                            // the four row groups (lane >> 3) of one column quad: (p0 + p1) + (p2 + p3)
+#pragma unroll
+                            for (int o = 8; o <= 16; o <<= 1)
+                                cs = make_float4(__fadd_rn(cs.x, __shfl_xor_sync(0xffffffffu, cs.x, o)),
+                                                 __fadd_rn(cs.y, __shfl_xor_sync(0xffffffffu, cs.y, o)),
+                                                 __fadd_rn(cs.z, __shfl_xor_sync(0xffffffffu, cs.z, o)),
+                                                 __fadd_rn(cs.w, __shfl_xor_sync(0xffffffffu, cs.w, o)));
+                            if (lane < 8 && col < p.N) *reinterpret_cast<float4*>(csum + col) = cs;
                         }
                         __syncwarp();
                     }

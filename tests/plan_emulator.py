@@ -448,6 +448,16 @@ def run_f16p(mem, a):
                 mem.view(a.e_hi, np.float16)[: a.M * a.N] = hi.reshape(-1)
                 mem.view(a.e_lo, np.float16)[: a.M * a.N] = lo.reshape(-1)
                 mem.view(a.e_sc, np.float32)[: sc.size] = sc.reshape(-1)
+        if a.epi_flags & 64:  # 32-row column partials: each lane's 8 rows in order, then (p0 + p1) + (p2 + p3)
+            rp = (a.M + 31) // 32
+            yy = np.zeros((rp * 32, a.N), dtype=np.float32)
+            yy[: a.M] = y
+            g = yy.reshape(rp, 8, 4, a.N)  # row 32 b + 4 i + g
+            part = np.zeros((rp, 4, a.N), dtype=np.float32)
+            for ii in range(8):
+                part = (part + g[:, ii]).astype(np.float32)
+            tot = ((part[:, 0] + part[:, 1]).astype(np.float32) + (part[:, 2] + part[:, 3]).astype(np.float32)).astype(np.float32)
+            mem.view(a.e_csum, np.float32)[: rp * a.N] = tot.reshape(-1)
         if not a.epi_flags & 32:
             C[base + i * a.c_sm + j * a.c_sn] = c
 

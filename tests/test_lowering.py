@@ -136,6 +136,8 @@ def test_f16_epilogue_planes_emulated():
     # Relu outputs are then never stored (their readers take planes / masks)
     assert sum(1 for L in f16 if L.args.epi_flags & 8) == 2 and sum(1 for L in f16 if L.args.epi_flags & 16) == 2
     assert all(L.args.epi_flags & 32 and not L.args.epi_flags & 1 for L in f16 if L.args.epi_kind == 1)
+    # the bias gradients reduce the Relu-gradient epilogues' 32-row column partials
+    assert sum(1 for L in f16 if L.args.epi_flags & 64) == 2 and sum(":part" in lb for lb in labels) == 2
     rng = np.random.default_rng(3)
     ins = W.step_inputs(st, W.parameter_shapes(st), seed=3)
     out = emulate(h, [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v) for v in ins])
