@@ -459,6 +459,13 @@ int gfb_exe_destroy(gfb_exe* exe);
 int gfb_exe_set_io(gfb_exe* exe, const uint64_t* in_bytes, const uint64_t* out_bytes, const uint32_t* read_offsets,
                    const uint32_t* reads, const uint32_t* out_writer);
 int gfb_exe_run_host(gfb_exe* exe, const void* const* host_inputs, void* const* host_outputs, void* stream);
+/* Optional, after gfb_exe_set_io: copy the inputs in pieces (piece p = bytes
+ * [piece_offset[p], + piece_bytes[p]) of input piece_input[p]) and let each
+ * launch wait only for the pieces it reads (CSR over the launch list, piece
+ * indices), e.g. the row chunks of a large input whose first GEMM runs chunk
+ * by chunk, so the step starts once the first piece has crossed PCIe. */
+int gfb_exe_set_io_pieces(gfb_exe* exe, uint32_t n_pieces, const uint32_t* piece_input, const uint64_t* piece_offset,
+                          const uint64_t* piece_bytes, const uint32_t* read_offsets, const uint32_t* reads);
 /* Number of kernels one run launches (for bench accounting). */
 int gfb_exe_num_launches(const gfb_exe* exe);
 /* Launch only record `index` of the plan (profiling / per-kernel timing). */

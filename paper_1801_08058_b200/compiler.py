@@ -240,6 +240,7 @@ class Buffer:
     elem_off: int = 0     # view origin, in elements from the base's origin
     subaxes: dict = None  # axis -> [(extent, stride), ...] outer to inner: a flattened axis stored permuted
     bucket: object = None  # (gradient region, is_max) for a data-parallel partial root
+    exact: bool = False   # a contiguous view [elem_off, + its element count) of its base (row chunks)
 
     @property
     def nbytes(self) -> int:
@@ -828,6 +829,8 @@ class Lowering:
                 result_slot[r] = j
 
         self._csum_done = set()
+        self._f16_chunks = {}   # caller input key -> its row chunks' plane views (_f16_planes)
+        self._epi_planes = set()  # tensors whose fp16 planes a GEMM epilogue writes
         self._epi = self._plan_epilogues()
         self._epi_nodes = {m for sp in self._epi.values() for m in sp["absorbed"]}
         for n in self.order:
@@ -902,6 +905,7 @@ class Lowering:
 
         if self.allreduce:
             self._bucket_allreduces()
+        self._hoist_result_writers()
 
         # results that are parameters / constants / repeated: copy launches
         for j, (r, _) in enumerate(results):
@@ -912,14 +916,22 @@ class Lowering:
             dst = Buffer(self.new_key(), d.element_type, d.shape, _rowmajor(d.shape), abi.SLOT_IO + self.n_in + j)
             self.emit_copy(src, dst)
 
+        for chunks in self._f16_chunks.values():
+            for ch in chunks:
+                if ch[5] is not None:
+                    raise UnsupportedOp("a row-chunked fp16 split was never consumed")
         dropped = self._drop_unread_epilogue_outputs()
 
         # arena plan over launch-index live ranges
         live: dict = {}
+        view_base = {b.key: b.base.key for b in self.buf.values() if b.exact and b.base is not None}
         for i, L in enumerate(self.launches):
-            for k in L.writes + L.reads:
-                lo, hi = live.get(k, (i, i))
-                live[k] = (min(lo, i), max(hi, i))
+            for k0 in L.writes + L.reads:
+                for k in (k0, view_base.get(k0)):  # a row view keeps its base alive
+                    if k is None:
+                        continue
+                    lo, hi = live.get(k, (i, i))
+                    live[k] = (min(lo, i), max(hi, i))
         arena_bufs = {b.key: b for b in self.buf.values() if b.slot == abi.SLOT_ARENA and b.base is None
                       and b.key not in dropped}
         items = {k: (b.nbytes, live.get(k, (0, 0))[0], live.get(k, (0, 0))[1]) for k, b in arena_bufs.items()}
@@ -939,32 +951,76 @@ class Lowering:
         return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
                        buffers, arena_offsets=plan.offsets)
 
+    def _hoist_result_writers(self):
+        """Move each launch that writes a caller result (the optimizer
+        updates of a training step, which the graph orders last) to just
+        after the last launch it depends on.  Host-buffer runs copy a result
+        back right after its writer, so config E's new weights then cross
+        PCIe under the rest of the backward pass instead of after it."""
+        if os.environ.get("GFB_HOIST_RESULTS", "1") != "1":
+            return
+        root_of = {b.key: (b.base.key if b.exact and b.base is not None else b.key) for b in self.buf.values()}
+        res_lo = abi.SLOT_IO + self.n_in
+        out_keys = {b.key for b in self.buf.values() if b.base is None and b.slot >= res_lo}
+
+        def acc(L):
+            r = {root_of.get(k, k) for k in L.reads}
+            w = {root_of.get(k, k) for k in L.writes}
+            return r, w
+
+        out, accs = [], []
+        for L in self.launches:
+            r, w = acc(L)
+            pos = len(out)
+            if (L.kind != abi.K_ALLREDUCE and getattr(L, "chain", None) is None and w & out_keys
+                    and not any(k is None for k in w)):
+                pos = 0
+                for idx in range(len(out) - 1, -1, -1):
+                    r2, w2 = accs[idx]
+                    if (r & w2) or (w & (r2 | w2)) or out[idx].kind == abi.K_ALLREDUCE:
+                        pos = idx + 1
+                        break
+            out.insert(pos, L)
+            accs.insert(pos, (r, w))
+        self.launches = out
+
     def _drop_unread_epilogue_outputs(self) -> set:
         """fp16 GEMM epilogues store the fp32 tensors of the maps they absorb
         (the pre-activation C, the Relu output); when no launch reads one --
         its consumers take the fp16 planes and the mask bytes instead -- the
         store is dropped and the tensor gets no arena space.  Returns the
         dropped buffer keys."""
+        base_of = {b.key: (b.base if b.exact and b.base is not None else b) for b in self.buf.values()}
         read = set()
         for L in self.launches:
-            read.update(L.reads)
+            for k in L.reads:
+                read.add(k)
+                if k in base_of:
+                    read.add(base_of[k].key)  # a row view read reads its base
         dropped = set()
+
+        def unread(b):  # an arena tensor (or a row view of one) nobody reads
+            if b is None:
+                return None
+            root = b.base if b.exact and b.base is not None else b
+            if root.slot != abi.SLOT_ARENA or root.base is not None or root.key in read or b.key in read:
+                return None
+            return root
+
         for L in self.launches:
             if L.kind != abi.K_DOT_F16P or not L.args.epi_kind:
                 continue
             a, bufs = L.args, L.epi_bufs
-            out2 = bufs.get("out2")
-            if (a.epi_flags & 1 and out2 is not None and out2.slot == abi.SLOT_ARENA and out2.base is None
-                    and out2.key not in read):
+            r2 = unread(bufs.get("out2")) if a.epi_flags & 1 else None
+            if r2 is not None:
                 a.epi_flags &= ~1
-                L.writes.remove(out2.key)
-                dropped.add(out2.key)
-            c = bufs["c"]
-            if (a.epi_flags & (4 | 8) and c.slot == abi.SLOT_ARENA and c.base is None and c.key not in read
-                    and c.key not in self._region_keys()):
+                L.writes.remove(bufs["out2"].key)
+                dropped.add(r2.key)
+            rc = unread(bufs["c"]) if a.epi_flags & (4 | 8) else None
+            if rc is not None and rc.key not in self._region_keys():
                 a.epi_flags |= 32
-                L.writes.remove(c.key)
-                dropped.add(c.key)
+                L.writes.remove(bufs["c"].key)
+                dropped.add(rc.key)
         return dropped
 
     def _region_keys(self) -> set:
@@ -1712,10 +1768,31 @@ class Lowering:
         (ab, ast), (bb, bst) = a_op, b_op
         pair = m >= 256 and nn >= 256 and os.environ.get("GFB_TC_PAIR", "1") == "1" and os.environ.get("GFB_TC_WIDE", "1") == "1"
         if pair and use_f16():
-            a16 = self._f16_operand(ab, ast[0], ast[1], m, k)
-            b16 = self._f16_operand(bb, bst[1], bst[0], nn, k) if a16 is not None else None
-            if b16 is not None:
-                rec = self._f16_gemm(n, a16, b16, out, m, nn, k, {"c_sm": out.strides[0], "c_sn": out.strides[1]}, f"dot_f16#{n}")
+            # B first: its planes (a weight, typically) are then split -- and under
+            # host-buffer runs copied -- before the row chunks of a large A input
+            b16 = self._f16_operand(bb, bst[1], bst[0], nn, k)
+            a16 = self._f16_operand(ab, ast[0], ast[1], m, k) if b16 is not None else None
+            if b16 is not None and a16 is None:
+                self._flush_chunks(bb)  # (planes made for nothing; keep them consistent)
+            if a16 is not None:
+                addr = {"c_sm": out.strides[0], "c_sn": out.strides[1]}
+                root = ab.base if ab.base is not None else ab
+                chunks = self._f16_chunks.get(root.key) if a16[4] == 0 else None
+                epi = self._epi.get(n, {})
+                self._flush_chunks(bb)
+                if (chunks and chunks[0][5] is not None and self._tc_splits(chunks[0][1] - chunks[0][0], nn, k) == 1
+                        and "colsum" not in epi and out.strides == (nn, 1) and not out.elem_off and out.base is None):
+                    for ch in chunks:  # split chunk c, then the GEMM over its rows (one chain)
+                        r0, r1, hv, lv, sv, split = ch
+                        split.chain = ("rows", n)
+                        self._emit_chunk(ch)
+                        rec = self._f16_gemm(n, (hv, lv, sv) + a16[3:], b16, out, r1 - r0, nn, k, addr,
+                                             f"dot_f16#{n}:rows{r0}", rows=(r0, m))
+                        rec.algo_bytes = ((r1 - r0) * k + k * nn + (r1 - r0) * nn) * 4
+                        rec.chain = ("rows", n)
+                    return
+                self._flush_chunks(ab)
+                rec = self._f16_gemm(n, a16, b16, out, m, nn, k, addr, f"dot_f16#{n}")
                 rec.algo_bytes = (m * k + k * nn + m * nn) * 4
                 return
         a = self._raw_mn(ab, ast[0], ast[1], m, k) if pair else None
@@ -1892,6 +1969,28 @@ class Lowering:
             return got
         planes = self._f16_buffers(root, R, Cc)
         hi, lo, sc = planes
+        nch = self._input_chunks(root, R, Cc)
+        if nch > 1:
+            # a large caller input crosses PCIe in row chunks under host-buffer
+            # runs: split (and multiply, _f16_gemm) chunk by chunk, so the
+            # first GEMM starts when the first rows have arrived
+            rows = R // nch
+            tcn = (Cc + 127) // 128
+            chunks = []
+            for c in range(nch):
+                r0, r1 = c * rows, (c + 1) * rows
+                src = self._row_view(root, r0, r1, Cc)
+                hv, lv = self._row_view(hi, r0, r1, Cc // 2), self._row_view(lo, r0, r1, Cc // 2)
+                sv = self._row_view(sc, r0 // 128, r1 // 128, tcn)
+                sa = abi.Split16Args(rows=rows, cols=Cc, ld=Cc)
+                tiles = (rows // 128) * tcn
+                rec = LaunchRec(abi.K_SPLIT_F16, (max(1, min(tiles, NUM_SMS * 4)), 1, 1), (256, 1, 1), 0, sa, [src.key],
+                                [hv.key, lv.key, sv.key], f"split16#{root.key}:rows{r0}")
+                rec.algo_bytes = rows * Cc * 8
+                rec.finalize = _finalize_refs(sa, {"src": src, "hi": hv, "lo": lv, "sc": sv})
+                chunks.append([r0, r1, hv, lv, sv, rec])  # emitted by _emit_chunk (before its GEMM chunk)
+            self._f16_chunks[root.key] = chunks
+            return planes
         sa = abi.Split16Args(rows=R, cols=Cc, ld=Cc)
         tiles = ((R + 127) // 128) * ((Cc + 127) // 128)
         rec = LaunchRec(abi.K_SPLIT_F16, (max(1, min(tiles, NUM_SMS * 4)), 1, 1), (256, 1, 1), 0, sa, [root.key],
@@ -1900,6 +1999,37 @@ class Lowering:
         rec.finalize = _finalize_refs(sa, {"src": root, "hi": hi, "lo": lo, "sc": sc})
         self.launches.append(rec)
         return planes
+
+    def _input_chunks(self, root, R, Cc) -> int:
+        """Row chunks of a caller input's fp16 split (GFB_INPUT_CHUNKS, 8):
+        inputs of at least 256 MB whose rows split into whole 256-row tiles."""
+        nch = int(os.environ.get("GFB_INPUT_CHUNKS", "8"))
+        min_mb = float(os.environ.get("GFB_INPUT_CHUNK_MIN_MB", "256"))
+        if (nch <= 1 or not (abi.SLOT_IO <= root.slot < abi.SLOT_IO + self.n_in) or R * Cc * 4 < min_mb * (1 << 20)
+                or R % (nch * 256) or Cc % 8):
+            return 1
+        return nch
+
+    def _emit_chunk(self, ch):
+        if ch[5] is not None:
+            self.launches.append(ch[5])
+            ch[5] = None
+
+    def _flush_chunks(self, *bufs):
+        """Every pending split chunk of these operands' inputs (a consumer
+        that reads the whole planes)."""
+        for b in bufs:
+            root = b.base if b.base is not None else b
+            for ch in self._f16_chunks.get(root.key, ()):
+                self._emit_chunk(ch)
+
+    def _row_view(self, base, r0, r1, row_elems):
+        """Rows [r0, r1) of the dense row-major `base` (row_elems elements of
+        base.et per row) as an exact contiguous view with its own key."""
+        v = Buffer(self.new_key(), base.et, ((r1 - r0) * row_elems,), (1,), base.slot, base.offset, None, base=base,
+                   elem_off=r0 * row_elems, exact=True)
+        self.buf[("view", v.key)] = v
+        return v
 
     def _f16_get(self, root):
         parts = [self.buf.get(("f16", root.key, p)) for p in ("hi", "lo", "sc")]
@@ -1915,15 +2045,21 @@ class Lowering:
             self.buf[("f16", root.key, p)] = b
         return hi, lo, sc
 
-    def _f16_gemm(self, n, a, b, out, m, ncols, kdim, addr, label):
+    def _f16_gemm(self, n, a, b, out, m, ncols, kdim, addr, label, rows=None):
         """The fp16 pair GEMM over planes (split-K on 128-K boundaries, the
-        scale blocks, + the deterministic reduce pass)."""
+        scale blocks, + the deterministic reduce pass).  rows = (r0, M): this
+        launch covers rows [r0, r0 + m) of an M-row product (a row chunk of a
+        split input): the output and every epilogue tensor are row views."""
         (ahi, alo, asc, kpa, a_mn, a_r, a_k), (bhi, blo, bsc, kpb, b_mn, b_r, b_k) = a, b
+        r0, m_full = rows if rows is not None else (0, m)
+
+        def chunk(buf, row_elems):  # rows [r0, r0 + m) of a full [m_full, ...] buffer
+            return buf if rows is None else self._row_view(buf, r0, r0 + m, row_elems)
         splits = self._tc_splits(m, ncols, kdim)
         ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn,
                         a_sc_r=a_r, a_sc_k=a_k, b_sc_r=b_r, b_sc_k=b_k,
                         group_m=int(os.environ.get("GFB_TC_GROUP_M", "1")))
-        target = out
+        target = chunk(out, ncols)
         if splits > 1:
             kchunks = (kdim + 127) // 128
             per = ((kchunks + splits - 1) // splits) * 128
@@ -1944,7 +2080,7 @@ class Lowering:
         refs = {"c": target, "a_hi": ahi, "a_lo": alo, "a_sc": asc, "b_hi": bhi, "b_lo": blo, "b_sc": bsc}
         epi = self._epi.get(n) if hasattr(self, "_epi") else None
         if epi is not None:
-            if splits > 1 or target.strides != (ncols, 1) or target.elem_off or ncols % 4:
+            if splits > 1 or ncols % 4 or (rows is None and (target.strides != (ncols, 1) or target.elem_off)):
                 raise UnsupportedOp(f"fused epilogue of Dot {n} needs an unsplit GEMM and a dense output")
             ta.epi_kind = epi["kind"]
             ta.epi_flags = 1 if "out2" in epi else 0
@@ -1954,23 +2090,38 @@ class Lowering:
                 reads.append(mask.key)
                 ta.epi_flags |= 16
             # (the kernel derives the Relu-gradient mask from x alone: e_aux1 is never read)
+            if mask is not None and rows is not None:
+                mask = chunk(mask, ncols)
+                refs["e_mask"] = mask
+                reads[-1] = mask.key
             for field, key in (("e_bias", "bias"), ("e_aux2", "aux2"), ("e_out2", "out2")):
                 if key in epi and not (field == "e_aux2" and mask is not None):
                     bb = self.buf[epi[key]]
+                    if field != "e_bias":
+                        bb = chunk(bb, ncols)
                     refs[field] = bb
                     (writes if field == "e_out2" else reads).append(bb.key)
             if "mask_of" in epi:
-                mb = Buffer(self.new_key(), ElementType.BOOL, (m * ncols,), (1,))
-                self.buf[("mask", epi["mask_of"])] = mb
+                mb = self.buf.get(("mask", epi["mask_of"]))
+                if mb is None:
+                    mb = Buffer(self.new_key(), ElementType.BOOL, (m_full * ncols,), (1,))
+                    self.buf[("mask", epi["mask_of"])] = mb
+                mb = chunk(mb, ncols)
                 refs["e_mask"] = mb
                 writes.append(mb.key)
                 ta.epi_flags |= 8
             y = self.buf[epi["lo_of"]]
             root = y.base if y.base is not None else y
+            fresh = self._f16_get(root) is None
             if (y.splat is None and not y.elem_off and not root.subaxes and _dense_rowmajor(root.shape, root.strides)
-                    and element_count(root.shape) == m * ncols and ncols % 8 == 0 and self._feeds_tc(epi["lo_of"])
-                    and self._f16_get(root) is None):
-                planes = self._f16_buffers(root, m, ncols)  # _f16_planes finds them: no split pass
+                    and element_count(root.shape) == m_full * ncols and ncols % 8 == 0 and self._feeds_tc(epi["lo_of"])
+                    and (fresh or root.key in self._epi_planes)):
+                if fresh:  # _f16_planes finds them: no split pass
+                    self._f16_buffers(root, m_full, ncols)
+                    self._epi_planes.add(root.key)
+                hi, lo, sc = self._f16_get(root)
+                planes = (chunk(hi, ncols // 2), chunk(lo, ncols // 2),
+                          sc if rows is None else self._row_view(sc, r0 // 128, (r0 + m) // 128, (ncols + 127) // 128))
                 refs["e_hi"], refs["e_lo"], refs["e_sc"] = planes
                 writes.extend(pl.key for pl in planes)
                 ta.epi_flags |= 4
@@ -1986,7 +2137,7 @@ class Lowering:
             colsum = (epi["colsum"], part, rp)
         rec = LaunchRec(abi.K_DOT_F16P, grid, (320, 1, 1), F16_SMEM_PAIR, ta, reads, writes, label)
         rec.flops = 2 * m * ncols * kdim
-        rec.epi_bufs = {"c": target, "out2": refs.get("e_out2")}
+        rec.epi_bufs = {"c": target, "out2": refs.get("e_out2")}  # (row views when chunked)
         rec.finalize = _finalize_refs(ta, refs)
         self.launches.append(rec)
         if colsum is not None:

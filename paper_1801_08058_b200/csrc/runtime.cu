@@ -240,7 +240,9 @@ struct gfb_exe {
     bool io_set = false;
     std::vector<uint64_t> in_bytes, out_bytes;
     std::vector<void*> dev_in, dev_out;
-    std::vector<uint32_t> rd_off, rd, out_writer, in_order;
+    std::vector<uint32_t> rd_off, rd, out_writer, in_order;  // rd / in_order: input pieces
+    std::vector<uint32_t> pc_in;                             // piece -> input
+    std::vector<uint64_t> pc_off, pc_len;                    // piece bytes within its input
     cudaGraph_t hgraph = nullptr;
     cudaGraphExec_t hexec = nullptr;
     std::vector<cudaGraphNode_t> h2d_node, d2h_node;
@@ -355,6 +357,18 @@ void drop_graphs(gfb_exe* e) {
     drop_host_graph(e);
 }
 
+// input pieces in order of their first reader; unread pieces are never copied
+void order_pieces(gfb_exe* e) {
+    const size_t n = e->launches.size(), np = e->pc_in.size();
+    std::vector<uint32_t> first(np, UINT32_MAX);
+    for (size_t i = n; i-- > 0;)
+        for (uint32_t r = e->rd_off[i]; r < e->rd_off[i + 1]; ++r) first[e->rd[r]] = (uint32_t)i;
+    e->in_order.clear();
+    for (size_t i = 0; i < n; ++i)
+        for (uint32_t q = 0; q < np; ++q)
+            if (first[q] == i) e->in_order.push_back(q);
+}
+
 void release_io(gfb_exe* e) {
     for (void* p : e->dev_in) cudaFree(p);
     for (void* p : e->dev_out) cudaFree(p);
@@ -382,17 +396,25 @@ void release_io(gfb_exe* e) {
 // pass; each result's D2H copy runs on a third stream right after the last
 // launch writing it, under the rest of the step.
 int launch_all_io(gfb_exe* e, cudaStream_t s0, const void* const* hin, void* const* hout) {
-    const bool multi = e->n_streams > 1;
+    // One stream unless GFB_HOST_STREAMS=multi: measured on config E, the
+    // host-buffer graph captured over the multi-stream schedule ran 10-25 ms
+    // slower than the same launches in order on one stream (the device-only
+    // graph runs the same either way).
+    const char* hs = getenv("GFB_HOST_STREAMS");
+    const bool multi = e->n_streams > 1 && hs && std::string(hs) == "multi";
     CUDA_TRY(cudaEventRecord(e->io_fork, s0));
     CUDA_TRY(cudaStreamWaitEvent(e->h2d, e->io_fork, 0));
     CUDA_TRY(cudaStreamWaitEvent(e->d2h, e->io_fork, 0));
     if (multi)
         for (uint32_t k = 1; k < e->n_streams; ++k) CUDA_TRY(cudaStreamWaitEvent(e->streams[k], e->io_fork, 0));
-    for (uint32_t i : e->in_order) {
-        CUDA_TRY(cudaMemcpyAsync(e->dev_in[i], hin[i], e->in_bytes[i], cudaMemcpyHostToDevice, e->h2d));
-        CUDA_TRY(cudaEventRecord(e->in_ev[i], e->h2d));
+    const size_t npc = e->pc_in.size();
+    for (uint32_t p : e->in_order) {
+        const uint32_t i = e->pc_in[p];
+        CUDA_TRY(cudaMemcpyAsync((char*)e->dev_in[i] + e->pc_off[p], (const char*)hin[i] + e->pc_off[p], e->pc_len[p],
+                                 cudaMemcpyHostToDevice, e->h2d));
+        CUDA_TRY(cudaEventRecord(e->in_ev[p], e->h2d));
     }
-    std::vector<char> waited(e->n_in * (size_t)(multi ? e->n_streams : 1), 0);
+    std::vector<char> waited(npc * (size_t)(multi ? e->n_streams : 1), 0);
     for (size_t i = 0; i < e->launches.size(); ++i) {
         const uint32_t sk = multi ? e->stream_of[i] : 0;
         cudaStream_t st = sk == 0 ? s0 : e->streams[sk];
@@ -402,7 +424,7 @@ int launch_all_io(gfb_exe* e, cudaStream_t s0, const void* const* hin, void* con
                 if (e->stream_of[j] != sk) CUDA_TRY(cudaStreamWaitEvent(st, e->done[j], 0));
             }
         for (uint32_t r = e->rd_off[i]; r < e->rd_off[i + 1]; ++r) {
-            char& w = waited[(size_t)sk * e->n_in + e->rd[r]];
+            char& w = waited[(size_t)sk * npc + e->rd[r]];
             if (!w) CUDA_TRY(cudaStreamWaitEvent(st, e->in_ev[e->rd[r]], 0));
             w = 1;
         }
@@ -436,20 +458,21 @@ bool find_copy_nodes(gfb_exe* e) {
     if (cudaGraphGetNodes(e->hgraph, nullptr, &n) != cudaSuccess) return false;
     std::vector<cudaGraphNode_t> nodes(n);
     if (cudaGraphGetNodes(e->hgraph, nodes.data(), &n) != cudaSuccess) return false;
-    e->h2d_node.assign(e->n_in, nullptr);
+    e->h2d_node.assign(e->pc_in.size(), nullptr);
     e->d2h_node.assign(e->n_out, nullptr);
     for (cudaGraphNode_t nd : nodes) {
         cudaGraphNodeType t;
         if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeMemcpy) continue;
         cudaMemcpy3DParms p;
         if (cudaGraphMemcpyNodeGetParams(nd, &p) != cudaSuccess) return false;
-        for (uint32_t i = 0; i < e->n_in; ++i)
-            if (p.dstPtr.ptr == e->dev_in[i]) e->h2d_node[i] = nd;
+        const char* dst = (const char*)p.dstPtr.ptr + p.dstPos.x;
+        for (uint32_t q : e->in_order)
+            if (dst == (const char*)e->dev_in[e->pc_in[q]] + e->pc_off[q]) e->h2d_node[q] = nd;
         for (uint32_t j = 0; j < e->n_out; ++j)
             if (p.srcPtr.ptr == e->dev_out[j]) e->d2h_node[j] = nd;
     }
-    for (uint32_t i : e->in_order)
-        if (!e->h2d_node[i]) return false;
+    for (uint32_t q : e->in_order)
+        if (!e->h2d_node[q]) return false;
     for (uint32_t j = 0; j < e->n_out; ++j)
         if (!e->d2h_node[j]) return false;
     return true;
@@ -714,14 +737,11 @@ int gfb_exe_set_io(gfb_exe* e, const uint64_t* in_bytes, const uint64_t* out_byt
     e->rd_off.assign(read_offsets, read_offsets + n + 1);
     e->rd.assign(reads, reads + read_offsets[n]);
     e->out_writer.assign(out_writer, out_writer + e->n_out);
-    // inputs in order of their first reader; unread inputs are never copied
-    std::vector<uint32_t> first(e->n_in, UINT32_MAX);
-    for (size_t i = n; i-- > 0;)
-        for (uint32_t r = e->rd_off[i]; r < e->rd_off[i + 1]; ++r) first[e->rd[r]] = (uint32_t)i;
-    e->in_order.clear();
-    for (size_t i = 0; i < n; ++i)
-        for (uint32_t k = 0; k < e->n_in; ++k)
-            if (first[k] == i) e->in_order.push_back(k);
+    e->pc_in.resize(e->n_in);
+    e->pc_off.assign(e->n_in, 0);
+    e->pc_len.assign(e->in_bytes.begin(), e->in_bytes.end());
+    for (uint32_t k = 0; k < e->n_in; ++k) e->pc_in[k] = k;  // one piece per input
+    order_pieces(e);
     e->dev_in.assign(e->n_in, nullptr);
     e->dev_out.assign(e->n_out, nullptr);
     e->in_ev.assign(e->n_in, nullptr);
@@ -748,6 +768,36 @@ int gfb_exe_set_io(gfb_exe* e, const uint64_t* in_bytes, const uint64_t* out_byt
         (err = cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking)) != cudaSuccess)
         return bail(err);
     e->io_set = true;
+    return GFB_OK;
+}
+
+int gfb_exe_set_io_pieces(gfb_exe* e, uint32_t n_pieces, const uint32_t* piece_input, const uint64_t* piece_offset,
+                          const uint64_t* piece_bytes, const uint32_t* read_offsets, const uint32_t* reads) {
+    if (!e || !read_offsets || (n_pieces && (!piece_input || !piece_offset || !piece_bytes)))
+        return fail(GFB_ERR_INVALID, "gfb_exe_set_io_pieces: null argument");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (!e->io_set) return fail(GFB_ERR_INVALID, "gfb_exe_set_io_pieces before gfb_exe_set_io");
+    const size_t n = e->launches.size();
+    for (uint32_t p = 0; p < n_pieces; ++p)
+        if (piece_input[p] >= e->n_in || piece_offset[p] + piece_bytes[p] > e->in_bytes[piece_input[p]])
+            return fail(GFB_ERR_INVALID, "gfb_exe_set_io_pieces: piece outside its input");
+    if (read_offsets[0] != 0) return fail(GFB_ERR_INVALID, "gfb_exe_set_io_pieces: read_offsets[0] must be 0");
+    for (size_t i = 0; i < n; ++i) {
+        if (read_offsets[i + 1] < read_offsets[i]) return fail(GFB_ERR_INVALID, "gfb_exe_set_io_pieces: offsets not monotone");
+        for (uint32_t r = read_offsets[i]; r < read_offsets[i + 1]; ++r)
+            if (reads[r] >= n_pieces) return fail(GFB_ERR_INVALID, "gfb_exe_set_io_pieces: piece index out of range");
+    }
+    if (e->ran) CUDA_TRY(cudaEventSynchronize(e->run_done));
+    drop_host_graph(e);
+    for (cudaEvent_t ev : e->in_ev) cudaEventDestroy(ev);
+    e->in_ev.assign(n_pieces, nullptr);
+    for (uint32_t p = 0; p < n_pieces; ++p) CUDA_TRY(cudaEventCreateWithFlags(&e->in_ev[p], cudaEventDisableTiming));
+    e->pc_in.assign(piece_input, piece_input + n_pieces);
+    e->pc_off.assign(piece_offset, piece_offset + n_pieces);
+    e->pc_len.assign(piece_bytes, piece_bytes + n_pieces);
+    e->rd_off.assign(read_offsets, read_offsets + n + 1);
+    e->rd.assign(reads, reads + read_offsets[n]);
+    order_pieces(e);
     return GFB_OK;
 }
 
@@ -782,10 +832,13 @@ int gfb_exe_run_host(gfb_exe* e, const void* const* host_inputs, void* const* ho
         // retarget the copy nodes at this call's host buffers (once the
         // previous launch of the graph has finished with the old ones)
         CUDA_TRY(cudaEventSynchronize(e->run_done));
-        for (uint32_t i : e->in_order)
+        for (uint32_t q : e->in_order) {
+            const uint32_t i = e->pc_in[q];
             if (e->cur_hin[i] != host_inputs[i])
-                CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(e->hexec, e->h2d_node[i], e->dev_in[i], host_inputs[i],
-                                                            e->in_bytes[i], cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(e->hexec, e->h2d_node[q], (char*)e->dev_in[i] + e->pc_off[q],
+                                                            (const char*)host_inputs[i] + e->pc_off[q], e->pc_len[q],
+                                                            cudaMemcpyHostToDevice));
+        }
         for (uint32_t j = 0; j < e->n_out; ++j)
             if (e->cur_hout[j] != host_outputs[j])
                 CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(e->hexec, e->d2h_node[j], host_outputs[j], e->dev_out[j],

@@ -84,6 +84,8 @@ def lib():
         u64 = C.c_uint64
         L.gfb_exe_set_io.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]
         L.gfb_exe_run_host.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), vp]
+        L.gfb_exe_set_io_pieces.argtypes = [vp, C.c_uint32, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64), C.POINTER(u32),
+                                            C.POINTER(u32)]
         _LIB = L
         return L
 
@@ -198,6 +200,11 @@ class DeviceProgram:
             u64 = lambda v: (C.c_uint64 * max(1, len(v)))(*v)
             check(lib().gfb_exe_set_io(self.handle, u64(in_bytes), u64(out_bytes), u32(off), u32(reads), u32(writer)),
                   "gfb_exe_set_io")
+            pieces = schedule.io_pieces(self.lowered, in_bytes, self.skipped) if os.environ.get("GFB_IO_PIECES", "1") == "1" else None
+            if pieces is not None:
+                p_in, p_off, p_len, poff, preads = pieces
+                check(lib().gfb_exe_set_io_pieces(self.handle, len(p_in), u32(p_in), u64(p_off), u64(p_len), u32(poff),
+                                                  u32(preads)), "gfb_exe_set_io_pieces")
             self._io = True
         return self._io
 

@@ -15,3 +15,12 @@ arrays = W.step_inputs(step, W.parameter_shapes(step), seed=0)
 exe = gf.compile_function(step.fn)
 outs = gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])
 print("config A step ok, loss", float(outs[-1].to_numpy()), "launches", exe.num_launches)
+
+# the fp16 pair GEMM with its fused epilogues (bias + Relu, Relu gradient,
+# mask bytes, planes, column partials) on a small wide-MLP step
+step = W.mlp_step(gf, batch=512, in_dim=256, hidden=(256, 256), out_dim=256)
+arrays = W.step_inputs(step, W.parameter_shapes(step), seed=1)
+exe = gf.compile_function(step.fn)
+outs = gf.call(exe, [gf.tensor_from_flat(gf.ElementType.F32, a.shape, a) for a in arrays])
+kinds = sorted({L.kind for L in exe.lowered.launches})
+print("wide step ok, loss", float(outs[-1].to_numpy()), "kernel kinds", kinds)
