@@ -90,6 +90,12 @@ enum {
     GFB_K_DOT_F16P = 34,  /* 2xFP16 block-scaled Dot on a 2-SM CTA pair (kind::f16, 256x256 tiles; gfb_tc_args
                              with the fp16 plane fields): the fp32 accuracy of the 3xTF32 kernel at the f16 rate */
     GFB_K_SPLIT_F16 = 35, /* F32 -> fp16 hi / lo planes + per-128x128-tile power-of-two scales (gfb_split16_args) */
+    GFB_K_CHMAX = 36,     /* per-block channel maxima of a channel-last activation (gfb_chsplit_args) */
+    GFB_K_CHSPLIT = 37,   /* channel-scaled fp16 hi / lo planes of a channel-last activation (gfb_chsplit_args) */
+    GFB_K_FSPLIT = 38,    /* filter -> fp16 hi / lo K-major planes divided by the activation's channel scales,
+                             row-scaled (gfb_fsplit_args) */
+    GFB_K_CONV_TCXH64 = 39,  /* 2xFP16 implicit-GEMM conv on TMA boxes of fp16 activation planes, 128x64 (gfb_tcxh_args) */
+    GFB_K_CONV_TCXH128 = 40, /* as GFB_K_CONV_TCXH64 with 128x128 tiles */
     GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
                              always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
                              entry only traps */
@@ -286,6 +292,50 @@ typedef struct GFB_ALIGN64 {
     int64_t pad[1];
     uint64_t tmap[4][16];
 } gfb_tc_args;
+
+/* Channel-scaled fp16 planes of a dense channel-last activation [P pixels, C]
+ * (C a power of two, 8 <= C <= 1024): GFB_K_CHMAX writes partial[b * C + c] =
+ * max |x[p, c]| over block b's pixel rows (gridDim.x == nblocks);
+ * GFB_K_CHSPLIT with mode 1 reduces the partials to sc[c] = 2^(14 -
+ * floor(log2 max_c)) (one block per 32 channels), with mode 0 writes
+ * hi = fp16_rn(x sc[c]), lo = fp16_rn(x sc[c] - hi), planes [P, C]. */
+typedef struct {
+    const void* const* tab;
+    uint64_t src, partial, sc, hi, lo; /* GFB_REF */
+    int64_t P, C;
+    int32_t nblocks, mode;
+} gfb_chsplit_args;
+
+/* Filter planes for a channel-scaled activation: B[row, k] with k = (d0, d1,
+ * d2) over extents (e0, e1, e2) reads w[row * s_r + d0 t0 + d1 t1 + d2 t2]
+ * (d2 = the activation channel); b = w / sc[d2] (exact), t_row = the power of
+ * two bringing max_k |b| into [2^14, 2^15); hi / lo = fp16 planes of b t_row,
+ * K-major [rows, K]; inv[row] = 1 / t_row.  One block per row. */
+typedef struct {
+    const void* const* tab;
+    uint64_t w, sc, hi, lo, inv; /* GFB_REF */
+    int64_t rows, K, s_r;
+    int64_t e0, e1, e2, t0, t1, t2;
+} gfb_fsplit_args;
+
+/* 2xFP16 implicit-GEMM convolution on TMA boxes of the activation's
+ * channel-scaled fp16 planes (gfb_chsplit_args): the layout and tile walk of
+ * gfb_tcx_args with K-blocks of 64 channels (C = 64 CB) and two activation
+ * maps (hi, lo); the channel scales cancel against the filter planes
+ * (gfb_fsplit_args), so C[p, n] = inv[n] * sum_k (Ahi Bhi + Ahi Blo + Alo Bhi),
+ * promoted every 128 K into round-to-nearest fp32 registers. */
+typedef struct GFB_ALIGN64 {
+    const void* const* tab;
+    uint64_t c, a_hi, a_lo, b_hi, b_lo, b_inv;
+    int64_t N, K;
+    int64_t o_n, o_y, o_x, c_sn;
+    int64_t a_dims[4];    /* C, W, H, N of the planes (innermost first) */
+    int64_t a_strides[4]; /* their element strides */
+    int32_t No, Yo, Xo, BX, BY, BNI, tiles_x, tiles_y;
+    int32_t sx, sy, ox, oy, S, CB, ksign, pad0;
+    int64_t pad[3];
+    uint64_t tmap[4][16];
+} gfb_tcxh_args;
 
 /* fp16 split of a dense F32 matrix [rows, cols] (row pitch ld elements, cols % 8 == 0):
  * per 128 x 128 tile, s = 2^(14 - floor(log2(max |x|))) (1 for an all-zero tile),

@@ -17,6 +17,7 @@ K_DOT_F32, K_DOT_F64, K_DOT_TC32, K_SPLIT_TF32, K_DOT_TC32W = 10, 11, 12, 13, 14
 K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
 K_DOT_TC32P = 19
 K_DOT_F16P, K_SPLIT_F16 = 34, 35
+K_CHMAX, K_CHSPLIT, K_FSPLIT, K_CONV_TCXH64, K_CONV_TCXH128 = 36, 37, 38, 39, 40
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
@@ -92,6 +93,38 @@ class Split16Args(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p), ("src", C.c_uint64), ("hi", C.c_uint64), ("lo", C.c_uint64), ("sc", C.c_uint64),
         ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64),
+    ]
+
+
+class ChsplitArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("src", C.c_uint64), ("partial", C.c_uint64), ("sc", C.c_uint64), ("hi", C.c_uint64),
+        ("lo", C.c_uint64), ("P", C.c_int64), ("C", C.c_int64), ("nblocks", C.c_int32), ("mode", C.c_int32),
+    ]
+
+
+class FsplitArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("w", C.c_uint64), ("sc", C.c_uint64), ("hi", C.c_uint64), ("lo", C.c_uint64),
+        ("inv", C.c_uint64), ("rows", C.c_int64), ("K", C.c_int64), ("s_r", C.c_int64),
+        ("e0", C.c_int64), ("e1", C.c_int64), ("e2", C.c_int64), ("t0", C.c_int64), ("t1", C.c_int64), ("t2", C.c_int64),
+    ]
+
+
+class TcxhArgs(C.Structure):
+    # 64-byte aligned in C: tmap sits at offset 256, size 768.
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64), ("a_hi", C.c_uint64), ("a_lo", C.c_uint64), ("b_hi", C.c_uint64),
+        ("b_lo", C.c_uint64), ("b_inv", C.c_uint64),
+        ("N", C.c_int64), ("K", C.c_int64),
+        ("o_n", C.c_int64), ("o_y", C.c_int64), ("o_x", C.c_int64), ("c_sn", C.c_int64),
+        ("a_dims", C.c_int64 * 4), ("a_strides", C.c_int64 * 4),
+        ("No", C.c_int32), ("Yo", C.c_int32), ("Xo", C.c_int32), ("BX", C.c_int32), ("BY", C.c_int32),
+        ("BNI", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+        ("sx", C.c_int32), ("sy", C.c_int32), ("ox", C.c_int32), ("oy", C.c_int32), ("S", C.c_int32),
+        ("CB", C.c_int32), ("ksign", C.c_int32), ("pad0", C.c_int32),
+        ("pad", C.c_int64 * 3),
+        ("tmap", (C.c_uint64 * 16) * 4),
     ]
 
 
@@ -222,5 +255,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

@@ -154,6 +154,8 @@ F16_SMEM_PAIR = TC_SMEM_PAIR  # gemm_f16.cu HCfg::SMEM_BYTES: same 64 KB stages 
 # gfb_conv_tcg_kernel: MMA stages + 4 raw A K-blocks + row table + barriers (gemm_tc.cu GCfg)
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
+TCXH_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 64 * 2 + 256 + 1024 for bn in (64, 128)}  # conv_f16.cu HXCfg
+CHMAX_BLOCKS = 296
 STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
 STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
 TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
@@ -2402,6 +2404,89 @@ class Lowering:
         return (os.environ.get("GFB_CONV_TMA", "1") == "1" and xb.slot == abi.SLOT_ARENA
                 and sx <= 2 and sy <= 2 and max(shape) < 2 ** 31)
 
+    @staticmethod
+    def _tcxh_ok(xb, xs, shape, sx, sy) -> bool:
+        """2xFP16 TMA-box convolution (conv_f16.cu): a dense channel-last
+        activation with a power-of-two channel count, 64 <= C <= 1024."""
+        N_, C_, H_, W_ = shape
+        return (use_f16() and os.environ.get("GFB_CONV_F16", "1") == "1" and xb.splat is None and xb.elem_off == 0
+                and C_ >= 64 and C_ <= 1024 and C_ & (C_ - 1) == 0 and tuple(xs) == (H_ * W_ * C_, 1, W_ * C_, C_)
+                and sx <= 2 and sy <= 2 and N_ * H_ * W_ * C_ < 2 ** 31)
+
+    def _ch_planes(self, xb, P, C):
+        """Channel-scaled fp16 planes of a dense channel-last activation
+        [P, C] (gfb_chmax_kernel + gfb_chsplit_kernel), shared by every
+        convolution that reads it."""
+        root = xb.base if xb.base is not None else xb
+        key = ("ch16", root.key)
+        got = self.buf.get(key + ("hi",))
+        if got is not None:
+            return got, self.buf[key + ("lo",)], self.buf[key + ("sc",)]
+        part = Buffer(self.new_key(), ElementType.F32, (CHMAX_BLOCKS * C,), (1,))
+        sc = Buffer(self.new_key(), ElementType.F32, (C,), (1,))
+        hi = Buffer(self.new_key(), ElementType.F32, ((P * C + 1) // 2,), (1,))
+        lo = Buffer(self.new_key(), ElementType.F32, ((P * C + 1) // 2,), (1,))
+        for p_, b_ in (("part", part), ("sc", sc), ("hi", hi), ("lo", lo)):
+            self.buf[key + (p_,)] = b_
+        a1 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS)
+        r1 = LaunchRec(abi.K_CHMAX, (CHMAX_BLOCKS, 1, 1), (256, 1, 1), 0, a1, [xb.key], [part.key], f"chmax#{root.key}")
+        r1.algo_bytes = P * C * 4
+        r1.finalize = _finalize_refs(a1, {"src": xb, "partial": part})
+        self.launches.append(r1)
+        a2 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS, mode=1)
+        r2 = LaunchRec(abi.K_CHSPLIT, ((C + 31) // 32, 1, 1), (256, 1, 1), 0, a2, [part.key], [sc.key], f"chscale#{root.key}")
+        r2.algo_bytes = CHMAX_BLOCKS * C * 4
+        r2.finalize = _finalize_refs(a2, {"src": xb, "partial": part, "sc": sc, "hi": hi, "lo": lo})
+        self.launches.append(r2)
+        a3 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS, mode=0)
+        grid = max(1, min(NUM_SMS * 4, (P * (C // 4) + 255) // 256))
+        r3 = LaunchRec(abi.K_CHSPLIT, (grid, 1, 1), (256, 1, 1), 0, a3, [xb.key, sc.key], [hi.key, lo.key], f"chsplit#{root.key}")
+        r3.algo_bytes = P * C * 8
+        r3.finalize = _finalize_refs(a3, {"src": xb, "partial": part, "sc": sc, "hi": hi, "lo": lo})
+        self.launches.append(r3)
+        return hi, lo, sc
+
+    def _conv_tcxh(self, n, xb, xshape, wb, wgeo, out, oshape, ncols, kdim, geo, label):
+        """Conv2D / ConvBackpropData on conv_f16.cu gfb_conv_tcxh_kernel: the
+        activation's channel-scaled fp16 planes by TMA pixel boxes, filter
+        planes divided by the same channel scales (rows scaled on their own,
+        undone in the epilogue).  wgeo = (row stride, e0, e1, e2, t0, t1, t2)
+        of the filter gather, e2 / t2 along the activation's channels."""
+        N_, C_, H_, W_ = xshape
+        ahi, alo, sc = self._ch_planes(xb, N_ * H_ * W_, C_)
+        s_r, e0, e1, e2, t0, t1, t2 = wgeo
+        bhi = Buffer(self.new_key(), ElementType.F32, ((ncols * kdim + 1) // 2,), (1,))
+        blo = Buffer(self.new_key(), ElementType.F32, ((ncols * kdim + 1) // 2,), (1,))
+        binv = Buffer(self.new_key(), ElementType.F32, (ncols,), (1,))
+        for p_, b_ in (("hi", bhi), ("lo", blo), ("inv", binv)):
+            self.buf[("fsplit", n, p_)] = b_
+        fa = abi.FsplitArgs(rows=ncols, K=kdim, s_r=s_r, e0=e0, e1=e1, e2=e2, t0=t0, t1=t1, t2=t2)
+        fr = LaunchRec(abi.K_FSPLIT, (ncols, 1, 1), (256, 1, 1), 0, fa, [wb.key, sc.key], [bhi.key, blo.key, binv.key],
+                       f"fsplit#{n}")
+        fr.algo_bytes = ncols * kdim * 8
+        fr.finalize = _finalize_refs(fa, {"w": wb, "sc": sc, "hi": bhi, "lo": blo, "inv": binv})
+        self.launches.append(fr)
+        No, Yo, Xo = oshape
+        BX = min(128, 1 << max(0, (Xo - 1).bit_length()))
+        BY = min(128 // BX, 1 << max(0, (Yo - 1).bit_length()))
+        BNI = 128 // (BX * BY)
+        tiles_x, tiles_y = (Xo + BX - 1) // BX, (Yo + BY - 1) // BY
+        tiles = tiles_x * tiles_y * ((No + BNI - 1) // BNI)
+        os_ = out.strides
+        ta = abi.TcxhArgs(N=ncols, K=kdim, o_n=os_[0], o_y=os_[2], o_x=os_[3], c_sn=os_[1], No=No, Yo=Yo, Xo=Xo,
+                          BX=BX, BY=BY, BNI=BNI, tiles_x=tiles_x, tiles_y=tiles_y, **geo)
+        ta.a_dims[:] = [C_, W_, H_, N_]
+        ta.a_strides[:] = [1, C_, W_ * C_, H_ * W_ * C_]
+        bn = 64 if ncols <= 64 else 128
+        kind = abi.K_CONV_TCXH64 if bn == 64 else abi.K_CONV_TCXH128
+        grid = (max(1, min(tiles * ((ncols + bn - 1) // bn), NUM_SMS)), 1, 1)
+        rec = LaunchRec(kind, grid, (192, 1, 1), TCXH_SMEM[bn], ta, [ahi.key, alo.key, bhi.key, blo.key, binv.key],
+                        [out.key], label)
+        rec.flops = 2 * No * Yo * Xo * ncols * kdim
+        rec.algo_bytes = xb.nbytes + wb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": out, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo, "b_inv": binv})
+        self.launches.append(rec)
+
     def _conv_tcx(self, n, xb, xs, xshape, b, out, oshape, ncols, kdim, geo, yb, label):
         """Conv2D / ConvBackpropData whose A tiles are TMA boxes of output
         pixels (gemm_tc.cu, gfb_conv_tcx_kernel)."""
@@ -2552,6 +2637,11 @@ class Lowering:
                 yb, ys = self._pad_channels(yb, ys, (K, Cc, R, S), cp)
                 Cc, kdim = cp, cp * R * S
             if self._gather_ok(xb, xs, Cc, m):
+                if self._tcxh_ok(xb, xs, (N, Cc, H, W), sw, sh):
+                    self._conv_tcxh(n, xb, (N, Cc, H, W), yb, (ys[0], R, S, Cc, ys[2], ys[3], ys[1]), out, (N, Ho, Wo),
+                                    ncols, kdim, dict(sx=sw, sy=sh, ox=-pl, oy=-pt, S=S, CB=Cc // 64, ksign=1),
+                                    f"{node.op.wire_name}_tcxh#{n}")
+                    return True
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[0], geo=(0,) * 12 + (R, S, Cc), st=(ys[2], ys[3], ys[1]))
                 if Cc % 32 == 0 and self._tma_box_ok(xb, (N, Cc, H, W), sw, sh):
                     self._conv_tcx(n, xb, xs, (N, Cc, H, W), b, out, (N, Ho, Wo), ncols, kdim,
@@ -2581,6 +2671,11 @@ class Lowering:
             if os_[2] != W * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
             if self._gather_ok(xb, xs, K, m):
+                if self._tcxh_ok(xb, xs, (N, K, Ho, Wo), 1, 1):
+                    self._conv_tcxh(n, xb, (N, K, Ho, Wo), yb, (ys[1], R, S, K, ys[2], ys[3], ys[0]), out, (N, H, W),
+                                    ncols, kdim, dict(sx=1, sy=1, ox=pl, oy=pt, S=S, CB=K // 64, ksign=-1),
+                                    f"{node.op.wire_name}_tcxh#{n}")
+                    return True
                 b = self._split(n, "b", yb, ncols, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (R, S, K), st=(ys[2], ys[3], ys[0]))
                 if K % 32 == 0 and self._tma_box_ok(xb, (N, K, Ho, Wo), 1, 1):
                     self._conv_tcx(n, xb, xs, (N, K, Ho, Wo), b, out, (N, H, W), ncols, kdim,

@@ -66,20 +66,6 @@ __device__ __forceinline__ HTile f16_tile(const gfb_tc_args& p, int t, int ntm, 
     return o;
 }
 
-__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
-    const __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<const uint32_t*>(&h);
-}
-// hi / lo fp16 pieces of four values already multiplied by their scale
-__device__ __forceinline__ void split4_f16(float4 v, uint2& hi, uint2& lo) {
-    const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
-    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-    hi = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
-    lo = make_uint2(pack_h2(__fsub_rn(v.x, f01.x), __fsub_rn(v.y, f01.y)), pack_h2(__fsub_rn(v.z, f23.x), __fsub_rn(v.w, f23.y)));
-}
-__device__ __forceinline__ float4 scale4(float4 v, float s) {
-    return make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
-}
 // Relu-gradient mask bytes (gfb_tc_args.e_mask): the value of
 // Maximum(Divide(Relu(x), x), 0) -- 1 for 0 < x < inf, -0 for x < 0, +0
 // otherwise -- as 1, 2, 0 (relu_grad_mask in tc_prims.cuh).
@@ -87,30 +73,6 @@ __device__ __forceinline__ uint32_t mask_code(float x) { return (x > 0.f && x < 
 __device__ __forceinline__ float mask_value(uint32_t code) {
     code &= 0xffu;
     return code == 1u ? 1.f : (code == 2u ? -0.f : 0.f);
-}
-// 16 TMEM columns of this warp's 32 lanes (one per thread), fp32
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
-          "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
-        : "memory");
-}
-__device__ __forceinline__ float amax4(float m, float4 v) {
-    return fmaxf(fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
 }
 }  // namespace tc
 

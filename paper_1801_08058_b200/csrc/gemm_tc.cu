@@ -735,25 +735,6 @@ struct XCfg {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
 };
 
-__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-            su32(dst)),
-        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
-        : "memory");
-}
-
-// Output rows of a pixel-box tile.
-struct BoxRows {
-    int n0, y0, x0, BX, BY, No, Yo, Xo;
-    int64_t o_n, o_y, o_x;
-    __device__ __forceinline__ int64_t operator()(int r) const {
-        const int xx = r % BX, t = r / BX, yy = t % BY, ni = t / BY;
-        const int n = n0 + ni, y = y0 + yy, x = x0 + xx;
-        if (n >= No || y >= Yo || x >= Xo) return -1;
-        return n * o_n + y * o_y + x * o_x;
-    }
-};
 }  // namespace tc
 
 template <int BN_>

@@ -25,6 +25,7 @@ extern "C" const void* gfb_ew_kernel_ptr(int kind);
 extern "C" const void* gfb_simt_kernel_ptr(int kind);
 extern "C" const void* gfb_tc_kernel_ptr(int kind);
 extern "C" const void* gfb_f16_kernel_ptr(int kind);
+extern "C" const void* gfb_conv_f16_kernel_ptr(int kind);
 
 namespace {
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -84,13 +85,13 @@ bool encode_mn_map(void* gaddr, int64_t mn, int64_t k, int64_t ld, void* out) {
 // k * ld + mn, mn % 64 == 0): 3-D view (64 MN, K, MN / 64) with (64, 64, 2)
 // boxes, i.e. two 8 KB chunks of 64 K rows x 128 B in the canonical
 // SWIZZLE_128B MN-major layout.
-bool encode_plane16_map(void* gaddr, int64_t rows, int64_t kp, void* out) {
+bool encode_plane16_map(void* gaddr, int64_t rows, int64_t kp, void* out, uint32_t box_rows = 128) {
     EncodeTiledFn fn = encode_fn();
     if (!fn || kp % 8) return false;
     alignas(64) CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, gaddr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -107,6 +108,23 @@ bool encode_mn16_map(void* gaddr, int64_t mn, int64_t k, int64_t ld, void* out) 
     cuuint32_t box[3] = {64, 64, 2};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, gaddr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out, &map, sizeof(map));
+    return true;
+}
+// Channel-last fp16 activation plane (C, W, H, N innermost first): boxes of
+// 64 channels (128 B rows) x bw x bh x bn, traversal strides (1, sx, sy, 1).
+bool encode_act16_map(void* gaddr, const int64_t* dims, const int64_t* estrides, uint32_t bw, uint32_t bh, uint32_t bn,
+                      uint32_t sx, uint32_t sy, void* out) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    alignas(64) CUtensorMap map;
+    cuuint64_t d[4] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2], (cuuint64_t)dims[3]};
+    cuuint64_t st[3] = {(cuuint64_t)estrides[1] * 2, (cuuint64_t)estrides[2] * 2, (cuuint64_t)estrides[3] * 2};
+    cuuint32_t box[4] = {64, bw, bh, bn};
+    cuuint32_t es[4] = {1, sx, sy, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, gaddr, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     std::memcpy(out, &map, sizeof(map));
@@ -265,6 +283,7 @@ const void* kernel_for(uint32_t kind) {
         kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128 || kind == GFB_K_CONV_STEM64)
         return gfb_tc_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F16P || kind == GFB_K_SPLIT_F16) return gfb_f16_kernel_ptr((int)kind);
+    if (kind >= GFB_K_CHMAX && kind <= GFB_K_CONV_TCXH128) return gfb_conv_f16_kernel_ptr((int)kind);
     return nullptr;
 }
 
@@ -609,6 +628,23 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
                 const bool ok = ld_mn > 0 ? encode_mn16_map(addr, rows, a->K, ld_mn, a->tmap[t]) : encode_plane16_map(addr, rows, kp, a->tmap[t]);
                 if (!ok) return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 plane) failed"));
             }
+        }
+        if (L.kind == GFB_K_CONV_TCXH64 || L.kind == GFB_K_CONV_TCXH128) {
+            gfb_tcxh_args* a = (gfb_tcxh_args*)(e->args.data() + L.arg_offset);
+            const uint64_t refs[4] = {a->a_hi, a->a_lo, a->b_hi, a->b_lo};
+            void* addr[4];
+            for (int t = 0; t < 4; ++t) {
+                if ((refs[t] >> 56) != GFB_SLOT_ARENA)
+                    return bail(fail(GFB_ERR_INVALID, "TMA convolution operands must live in the arena"));
+                addr[t] = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
+            }
+            for (int t = 0; t < 2; ++t)
+                if (!encode_act16_map(addr[t], a->a_dims, a->a_strides, (uint32_t)(a->BX * a->sx), (uint32_t)(a->BY * a->sy),
+                                      (uint32_t)a->BNI, (uint32_t)a->sx, (uint32_t)a->sy, a->tmap[t]))
+                    return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 activation box) failed"));
+            for (int t = 2; t < 4; ++t)
+                if (!encode_plane16_map(addr[t], a->N, a->K, a->tmap[t], L.kind == GFB_K_CONV_TCXH64 ? 64 : 128))
+                    return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 filter plane) failed"));
         }
         if (L.kind == GFB_K_CONV_TCX64 || L.kind == GFB_K_CONV_TCX128) {
             gfb_tcx_args* a = (gfb_tcx_args*)(e->args.data() + L.arg_offset);

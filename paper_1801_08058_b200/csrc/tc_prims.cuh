@@ -2,6 +2,8 @@
 // UMMA descriptors, tcgen05.mma / commit (single CTA and CTA pair).
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include <cstdint>
 
 #include "gfb_common.cuh"
@@ -144,6 +146,26 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
                  : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
+        : "memory");
+}
+
+// Output rows of a pixel-box tile.
+struct BoxRows {
+    int n0, y0, x0, BX, BY, No, Yo, Xo;
+    int64_t o_n, o_y, o_x;
+    __device__ __forceinline__ int64_t operator()(int r) const {
+        const int xx = r % BX, t = r / BX, yy = t % BY, ni = t / BY;
+        const int n = n0 + ni, y = y0 + yy, x = x0 + xx;
+        if (n >= No || y >= Yo || x >= Xo) return -1;
+        return n * o_n + y * o_y + x * o_x;
+    }
+};
+
 // ---- kind::f16 (the 2xFP16 block-scaled GEMM, gemm_f16.cu) ----
 // Instruction descriptor: F16 A and B, F32 accumulate; bits 15 / 16 select
 // MN-major A / B.
@@ -183,6 +205,45 @@ __device__ __forceinline__ float f16_tile_scale(float mx) {
     int k = 15 - e;           // 14 - floor(log2 mx)
     k = k > 126 ? 126 : k;
     return ldexpf(1.f, k);
+}
+// fp16 hi / lo pieces
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// hi / lo fp16 pieces of four values already multiplied by their scale
+__device__ __forceinline__ void split4_f16(float4 v, uint2& hi, uint2& lo) {
+    const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
+    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+    hi = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+    lo = make_uint2(pack_h2(__fsub_rn(v.x, f01.x), __fsub_rn(v.y, f01.y)), pack_h2(__fsub_rn(v.z, f23.x), __fsub_rn(v.w, f23.y)));
+}
+__device__ __forceinline__ float4 scale4(float4 v, float s) {
+    return make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
+}
+__device__ __forceinline__ float amax4(float m, float4 v) {
+    return fmaxf(fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+// 16 TMEM columns of this warp's 32 lanes (one per thread), fp32
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+          "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
 }
 }  // namespace tc
 }  // namespace gfb

@@ -552,6 +552,77 @@ def run_tcx(mem, a):
     mem.view(a.c, np.float32)[n * a.o_n + y * a.o_y + x * a.o_x + j * a.c_sn] = out
 
 
+def _ch_scale_vec(m):
+    return np.array([_f16_scale(v) for v in m], dtype=np.float32)
+
+
+def run_chmax(mem, a):
+    x = mem.view(a.src, np.float32)[: a.P * a.C].reshape(a.P, a.C)
+    per = (a.P + a.nblocks - 1) // a.nblocks
+    part = mem.view(a.partial, np.float32)
+    for b in range(a.nblocks):
+        blk = np.abs(x[b * per:(b + 1) * per])
+        part[b * a.C:(b + 1) * a.C] = blk.max(axis=0) if blk.size else 0.0
+
+
+def run_chsplit(mem, a):
+    if a.mode == 1:
+        part = mem.view(a.partial, np.float32)[: a.nblocks * a.C].reshape(a.nblocks, a.C)
+        mem.view(a.sc, np.float32)[: a.C] = _ch_scale_vec(part.max(axis=0))
+        return
+    s = mem.view(a.sc, np.float32)[: a.C].copy()
+    x = mem.view(a.src, np.float32)[: a.P * a.C].reshape(a.P, a.C)
+    with np.errstate(all="ignore"):
+        v = (x * s[None, :]).astype(np.float32)
+        hi = v.astype(np.float16)
+        lo = (v - hi.astype(np.float32)).astype(np.float16)
+    mem.view(a.hi, np.float16)[: a.P * a.C] = hi.reshape(-1)
+    mem.view(a.lo, np.float16)[: a.P * a.C] = lo.reshape(-1)
+
+
+def run_fsplit(mem, a):
+    w = mem.view(a.w, np.float32)
+    sc = mem.view(a.sc, np.float32)
+    k = np.arange(a.K, dtype=np.int64)
+    d2, d01 = k % a.e2, k // a.e2
+    d1, d0 = d01 % a.e1, d01 // a.e1
+    rows = np.arange(a.rows, dtype=np.int64)[:, None]
+    b = (w[rows * a.s_r + (d0 * a.t0 + d1 * a.t1 + d2 * a.t2)[None, :]] / sc[d2][None, :]).astype(np.float32)
+    t = _ch_scale_vec(np.abs(b).max(axis=1))
+    v = (b * t[:, None]).astype(np.float32)
+    hi = v.astype(np.float16)
+    lo = (v - hi.astype(np.float32)).astype(np.float16)
+    mem.view(a.hi, np.float16)[: a.rows * a.K] = hi.reshape(-1)
+    mem.view(a.lo, np.float16)[: a.rows * a.K] = lo.reshape(-1)
+    mem.view(a.inv, np.float32)[: a.rows] = (1.0 / t).astype(np.float32)
+
+
+def run_tcxh(mem, a):
+    """gfb_conv_tcxh_kernel: the tcx gather over the fp16 activation planes
+    (64-channel K-blocks), products in float64, then times 1 / t_n."""
+    Cc, Wd, Hd, Nd = list(a.a_dims)
+    sc, sw, sh, sn = list(a.a_strides)
+    K = a.K
+    n, y, x = np.meshgrid(np.arange(a.No), np.arange(a.Yo), np.arange(a.Xo), indexing="ij")
+    n, y, x = (v.reshape(-1, 1).astype(np.int64) for v in (n, y, x))
+    k = np.arange(K, dtype=np.int64)[None, :]
+    C = 64 * a.CB
+    c, rs = k % C, k // C
+    h = y * a.sy + a.oy + a.ksign * (rs // a.S)
+    w = x * a.sx + a.ox + a.ksign * (rs % a.S)
+    ok = (h >= 0) & (h < Hd) & (w >= 0) & (w < Wd)
+    off = np.where(ok, n * sn + h * sh + w * sw + c * sc, 0)
+    ahi = np.where(ok, mem.view(a.a_hi, np.float16)[off].astype(np.float64), 0.0)
+    alo = np.where(ok, mem.view(a.a_lo, np.float16)[off].astype(np.float64), 0.0)
+    bhi = mem.view(a.b_hi, np.float16)[: a.N * K].reshape(a.N, K).astype(np.float64)
+    blo = mem.view(a.b_lo, np.float16)[: a.N * K].reshape(a.N, K).astype(np.float64)
+    out = (ahi @ bhi.T + ahi @ blo.T + alo @ bhi.T).astype(np.float32)
+    inv = mem.view(a.b_inv, np.float32)[: a.N]
+    out = (out * inv[None, :]).astype(np.float32)
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    mem.view(a.c, np.float32)[n * a.o_n + y * a.o_y + x * a.o_x + j * a.c_sn] = out
+
+
 def run_tcgg(mem, a):
     """gfb_conv_tcgg_kernel: generic row / K decompositions (gfb_tcgg_args)."""
     src = mem.view(a.a, np.float32)
@@ -655,6 +726,14 @@ def _run_launch(mem, L):
         run_split16(mem, L.args)
     elif L.kind == abi.K_DOT_F16P:
         run_f16p(mem, L.args)
+    elif L.kind == abi.K_CHMAX:
+        run_chmax(mem, L.args)
+    elif L.kind == abi.K_CHSPLIT:
+        run_chsplit(mem, L.args)
+    elif L.kind == abi.K_FSPLIT:
+        run_fsplit(mem, L.args)
+    elif L.kind in (abi.K_CONV_TCXH64, abi.K_CONV_TCXH128):
+        run_tcxh(mem, L.args)
     elif L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128):
         run_tcg(mem, L.args)
     elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):

@@ -139,6 +139,7 @@ def test_conv_fused_gather_matches_oracle(monkeypatch, op, shape, stride, pad):
     from paper_1801_08058_b200 import abi
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_CONV_F16", "0")
     monkeypatch.setenv("GFB_PAD_CHANNELS_FWD", "1")
     monkeypatch.setenv("GFB_CONV_STEM", "0")
     N, C, Ko, H, W, R, S = shape
@@ -169,6 +170,7 @@ def test_conv_tma_box_matches_oracle(monkeypatch, op, shape, stride, pad):
     from paper_1801_08058_b200 import abi
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_CONV_F16", "0")
     Ko = gf.OpKind
     N, C, K, H, W, R, S = shape
     fn = gf.Function("conv")
@@ -385,3 +387,31 @@ def test_f16_epilogue_planes_bit_identical(monkeypatch, width, batch):
     tf32 = [t.to_numpy() for t in gf.call(gf.compile_function(step.fn), tens)]
     for a, b in zip(fused, tf32):
         assert G.normwise(a, b) <= 1e-5
+
+
+@pytest.mark.parametrize("op,shape,stride,pad", [
+    ("fwd", (4, 64, 64, 32, 32, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (3, 64, 96, 19, 17, 3, 3), (2, 2), (1, 1, 1, 1)),
+    ("fwd", (2, 128, 256, 14, 14, 1, 1), (2, 2), (0, 0, 0, 0)),
+    ("fwd", (2, 256, 128, 14, 14, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("dgrad", (4, 40, 64, 16, 15, 3, 3), (1, 1), (1, 0, 0, 1)),
+    ("dgrad", (2, 64, 128, 14, 14, 3, 3), (1, 1), (1, 1, 1, 1)),
+])
+def test_conv_tcxh_matches_oracle(monkeypatch, op, shape, stride, pad):
+    """2xFP16 TMA-box convolution (conv_f16.cu): channel-scaled fp16
+    activation planes and filter planes divided by the same scales, channels
+    1e20 apart: normwise within 1e-6 of the oracle (the contract is 1e-5)."""
+    import test_lowering as TL
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    fn = TL._conv_fn(gf, op, shape, stride, pad)
+    exe = gf.compile_function(fn, conv_layout="nhwc", optimize=False)
+    assert any(L.kind in (abi.K_CONV_TCXH64, abi.K_CONV_TCXH128) for L in exe.lowered.launches)
+    rng = np.random.default_rng(19)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][:, 1] *= np.float32(1e-12)
+    ins[0][:, 2] *= np.float32(1e8)
+    out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6

@@ -243,6 +243,7 @@ def test_conv_fused_gather_emulated(monkeypatch, op, shape, stride, pad):
     from oracle import interp
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_CONV_F16", "0")
     N, C, K, H, W, R, S = shape
     fn = _conv_graph(op, N, C, K, H, W, R, S, stride, pad)
     nhwc = (0, 2, 3, 1)
@@ -273,6 +274,7 @@ def test_conv_tma_box_emulated(monkeypatch, op, shape, stride, pad):
     from oracle import interp
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_CONV_F16", "0")
     Ko, F32 = gf.OpKind, gf.ElementType.F32
     N, C, K, H, W, R, S = shape
     fn = gf.Function("conv")
@@ -407,3 +409,51 @@ def test_input_row_chunks_emulated(monkeypatch):
     stream_of, doff, deps = schedule.build(h.lowered)
     g0 = next(i for i, L in enumerate(h.lowered.launches) if L.label.startswith("dot_f16#") and ":rows0" in L.label)
     assert not set(deps[doff[g0]:doff[g0 + 1]]) & set(splits[1:])
+
+
+def _conv_fn(gf, op, shape, stride, pad):
+    Ko, F32 = gf.OpKind, gf.ElementType.F32
+    N, C, K, H, W, R, S = shape
+    fn = gf.Function("conv")
+    if op == "fwd":
+        x = fn.add_parameter(F32, (N, C, H, W))
+        f = fn.add_parameter(F32, (K, C, R, S))
+        c = fn.add_node(Ko.CONV2D, [fn.add_node(Ko.RELU, [x]), f], {"strides": stride, "padding": pad})
+    else:
+        d = fn.add_parameter(F32, (N, K, H, W))
+        f = fn.add_parameter(F32, (K, C, R, S))
+        Hi, Wi = H - pad[0] - pad[1] + R - 1, W - pad[2] - pad[3] + S - 1
+        c = fn.add_node(Ko.CONV_BACKPROP_DATA, [fn.add_node(Ko.RELU, [d]), f],
+                        {"data_shape": (N, C, Hi, Wi), "padding": pad}, allow_internal=True)
+    fn.set_results([fn.add_node(Ko.NEGATE, [c])])
+    return fn
+
+
+@pytest.mark.parametrize("op,shape,stride,pad", [
+    ("fwd", (2, 64, 64, 8, 9, 3, 3), (1, 1), (1, 1, 1, 1)),
+    ("fwd", (3, 64, 96, 9, 9, 3, 3), (2, 2), (1, 1, 1, 1)),
+    ("fwd", (2, 128, 200, 7, 7, 1, 1), (2, 2), (0, 0, 0, 0)),
+    ("dgrad", (2, 40, 64, 8, 7, 3, 3), (1, 1), (1, 0, 0, 1)),
+])
+def test_conv_tcxh_emulated(monkeypatch, op, shape, stride, pad):
+    """Channel-scaled fp16 activation planes + filter planes divided by the
+    same scales (2xFP16 TMA-box convolution), with channels 1e20 apart:
+    normwise within 1e-6 of the oracle."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    fn = _conv_fn(gf, op, shape, stride, pad)
+    h = host_compile(fn, optimize=False, conv_layout="nhwc")
+    kinds = [L.kind for L in h.lowered.launches]
+    assert {abi.K_CHMAX, abi.K_CHSPLIT, abi.K_FSPLIT} <= set(kinds), [L.label for L in h.lowered.launches]
+    assert set(kinds) & {abi.K_CONV_TCXH64, abi.K_CONV_TCXH128}
+    rng = np.random.default_rng(17)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][:, 1] *= np.float32(1e-12)  # one channel far below the others: scales are per channel
+    ins[0][:, 2] *= np.float32(1e8)
+    tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v) for v in ins]
+    out = emulate(h, tens)[0]
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
