@@ -96,6 +96,8 @@ enum {
                              row-scaled (gfb_fsplit_args) */
     GFB_K_CONV_TCXH64 = 39,  /* 2xFP16 implicit-GEMM conv on TMA boxes of fp16 activation planes, 128x64 (gfb_tcxh_args) */
     GFB_K_CONV_TCXH128 = 40, /* as GFB_K_CONV_TCXH64 with 128x128 tiles */
+    GFB_K_CONV_TCGWH64 = 41,  /* 2xFP16 weight gradient on TMA boxes of the fp16 planes of x and dy, 128x64 (gfb_tcgwh_args) */
+    GFB_K_CONV_TCGWH128 = 42, /* as GFB_K_CONV_TCGWH64 with 128x128 tiles */
     GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
                              always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
                              entry only traps */
@@ -336,6 +338,28 @@ typedef struct GFB_ALIGN64 {
     int64_t pad[3];
     uint64_t tmap[4][16];
 } gfb_tcxh_args;
+
+/* 2xFP16 ConvBackpropFilter (stride 1) on the channel-scaled fp16 planes of
+ * x [N, H, W, C] and dy [N, Ho, Wo, K] (gfb_chsplit_args): GEMM rows (r, s, c)
+ * (tap-major, C % 64 == 0), columns the K output channels, contraction over
+ * the output pixels in boxes of 64 (BX x BY x BNI, tile walk as gfb_tcxh_args).
+ * The A tile of a box is two 64-channel TMA boxes of x shifted by their tap
+ * (zero-filled padding), B one or two 64-channel boxes of dy, both MN-major;
+ * dW[row, col] = sum / (a_sc[c] b_sc[col]) at (row / C) * c_s_hi + (row % C) *
+ * c_s_lo + col * c_sn, or, with k_splits > 1, split z's partial at
+ * c + z * split_stride + row * N + col (reduced by a second pass). */
+typedef struct GFB_ALIGN64 {
+    const void* const* tab;
+    uint64_t c, a_hi, a_lo, b_hi, b_lo, a_sc, b_sc;
+    int64_t M, N, C, S, pt, pl;
+    int64_t c_s_hi, c_s_lo, c_sn;
+    int64_t k_splits, boxes_per_split, split_stride;
+    int64_t a_dims[4], a_strides[4]; /* x planes: C, W, H, N innermost first */
+    int64_t b_dims[4], b_strides[4]; /* dy planes: K, Wo, Ho, N */
+    int32_t No, Yo, Xo, BX, BY, BNI, tiles_x, tiles_y;
+    int64_t pad[8];
+    uint64_t tmap[4][16];
+} gfb_tcgwh_args;
 
 /* fp16 split of a dense F32 matrix [rows, cols] (row pitch ld elements, cols % 8 == 0):
  * per 128 x 128 tile, s = 2^(14 - floor(log2(max |x|))) (1 for an all-zero tile),

@@ -18,6 +18,7 @@ K_DOT_SM_F32, K_DOT_SM_F64 = 15, 16
 K_DOT_TC32P = 19
 K_DOT_F16P, K_SPLIT_F16 = 34, 35
 K_CHMAX, K_CHSPLIT, K_FSPLIT, K_CONV_TCXH64, K_CONV_TCXH128 = 36, 37, 38, 39, 40
+K_CONV_TCGWH64, K_CONV_TCGWH128 = 41, 42
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
@@ -124,6 +125,22 @@ class TcxhArgs(C.Structure):
         ("sx", C.c_int32), ("sy", C.c_int32), ("ox", C.c_int32), ("oy", C.c_int32), ("S", C.c_int32),
         ("CB", C.c_int32), ("ksign", C.c_int32), ("pad0", C.c_int32),
         ("pad", C.c_int64 * 3),
+        ("tmap", (C.c_uint64 * 16) * 4),
+    ]
+
+
+class TcgwhArgs(C.Structure):
+    # 64-byte aligned in C: tmap sits at offset 384, size 896.
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64), ("a_hi", C.c_uint64), ("a_lo", C.c_uint64), ("b_hi", C.c_uint64),
+        ("b_lo", C.c_uint64), ("a_sc", C.c_uint64), ("b_sc", C.c_uint64),
+        ("M", C.c_int64), ("N", C.c_int64), ("C", C.c_int64), ("S", C.c_int64), ("pt", C.c_int64), ("pl", C.c_int64),
+        ("c_s_hi", C.c_int64), ("c_s_lo", C.c_int64), ("c_sn", C.c_int64),
+        ("k_splits", C.c_int64), ("boxes_per_split", C.c_int64), ("split_stride", C.c_int64),
+        ("a_dims", C.c_int64 * 4), ("a_strides", C.c_int64 * 4), ("b_dims", C.c_int64 * 4), ("b_strides", C.c_int64 * 4),
+        ("No", C.c_int32), ("Yo", C.c_int32), ("Xo", C.c_int32), ("BX", C.c_int32), ("BY", C.c_int32),
+        ("BNI", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+        ("pad", C.c_int64 * 8),
         ("tmap", (C.c_uint64 * 16) * 4),
     ]
 
@@ -255,5 +272,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tcgwh_args": TcgwhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

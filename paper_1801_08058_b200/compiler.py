@@ -155,6 +155,7 @@ F16_SMEM_PAIR = TC_SMEM_PAIR  # gemm_f16.cu HCfg::SMEM_BYTES: same 64 KB stages 
 # gfb_conv_tcx_kernel: MMA stages (3 at BN=128, 4 at BN=64) + barriers (gemm_tc.cu XCfg)
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
 TCXH_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 64 * 2 + 256 + 1024 for bn in (64, 128)}  # conv_f16.cu HXCfg
+TCGWH_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 64 * 2 + 256 + 1024 for bn in (64, 128)}  # conv_f16.cu HWCfg
 CHMAX_BLOCKS = 296
 STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
 STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
@@ -2487,6 +2488,59 @@ class Lowering:
         rec.finalize = _finalize_refs(ta, {"c": out, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo, "b_inv": binv})
         self.launches.append(rec)
 
+    def _conv_tcgwh(self, n, xb, xshape, yb, yshape, out, R, S, pt, pl, label):
+        """ConvBackpropFilter on conv_f16.cu gfb_conv_tcgwh_kernel: the fp16
+        planes of x and dy (shared with the forward / data-gradient
+        convolutions that read them) by TMA boxes of 64 output pixels, rows
+        (r, s, c), split-K over the pixel boxes (+ the reduce pass)."""
+        N_, C_, H_, W_ = xshape
+        _, K_, Ho, Wo = yshape
+        ahi, alo, asc = self._ch_planes(xb, N_ * H_ * W_, C_)
+        bhi, blo, bsc = self._ch_planes(yb, N_ * Ho * Wo, K_)
+        m, ncols = R * S * C_, K_
+        BX = min(64, 1 << max(0, (Wo - 1).bit_length()))
+        BY = min(64 // BX, 1 << max(0, (Ho - 1).bit_length()))
+        BNI = 64 // (BX * BY)
+        tiles_x, tiles_y = (Wo + BX - 1) // BX, (Ho + BY - 1) // BY
+        nbox = tiles_x * tiles_y * ((N_ + BNI - 1) // BNI)
+        bn = 64 if ncols <= 64 else 128
+        tiles = ((m + 127) // 128) * ((ncols + bn - 1) // bn)
+        splits = max(1, min(max(1, nbox // 16), -(-2 * NUM_SMS // tiles)))
+        per = -(-nbox // splits)
+        splits = -(-nbox // per)
+        os_ = out.strides
+        addr = {"c_rdiv": C_, "c_s_hi": os_[3], "c_s_lo": os_[1], "c_sn": os_[0]}
+        ta = abi.TcgwhArgs(M=m, N=ncols, C=C_, S=S, pt=pt, pl=pl, c_s_hi=os_[3], c_s_lo=os_[1], c_sn=os_[0],
+                           k_splits=splits, boxes_per_split=per, No=N_, Yo=Ho, Xo=Wo, BX=BX, BY=BY, BNI=BNI,
+                           tiles_x=tiles_x, tiles_y=tiles_y)
+        ta.a_dims[:] = [C_, W_, H_, N_]
+        ta.a_strides[:] = [1, C_, W_ * C_, H_ * W_ * C_]
+        ta.b_dims[:] = [K_, Wo, Ho, N_]
+        ta.b_strides[:] = [1, K_, Wo * K_, Ho * Wo * K_]
+        target = out
+        if splits > 1:
+            scratch = Buffer(self.new_key(), ElementType.F32, (splits, m, ncols), (m * ncols, ncols, 1))
+            self.buf[("splitk", n)] = scratch
+            ta.split_stride = m * ncols
+            target = scratch
+        kind = abi.K_CONV_TCGWH64 if bn == 64 else abi.K_CONV_TCGWH128
+        grid = (max(1, min(tiles * splits, NUM_SMS)), 1, 1)
+        rec = LaunchRec(kind, grid, (192, 1, 1), TCGWH_SMEM[bn], ta, [ahi.key, alo.key, asc.key, bhi.key, blo.key, bsc.key],
+                        [target.key], label)
+        rec.flops = 2 * m * ncols * N_ * Ho * Wo
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": target, "a_hi": ahi, "a_lo": alo, "b_hi": bhi, "b_lo": blo, "a_sc": asc,
+                                           "b_sc": bsc})
+        self.launches.append(rec)
+        if splits > 1:
+            p2 = Program(self, extents=(m * ncols, splits), vec_src=0, et=ElementType.F32)
+            k = p2.leaf(target, [(1, 1, splits), (0, ncols, m), (0, 1, ncols)])
+            p2.emit(I_LOAD, k=k)
+            p2.red_out = LeafSpec(out, _conv_out_digits(addr, m, ncols), True)
+            p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+            self._col_launch(p2, m * ncols, splits, 1, label + ":splitk", ElementType.F32)
+        return rec
+
     def _conv_tcx(self, n, xb, xs, xshape, b, out, oshape, ncols, kdim, geo, yb, label):
         """Conv2D / ConvBackpropData whose A tiles are TMA boxes of output
         pixels (gemm_tc.cu, gfb_conv_tcx_kernel)."""
@@ -2718,6 +2772,11 @@ class Lowering:
                     n, "b", yb, K, kdim, 3, s_r=ys[1], geo=(0,) * 12 + (N, Ho, Wo), st=(ys[0], ys[2], ys[3]))
                 kgeo = dict(Ke1=Ho, Ke2=Wo, ko0=xs[0], ko1=xs[2], ko2=xs[3], kbase=-pt * xs[2] - pl * xs[3],
                             kh=1, kw=1, dh0=0, dw0=0)
+                if (real_c is None and self._tcxh_ok(xb, xs, (N, Cc, H, W), 1, 1)
+                        and self._tcxh_ok(yb, ys, (N, K, Ho, Wo), 1, 1)):
+                    self._conv_tcgwh(n, xb, (N, Cc, H, W), yb, (N, K, Ho, Wo), out, R, S, pt, pl,
+                                     f"{node.op.wire_name}_tcgwh#{n}")
+                    return True
                 if self._wgrad_mn_ok(xb, xs, yb, ys, Cc, K):
                     # channel-last x and dy: 16-byte MN-major loads of both raw
                     # operands, split to TF32 in the kernel (no dy planes)

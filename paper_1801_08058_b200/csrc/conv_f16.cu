@@ -358,6 +358,222 @@ __global__ void __launch_bounds__(tc::HXCfg<BN_>::THREADS, 1) gfb_conv_tcxh_kern
 template __global__ void gfb_conv_tcxh_kernel<64>(const __grid_constant__ gfb_tcxh_args);
 template __global__ void gfb_conv_tcxh_kernel<128>(const __grid_constant__ gfb_tcxh_args);
 
+// ---------------------------------------------------------------------------
+// Weight gradient (gfb_tcgwh_args): rows (r, s, c), columns dy's channels,
+// contraction over 64-pixel boxes.  Stage = [A hi | A lo | B hi | B lo], A as
+// two 64-channel x boxes (8 KB each: 64 pixels x 128 B, the canonical
+// SWIZZLE_128B MN-major layout), B as one or two dy boxes.
+namespace tc {
+template <int BN_>
+struct HWCfg {
+    static constexpr int BM = 128, BN = BN_, BKP = 64;  // pixels per stage
+    static constexpr int BOX_BYTES = 64 * BKP * 2;       // 64 channels x 64 pixels fp16
+    static constexpr int A_BYTES = 2 * BOX_BYTES, B_BYTES = (BN / 64) * BOX_BYTES;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int STAGES = BN_ == 128 ? 3 : 4;
+    static constexpr int CHUNK_KB = 2, NBUF = 512 / BN;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4;
+    static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+};
+}  // namespace tc
+
+template <int BN_>
+__global__ void __launch_bounds__(tc::HWCfg<BN_>::THREADS, 1) gfb_conv_tcgwh_kernel(const __grid_constant__ gfb_tcgwh_args p) {
+    using namespace tc;
+    using C_ = HWCfg<BN_>;
+    constexpr int BN = C_::BN, STAGES = C_::STAGES, NBUF = C_::NBUF, BOX = C_::BOX_BYTES;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntm = (int)((p.M + 127) / 128), ntn = (int)((p.N + BN - 1) / BN);
+    const int nbox = p.tiles_x * p.tiles_y * ((p.No + p.BNI - 1) / p.BNI);
+    const int splits = p.k_splits > 1 ? (int)p.k_splits : 1;
+    const int nitems = ntm * ntn * splits;
+    struct Item {
+        int mt, nt, z, b0, nk;
+    };
+    auto item_at = [&](int it) {
+        Item r;
+        r.mt = it % ntm;
+        r.nt = (it / ntm) % ntn;
+        r.z = it / (ntm * ntn);
+        r.b0 = splits > 1 ? r.z * (int)p.boxes_per_split : 0;
+        const int b1 = splits > 1 ? min(nbox, r.b0 + (int)p.boxes_per_split) : nbox;
+        r.nk = max(0, b1 - r.b0);
+        return r;
+    };
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 4; ++i) prefetch_tmap(p.tmap[i]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t gk = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const Item I = item_at(it);
+                // the two 64-row halves of the A tile: tap and first channel of each
+                int acx[2], acy[2], acc_[2];
+                bool aok[2];
+                for (int j = 0; j < 2; ++j) {
+                    const int64_t row = (int64_t)I.mt * 128 + 64 * j;
+                    aok[j] = row < p.M;
+                    const int tap = (int)(row / p.C);
+                    acc_[j] = (int)(row % p.C);
+                    acx[j] = (int)(tap % p.S) - (int)p.pl;
+                    acy[j] = (int)(tap / p.S) - (int)p.pt;
+                }
+                uint32_t bytes = 0;
+                for (int j = 0; j < 2; ++j) bytes += aok[j] ? 2 * BOX : 0;
+                for (int jj = 0; jj < BN / 64; ++jj) bytes += (I.nt * BN + 64 * jj < p.N) ? 2 * BOX : 0;
+                for (int kb = 0; kb < I.nk; ++kb, ++gk) {
+                    const int s = gk % STAGES;
+                    mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], bytes);
+                    const int box = I.b0 + kb;
+                    const int tx = box % p.tiles_x, ty = (box / p.tiles_x) % p.tiles_y, tn = box / (p.tiles_x * p.tiles_y);
+                    const int x0 = tx * p.BX, y0 = ty * p.BY, n0 = tn * p.BNI;
+                    for (int j = 0; j < 2; ++j) {
+                        if (!aok[j]) continue;
+                        tma_load_4d(st + j * BOX, p.tmap[0], acc_[j], x0 + acx[j], y0 + acy[j], n0, &full[s]);
+                        tma_load_4d(st + A_BYTES + j * BOX, p.tmap[1], acc_[j], x0 + acx[j], y0 + acy[j], n0, &full[s]);
+                    }
+                    for (int jj = 0; jj < BN / 64; ++jj) {
+                        const int kc = I.nt * BN + 64 * jj;
+                        if (kc >= p.N) continue;
+                        tma_load_4d(st + 2 * A_BYTES + jj * BOX, p.tmap[2], kc, x0, y0, n0, &full[s]);
+                        tma_load_4d(st + 2 * A_BYTES + B_BYTES + jj * BOX, p.tmap[3], kc, x0, y0, n0, &full[s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(128, BN) | (1u << 15) | (1u << 16);  // MN-major A and B
+            uint32_t gk = 0, gc = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const Item I = item_at(it);
+                for (int i = 0; i < I.nk; ++i, ++gk) {
+                    const int s = gk % STAGES;
+                    const uint32_t chunk = gc + i / CHUNK_KB;
+                    const int b = chunk % NBUF;
+                    const bool chunk_start = i % CHUNK_KB == 0;
+                    if (chunk_start) {
+                        mbar_wait(&tempty[b], ((chunk / NBUF) & 1) ^ 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = su32(smem + s * STAGE_BYTES), sb = sa + 2 * A_BYTES;
+                    const uint32_t d = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int j = 0; j < C_::BKP / 16; ++j) {
+                        // 16 pixels (K rows) = two 1 KB atoms; 64-channel MN chunks one box apart
+                        const uint32_t acc = !(chunk_start && j == 0);
+                        const uint64_t ah = smem_desc_mn16(sa + j * 2048, BOX), al = smem_desc_mn16(sa + A_BYTES + j * 2048, BOX);
+                        const uint64_t bh = smem_desc_mn16(sb + j * 2048, BOX), bl = smem_desc_mn16(sb + B_BYTES + j * 2048, BOX);
+                        mma_f16_cta(d, ah, bh, idesc, acc);
+                        mma_f16_cta(d, ah, bl, idesc, 1);
+                        mma_f16_cta(d, al, bh, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                    if (i % CHUNK_KB == CHUNK_KB - 1 || i == I.nk - 1) mma_commit(&tfull[b]);
+                }
+                gc += (I.nk + CHUNK_KB - 1) / CHUNK_KB;
+            }
+        }
+    } else {
+        constexpr int EC = BN;
+        const int q = warp & 3;
+        uint32_t gc = 0;
+        const float* asc = resolve<const float>(p.tab, p.a_sc);
+        const float* bsc = resolve<const float>(p.tab, p.b_sc);
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const Item I = item_at(it);
+            const int nchunk = (I.nk + CHUNK_KB - 1) / CHUNK_KB;
+            float acc[EC];
+#pragma unroll
+            for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+            for (int c0 = 0; c0 < nchunk; ++c0) {
+                const uint32_t chunk = gc + c0;
+                const int b = chunk % NBUF;
+                mbar_wait(&tfull[b], (chunk / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int c = 0; c < EC / 16; ++c) {
+                    float v[16];
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 16), v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], v[j]);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            }
+            gc += nchunk;
+            const int64_t row = (int64_t)I.mt * 128 + q * 32 + lane;
+            if (row >= p.M) continue;
+            const float ia = __frcp_rn(__ldg(asc + row % p.C));
+            const int col0 = I.nt * BN;
+            if (splits > 1) {
+                float* dst = resolve<float>(p.tab, p.c) + (int64_t)I.z * p.split_stride + row * p.N;
+#pragma unroll
+                for (int j = 0; j < EC; j += 4) {
+                    if (col0 + j >= p.N) break;
+                    const float4 f = __ldg(reinterpret_cast<const float4*>(bsc + col0 + j));
+                    *reinterpret_cast<float4*>(dst + col0 + j) =
+                        make_float4(__fmul_rn(__fmul_rn(acc[j], ia), __frcp_rn(f.x)), __fmul_rn(__fmul_rn(acc[j + 1], ia), __frcp_rn(f.y)),
+                                    __fmul_rn(__fmul_rn(acc[j + 2], ia), __frcp_rn(f.z)), __fmul_rn(__fmul_rn(acc[j + 3], ia), __frcp_rn(f.w)));
+                }
+            } else {
+                float* dst = resolve<float>(p.tab, p.c) + (row / p.C) * p.c_s_hi + (row % p.C) * p.c_s_lo;
+#pragma unroll
+                for (int j = 0; j < EC; ++j)
+                    if (col0 + j < p.N)
+                        dst[(int64_t)(col0 + j) * p.c_sn] = __fmul_rn(__fmul_rn(acc[j], ia), __frcp_rn(__ldg(bsc + col0 + j)));
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
+template __global__ void gfb_conv_tcgwh_kernel<64>(const __grid_constant__ gfb_tcgwh_args);
+template __global__ void gfb_conv_tcgwh_kernel<128>(const __grid_constant__ gfb_tcgwh_args);
+
 }  // namespace gfb
 
 extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
@@ -366,6 +582,9 @@ extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
     if (kind == GFB_K_FSPLIT) return (const void*)gfb::gfb_fsplit_kernel;
     if (kind == GFB_K_CONV_TCXH64) return (const void*)gfb::gfb_conv_tcxh_kernel<64>;
     if (kind == GFB_K_CONV_TCXH128) return (const void*)gfb::gfb_conv_tcxh_kernel<128>;
+    if (kind == GFB_K_CONV_TCGWH64) return (const void*)gfb::gfb_conv_tcgwh_kernel<64>;
+    if (kind == GFB_K_CONV_TCGWH128) return (const void*)gfb::gfb_conv_tcgwh_kernel<128>;
     return nullptr;
 }
+extern "C" int gfb_tcgwh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HWCfg<64>::SMEM_BYTES : gfb::tc::HWCfg<128>::SMEM_BYTES; }
 extern "C" int gfb_tcxh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HXCfg<64>::SMEM_BYTES : gfb::tc::HXCfg<128>::SMEM_BYTES; }

@@ -283,7 +283,7 @@ const void* kernel_for(uint32_t kind) {
         kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128 || kind == GFB_K_CONV_STEM64)
         return gfb_tc_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F16P || kind == GFB_K_SPLIT_F16) return gfb_f16_kernel_ptr((int)kind);
-    if (kind >= GFB_K_CHMAX && kind <= GFB_K_CONV_TCXH128) return gfb_conv_f16_kernel_ptr((int)kind);
+    if (kind >= GFB_K_CHMAX && kind <= GFB_K_CONV_TCGWH128) return gfb_conv_f16_kernel_ptr((int)kind);
     return nullptr;
 }
 
@@ -645,6 +645,18 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
             for (int t = 2; t < 4; ++t)
                 if (!encode_plane16_map(addr[t], a->N, a->K, a->tmap[t], L.kind == GFB_K_CONV_TCXH64 ? 64 : 128))
                     return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 filter plane) failed"));
+        }
+        if (L.kind == GFB_K_CONV_TCGWH64 || L.kind == GFB_K_CONV_TCGWH128) {
+            gfb_tcgwh_args* a = (gfb_tcgwh_args*)(e->args.data() + L.arg_offset);
+            const uint64_t refs[4] = {a->a_hi, a->a_lo, a->b_hi, a->b_lo};
+            for (int t = 0; t < 4; ++t) {
+                if ((refs[t] >> 56) != GFB_SLOT_ARENA)
+                    return bail(fail(GFB_ERR_INVALID, "TMA convolution operands must live in the arena"));
+                void* addr = (char*)e->arena + (refs[t] & ((1ull << 56) - 1));
+                if (!encode_act16_map(addr, t < 2 ? a->a_dims : a->b_dims, t < 2 ? a->a_strides : a->b_strides, (uint32_t)a->BX,
+                                      (uint32_t)a->BY, (uint32_t)a->BNI, 1, 1, a->tmap[t]))
+                    return bail(fail(GFB_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 gradient box) failed"));
+            }
         }
         if (L.kind == GFB_K_CONV_TCX64 || L.kind == GFB_K_CONV_TCX128) {
             gfb_tcx_args* a = (gfb_tcx_args*)(e->args.data() + L.arg_offset);

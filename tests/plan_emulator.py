@@ -623,6 +623,45 @@ def run_tcxh(mem, a):
     mem.view(a.c, np.float32)[n * a.o_n + y * a.o_y + x * a.o_x + j * a.c_sn] = out
 
 
+def run_tcgwh(mem, a):
+    """gfb_conv_tcgwh_kernel: dW[(r, s, c), k] = sum over output pixels of the
+    x planes at the tap-shifted pixel times the dy planes, unscaled."""
+    Cc, Wd, Hd, Nd = list(a.a_dims)
+    K_, Wo, Ho, _ = list(a.b_dims)
+    xs = np.zeros((Nd, Hd + 2 * 8, Wd + 2 * 8, Cc))  # zero border for the taps (|shift| <= 8 here)
+    sc_a = mem.view(a.a_sc, np.float32)[:Cc].astype(np.float64)
+    sc_b = mem.view(a.b_sc, np.float32)[:K_].astype(np.float64)
+    xhl = (mem.view(a.a_hi, np.float16)[: Nd * Hd * Wd * Cc].astype(np.float64),
+           mem.view(a.a_lo, np.float16)[: Nd * Hd * Wd * Cc].astype(np.float64))
+    dhl = (mem.view(a.b_hi, np.float16)[: Nd * Ho * Wo * K_].astype(np.float64).reshape(-1, K_),
+           mem.view(a.b_lo, np.float16)[: Nd * Ho * Wo * K_].astype(np.float64).reshape(-1, K_))
+    R = a.M // (Cc * a.S)
+    rows = []
+    for r in range(R):
+        for s_ in range(a.S):
+            dy_ = r - a.pt
+            dx_ = s_ - a.pl
+            parts = []
+            for xv in xhl:
+                xs[:] = 0
+                xs[:, 8:8 + Hd, 8:8 + Wd, :] = xv.reshape(Nd, Hd, Wd, Cc)
+                win = xs[:, 8 + dy_:8 + dy_ + Ho, 8 + dx_:8 + dx_ + Wo, :].reshape(-1, Cc)
+                parts.append(win)
+            g = parts[0].T @ dhl[0] + parts[0].T @ dhl[1] + parts[1].T @ dhl[0]
+            rows.append(g)
+    dw = np.concatenate(rows, axis=0) / sc_a[np.arange(a.M) % Cc][:, None] / sc_b[None, :]
+    dw = dw.astype(np.float32)
+    i = np.arange(a.M, dtype=np.int64)[:, None]
+    j = np.arange(a.N, dtype=np.int64)[None, :]
+    C = mem.view(a.c, np.float32)
+    if a.k_splits > 1:  # the whole sum in split 0, zeros in the others (the reduce pass adds them)
+        C[i * a.N + j] = dw
+        for z in range(1, a.k_splits):
+            C[z * a.split_stride + i * a.N + j] = 0.0
+    else:
+        C[(i // Cc) * a.c_s_hi + (i % Cc) * a.c_s_lo + j * a.c_sn] = dw
+
+
 def run_tcgg(mem, a):
     """gfb_conv_tcgg_kernel: generic row / K decompositions (gfb_tcgg_args)."""
     src = mem.view(a.a, np.float32)
@@ -734,6 +773,8 @@ def _run_launch(mem, L):
         run_fsplit(mem, L.args)
     elif L.kind in (abi.K_CONV_TCXH64, abi.K_CONV_TCXH128):
         run_tcxh(mem, L.args)
+    elif L.kind in (abi.K_CONV_TCGWH64, abi.K_CONV_TCGWH128):
+        run_tcgwh(mem, L.args)
     elif L.kind in (abi.K_CONV_TCG64, abi.K_CONV_TCG128):
         run_tcg(mem, L.args)
     elif L.kind in (abi.K_CONV_TCX64, abi.K_CONV_TCX128):

@@ -222,6 +222,7 @@ def test_wgrad_channel_last_matches_oracle(monkeypatch, shape, pad, mn):
     import test_lowering as TL
     from paper_1801_08058_b200 import abi
 
+    monkeypatch.setenv("GFB_CONV_F16", "0")
     monkeypatch.setenv("GFB_CONV", "tc")
     monkeypatch.setenv("GFB_TCGW", "1" if mn else "0")
     N, C, Ko, H, W, R, S = shape
@@ -412,6 +413,37 @@ def test_conv_tcxh_matches_oracle(monkeypatch, op, shape, stride, pad):
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     ins[0][:, 1] *= np.float32(1e-12)
     ins[0][:, 2] *= np.float32(1e8)
+    out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
+
+
+@pytest.mark.parametrize("shape,pad", [
+    ((8, 64, 64, 28, 28, 3, 3), (1, 1, 1, 1)),
+    ((4, 128, 256, 14, 14, 1, 1), (0, 0, 0, 0)),
+    ((4, 64, 128, 15, 13, 3, 3), (1, 0, 0, 1)),
+    ((2, 512, 512, 7, 7, 3, 3), (1, 1, 1, 1)),
+])
+def test_conv_tcgwh_matches_oracle(monkeypatch, shape, pad):
+    """2xFP16 weight gradient (conv_f16.cu gfb_conv_tcgwh_kernel) on the
+    channel-scaled planes of x and dy vs the oracle: normwise within 1e-6."""
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    Ko = gf.OpKind
+    N, C, K, H, W, R, S = shape
+    fn = gf.Function("wgrad")
+    x = fn.add_parameter(F32, (N, C, H, W))
+    Ho, Wo = H + pad[0] + pad[1] - R + 1, W + pad[2] + pad[3] - S + 1
+    d = fn.add_parameter(F32, (N, K, Ho, Wo))
+    g = fn.add_node(Ko.CONV_BACKPROP_FILTER, [fn.add_node(Ko.RELU, [x]), fn.add_node(Ko.NEGATE, [d])],
+                    {"filter_shape": (K, C, R, S), "padding": pad}, allow_internal=True)
+    fn.set_results([g])
+    exe = gf.compile_function(fn, conv_layout="nhwc", optimize=False)
+    assert any(L.kind in (abi.K_CONV_TCGWH64, abi.K_CONV_TCGWH128) for L in exe.lowered.launches)
+    rng = np.random.default_rng(29)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][:, 3] *= np.float32(1e-9)
     out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6

@@ -457,3 +457,34 @@ def test_conv_tcxh_emulated(monkeypatch, op, shape, stride, pad):
     out = emulate(h, tens)[0]
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
+
+
+@pytest.mark.parametrize("shape,pad", [((2, 64, 64, 9, 10, 3, 3), (1, 1, 1, 1)), ((3, 128, 64, 7, 7, 1, 1), (0, 0, 0, 0)),
+                                       ((2, 64, 128, 8, 8, 3, 3), (1, 0, 0, 1))])
+def test_conv_tcgwh_emulated(monkeypatch, shape, pad):
+    """2xFP16 weight gradient on the channel-scaled planes of x and dy:
+    normwise within 1e-6 of the oracle."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    Ko, F32 = gf.OpKind, gf.ElementType.F32
+    N, C, K, H, W, R, S = shape
+    fn = gf.Function("wgrad")
+    x = fn.add_parameter(F32, (N, C, H, W))
+    Ho, Wo = H + pad[0] + pad[1] - R + 1, W + pad[2] + pad[3] - S + 1
+    d = fn.add_parameter(F32, (N, K, Ho, Wo))
+    g = fn.add_node(Ko.CONV_BACKPROP_FILTER, [fn.add_node(Ko.RELU, [x]), fn.add_node(Ko.NEGATE, [d])],
+                    {"filter_shape": (K, C, R, S), "padding": pad}, allow_internal=True)
+    fn.set_results([g])
+    h = host_compile(fn, optimize=False, conv_layout="nhwc")
+    kinds = [L.kind for L in h.lowered.launches]
+    assert set(kinds) & {abi.K_CONV_TCGWH64, abi.K_CONV_TCGWH128}, [L.label for L in h.lowered.launches]
+    rng = np.random.default_rng(23)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][:, 3] *= np.float32(1e-9)
+    tens = [gf.tensor_from_flat(F32, v.shape, v) for v in ins]
+    out = emulate(h, tens)[0]
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
