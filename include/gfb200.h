@@ -98,6 +98,7 @@ enum {
     GFB_K_CONV_TCXH128 = 40, /* as GFB_K_CONV_TCXH64 with 128x128 tiles */
     GFB_K_CONV_TCGWH64 = 41,  /* 2xFP16 weight gradient on TMA boxes of the fp16 planes of x and dy, 128x64 (gfb_tcgwh_args) */
     GFB_K_CONV_TCGWH128 = 42, /* as GFB_K_CONV_TCGWH64 with 128x128 tiles */
+    GFB_K_MEMSET = 43,        /* zero a byte range of the arena (gfb_memset_args; a memset node of the graph) */
     GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
                              always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
                              entry only traps */
@@ -296,11 +297,11 @@ typedef struct GFB_ALIGN64 {
 } gfb_tc_args;
 
 /* Channel-scaled fp16 planes of a dense channel-last activation [P pixels, C]
- * (C a power of two, 8 <= C <= 1024): GFB_K_CHMAX writes partial[b * C + c] =
- * max |x[p, c]| over block b's pixel rows (gridDim.x == nblocks);
- * GFB_K_CHSPLIT with mode 1 reduces the partials to sc[c] = 2^(14 -
- * floor(log2 max_c)) (one block per 32 channels), with mode 0 writes
- * hi = fp16_rn(x sc[c]), lo = fp16_rn(x sc[c] - hi), planes [P, C]. */
+ * (C a power of two, 8 <= C <= 1024): GFB_K_CHMAX folds max |x[p, c]| into
+ * partial[c] (float bits, atomicMax; zeroed by a GFB_K_MEMSET launch before
+ * it); GFB_K_CHSPLIT takes sc[c] = 2^(14 - floor(log2 partial[c])) (block 0
+ * stores them in sc) and writes hi = fp16_rn(x sc[c]), lo = fp16_rn(x sc[c] -
+ * hi), planes [P, C]. */
 typedef struct {
     const void* const* tab;
     uint64_t src, partial, sc, hi, lo; /* GFB_REF */
@@ -472,6 +473,12 @@ typedef struct {
     int32_t dtype;  /* 0 f32, 1 f64 */
     int32_t op;     /* 0 sum (partial gradients), 1 max (a max-reduction over the sharded batch axis) */
 } gfb_allreduce_args;
+
+typedef struct {
+    const void* const* tab;
+    uint64_t buf;   /* GFB_REF into the arena */
+    uint64_t bytes;
+} gfb_memset_args;
 
 /* Row-fused launch: the generated kernel's tensors, by position (inputs,
  * outputs, per-team partials of cross-row reductions; rowfuse.py). */

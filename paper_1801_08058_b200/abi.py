@@ -19,6 +19,7 @@ K_DOT_TC32P = 19
 K_DOT_F16P, K_SPLIT_F16 = 34, 35
 K_CHMAX, K_CHSPLIT, K_FSPLIT, K_CONV_TCXH64, K_CONV_TCXH128 = 36, 37, 38, 39, 40
 K_CONV_TCGWH64, K_CONV_TCGWH128 = 41, 42
+K_MEMSET = 43
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
@@ -239,6 +240,10 @@ class ConvArgs(C.Structure):
     ]
 
 
+class MemsetArgs(C.Structure):
+    _fields_ = [("tab", C.c_void_p), ("buf", C.c_uint64), ("bytes", C.c_uint64)]
+
+
 class AllReduceArgs(C.Structure):
     _fields_ = [
         ("tab", C.c_void_p), ("buf", C.c_uint64), ("count", C.c_uint64),
@@ -272,5 +277,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tcgwh_args": TcgwhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tcgwh_args": TcgwhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_memset_args": MemsetArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

@@ -2423,25 +2423,26 @@ class Lowering:
         got = self.buf.get(key + ("hi",))
         if got is not None:
             return got, self.buf[key + ("lo",)], self.buf[key + ("sc",)]
-        part = Buffer(self.new_key(), ElementType.F32, (CHMAX_BLOCKS * C,), (1,))
+        part = Buffer(self.new_key(), ElementType.F32, (C,), (1,))
         sc = Buffer(self.new_key(), ElementType.F32, (C,), (1,))
         hi = Buffer(self.new_key(), ElementType.F32, ((P * C + 1) // 2,), (1,))
         lo = Buffer(self.new_key(), ElementType.F32, ((P * C + 1) // 2,), (1,))
         for p_, b_ in (("part", part), ("sc", sc), ("hi", hi), ("lo", lo)):
             self.buf[key + (p_,)] = b_
+        a0 = abi.MemsetArgs(bytes=C * 4)
+        r0 = LaunchRec(abi.K_MEMSET, (1, 1, 1), (1, 1, 1), 0, a0, [], [part.key], f"memset#{root.key}")
+        r0.finalize = _finalize_refs(a0, {"buf": part})
+        self.launches.append(r0)
         a1 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS)
-        r1 = LaunchRec(abi.K_CHMAX, (CHMAX_BLOCKS, 1, 1), (256, 1, 1), 0, a1, [xb.key], [part.key], f"chmax#{root.key}")
+        r1 = LaunchRec(abi.K_CHMAX, (CHMAX_BLOCKS, 1, 1), (256, 1, 1), 0, a1, [xb.key, part.key], [part.key],
+                       f"chmax#{root.key}")
         r1.algo_bytes = P * C * 4
         r1.finalize = _finalize_refs(a1, {"src": xb, "partial": part})
         self.launches.append(r1)
-        a2 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS, mode=1)
-        r2 = LaunchRec(abi.K_CHSPLIT, ((C + 31) // 32, 1, 1), (256, 1, 1), 0, a2, [part.key], [sc.key], f"chscale#{root.key}")
-        r2.algo_bytes = CHMAX_BLOCKS * C * 4
-        r2.finalize = _finalize_refs(a2, {"src": xb, "partial": part, "sc": sc, "hi": hi, "lo": lo})
-        self.launches.append(r2)
-        a3 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS, mode=0)
+        a3 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS)
         grid = max(1, min(NUM_SMS * 4, (P * (C // 4) + 255) // 256))
-        r3 = LaunchRec(abi.K_CHSPLIT, (grid, 1, 1), (256, 1, 1), 0, a3, [xb.key, sc.key], [hi.key, lo.key], f"chsplit#{root.key}")
+        r3 = LaunchRec(abi.K_CHSPLIT, (grid, 1, 1), (256, 1, 1), 0, a3, [xb.key, part.key], [sc.key, hi.key, lo.key],
+                       f"chsplit#{root.key}")
         r3.algo_bytes = P * C * 8
         r3.finalize = _finalize_refs(a3, {"src": xb, "partial": part, "sc": sc, "hi": hi, "lo": lo})
         self.launches.append(r3)

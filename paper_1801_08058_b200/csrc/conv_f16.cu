@@ -55,8 +55,8 @@ __device__ __forceinline__ void mma_f16_cta(uint32_t tmem_d, uint64_t ad, uint64
 
 // ---------------------------------------------------------------------------
 // Channel maxima (gfb_chsplit_args): block b folds |x| over its share of the
-// P pixel rows, four rows per thread in flight; thread t owns the 4 channels
-// 4 (t % C4) (C4 = C / 4 divides 256).
+// P pixel rows, four rows per thread in flight (thread t owns the 4 channels
+// 4 (t % C4), C4 = C / 4 divides 256), then one atomicMax per channel.
 __global__ void __launch_bounds__(256) gfb_chmax_kernel(const __grid_constant__ gfb_chsplit_args p) {
     using namespace tc;
     __shared__ float4 red[256];
@@ -84,47 +84,27 @@ __global__ void __launch_bounds__(256) gfb_chmax_kernel(const __grid_constant__ 
             const float4 v = red[i];
             m = make_float4(fmaxf(m.x, v.x), fmaxf(m.y, v.y), fmaxf(m.z, v.z), fmaxf(m.w, v.w));
         }
-        reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * p.C)[t] = m;
+        // non-negative floats order like their bit patterns
+        unsigned int* pm = reinterpret_cast<unsigned int*>(part) + 4 * t;
+        atomicMax(pm, __float_as_uint(m.x));
+        atomicMax(pm + 1, __float_as_uint(m.y));
+        atomicMax(pm + 2, __float_as_uint(m.z));
+        atomicMax(pm + 3, __float_as_uint(m.w));
     }
 }
 
-// Channel scales (mode 1, one block per 32 channels: eight warps fold the
-// partial maxima, four loads in flight per thread) and the
-// channel-scaled planes (mode 0, pixel rows streamed four per thread).
+// Channel-scaled planes: the scales from the channel maxima (block 0
+// publishes them for the filter split), pixel rows streamed four per thread.
 __global__ void __launch_bounds__(256) gfb_chsplit_kernel(const __grid_constant__ gfb_chsplit_args p) {
     using namespace tc;
     const int t = threadIdx.x;
-    if (p.mode == 1) {
-        // block: 32 channels (lane), its 8 warps split the partial rows, 4 loads in flight
-        __shared__ float red[8][32];
-        const int lane = t & 31, wp = t >> 5, c = blockIdx.x * 32 + lane;
-        const float* part = resolve<const float>(p.tab, p.partial);
-        float m = 0.f;
-        if (c < p.C) {
-            int b = wp;
-            for (; b + 24 < p.nblocks; b += 32) {
-                float v[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) v[i] = __ldg(part + (int64_t)(b + 8 * i) * p.C + c);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) m = fmaxf(m, v[i]);
-            }
-            for (; b < p.nblocks; b += 8) m = fmaxf(m, __ldg(part + (int64_t)b * p.C + c));
-        }
-        red[wp][lane] = m;
-        __syncthreads();
-        if (wp == 0 && c < p.C) {
-#pragma unroll
-            for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i][lane]);
-            resolve<float>(p.tab, p.sc)[c] = f16_tile_scale(m);
-        }
-        return;
-    }
     const float* src = resolve<const float>(p.tab, p.src);
     __half* hi = resolve<__half>(p.tab, p.hi);
     __half* lo = resolve<__half>(p.tab, p.lo);
     const int C4 = (int)(p.C / 4), g = t % C4, rpi = 256 / C4;
-    const float4 s4 = __ldg(reinterpret_cast<const float4*>(resolve<const float>(p.tab, p.sc)) + g);
+    const float4 m4 = __ldg(reinterpret_cast<const float4*>(resolve<const float>(p.tab, p.partial)) + g);
+    const float4 s4 = make_float4(f16_tile_scale(m4.x), f16_tile_scale(m4.y), f16_tile_scale(m4.z), f16_tile_scale(m4.w));
+    if (blockIdx.x == 0 && t < C4) reinterpret_cast<float4*>(resolve<float>(p.tab, p.sc))[g] = s4;
     auto put = [&](int64_t row, float4 v) {
         uint2 h, l;
         split4_f16(make_float4(__fmul_rn(v.x, s4.x), __fmul_rn(v.y, s4.y), __fmul_rn(v.z, s4.z), __fmul_rn(v.w, s4.w)), h, l);
@@ -149,15 +129,26 @@ __global__ void __launch_bounds__(256) gfb_chsplit_kernel(const __grid_constant_
 __global__ void __launch_bounds__(256) gfb_fsplit_kernel(const __grid_constant__ gfb_fsplit_args p) {
     using namespace tc;
     __shared__ float red[8];
+    __shared__ float isc[1024];  // 1 / s_c (exact: powers of two)
     const float* w = resolve<const float>(p.tab, p.w) + (int64_t)blockIdx.x * p.s_r;
     const float* sc = resolve<const float>(p.tab, p.sc);
     const int K = (int)p.K, e1 = (int)p.e1, e2 = (int)p.e2, t0 = (int)p.t0, t1 = (int)p.t1, t2 = (int)p.t2;
+    for (int c = threadIdx.x; c < e2; c += 256) isc[c] = __frcp_rn(__ldg(sc + c));
+    __syncthreads();
     auto value = [&](int k) {
         const int d2 = k % e2, d01 = k / e2, d1 = d01 % e1, d0 = d01 / e1;
-        return __fmul_rn(__ldg(w + d0 * t0 + d1 * t1 + d2 * t2), __frcp_rn(__ldg(sc + d2)));
+        return __fmul_rn(__ldg(w + d0 * t0 + d1 * t1 + d2 * t2), isc[d2]);
     };
     float m = 0.f;
-    for (int k = threadIdx.x; k < K; k += 256) m = fmaxf(m, fabsf(value(k)));
+    int k = threadIdx.x;
+    for (; k + 768 < K; k += 1024) {  // four gathers in flight
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = value(k + 256 * i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m = fmaxf(m, fabsf(v[i]));
+    }
+    for (; k < K; k += 256) m = fmaxf(m, fabsf(value(k)));
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -169,12 +160,21 @@ __global__ void __launch_bounds__(256) gfb_fsplit_kernel(const __grid_constant__
     if (threadIdx.x == 0) resolve<float>(p.tab, p.inv)[blockIdx.x] = __frcp_rn(t);
     __half* hi = resolve<__half>(p.tab, p.hi) + (int64_t)blockIdx.x * K;
     __half* lo = resolve<__half>(p.tab, p.lo) + (int64_t)blockIdx.x * K;
-    for (int k = threadIdx.x; k < K; k += 256) {
-        const float v = __fmul_rn(value(k), t);
+    auto put = [&](int kk, float x) {
+        const float v = __fmul_rn(x, t);
         const __half h = __float2half_rn(v);
-        hi[k] = h;
-        lo[k] = __float2half_rn(__fsub_rn(v, __half2float(h)));
+        hi[kk] = h;
+        lo[kk] = __float2half_rn(__fsub_rn(v, __half2float(h)));
+    };
+    k = threadIdx.x;
+    for (; k + 768 < K; k += 1024) {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = value(k + 256 * i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) put(k + 256 * i, v[i]);
     }
+    for (; k < K; k += 256) put(k, value(k));
 }
 
 // ---------------------------------------------------------------------------

