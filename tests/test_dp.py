@@ -35,7 +35,10 @@ def _split_inputs(step, arrays, world):
 
 
 def _dp_case(kind, world):
-    if kind == "mlp":
+    if kind == "wide":  # pair-sized layers: the fp16 GEMM, its fused epilogues and bias-gradient partials
+        glob = W.mlp_step(gf, batch=1024, in_dim=256, hidden=(256, 256), out_dim=256)
+        loc = W.mlp_step(gf, batch=1024 // world, in_dim=256, hidden=(256, 256), out_dim=256, loss_batch=1024)
+    elif kind == "mlp":
         glob = W.mlp_step(gf, batch=16, in_dim=12, hidden=(16,), out_dim=5)
         loc = W.mlp_step(gf, batch=16 // world, in_dim=12, hidden=(16,), out_dim=5, loss_batch=16)
     else:
@@ -113,9 +116,12 @@ def test_max_over_batch_is_a_max_allreduce():
         assert G.same_bits(outs[r][0], want.reshape(-1))
 
 
-@pytest.mark.parametrize("kind,world", [("mlp", 2), ("mlp", 4), ("cnn", 2)])
+@pytest.mark.parametrize("kind,world", [("mlp", 2), ("mlp", 4), ("cnn", 2), ("wide", 2)])
 def test_lockstep_ranks_match_global_batch(kind, world):
     loc, h, arrays, want = _dp_case(kind, world)
+    if kind == "wide":
+        f16 = [L for L in h.lowered.launches if L.kind == abi.K_DOT_F16P]
+        assert f16 and any(L.args.epi_flags & 64 for L in f16)  # bias partials feed all-reduced Sums
     specs = [(d.element_type.numpy_dtype, d.element_count) for d, _ in h.result_signature]
     outs = plan_emulator.execute_ranks(h.lowered, _split_inputs(loc, arrays, world), specs)
     for r in range(world):
