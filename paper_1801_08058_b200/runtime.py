@@ -22,9 +22,11 @@ entry point raises `BackendUnavailable`.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
+import weakref
 from collections.abc import Mapping
 from dataclasses import dataclass
 
@@ -387,6 +389,23 @@ def prepare_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
                         param_sig, result_sig, lowered, roots)
 
 
+@contextlib.contextmanager
+def _nvtx(name: str):
+    """NVTX range (visible to nsys / ncu --nvtx); a no-op without torch's NVTX bindings."""
+    try:
+        import torch
+
+        torch.cuda.nvtx.range_push(name)
+        pushed = True
+    except Exception:
+        pushed = False
+    try:
+        yield
+    finally:
+        if pushed:
+            torch.cuda.nvtx.range_pop()
+
+
 def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = "identity",
                      parameter_layouts=None, cuda_graph: bool = True, data_parallel=None,
                      comm=None) -> Executable:
@@ -397,7 +416,7 @@ def compile_function(fn: Function, *, optimize: bool = True, conv_layout: str = 
     from .refcompat import as_function, as_layout, caller_errors, foreign_errors
 
     errors_mod = foreign_errors(fn)
-    with caller_errors(errors_mod):
+    with caller_errors(errors_mod), _nvtx("compile_function"):
         fn = as_function(fn)  # a reference-built graphforge.Function is mirrored node for node
         if parameter_layouts is not None:
             parameter_layouts = [as_layout(lay) for lay in parameter_layouts]
@@ -486,6 +505,10 @@ def to_device(t: TensorValue):
     return host.to("cuda", non_blocking=host.is_pinned())
 
 
+def _forget_pinned(addr):
+    _PINNED.pop(addr, None)
+
+
 def pinned_tensor(et, shape) -> TensorValue:
     """Zero host TensorValue in page-locked memory (fast H2D / D2H DMA)."""
     import torch
@@ -494,16 +517,26 @@ def pinned_tensor(et, shape) -> TensorValue:
     from .layout import identity_layout
 
     buf = torch.zeros(element_count(shape), dtype=torch_dtype(et), pin_memory=True).numpy()
+    if buf.size:
+        _PINNED[buf.ctypes.data] = buf.nbytes  # page-locked for as long as the array lives
+        weakref.finalize(buf, _forget_pinned, buf.ctypes.data)
     return TensorValue(TensorDescriptor(et, tuple(shape)), identity_layout(len(shape)), buf)
+
+
+# host buffers allocated by pinned_tensor (address -> bytes), dropped when freed
+_PINNED: dict = {}
 
 
 def _pinned_host(t: TensorValue, desc) -> bool:
     import torch
 
     b = t.buffer
-    return (not t.is_device and isinstance(b, np.ndarray) and b.flags.c_contiguous and b.size > 0
-            and t.descriptor == desc and b.nbytes == element_count(desc.shape) * desc.element_type.byte_size
-            and torch.from_numpy(b).is_pinned())
+    if not (not t.is_device and isinstance(b, np.ndarray) and b.flags.c_contiguous and b.size > 0
+            and t.descriptor == desc and b.nbytes == element_count(desc.shape) * desc.element_type.byte_size):
+        return False
+    if _PINNED.get(b.ctypes.data, -1) >= b.nbytes:  # one of ours (no driver query per call)
+        return True
+    return torch.from_numpy(b).is_pinned()
 
 
 def _host_run(exe: Executable, inputs: list, out: list, stream) -> bool:
