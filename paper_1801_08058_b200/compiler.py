@@ -2062,6 +2062,7 @@ class Lowering:
         ta = abi.TcArgs(M=m, N=ncols, K=kdim, kp_a=kpa, kp_b=kpb, a_ld_mn=a_mn, b_ld_mn=b_mn,
                         a_sc_r=a_r, a_sc_k=a_k, b_sc_r=b_r, b_sc_k=b_k,
                         group_m=int(os.environ.get("GFB_TC_GROUP_M", "1")))
+        ta.pad[0] = int(os.environ.get("GFB_F16_L2", "0"))  # L2 policy bits (gemm_f16.cu producer): 1 keep A, 2 keep B
         target = chunk(out, ncols)
         if splits > 1:
             kchunks = (kdim + 127) // 128

@@ -185,19 +185,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                     if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
                     const uint32_t bar = full0 + s * 8;
                     const int kc = (int)T.k_begin + kb * BK;
-                    if (p.a_ld_mn > 0) {  // MN-major: (64 MN, 64 K, 2 MN chunks) boxes
+                    if (p.pad[0] & 3) {  // L2 policies per operand (gfb_tc_args.pad[0]: bit 0 keep A, bit 1 keep B)
+                        const uint64_t pa = l2_policy(p.pad[0] & 1), pb = l2_policy(p.pad[0] & 2);
+                        if (p.a_ld_mn > 0) {
+                            tma_load_3d_pair_hint(st, p.tmap[0], 0, kc, am >> 6, bar, pa);
+                            tma_load_3d_pair_hint(st + A_BYTES, p.tmap[1], 0, kc, am >> 6, bar, pa);
+                        } else {
+                            tma_load_2d_pair_hint(st, p.tmap[0], kc, am, bar, pa);
+                            tma_load_2d_pair_hint(st + A_BYTES, p.tmap[1], kc, am, bar, pa);
+                        }
+                        if (p.b_ld_mn > 0) {
+                            tma_load_3d_pair_hint(st + 2 * A_BYTES, p.tmap[2], 0, kc, bn >> 6, bar, pb);
+                            tma_load_3d_pair_hint(st + 2 * A_BYTES + B_BYTES, p.tmap[3], 0, kc, bn >> 6, bar, pb);
+                        } else {
+                            tma_load_2d_pair_hint(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar, pb);
+                            tma_load_2d_pair_hint(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar, pb);
+                        }
+                    } else if (p.a_ld_mn > 0) {  // MN-major: (64 MN, 64 K, 2 MN chunks) boxes
                         tma_load_3d_pair(st, p.tmap[0], 0, kc, am >> 6, bar);
                         tma_load_3d_pair(st + A_BYTES, p.tmap[1], 0, kc, am >> 6, bar);
                     } else {
                         tma_load_2d_pair(st, p.tmap[0], kc, am, bar);
                         tma_load_2d_pair(st + A_BYTES, p.tmap[1], kc, am, bar);
                     }
-                    if (p.b_ld_mn > 0) {
-                        tma_load_3d_pair(st + 2 * A_BYTES, p.tmap[2], 0, kc, bn >> 6, bar);
-                        tma_load_3d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], 0, kc, bn >> 6, bar);
-                    } else {
-                        tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
-                        tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+                    if (!(p.pad[0] & 3)) {
+                        if (p.b_ld_mn > 0) {
+                            tma_load_3d_pair(st + 2 * A_BYTES, p.tmap[2], 0, kc, bn >> 6, bar);
+                            tma_load_3d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], 0, kc, bn >> 6, bar);
+                        } else {
+                            tma_load_2d_pair(st + 2 * A_BYTES, p.tmap[2], kc, bn, bar);
+                            tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, p.tmap[3], kc, bn, bar);
+                        }
                     }
                 }
             }

@@ -107,6 +107,32 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, in
         "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster)
         : "memory");
 }
+// The same loads with an L2 cache policy (createpolicy: evict_first for a
+// streamed operand, evict_last for one every tile re-reads).
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t p;
+    if (keep)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const void* tmap, int c0, int c1, uint32_t bar_cluster,
+                                                      uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_hint(void* dst, const void* tmap, int c0, int c1, int c2, uint32_t bar_cluster,
+                                                      uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(
+            su32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, int c0, int c1, int c2, uint32_t bar_cluster) {
     asm volatile(
         "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
