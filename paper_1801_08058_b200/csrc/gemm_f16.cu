@@ -348,6 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
             const int64_t prow = rowA + lane, colb = T.n0 + cg * EC;
             const bool rok = prow < p.M;
             const bool coalesced = p.c_sn == 1 && (p.c_sm & 3) == 0 && (p.N & 3) == 0;
+            bool released = false;
             if (!coalesced) {
                 if (p.epi_kind != 0 || (p.epi_flags & 4)) __trap();  // the lowering fuses epilogues into dense outputs only
 #pragma unroll 1
@@ -471,20 +472,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                 const bool c_pass2 = store_c && p.epi_kind != 1;  // C == y
                 float* csum = (p.epi_flags & 64) ? resolve<float>(p.tab, p.e_csum) + (rowA >> 5) * p.N : nullptr;
                 if (c_pass2 || planes || csum) {
+                    // y back into registers, then the TMEM buffer goes back to the MMA
+                    // warp before the stores: the next tile's MMAs overlap them
+                    float yv[EC];
+#pragma unroll
+                    for (int c = 0; c < EC / 16; ++c) tmem_ld16(tsum + c * 16, &yv[c * 16]);
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b_last * 8) : "memory");
+                    released = true;
                     float* xt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
                     const int qd = lane & 7;
 #pragma unroll
                     for (int c = 0; c < EC / 32; ++c) {
-                        float v[16];
                         // lane r writes its row's 32 values as 8 swizzled 16-byte pieces
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            tmem_ld16(tsum + c * 32 + 16 * h, v);
-#pragma unroll
-                            for (int d = 0; d < 4; ++d)
-                                *reinterpret_cast<float4*>(xt + lane * 32 + (((4 * h + d) ^ (lane & 7)) << 2)) =
-                                    make_float4(v[4 * d], v[4 * d + 1], v[4 * d + 2], v[4 * d + 3]);
-                        }
+                        for (int d = 0; d < 8; ++d)
+                            *reinterpret_cast<float4*>(xt + lane * 32 + ((d ^ (lane & 7)) << 2)) =
+                                make_float4(yv[c * 32 + 4 * d], yv[c * 32 + 4 * d + 1], yv[c * 32 + 4 * d + 2], yv[c * 32 + 4 * d + 3]);
                         __syncwarp();
                         const int64_t col = colb + c * 32 + 4 * qd;
                         float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // this lane's rows, in order
@@ -517,11 +523,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::HCfg::THREADS, 1
                     }
                 }
             }
-            // release the staged buffer to the MMA warp
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b_last * 8) : "memory");
+            if (!released) {  // release the staged buffer to the MMA warp
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b_last * 8) : "memory");
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
