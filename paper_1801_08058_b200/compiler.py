@@ -833,6 +833,7 @@ class Lowering:
 
         self._csum_done = set()
         self._f16_chunks = {}   # caller input key -> its row chunks' plane views (_f16_planes)
+        self._row_chunked = {}  # tensor key -> row chunks its fp16 planes were written in (chunked epilogues)
         self._epi_planes = set()  # tensors whose fp16 planes a GEMM epilogue writes
         self._epi = self._plan_epilogues()
         self._epi_nodes = {m for sp in self._epi.values() for m in sp["absorbed"]}
@@ -908,6 +909,7 @@ class Lowering:
 
         if self.allreduce:
             self._bucket_allreduces()
+        self._interleave_row_chunks()
         self._hoist_result_writers()
 
         # results that are parameters / constants / repeated: copy launches
@@ -953,6 +955,59 @@ class Lowering:
             buffers[region.key] = region
         return Lowered(self.launches, plan.arena_size, bytes(const_blob), self.n_in, self.n_out,
                        buffers, arena_offsets=plan.offsets)
+
+    def _interleave_row_chunks(self):
+        """Chunk-major order for the row-chunked launches (a large input's
+        split chunks and the GEMMs of every layer that follows them): chunk
+        c's path through all the layers runs as soon as its input piece has
+        arrived, while the later pieces cross PCIe.  A list schedule over the
+        span from the first to the last chunk launch: each step places the
+        ready launch of the smallest chunk index (a launch without one takes
+        the smallest chunk index of the chunk launches that depend on it)."""
+        idx = [i for i, L in enumerate(self.launches) if getattr(L, "row_chunk", None) is not None]
+        if not idx or os.environ.get("GFB_CHUNK_MAJOR", "1") != "1":
+            return
+        lo, hi = idx[0], idx[-1] + 1
+        span = self.launches[lo:hi]
+        by_key = {b.key: b for b in self.buf.values()}
+
+        def extents(keys, write):
+            out = []
+            for k in keys:
+                b = by_key.get(k)
+                if b is None:
+                    out.append((("?", k), 0, 1 << 62, write))
+                elif b.exact and b.base is not None:
+                    a0 = b.elem_off * b.et.byte_size
+                    out.append((b.base.key, a0, a0 + b.nbytes, write))
+                else:
+                    root = b.base if b.base is not None else b
+                    out.append((root.key, 0, 1 << 62, write))
+            return out
+
+        acc = [extents(L.reads, False) + extents(L.writes, True) for L in span]
+
+        def conflict(a, b):
+            return any((wa or wb) and ka == kb and la < hb and lb < ha for ka, la, ha, wa in a for kb, lb, hb, wb in b)
+
+        n = len(span)
+        deps = [[j for j in range(i) if conflict(acc[i], acc[j])] for i in range(n)]
+        key = [getattr(L, "row_chunk", None) for L in span]
+        users = [[] for _ in range(n)]
+        for i in range(n):
+            for j in deps[i]:
+                users[j].append(i)
+        for i in range(n - 1, -1, -1):  # a launch takes the earliest chunk that needs it
+            if key[i] is None:
+                ks = [key[u] for u in users[i] if key[u] is not None]
+                key[i] = min(ks) if ks else 1 << 30
+        placed, order = [False] * n, []
+        for _ in range(n):
+            ready = [i for i in range(n) if not placed[i] and all(placed[j] for j in deps[i])]
+            i = min(ready, key=lambda t: (key[t], t))
+            placed[i] = True
+            order.append(i)
+        self.launches[lo:hi] = [span[i] for i in order]
 
     def _hoist_result_writers(self):
         """Move each launch that writes a caller result (the optimizer
@@ -1781,18 +1836,32 @@ class Lowering:
                 addr = {"c_sm": out.strides[0], "c_sn": out.strides[1]}
                 root = ab.base if ab.base is not None else ab
                 chunks = self._f16_chunks.get(root.key) if a16[4] == 0 else None
+                if a16[4] == 0 and chunks is None and root.key in self._row_chunked:
+                    # A's planes were written row chunk by row chunk by the previous
+                    # layer's GEMM: this layer follows the same chunks (the forward
+                    # pipelines with the input's row pieces)
+                    hi, lo, sc = a16[:3]
+                    tcn = (k + 127) // 128
+                    chunks = [[r0, r1, self._row_view(hi, r0, r1, k // 2), self._row_view(lo, r0, r1, k // 2),
+                               self._row_view(sc, r0 // 128, r1 // 128, tcn), None] for r0, r1 in self._row_chunked[root.key]]
                 epi = self._epi.get(n, {})
                 self._flush_chunks(bb)
-                if (chunks and chunks[0][5] is not None and self._tc_splits(chunks[0][1] - chunks[0][0], nn, k) == 1
+                if (chunks and self._tc_splits(chunks[0][1] - chunks[0][0], nn, k) == 1 and k % 2 == 0
+                        and (chunks[0][5] is not None or root.key in self._row_chunked)
                         and "colsum" not in epi and out.strides == (nn, 1) and not out.elem_off and out.base is None):
-                    for ch in chunks:  # split chunk c, then the GEMM over its rows (one chain)
+                    for c, ch in enumerate(chunks):  # split chunk c (an input), then the GEMM over its rows
                         r0, r1, hv, lv, sv, split = ch
-                        split.chain = ("rows", n)
+                        if split is not None:
+                            split.chain, split.row_chunk = ("rows",), c
                         self._emit_chunk(ch)
                         rec = self._f16_gemm(n, (hv, lv, sv) + a16[3:], b16, out, r1 - r0, nn, k, addr,
                                              f"dot_f16#{n}:rows{r0}", rows=(r0, m))
                         rec.algo_bytes = ((r1 - r0) * k + k * nn + (r1 - r0) * nn) * 4
-                        rec.chain = ("rows", n)
+                        rec.chain, rec.row_chunk = ("rows",), c  # one chain: persistent GEMMs never overlap
+                        if rec.args.epi_flags & 4 and epi:
+                            y = self.buf[epi["lo_of"]]
+                            yroot = y.base if y.base is not None else y
+                            self._row_chunked[yroot.key] = [(ch_[0], ch_[1]) for ch_ in chunks]
                     return
                 self._flush_chunks(ab)
                 rec = self._f16_gemm(n, a16, b16, out, m, nn, k, addr, f"dot_f16#{n}")
@@ -2004,9 +2073,9 @@ class Lowering:
         return planes
 
     def _input_chunks(self, root, R, Cc) -> int:
-        """Row chunks of a caller input's fp16 split (GFB_INPUT_CHUNKS, 8):
+        """Row chunks of a caller input's fp16 split (GFB_INPUT_CHUNKS, 4):
         inputs of at least 256 MB whose rows split into whole 256-row tiles."""
-        nch = int(os.environ.get("GFB_INPUT_CHUNKS", "8"))
+        nch = int(os.environ.get("GFB_INPUT_CHUNKS", "4"))
         min_mb = float(os.environ.get("GFB_INPUT_CHUNK_MIN_MB", "256"))
         if (nch <= 1 or not (abi.SLOT_IO <= root.slot < abi.SLOT_IO + self.n_in) or R * Cc * 4 < min_mb * (1 << 20)
                 or R % (nch * 256) or Cc % 8):

@@ -392,7 +392,10 @@ def test_input_row_chunks_emulated(monkeypatch):
     h = host_compile(st.fn)
     labels = [L.label for L in h.lowered.launches]
     assert sum(lb.startswith("split16#") and ":rows" in lb for lb in labels) == 4, labels
-    assert sum(lb.startswith("dot_f16#") and ":rows" in lb for lb in labels) == 4, labels
+    # both layers follow the input's row chunks, in chunk-major order
+    assert sum(lb.startswith("dot_f16#") and ":rows" in lb for lb in labels) == 8, labels
+    chunked = [lb for lb in labels if ":rows" in lb]
+    assert [lb.split(":rows")[1].split(":")[0] for lb in chunked] == [r for r in ("0", "512", "1024", "1536") for _ in range(3)]
     chunked = emulate(h, tens)
     monkeypatch.setenv("GFB_INPUT_CHUNKS", "1")
     plain = emulate(host_compile(st.fn), tens)
