@@ -156,7 +156,7 @@ F16_SMEM_PAIR = TC_SMEM_PAIR  # gemm_f16.cu HCfg::SMEM_BYTES: same 64 KB stages 
 TCX_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 32 * 4 + 256 + 1024 for bn in (64, 128)}
 TCXH_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 64 * 2 + 256 + 1024 for bn in (64, 128)}  # conv_f16.cu HXCfg
 TCGWH_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 64 * 2 + 256 + 1024 for bn in (64, 128)}  # conv_f16.cu HWCfg
-CHMAX_BLOCKS = 296
+CHMAX_BLOCKS = 2 * 148  # channel-max blocks: more only adds atomicMax contention
 STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
 STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
 TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
@@ -2503,14 +2503,15 @@ class Lowering:
         r0 = LaunchRec(abi.K_MEMSET, (1, 1, 1), (1, 1, 1), 0, a0, [], [part.key], f"memset#{root.key}")
         r0.finalize = _finalize_refs(a0, {"buf": part})
         self.launches.append(r0)
-        a1 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS)
-        r1 = LaunchRec(abi.K_CHMAX, (CHMAX_BLOCKS, 1, 1), (256, 1, 1), 0, a1, [xb.key, part.key], [part.key],
+        nb = max(1, min(CHMAX_BLOCKS, (P * (C // 4)) // (256 * 16)))  # >= 16 rows of float4 per thread
+        a1 = abi.ChsplitArgs(P=P, C=C, nblocks=nb)
+        r1 = LaunchRec(abi.K_CHMAX, (nb, 1, 1), (256, 1, 1), 0, a1, [xb.key, part.key], [part.key],
                        f"chmax#{root.key}")
         r1.algo_bytes = P * C * 4
         r1.finalize = _finalize_refs(a1, {"src": xb, "partial": part})
         self.launches.append(r1)
         a3 = abi.ChsplitArgs(P=P, C=C, nblocks=CHMAX_BLOCKS)
-        grid = max(1, min(NUM_SMS * 4, (P * (C // 4) + 255) // 256))
+        grid = max(1, min(NUM_SMS * 8, (P * (C // 4) + 255) // 256))
         r3 = LaunchRec(abi.K_CHSPLIT, (grid, 1, 1), (256, 1, 1), 0, a3, [xb.key, part.key], [sc.key, hi.key, lo.key],
                        f"chsplit#{root.key}")
         r3.algo_bytes = P * C * 8

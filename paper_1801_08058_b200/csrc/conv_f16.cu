@@ -55,7 +55,7 @@ __device__ __forceinline__ void mma_f16_cta(uint32_t tmem_d, uint64_t ad, uint64
 
 // ---------------------------------------------------------------------------
 // Channel maxima (gfb_chsplit_args): block b folds |x| over its share of the
-// P pixel rows, four rows per thread in flight (thread t owns the 4 channels
+// P pixel rows, eight rows per thread in flight (thread t owns the 4 channels
 // 4 (t % C4), C4 = C / 4 divides 256), then one atomicMax per channel.
 __global__ void __launch_bounds__(256) gfb_chmax_kernel(const __grid_constant__ gfb_chsplit_args p) {
     using namespace tc;
@@ -69,12 +69,12 @@ __global__ void __launch_bounds__(256) gfb_chmax_kernel(const __grid_constant__ 
         m = make_float4(fmaxf(m.x, fabsf(v.x)), fmaxf(m.y, fabsf(v.y)), fmaxf(m.z, fabsf(v.z)), fmaxf(m.w, fabsf(v.w)));
     };
     int64_t row = r0 + t / C4;
-    for (; row + 3 * rpi < r1; row += 4 * rpi) {
-        float4 v[4];
+    for (; row + 7 * rpi < r1; row += 8 * rpi) {
+        float4 v[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src + (row + i * rpi) * p.C) + g);
+        for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src + (row + i * rpi) * p.C) + g);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) fold(v[i]);
+        for (int i = 0; i < 8; ++i) fold(v[i]);
     }
     for (; row < r1; row += rpi) fold(__ldg(reinterpret_cast<const float4*>(src + row * p.C) + g));
     red[t] = m;
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) gfb_chmax_kernel(const __grid_constant__ 
 }
 
 // Channel-scaled planes: the scales from the channel maxima (block 0
-// publishes them for the filter split), pixel rows streamed four per thread.
+// publishes them for the filter split), pixel rows streamed eight per thread.
 __global__ void __launch_bounds__(256) gfb_chsplit_kernel(const __grid_constant__ gfb_chsplit_args p) {
     using namespace tc;
     const int t = threadIdx.x;
@@ -114,12 +114,12 @@ __global__ void __launch_bounds__(256) gfb_chsplit_kernel(const __grid_constant_
     };
     const int64_t stride = (int64_t)gridDim.x * rpi;
     int64_t row = (int64_t)blockIdx.x * rpi + t / C4;
-    for (; row + 3 * stride < p.P; row += 4 * stride) {
-        float4 v[4];
+    for (; row + 7 * stride < p.P; row += 8 * stride) {
+        float4 v[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src + (row + i * stride) * p.C) + g);
+        for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(src + (row + i * stride) * p.C) + g);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) put(row + i * stride, v[i]);
+        for (int i = 0; i < 8; ++i) put(row + i * stride, v[i]);
     }
     for (; row < p.P; row += stride) put(row, __ldg(reinterpret_cast<const float4*>(src + row * p.C) + g));
 }

@@ -116,8 +116,12 @@ def test_max_over_batch_is_a_max_allreduce():
         assert G.same_bits(outs[r][0], want.reshape(-1))
 
 
-@pytest.mark.parametrize("kind,world", [("mlp", 2), ("mlp", 4), ("cnn", 2), ("wide", 2)])
-def test_lockstep_ranks_match_global_batch(kind, world):
+@pytest.mark.parametrize("kind,world", [("mlp", 2), ("mlp", 4), ("cnn", 2), ("wide", 2), ("wide-chunked", 2)])
+def test_lockstep_ranks_match_global_batch(kind, world, monkeypatch):
+    if kind == "wide-chunked":  # each rank's x split and multiplied in row chunks, chunk-major forward
+        monkeypatch.setenv("GFB_INPUT_CHUNK_MIN_MB", "0.1")
+        monkeypatch.setenv("GFB_INPUT_CHUNKS", "2")
+        kind = "wide"
     loc, h, arrays, want = _dp_case(kind, world)
     if kind == "wide":
         f16 = [L for L in h.lowered.launches if L.kind == abi.K_DOT_F16P]
