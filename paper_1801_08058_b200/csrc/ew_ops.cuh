@@ -240,6 +240,22 @@ __device__ __forceinline__ void apply_unary_c(T (&a)[V]) {
     }
 }
 
+// Row-fused launches (rowfuse.py): F32 Exp / Log in single precision (CUDA
+// expf / logf, <= 2 / 1 ulp -- inside the 1e-5 transcendental contract of
+// SURVEY.md §8(c), not bit-identical to the reference's double evaluation).
+// A softmax row group is then bound by HBM instead of the FP64 pipe.
+// Special values as the reference's: exp overflow -> inf, log(0) = -inf,
+// log(x < 0) = NaN, NaN in -> NaN out.
+template <uint32_t OP, typename T, int V>
+__device__ __forceinline__ void apply_unary_row(T (&a)[V]) {
+    if constexpr (std::is_same<T, float>::value && (OP == OP_EXP || OP == OP_LOG)) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[v] = OP == OP_EXP ? expf(a[v]) : logf(a[v]);
+    } else {
+        apply_unary_c<OP, T, V>(a);
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ T bin1(uint32_t op, T x, T y) {
     if constexpr (std::is_same<T, float>::value) {

@@ -307,6 +307,7 @@ def splat_bits(et: ElementType, value) -> int:
 def generate_source(spec: RowSpec) -> str:
     """CUDA C of a row group's kernel (entry `gfb_jit_ew`, like jit.py's)."""
     T, TEAM, BLOCK, VEC, C, R = spec.dtype, spec.team, spec.block, spec.vec, spec.C, spec.R
+    ufn = "row" if os.environ.get("GFB_ROW_F32_TRANSCENDENTALS", "0") == "1" else "c"  # (off: the reference's bits)
     NSLOT = (C + TEAM * VEC - 1) // (TEAM * VEC)
     EPT = NSLOT * VEC
     full_rows = C % (TEAM * VEC) == 0
@@ -349,7 +350,7 @@ def generate_source(spec: RowSpec) -> str:
         elif e[0] == "loadu":
             L.append(f"const T v{k} = P{e[1]}[0];")
         elif e[0] == "un":
-            L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary_c<{e[1]}u, T, 1>(v{k}_); const T v{k} = v{k}_[0];")
+            L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary_{ufn}<{e[1]}u, T, 1>(v{k}_); const T v{k} = v{k}_[0];")
         elif e[0] == "bin":
             L.append(f"const T v{k} = bin1<T>({e[1]}u, v{e[2]}, v{e[3]});")
         else:
@@ -380,7 +381,7 @@ def generate_source(spec: RowSpec) -> str:
             elif op == "bcast":  # a ROWV / UNI value across the columns
                 L.append(f"T v{k}[EPT]; _Pragma(\"unroll\") for (int i = 0; i < EPT; ++i) v{k}[i] = v{e[1]};")
             elif op == "un":
-                L.append(f"T v{k}[EPT]; copyV<T, EPT>(v{k}, v{e[2]}); apply_unary_c<{e[1]}u, T, EPT>(v{k});")
+                L.append(f"T v{k}[EPT]; copyV<T, EPT>(v{k}, v{e[2]}); apply_unary_{ufn}<{e[1]}u, T, EPT>(v{k});")
             elif op == "bin":
                 L.append(f"T v{k}[EPT]; _Pragma(\"unroll\") for (int i = 0; i < EPT; ++i) v{k}[i] = bin1<T>({e[1]}u, v{e[2]}[i], v{e[3]}[i]);")
             else:
@@ -391,7 +392,7 @@ def generate_source(spec: RowSpec) -> str:
             elif op == "bcast":
                 L.append(f"const T v{k} = v{e[1]};")
             elif op == "un":
-                L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary_c<{e[1]}u, T, 1>(v{k}_); const T v{k} = v{k}_[0];")
+                L.append(f"T v{k}_[1] = {{v{e[2]}}}; apply_unary_{ufn}<{e[1]}u, T, 1>(v{k}_); const T v{k} = v{k}_[0];")
             elif op == "bin":
                 L.append(f"const T v{k} = bin1<T>({e[1]}u, v{e[2]}, v{e[3]});")
             elif op == "rred":
