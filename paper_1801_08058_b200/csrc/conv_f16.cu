@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) gfb_chmax_kernel(const __grid_constant__ 
     const int64_t per = (p.P + gridDim.x - 1) / gridDim.x, r0 = (int64_t)blockIdx.x * per, r1 = min(p.P, r0 + per);
     float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
     auto fold = [&](float4 v) {
-        m = make_float4(fmaxf(m.x, fabsf(v.x)), fmaxf(m.y, fabsf(v.y)), fmaxf(m.z, fabsf(v.z)), fmaxf(m.w, fabsf(v.w)));
+        m = make_float4(fmaxf(m.x, fin_abs(v.x)), fmaxf(m.y, fin_abs(v.y)), fmaxf(m.z, fin_abs(v.z)), fmaxf(m.w, fin_abs(v.w)));
     };
     int64_t row = r0 + t / C4;
     for (; row + 7 * rpi < r1; row += 8 * rpi) {
@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(256) gfb_fsplit_kernel(const __grid_constant__
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[i] = value(k + 256 * i);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) m = fmaxf(m, fabsf(v[i]));
+        for (int i = 0; i < 4; ++i) m = fmaxf(m, fin_abs(v[i]));
     }
-    for (; k < K; k += 256) m = fmaxf(m, fabsf(value(k)));
+    for (; k < K; k += 256) m = fmaxf(m, fin_abs(value(k)));
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;

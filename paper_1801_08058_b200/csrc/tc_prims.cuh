@@ -247,8 +247,12 @@ __device__ __forceinline__ void split4_f16(float4 v, uint2& hi, uint2& lo) {
 __device__ __forceinline__ float4 scale4(float4 v, float s) {
     return make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
 }
+// |x| for the scale maxima: infinities (and NaN, which fmaxf drops) do not
+// count, so a tile holding an inf keeps the scale of its finite values (inf
+// * s stays inf; with scale 1 its finite neighbours could overflow fp16)
+__device__ __forceinline__ float fin_abs(float x) { return fabsf(x) < INFINITY ? fabsf(x) : 0.f; }
 __device__ __forceinline__ float amax4(float m, float4 v) {
-    return fmaxf(fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+    return fmaxf(fmaxf(m, fmaxf(fin_abs(v.x), fin_abs(v.y))), fmaxf(fin_abs(v.z), fin_abs(v.w)));
 }
 // 16 TMEM columns of this warp's 32 lanes (one per thread), fp32
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {

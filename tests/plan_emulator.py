@@ -377,7 +377,8 @@ def _f16_split(y, R, Cc):
         for i in range(tr):
             for j in range(tc):
                 blk = y[128 * i:128 * (i + 1), 128 * j:128 * (j + 1)]
-                sc[i, j] = _f16_scale(np.abs(blk).max() if blk.size else 0.0)
+                fin = np.abs(blk)[np.isfinite(blk)]  # the scale counts finite values only
+                sc[i, j] = _f16_scale(fin.max() if fin.size else 0.0)
                 full[128 * i:128 * (i + 1), 128 * j:128 * (j + 1)] = sc[i, j]
         v = (y * full).astype(np.float32)
         hi = v.astype(np.float16)
@@ -559,7 +560,8 @@ def _ch_scale_vec(m):
 def run_chmax(mem, a):
     x = mem.view(a.src, np.float32)[: a.P * a.C].reshape(a.P, a.C)
     part = mem.view(a.partial, np.float32)
-    part[: a.C] = np.maximum(part[: a.C], np.abs(x).max(axis=0))
+    ax = np.where(np.isfinite(x), np.abs(x), 0)
+    part[: a.C] = np.maximum(part[: a.C], ax.max(axis=0))
 
 
 def run_chsplit(mem, a):
@@ -582,7 +584,7 @@ def run_fsplit(mem, a):
     d1, d0 = d01 % a.e1, d01 // a.e1
     rows = np.arange(a.rows, dtype=np.int64)[:, None]
     b = (w[rows * a.s_r + (d0 * a.t0 + d1 * a.t1 + d2 * a.t2)[None, :]] / sc[d2][None, :]).astype(np.float32)
-    t = _ch_scale_vec(np.abs(b).max(axis=1))
+    t = _ch_scale_vec(np.where(np.isfinite(b), np.abs(b), 0).max(axis=1))
     v = (b * t[:, None]).astype(np.float32)
     hi = v.astype(np.float16)
     lo = (v - hi.astype(np.float32)).astype(np.float16)

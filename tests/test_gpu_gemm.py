@@ -449,3 +449,28 @@ def test_conv_tcgwh_matches_oracle(monkeypatch, shape, pad):
     out = gf.call(exe, [gf.tensor_from_flat(F32, v.shape, v) for v in ins])[0].to_numpy()
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+def test_f16_dot_special_values():
+    """inf / NaN operands on the fp16 GEMM: the scales count finite values
+    only, so exactly the outputs the reference makes non-finite are
+    non-finite, and every other output stays within the Dot contract.  (An
+    inf operand can give NaN where the reference has +-inf: the split's
+    cross products multiply it by a zero lo part -- as in the 3xTF32
+    kernel.)"""
+    m, k, n = 512, 512, 512
+    fn = _dot_graph(m, k, n)
+    rng = np.random.default_rng(31)
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32) * np.float32(1e3)
+    b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    a[5, 7] = np.inf
+    a[300, 2] = np.nan
+    b[9, 400] = -np.inf
+    out = gf.call(gf.compile_function(fn), [gf.tensor_from_flat(F32, a.shape, a), gf.tensor_from_flat(F32, b.shape, b)])[0]
+    out = out.to_numpy()
+    with np.errstate(all="ignore"):
+        ref = a.astype(np.float64) @ b.astype(np.float64)
+    bad = ~np.isfinite(ref)
+    assert np.array_equal(~np.isfinite(out), bad)
+    good = ~bad
+    assert G.normwise(out[good], ref[good]) <= 1e-6
