@@ -99,6 +99,8 @@ enum {
     GFB_K_CONV_TCGWH64 = 41,  /* 2xFP16 weight gradient on TMA boxes of the fp16 planes of x and dy, 128x64 (gfb_tcgwh_args) */
     GFB_K_CONV_TCGWH128 = 42, /* as GFB_K_CONV_TCGWH64 with 128x128 tiles */
     GFB_K_MEMSET = 43,        /* zero a byte range of the arena (gfb_memset_args; a memset node of the graph) */
+    GFB_K_CONV_STEMH = 44,    /* few-channel forward conv in 2xFP16: 4x32 pixel tiles built from a shared-memory
+                                 input patch, filter split in the prologue (gfb_stemh_args) */
     GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
                              always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
                              entry only traps */
@@ -361,6 +363,25 @@ typedef struct GFB_ALIGN64 {
     int64_t pad[8];
     uint64_t tmap[4][16];
 } gfb_tcgwh_args;
+
+/* Few-channel forward convolution in 2xFP16 (the 3-channel ResNet stem,
+ * stride 1): GEMM row (n, y, x) over (*, Y, X), K index k = (r, s, c) over
+ * (R, S, C), K = R S C <= 192, reads x[n, c, y + oy + r, x + ox + s] through
+ * the element strides xs0..xs3 (along n, c, h, w; zero outside [0, H) x
+ * [0, W)) and the filter w[col, c, r, s] through ws0..ws3 (along the output
+ * channel, c, r, s); N <= 64 output channels.  Each 4 x 32 pixel tile takes
+ * its own power-of-two activation scale, each filter row its own; both are
+ * undone in the epilogue.  Output row (n, y, x), column j at n * c_s_hi +
+ * y * c_sm + x * c_s_lo + j * c_sn. */
+typedef struct {
+    const void* const* tab;
+    uint64_t c, a, w; /* GFB_REF */
+    int64_t M, N, K;
+    int64_t c_s_hi, c_sm, c_s_lo, c_sn;
+    int64_t xs0, xs1, xs2, xs3;
+    int64_t ws0, ws1, ws2, ws3;
+    int32_t Y, X, oy, ox, H, W, S, C;
+} gfb_stemh_args;
 
 /* fp16 split of a dense F32 matrix [rows, cols] (row pitch ld elements, cols % 8 == 0):
  * per 128 x 128 tile, s = 2^(14 - floor(log2(max |x|))) (1 for an all-zero tile),

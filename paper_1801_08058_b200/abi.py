@@ -20,6 +20,7 @@ K_DOT_F16P, K_SPLIT_F16 = 34, 35
 K_CHMAX, K_CHSPLIT, K_FSPLIT, K_CONV_TCXH64, K_CONV_TCXH128 = 36, 37, 38, 39, 40
 K_CONV_TCGWH64, K_CONV_TCGWH128 = 41, 42
 K_MEMSET = 43
+K_CONV_STEMH = 44
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25
@@ -181,6 +182,18 @@ class TcgArgs(C.Structure):
     ]
 
 
+class StemhArgs(C.Structure):
+    _fields_ = [
+        ("tab", C.c_void_p), ("c", C.c_uint64), ("a", C.c_uint64), ("w", C.c_uint64),
+        ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
+        ("c_s_hi", C.c_int64), ("c_sm", C.c_int64), ("c_s_lo", C.c_int64), ("c_sn", C.c_int64),
+        ("xs0", C.c_int64), ("xs1", C.c_int64), ("xs2", C.c_int64), ("xs3", C.c_int64),
+        ("ws0", C.c_int64), ("ws1", C.c_int64), ("ws2", C.c_int64), ("ws3", C.c_int64),
+        ("Y", C.c_int32), ("X", C.c_int32), ("oy", C.c_int32), ("ox", C.c_int32),
+        ("H", C.c_int32), ("W", C.c_int32), ("S", C.c_int32), ("C", C.c_int32),
+    ]
+
+
 class TcxArgs(C.Structure):
     # 64-byte aligned in C: tmap sits at offset 256, size 640.
     _fields_ = [
@@ -277,5 +290,5 @@ class Plan(C.Structure):
 
 STRUCTS = {
     "gfb_digit": Digit, "gfb_leaf": Leaf, "gfb_ew_args": EwArgs, "gfb_dot_args": DotArgs,
-    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tcgwh_args": TcgwhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_memset_args": MemsetArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
+    "gfb_conv_args": ConvArgs, "gfb_split_args": SplitArgs, "gfb_split16_args": Split16Args, "gfb_chsplit_args": ChsplitArgs, "gfb_fsplit_args": FsplitArgs, "gfb_tcxh_args": TcxhArgs, "gfb_tcgwh_args": TcgwhArgs, "gfb_tc_args": TcArgs, "gfb_tcg_args": TcgArgs, "gfb_stemh_args": StemhArgs, "gfb_tcx_args": TcxArgs, "gfb_tcgg_args": TcggArgs, "gfb_tcgw_args": TcgwArgs, "gfb_allreduce_args": AllReduceArgs, "gfb_memset_args": MemsetArgs, "gfb_row_args": RowArgs, "gfb_launch": Launch, "gfb_plan": Plan,
 }

@@ -159,6 +159,7 @@ TCGWH_SMEM = {bn: (3 if bn == 128 else 4) * (2 * 128 + 2 * bn) * 64 * 2 + 256 + 
 CHMAX_BLOCKS = 2 * 148  # channel-max blocks: more only adds atomicMax contention
 STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
 STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
+STEMH_SMEM = 4 * 32768 + 3 * 2 * 8192 + 32768 + 2 * 1536 * 4 + 3 * 64 * 4 + (16 + 64 + 16) * 4 + 256 + 1024  # conv_f16.cu HSCfg
 TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
 TCGW_SMEM = {64: 3 * (2 * 16384 + 2 * 8192) + 3 * (16384 + 8192) + 1280,
              128: 2 * (2 * 16384 + 2 * 16384) + 2 * (16384 + 16384) + 1280}  # WCfg::SMEM_BYTES
@@ -2655,6 +2656,20 @@ class Lowering:
         rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "b_hi": bhi, "b_lo": blo})
         self.launches.append(rec)
 
+    def _conv_stemh(self, n, xb, xs, yb, ys, out, m, ncols, kdim, geo, label):
+        """Few-channel forward convolution in 2xFP16 on conv_f16.cu
+        gfb_conv_stemh_kernel (persistent over 4x32 output-pixel tiles; reads
+        x and the fp32 filter directly, no split launches)."""
+        ta = abi.StemhArgs(M=m, N=ncols, K=kdim, xs0=xs[0], xs1=xs[1], xs2=xs[2], xs3=xs[3],
+                           ws0=ys[0], ws1=ys[1], ws2=ys[2], ws3=ys[3], **geo)
+        tiles = (m // (geo["Y"] * geo["X"])) * ((geo["Y"] + 3) // 4) * ((geo["X"] + 31) // 32)
+        grid = (max(1, min(tiles, NUM_SMS)), 1, 1)
+        rec = LaunchRec(abi.K_CONV_STEMH, grid, (STEM_THREADS, 1, 1), STEMH_SMEM, ta, [xb.key, yb.key], [out.key], label)
+        rec.flops = 2 * m * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "w": yb})
+        self.launches.append(rec)
+
     def _conv_tcg(self, n, xb, xs, b, out, m, ncols, kdim, geo, addr, yb, label):
         """Conv2D / ConvBackpropData with the activation gather and TF32
         split inside the tensor-core kernel (gemm_tc.cu, gfb_conv_tcg_kernel)."""
@@ -2742,6 +2757,18 @@ class Lowering:
             m, ncols, kdim = N * Ho * Wo, K, Cc * R * S
             if os_[2] != Wo * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if (Cc < 16 and ncols <= 64 and kdim <= 192 and (sh, sw) == (1, 1) and xb.splat is None and yb.splat is None
+                    and (4 + R - 1) * (32 + S - 1) * Cc + 3 * (32 + S - 1) + 32 <= 1536  # 4x32 tile patch + zero pad
+                    and os.environ.get("GFB_CONV_STEM", "1") == "1"
+                    and os.environ.get("GFB_CONV_F16", "1") == "1"
+                    and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 62):
+                # the same tiles in 2xFP16 (conv_f16.cu gfb_conv_stemh_kernel): per-tile
+                # activation scales, the filter split inside the kernel
+                self._conv_stemh(n, xb, xs, yb, ys, out, m, ncols, kdim,
+                                 dict(Y=Ho, X=Wo, oy=-pt, ox=-pl, H=H, W=W, S=S, C=Cc,
+                                      c_s_hi=os_[0], c_sm=os_[2], c_s_lo=os_[3], c_sn=os_[1]),
+                                 f"{node.op.wire_name}_stemh#{n}")
+                return True
             if (Cc < 16 and ncols <= 64 and kdim <= 160 and (sh, sw) == (1, 1) and xb.splat is None
                     and (8 + R - 1) * (16 + S - 1) * Cc <= 1536 and os.environ.get("GFB_CONV_STEM", "1") == "1"
                     and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 62):

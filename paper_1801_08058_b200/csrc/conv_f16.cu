@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(tc::HXCfg<BN_>::THREADS, 1) gfb_conv_tcxh_kern
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(tc::HWCfg<BN_>::THREADS, 1) gfb_conv_tcgwh_ker
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -574,6 +574,365 @@ __global__ void __launch_bounds__(tc::HWCfg<BN_>::THREADS, 1) gfb_conv_tcgwh_ker
 template __global__ void gfb_conv_tcgwh_kernel<64>(const __grid_constant__ gfb_tcgwh_args);
 template __global__ void gfb_conv_tcgwh_kernel<128>(const __grid_constant__ gfb_tcgwh_args);
 
+// ---------------------------------------------------------------------------
+// Few-channel forward convolution (the 3-channel ResNet stem) in 2xFP16
+// (gfb_stemh_args): the tile walk and shared-memory input patch of
+// gemm_tc.cu's gfb_conv_stem_kernel, on kind::f16.  The K = R S C <= 192
+// columns (r, s, c) are one to three 64-wide K-blocks; a K-block issues only
+// the 16-wide K-steps below K.  Scales, all exact powers of two:
+//   * activation: one per 128-pixel tile, u = 2^(14 - floor(log2 m)), m the
+//     largest finite |x| of the tile's input patch (computed while the patch
+//     is staged, no extra pass); the patch is parked as fp16 hi / lo words
+//     of x u, from which the builders assemble A;
+//   * filter: one per output channel, t_n from the row's largest finite |w|;
+//     every CTA splits the (tiny) filter into resident SW128 hi / lo planes
+//     in its prologue.
+//   y[p, n] = ((sum_k AhBh + AhBl + AlBh) / u) / t_n
+// Warp roles: 1 TMEM + MMA issuer, 2..5 epilogue, 6..13 patch + A builders.
+namespace tc {
+struct HSCfg {
+    static constexpr int BM = 128, BN = 64, BK = 64, TH = 4, TW = 32;
+    static constexpr int MAXKB = 3;  // K <= 192 (the filter stays resident)
+    static constexpr int STAGES = 4;
+    static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES;
+    static constexpr int BRES_BYTES = MAXKB * 2 * B_BYTES;
+    static constexpr int PATCH_FLOATS = 1536;  // (4 + R - 1)(32 + S - 1) C + zero pad <= 1536
+    static constexpr int OUT_BYTES = 4 * 32 * BN * 4;  // per epilogue warp: one 32-pixel row of the tile
+    static constexpr int NBUF = 8, RING = 2 * NBUF;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 4, LOAD_WARPS = 8;
+    static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LOAD_WARPS);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BRES_BYTES + OUT_BYTES + 2 * PATCH_FLOATS * 4 + MAXKB * BK * 4 +
+                                      (RING + BN + 2 * LOAD_WARPS) * 4 + 256 + 1024;
+};
+}  // namespace tc
+
+__global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(const __grid_constant__ gfb_stemh_args p) {
+    using namespace tc;
+    using C_ = HSCfg;
+    constexpr int BN = C_::BN, BK = C_::BK, TH = C_::TH, TW = C_::TW, STAGES = C_::STAGES, NBUF = C_::NBUF;
+    constexpr int RING = C_::RING, A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int EPI_WARPS = C_::EPI_WARPS, LW = C_::LOAD_WARPS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // (offset from the __shared__ array itself, so every derived pointer stays a
+    // shared-space pointer: LDS / STS, not generic loads)
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* bres = smem + STAGES * STAGE_BYTES;  // K-block kb: hi at kb * 2 * B_BYTES, lo after it
+    unsigned char* ostage = bres + C_::BRES_BYTES;                     // epilogue staging
+    float* patch = reinterpret_cast<float*>(ostage + C_::OUT_BYTES);  // two buffers of PATCH_FLOATS
+    int* ktab = reinterpret_cast<int*>(patch + 2 * C_::PATCH_FLOATS);  // patch offset of every k
+    float* iu = reinterpret_cast<float*>(ktab + C_::MAXKB * BK);       // 1 / u of tile gt at gt % RING
+    float* invt = iu + RING;                                           // 1 / t_n
+    float* wmax = invt + BN;                                           // per loader warp patch maxima
+    uint64_t* full = reinterpret_cast<uint64_t*>(wmax + 2 * LW);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int K = (int)p.K, nk = (K + BK - 1) / BK;
+    const int Cc = p.C, S = p.S, R = K / (Cc * S);
+    const int PH = TH + R - 1, PW = TW + S - 1, PSZ = PH * PW * Cc;
+    const int tiles_x = (p.X + TW - 1) / TW, tiles_y = (p.Y + TH - 1) / TH;
+    const int nitems = (int)(p.M / ((int64_t)p.Y * p.X)) * tiles_y * tiles_x;  // M = N * Y * X
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], LW);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // K -> patch offset table: k = (r, s, c), c fastest; patch layout [c][py][px]
+    for (int k = threadIdx.x; k < C_::MAXKB * BK; k += blockDim.x) {
+        int off = PSZ;  // k >= K: the zero pad (PSZ + (TH - 1) PW + TW <= PATCH_FLOATS)
+        if (k < K) {
+            const int tap = k / Cc, c = k - tap * Cc, r = tap / S, s = tap - r * S;
+            off = (c * PH + r) * PW + s;
+        }
+        ktab[k] = off;
+    }
+    // the filter: row n's scale t_n, then its fp16 hi / lo pieces in the SW128
+    // K-major layout (row n at n * 128 B, 16-byte chunk j at (j ^ (n & 7)) * 16)
+    {
+        const float* w = resolve<const float>(p.tab, p.w);
+        auto wv = [&](int n, int k) {
+            if (n >= p.N || k >= K) return 0.0f;
+            const int tap = k / Cc, c = k - tap * Cc, r = tap / S, s = tap - r * S;
+            return __ldg(w + n * p.ws0 + c * p.ws1 + r * p.ws2 + s * p.ws3);
+        };
+        for (int n = warp; n < BN; n += C_::THREADS / 32) {
+            float m = 0.0f;
+            for (int k = lane; k < K; k += 32) m = fmaxf(m, fin_abs(wv(n, k)));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const float t = f16_tile_scale(m);
+            if (lane == 0) invt[n] = __frcp_rn(t);
+            for (int k = lane; k < nk * BK; k += 32) {
+                const float v = __fmul_rn(wv(n, k), t);
+                const __half h = __float2half_rn(v), l = __float2half_rn(__fsub_rn(v, __half2float(h)));
+                const int kb = k / BK, kk = k - kb * BK;
+                const int off = kb * 2 * B_BYTES + n * 128 + ((((kk >> 3) ^ (n & 7))) << 4) + (kk & 7) * 2;
+                *reinterpret_cast<__half*>(bres + off) = h;
+                *reinterpret_cast<__half*>(bres + off + B_BYTES) = l;
+            }
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    // item -> (image, tile row, tile column) with float-reciprocal divisions
+    // (item indices < 2^24 are exact in float; one correction step each)
+    const float inv_tx = 1.0f / (float)tiles_x, inv_ty = 1.0f / (float)tiles_y;
+    auto divmod = [](int a, int d, float inv, int& q) {
+        q = (int)((float)a * inv);
+        if (q * d > a) --q;
+        else if ((q + 1) * d <= a) ++q;
+        return a - q * d;
+    };
+    auto item_at = [&](int it, int& n, int& y0, int& x0) {
+        int t;
+        const int tx = divmod(it, tiles_x, inv_tx, t);
+        const int ty = divmod(t, tiles_y, inv_ty, n);
+        y0 = ty * TH;
+        x0 = tx * TW;
+    };
+
+    if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(128, BN);
+            uint32_t gk = 0, gt = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
+                const int b = gt % NBUF;
+                mbar_wait(&tempty[b], ((gt / NBUF) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(b * BN);
+                for (int kb = 0; kb < nk; ++kb, ++gk) {
+                    const int s = gk % STAGES;
+                    mbar_wait(&full[s], (gk / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    unsigned char* st = smem + s * STAGE_BYTES;
+                    const uint64_t ah = smem_desc(st), al = smem_desc(st + A_BYTES);
+                    const uint64_t bh = smem_desc(bres + kb * 2 * B_BYTES), bl = smem_desc(bres + kb * 2 * B_BYTES + B_BYTES);
+                    const int ks = min(4, (K - kb * BK + 15) / 16);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (j < ks) {
+                            const uint64_t adv = (uint64_t)(j * 32) >> 4;  // 16 fp16 = 32 B along K
+                            const uint32_t acc = !(kb == 0 && j == 0);
+                            mma_f16_cta(d, ah + adv, bh + adv, idesc, acc);
+                            mma_f16_cta(d, ah + adv, bl + adv, idesc, 1);
+                            mma_f16_cta(d, al + adv, bh + adv, idesc, 1);
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[b]);
+            }
+        }
+    } else if (warp >= 2 && warp < 2 + EPI_WARPS) {
+        // warp q owns TMEM lanes 32q.. = tile row q (TW = 32 pixels).  Dense
+        // channel-last output: the row's 32 x 64 values go through a swizzled
+        // per-warp staging buffer and leave as 512-byte contiguous stores
+        // (two whole pixels per instruction) instead of 16-byte pieces of 32
+        // different pixels.
+        static_assert(TW == 32, "one tile row per epilogue warp");
+        const int q = warp & 3;
+        float* C = resolve<float>(p.tab, p.c);
+        unsigned char* ost = ostage + q * (32 * BN * 4);
+        const bool dense = p.c_sn == 1 && p.N == BN && p.c_s_lo == BN && p.c_sm % 4 == 0 && p.c_s_hi % 4 == 0 &&
+                           (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+        uint32_t gt = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
+            int n, y0, x0;
+            item_at(it, n, y0, x0);
+            const int b = gt % NBUF;
+            mbar_wait(&tfull[b], (gt / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float acc[BN];
+#pragma unroll
+            for (int c = 0; c < BN / 16; ++c) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 16), acc + c * 16);
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+            const float f = iu[gt % RING];
+            const int y = y0 + q;
+            if (dense) {
+#pragma unroll
+                for (int j = 0; j < BN / 4; ++j)
+                    *reinterpret_cast<float4*>(ost + lane * (BN * 4) + ((j ^ (lane & 7)) << 4)) =
+                        make_float4(__fmul_rn(__fmul_rn(acc[4 * j], f), invt[4 * j]),
+                                    __fmul_rn(__fmul_rn(acc[4 * j + 1], f), invt[4 * j + 1]),
+                                    __fmul_rn(__fmul_rn(acc[4 * j + 2], f), invt[4 * j + 2]),
+                                    __fmul_rn(__fmul_rn(acc[4 * j + 3], f), invt[4 * j + 3]));
+                __syncwarp();
+                if (y < p.Y) {
+                    float* row = C + (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm;
+                    const int quad = lane & 15;
+#pragma unroll 4
+                    for (int i2 = 0; i2 < 16; ++i2) {
+                        const int pp = 2 * i2 + (lane >> 4), x = x0 + pp;
+                        const float4 v = *reinterpret_cast<const float4*>(ost + pp * (BN * 4) + ((quad ^ (pp & 7)) << 4));
+                        if (x < p.X) *reinterpret_cast<float4*>(row + (int64_t)x * BN + quad * 4) = v;
+                    }
+                }
+                __syncwarp();
+            } else {
+                const int x = x0 + lane;
+                if (y < p.Y && x < p.X) {
+                    float* dst = C + (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm + (int64_t)x * p.c_s_lo;
+#pragma unroll
+                    for (int j = 0; j < BN; ++j)
+                        if (j < p.N) dst[(int64_t)j * p.c_sn] = __fmul_rn(__fmul_rn(acc[j], f), invt[j]);
+                }
+            }
+        }
+    } else if (warp >= 2 + EPI_WARPS) {
+        // builders.  The next tile's input patch is loaded into registers
+        // while this tile's A blocks are built; its largest finite |x| gives
+        // the tile scale u, and the patch is parked already scaled and split:
+        // one 32-bit word per element, fp16 hi in the low half, lo in the
+        // high half.  A K-block chunk (8 consecutive k of one row) is then 8
+        // word gathers and 8 byte permutes; k >= K points into a zero pad
+        // after the patch.  Thread t builds row m = t & 127; of each K-block's
+        // used 16-byte chunks (2 per 16-wide K-step) it takes half.
+        const int t = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0 .. 32 * LW - 1
+        const int m = t & 127, hf = t >> 7, lw = t >> 5;
+        const int py = m / TW, px = m % TW;
+        const uint32_t rsw = (uint32_t)(m & 7);
+        const float* X = resolve<const float>(p.tab, p.a);
+        uint32_t* pw = reinterpret_cast<uint32_t*>(patch);
+        constexpr int PPT = (C_::PATCH_FLOATS + 32 * LW - 1) / (32 * LW);  // patch elements per thread
+        float pre[PPT];
+        int pyy[PPT], pxx[PPT];
+        int64_t poff[PPT];
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int i = t + u * 32 * LW;
+            const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
+            pyy[u] = i < PSZ ? yy + p.oy : -(1 << 28);
+            pxx[u] = xx + p.ox;
+            poff[u] = (int64_t)c * p.xs1 + (int64_t)(yy + p.oy) * p.xs2 + (int64_t)(xx + p.ox) * p.xs3;
+        }
+        // zero pads of both patch buffers (never overwritten)
+        for (int i = PSZ + t; i < C_::PATCH_FLOATS; i += 32 * LW) pw[i] = pw[C_::PATCH_FLOATS + i] = 0u;
+        auto fetch = [&](int it2) {
+            int n2, ya, xa;
+            item_at(it2, n2, ya, xa);
+            const float* base = X + (int64_t)n2 * p.xs0 + (int64_t)ya * p.xs2 + (int64_t)xa * p.xs3;
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) {
+                const int h = ya + pyy[u], w = xa + pxx[u];
+                pre[u] = ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W) ? __ldg(base + poff[u]) : 0.0f;
+            }
+        };
+        // the fetched patch's scale (two loader barriers) and its parked words;
+        // thread 0 publishes 1 / u for tile gt2 before any arrive of that tile
+        auto park = [&](uint32_t* pt, uint32_t gt2) {
+            float mm = 0.0f;
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) mm = fmaxf(mm, fin_abs(pre[u]));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+            if (lane == 0) wmax[lw] = mm;
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
+            float mx = wmax[0];
+#pragma unroll
+            for (int i = 1; i < LW; ++i) mx = fmaxf(mx, wmax[i]);
+            const float u = f16_tile_scale(mx);
+            if (t == 0) iu[gt2 % RING] = __frcp_rn(u);
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                if (t + q * 32 * LW < PSZ) {
+                    const float v = __fmul_rn(pre[q], u);
+                    const __half h = __float2half_rn(v), l = __float2half_rn(__fsub_rn(v, __half2float(h)));
+                    pt[t + q * 32 * LW] = (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(l) << 16);
+                }
+            }
+        };
+        if ((int)blockIdx.x < nitems) {
+            fetch(blockIdx.x);
+            park(pw, 0);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
+        uint32_t gk = 0, gt = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++gt) {
+            const bool more = it + (int)gridDim.x < nitems;
+            if (more) fetch(it + gridDim.x);
+            const uint32_t* prow = pw + (gt & 1) * C_::PATCH_FLOATS + py * PW + px;
+            for (int kb = 0; kb < nk; ++kb, ++gk) {
+                const int s = gk % STAGES;
+                mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
+                unsigned char* st = smem + s * STAGE_BYTES + m * 128;
+                const int ks = min(4, (K - kb * BK + 15) / 16);  // chunks 2 ks; this thread: [hf ks, hf ks + ks)
+                // all offsets, then all gathers, then the permutes and stores (no
+                // per-chunk load -> load -> store chain)
+                int4 ko[8];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (jj < ks) {
+                        const int j = hf * ks + jj;
+                        ko[2 * jj] = *reinterpret_cast<const int4*>(ktab + kb * BK + 8 * j);
+                        ko[2 * jj + 1] = *reinterpret_cast<const int4*>(ktab + kb * BK + 8 * j + 4);
+                    }
+                }
+                uint32_t e[32];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (jj < ks) {
+                        e[8 * jj + 0] = prow[ko[2 * jj].x];
+                        e[8 * jj + 1] = prow[ko[2 * jj].y];
+                        e[8 * jj + 2] = prow[ko[2 * jj].z];
+                        e[8 * jj + 3] = prow[ko[2 * jj].w];
+                        e[8 * jj + 4] = prow[ko[2 * jj + 1].x];
+                        e[8 * jj + 5] = prow[ko[2 * jj + 1].y];
+                        e[8 * jj + 6] = prow[ko[2 * jj + 1].z];
+                        e[8 * jj + 7] = prow[ko[2 * jj + 1].w];
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (jj < ks) {
+                        const uint32_t* q = e + 8 * jj;
+                        const int o = (((hf * ks + jj) ^ (int)rsw) << 4);
+                        *reinterpret_cast<uint4*>(st + o) = make_uint4(__byte_perm(q[0], q[1], 0x5410), __byte_perm(q[2], q[3], 0x5410),
+                                                                       __byte_perm(q[4], q[5], 0x5410), __byte_perm(q[6], q[7], 0x5410));
+                        *reinterpret_cast<uint4*>(st + A_BYTES + o) =
+                            make_uint4(__byte_perm(q[0], q[1], 0x7632), __byte_perm(q[2], q[3], 0x7632), __byte_perm(q[4], q[5], 0x7632),
+                                       __byte_perm(q[6], q[7], 0x7632));
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+            }
+            // the other buffer's last readers (tile it - gridDim.x) passed the previous barrier
+            if (more) park(pw + ((gt + 1) & 1) * C_::PATCH_FLOATS, gt + 1);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 }  // namespace gfb
 
 extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
@@ -584,7 +943,9 @@ extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
     if (kind == GFB_K_CONV_TCXH128) return (const void*)gfb::gfb_conv_tcxh_kernel<128>;
     if (kind == GFB_K_CONV_TCGWH64) return (const void*)gfb::gfb_conv_tcgwh_kernel<64>;
     if (kind == GFB_K_CONV_TCGWH128) return (const void*)gfb::gfb_conv_tcgwh_kernel<128>;
+    if (kind == GFB_K_CONV_STEMH) return (const void*)gfb::gfb_conv_stemh_kernel;
     return nullptr;
 }
 extern "C" int gfb_tcgwh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HWCfg<64>::SMEM_BYTES : gfb::tc::HWCfg<128>::SMEM_BYTES; }
+extern "C" int gfb_stemh_smem_bytes(void) { return gfb::tc::HSCfg::SMEM_BYTES; }
 extern "C" int gfb_tcxh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HXCfg<64>::SMEM_BYTES : gfb::tc::HXCfg<128>::SMEM_BYTES; }

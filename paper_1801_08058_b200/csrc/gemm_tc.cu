@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(tc::Cfg<BN_>::THREADS, 1) gfb_gemm_tc_kernel(c
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
     constexpr uint32_t TMEM_COLS = C_::TMEM_COLS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;   // [NBUF] accumulator chunk ready
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS, 1) gfb_conv_tcg_kernel
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GATHER_WARPS = C_::GATHER_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     unsigned char* raw = smem + STAGES * STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(raw + RAW * A_BYTES + C_::ROWTAB);
     uint64_t* empty = full + STAGES;
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(tc::XCfg<BN_>::THREADS, 1) gfb_conv_tcx_kernel
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, CONV_WARPS = C_::CONV_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* afull = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // A box landed
     uint64_t* full = afull + STAGES;    // A split + B planes landed
     uint64_t* empty = full + STAGES;
@@ -1009,7 +1009,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::PCfg::THREADS, 1
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -1342,7 +1342,7 @@ __global__ void __launch_bounds__(tc::GCfg<BN_>::THREADS_GG, 1) gfb_conv_tcgg_ke
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GATHER_WARPS = C_::GATHER_WARPS_GG;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     unsigned char* raw = smem + STAGES * STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(raw + RAW * A_BYTES + C_::ROWTAB);
     uint64_t* empty = full + STAGES;
@@ -1647,7 +1647,7 @@ __global__ void __launch_bounds__(tc::WCfg<BN_>::THREADS, 1) gfb_conv_tcgw_kerne
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES, RAW_BYTES = C_::RAW_BYTES;
     constexpr int CHUNK_KB = C_::CHUNK_KB, EPI_WARPS = C_::EPI_WARPS, GW = C_::GATHER_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     unsigned char* raw = smem + STAGES * STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(raw + RAW * RAW_BYTES);
     uint64_t* empty = full + STAGES;
@@ -1955,7 +1955,7 @@ __global__ void __launch_bounds__(tc::SCfg::THREADS, 1) gfb_conv_stem_kernel(con
     constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
     constexpr int EPI_WARPS = C_::EPI_WARPS, LW = C_::LOAD_WARPS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     unsigned char* bres = smem + STAGES * STAGE_BYTES;  // K-block kb: hi at kb * 2 * B_BYTES, lo after it
     float* patch = reinterpret_cast<float*>(bres + C_::BRES_BYTES);  // two buffers of PATCH_FLOATS
     int* ktab = reinterpret_cast<int*>(patch + 2 * C_::PATCH_FLOATS);  // patch offset of every k (-1: k >= K)

@@ -110,7 +110,7 @@ def test_conv_tensor_cores_match_oracle(monkeypatch, op, shape, stride, pad, lay
     N, C, Ko, H, W, R, S = shape
     fn = TL._conv_graph(op, N, C, Ko, H, W, R, S, stride, pad)
     exe = gf.compile_function(fn, conv_layout=layout) if op == "fwd" else gf.compile_function(fn)
-    assert any("_tc" in L.label or "_stem#" in L.label for L in exe.lowered.launches)
+    assert any("_tc" in L.label or "_stem" in L.label for L in exe.lowered.launches)
     rng = np.random.default_rng(7)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
@@ -252,6 +252,7 @@ def test_conv_stem_kernel_matches_oracle(monkeypatch, shape, pad, layout):
     from paper_1801_08058_b200 import abi
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_CONV_F16", "0")
     N, C, Ko, H, W, R, S = shape
     fn = TL._conv_graph("fwd", N, C, Ko, H, W, R, S, (1, 1), pad)
     lay = [gf.Layout((0, 2, 3, 1)), None] if layout == "nhwc" else None
@@ -263,6 +264,39 @@ def test_conv_stem_kernel_matches_oracle(monkeypatch, shape, pad, layout):
     out = gf.call(exe, tens)[0].to_numpy()
     interp.set_threads(interp.max_threads())
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("shape,pad,layout", [
+    ((4, 3, 64, 40, 36, 7, 7), (3, 3, 3, 3), "identity"),   # the ResNet stem, NCHW input
+    ((2, 3, 16, 32, 32, 3, 3), (1, 1, 1, 1), "identity"),   # config C's first layer (16 < 64 columns)
+    ((3, 4, 64, 17, 23, 5, 5), (2, 1, 0, 3), "nhwc"),       # channel-last input, partial tiles
+    ((2, 1, 40, 9, 11, 3, 3), (0, 0, 1, 1), "identity"),    # one channel, no padding rows
+    ((2, 3, 48, 20, 19, 8, 8), (4, 3, 3, 4), "nhwc"),       # K = 192: three full K-blocks
+    ((37, 3, 64, 24, 24, 7, 7), (3, 3, 3, 3), "nhwc"),      # more tiles than CTAs: the persistent walk
+])
+def test_conv_stemh_kernel_matches_oracle(monkeypatch, shape, pad, layout):
+    """gfb_conv_stemh_kernel (the stem's tiles in 2xFP16: per-tile activation
+    scales, the filter split in the prologue) vs the oracle, with inputs
+    whose magnitude varies by 10^6 between images and tiles."""
+    import test_lowering as TL
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, Ko, H, W, R, S = shape
+    fn = TL._conv_graph("fwd", N, C, Ko, H, W, R, S, (1, 1), pad)
+    lay = [gf.Layout((0, 2, 3, 1)), None] if layout == "nhwc" else None
+    exe = gf.compile_function(fn, conv_layout=layout, parameter_layouts=lay)
+    assert any(L.kind == abi.K_CONV_STEMH for L in exe.lowered.launches), [L.label for L in exe.lowered.launches]
+    rng = np.random.default_rng(37)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][0] *= np.float32(1e-6)
+    ins[0][:, :, : H // 3] *= np.float32(1e3)
+    tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = gf.call(exe, tens)[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    ref = interp.run_function(fn, ins)[0]
+    assert G.normwise(out, ref) <= 1e-5
+    assert G.normwise(out[0], ref[0]) <= 1e-5  # the 1e-6 image on its own scale
 
 
 @pytest.mark.parametrize("m,k,n", [(512, 4096, 256), (288, 1000, 352), (4096, 2048, 4096)])

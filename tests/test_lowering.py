@@ -211,8 +211,8 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     h = host_compile(fn, optimize=False, conv_layout=layout) if op == "fwd" else host_compile(fn, optimize=False)
     labels = [L.label for L in h.lowered.launches]
     assert any("_tc" in l or "_stem" in l for l in labels), labels
-    if op == "fwd" and C < 16 and stride == (1, 1):  # few channels: the patch-staged stem kernel
-        assert any("_stem#" in l for l in labels), labels
+    if op == "fwd" and C < 16 and stride == (1, 1):  # few channels: the patch-staged stem kernel (2xFP16)
+        assert any("_stemh#" in l for l in labels), labels
     if op == "wgrad" and N * H * W >= 2048:  # long K: split-K with a deterministic second pass
         assert any(":splitk" in l for l in labels), labels
     rng = np.random.default_rng(5)
@@ -220,6 +220,37 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
     out = emulate(h, tens)[0]
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("shape,pad,layout", [
+    ((2, 3, 64, 12, 20, 7, 7), (3, 3, 3, 3), "identity"),  # the ResNet stem shape, partial tiles
+    ((2, 3, 40, 9, 11, 8, 8), (4, 3, 3, 4), "nhwc"),       # K = 192 (three full K-blocks), 40 columns
+    ((1, 1, 16, 10, 17, 3, 3), (0, 1, 1, 0), "identity"),  # one channel, K = 9 (one K-step)
+])
+def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
+    """The few-channel forward convolution in 2xFP16 (per-tile activation
+    scales, per-row filter scales), emulated, within 1e-5 normwise of the
+    oracle; with GFB_CONV_F16=0 the TF32 stem kernel runs instead."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, K, H, W, R, S = shape
+    fn = _conv_graph("fwd", N, C, K, H, W, R, S, (1, 1), pad)
+    lay = [(0, 2, 3, 1), None] if layout == "nhwc" else None
+    h = host_compile(fn, optimize=False, conv_layout=layout, parameter_layouts=lay)
+    kinds = [L.kind for L in h.lowered.launches]
+    assert abi.K_CONV_STEMH in kinds and abi.K_SPLIT_TF32 not in kinds, [L.label for L in h.lowered.launches]
+    rng = np.random.default_rng(17)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][:, :, : H // 2] *= 1e-3  # tiles of different magnitude: the per-tile scales differ
+    tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = emulate(h, tens)[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+    monkeypatch.setenv("GFB_CONV_F16", "0")
+    h2 = host_compile(fn, optimize=False, conv_layout=layout, parameter_layouts=lay)
+    assert abi.K_CONV_STEMH not in [L.kind for L in h2.lowered.launches]
 
 
 @pytest.mark.parametrize("op,shape,stride,pad", [
