@@ -2664,7 +2664,9 @@ class Lowering:
                            ws0=ys[0], ws1=ys[1], ws2=ys[2], ws3=ys[3], **geo)
         tiles = (m // (geo["Y"] * geo["X"])) * ((geo["Y"] + 3) // 4) * ((geo["X"] + 31) // 32)
         grid = (max(1, min(tiles, NUM_SMS)), 1, 1)
-        rec = LaunchRec(abi.K_CONV_STEMH, grid, (STEM_THREADS, 1, 1), STEMH_SMEM, ta, [xb.key, yb.key], [out.key], label)
+        # the 3-channel 7x7 stem: a build with immediate gather offsets
+        kind = abi.K_CONV_STEMH_C3R7 if (geo["C"], kdim // geo["C"] // geo["S"], geo["S"]) == (3, 7, 7) else abi.K_CONV_STEMH
+        rec = LaunchRec(kind, grid, (STEM_THREADS, 1, 1), STEMH_SMEM, ta, [xb.key, yb.key], [out.key], label)
         rec.flops = 2 * m * ncols * kdim
         rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
         rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "w": yb})

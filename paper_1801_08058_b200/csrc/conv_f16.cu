@@ -608,6 +608,55 @@ struct HSCfg {
 };
 }  // namespace tc
 
+// patch word offset of K index k = (r, s, c) (c fastest) in the [c][py][px]
+// patch; k >= K: the zero pad
+__host__ __device__ constexpr int stemh_off(int C, int R, int S, int PH, int PW, int k) {
+    return k < C * R * S ? ((k % C) * PH + (k / C) / S) * PW + (k / C) % S : PH * PW * C;
+}
+
+// One tile's A blocks for a compile-time (C, R, S): every gather offset is an
+// immediate (LDS [row + imm]), no offset table.  Thread half HF of row m.
+template <int CC, int RR, int SS, int HF>
+__device__ __forceinline__ void stemh_build(unsigned char* smem, const uint32_t* prow, uint32_t& gk, uint64_t* empty,
+                                            uint64_t* full, int m, int rsw, int lane) {
+    using C_ = tc::HSCfg;
+    constexpr int K_ = CC * RR * SS, NK = (K_ + C_::BK - 1) / C_::BK;
+    constexpr int PH_ = C_::TH + RR - 1, PW_ = C_::TW + SS - 1;
+    static_assert(NK <= C_::MAXKB, "K <= 192");
+#pragma unroll
+    for (int kb = 0; kb < NK; ++kb, ++gk) {
+        const int s = gk % C_::STAGES;
+        tc::mbar_wait(&empty[s], ((gk / C_::STAGES) & 1) ^ 1);
+        unsigned char* st = smem + s * C_::STAGE_BYTES + m * 128;
+        const int ks = (K_ - kb * C_::BK + 15) / 16 < 4 ? (K_ - kb * C_::BK + 15) / 16 : 4;
+        uint32_t e[32];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            if (jj < ks) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) e[8 * jj + q] = prow[stemh_off(CC, RR, SS, PH_, PW_, kb * C_::BK + 8 * (HF * ks + jj) + q)];
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            if (jj < ks) {
+                const uint32_t* q = e + 8 * jj;
+                const int o = (((HF * ks + jj) ^ rsw) << 4);
+                *reinterpret_cast<uint4*>(st + o) = make_uint4(__byte_perm(q[0], q[1], 0x5410), __byte_perm(q[2], q[3], 0x5410),
+                                                               __byte_perm(q[4], q[5], 0x5410), __byte_perm(q[6], q[7], 0x5410));
+                *reinterpret_cast<uint4*>(st + C_::A_BYTES + o) = make_uint4(
+                    __byte_perm(q[0], q[1], 0x7632), __byte_perm(q[2], q[3], 0x7632), __byte_perm(q[4], q[5], 0x7632),
+                    __byte_perm(q[6], q[7], 0x7632));
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::su32(&full[s])) : "memory");
+    }
+}
+
+// CC > 0: specialised for that (C, R, S) (the 3-channel 7x7 stem); 0: any
+template <int CC, int RR, int SS>
 __global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(const __grid_constant__ gfb_stemh_args p) {
     using namespace tc;
     using C_ = HSCfg;
@@ -874,6 +923,10 @@ __global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(c
             const bool more = it + (int)gridDim.x < nitems;
             if (more) fetch(it + gridDim.x);
             const uint32_t* prow = pw + (gt & 1) * C_::PATCH_FLOATS + py * PW + px;
+            if constexpr (CC > 0) {
+                if (hf == 0) stemh_build<CC, RR, SS, 0>(smem, prow, gk, empty, full, m, (int)rsw, lane);
+                else stemh_build<CC, RR, SS, 1>(smem, prow, gk, empty, full, m, (int)rsw, lane);
+            } else
             for (int kb = 0; kb < nk; ++kb, ++gk) {
                 const int s = gk % STAGES;
                 mbar_wait(&empty[s], ((gk / STAGES) & 1) ^ 1);
@@ -933,6 +986,9 @@ __global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(c
     }
 }
 
+template __global__ void gfb_conv_stemh_kernel<0, 0, 0>(const __grid_constant__ gfb_stemh_args);
+template __global__ void gfb_conv_stemh_kernel<3, 7, 7>(const __grid_constant__ gfb_stemh_args);
+
 }  // namespace gfb
 
 extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
@@ -943,7 +999,8 @@ extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
     if (kind == GFB_K_CONV_TCXH128) return (const void*)gfb::gfb_conv_tcxh_kernel<128>;
     if (kind == GFB_K_CONV_TCGWH64) return (const void*)gfb::gfb_conv_tcgwh_kernel<64>;
     if (kind == GFB_K_CONV_TCGWH128) return (const void*)gfb::gfb_conv_tcgwh_kernel<128>;
-    if (kind == GFB_K_CONV_STEMH) return (const void*)gfb::gfb_conv_stemh_kernel;
+    if (kind == GFB_K_CONV_STEMH) return (const void*)gfb::gfb_conv_stemh_kernel<0, 0, 0>;
+    if (kind == GFB_K_CONV_STEMH_C3R7) return (const void*)gfb::gfb_conv_stemh_kernel<3, 7, 7>;
     return nullptr;
 }
 extern "C" int gfb_tcgwh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HWCfg<64>::SMEM_BYTES : gfb::tc::HWCfg<128>::SMEM_BYTES; }

@@ -832,7 +832,7 @@ def _run_launch(mem, L):
         run_tcx(mem, L.args)
     elif L.kind == abi.K_CONV_STEM64:
         run_stem(mem, L.args)
-    elif L.kind == abi.K_CONV_STEMH:
+    elif L.kind in (abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7):
         run_stemh(mem, L.args)
     elif L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128):
         run_tcgw(mem, L.args)

@@ -286,7 +286,8 @@ def test_conv_stemh_kernel_matches_oracle(monkeypatch, shape, pad, layout):
     fn = TL._conv_graph("fwd", N, C, Ko, H, W, R, S, (1, 1), pad)
     lay = [gf.Layout((0, 2, 3, 1)), None] if layout == "nhwc" else None
     exe = gf.compile_function(fn, conv_layout=layout, parameter_layouts=lay)
-    assert any(L.kind == abi.K_CONV_STEMH for L in exe.lowered.launches), [L.label for L in exe.lowered.launches]
+    assert any(L.kind in (abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7) for L in exe.lowered.launches), \
+        [L.label for L in exe.lowered.launches]
     rng = np.random.default_rng(37)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     ins[0][0] *= np.float32(1e-6)

@@ -241,7 +241,10 @@ def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
     lay = [(0, 2, 3, 1), None] if layout == "nhwc" else None
     h = host_compile(fn, optimize=False, conv_layout=layout, parameter_layouts=lay)
     kinds = [L.kind for L in h.lowered.launches]
-    assert abi.K_CONV_STEMH in kinds and abi.K_SPLIT_TF32 not in kinds, [L.label for L in h.lowered.launches]
+    assert {abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7} & set(kinds) and abi.K_SPLIT_TF32 not in kinds, \
+        [L.label for L in h.lowered.launches]
+    if (C, R, S) == (3, 7, 7):
+        assert abi.K_CONV_STEMH_C3R7 in kinds
     rng = np.random.default_rng(17)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     ins[0][:, :, : H // 2] *= 1e-3  # tiles of different magnitude: the per-tile scales differ
@@ -250,7 +253,7 @@ def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
     assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
     monkeypatch.setenv("GFB_CONV_F16", "0")
     h2 = host_compile(fn, optimize=False, conv_layout=layout, parameter_layouts=lay)
-    assert abi.K_CONV_STEMH not in [L.kind for L in h2.lowered.launches]
+    assert not {abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7} & {L.kind for L in h2.lowered.launches}
 
 
 @pytest.mark.parametrize("op,shape,stride,pad", [
