@@ -388,7 +388,7 @@ def _time_launch(exe, idx, dev_in, outs, stream, reps):
 
 
 _KIND_NAMES = {34: "gfb_gemm_f16p_kernel", 39: "gfb_conv_tcxh_kernel<64>", 40: "gfb_conv_tcxh_kernel<128>",
-               41: "gfb_conv_tcgwh_kernel<64>", 42: "gfb_conv_tcgwh_kernel<128>", 44: "gfb_conv_stemh_kernel<0,0,0>", 45: "gfb_conv_stemh_kernel<3,7,7>", 19: "gfb_gemm_tc2_kernel", 12: "gfb_gemm_tc_kernel<128>", 14: "gfb_gemm_tc_kernel<256>",
+               41: "gfb_conv_tcgwh_kernel<64>", 42: "gfb_conv_tcgwh_kernel<128>", 44: "gfb_conv_stemh_kernel<0,0,0>", 45: "gfb_conv_stemh_kernel<3,7,7>", 46: "gfb_conv_stemwh_kernel<3,7,7>", 19: "gfb_gemm_tc2_kernel", 12: "gfb_gemm_tc_kernel<128>", 14: "gfb_gemm_tc_kernel<256>",
                22: "gfb_conv_tcx_kernel<64>", 23: "gfb_conv_tcx_kernel<128>", 17: "gfb_conv_tcg_kernel<64>",
                18: "gfb_conv_tcg_kernel<128>", 24: "gfb_conv_tcgg_kernel<64>", 25: "gfb_conv_tcgg_kernel<128>",
                28: "gfb_conv_tcgw_kernel<64>", 29: "gfb_conv_tcgw_kernel<128>", 32: "gfb_conv_stem_kernel",
@@ -548,7 +548,7 @@ def bench_step(args, ws, rank, local):
     dom_flops = sum(L.flops for _, _, L in dom_rows)
     kernel_ms = dom_ms / len(dom_rows)
     tf32, tf32_sus, tf_src = tf32_peak()
-    if dom_kind in (34, 39, 40, 41, 42, 44, 45):  # 2xFP16: three kind::f16 MMAs per useful product
+    if dom_kind in (34, 39, 40, 41, 42, 44, 45, 46):  # 2xFP16: three kind::f16 MMAs per useful product
         mma_sus, mma_name = f16_peak(), "2xFP16 useful ceiling = kind::f16"
     else:  # 3xTF32: three kind::tf32 MMAs per useful product
         mma_sus, mma_name = tf32_sus, "3xTF32 useful ceiling = kind::tf32"

@@ -102,6 +102,7 @@ enum {
     GFB_K_CONV_STEMH = 44,    /* few-channel forward conv in 2xFP16: 4x32 pixel tiles built from a shared-memory
                                  input patch, filter split in the prologue (gfb_stemh_args) */
     GFB_K_CONV_STEMH_C3R7 = 45, /* GFB_K_CONV_STEMH compiled for C = 3, R = S = 7 (immediate gather offsets) */
+    GFB_K_CONV_STEMWH_C3R7 = 46, /* its weight gradient in 2xFP16 (gfb_stemh_args, w = dy; per-CTA partials) */
     GFB_K_ROWJIT = 33,    /* row-fused launch (softmax-shaped subgraph, one team per row; gfb_row_args):
                              always a runtime-generated kernel (jit.py / rowfuse.py), the built-in
                              entry only traps */

@@ -22,6 +22,7 @@ K_CONV_TCGWH64, K_CONV_TCGWH128 = 41, 42
 K_MEMSET = 43
 K_CONV_STEMH = 44
 K_CONV_STEMH_C3R7 = 45
+K_CONV_STEMWH_C3R7 = 46
 K_CONV_TCG64, K_CONV_TCG128 = 17, 18
 K_CONV_TCX64, K_CONV_TCX128 = 22, 23
 K_CONV_TCGG64, K_CONV_TCGG128 = 24, 25

@@ -160,6 +160,8 @@ CHMAX_BLOCKS = 2 * 148  # channel-max blocks: more only adds atomicMax contentio
 STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
 STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
 STEMH_SMEM = 4 * 32768 + 3 * 2 * 8192 + 32768 + 2 * 1536 * 4 + 3 * 64 * 4 + (16 + 64 + 16) * 4 + 256 + 1024  # conv_f16.cu HSCfg
+STEMWH_THREADS = 64 + 32 * (8 + 4)  # conv_f16.cu HSWCfg
+STEMWH_SMEM = 3 * 65536 + 2 * 1024 * 4 + (16 + 8) * 4 + 256 + 1024
 TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
 TCGW_SMEM = {64: 3 * (2 * 16384 + 2 * 8192) + 3 * (16384 + 8192) + 1280,
              128: 2 * (2 * 16384 + 2 * 16384) + 2 * (16384 + 16384) + 1280}  # WCfg::SMEM_BYTES
@@ -2672,6 +2674,33 @@ class Lowering:
         rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "w": yb})
         self.launches.append(rec)
 
+    def _conv_stemwh(self, n, xb, xs, yb, ys, out, xshape, oshape, pt, pl, addr, label):
+        """The 3-channel 7x7 weight gradient on conv_f16.cu
+        gfb_conv_stemwh_kernel: every CTA reduces a contiguous range of
+        2 x 32 output-pixel tiles into its own [K, 64] partial; a second pass
+        sums the partials in CTA order into dW."""
+        N_, Cc, H, W = xshape
+        Ho, Wo = oshape
+        kdim, ncols = Cc * 49, 64
+        tiles = N_ * ((Ho + 1) // 2) * ((Wo + 31) // 32)
+        grid = max(1, min(tiles, NUM_SMS))
+        scratch = Buffer(self.new_key(), ElementType.F32, (grid, kdim, ncols), (kdim * ncols, ncols, 1))
+        self.buf[("splitk", n)] = scratch
+        ta = abi.StemhArgs(M=N_ * Ho * Wo, N=ncols, K=kdim, xs0=xs[0], xs1=xs[1], xs2=xs[2], xs3=xs[3],
+                           ws0=ys[0], ws1=ys[1], ws2=ys[2], ws3=ys[3], Y=Ho, X=Wo, oy=-pt, ox=-pl, H=H, W=W, S=7, C=Cc)
+        rec = LaunchRec(abi.K_CONV_STEMWH_C3R7, (grid, 1, 1), (STEMWH_THREADS, 1, 1), STEMWH_SMEM, ta, [xb.key, yb.key],
+                        [scratch.key], label)
+        rec.flops = 2 * N_ * Ho * Wo * ncols * kdim
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
+        rec.finalize = _finalize_refs(ta, {"c": scratch, "a": xb, "w": yb})
+        self.launches.append(rec)
+        p2 = Program(self, extents=(kdim * ncols, grid), vec_src=0, et=ElementType.F32)
+        k = p2.leaf(scratch, [(1, 1, grid), (0, ncols, kdim), (0, 1, ncols)])
+        p2.emit(I_LOAD, k=k)
+        p2.red_out = LeafSpec(out, _conv_out_digits(addr, kdim, ncols), True)
+        p2.red_out.vec = vec_class(p2.red_out.digits, 0, True, vec_width(ElementType.F32), 4)
+        self._col_launch(p2, kdim * ncols, grid, 1, label + ":splitk", ElementType.F32)
+
     def _conv_tcg(self, n, xb, xs, b, out, m, ncols, kdim, geo, addr, yb, label):
         """Conv2D / ConvBackpropData with the activation gather and TF32
         split inside the tensor-core kernel (gemm_tc.cu, gfb_conv_tcg_kernel)."""
@@ -2859,6 +2888,16 @@ class Lowering:
             m, ncols, kdim = K, Cc * R * S, N * Ho * Wo
             if os_[1] != R * S * os_[3] or os_[2] != S * os_[3] or not (force or _conv_tc_ok(m, ncols, kdim)):
                 return False
+            if ((Cc, R, S, K) == (3, 7, 7, 64) and xb.splat is None and yb.splat is None and ys[1] == 1
+                    and all(v % 4 == 0 for v in (ys[0], ys[2], ys[3])) and yb.elem_off % 4 == 0
+                    and os.environ.get("GFB_CONV_F16", "1") == "1" and os.environ.get("GFB_CONV_STEM", "1") == "1"
+                    and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 62 and max(abs(v) for v in ys) * max(yb.shape) < 2 ** 62):
+                # the 3-channel 7x7 stem's dW: 2xFP16 on the forward's patch tiles
+                # (conv_f16.cu gfb_conv_stemwh_kernel), per-CTA partials + a reduction
+                self._conv_stemwh(n, xb, xs, yb, ys, out, (N, Cc, H, W), (Ho, Wo), pt, pl,
+                                  {"c_rdiv": Cc, "c_s_hi": os_[3], "c_s_lo": os_[1], "c_sn": os_[0]},
+                                  f"{node.op.wire_name}_stemwh#{n}")
+                return True
             real_c = None
             if (Cc % 4 and Cc < 32 and xb.splat is None and os.environ.get("GFB_PAD_CHANNELS", "1") == "1"
                     and self._wgrad_mn_ok(xb, (4 * H * W, 1, 4 * W, 4), yb, ys, 4, K)):

@@ -986,7 +986,306 @@ __global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(c
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Few-channel weight gradient in 2xFP16 (the 3-channel 7x7 stem's dW), the
+// transpose of gfb_conv_stemh_kernel's product: rows k = (r, s, c) (M, two
+// 128-row MMA tiles over K = C R S <= 192), columns the 64 output channels,
+// contraction over the output pixels in 2 x 32 tiles (one 64-pixel stage
+// each).  Per tile the builders stage the x patch (pre-split words, scale u)
+// and dy's 64 x 64 block (scale v, split straight into the stage), then
+// assemble the im2col block exactly as the forward does: the same bytes read
+// as MN-major operands (pixel = K row of 128 B, k = M within it).  The
+// tile's products carry u v, so each tile's accumulator is promoted into
+// fp32 registers with one FFMA by 1 / (u v) (exact power of two).  CTA z
+// walks a contiguous range of tiles and writes its partial dW[k, n] at
+// c + z K N (the compiler adds the split reduction).  Arguments:
+// gfb_stemh_args with w = dy, strides ws0..ws3 along (n, k_out, y, x) (k_out
+// contiguous, ws1 = 1), (Y, X) = dy's (Ho, Wo), N = 64.
+namespace tc {
+struct HSWCfg {
+    static constexpr int BN = 64, TH = 2, TW = 32, PIX = TH * TW;  // 64 pixels per stage
+    static constexpr int MAXKB = 3;
+    static constexpr int BLK = PIX * 128;                  // one 64-k block of one plane: 8 KB
+    static constexpr int A_BYTES = MAXKB * BLK;            // per plane
+    static constexpr int B_BYTES = PIX * 128;              // dy: 64 pixels x 64 channels fp16, per plane
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 64 KB
+    static constexpr int STAGES = 3;
+    static constexpr int PATCH_WORDS = 1024;               // (2 + R - 1)(32 + S - 1) C + zero pad
+    static constexpr int NBUF = 4, RING = 16;              // TMEM: 4 x (2 M-tiles x 64 columns)
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int EPI_WARPS = 8, LOAD_WARPS = 4;
+    static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LOAD_WARPS);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * PATCH_WORDS * 4 + (RING + 2 * LOAD_WARPS) * 4 + 256 + 1024;
+};
+}  // namespace tc
+
+template <int CC, int RR, int SS>
+__global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel(const __grid_constant__ gfb_stemh_args p) {
+    using namespace tc;
+    using C_ = HSWCfg;
+    constexpr int BN = C_::BN, TH = C_::TH, TW = C_::TW, PIX = C_::PIX, STAGES = C_::STAGES, NBUF = C_::NBUF, RING = C_::RING;
+    constexpr int BLK = C_::BLK, A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int LW = C_::LOAD_WARPS, EPI_WARPS = C_::EPI_WARPS;
+    constexpr int K_ = CC * RR * SS, NK = (K_ + 63) / 64;
+    constexpr int PH = TH + RR - 1, PW = TW + SS - 1, PSZ = PH * PW * CC;
+    static_assert(PSZ + (TH - 1) * PW + TW <= C_::PATCH_WORDS && NK <= C_::MAXKB, "stem shape");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    uint32_t* pw = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);  // two patch buffers
+    float* ifac = reinterpret_cast<float*>(pw + 2 * C_::PATCH_WORDS);         // 1 / (u v) of tile gt at gt % RING
+    float* wmax = ifac + RING;                                                // [2][LW]: x and dy maxima
+    uint64_t* full = reinterpret_cast<uint64_t*>(wmax + 2 * LW);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_x = (p.X + TW - 1) / TW, tiles_y = (p.Y + TH - 1) / TH;
+    const int ntiles = (int)(p.M / ((int64_t)p.Y * p.X)) * tiles_y * tiles_x;  // M = N * Y * X pixels
+    const int per = (ntiles + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int t0 = min(ntiles, (int)blockIdx.x * per), t1 = min(ntiles, t0 + per);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], LW);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(C_::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    auto item_at = [&](int it, int& n, int& y0, int& x0) {
+        const int tx = it % tiles_x, r = it / tiles_x, ty = r % tiles_y;
+        n = r / tiles_y;
+        y0 = ty * TH;
+        x0 = tx * TW;
+    };
+
+    if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(128, BN) | (1u << 15) | (1u << 16);  // MN-major A and B
+            uint32_t g = 0;
+            for (int it = t0; it < t1; ++it, ++g) {
+                const int s = g % STAGES, b = g % NBUF;
+                mbar_wait(&tempty[b], ((g / NBUF) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                mbar_wait(&full[s], (g / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa = su32(smem + s * STAGE_BYTES), sb = sa + 2 * A_BYTES;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    if (mt * 128 >= K_) continue;
+                    const uint32_t d = tmem + (uint32_t)(b * 2 * BN + mt * BN);
+#pragma unroll
+                    for (int j = 0; j < PIX / 16; ++j) {
+                        // 16 pixels (K rows) = two 1 KB atoms; the two 64-k M chunks one block apart
+                        const uint64_t ah = smem_desc_mn16(sa + mt * 2 * BLK + j * 2048, BLK);
+                        const uint64_t al = smem_desc_mn16(sa + A_BYTES + mt * 2 * BLK + j * 2048, BLK);
+                        const uint64_t bh = smem_desc_mn16(sb + j * 2048, BLK), bl = smem_desc_mn16(sb + B_BYTES + j * 2048, BLK);
+                        mma_f16_cta(d, ah, bh, idesc, j > 0);
+                        mma_f16_cta(d, ah, bl, idesc, 1);
+                        mma_f16_cta(d, al, bh, idesc, 1);
+                    }
+                }
+                mma_commit(&empty[s]);
+                mma_commit(&tfull[b]);
+            }
+        }
+    } else if (warp >= 2 && warp < 2 + EPI_WARPS) {
+        // warp w: TMEM lanes 32 (w & 3) .., M-tile (w - 2) / 4; 64 fp32 partials per thread
+        const int q = warp & 3, mt = (warp - 2) >> 2;
+        float acc[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+        uint32_t g = 0;
+        for (int it = t0; it < t1; ++it, ++g) {
+            const int b = g % NBUF;
+            mbar_wait(&tfull[b], (g / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float f = ifac[g % RING];
+            if (mt * 128 < K_) {
+#pragma unroll
+                for (int c = 0; c < BN / 16; ++c) {
+                    float v[16];
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 2 * BN + mt * BN + c * 16), v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fmaf_rn(v[j], f, acc[c * 16 + j]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[b])) : "memory");
+        }
+        const int row = mt * 128 + q * 32 + lane;
+        if (row < K_) {
+            float* dst = resolve<float>(p.tab, p.c) + ((int64_t)blockIdx.x * K_ + row) * BN;
+#pragma unroll
+            for (int j = 0; j < BN; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        }
+    } else if (warp >= 2 + EPI_WARPS) {
+        // builders: thread t takes pixel row m = t & 63 (half hf of its chunks)
+        // for A, and 8 float4 of dy's 64 x 64 block for B
+        const int t = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0 .. 127
+        const int m = t & 63, hf = t >> 6, lw = t >> 5;
+        const int py = m / TW, px = m % TW;
+        const int rsw = m & 7;
+        const float* X = resolve<const float>(p.tab, p.a);
+        const float* DY = resolve<const float>(p.tab, p.w);
+        constexpr int PPT = (PSZ + 32 * LW - 1) / (32 * LW);
+        float pre[PPT];
+        float4 dv[8];
+        int pyy[PPT], pxx[PPT];
+        int64_t poff[PPT];
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int i = t + u * 32 * LW;
+            const int c = i / (PH * PW), rem = i - c * (PH * PW), yy = rem / PW, xx = rem - yy * PW;
+            pyy[u] = i < PSZ ? yy + p.oy : -(1 << 28);
+            pxx[u] = xx + p.ox;
+            poff[u] = (int64_t)c * p.xs1 + (int64_t)(yy + p.oy) * p.xs2 + (int64_t)(xx + p.ox) * p.xs3;
+        }
+        for (int i = PSZ + t; i < C_::PATCH_WORDS; i += 32 * LW) pw[i] = pw[C_::PATCH_WORDS + i] = 0u;
+        auto fetch = [&](int it2) {
+            int n2, ya, xa;
+            item_at(it2, n2, ya, xa);
+            const float* base = X + (int64_t)n2 * p.xs0 + (int64_t)ya * p.xs2 + (int64_t)xa * p.xs3;
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) {
+                const int h = ya + pyy[u], w = xa + pxx[u];
+                pre[u] = ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W) ? __ldg(base + poff[u]) : 0.0f;
+            }
+            // dy: float4 i = t + 128 u is pixel i / 16 of the tile, channels 4 (i % 16) ..
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = t + 128 * u, pp = i >> 4, y = ya + pp / TW, x = xa + pp % TW;
+                dv[u] = (y < p.Y && x < p.X)
+                            ? __ldg(reinterpret_cast<const float4*>(DY + (int64_t)n2 * p.ws0 + (int64_t)y * p.ws2 + (int64_t)x * p.ws3) +
+                                    (i & 15))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        // tile g2's scales (two loader barriers), its parked patch words, and
+        // its dy block split into stage g2 % STAGES (acquired here)
+        auto park = [&](uint32_t g2) {
+            float mx = 0.0f, md = 0.0f;
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) mx = fmaxf(mx, fin_abs(pre[u]));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) md = amax4(md, dv[u]);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o));
+            }
+            if (lane == 0) {
+                wmax[lw] = mx;
+                wmax[LW + lw] = md;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
+            mx = wmax[0];
+            md = wmax[LW];
+#pragma unroll
+            for (int i = 1; i < LW; ++i) {
+                mx = fmaxf(mx, wmax[i]);
+                md = fmaxf(md, wmax[LW + i]);
+            }
+            const float u = f16_tile_scale(mx), v = f16_tile_scale(md);
+            if (t == 0) ifac[g2 % RING] = __fmul_rn(__frcp_rn(u), __frcp_rn(v));
+            uint32_t* pt = pw + (g2 & 1) * C_::PATCH_WORDS;
+#pragma unroll
+            for (int q2 = 0; q2 < PPT; ++q2) {
+                if (t + q2 * 32 * LW < PSZ) {
+                    const float x = __fmul_rn(pre[q2], u);
+                    const __half h = __float2half_rn(x), l = __float2half_rn(__fsub_rn(x, __half2float(h)));
+                    pt[t + q2 * 32 * LW] = (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(l) << 16);
+                }
+            }
+            const int s = g2 % STAGES;
+            mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
+            unsigned char* sb = smem + s * STAGE_BYTES + 2 * A_BYTES;
+#pragma unroll
+            for (int u2 = 0; u2 < 8; ++u2) {
+                const int i = t + 128 * u2, pp = i >> 4, qd = i & 15;
+                uint2 h, l;
+                split4_f16(scale4(dv[u2], v), h, l);
+                const int o = pp * 128 + (((qd >> 1) ^ (pp & 7)) << 4) + (qd & 1) * 8;
+                *reinterpret_cast<uint2*>(sb + o) = h;
+                *reinterpret_cast<uint2*>(sb + B_BYTES + o) = l;
+            }
+        };
+        if (t0 < t1) {
+            fetch(t0);
+            park(0);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
+        uint32_t g = 0;
+        for (int it = t0; it < t1; ++it, ++g) {
+            const bool more = it + 1 < t1;
+            if (more) fetch(it + 1);
+            const uint32_t* prow = pw + (g & 1) * C_::PATCH_WORDS + py * PW + px;
+            const int s = g % STAGES;
+            unsigned char* st = smem + s * STAGE_BYTES + m * 128;
+#pragma unroll
+            for (int kb = 0; kb < NK; ++kb) {
+                const int ks = (K_ - kb * 64 + 15) / 16 < 4 ? (K_ - kb * 64 + 15) / 16 : 4;
+                uint32_t e[32];
+                if (hf == 0) {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (jj < ks)
+#pragma unroll
+                            for (int q2 = 0; q2 < 8; ++q2) e[8 * jj + q2] = prow[stemh_off(CC, RR, SS, PH, PW, kb * 64 + 8 * jj + q2)];
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (jj < ks)
+#pragma unroll
+                            for (int q2 = 0; q2 < 8; ++q2) e[8 * jj + q2] = prow[stemh_off(CC, RR, SS, PH, PW, kb * 64 + 8 * (ks + jj) + q2)];
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (jj < ks) {
+                        const uint32_t* q2 = e + 8 * jj;
+                        const int o = kb * BLK + (((hf * ks + jj) ^ rsw) << 4);
+                        *reinterpret_cast<uint4*>(st + o) = make_uint4(__byte_perm(q2[0], q2[1], 0x5410), __byte_perm(q2[2], q2[3], 0x5410),
+                                                                       __byte_perm(q2[4], q2[5], 0x5410), __byte_perm(q2[6], q2[7], 0x5410));
+                        *reinterpret_cast<uint4*>(st + A_BYTES + o) = make_uint4(
+                            __byte_perm(q2[0], q2[1], 0x7632), __byte_perm(q2[2], q2[3], 0x7632), __byte_perm(q2[4], q2[5], 0x7632),
+                            __byte_perm(q2[6], q2[7], 0x7632));
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+            if (more) park(g + 1);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C_::TMEM_COLS));
+    }
+}
+
 template __global__ void gfb_conv_stemh_kernel<0, 0, 0>(const __grid_constant__ gfb_stemh_args);
+template __global__ void gfb_conv_stemwh_kernel<3, 7, 7>(const __grid_constant__ gfb_stemh_args);
 template __global__ void gfb_conv_stemh_kernel<3, 7, 7>(const __grid_constant__ gfb_stemh_args);
 
 }  // namespace gfb
@@ -1001,8 +1300,10 @@ extern "C" const void* gfb_conv_f16_kernel_ptr(int kind) {
     if (kind == GFB_K_CONV_TCGWH128) return (const void*)gfb::gfb_conv_tcgwh_kernel<128>;
     if (kind == GFB_K_CONV_STEMH) return (const void*)gfb::gfb_conv_stemh_kernel<0, 0, 0>;
     if (kind == GFB_K_CONV_STEMH_C3R7) return (const void*)gfb::gfb_conv_stemh_kernel<3, 7, 7>;
+    if (kind == GFB_K_CONV_STEMWH_C3R7) return (const void*)gfb::gfb_conv_stemwh_kernel<3, 7, 7>;
     return nullptr;
 }
 extern "C" int gfb_tcgwh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HWCfg<64>::SMEM_BYTES : gfb::tc::HWCfg<128>::SMEM_BYTES; }
 extern "C" int gfb_stemh_smem_bytes(void) { return gfb::tc::HSCfg::SMEM_BYTES; }
+extern "C" int gfb_stemwh_smem_bytes(void) { return gfb::tc::HSWCfg::SMEM_BYTES; }
 extern "C" int gfb_tcxh_smem_bytes(int bn) { return bn == 64 ? gfb::tc::HXCfg<64>::SMEM_BYTES : gfb::tc::HXCfg<128>::SMEM_BYTES; }

@@ -284,7 +284,8 @@ const void* kernel_for(uint32_t kind) {
         kind == GFB_K_CONV_TCGG128 || kind == GFB_K_CONV_TCGW64 || kind == GFB_K_CONV_TCGW128 || kind == GFB_K_CONV_STEM64)
         return gfb_tc_kernel_ptr((int)kind);
     if (kind == GFB_K_DOT_F16P || kind == GFB_K_SPLIT_F16) return gfb_f16_kernel_ptr((int)kind);
-    if ((kind >= GFB_K_CHMAX && kind <= GFB_K_CONV_TCGWH128) || kind == GFB_K_CONV_STEMH || kind == GFB_K_CONV_STEMH_C3R7)
+    if ((kind >= GFB_K_CHMAX && kind <= GFB_K_CONV_TCGWH128) || kind == GFB_K_CONV_STEMH || kind == GFB_K_CONV_STEMH_C3R7 ||
+        kind == GFB_K_CONV_STEMWH_C3R7)
         return gfb_conv_f16_kernel_ptr((int)kind);
     return nullptr;
 }

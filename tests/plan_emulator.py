@@ -579,6 +579,38 @@ def run_stemh(mem, a):
     mem.view(a.c, np.float32)[(n * a.c_s_hi + y * a.c_sm + x * a.c_s_lo)[:, None] + j[None, :] * a.c_sn] = out
 
 
+def run_stemwh(mem, a, grid):
+    """gfb_conv_stemwh_kernel: CTA z's partial dW[k, n] over its contiguous
+    range of 2 x 32 output-pixel tiles (float64 sums, rounded to fp32; the
+    kernel's per-tile 2xFP16 scaling is exact to ~2^-22 and not modelled)."""
+    src, dy = mem.view(a.a, np.float32), mem.view(a.w, np.float32)
+    K, C, S = a.K, a.C, a.S
+    R = K // (C * S)
+    tiles_x, tiles_y = (a.X + 31) // 32, (a.Y + 1) // 2
+    nimg = a.M // (a.Y * a.X)
+    ntiles = nimg * tiles_y * tiles_x
+    per = (ntiles + grid - 1) // grid
+    k = np.arange(K, dtype=np.int64)
+    c, tap = k % C, k // C
+    r, s = tap // S, tap % S
+    part = mem.view(a.c, np.float32)
+    for z in range(grid):
+        acc = np.zeros((K, a.N))
+        for it in range(min(ntiles, z * per), min(ntiles, (z + 1) * per)):
+            tx, rr = it % tiles_x, it // tiles_x
+            ty, n = rr % tiles_y, rr // tiles_y
+            yy, xx = np.meshgrid(np.arange(ty * 2, min(a.Y, ty * 2 + 2)), np.arange(tx * 32, min(a.X, tx * 32 + 32)), indexing="ij")
+            yy, xx = yy.reshape(-1).astype(np.int64), xx.reshape(-1).astype(np.int64)
+            d = dy[n * a.ws0 + yy[:, None] * a.ws2 + xx[:, None] * a.ws3 + np.arange(a.N)[None, :] * a.ws1].astype(np.float64)
+            h = (yy + a.oy)[:, None] + r[None, :]
+            w = (xx + a.ox)[:, None] + s[None, :]
+            ok = (h >= 0) & (h < a.H) & (w >= 0) & (w < a.W)
+            off = n * a.xs0 + c[None, :] * a.xs1 + h * a.xs2 + w * a.xs3
+            xv = np.where(ok, src[np.where(ok, off, 0)], 0.0).astype(np.float64)
+            acc += xv.T @ d
+        part[z * K * a.N:(z + 1) * K * a.N] = acc.astype(np.float32).reshape(-1)
+
+
 def run_tcx(mem, a):
     """gfb_conv_tcx_kernel: rows are output pixels (n, y, x); the TMA box for
     K-block (r, s, cb) reads act[n, y*sy + oy + ksign*r, x*sx + ox + ksign*s,
@@ -834,6 +866,8 @@ def _run_launch(mem, L):
         run_stem(mem, L.args)
     elif L.kind in (abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7):
         run_stemh(mem, L.args)
+    elif L.kind == abi.K_CONV_STEMWH_C3R7:
+        run_stemwh(mem, L.args, L.grid[0])
     elif L.kind in (abi.K_CONV_TCGW64, abi.K_CONV_TCGW128):
         run_tcgw(mem, L.args)
     elif L.kind in (abi.K_CONV_TCGG64, abi.K_CONV_TCGG128):

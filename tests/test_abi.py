@@ -75,6 +75,7 @@ def test_launch_shared_memory_matches_kernels():
     assert lib.gfb_tc_smem_bytes(1) == Cm.TC_SMEM_W
     assert lib.gfb_stem_smem_bytes() == Cm.STEM_SMEM
     assert lib.gfb_stemh_smem_bytes() == Cm.STEMH_SMEM
+    assert lib.gfb_stemwh_smem_bytes() == Cm.STEMWH_SMEM
     assert lib.gfb_f16_pair_smem_bytes() == Cm.F16_SMEM_PAIR
     assert lib.gfb_tc_pair_smem_bytes() == Cm.TC_SMEM_PAIR
     for bn in (64, 128):

@@ -300,6 +300,35 @@ def test_conv_stemh_kernel_matches_oracle(monkeypatch, shape, pad, layout):
     assert G.normwise(out[0], ref[0]) <= 1e-5  # the 1e-6 image on its own scale
 
 
+@pytest.mark.parametrize("shape,pad,xlay", [
+    ((2, 3, 64, 64, 64, 7, 7), (3, 3, 3, 3), "identity"),     # fewer tiles than CTAs
+    ((4, 3, 64, 112, 112, 7, 7), (3, 3, 3, 3), "identity"),   # D's stem at half resolution, NCHW image
+    ((3, 3, 64, 37, 45, 7, 7), (2, 4, 3, 1), "nhwc"),         # partial 2 x 32 tiles, asymmetric padding
+])
+def test_conv_stemwh_kernel_matches_oracle(monkeypatch, shape, pad, xlay):
+    """gfb_conv_stemwh_kernel (the 3-channel 7x7 weight gradient in 2xFP16,
+    per-tile scales promoted per tile, per-CTA partials) vs the oracle, with
+    x and dy magnitudes varying by 10^6 between images and tiles."""
+    import test_lowering as TL
+    from paper_1801_08058_b200 import abi
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, Ko, H, W, R, S = shape
+    fn = TL._conv_graph("wgrad", N, C, Ko, H, W, R, S, (1, 1), pad)
+    nhwc = gf.Layout((0, 2, 3, 1))
+    exe = gf.compile_function(fn, parameter_layouts=[nhwc if xlay == "nhwc" else None, None, nhwc])
+    assert any(L.kind == abi.K_CONV_STEMWH_C3R7 for L in exe.lowered.launches), [L.label for L in exe.lowered.launches]
+    rng = np.random.default_rng(41)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    ins[0][0] *= np.float32(1e-3)
+    ins[2][-1] *= np.float32(1e3)
+    ins[2][:, :, : H // 4] *= np.float32(1e-3)
+    tens = [gf.tensor_from_flat(F32, v.shape, v, exe.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = gf.call(exe, tens)[0].to_numpy()
+    interp.set_threads(interp.max_threads())
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
 @pytest.mark.parametrize("m,k,n", [(512, 4096, 256), (288, 1000, 352), (4096, 2048, 4096)])
 @pytest.mark.parametrize("raw", ["mn", "kmajor", "split"])
 def test_raw_hi_operands(monkeypatch, m, k, n, raw):

@@ -256,6 +256,33 @@ def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
     assert not {abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7} & {L.kind for L in h2.lowered.launches}
 
 
+@pytest.mark.parametrize("shape,pad,xlay", [
+    ((2, 3, 64, 12, 40, 7, 7), (3, 3, 3, 3), "identity"),  # the stem's shapes: NCHW image, channel-last dy
+    ((3, 3, 64, 9, 33, 7, 7), (2, 4, 3, 1), "nhwc"),       # partial 2 x 32 tiles, asymmetric padding
+])
+def test_conv_stemwh_emulated(monkeypatch, shape, pad, xlay):
+    """The 3-channel 7x7 weight gradient on gfb_conv_stemwh_kernel (per-CTA
+    partials over contiguous pixel-tile ranges + the ordered reduction),
+    emulated, within 1e-5 normwise of the oracle."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    N, C, K, H, W, R, S = shape
+    fn = _conv_graph("wgrad", N, C, K, H, W, R, S, (1, 1), pad)
+    nhwc = (0, 2, 3, 1)
+    h = host_compile(fn, optimize=False, parameter_layouts=[nhwc if xlay == "nhwc" else None, None, nhwc])
+    kinds = [L.kind for L in h.lowered.launches]
+    assert abi.K_CONV_STEMWH_C3R7 in kinds, [L.label for L in h.lowered.launches]
+    assert any(":splitk" in L.label for L in h.lowered.launches)
+    rng = np.random.default_rng(23)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(gf.ElementType.F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    out = emulate(h, tens)[0]
+    assert G.normwise(out, interp.run_function(fn, ins)[0]) <= 1e-5
+
+
 @pytest.mark.parametrize("op,shape,stride,pad", [
     ("fwd", (2, 32, 64, 8, 9, 3, 3), (1, 1), (1, 1, 1, 1)),
     ("fwd", (2, 64, 96, 9, 9, 3, 3), (2, 2), (1, 1, 1, 1)),
