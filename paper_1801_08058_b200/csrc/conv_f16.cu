@@ -1010,15 +1010,46 @@ struct HSWCfg {
     static constexpr int A_BYTES = MAXKB * BLK;            // per plane
     static constexpr int B_BYTES = PIX * 128;              // dy: 64 pixels x 64 channels fp16, per plane
     static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 64 KB
-    static constexpr int STAGES = 3;
+    static constexpr int STAGES = 2;
+    static constexpr int RAW = 3, RAW_BYTES = PIX * BN * 4;  // dy blocks in flight (cp.async), fp32
     static constexpr int PATCH_WORDS = 1024;               // (2 + R - 1)(32 + S - 1) C + zero pad
     static constexpr int NBUF = 4, RING = 16;              // TMEM: 4 x (2 M-tiles x 64 columns)
     static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr int EPI_WARPS = 8, LOAD_WARPS = 4;
+    static constexpr int EPI_WARPS = 8, LOAD_WARPS = 8;
     static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LOAD_WARPS);
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * PATCH_WORDS * 4 + (RING + 2 * LOAD_WARPS) * 4 + 256 + 1024;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RAW * RAW_BYTES + 2 * PATCH_WORDS * 4 + (RING + 2 * LOAD_WARPS) * 4 +
+                                      256 + 1024;
 };
 }  // namespace tc
+
+// Quarter HQ of one pixel row's im2col chunks (chunk c = k 8c .. 8c + 7, at
+// K-block c / 8, slot c % 8), immediate gather offsets.
+template <int CC, int RR, int SS, int HQ, int NQ>
+__device__ __forceinline__ void stemwh_build(unsigned char* st, const uint32_t* prow, int rsw) {
+    using C_ = tc::HSWCfg;
+    constexpr int K_ = CC * RR * SS, NCH = 2 * ((K_ + 15) / 16), PER = (NCH + NQ - 1) / NQ;
+    constexpr int PH = C_::TH + RR - 1, PW = C_::TW + SS - 1;
+    uint32_t e[8 * PER];
+#pragma unroll
+    for (int cc = 0; cc < PER; ++cc) {
+        const int c = HQ * PER + cc;
+        if (c < NCH)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) e[8 * cc + q] = prow[stemh_off(CC, RR, SS, PH, PW, 8 * c + q)];
+    }
+#pragma unroll
+    for (int cc = 0; cc < PER; ++cc) {
+        const int c = HQ * PER + cc;
+        if (c < NCH) {
+            const uint32_t* q = e + 8 * cc;
+            const int o = (c / 8) * C_::BLK + (((c % 8) ^ rsw) << 4);
+            *reinterpret_cast<uint4*>(st + o) = make_uint4(__byte_perm(q[0], q[1], 0x5410), __byte_perm(q[2], q[3], 0x5410),
+                                                           __byte_perm(q[4], q[5], 0x5410), __byte_perm(q[6], q[7], 0x5410));
+            *reinterpret_cast<uint4*>(st + C_::A_BYTES + o) = make_uint4(__byte_perm(q[0], q[1], 0x7632), __byte_perm(q[2], q[3], 0x7632),
+                                                                         __byte_perm(q[4], q[5], 0x7632), __byte_perm(q[6], q[7], 0x7632));
+        }
+    }
+}
 
 template <int CC, int RR, int SS>
 __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel(const __grid_constant__ gfb_stemh_args p) {
@@ -1032,7 +1063,8 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
     static_assert(PSZ + (TH - 1) * PW + TW <= C_::PATCH_WORDS && NK <= C_::MAXKB, "stem shape");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-    uint32_t* pw = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);  // two patch buffers
+    unsigned char* raw = smem + STAGES * STAGE_BYTES;                          // dy blocks, fp32 [64 px][64]
+    uint32_t* pw = reinterpret_cast<uint32_t*>(raw + C_::RAW * C_::RAW_BYTES);  // two patch buffers
     float* ifac = reinterpret_cast<float*>(pw + 2 * C_::PATCH_WORDS);         // 1 / (u v) of tile gt at gt % RING
     float* wmax = ifac + RING;                                                // [2][LW]: x and dy maxima
     uint64_t* full = reinterpret_cast<uint64_t*>(wmax + 2 * LW);
@@ -1137,17 +1169,16 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
             for (int j = 0; j < BN; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         }
     } else if (warp >= 2 + EPI_WARPS) {
-        // builders: thread t takes pixel row m = t & 63 (half hf of its chunks)
-        // for A, and 8 float4 of dy's 64 x 64 block for B
-        const int t = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0 .. 127
-        const int m = t & 63, hf = t >> 6, lw = t >> 5;
+        // builders: thread t takes pixel row m = t & 63 (a quarter hq of its
+        // 16-byte chunks) for A, and 4 float4 of dy's 64 x 64 block for B
+        const int t = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0 .. 255
+        const int m = t & 63, hq = t >> 6, lw = t >> 5;
         const int py = m / TW, px = m % TW;
         const int rsw = m & 7;
         const float* X = resolve<const float>(p.tab, p.a);
         const float* DY = resolve<const float>(p.tab, p.w);
-        constexpr int PPT = (PSZ + 32 * LW - 1) / (32 * LW);
+        constexpr int PPT = (PSZ + 32 * LW - 1) / (32 * LW), DPT = PIX * 16 / (32 * LW);  // patch words, dy float4
         float pre[PPT];
-        float4 dv[8];
         int pyy[PPT], pxx[PPT];
         int64_t poff[PPT];
 #pragma unroll
@@ -1168,24 +1199,38 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
                 const int h = ya + pyy[u], w = xa + pxx[u];
                 pre[u] = ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W) ? __ldg(base + poff[u]) : 0.0f;
             }
-            // dy: float4 i = t + 128 u is pixel i / 16 of the tile, channels 4 (i % 16) ..
+        };
+        // dy block of tile g2 into raw buffer g2 % RAW with 16-byte cp.async
+        // (zero-filled outside the image), one commit group per tile (empty
+        // past the range, so the group count stays uniform): float4 i = t +
+        // 128 u is pixel i / 16 of the tile, channels 4 (i % 16) ..
+        auto issue = [&](uint32_t g2) {
+            const int it2 = t0 + (int)g2;
+            if (it2 < t1) {
+                int n2, ya, xa;
+                item_at(it2, n2, ya, xa);
+                const uint32_t dst0 = su32(raw + (g2 % C_::RAW) * C_::RAW_BYTES);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = t + 128 * u, pp = i >> 4, y = ya + pp / TW, x = xa + pp % TW;
-                dv[u] = (y < p.Y && x < p.X)
-                            ? __ldg(reinterpret_cast<const float4*>(DY + (int64_t)n2 * p.ws0 + (int64_t)y * p.ws2 + (int64_t)x * p.ws3) +
-                                    (i & 15))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int u = 0; u < DPT; ++u) {
+                    const int i = t + 32 * LW * u, pp = i >> 4, y = ya + pp / TW, x = xa + pp % TW;
+                    const bool in = y < p.Y && x < p.X;
+                    const float* src = in ? DY + (int64_t)n2 * p.ws0 + (int64_t)y * p.ws2 + (int64_t)x * p.ws3 + 4 * (i & 15) : DY;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + i * 16), "l"(src), "r"(in ? 16 : 0)
+                                 : "memory");
+                }
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");
         };
         // tile g2's scales (two loader barriers), its parked patch words, and
         // its dy block split into stage g2 % STAGES (acquired here)
         auto park = [&](uint32_t g2) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's copies of tile g2 landed
+            const float4* dr = reinterpret_cast<const float4*>(raw + (g2 % C_::RAW) * C_::RAW_BYTES);
             float mx = 0.0f, md = 0.0f;
 #pragma unroll
             for (int u = 0; u < PPT; ++u) mx = fmaxf(mx, fin_abs(pre[u]));
 #pragma unroll
-            for (int u = 0; u < 8; ++u) md = amax4(md, dv[u]);
+            for (int u = 0; u < DPT; ++u) md = amax4(md, dr[t + 32 * LW * u]);
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1218,15 +1263,17 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
             mbar_wait(&empty[s], ((g2 / STAGES) & 1) ^ 1);
             unsigned char* sb = smem + s * STAGE_BYTES + 2 * A_BYTES;
 #pragma unroll
-            for (int u2 = 0; u2 < 8; ++u2) {
-                const int i = t + 128 * u2, pp = i >> 4, qd = i & 15;
+            for (int u2 = 0; u2 < DPT; ++u2) {
+                const int i = t + 32 * LW * u2, pp = i >> 4, qd = i & 15;
                 uint2 h, l;
-                split4_f16(scale4(dv[u2], v), h, l);
+                split4_f16(scale4(dr[i], v), h, l);
                 const int o = pp * 128 + (((qd >> 1) ^ (pp & 7)) << 4) + (qd & 1) * 8;
                 *reinterpret_cast<uint2*>(sb + o) = h;
                 *reinterpret_cast<uint2*>(sb + B_BYTES + o) = l;
             }
         };
+        issue(0);
+        issue(1);
         if (t0 < t1) {
             fetch(t0);
             park(0);
@@ -1235,40 +1282,15 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
         uint32_t g = 0;
         for (int it = t0; it < t1; ++it, ++g) {
             const bool more = it + 1 < t1;
+            issue(g + 2);  // raw buffer (g + 2) % 3 was last read by park(g - 1)
             if (more) fetch(it + 1);
             const uint32_t* prow = pw + (g & 1) * C_::PATCH_WORDS + py * PW + px;
             const int s = g % STAGES;
             unsigned char* st = smem + s * STAGE_BYTES + m * 128;
-#pragma unroll
-            for (int kb = 0; kb < NK; ++kb) {
-                const int ks = (K_ - kb * 64 + 15) / 16 < 4 ? (K_ - kb * 64 + 15) / 16 : 4;
-                uint32_t e[32];
-                if (hf == 0) {
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        if (jj < ks)
-#pragma unroll
-                            for (int q2 = 0; q2 < 8; ++q2) e[8 * jj + q2] = prow[stemh_off(CC, RR, SS, PH, PW, kb * 64 + 8 * jj + q2)];
-                } else {
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        if (jj < ks)
-#pragma unroll
-                            for (int q2 = 0; q2 < 8; ++q2) e[8 * jj + q2] = prow[stemh_off(CC, RR, SS, PH, PW, kb * 64 + 8 * (ks + jj) + q2)];
-                }
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    if (jj < ks) {
-                        const uint32_t* q2 = e + 8 * jj;
-                        const int o = kb * BLK + (((hf * ks + jj) ^ rsw) << 4);
-                        *reinterpret_cast<uint4*>(st + o) = make_uint4(__byte_perm(q2[0], q2[1], 0x5410), __byte_perm(q2[2], q2[3], 0x5410),
-                                                                       __byte_perm(q2[4], q2[5], 0x5410), __byte_perm(q2[6], q2[7], 0x5410));
-                        *reinterpret_cast<uint4*>(st + A_BYTES + o) = make_uint4(
-                            __byte_perm(q2[0], q2[1], 0x7632), __byte_perm(q2[2], q2[3], 0x7632), __byte_perm(q2[4], q2[5], 0x7632),
-                            __byte_perm(q2[6], q2[7], 0x7632));
-                    }
-                }
-            }
+            if (hq == 0) stemwh_build<CC, RR, SS, 0, 4>(st, prow, rsw);
+            else if (hq == 1) stemwh_build<CC, RR, SS, 1, 4>(st, prow, rsw);
+            else if (hq == 2) stemwh_build<CC, RR, SS, 2, 4>(st, prow, rsw);
+            else stemwh_build<CC, RR, SS, 3, 4>(st, prow, rsw);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
