@@ -1017,8 +1017,8 @@ struct HSWCfg {
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int EPI_WARPS = 8, LOAD_WARPS = 8;
     static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LOAD_WARPS);
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RAW * RAW_BYTES + 2 * PATCH_WORDS * 4 + (RING + 2 * LOAD_WARPS) * 4 +
-                                      256 + 1024;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RAW * RAW_BYTES + RAW * PATCH_WORDS * 4 + 2 * PATCH_WORDS * 4 +
+                                      (RING + 2 * LOAD_WARPS) * 4 + 256 + 1024;
 };
 }  // namespace tc
 
@@ -1064,7 +1064,8 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     unsigned char* raw = smem + STAGES * STAGE_BYTES;                          // dy blocks, fp32 [64 px][64]
-    uint32_t* pw = reinterpret_cast<uint32_t*>(raw + C_::RAW * C_::RAW_BYTES);  // two patch buffers
+    float* rawp = reinterpret_cast<float*>(raw + C_::RAW * C_::RAW_BYTES);     // x patches in flight (cp.async)
+    uint32_t* pw = reinterpret_cast<uint32_t*>(rawp + C_::RAW * C_::PATCH_WORDS);  // two parked patch buffers
     float* ifac = reinterpret_cast<float*>(pw + 2 * C_::PATCH_WORDS);         // 1 / (u v) of tile gt at gt % RING
     float* wmax = ifac + RING;                                                // [2][LW]: x and dy maxima
     uint64_t* full = reinterpret_cast<uint64_t*>(wmax + 2 * LW);
@@ -1178,7 +1179,6 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
         const float* X = resolve<const float>(p.tab, p.a);
         const float* DY = resolve<const float>(p.tab, p.w);
         constexpr int PPT = (PSZ + 32 * LW - 1) / (32 * LW), DPT = PIX * 16 / (32 * LW);  // patch words, dy float4
-        float pre[PPT];
         int pyy[PPT], pxx[PPT];
         int64_t poff[PPT];
 #pragma unroll
@@ -1190,16 +1190,6 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
             poff[u] = (int64_t)c * p.xs1 + (int64_t)(yy + p.oy) * p.xs2 + (int64_t)(xx + p.ox) * p.xs3;
         }
         for (int i = PSZ + t; i < C_::PATCH_WORDS; i += 32 * LW) pw[i] = pw[C_::PATCH_WORDS + i] = 0u;
-        auto fetch = [&](int it2) {
-            int n2, ya, xa;
-            item_at(it2, n2, ya, xa);
-            const float* base = X + (int64_t)n2 * p.xs0 + (int64_t)ya * p.xs2 + (int64_t)xa * p.xs3;
-#pragma unroll
-            for (int u = 0; u < PPT; ++u) {
-                const int h = ya + pyy[u], w = xa + pxx[u];
-                pre[u] = ((uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W) ? __ldg(base + poff[u]) : 0.0f;
-            }
-        };
         // dy block of tile g2 into raw buffer g2 % RAW with 16-byte cp.async
         // (zero-filled outside the image), one commit group per tile (empty
         // past the range, so the group count stays uniform): float4 i = t +
@@ -1210,6 +1200,17 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
                 int n2, ya, xa;
                 item_at(it2, n2, ya, xa);
                 const uint32_t dst0 = su32(raw + (g2 % C_::RAW) * C_::RAW_BYTES);
+                const float* base = X + (int64_t)n2 * p.xs0 + (int64_t)ya * p.xs2 + (int64_t)xa * p.xs3;
+                const uint32_t dstp = su32(rawp + (g2 % C_::RAW) * C_::PATCH_WORDS);
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) {
+                    const int h = ya + pyy[u], w = xa + pxx[u];
+                    const bool in = (uint32_t)h < (uint32_t)p.H && (uint32_t)w < (uint32_t)p.W;
+                    if (t + u * 32 * LW < PSZ)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dstp + (t + u * 32 * LW) * 4),
+                                     "l"(in ? base + poff[u] : X), "r"(in ? 4 : 0)
+                                     : "memory");
+                }
 #pragma unroll
                 for (int u = 0; u < DPT; ++u) {
                     const int i = t + 32 * LW * u, pp = i >> 4, y = ya + pp / TW, x = xa + pp % TW;
@@ -1226,6 +1227,10 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
         auto park = [&](uint32_t g2) {
             asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's copies of tile g2 landed
             const float4* dr = reinterpret_cast<const float4*>(raw + (g2 % C_::RAW) * C_::RAW_BYTES);
+            const float* xr = rawp + (g2 % C_::RAW) * C_::PATCH_WORDS;
+            float pre[PPT];
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) pre[u] = t + u * 32 * LW < PSZ ? xr[t + u * 32 * LW] : 0.0f;
             float mx = 0.0f, md = 0.0f;
 #pragma unroll
             for (int u = 0; u < PPT; ++u) mx = fmaxf(mx, fin_abs(pre[u]));
@@ -1274,16 +1279,12 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
         };
         issue(0);
         issue(1);
-        if (t0 < t1) {
-            fetch(t0);
-            park(0);
-        }
+        if (t0 < t1) park(0);
         asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
         uint32_t g = 0;
         for (int it = t0; it < t1; ++it, ++g) {
             const bool more = it + 1 < t1;
-            issue(g + 2);  // raw buffer (g + 2) % 3 was last read by park(g - 1)
-            if (more) fetch(it + 1);
+            issue(g + 2);  // raw buffers (g + 2) % 3 were last read by park(g - 1)
             const uint32_t* prow = pw + (g & 1) * C_::PATCH_WORDS + py * PW + px;
             const int s = g % STAGES;
             unsigned char* st = smem + s * STAGE_BYTES + m * 128;
