@@ -19,4 +19,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gfb_
 bash scripts/ncu_top.sh E gfb_gemm_f16p 0 > /dev/null 2>&1
 bash scripts/ncu_top.sh D gfb_conv_tcxh 0 > /dev/null 2>&1
 bash scripts/ncu_top.sh D gfb_conv_tcgwh 0 > /dev/null 2>&1
+bash scripts/ncu_top.sh D gfb_conv_stemh 0 > /dev/null 2>&1
+bash scripts/ncu_top.sh D gfb_conv_stemwh 0 > /dev/null 2>&1
 echo done
