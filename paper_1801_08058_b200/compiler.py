@@ -2792,9 +2792,13 @@ class Lowering:
                     and (4 + R - 1) * (32 + S - 1) * Cc + 3 * (32 + S - 1) + 32 <= 1536  # 4x32 tile patch + zero pad
                     and os.environ.get("GFB_CONV_STEM", "1") == "1"
                     and os.environ.get("GFB_CONV_F16", "1") == "1"
+                    and ((Cc, R, S) == (3, 7, 7) or kdim > 160 or os.environ.get("GFB_STEMH_ALL", "0") == "1")
                     and max(abs(v) for v in xs) * max(xb.shape) < 2 ** 62):
                 # the same tiles in 2xFP16 (conv_f16.cu gfb_conv_stemh_kernel): per-tile
-                # activation scales, the filter split inside the kernel
+                # activation scales, the filter split inside the kernel.  For the
+                # 3-channel 7x7 stem (and K > 160); smaller few-channel layers (config
+                # C's 3x3 x 16 columns: 4x the MMA work at N = 64, a short walk per CTA)
+                # stay on the TF32 stem kernel, 0.039 vs 0.058 ms
                 self._conv_stemh(n, xb, xs, yb, ys, out, m, ncols, kdim,
                                  dict(Y=Ho, X=Wo, oy=-pt, ox=-pl, H=H, W=W, S=S, C=Cc,
                                       c_s_hi=os_[0], c_sm=os_[2], c_s_lo=os_[3], c_sn=os_[1]),

@@ -277,11 +277,13 @@ def test_conv_stem_kernel_matches_oracle(monkeypatch, shape, pad, layout):
 def test_conv_stemh_kernel_matches_oracle(monkeypatch, shape, pad, layout):
     """gfb_conv_stemh_kernel (the stem's tiles in 2xFP16: per-tile activation
     scales, the filter split in the prologue) vs the oracle, with inputs
-    whose magnitude varies by 10^6 between images and tiles."""
+    whose magnitude varies by 10^6 between images and tiles (GFB_STEMH_ALL:
+    also the shapes that default to the TF32 stem kernel)."""
     import test_lowering as TL
     from paper_1801_08058_b200 import abi
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_STEMH_ALL", "1")
     N, C, Ko, H, W, R, S = shape
     fn = TL._conv_graph("fwd", N, C, Ko, H, W, R, S, (1, 1), pad)
     lay = [gf.Layout((0, 2, 3, 1)), None] if layout == "nhwc" else None

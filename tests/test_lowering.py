@@ -211,8 +211,8 @@ def test_conv_tensor_core_lowering_emulated(monkeypatch, op, shape, stride, pad,
     h = host_compile(fn, optimize=False, conv_layout=layout) if op == "fwd" else host_compile(fn, optimize=False)
     labels = [L.label for L in h.lowered.launches]
     assert any("_tc" in l or "_stem" in l for l in labels), labels
-    if op == "fwd" and C < 16 and stride == (1, 1):  # few channels: the patch-staged stem kernel (2xFP16)
-        assert any("_stemh#" in l for l in labels), labels
+    if op == "fwd" and C < 16 and stride == (1, 1):  # few channels: the patch-staged stem kernels
+        assert any(("_stemh#" if (C, R, S) == (3, 7, 7) else "_stem#") in l for l in labels), labels
     if op == "wgrad" and N * H * W >= 2048:  # long K: split-K with a deterministic second pass
         assert any(":splitk" in l for l in labels), labels
     rng = np.random.default_rng(5)
@@ -236,6 +236,7 @@ def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
     from oracle import interp
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    monkeypatch.setenv("GFB_STEMH_ALL", "1")
     N, C, K, H, W, R, S = shape
     fn = _conv_graph("fwd", N, C, K, H, W, R, S, (1, 1), pad)
     lay = [(0, 2, 3, 1), None] if layout == "nhwc" else None
