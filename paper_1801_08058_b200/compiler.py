@@ -161,7 +161,7 @@ STEM_THREADS = 64 + 32 * (4 + 8)  # csrc/gemm_tc.cu SCfg
 STEM_SMEM = 4 * 32768 + 5 * 2 * 8192 + 2 * 1536 * 4 + 5 * 32 * 4 + 256 + 1024
 STEMH_SMEM = 4 * 32768 + 3 * 2 * 8192 + 32768 + 2 * 1536 * 4 + 3 * 64 * 4 + (16 + 64 + 16) * 4 + 256 + 1024  # conv_f16.cu HSCfg
 STEMWH_THREADS = 64 + 32 * (8 + 8)  # conv_f16.cu HSWCfg
-STEMWH_SMEM = 2 * 65536 + 3 * 16384 + 3 * 1024 * 4 + 2 * 1024 * 4 + (16 + 2 * 8) * 4 + 256 + 1024
+STEMWH_SMEM = 2 * 65536 + 4 * 16384 + 4 * 1024 * 4 + 2 * 1024 * 4 + (16 + 2 * 8) * 4 + 256 + 1024
 TCGW_THREADS = {64: 64 + 32 * (4 + 8), 128: 64 + 32 * (4 + 4)}  # csrc/gemm_tc.cu WCfg::THREADS
 TCGW_SMEM = {64: 3 * (2 * 16384 + 2 * 8192) + 3 * (16384 + 8192) + 1280,
              128: 2 * (2 * 16384 + 2 * 16384) + 2 * (16384 + 16384) + 1280}  # WCfg::SMEM_BYTES

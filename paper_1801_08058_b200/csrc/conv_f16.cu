@@ -1011,7 +1011,7 @@ struct HSWCfg {
     static constexpr int B_BYTES = PIX * 128;              // dy: 64 pixels x 64 channels fp16, per plane
     static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 64 KB
     static constexpr int STAGES = 2;
-    static constexpr int RAW = 3, RAW_BYTES = PIX * BN * 4;  // dy blocks in flight (cp.async), fp32
+    static constexpr int RAW = 4, RAW_BYTES = PIX * BN * 4;  // dy blocks in flight (cp.async), fp32: 3 tiles ahead
     static constexpr int PATCH_WORDS = 1024;               // (2 + R - 1)(32 + S - 1) C + zero pad
     static constexpr int NBUF = 4, RING = 16;              // TMEM: 4 x (2 M-tiles x 64 columns)
     static constexpr uint32_t TMEM_COLS = 512;
@@ -1225,7 +1225,7 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
         // tile g2's scales (two loader barriers), its parked patch words, and
         // its dy block split into stage g2 % STAGES (acquired here)
         auto park = [&](uint32_t g2) {
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's copies of tile g2 landed
+            asm volatile("cp.async.wait_group %0;" ::"n"(C_::RAW - 2) : "memory");  // this thread's copies of tile g2 landed
             const float4* dr = reinterpret_cast<const float4*>(raw + (g2 % C_::RAW) * C_::RAW_BYTES);
             const float* xr = rawp + (g2 % C_::RAW) * C_::PATCH_WORDS;
             float pre[PPT];
@@ -1277,14 +1277,14 @@ __global__ void __launch_bounds__(tc::HSWCfg::THREADS, 1) gfb_conv_stemwh_kernel
                 *reinterpret_cast<uint2*>(sb + B_BYTES + o) = l;
             }
         };
-        issue(0);
-        issue(1);
+#pragma unroll
+        for (int g2 = 0; g2 < C_::RAW - 1; ++g2) issue(g2);
         if (t0 < t1) park(0);
         asm volatile("bar.sync 1, %0;" ::"n"(32 * LW) : "memory");
         uint32_t g = 0;
         for (int it = t0; it < t1; ++it, ++g) {
             const bool more = it + 1 < t1;
-            issue(g + 2);  // raw buffers (g + 2) % 3 were last read by park(g - 1)
+            issue(g + C_::RAW - 1);  // raw buffers (g + RAW - 1) % RAW were last read by park(g - 1)
             const uint32_t* prow = pw + (g & 1) * C_::PATCH_WORDS + py * PW + px;
             const int s = g % STAGES;
             unsigned char* st = smem + s * STAGE_BYTES + m * 128;
