@@ -374,7 +374,8 @@ typedef struct GFB_ALIGN64 {
  * channel, c, r, s); N <= 64 output channels.  Each 4 x 32 pixel tile takes
  * its own power-of-two activation scale, each filter row its own; both are
  * undone in the epilogue.  Output row (n, y, x), column j at n * c_s_hi +
- * y * c_sm + x * c_s_lo + j * c_sn. */
+ * y * c_sm + x * c_s_lo + j * c_sn (and, with flags bit 0, Relu of it at c2:
+ * the Relu map of the stem folded into the epilogue). */
 typedef struct {
     const void* const* tab;
     uint64_t c, a, w; /* GFB_REF */
@@ -383,6 +384,8 @@ typedef struct {
     int64_t xs0, xs1, xs2, xs3;
     int64_t ws0, ws1, ws2, ws3;
     int32_t Y, X, oy, ox, H, W, S, C;
+    uint64_t c2;   /* GFB_REF: flags bit 0 -- also write Relu(y) (x > 0 ? x : 0) here, same addressing */
+    int64_t flags;
 } gfb_stemh_args;
 
 /* fp16 split of a dense F32 matrix [rows, cols] (row pitch ld elements, cols % 8 == 0):

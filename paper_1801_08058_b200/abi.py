@@ -193,6 +193,7 @@ class StemhArgs(C.Structure):
         ("ws0", C.c_int64), ("ws1", C.c_int64), ("ws2", C.c_int64), ("ws3", C.c_int64),
         ("Y", C.c_int32), ("X", C.c_int32), ("oy", C.c_int32), ("ox", C.c_int32),
         ("H", C.c_int32), ("W", C.c_int32), ("S", C.c_int32), ("C", C.c_int32),
+        ("c2", C.c_uint64), ("flags", C.c_int64),
     ]
 
 

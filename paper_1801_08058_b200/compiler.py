@@ -840,6 +840,9 @@ class Lowering:
         self._epi_planes = set()  # tensors whose fp16 planes a GEMM epilogue writes
         self._epi = self._plan_epilogues()
         self._epi_nodes = {m for sp in self._epi.values() for m in sp["absorbed"]}
+        self._conv_relu = self._plan_conv_relu()  # stem conv -> the Relu its epilogue writes
+        self._conv_relu_done = set()
+        self._epi_nodes |= set(self._conv_relu.values())
         for n in self.order:
             node = self.nodes[n]
             d = node.output
@@ -1971,6 +1974,38 @@ class Lowering:
                     out[writer[sp["aux2"]]]["mask_of"] = sp["aux2"]
         return out
 
+    def _plan_conv_relu(self) -> dict:
+        """The 3-channel 7x7 stem conv whose output feeds a Relu: the 2xFP16
+        stem kernel writes Relu(y) beside y (gfb_stemh_args.c2), so the Relu
+        map (a 1.6 GB read + write at config D's 224x224) is not launched.
+        If the conv takes another kernel after all, emit_heavy emits the map."""
+        if os.environ.get("GFB_STEM_RELU", "1") != "1" or os.environ.get("GFB_CONV_F16", "1") != "1":
+            return {}
+        out = {}
+        results = {r for r, _ in self.g.results}
+        for d in self.order:
+            nd = self.nodes[d]
+            if nd.op is not OpKind.CONV2D or nd.output.element_type is not ElementType.F32 or not self.is_heavy(d):
+                continue
+            xs_, ws_ = self.nodes[nd.inputs[0][0]].output.shape, self.nodes[nd.inputs[1][0]].output.shape
+            if tuple(nd.attrs["strides"]) != (1, 1) or tuple(ws_[1:]) != (3, 7, 7) or ws_[0] != 64 or xs_[1] != 3:
+                continue
+            # the Relu reads y directly or through a ConvertLayout (an index view: same
+            # values at the same logical index); _conv_stemh checks the two buffers'
+            # strides agree before it takes the Relu
+            cands = [r for r in self.consumers[d]]
+            for c in self.consumers[d]:
+                if self.nodes[c].op is OpKind.CONVERT_LAYOUT and c not in self.M:
+                    cands += self.consumers[c]
+            for r in cands:
+                rn = self.nodes[r]
+                if (rn.op is OpKind.RELU and r in self.M and r not in results and r not in self._row_nodes
+                        and r not in self.allreduce and r not in self._epi_nodes
+                        and tuple(rn.output.shape) == tuple(nd.output.shape)):
+                    out[d] = r
+                    break
+        return out
+
     def _feeds_tc(self, n) -> bool:
         """Some Dot reads `n` (directly or through index views) on the tensor cores."""
         stack, seen = [n], set()
@@ -2664,14 +2699,20 @@ class Lowering:
         x and the fp32 filter directly, no split launches)."""
         ta = abi.StemhArgs(M=m, N=ncols, K=kdim, xs0=xs[0], xs1=xs[1], xs2=xs[2], xs3=xs[3],
                            ws0=ys[0], ws1=ys[1], ws2=ys[2], ws3=ys[3], **geo)
+        refs, writes = {"c": out, "a": xb, "w": yb}, [out.key]
+        r = self._conv_relu.get(n)
+        if r is not None and self.buf[r].strides == out.strides and self.buf[r].et is out.et:
+            refs["c2"], ta.flags = self.buf[r], 1  # Relu(y) from the epilogue
+            writes.append(self.buf[r].key)
+            self._conv_relu_done.add(n)
         tiles = (m // (geo["Y"] * geo["X"])) * ((geo["Y"] + 3) // 4) * ((geo["X"] + 31) // 32)
         grid = (max(1, min(tiles, NUM_SMS)), 1, 1)
         # the 3-channel 7x7 stem: a build with immediate gather offsets
         kind = abi.K_CONV_STEMH_C3R7 if (geo["C"], kdim // geo["C"] // geo["S"], geo["S"]) == (3, 7, 7) else abi.K_CONV_STEMH
-        rec = LaunchRec(kind, grid, (STEM_THREADS, 1, 1), STEMH_SMEM, ta, [xb.key, yb.key], [out.key], label)
+        rec = LaunchRec(kind, grid, (STEM_THREADS, 1, 1), STEMH_SMEM, ta, [xb.key, yb.key], writes, label)
         rec.flops = 2 * m * ncols * kdim
-        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes
-        rec.finalize = _finalize_refs(ta, {"c": out, "a": xb, "w": yb})
+        rec.algo_bytes = xb.nbytes + yb.nbytes + out.nbytes * len(writes)
+        rec.finalize = _finalize_refs(ta, refs)
         self.launches.append(rec)
 
     def _conv_stemwh(self, n, xb, xs, yb, ys, out, xshape, oshape, pt, pl, addr, label):
@@ -2962,7 +3003,12 @@ class Lowering:
         out = self.buf[n]
         et = node.output.element_type
         if node.op is not OpKind.DOT and self.emit_conv_tc(n):
+            r = self._conv_relu.get(n)
+            if r is not None and n not in self._conv_relu_done:
+                self.emit_map(r, [r])  # the conv took a kernel without the Relu side output
             return
+        if n in self._conv_relu:
+            raise AssertionError("a stem conv planned with a Relu side output did not lower to a tensor-core kernel")
         if node.op is OpKind.DOT:
             (ab, ast), (bb, bst) = self.operand(node.inputs[0][0]), self.operand(node.inputs[1][0])
             m, k = self.nodes[node.inputs[0][0]].output.shape

@@ -802,6 +802,7 @@ __global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(c
         static_assert(TW == 32, "one tile row per epilogue warp");
         const int q = warp & 3;
         float* C = resolve<float>(p.tab, p.c);
+        float* C2 = (p.flags & 1) ? resolve<float>(p.tab, p.c2) : nullptr;  // Relu side output
         unsigned char* ost = ostage + q * (32 * BN * 4);
         const bool dense = p.c_sn == 1 && p.N == BN && p.c_s_lo == BN && p.c_sm % 4 == 0 && p.c_s_hi % 4 == 0 &&
                            (reinterpret_cast<uintptr_t>(C) & 15) == 0;
@@ -830,23 +831,33 @@ __global__ void __launch_bounds__(tc::HSCfg::THREADS, 1) gfb_conv_stemh_kernel(c
                                     __fmul_rn(__fmul_rn(acc[4 * j + 3], f), invt[4 * j + 3]));
                 __syncwarp();
                 if (y < p.Y) {
-                    float* row = C + (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm;
+                    const int64_t ro = (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm;
                     const int quad = lane & 15;
 #pragma unroll 4
                     for (int i2 = 0; i2 < 16; ++i2) {
                         const int pp = 2 * i2 + (lane >> 4), x = x0 + pp;
                         const float4 v = *reinterpret_cast<const float4*>(ost + pp * (BN * 4) + ((quad ^ (pp & 7)) << 4));
-                        if (x < p.X) *reinterpret_cast<float4*>(row + (int64_t)x * BN + quad * 4) = v;
+                        if (x < p.X) {
+                            *reinterpret_cast<float4*>(C + ro + (int64_t)x * BN + quad * 4) = v;
+                            if (C2)
+                                *reinterpret_cast<float4*>(C2 + ro + (int64_t)x * BN + quad * 4) =
+                                    make_float4(v.x > 0.f ? v.x : 0.f, v.y > 0.f ? v.y : 0.f, v.z > 0.f ? v.z : 0.f, v.w > 0.f ? v.w : 0.f);
+                        }
                     }
                 }
                 __syncwarp();
             } else {
                 const int x = x0 + lane;
                 if (y < p.Y && x < p.X) {
-                    float* dst = C + (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm + (int64_t)x * p.c_s_lo;
+                    const int64_t ro = (int64_t)n * p.c_s_hi + (int64_t)y * p.c_sm + (int64_t)x * p.c_s_lo;
 #pragma unroll
-                    for (int j = 0; j < BN; ++j)
-                        if (j < p.N) dst[(int64_t)j * p.c_sn] = __fmul_rn(__fmul_rn(acc[j], f), invt[j]);
+                    for (int j = 0; j < BN; ++j) {
+                        if (j < p.N) {
+                            const float v = __fmul_rn(__fmul_rn(acc[j], f), invt[j]);
+                            C[ro + (int64_t)j * p.c_sn] = v;
+                            if (C2) C2[ro + (int64_t)j * p.c_sn] = v > 0.f ? v : 0.f;
+                        }
+                    }
                 }
             }
         }

@@ -577,6 +577,9 @@ def run_stemh(mem, a):
         out = (A[0] @ B[0].T + A[0] @ B[1].T + A[1] @ B[0].T).astype(np.float32)
         out = ((out * (np.float32(1) / u[tile])[:, None]).astype(np.float32) * (np.float32(1) / t_n)[None, :]).astype(np.float32)
     mem.view(a.c, np.float32)[(n * a.c_s_hi + y * a.c_sm + x * a.c_s_lo)[:, None] + j[None, :] * a.c_sn] = out
+    if a.flags & 1:  # the Relu side output (x > 0 ? x : 0)
+        mem.view(a.c2, np.float32)[(n * a.c_s_hi + y * a.c_sm + x * a.c_s_lo)[:, None] + j[None, :] * a.c_sn] = \
+            np.where(out > 0, out, np.float32(0)).astype(np.float32)
 
 
 def run_stemwh(mem, a, grid):

@@ -257,6 +257,39 @@ def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
     assert not {abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7} & {L.kind for L in h2.lowered.launches}
 
 
+@pytest.mark.parametrize("layout", ["identity", "nhwc"])
+def test_stem_relu_side_output_emulated(monkeypatch, layout):
+    """Relu(Conv2D) of the 3-channel 7x7 stem: the stem kernel writes Relu(y)
+    beside y (gfb_stemh_args.flags bit 0) and no Relu map is launched; both
+    results within 1e-5 of the oracle, the Relu exactly Relu of the conv."""
+    import paper_1801_08058_b200 as gf
+    from paper_1801_08058_b200 import abi
+    from oracle import interp
+
+    monkeypatch.setenv("GFB_CONV", "tc")
+    Ko, F32 = gf.OpKind, gf.ElementType.F32
+    fn = gf.Function("stem_relu")
+    x = fn.add_parameter(F32, (2, 3, 12, 40))
+    w = fn.add_parameter(F32, (64, 3, 7, 7))
+    c = fn.add_node(Ko.CONV2D, [x, w], {"strides": (1, 1), "padding": (3, 3, 3, 3)})
+    r = fn.add_node(Ko.RELU, [c])
+    # y and Relu(y) stay materialised intermediates (two readers each, as in config D)
+    fn.set_results([fn.add_node(Ko.NEGATE, [c]), fn.add_node(Ko.NEGATE, [r]),
+                    fn.add_node(Ko.MULTIPLY, [c, r]), fn.add_node(Ko.SUM, [r], {"reduction_axes": (1,)})])
+    h = host_compile(fn, optimize=False, conv_layout=layout)
+    stem = [L for L in h.lowered.launches if L.kind in (abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7)]
+    assert stem and stem[0].args.flags == 1, [L.label for L in h.lowered.launches]
+    assert not any("map:Relu" in L.label for L in h.lowered.launches), [L.label for L in h.lowered.launches]
+    rng = np.random.default_rng(29)
+    ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
+    tens = [gf.tensor_from_flat(F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
+    got = emulate(h, tens)
+    ref = interp.run_function(fn, ins)
+    assert G.normwise(got[0], ref[0]) <= 1e-5
+    # -Relu(y) from -y: y > 0 -> -y, else -0
+    assert G.same_bits(got[1], np.where(got[0] < 0, got[0], np.float32(-0.0)).astype(np.float32))
+
+
 @pytest.mark.parametrize("shape,pad,xlay", [
     ((2, 3, 64, 12, 40, 7, 7), (3, 3, 3, 3), "identity"),  # the stem's shapes: NCHW image, channel-last dy
     ((3, 3, 64, 9, 33, 7, 7), (2, 4, 3, 1), "nhwc"),       # partial 2 x 32 tiles, asymmetric padding
