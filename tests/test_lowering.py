@@ -257,16 +257,20 @@ def test_conv_stemh_emulated(monkeypatch, shape, pad, layout):
     assert not {abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7} & {L.kind for L in h2.lowered.launches}
 
 
-@pytest.mark.parametrize("layout", ["identity", "nhwc"])
-def test_stem_relu_side_output_emulated(monkeypatch, layout):
+@pytest.mark.parametrize("layout,fallback", [("identity", False), ("nhwc", False), ("nhwc", True)])
+def test_stem_relu_side_output_emulated(monkeypatch, layout, fallback):
     """Relu(Conv2D) of the 3-channel 7x7 stem: the stem kernel writes Relu(y)
     beside y (gfb_stemh_args.flags bit 0) and no Relu map is launched; both
-    results within 1e-5 of the oracle, the Relu exactly Relu of the conv."""
+    results within 1e-5 of the oracle, the Relu exactly Relu of the conv.
+    With the stem kernels off (GFB_CONV_STEM=0) the planned Relu is emitted
+    as a map after the conv's other kernel."""
     import paper_1801_08058_b200 as gf
     from paper_1801_08058_b200 import abi
     from oracle import interp
 
     monkeypatch.setenv("GFB_CONV", "tc")
+    if fallback:
+        monkeypatch.setenv("GFB_CONV_STEM", "0")
     Ko, F32 = gf.OpKind, gf.ElementType.F32
     fn = gf.Function("stem_relu")
     x = fn.add_parameter(F32, (2, 3, 12, 40))
@@ -278,8 +282,11 @@ def test_stem_relu_side_output_emulated(monkeypatch, layout):
                     fn.add_node(Ko.MULTIPLY, [c, r]), fn.add_node(Ko.SUM, [r], {"reduction_axes": (1,)})])
     h = host_compile(fn, optimize=False, conv_layout=layout)
     stem = [L for L in h.lowered.launches if L.kind in (abi.K_CONV_STEMH, abi.K_CONV_STEMH_C3R7)]
-    assert stem and stem[0].args.flags == 1, [L.label for L in h.lowered.launches]
-    assert not any("map:Relu" in L.label for L in h.lowered.launches), [L.label for L in h.lowered.launches]
+    relu_maps = [L for L in h.lowered.launches if "map:Relu" in L.label]
+    if fallback:
+        assert not stem and len(relu_maps) == 1, [L.label for L in h.lowered.launches]
+    else:
+        assert stem and stem[0].args.flags == 1 and not relu_maps, [L.label for L in h.lowered.launches]
     rng = np.random.default_rng(29)
     ins = [rng.uniform(-1, 1, size=fn.nodes[p].output.shape).astype(np.float32) for p in fn.parameters]
     tens = [gf.tensor_from_flat(F32, v.shape, v, h.parameter_signature[i][1]) for i, v in enumerate(ins)]
