@@ -550,7 +550,8 @@ const char* gfb_last_error(void);
 int gfb_device_info(int* sm_major, int* sm_minor, int* num_sms);
 
 int gfb_exe_create(const gfb_plan* plan, gfb_exe** out);
-/* inputs[i] / outputs[j]: device pointers for this run (caller-owned). */
+/* inputs[i] / outputs[j]: device pointers for this run (caller-owned), each
+ * 16-byte aligned (vector, cp.async and TMA operands; GFB_ERR_INVALID otherwise). */
 int gfb_exe_run(gfb_exe* exe, void* const* inputs, void* const* outputs, void* stream);
 int gfb_exe_destroy(gfb_exe* exe);
 /* Host-buffer runs.  gfb_exe_set_io gives the byte size of every input and

@@ -353,6 +353,13 @@ int launch_all_streams(gfb_exe* e, cudaStream_t s0) {
 }
 
 int upload_table(gfb_exe* e, void* const* inputs, void* const* outputs, cudaStream_t s) {
+    // kernels read caller buffers with 16-byte vector loads, cp.async and TMA
+    for (uint32_t i = 0; i < e->n_in; ++i)
+        if (reinterpret_cast<uintptr_t>(inputs[i]) & 15)
+            return fail(GFB_ERR_INVALID, "input " + std::to_string(i) + ": device pointer not 16-byte aligned");
+    for (uint32_t j = 0; j < e->n_out; ++j)
+        if (reinterpret_cast<uintptr_t>(outputs[j]) & 15)
+            return fail(GFB_ERR_INVALID, "output " + std::to_string(j) + ": device pointer not 16-byte aligned");
     CUDA_TRY(cudaEventSynchronize(e->tab_done));  // previous run consumed the staging copy
     // the previous run may be in flight on another stream: its kernels still
     // read the device table and the arena this run is about to reuse

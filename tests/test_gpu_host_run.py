@@ -105,3 +105,26 @@ def test_host_run_input_pieces(streams, monkeypatch):
         res = gf.call(exe, ins, out=outs)
         for r, w in zip(res, want):
             assert np.array_equal(r.to_numpy().view(np.uint32), w.view(np.uint32))
+
+
+def test_misaligned_device_pointer_fails_loudly():
+    """gfb_exe_run rejects a caller buffer that is not 16-byte aligned (the
+    kernels read caller buffers with 16-byte vector loads, cp.async and TMA)
+    with GFB_ERR_INVALID instead of faulting on the device."""
+    import torch
+
+    fn = gf.Function("axpy")
+    x = fn.add_parameter(gf.ElementType.F32, (1024,))
+    y = fn.add_parameter(gf.ElementType.F32, (1024,))
+    fn.set_results([fn.add_node(gf.OpKind.ADD, [x, y])])
+    exe = gf.compile_function(fn)
+    a = torch.ones(1025, device="cuda")
+    b = torch.ones(1024, device="cuda")
+    out = exe.allocate_outputs()
+    exe.run_device([a[:1024], b], out)  # aligned: fine
+    torch.cuda.synchronize()
+    assert float(out[0][0]) == 2.0
+    from paper_1801_08058_b200.errors import DeviceError
+
+    with pytest.raises(DeviceError, match="16-byte aligned"):
+        exe.run_device([a[1:], b], out)
